@@ -1,0 +1,200 @@
+/*
+ * gs2b200.h -- C ABI of libgs2b200.so, the B200 (sm_100a) implementation of the
+ * two-stage Gauss-Seidel (GS2) relaxation path of arXiv 2104.01196.
+ *
+ * Every entry point is plain C: opaque handles, raw pointers, sizes and an
+ * int status (RS_OK = 0, negative on error; rs_last_error() /
+ * rs_last_error_index() give the message and the offending row / entry).
+ * Vector arguments are DEVICE pointers (caller-owned, e.g. torch tensors);
+ * `stream` is a cudaStream_t (NULL = legacy default stream).  Nothing here
+ * synchronises the stream unless its comment says so.
+ *
+ * Each function names the reference interface it replaces (paths relative to
+ * /root/reference/pkg/src/relaxsolve).  The reference's native seam is the
+ * numba kernel ABI of _kernels.py (flat arrays, caller-allocated outputs, no
+ * return values); the reference-side bindings are shown in INTEGRATION.md.
+ */
+#ifndef GS2B200_H
+#define GS2B200_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RS_ABI_VERSION 1
+
+/* status codes */
+#define RS_OK 0
+#define RS_ERR_ARG (-1)       /* bad argument (ValueError in the reference) */
+#define RS_ERR_CUDA (-2)      /* CUDA runtime error */
+#define RS_ERR_DIAG (-3)      /* missing / zero / non-finite diagonal; index = row (sparse.py:213-219) */
+#define RS_ERR_OVERFLOW (-4)  /* float32 downcast overflow; index = entry (sparse.py:253-256) */
+#define RS_ERR_NONFINITE (-5) /* non-finite values (DivergenceError, krylov.py:157-159) */
+#define RS_ERR_SHAPE (-6)     /* dimension mismatch (sparse.py:172-176, relax.py:95-103) */
+#define RS_ERR_UNSUPPORTED (-7)
+
+/* value dtypes (sparse.py:25 PRECISION_DTYPES) */
+#define RS_F64 0
+#define RS_F32 1
+
+/* directions / forms (relax.py:34-35) */
+#define RS_FORWARD 0
+#define RS_BACKWARD 1
+#define RS_SYMMETRIC 2
+#define RS_NON_COMPACT 0
+#define RS_COMPACT 1
+
+/* preconditioner kinds (krylov.py:24 PRECOND_KINDS; mt_* are not on this path) */
+#define RS_PC_NONE 0
+#define RS_PC_JR 1
+#define RS_PC_GS_SEQ 2
+#define RS_PC_SGS_SEQ 3
+#define RS_PC_GS2 4
+#define RS_PC_SGS2 5
+
+/* stencil generators for rs_mat_create_stencil */
+#define RS_STENCIL_LAPLACE2D 0  /* problems.py:58-73, params unused */
+#define RS_STENCIL_LAPLACE3D 1  /* problems.py:76-97, params unused */
+#define RS_STENCIL_CONVDIFF3D 2 /* upwind -Lap + beta.grad, params = beta[3] */
+
+typedef struct rs_matrix *rs_matrix_t;
+typedef void *rs_stream_t; /* cudaStream_t */
+
+/* RelaxConfig (relax.py:38-69) */
+typedef struct {
+  int n_t, n_k, n_j;
+  int direction; /* RS_FORWARD / RS_BACKWARD / RS_SYMMETRIC */
+  int form;      /* RS_NON_COMPACT / RS_COMPACT */
+  double omega, gamma;
+} rs_relax_cfg;
+
+int rs_abi_version(void);
+/* number of CUDA kernels the library has launched since load (all threads) */
+int64_t rs_launch_count(void);
+const char *rs_last_error(void);
+int64_t rs_last_error_index(void);
+
+/* ---- matrix handles: CsrMatrix + extract_splitting (sparse.py:31-103, 195-232) ---- */
+
+/* Upload a host CSR in the reference layout (int64 row_ptr[nrows+1], int64
+ * col_idx[nnz], values float64 or float32 per dtype) and split it on device
+ * into L / D / U (+ D^-1 L, D^-1 U).  For a distributed row block, the rows
+ * are global rows [row0, row0+nrows) of an ncols-column matrix: row_ptr and
+ * col_idx describe only those rows (col_idx global).  Synchronises. */
+int rs_mat_create_csr(int device, int64_t nrows, int64_t ncols, int64_t row0, const int64_t *row_ptr,
+                      const int64_t *col_idx, const void *values, int dtype, rs_matrix_t *out);
+
+/* Generate a stencil matrix directly on device (laplace2d/3d, problems.py:58-97;
+ * convection-diffusion for config C4), rows [row0, row0+nrows) of the
+ * natural ordering i = (iz*ny + iy)*nx + ix.  Synchronises. */
+int rs_mat_create_stencil(int device, int kind, int64_t nx, int64_t ny, int64_t nz, const double *params,
+                          int64_t row0, int64_t nrows, int dtype, rs_matrix_t *out);
+
+/* cast_matrix + extract_splitting in float32 (krylov.py:101-103): values
+ * rounded to float32 (RS_ERR_OVERFLOW on a finite value that overflows), then
+ * d and D^-1 L, D^-1 U recomputed in float32.  Synchronises. */
+int rs_mat_cast(rs_matrix_t src, int dtype, rs_matrix_t *out);
+
+int rs_mat_destroy(rs_matrix_t m);
+
+/* sizes: nrows, ncols, row0, nnz (all stored entries), nnz_l, nnz_u, halo_lo, halo_hi */
+int rs_mat_info(rs_matrix_t m, int64_t *info8, int *dtype);
+
+/* Copy d, and the raw / prescaled strict triangles back as CSR (int64 row_ptr,
+ * int64 col_idx) for inspection and tests; any pointer may be NULL.
+ * which: 0 = L, 1 = U.  Synchronises. */
+int rs_mat_export_tri(rs_matrix_t m, int which, int64_t *row_ptr, int64_t *col_idx, void *values, void *dvalues);
+int rs_mat_export_diag(rs_matrix_t m, void *d);
+
+/* ---- kernels of the numba ABI (_kernels.py) ---- */
+
+/* csr_matvec (_kernels.py:15-21) / spmv (sparse.py:179-184): y = A x.
+ * x_lo / x_hi: halo values below / above the block (NULL when halo is empty). */
+int rs_spmv(rs_matrix_t m, const void *x, const void *x_lo, const void *x_hi, void *y, rs_stream_t stream);
+
+/* gs_sequential_sweep (relax.py:177-190) / gs_ordered_sweep (_kernels.py:24-39),
+ * level-scheduled: rows of one dependency level run in parallel, x in place.
+ * Bitwise equal to the sequential natural-order sweep. */
+int rs_gs_sweep(rs_matrix_t m, const void *b, void *x, int direction, double omega, rs_stream_t stream);
+
+/* ---- relaxation (relax.py) ---- */
+
+/* jr_sweeps (relax.py:145-154): x <- x + w D^-1 (b - A x), `sweeps` times. */
+int rs_jr_sweeps(rs_matrix_t m, const void *b, void *x, int sweeps, double omega, rs_stream_t stream);
+
+/* inner_jr_solve / _inner_jr (relax.py:110-142): g = truncated JR solve of
+ * (D + wT) g = r, T = L (backward=0) or U (backward=1). */
+int rs_inner_jr(rs_matrix_t m, const void *r, void *g, int n_j, int backward, double omega, double gamma,
+                rs_stream_t stream);
+
+/* gs2_apply (relax.py:208-220) incl. _two_stage_sweep (193-205): x in place. */
+int rs_gs2_apply(rs_matrix_t m, const void *b, void *x, const rs_relax_cfg *cfg, rs_stream_t stream);
+
+/* hybrid_relax right-hand side (relax.py:261-264) for one row block:
+ * bhat = (b - A_full x) + A_pp x, with x_lo / x_hi the halo values. */
+int rs_hybrid_bhat(rs_matrix_t m, const void *b, const void *x, const void *x_lo, const void *x_hi, void *bhat,
+                   rs_stream_t stream);
+
+/* ---- preconditioner (krylov.py:59-137) ---- */
+
+/* z = P(r): zero-start relaxation of kind RS_PC_* with cfg (sweeps = n_t*n_k
+ * for jr / gs_seq kinds).  r, z are float64.  If m is float32 the residual is
+ * rounded to float32 first (cast_vector, sparse.py:244-257) and z upcast; an
+ * overflowing entry lowers *overflow_flag (device int64 the caller initialises
+ * to INT64_MAX; may be NULL) to its index instead of raising, so the call
+ * stays asynchronous; the caller raises OverflowError when it reads it back. */
+int rs_precond_apply(rs_matrix_t m, int kind, const rs_relax_cfg *cfg, const double *r, double *z,
+                     int64_t *overflow_flag, rs_stream_t stream);
+
+/* ---- GMRES building blocks (krylov.py:162-250), float64 ----
+ * Reductions are deterministic (fixed block partition, partials summed in
+ * block order) and need a caller-owned device workspace of
+ * rs_reduce_work_doubles(k) doubles.  V is row-major: Arnoldi vector i is
+ * V + i*ldv.  h / y / nrm2 are device pointers. */
+
+int64_t rs_reduce_work_doubles(int k);
+
+/* h[i] = V_i . w for i < k (the dot half of one Gram-Schmidt pass,
+ * krylov.py:218).  nonfinite (device int, may be NULL) is set to 1 when w has
+ * a non-finite entry (krylov.py:157-159, 216). */
+int rs_gemv_t(const double *V, int64_t ldv, int k, int64_t n, const double *w, double *h, int *nonfinite,
+              double *work, rs_stream_t stream);
+
+/* w[r] -= sum_{i<k} h[i] V_i[r] (the update half, krylov.py:219); if nrm2 is
+ * not NULL also nrm2[0] = w.w after the update (krylov.py:220). */
+int rs_gemv_n_update(const double *V, int64_t ldv, int k, int64_t n, const double *h, double *w, double *nrm2,
+                     double *work, rs_stream_t stream);
+
+/* out[r] = sum_{i<k} y[i] V_i[r]  (krylov.py:244 v[:j+1].T @ y) */
+int rs_gemv_n(const double *V, int64_t ldv, int k, int64_t n, const double *y, double *out, rs_stream_t stream);
+
+/* out = w / sqrt(nrm2[0])  (krylov.py:208, 223: v = w / ||w||) */
+int rs_scale_by_norm(int64_t n, const double *w, const double *nrm2, double *out, rs_stream_t stream);
+
+/* r = b - y and nrm2[0] = r.r  (krylov.py:193-194, 245-246) */
+int rs_sub_norm(int64_t n, const double *b, const double *y, double *r, double *nrm2, double *work,
+                rs_stream_t stream);
+
+/* out[0] = x.y */
+int rs_dot(int64_t n, const double *x, const double *y, double *out, double *work, rs_stream_t stream);
+
+/* x += z */
+int rs_axpy1(int64_t n, const double *z, double *x, rs_stream_t stream);
+
+/* ---- generators ---- */
+
+/* random_rhs (problems.py:228-242): out[i] = value number (offset+i) of the LCG
+ * seeded with `seed` (jump-ahead, bitwise identical to the sequential loop). */
+int rs_lcg_fill(uint64_t seed, int64_t offset, int64_t n, double *out, rs_stream_t stream);
+
+/* cast_vector (sparse.py:244-257) */
+int rs_cast_f64_f32(int64_t n, const double *in, float *out, int64_t *overflow_flag /* INT64_MAX-initialised */,
+                    rs_stream_t stream);
+int rs_cast_f32_f64(int64_t n, const float *in, double *out, rs_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,377 @@
+/*
+ * oracle.c -- CPU restatement of the reference GS2 path.  TEST INFRASTRUCTURE
+ * (parity checker + CPU baseline); see oracle.h for scope and citations.
+ * Build: oracle/Makefile  (gcc -O2 -ffp-contract=off -fopenmp -shared).
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+int orc_num_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+void orc_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
+#define T double
+#define SFX f64
+#include "oracle_t.inc"
+#undef T
+#undef SFX
+#define T float
+#define SFX f32
+#include "oracle_t.inc"
+#undef T
+#undef SFX
+
+int orc_split_build(const orc_csr *a, int is_f32, orc_split *s, int64_t *err_index) {
+  int st = is_f32 ? split_build_f32(a, s, err_index) : split_build_f64(a, s, err_index);
+  s->is_f32 = is_f32;
+  return st;
+}
+
+void orc_split_free(orc_split *s) {
+  free(s->d); free(s->l_rp); free(s->l_ci); free(s->u_rp); free(s->u_ci);
+  free(s->l_v); free(s->u_v); free(s->dl_v); free(s->du_v);
+  memset(s, 0, sizeof(*s));
+}
+
+static size_t esz(int is_f32) { return is_f32 ? sizeof(float) : sizeof(double); }
+
+int orc_jr_sweeps(const orc_csr *a, const orc_split *s, const void *b, void *x, int sweeps, double omega) {
+  void *t = malloc(esz(s->is_f32) * (size_t)(a->n ? a->n : 1));
+  if (s->is_f32) jr_sweeps_f32(a, s, (const float *)b, (float *)x, sweeps, omega, (float *)t);
+  else jr_sweeps_f64(a, s, (const double *)b, (double *)x, sweeps, omega, (double *)t);
+  free(t);
+  return ORC_OK;
+}
+
+int orc_gs_sweep(const orc_csr *a, const orc_split *s, const void *b, void *x, int direction, double omega) {
+  for (int pass = 0; pass < 2; ++pass) {
+    int bwd = pass == 1;
+    if (direction == 0 && bwd) continue;
+    if (direction == 1 && !bwd) continue;
+    if (s->is_f32) gs_sweep_dir_f32(a, (const float *)s->d, (const float *)b, (float *)x, bwd, omega);
+    else gs_sweep_dir_f64(a, (const double *)s->d, (const double *)b, (double *)x, bwd, omega);
+  }
+  return ORC_OK;
+}
+
+int orc_inner_jr(const orc_split *s, const void *r, int n_j, int backward, double omega, double gamma, void *g_out) {
+  size_t n = (size_t)(s->n ? s->n : 1);
+  void *rd = malloc(esz(s->is_f32) * n), *t = malloc(esz(s->is_f32) * n);
+  if (s->is_f32) inner_jr_f32(s, (const float *)r, n_j, backward, omega, gamma, (float *)g_out, (float *)rd, (float *)t);
+  else inner_jr_f64(s, (const double *)r, n_j, backward, omega, gamma, (double *)g_out, (double *)rd, (double *)t);
+  free(rd); free(t);
+  return ORC_OK;
+}
+
+int orc_gs2_apply(const orc_csr *a, const orc_split *s, const void *b, void *x, const orc_cfg *cfg) {
+  void *w = malloc(esz(s->is_f32) * 4 * (size_t)(a->n ? a->n : 1));
+  if (s->is_f32) gs2_apply_f32(a, s, (const float *)b, (float *)x, cfg, (float *)w);
+  else gs2_apply_f64(a, s, (const double *)b, (double *)x, cfg, (double *)w);
+  free(w);
+  return ORC_OK;
+}
+
+int orc_hybrid_relax(const orc_csr *a, int is_f32, const int64_t *off, int nb, const void *b, void *x,
+                     const orc_cfg *cfg, int local, int64_t *err_index) {
+  size_t n = (size_t)(a->n ? a->n : 1);
+  int st;
+  if (is_f32) {
+    block_f32 *blk = (block_f32 *)calloc((size_t)nb, sizeof(block_f32));
+    st = blocks_build_f32(a, off, nb, blk, err_index);
+    if (!st) {
+      float *w = (float *)malloc(sizeof(float) * 7 * n);
+      hybrid_f32(a, blk, nb, (const float *)b, (float *)x, cfg, local, w);
+      free(w);
+    }
+    blocks_free_f32(blk, nb);
+    free(blk);
+  } else {
+    block_f64 *blk = (block_f64 *)calloc((size_t)nb, sizeof(block_f64));
+    st = blocks_build_f64(a, off, nb, blk, err_index);
+    if (!st) {
+      double *w = (double *)malloc(sizeof(double) * 7 * n);
+      hybrid_f64(a, blk, nb, (const double *)b, (double *)x, cfg, local, w);
+      free(w);
+    }
+    blocks_free_f64(blk, nb);
+    free(blk);
+  }
+  return st;
+}
+
+/* ---------------------------------------------------------------- preconditioner (krylov.py:59-137) */
+struct orc_precond {
+  int kind, single, nblocks;
+  orc_cfg cfg;
+  orc_csr a64, a32;
+  float *v32;
+  orc_split s64, s32;
+  block_f64 *blk64;
+  block_f32 *blk32;
+  int64_t n;
+  void *work; /* 7n of the working dtype */
+  void *rhs, *z;
+};
+
+orc_precond *orc_precond_create(const orc_csr *a64, int kind, const orc_cfg *cfg, int single, const int64_t *offsets,
+                                int nblocks, int64_t *err_index, int *status) {
+  orc_precond *p = (orc_precond *)calloc(1, sizeof(orc_precond));
+  int64_t n = a64->n;
+  p->kind = kind;
+  p->single = single;
+  p->cfg = *cfg;
+  p->n = n;
+  p->a64 = *a64;
+  p->nblocks = nblocks;
+  /* symmetric kinds force the symmetric direction (krylov.py:86-87) */
+  if (kind == ORC_SGS_SEQ || kind == ORC_SGS2) p->cfg.direction = 2;
+  *status = ORC_OK;
+  if (kind == ORC_NONE) return p;
+  int64_t nnz = a64->row_ptr[n];
+  if (single) {
+    /* cast_matrix (sparse.py:260-269): values rounded to float32, overflow is an error */
+    const double *v = (const double *)a64->values;
+    p->v32 = (float *)malloc(sizeof(float) * (size_t)(nnz ? nnz : 1));
+    for (int64_t k = 0; k < nnz; ++k) {
+      p->v32[k] = (float)v[k];
+      if (isinf(p->v32[k]) && isfinite(v[k])) { *err_index = k; *status = ORC_EOVERFLOW; return p; }
+    }
+    p->a32 = *a64;
+    p->a32.values = p->v32;
+  }
+  const orc_csr *aw = single ? &p->a32 : &p->a64;
+  if (kind == ORC_HYBRID_GS2 || kind == ORC_HYBRID_GS) {
+    if (single) {
+      p->blk32 = (block_f32 *)calloc((size_t)nblocks, sizeof(block_f32));
+      *status = blocks_build_f32(aw, offsets, nblocks, p->blk32, err_index);
+    } else {
+      p->blk64 = (block_f64 *)calloc((size_t)nblocks, sizeof(block_f64));
+      *status = blocks_build_f64(aw, offsets, nblocks, p->blk64, err_index);
+    }
+  } else {
+    *status = orc_split_build(aw, single, single ? &p->s32 : &p->s64, err_index);
+  }
+  size_t es = single ? sizeof(float) : sizeof(double);
+  p->work = malloc(es * 8 * (size_t)(n ? n : 1));
+  p->rhs = malloc(es * (size_t)(n ? n : 1));
+  p->z = malloc(es * (size_t)(n ? n : 1));
+  return p;
+}
+
+void orc_precond_free(orc_precond *p) {
+  if (!p) return;
+  free(p->v32);
+  if (p->s64.d) orc_split_free(&p->s64);
+  if (p->s32.d) orc_split_free(&p->s32);
+  if (p->blk64) { blocks_free_f64(p->blk64, p->nblocks); free(p->blk64); }
+  if (p->blk32) { blocks_free_f32(p->blk32, p->nblocks); free(p->blk32); }
+  free(p->work); free(p->rhs); free(p->z);
+  free(p);
+}
+
+#define PREC_BODY(T, SFX, aw, sw, blk)                                                          \
+  do {                                                                                          \
+    T *z = (T *)p->z, *rhs = (T *)p->rhs, *w = (T *)p->work;                                    \
+    memset(z, 0, sizeof(T) * (size_t)n);                                                        \
+    int sweeps = p->cfg.n_t * p->cfg.n_k;                                                       \
+    switch (p->kind) {                                                                          \
+      case ORC_JR: jr_sweeps_##SFX(aw, sw, rhs, z, sweeps, p->cfg.omega, w); break;            \
+      case ORC_GS_SEQ:                                                                          \
+      case ORC_SGS_SEQ:                                                                         \
+        for (int it = 0; it < sweeps; ++it) {                                                   \
+          if (p->cfg.direction != 1) gs_sweep_dir_##SFX(aw, (const T *)(sw)->d, rhs, z, 0, p->cfg.omega); \
+          if (p->cfg.direction != 0) gs_sweep_dir_##SFX(aw, (const T *)(sw)->d, rhs, z, 1, p->cfg.omega); \
+        }                                                                                       \
+        break;                                                                                  \
+      case ORC_GS2:                                                                             \
+      case ORC_SGS2: gs2_apply_##SFX(aw, sw, rhs, z, &p->cfg, w); break;                        \
+      case ORC_HYBRID_GS2: hybrid_##SFX(aw, blk, p->nblocks, rhs, z, &p->cfg, 1, w); break;     \
+      case ORC_HYBRID_GS: hybrid_##SFX(aw, blk, p->nblocks, rhs, z, &p->cfg, 0, w); break;      \
+    }                                                                                           \
+  } while (0)
+
+int orc_precond_apply(orc_precond *p, const double *r, double *zout, int64_t *err_index) {
+  int64_t n = p->n;
+  if (p->kind == ORC_NONE) { memcpy(zout, r, sizeof(double) * (size_t)n); return ORC_OK; }
+  if (p->single) {
+    /* cast_vector (sparse.py:244-257): finite inputs that overflow float32 are an error */
+    float *rhs = (float *)p->rhs;
+    for (int64_t i = 0; i < n; ++i) {
+      rhs[i] = (float)r[i];
+      if (isinf(rhs[i]) && isfinite(r[i])) { *err_index = i; return ORC_EOVERFLOW; }
+    }
+    PREC_BODY(float, f32, &p->a32, &p->s32, p->blk32);
+    const float *z = (const float *)p->z;
+    for (int64_t i = 0; i < n; ++i) zout[i] = (double)z[i];
+  } else {
+    memcpy(p->rhs, r, sizeof(double) * (size_t)n);
+    PREC_BODY(double, f64, &p->a64, &p->s64, p->blk64);
+    memcpy(zout, p->z, sizeof(double) * (size_t)n);
+  }
+  return ORC_OK;
+}
+
+/* ---------------------------------------------------------------- BLAS-1 */
+#define DOT_CHUNK 4096
+double orc_dot(int64_t n, const double *x, const double *y) {
+  int64_t nc = (n + DOT_CHUNK - 1) / DOT_CHUNK;
+  if (nc <= 1) {
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) { double p = x[i] * y[i]; s = s + p; }
+    return s;
+  }
+  double *part = (double *)malloc(sizeof(double) * (size_t)nc);
+#pragma omp parallel for schedule(static) if (n > 65536)
+  for (int64_t c = 0; c < nc; ++c) {
+    int64_t lo = c * DOT_CHUNK, hi = lo + DOT_CHUNK < n ? lo + DOT_CHUNK : n;
+    double s = 0.0;
+    for (int64_t i = lo; i < hi; ++i) { double p = x[i] * y[i]; s = s + p; }
+    part[c] = s;
+  }
+  double s = 0.0;
+  for (int64_t c = 0; c < nc; ++c) s = s + part[c];
+  free(part);
+  return s;
+}
+
+static double nrm2(int64_t n, const double *x) { return sqrt(orc_dot(n, x, x)); }
+
+/* ---------------------------------------------------------------- GMRES (krylov.py:162-250) */
+#define BREAKDOWN_RTOL 1e-14
+
+int orc_gmres(const orc_csr *a, const double *b, orc_precond *m, int restart, double tol, int maxit,
+              const double *x0, double *x, double *hist, int *iters, int *conv) {
+  int64_t n = a->n;
+  int nh = 0;
+  *iters = 0;
+  *conv = 0;
+  if (x0) memcpy(x, x0, sizeof(double) * (size_t)n);
+  else memset(x, 0, sizeof(double) * (size_t)n);
+  double bnorm = nrm2(n, b);
+  if (bnorm == 0.0) {
+    memset(x, 0, sizeof(double) * (size_t)n);
+    hist[0] = 0.0;
+    *conv = 1;
+    return ORC_OK;
+  }
+  double *r = (double *)malloc(sizeof(double) * (size_t)n);
+  double *t = (double *)malloc(sizeof(double) * (size_t)n);
+  double *w = (double *)malloc(sizeof(double) * (size_t)n);
+  double *z = (double *)malloc(sizeof(double) * (size_t)n);
+  double *v = (double *)malloc(sizeof(double) * (size_t)n * (size_t)(restart + 1));
+  double *h = (double *)malloc(sizeof(double) * (size_t)(restart + 1) * (size_t)restart);
+  double *cs = (double *)malloc(sizeof(double) * (size_t)restart);
+  double *sn = (double *)malloc(sizeof(double) * (size_t)restart);
+  double *g = (double *)malloc(sizeof(double) * (size_t)(restart + 1));
+  double *y = (double *)malloc(sizeof(double) * (size_t)(restart + 1));
+  int status = ORC_OK;
+  int64_t ei = 0;
+#define H(i, j) h[(size_t)(i) * (size_t)restart + (size_t)(j)]
+  orc_spmv_f64(a, x, t);
+  for (int64_t i = 0; i < n; ++i) r[i] = b[i] - t[i];
+  hist[nh++] = nrm2(n, r) / bnorm;
+  if (hist[0] <= tol) { *conv = 1; goto done; }
+  int total = 0, converged = 0;
+  double breakdown_tol = BREAKDOWN_RTOL * bnorm;
+  while (total < maxit && !converged) {
+    double beta = nrm2(n, r);
+    memset(h, 0, sizeof(double) * (size_t)(restart + 1) * (size_t)restart);
+    memset(cs, 0, sizeof(double) * (size_t)restart);
+    memset(sn, 0, sizeof(double) * (size_t)restart);
+    memset(g, 0, sizeof(double) * (size_t)(restart + 1));
+    for (int64_t i = 0; i < n; ++i) v[i] = r[i] / beta;
+    g[0] = beta;
+    int j = -1, lucky = 0;
+    while (j + 1 < restart && total < maxit) {
+      ++j;
+      ++total;
+      if (m) { status = orc_precond_apply(m, v + (size_t)j * n, z, &ei); if (status) goto done; }
+      else memcpy(z, v + (size_t)j * n, sizeof(double) * (size_t)n);
+      orc_spmv_f64(a, z, w);
+      for (int64_t i = 0; i < n; ++i)
+        if (!isfinite(w[i])) { status = ORC_EDIVERGE; goto done; }
+      for (int i = 0; i <= j; ++i) { /* MGS (krylov.py:217-219) */
+        const double *vi = v + (size_t)i * n;
+        double hij = orc_dot(n, vi, w);
+        H(i, j) = hij;
+        for (int64_t k = 0; k < n; ++k) { double p = hij * vi[k]; w[k] = w[k] - p; }
+      }
+      H(j + 1, j) = nrm2(n, w);
+      lucky = H(j + 1, j) < breakdown_tol;
+      if (!lucky) {
+        double hh = H(j + 1, j);
+        double *vn = v + (size_t)(j + 1) * n;
+        for (int64_t k = 0; k < n; ++k) vn[k] = w[k] / hh;
+      }
+      for (int i = 0; i < j; ++i) { /* Givens (krylov.py:224-234) */
+        double a1 = cs[i] * H(i, j), a2 = sn[i] * H(i + 1, j);
+        double hi = a1 + a2;
+        double b1 = -sn[i] * H(i, j), b2 = cs[i] * H(i + 1, j);
+        H(i + 1, j) = b1 + b2;
+        H(i, j) = hi;
+      }
+      double denom = hypot(H(j, j), H(j + 1, j));
+      cs[j] = H(j, j) / denom;
+      sn[j] = H(j + 1, j) / denom;
+      H(j, j) = denom;
+      H(j + 1, j) = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      double est = fabs(g[j + 1]) / bnorm;
+      if (!isfinite(est)) { status = ORC_EDIVERGE; goto done; }
+      hist[nh++] = est;
+      if (est <= tol || lucky) break;
+    }
+    for (int i = j; i >= 0; --i) { /* back substitution (krylov.py:241-243) */
+      double s = 0.0;
+      for (int k = i + 1; k <= j; ++k) { double p = H(i, k) * y[k]; s = s + p; }
+      y[i] = (g[i] - s) / H(i, i);
+    }
+    for (int64_t k = 0; k < n; ++k) { /* V^T y (krylov.py:244) */
+      double s = 0.0;
+      for (int i = 0; i <= j; ++i) { double p = v[(size_t)i * n + k] * y[i]; s = s + p; }
+      t[k] = s;
+    }
+    if (m) { status = orc_precond_apply(m, t, z, &ei); if (status) goto done; }
+    else memcpy(z, t, sizeof(double) * (size_t)n);
+    for (int64_t k = 0; k < n; ++k) x[k] = x[k] + z[k];
+    orc_spmv_f64(a, x, t);
+    for (int64_t k = 0; k < n; ++k) r[k] = b[k] - t[k];
+    double true_rel = nrm2(n, r) / bnorm;
+    hist[nh - 1] = true_rel;
+    if (lucky || true_rel <= tol) converged = 1;
+  }
+  *conv = converged;
+#undef H
+done:
+  *iters = nh - 1;
+  free(r); free(t); free(w); free(z); free(v); free(h); free(cs); free(sn); free(g); free(y);
+  return status;
+}
+
+/* ---------------------------------------------------------------- random_rhs (problems.py:228-242) */
+void orc_random_rhs(int64_t n, uint64_t seed, double *out) {
+  uint64_t s = seed;
+  for (int64_t i = 0; i < n; ++i) {
+    s = 6364136223846793005ULL * s + 1442695040888963407ULL;
+    out[i] = (double)(s >> 11) * 0x1p-53 * 2.0 - 1.0;
+  }
+}

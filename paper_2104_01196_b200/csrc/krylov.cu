@@ -1,0 +1,372 @@
+// krylov.cu -- tall-skinny GEMV / dot kernels for GMRES(m) with CGS2
+// orthogonalisation (replacing the MGS loop of krylov.py:217-220), vector
+// helpers, the device LCG (problems.py:228-242) and precision casts.
+//
+// Reductions are deterministic: a fixed grid of kRedBlocks persistent blocks
+// each owns one contiguous row range, writes one partial per output, and a
+// single-block second pass sums the partials in block order.
+#include <algorithm>
+
+#include "rs_internal.cuh"
+
+namespace rs {
+
+constexpr int kRedBlocks = 2 * 148;  // 2 persistent blocks per SM
+constexpr int kDotThreads = 512;     // 16 warps
+constexpr int kDotWarps = kDotThreads / 32;
+constexpr int kMaxQ = 8;             // vectors per warp per call -> k <= 128
+constexpr int kMaxK = kDotWarps * kMaxQ;
+constexpr int kTile = 2048;          // rows of w staged in shared memory per step
+
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+// partial[blk*k + i] = sum over the block's rows of V_i[r] * w[r]
+__global__ void __launch_bounds__(kDotThreads) k_gemv_t(const double* __restrict__ V, int64_t ldv, int k, int64_t n,
+                                                        const double* __restrict__ w, double* __restrict__ partial,
+                                                        int* nonfinite) {
+  __shared__ double ws[kTile];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t chunk = ((n + gridDim.x - 1) / gridDim.x + 31) & ~int64_t(31);
+  const int64_t r0 = (int64_t)blockIdx.x * chunk;
+  const int64_t r1 = n < r0 + chunk ? n : r0 + chunk;
+  double acc[kMaxQ];
+#pragma unroll
+  for (int q = 0; q < kMaxQ; ++q) acc[q] = 0.0;
+  bool bad = false;
+  for (int64_t t0 = r0; t0 < r1; t0 += kTile) {
+    const int len = (int)(r1 - t0 < kTile ? r1 - t0 : kTile);
+    __syncthreads();
+    for (int r = threadIdx.x; r < len; r += kDotThreads) {
+      double v = w[t0 + r];
+      bad |= !isfinite(v);
+      ws[r] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kMaxQ; ++q) {
+      const int i = warp + q * kDotWarps;
+      if (i < k) {
+        const double* vi = V + (int64_t)i * ldv + t0;
+        double a = acc[q];
+        for (int r = lane; r < len; r += 32) a += vi[r] * ws[r];
+        acc[q] = a;
+      }
+    }
+  }
+  if (nonfinite && __syncthreads_or(bad) && threadIdx.x == 0) *nonfinite = 1;
+#pragma unroll
+  for (int q = 0; q < kMaxQ; ++q) {
+    const int i = warp + q * kDotWarps;
+    if (i < k) {
+      double s = warp_sum(acc[q]);
+      if (lane == 0) partial[(int64_t)blockIdx.x * k + i] = s;
+    }
+  }
+}
+
+// out[i] (+)= sum_b partial[b*k + i], b ascending
+__global__ void k_reduce_partials(const double* __restrict__ partial, int nblk, int k, double* __restrict__ out,
+                                  int accumulate) {
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += partial[(int64_t)b * k + i];
+    out[i] = accumulate ? out[i] + s : s;
+  }
+}
+
+// w[r] -= sum_i h[i] V_i[r]; optional partial of w.w per block
+template <bool NORM>
+__global__ void __launch_bounds__(256) k_gemv_n_update(const double* __restrict__ V, int64_t ldv, int k, int64_t n,
+                                                       const double* __restrict__ h, double* __restrict__ w,
+                                                       double* __restrict__ partial) {
+  extern __shared__ double hs[];
+  for (int i = threadIdx.x; i < k; i += blockDim.x) hs[i] = h[i];
+  __syncthreads();
+  double nrm = 0.0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    int i = 0;
+    for (; i + 4 <= k; i += 4) {
+      double v0 = V[(int64_t)i * ldv + r], v1 = V[(int64_t)(i + 1) * ldv + r];
+      double v2 = V[(int64_t)(i + 2) * ldv + r], v3 = V[(int64_t)(i + 3) * ldv + r];
+      s += hs[i] * v0;
+      s += hs[i + 1] * v1;
+      s += hs[i + 2] * v2;
+      s += hs[i + 3] * v3;
+    }
+    for (; i < k; ++i) s += hs[i] * V[(int64_t)i * ldv + r];
+    double wn = w[r] - s;
+    w[r] = wn;
+    if (NORM) nrm += wn * wn;
+  }
+  if (NORM) {
+    __shared__ double red[8];
+    nrm = warp_sum(nrm);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q];
+      partial[blockIdx.x] = t;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_gemv_n(const double* __restrict__ V, int64_t ldv, int k, int64_t n,
+                                                const double* __restrict__ y, double* __restrict__ out) {
+  extern __shared__ double ys[];
+  for (int i = threadIdx.x; i < k; i += blockDim.x) ys[i] = y[i];
+  __syncthreads();
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int i = 0; i < k; ++i) s += ys[i] * V[(int64_t)i * ldv + r];
+    out[r] = s;
+  }
+}
+
+__global__ void k_scale_by_norm(int64_t n, const double* __restrict__ w, const double* __restrict__ nrm2,
+                                double* __restrict__ out) {
+  const double h = sqrt(nrm2[0]);
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    out[r] = w[r] / h;
+}
+
+// r = b - y; partial of r.r
+__global__ void __launch_bounds__(256) k_sub_norm(int64_t n, const double* __restrict__ b, const double* __restrict__ y,
+                                                  double* __restrict__ r, double* __restrict__ partial) {
+  double nrm = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double v = b[i] - y[i];
+    if (r) r[i] = v;
+    nrm += v * v;
+  }
+  __shared__ double red[8];
+  nrm = warp_sum(nrm);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q];
+    partial[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_dot(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
+                                             double* __restrict__ partial) {
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    acc += x[i] * y[i];
+  __shared__ double red[8];
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q];
+    partial[blockIdx.x] = t;
+  }
+}
+
+__global__ void k_axpy1(int64_t n, const double* __restrict__ z, double* __restrict__ x) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = x[i] + z[i];
+}
+
+// ------------------------------------------------------------------ LCG (problems.py:228-242)
+// state_m = A^m seed + C_m with the affine map s -> a s + c; jump-ahead by
+// composing the precomputed power-of-two maps.
+struct Affine {
+  unsigned long long a, c;
+};
+__host__ __device__ inline Affine compose(Affine f, Affine g) {  // g after f
+  return Affine{g.a * f.a, g.a * f.c + g.c};
+}
+
+struct LcgTable {
+  Affine pow2[64];
+  Affine stride;
+};
+
+__global__ void k_lcg(unsigned long long seed, int64_t offset, int64_t n, double* __restrict__ out, LcgTable tab) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  // state after (offset + i + 1) steps
+  unsigned long long m = (unsigned long long)(offset + i + 1);
+  Affine f{1ull, 0ull};
+  for (int b = 0; m; ++b, m >>= 1)
+    if (m & 1) f = compose(f, tab.pow2[b]);
+  unsigned long long s = f.a * seed + f.c;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  for (; i < n; i += step) {
+    out[i] = __dsub_rn(__dmul_rn(__dmul_rn((double)(s >> 11), 0x1p-53), 2.0), 1.0);
+    s = tab.stride.a * s + tab.stride.c;
+  }
+}
+
+__global__ void k_cast_down(int64_t n, const double* __restrict__ in, float* __restrict__ out, long long* flag) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double v = in[i];
+  float f = (float)v;
+  out[i] = f;
+  if (flag && isinf(f) && isfinite(v)) atomicMin(flag, (long long)i);
+}
+
+__global__ void k_cast_up(int64_t n, const float* __restrict__ in, double* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (double)in[i];
+}
+
+static int grid_stride_blocks(int64_t n) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+}
+
+}  // namespace rs
+
+using namespace rs;
+
+extern "C" {
+
+int64_t rs_reduce_work_doubles(int k) { return (int64_t)kRedBlocks * std::max(k, 1); }
+
+int rs_gemv_t(const double* V, int64_t ldv, int k, int64_t n, const double* w, double* h, int* nonfinite,
+              double* work, rs_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (k < 0 || n < 0 || !work) {
+    set_error(RS_ERR_ARG, "rs_gemv_t: bad arguments");
+    return RS_ERR_ARG;
+  }
+  for (int k0 = 0; k0 < k; k0 += kMaxK) {
+    int kk = std::min(kMaxK, k - k0);
+    k_gemv_t<<<kRedBlocks, kDotThreads, 0, st>>>(V + (int64_t)k0 * ldv, ldv, kk, n, w, work,
+                                                  k0 == 0 ? nonfinite : nullptr);
+    RS_COUNT_LAUNCH();
+    k_reduce_partials<<<1, 128, 0, st>>>(work, kRedBlocks, kk, h + k0, 0);
+    RS_COUNT_LAUNCH();
+  }
+  RS_CHECK_LAUNCH("rs_gemv_t");
+  return RS_OK;
+}
+
+int rs_gemv_n_update(const double* V, int64_t ldv, int k, int64_t n, const double* h, double* w, double* nrm2,
+                     double* work, rs_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (k < 0 || n < 0 || (nrm2 && !work)) {
+    set_error(RS_ERR_ARG, "rs_gemv_n_update: bad arguments");
+    return RS_ERR_ARG;
+  }
+  size_t sm = sizeof(double) * std::max(k, 1);
+  if (nrm2) {
+    k_gemv_n_update<true><<<kRedBlocks, 256, sm, st>>>(V, ldv, k, n, h, w, work);
+    RS_COUNT_LAUNCH();
+    k_reduce_partials<<<1, 32, 0, st>>>(work, kRedBlocks, 1, nrm2, 0);
+    RS_COUNT_LAUNCH();
+  } else {
+    k_gemv_n_update<false><<<kRedBlocks, 256, sm, st>>>(V, ldv, k, n, h, w, nullptr);
+    RS_COUNT_LAUNCH();
+  }
+  RS_CHECK_LAUNCH("rs_gemv_n_update");
+  return RS_OK;
+}
+
+int rs_gemv_n(const double* V, int64_t ldv, int k, int64_t n, const double* y, double* out, rs_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n) {
+    k_gemv_n<<<grid_stride_blocks(n), 256, sizeof(double) * std::max(k, 1), st>>>(V, ldv, k, n, y, out);
+    RS_COUNT_LAUNCH();
+  }
+  RS_CHECK_LAUNCH("rs_gemv_n");
+  return RS_OK;
+}
+
+int rs_scale_by_norm(int64_t n, const double* w, const double* nrm2, double* out, rs_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n) {
+    k_scale_by_norm<<<grid_stride_blocks(n), 256, 0, st>>>(n, w, nrm2, out);
+    RS_COUNT_LAUNCH();
+  }
+  RS_CHECK_LAUNCH("rs_scale_by_norm");
+  return RS_OK;
+}
+
+int rs_sub_norm(int64_t n, const double* b, const double* y, double* r, double* nrm2, double* work,
+                rs_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  k_sub_norm<<<kRedBlocks, 256, 0, st>>>(n, b, y, r, work);
+  RS_COUNT_LAUNCH();
+  k_reduce_partials<<<1, 32, 0, st>>>(work, kRedBlocks, 1, nrm2, 0);
+  RS_COUNT_LAUNCH();
+  RS_CHECK_LAUNCH("rs_sub_norm");
+  return RS_OK;
+}
+
+int rs_dot(int64_t n, const double* x, const double* y, double* out, double* work, rs_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  k_dot<<<kRedBlocks, 256, 0, st>>>(n, x, y, work);
+  RS_COUNT_LAUNCH();
+  k_reduce_partials<<<1, 32, 0, st>>>(work, kRedBlocks, 1, out, 0);
+  RS_COUNT_LAUNCH();
+  RS_CHECK_LAUNCH("rs_dot");
+  return RS_OK;
+}
+
+int rs_axpy1(int64_t n, const double* z, double* x, rs_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n) {
+    k_axpy1<<<grid_stride_blocks(n), 256, 0, st>>>(n, z, x);
+    RS_COUNT_LAUNCH();
+  }
+  RS_CHECK_LAUNCH("rs_axpy1");
+  return RS_OK;
+}
+
+int rs_lcg_fill(uint64_t seed, int64_t offset, int64_t n, double* out, rs_stream_t stream) {
+  if (n < 0 || offset < 0) {
+    set_error(RS_ERR_ARG, "n must be nonnegative");
+    return RS_ERR_ARG;
+  }
+  if (n == 0) return RS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  LcgTable tab;
+  Affine f{6364136223846793005ull, 1442695040888963407ull};
+  for (int b = 0; b < 64; ++b) {
+    tab.pow2[b] = f;
+    f = compose(f, f);
+  }
+  int block = 256;
+  int grid = (int)std::min<int64_t>((n + block - 1) / block, 148 * 16);
+  unsigned long long stride = (unsigned long long)grid * block;
+  Affine s{1ull, 0ull};
+  for (int b = 0; stride; ++b, stride >>= 1)
+    if (stride & 1) s = compose(s, tab.pow2[b]);
+  tab.stride = s;
+  k_lcg<<<grid, block, 0, st>>>(seed, offset, n, out, tab);
+  RS_COUNT_LAUNCH();
+  RS_CHECK_LAUNCH("rs_lcg_fill");
+  return RS_OK;
+}
+
+int rs_cast_f64_f32(int64_t n, const double* in, float* out, int64_t* overflow_flag, rs_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n) {
+    k_cast_down<<<grid_for(n, 256), 256, 0, st>>>(n, in, out, (long long*)overflow_flag);
+    RS_COUNT_LAUNCH();
+  }
+  RS_CHECK_LAUNCH("rs_cast_f64_f32");
+  return RS_OK;
+}
+
+int rs_cast_f32_f64(int64_t n, const float* in, double* out, rs_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n) {
+    k_cast_up<<<grid_for(n, 256), 256, 0, st>>>(n, in, out);
+    RS_COUNT_LAUNCH();
+  }
+  RS_CHECK_LAUNCH("rs_cast_f32_f64");
+  return RS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,766 @@
+// matrix.cu -- device-resident split matrices (CsrMatrix + extract_splitting,
+// sparse.py:31-103 / 195-232) and stencil generators (problems.py:58-97).
+//
+// Construction is a two-pass device build shared by every row source (an
+// uploaded CSR or an on-device stencil): (1) count the entries of each row in
+// the five column ranges  [0,row0) | [row0,i) | i | (i,row0+nrows) | rest
+// (= E_lo, L, D, U, E_hi), validate the diagonal, take per-slice maxima;
+// (2) exclusive-scan the slice widths and scatter every row into its SELL-32
+// slots, keeping ascending column order and padding with col = -1.
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "rs_internal.cuh"
+
+namespace rs {
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static thread_local std::string g_err;
+static thread_local int64_t g_err_index = -1;
+
+void set_error(int code, const std::string& msg, int64_t index) {
+  (void)code;
+  g_err = msg;
+  g_err_index = index;
+}
+
+int cuda_error(cudaError_t e, const char* where) {
+  set_error(RS_ERR_CUDA, std::string("CUDA error ") + cudaGetErrorString(e) + " in " + where);
+  return RS_ERR_CUDA;
+}
+
+// ------------------------------------------------------------------ row sources
+struct CsrSource {
+  const int64_t* rp;  // local row pointer [nrows+1] (rp[0] may be nonzero)
+  const int64_t* ci;  // global columns
+  const double* v64;
+  const float* v32;
+  __device__ int64_t len(int64_t i) const { return rp[i + 1] - rp[i]; }
+  __device__ void entry(int64_t i, int64_t k, int64_t& c, double& v) const {
+    int64_t p = rp[i] + k;
+    c = ci[p];
+    v = v64 ? v64[p] : (double)v32[p];
+  }
+};
+
+struct StencilSource {
+  int kind;
+  int64_t nx, ny, nz, row0;
+  double off[3];  // value of the backward neighbour along x, y, z
+  double diag;
+  // neighbours in ascending column order: -z, -y, -x, diag, +x, +y, +z
+  __device__ int gather(int64_t i, int64_t* c, double* v) const {
+    int64_t g = row0 + i;
+    int64_t ix, iy, iz;
+    if (kind == RS_STENCIL_LAPLACE2D) {
+      ix = g % nx; iy = g / nx; iz = 0;
+    } else {
+      ix = g % nx; iy = (g / nx) % ny; iz = g / (nx * ny);
+    }
+    int m = 0;
+    const int64_t sy = nx, sz = nx * ny;
+    if (kind != RS_STENCIL_LAPLACE2D && iz > 0) { c[m] = g - sz; v[m] = off[2]; ++m; }
+    if (iy > 0) { c[m] = g - sy; v[m] = off[1]; ++m; }
+    if (ix > 0) { c[m] = g - 1; v[m] = off[0]; ++m; }
+    c[m] = g; v[m] = diag; ++m;
+    if (ix + 1 < nx) { c[m] = g + 1; v[m] = -1.0; ++m; }
+    if (iy + 1 < ny) { c[m] = g + sy; v[m] = -1.0; ++m; }
+    if (kind != RS_STENCIL_LAPLACE2D && iz + 1 < nz) { c[m] = g + sz; v[m] = -1.0; ++m; }
+    return m;
+  }
+  __device__ int64_t len(int64_t i) const {
+    int64_t c[7];
+    double v[7];
+    return gather(i, c, v);
+  }
+  __device__ void entry(int64_t i, int64_t k, int64_t& cc, double& vv) const {
+    int64_t c[7];
+    double v[7];
+    gather(i, c, v);
+    cc = c[k];
+    vv = v[k];
+  }
+};
+
+struct BuildShape {
+  int64_t nrows, row0, rowe;  // local rows, first global row, one past last
+};
+
+__device__ __forceinline__ int range_of(int64_t c, int64_t g, const BuildShape& s) {
+  if (c < s.row0) return 2;   // E_lo
+  if (c < g) return 0;        // L
+  if (c == g) return 4;       // D
+  if (c < s.rowe) return 1;   // U
+  return 3;                   // E_hi
+}
+
+struct CountOut {
+  int32_t* width[4];  // per-slice width of L, U, Elo, Ehi
+  unsigned long long* nnz;  // [4] stored entries
+  long long* bad_row;       // min bad row (diag missing/zero/non-finite)
+  long long* min_col;
+  long long* max_col;
+  double* diag;             // [nrows]
+  int* unsorted;            // rows not strictly increasing
+};
+
+template <class Src>
+__global__ void k_count(Src src, BuildShape s, CountOut o) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int lane = threadIdx.x & 31;
+  int cnt[4] = {0, 0, 0, 0};
+  if (i < s.nrows) {
+    int64_t g = s.row0 + i;
+    int64_t n = src.len(i);
+    bool have = false;
+    double dv = 0.0;
+    int64_t prev = -1;
+    long long mn = LLONG_MAX, mx = -1;
+    for (int64_t k = 0; k < n; ++k) {
+      int64_t c;
+      double v;
+      src.entry(i, k, c, v);
+      if (c <= prev) atomicOr(o.unsorted, 1);
+      prev = c;
+      int r = range_of(c, g, s);
+      if (r == 4) { have = true; dv = v; }
+      else ++cnt[r];
+      if (c < mn) mn = c;
+      if (c > mx) mx = c;
+    }
+    o.diag[i] = dv;
+    if (!have || !isfinite(dv) || dv == 0.0) atomicMin(o.bad_row, (long long)g);
+    if (mn != LLONG_MAX) { atomicMin(o.min_col, mn); atomicMax(o.max_col, mx); }
+    for (int r = 0; r < 4; ++r)
+      if (cnt[r]) atomicAdd(&o.nnz[r], (unsigned long long)cnt[r]);
+  }
+  // per-slice (warp) maxima; blockDim is a multiple of 32 and slices align with warps
+  for (int r = 0; r < 4; ++r) {
+    int w = cnt[r];
+    for (int off = 16; off > 0; off >>= 1) w = max(w, __shfl_xor_sync(0xffffffffu, w, off));
+    int64_t slice = i >> 5;
+    if (lane == 0 && slice * 32 < s.nrows) o.width[r][slice] = w;
+  }
+}
+
+__global__ void k_widths_to_slots(const int32_t* w, int64_t* slots, int64_t ns) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < ns) slots[s] = (int64_t)w[s] * kSlice;
+  if (s == ns) slots[s] = 0;
+}
+
+template <typename T>
+struct SellOut {
+  const int64_t* sp;
+  int32_t* col;
+  T* val;
+  T* dval;
+  int64_t base;  // column base subtracted (0 for L/U, halo base for E)
+};
+
+template <class Src, typename T>
+__global__ void k_fill(Src src, BuildShape s, SellOut<T> L, SellOut<T> U, SellOut<T> Elo, SellOut<T> Ehi,
+                       const double* diag) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= s.nrows) return;
+  int64_t g = s.row0 + i;
+  int64_t slice = i >> 5, lane = i & 31;
+  int64_t pos[4] = {0, 0, 0, 0};
+  SellOut<T>* outs[4] = {&L, &U, &Elo, &Ehi};
+  T d = (T)diag[i];
+  int64_t n = src.len(i);
+  for (int64_t k = 0; k < n; ++k) {
+    int64_t c;
+    double v;
+    src.entry(i, k, c, v);
+    int r = range_of(c, g, s);
+    if (r == 4) continue;
+    SellOut<T>& o = *outs[r];
+    int64_t slot = o.sp[slice] + pos[r] * kSlice + lane;
+    o.col[slot] = (int32_t)(c - o.base);
+    T tv = (T)v;
+    o.val[slot] = tv;
+    if (o.dval) o.dval[slot] = div_rn<T>(tv, d);  // dinv_l = l / d[row] (sparse.py:227)
+    ++pos[r];
+  }
+  // pad the rest of this row's slots in each triangle
+  for (int r = 0; r < 4; ++r) {
+    SellOut<T>& o = *outs[r];
+    int64_t w = (o.sp[slice + 1] - o.sp[slice]) / kSlice;
+    for (int64_t j = pos[r]; j < w; ++j) {
+      int64_t slot = o.sp[slice] + j * kSlice + lane;
+      o.col[slot] = -1;
+      o.val[slot] = (T)0;
+      if (o.dval) o.dval[slot] = (T)0;
+    }
+  }
+}
+
+// padding of slices past nrows (last partial slice): rows >= nrows never run k_fill
+template <typename T>
+__global__ void k_pad_tail(SellOut<T> o, int64_t nrows) {
+  int64_t slice = (nrows - 1) >> 5;
+  int lane = threadIdx.x;
+  int64_t row = slice * 32 + lane;
+  if (row < nrows) return;
+  int64_t w = (o.sp[slice + 1] - o.sp[slice]) / kSlice;
+  for (int64_t j = 0; j < w; ++j) {
+    int64_t slot = o.sp[slice] + j * kSlice + lane;
+    o.col[slot] = -1;
+    o.val[slot] = (T)0;
+    if (o.dval) o.dval[slot] = (T)0;
+  }
+}
+
+template <typename T>
+__global__ void k_cast_diag(const double* in, T* out, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (T)in[i];
+}
+
+template <typename T>
+static void free_sell(Sell<T>& s) {
+  cudaFree(s.slice_ptr);
+  cudaFree(s.col);
+  cudaFree(s.val);
+  cudaFree(s.dval);
+  s = Sell<T>();
+}
+
+static void free_levels(Levels& l) {
+  free(l.level_ptr_host);
+  cudaFree(l.rows);
+  l = Levels();
+}
+
+template <typename T>
+static int alloc_sell(Sell<T>& s, int64_t nrows, int64_t nnz, const int32_t* d_width, bool with_d) {
+  s.nrows = nrows;
+  s.nslices = (nrows + kSlice - 1) / kSlice;
+  s.nnz = nnz;
+  RS_CUDA(cudaMalloc(&s.slice_ptr, sizeof(int64_t) * (s.nslices + 1)));
+  // slice_ptr = exclusive scan of width*32
+  int64_t* tmp = nullptr;
+  RS_CUDA(cudaMalloc(&tmp, sizeof(int64_t) * (s.nslices + 1)));
+  k_widths_to_slots<<<grid_for(s.nslices + 1, 256), 256>>>(d_width, tmp, s.nslices);
+  RS_COUNT_LAUNCH();
+  RS_CHECK_LAUNCH("k_widths_to_slots");
+  size_t tb = 0;
+  RS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, tmp, s.slice_ptr, s.nslices + 1));
+  void* tbuf = nullptr;
+  RS_CUDA(cudaMalloc(&tbuf, tb));
+  RS_CUDA(cub::DeviceScan::ExclusiveSum(tbuf, tb, tmp, s.slice_ptr, s.nslices + 1));
+  RS_CUDA(cudaMemcpy(&s.nslots, s.slice_ptr + s.nslices, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  cudaFree(tbuf);
+  cudaFree(tmp);
+  size_t ns = (size_t)std::max<int64_t>(s.nslots, 1);
+  RS_CUDA(cudaMalloc(&s.col, sizeof(int32_t) * ns));
+  RS_CUDA(cudaMalloc(&s.val, sizeof(T) * ns));
+  if (with_d) RS_CUDA(cudaMalloc(&s.dval, sizeof(T) * ns));
+  return RS_OK;
+}
+
+template <typename T>
+static SellOut<T> out_of(Sell<T>& s, int64_t base) {
+  SellOut<T> o;
+  o.sp = s.slice_ptr;
+  o.col = s.col;
+  o.val = s.val;
+  o.dval = s.dval;
+  o.base = base;
+  return o;
+}
+
+template <class Src, typename T>
+static int build_split(rs_matrix* m, const Src& src) {
+  BuildShape s{m->nrows, m->row0, m->row0 + m->nrows};
+  int64_t ns = (m->nrows + kSlice - 1) / kSlice;
+  // scratch for counting
+  int32_t* width = nullptr;
+  unsigned long long* nnz = nullptr;
+  long long* stats = nullptr;  // bad_row, min_col, max_col
+  int* unsorted = nullptr;
+  double* diag = nullptr;
+  RS_CUDA(cudaMalloc(&width, sizeof(int32_t) * 4 * std::max<int64_t>(ns, 1)));
+  RS_CUDA(cudaMemset(width, 0, sizeof(int32_t) * 4 * std::max<int64_t>(ns, 1)));
+  RS_CUDA(cudaMalloc(&nnz, sizeof(unsigned long long) * 4));
+  RS_CUDA(cudaMemset(nnz, 0, sizeof(unsigned long long) * 4));
+  RS_CUDA(cudaMalloc(&stats, sizeof(long long) * 3));
+  long long init[3] = {LLONG_MAX, LLONG_MAX, -1};
+  RS_CUDA(cudaMemcpy(stats, init, sizeof(init), cudaMemcpyHostToDevice));
+  RS_CUDA(cudaMalloc(&unsorted, sizeof(int)));
+  RS_CUDA(cudaMemset(unsorted, 0, sizeof(int)));
+  RS_CUDA(cudaMalloc(&diag, sizeof(double) * std::max<int64_t>(m->nrows, 1)));
+  CountOut co;
+  for (int r = 0; r < 4; ++r) co.width[r] = width + r * std::max<int64_t>(ns, 1);
+  co.nnz = nnz;
+  co.bad_row = stats;
+  co.min_col = stats + 1;
+  co.max_col = stats + 2;
+  co.diag = diag;
+  co.unsorted = unsorted;
+  const int B = 256;
+  if (m->nrows > 0) {
+    k_count<Src><<<grid_for(ns * 32, B), B>>>(src, s, co);
+    RS_COUNT_LAUNCH();
+    RS_CHECK_LAUNCH("k_count");
+  }
+  unsigned long long hn[4];
+  long long hs[3];
+  int hu = 0;
+  RS_CUDA(cudaMemcpy(hn, nnz, sizeof(hn), cudaMemcpyDeviceToHost));
+  RS_CUDA(cudaMemcpy(hs, stats, sizeof(hs), cudaMemcpyDeviceToHost));
+  RS_CUDA(cudaMemcpy(&hu, unsorted, sizeof(int), cudaMemcpyDeviceToHost));
+  int status = RS_OK;
+  if (hu) {
+    set_error(RS_ERR_ARG, "column indices not strictly increasing within a row");
+    status = RS_ERR_ARG;
+  } else if (hs[0] != LLONG_MAX) {
+    set_error(RS_ERR_DIAG, "row " + std::to_string(hs[0]) + " has a missing, zero or non-finite diagonal entry",
+              hs[0]);
+    status = RS_ERR_DIAG;
+  } else if (hs[1] != LLONG_MAX && (hs[1] < 0 || hs[2] >= m->ncols)) {
+    set_error(RS_ERR_ARG, "column index out of range");
+    status = RS_ERR_ARG;
+  }
+  if (status == RS_OK) {
+    m->halo_lo = (hs[1] != LLONG_MAX && hs[1] < m->row0) ? m->row0 - hs[1] : 0;
+    m->halo_hi = (hs[2] >= s.rowe) ? hs[2] + 1 - s.rowe : 0;
+    m->nnz = (int64_t)(hn[0] + hn[1] + hn[2] + hn[3]) + m->nrows;
+    Sell<T>& L = tri<T>(m, 0);
+    Sell<T>& U = tri<T>(m, 1);
+    Sell<T>& Elo = tri<T>(m, 2);
+    Sell<T>& Ehi = tri<T>(m, 3);
+    int st = RS_OK;
+    if ((st = alloc_sell(L, m->nrows, (int64_t)hn[0], co.width[0], true))) status = st;
+    else if ((st = alloc_sell(U, m->nrows, (int64_t)hn[1], co.width[1], true))) status = st;
+    else if ((st = alloc_sell(Elo, m->nrows, (int64_t)hn[2], co.width[2], false))) status = st;
+    else if ((st = alloc_sell(Ehi, m->nrows, (int64_t)hn[3], co.width[3], false))) status = st;
+    if (status == RS_OK) {
+      T* d = nullptr;
+      if (cudaMalloc(&d, sizeof(T) * std::max<int64_t>(m->nrows, 1)) != cudaSuccess) {
+        status = cuda_error(cudaErrorMemoryAllocation, "cudaMalloc(d)");
+      } else {
+        m->d = d;
+        if (m->nrows > 0) {
+          k_cast_diag<T><<<grid_for(m->nrows, B), B>>>(diag, d, m->nrows);
+          RS_COUNT_LAUNCH();
+          k_fill<Src, T><<<grid_for(m->nrows, B), B>>>(src, s, out_of(L, 0), out_of(U, 0),
+                                                         out_of(Elo, m->row0 - m->halo_lo), out_of(Ehi, s.rowe),
+                                                         diag);
+          RS_COUNT_LAUNCH();
+          if (m->nrows % 32) {
+            k_pad_tail<T><<<1, 32>>>(out_of(L, 0), m->nrows);
+            RS_COUNT_LAUNCH();
+            k_pad_tail<T><<<1, 32>>>(out_of(U, 0), m->nrows);
+            RS_COUNT_LAUNCH();
+            k_pad_tail<T><<<1, 32>>>(out_of(Elo, 0), m->nrows);
+            RS_COUNT_LAUNCH();
+            k_pad_tail<T><<<1, 32>>>(out_of(Ehi, 0), m->nrows);
+            RS_COUNT_LAUNCH();
+          }
+          cudaError_t e = cudaDeviceSynchronize();
+          if (e != cudaSuccess) status = cuda_error(e, "k_fill");
+        }
+      }
+    }
+  }
+  cudaFree(width);
+  cudaFree(nnz);
+  cudaFree(stats);
+  cudaFree(unsorted);
+  cudaFree(diag);
+  return status;
+}
+
+void destroy(rs_matrix* m) {
+  if (!m) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(m->device);
+  cudaFree(m->d);
+  free_sell(m->L64); free_sell(m->U64); free_sell(m->Elo64); free_sell(m->Ehi64);
+  free_sell(m->L32); free_sell(m->U32); free_sell(m->Elo32); free_sell(m->Ehi32);
+  free_levels(m->fwd);
+  free_levels(m->bwd);
+  cudaFree(m->scratch);
+  cudaFree(m->scratch2);
+  cudaFree(m->red);
+  cudaFree(m->ticket);
+  cudaSetDevice(prev);
+  delete m;
+}
+
+int ensure_scratch(rs_matrix* m) {
+  if (m->scratch) return RS_OK;
+  size_t es = m->dtype == RS_F32 ? 4 : 8;
+  size_t n = (size_t)std::max<int64_t>(m->nrows, 1);
+  // [rd | g_a | g_b | alt/snapshot | f32 rhs | f32 z]
+  RS_CUDA(cudaMalloc(&m->scratch, es * 6 * n));
+  return RS_OK;
+}
+
+// ------------------------------------------------------------------ structural symmetry (host)
+// Needed by the level-scheduled GS: an in-place level sweep reads the OLD x
+// through U only if every a_ij (j>i) has a_ji stored (SURVEY.md §7 hard part 5).
+template <typename T>
+static int host_tri(const Sell<T>& s, std::vector<int64_t>& sp, std::vector<int32_t>& col) {
+  sp.resize(s.nslices + 1);
+  col.resize(std::max<int64_t>(s.nslots, 1));
+  RS_CUDA(cudaMemcpy(sp.data(), s.slice_ptr, sizeof(int64_t) * (s.nslices + 1), cudaMemcpyDeviceToHost));
+  if (s.nslots) RS_CUDA(cudaMemcpy(col.data(), s.col, sizeof(int32_t) * s.nslots, cudaMemcpyDeviceToHost));
+  return RS_OK;
+}
+
+template <typename T>
+int build_levels_t(rs_matrix* m, int backward) {
+  Levels& lv = backward ? m->bwd : m->fwd;
+  if (lv.rows) return RS_OK;
+  const Sell<T>& dep = backward ? tri<T>(m, 1) : tri<T>(m, 0);
+  const Sell<T>& oth = backward ? tri<T>(m, 0) : tri<T>(m, 1);
+  std::vector<int64_t> sp, sp2;
+  std::vector<int32_t> col, col2;
+  int st;
+  if ((st = host_tri(dep, sp, col))) return st;
+  if ((st = host_tri(oth, sp2, col2))) return st;
+  int64_t n = m->nrows;
+  std::vector<int32_t> level(n, 0);
+  auto row_cols = [&](const std::vector<int64_t>& p, const std::vector<int32_t>& c, int64_t i, auto&& f) {
+    int64_t s = i >> 5, lane = i & 31, w = (p[s + 1] - p[s]) / kSlice;
+    for (int64_t j = 0; j < w; ++j) {
+      int32_t cc = c[p[s] + j * kSlice + lane];
+      if (cc >= 0) f(cc);
+    }
+  };
+  int32_t maxl = 0;
+  if (!backward) {
+    for (int64_t i = 0; i < n; ++i) {
+      int32_t l = 0;
+      row_cols(sp, col, i, [&](int32_t c) { l = std::max(l, level[c] + 1); });
+      level[i] = l;
+      maxl = std::max(maxl, l);
+    }
+  } else {
+    for (int64_t i = n - 1; i >= 0; --i) {
+      int32_t l = 0;
+      row_cols(sp, col, i, [&](int32_t c) { l = std::max(l, level[c] + 1); });
+      level[i] = l;
+      maxl = std::max(maxl, l);
+    }
+  }
+  // structural symmetry: every entry (i, c) of the "other" triangle must appear as (c, i) in dep.
+  int sym = 1;
+  for (int64_t i = 0; i < n && sym; ++i) {
+    row_cols(sp2, col2, i, [&](int32_t c) {
+      if (!sym) return;
+      bool found = false;
+      row_cols(sp, col, c, [&](int32_t cc) { if (cc == i) found = true; });
+      if (!found) sym = 0;
+    });
+  }
+  m->structurally_symmetric = sym;
+  lv.nlevels = (int64_t)maxl + 1;
+  lv.level_ptr_host = (int64_t*)calloc(lv.nlevels + 1, sizeof(int64_t));
+  for (int64_t i = 0; i < n; ++i) lv.level_ptr_host[level[i] + 1]++;
+  for (int64_t l = 0; l < lv.nlevels; ++l) lv.level_ptr_host[l + 1] += lv.level_ptr_host[l];
+  std::vector<int64_t> fillp(lv.level_ptr_host, lv.level_ptr_host + lv.nlevels);
+  std::vector<int32_t> rows(std::max<int64_t>(n, 1));
+  for (int64_t i = 0; i < n; ++i) rows[fillp[level[i]]++] = (int32_t)i;
+  RS_CUDA(cudaMalloc(&lv.rows, sizeof(int32_t) * std::max<int64_t>(n, 1)));
+  RS_CUDA(cudaMemcpy(lv.rows, rows.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  return RS_OK;
+}
+
+int build_levels(rs_matrix* m, int backward) {
+  return m->dtype == RS_F32 ? build_levels_t<float>(m, backward) : build_levels_t<double>(m, backward);
+}
+
+// ------------------------------------------------------------------ export (tests / inspection)
+template <typename T>
+static int export_tri_t(rs_matrix* m, int which, int64_t* row_ptr, int64_t* col_idx, void* values, void* dvalues) {
+  const Sell<T>& s = tri<T>(m, which);
+  std::vector<int64_t> sp(s.nslices + 1);
+  std::vector<int32_t> col(std::max<int64_t>(s.nslots, 1));
+  std::vector<T> val(std::max<int64_t>(s.nslots, 1)), dval(std::max<int64_t>(s.nslots, 1));
+  RS_CUDA(cudaMemcpy(sp.data(), s.slice_ptr, sizeof(int64_t) * (s.nslices + 1), cudaMemcpyDeviceToHost));
+  if (s.nslots) {
+    RS_CUDA(cudaMemcpy(col.data(), s.col, sizeof(int32_t) * s.nslots, cudaMemcpyDeviceToHost));
+    RS_CUDA(cudaMemcpy(val.data(), s.val, sizeof(T) * s.nslots, cudaMemcpyDeviceToHost));
+    if (s.dval) RS_CUDA(cudaMemcpy(dval.data(), s.dval, sizeof(T) * s.nslots, cudaMemcpyDeviceToHost));
+  }
+  int64_t q = 0;
+  if (row_ptr) row_ptr[0] = 0;
+  for (int64_t i = 0; i < m->nrows; ++i) {
+    int64_t sl = i >> 5, lane = i & 31, w = (sp[sl + 1] - sp[sl]) / kSlice;
+    for (int64_t j = 0; j < w; ++j) {
+      int64_t slot = sp[sl] + j * kSlice + lane;
+      if (col[slot] < 0) continue;
+      if (col_idx) col_idx[q] = col[slot];
+      if (values) ((T*)values)[q] = val[slot];
+      if (dvalues && s.dval) ((T*)dvalues)[q] = dval[slot];
+      ++q;
+    }
+    if (row_ptr) row_ptr[i + 1] = q;
+  }
+  return RS_OK;
+}
+
+// ------------------------------------------------------------------ cast to float32
+__global__ void k_cast_vals(const double* in, float* out, int64_t n, long long* bad) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double v = in[i];
+  float f = (float)v;
+  out[i] = f;
+  if (isinf(f) && isfinite(v)) atomicMin(bad, (long long)i);
+}
+
+__global__ void k_recompute_dinv(const int32_t* col, const float* val, float* dval, const int64_t* sp, const float* d,
+                                 int64_t nrows) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  int64_t s = i >> 5, lane = i & 31, w = (sp[s + 1] - sp[s]) / kSlice;
+  float di = d[i];
+  for (int64_t j = 0; j < w; ++j) {
+    int64_t slot = sp[s] + j * kSlice + lane;
+    dval[slot] = col[slot] >= 0 ? __fdiv_rn(val[slot], di) : 0.0f;
+  }
+}
+
+static int cast_sell(const Sell<double>& a, Sell<float>& b, long long* bad, const float* d32) {
+  b.nrows = a.nrows;
+  b.nslices = a.nslices;
+  b.nnz = a.nnz;
+  b.nslots = a.nslots;
+  size_t ns = (size_t)std::max<int64_t>(a.nslots, 1);
+  RS_CUDA(cudaMalloc(&b.slice_ptr, sizeof(int64_t) * (a.nslices + 1)));
+  RS_CUDA(cudaMemcpy(b.slice_ptr, a.slice_ptr, sizeof(int64_t) * (a.nslices + 1), cudaMemcpyDeviceToDevice));
+  RS_CUDA(cudaMalloc(&b.col, sizeof(int32_t) * ns));
+  RS_CUDA(cudaMemcpy(b.col, a.col, sizeof(int32_t) * ns, cudaMemcpyDeviceToDevice));
+  RS_CUDA(cudaMalloc(&b.val, sizeof(float) * ns));
+  if (a.nslots) {
+    k_cast_vals<<<grid_for(a.nslots, 256), 256>>>(a.val, b.val, a.nslots, bad);
+    RS_COUNT_LAUNCH();
+  }
+  if (a.dval) {
+    RS_CUDA(cudaMalloc(&b.dval, sizeof(float) * ns));
+    if (a.nrows) {
+      k_recompute_dinv<<<grid_for(a.nrows, 256), 256>>>(b.col, b.val, b.dval, b.slice_ptr, d32, a.nrows);
+      RS_COUNT_LAUNCH();
+    }
+  }
+  RS_CHECK_LAUNCH("cast_sell");
+  return RS_OK;
+}
+
+}  // namespace rs
+
+using namespace rs;
+
+extern "C" {
+
+int rs_abi_version(void) { return RS_ABI_VERSION; }
+int64_t rs_launch_count(void) { return (int64_t)g_launches.load(); }
+const char* rs_last_error(void) { return g_err.c_str(); }
+int64_t rs_last_error_index(void) { return g_err_index; }
+
+int rs_mat_create_csr(int device, int64_t nrows, int64_t ncols, int64_t row0, const int64_t* row_ptr,
+                      const int64_t* col_idx, const void* values, int dtype, rs_matrix_t* out) {
+  if (!out || nrows < 0 || ncols < 0 || row0 < 0 || !row_ptr || (dtype != RS_F64 && dtype != RS_F32)) {
+    set_error(RS_ERR_ARG, "rs_mat_create_csr: bad arguments");
+    return RS_ERR_ARG;
+  }
+  if (row0 + nrows > ncols) {
+    set_error(RS_ERR_ARG, "splitting requires a square matrix");
+    return RS_ERR_ARG;
+  }
+  RS_CUDA(cudaSetDevice(device));
+  int64_t nnz = row_ptr[nrows] - row_ptr[0];
+  for (int64_t i = 0; i < nrows; ++i)
+    if (row_ptr[i + 1] < row_ptr[i]) {
+      set_error(RS_ERR_ARG, "row_ptr must be non-decreasing");
+      return RS_ERR_ARG;
+    }
+  rs_matrix* m = new rs_matrix();
+  m->device = device;
+  m->dtype = dtype;
+  m->nrows = nrows;
+  m->ncols = ncols;
+  m->row0 = row0;
+  int64_t *d_rp = nullptr, *d_ci = nullptr;
+  void* d_v = nullptr;
+  size_t es = dtype == RS_F32 ? 4 : 8;
+  int st = RS_OK;
+  std::vector<int64_t> rp(row_ptr, row_ptr + nrows + 1);
+  for (auto& p : rp) p -= row_ptr[0];
+  if (cudaMalloc(&d_rp, sizeof(int64_t) * (nrows + 1)) != cudaSuccess ||
+      cudaMalloc(&d_ci, sizeof(int64_t) * std::max<int64_t>(nnz, 1)) != cudaSuccess ||
+      cudaMalloc(&d_v, es * std::max<int64_t>(nnz, 1)) != cudaSuccess) {
+    st = cuda_error(cudaErrorMemoryAllocation, "rs_mat_create_csr upload");
+  } else {
+    cudaMemcpy(d_rp, rp.data(), sizeof(int64_t) * (nrows + 1), cudaMemcpyHostToDevice);
+    if (nnz) {
+      cudaMemcpy(d_ci, col_idx + row_ptr[0], sizeof(int64_t) * nnz, cudaMemcpyHostToDevice);
+      cudaMemcpy(d_v, (const char*)values + es * row_ptr[0], es * nnz, cudaMemcpyHostToDevice);
+    }
+    CsrSource src{d_rp, d_ci, dtype == RS_F64 ? (const double*)d_v : nullptr,
+                  dtype == RS_F32 ? (const float*)d_v : nullptr};
+    st = dtype == RS_F32 ? build_split<CsrSource, float>(m, src) : build_split<CsrSource, double>(m, src);
+  }
+  cudaFree(d_rp);
+  cudaFree(d_ci);
+  cudaFree(d_v);
+  if (st != RS_OK) {
+    destroy(m);
+    return st;
+  }
+  *out = m;
+  return RS_OK;
+}
+
+int rs_mat_create_stencil(int device, int kind, int64_t nx, int64_t ny, int64_t nz, const double* params, int64_t row0,
+                          int64_t nrows, int dtype, rs_matrix_t* out) {
+  if (!out || nx < 1 || ny < 1 || nz < 1 || (dtype != RS_F64 && dtype != RS_F32) || kind < 0 || kind > 2) {
+    set_error(RS_ERR_ARG, "grid counts must be >= 1 / bad stencil arguments");
+    return RS_ERR_ARG;
+  }
+  int64_t n = kind == RS_STENCIL_LAPLACE2D ? nx * ny : nx * ny * nz;
+  if (nrows < 0) nrows = n - row0;
+  if (row0 < 0 || row0 + nrows > n) {
+    set_error(RS_ERR_ARG, "row block out of range");
+    return RS_ERR_ARG;
+  }
+  RS_CUDA(cudaSetDevice(device));
+  StencilSource src;
+  src.kind = kind;
+  src.nx = nx;
+  src.ny = ny;
+  src.nz = kind == RS_STENCIL_LAPLACE2D ? 1 : nz;
+  src.row0 = row0;
+  if (kind == RS_STENCIL_CONVDIFF3D) {
+    // h^2-scaled first-order upwind -Lap u + beta.grad u:
+    // diag 6 + h*sum(beta), backward neighbours -1 - h*beta_d, forward -1.
+    double h = 1.0 / (double)(nx + 1);
+    double sb = ((0.0 + params[0]) + params[1]) + params[2];
+    src.diag = 6.0 + h * sb;
+    for (int a = 0; a < 3; ++a) src.off[a] = -1.0 - h * params[a];
+  } else {
+    src.diag = kind == RS_STENCIL_LAPLACE2D ? 4.0 : 6.0;
+    src.off[0] = src.off[1] = src.off[2] = -1.0;
+  }
+  rs_matrix* m = new rs_matrix();
+  m->device = device;
+  m->dtype = dtype;
+  m->nrows = nrows;
+  m->ncols = n;
+  m->row0 = row0;
+  int st = dtype == RS_F32 ? build_split<StencilSource, float>(m, src) : build_split<StencilSource, double>(m, src);
+  if (st != RS_OK) {
+    destroy(m);
+    return st;
+  }
+  *out = m;
+  return RS_OK;
+}
+
+int rs_mat_cast(rs_matrix_t src, int dtype, rs_matrix_t* out) {
+  if (!src || !out || dtype != RS_F32 || src->dtype != RS_F64) {
+    set_error(RS_ERR_ARG, "rs_mat_cast: only float64 -> float32 is supported");
+    return RS_ERR_ARG;
+  }
+  RS_CUDA(cudaSetDevice(src->device));
+  rs_matrix* m = new rs_matrix();
+  m->device = src->device;
+  m->dtype = RS_F32;
+  m->nrows = src->nrows;
+  m->ncols = src->ncols;
+  m->row0 = src->row0;
+  m->nnz = src->nnz;
+  m->halo_lo = src->halo_lo;
+  m->halo_hi = src->halo_hi;
+  long long* bad = nullptr;
+  int st = RS_OK;
+  float* d32 = nullptr;
+  long long init = LLONG_MAX, hb = LLONG_MAX;
+  if (cudaMalloc(&bad, sizeof(long long)) != cudaSuccess ||
+      cudaMalloc(&d32, sizeof(float) * std::max<int64_t>(m->nrows, 1)) != cudaSuccess) {
+    st = cuda_error(cudaErrorMemoryAllocation, "rs_mat_cast");
+  } else {
+    m->d = d32;
+    cudaMemcpy(bad, &init, sizeof(init), cudaMemcpyHostToDevice);
+    if (m->nrows) {
+      k_cast_vals<<<grid_for(m->nrows, 256), 256>>>((const double*)src->d, d32, m->nrows, bad);
+      RS_COUNT_LAUNCH();
+    }
+    if (!(st = cast_sell(src->L64, m->L32, bad, d32)) && !(st = cast_sell(src->U64, m->U32, bad, d32)) &&
+        !(st = cast_sell(src->Elo64, m->Elo32, bad, d32)) && !(st = cast_sell(src->Ehi64, m->Ehi32, bad, d32))) {
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) st = cuda_error(e, "rs_mat_cast");
+      cudaMemcpy(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost);
+      if (st == RS_OK && hb != LLONG_MAX) {
+        set_error(RS_ERR_OVERFLOW, "matrix value overflows single precision", hb);
+        st = RS_ERR_OVERFLOW;
+      }
+    }
+  }
+  cudaFree(bad);
+  if (st != RS_OK) {
+    destroy(m);
+    return st;
+  }
+  *out = m;
+  return RS_OK;
+}
+
+int rs_mat_destroy(rs_matrix_t m) {
+  destroy(m);
+  return RS_OK;
+}
+
+int rs_mat_info(rs_matrix_t m, int64_t* info, int* dtype) {
+  if (!m || !info) {
+    set_error(RS_ERR_ARG, "rs_mat_info: null");
+    return RS_ERR_ARG;
+  }
+  info[0] = m->nrows;
+  info[1] = m->ncols;
+  info[2] = m->row0;
+  info[3] = m->nnz;
+  info[4] = m->dtype == RS_F32 ? m->L32.nnz : m->L64.nnz;
+  info[5] = m->dtype == RS_F32 ? m->U32.nnz : m->U64.nnz;
+  info[6] = m->halo_lo;
+  info[7] = m->halo_hi;
+  if (dtype) *dtype = m->dtype;
+  return RS_OK;
+}
+
+int rs_mat_export_tri(rs_matrix_t m, int which, int64_t* row_ptr, int64_t* col_idx, void* values, void* dvalues) {
+  if (!m || which < 0 || which > 3) {
+    set_error(RS_ERR_ARG, "rs_mat_export_tri: bad arguments");
+    return RS_ERR_ARG;
+  }
+  RS_CUDA(cudaSetDevice(m->device));
+  RS_CUDA(cudaDeviceSynchronize());
+  return m->dtype == RS_F32 ? export_tri_t<float>(m, which, row_ptr, col_idx, values, dvalues)
+                            : export_tri_t<double>(m, which, row_ptr, col_idx, values, dvalues);
+}
+
+int rs_mat_export_diag(rs_matrix_t m, void* d) {
+  if (!m || !d) {
+    set_error(RS_ERR_ARG, "rs_mat_export_diag: null");
+    return RS_ERR_ARG;
+  }
+  RS_CUDA(cudaSetDevice(m->device));
+  RS_CUDA(cudaMemcpy(d, m->d, (m->dtype == RS_F32 ? 4 : 8) * m->nrows, cudaMemcpyDeviceToHost));
+  return RS_OK;
+}
+
+}  // extern "C"

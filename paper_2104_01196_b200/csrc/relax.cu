@@ -1,0 +1,634 @@
+// relax.cu -- GS2 / JR / level-scheduled GS sweeps on SELL-32 split matrices.
+//
+// Reference semantics (relax.py, _kernels.py) and the exact operation forms
+// kept for bitwise parity (SURVEY.md §8(c) parity recipe):
+//   r  = b - (A x)          A x summed per row from 0 in ascending column order
+//   rd = r / d              true division
+//   g  = rd - w*(D^-1T g)   (gamma == 1)
+//   g  = (1-gamma)*g + gamma*(rd - w*(D^-1T g))
+//   x  = x + w*g            non-compact;  x = w*g  compact
+// All products / sums use __d*_rn / __f*_rn so nvcc cannot contract to FMA.
+//
+// Kernel inventory (one thread per row, rows of a warp = one SELL slice):
+//   k_resid      r = b - A x fused with the D^-1 scale (GS2 pass 0) or the JR
+//                update (x_out = x + w r/d, ping-pong buffers), or y = A x.
+//   k_inner      one inner JR step on D^-1 L / D^-1 U; the last step is fused
+//                with the x update.
+//   k_compact    t = b - U x - (1 - 1/w) d x, scaled by D^-1 (compact pass 0).
+//   k_gs_level   one dependency level of the in-place Gauss-Seidel sweep.
+#include <algorithm>
+
+#include "rs_internal.cuh"
+
+namespace rs {
+
+int build_levels(rs_matrix* m, int backward);
+
+template <typename T>
+struct SellView {
+  const int64_t* __restrict__ sp;
+  const int32_t* __restrict__ col;
+  const T* __restrict__ val;
+  bool empty;
+};
+
+template <typename T>
+static SellView<T> view(const Sell<T>& s, bool scaled) {
+  SellView<T> v;
+  v.sp = s.slice_ptr;
+  v.col = s.col;
+  v.val = scaled ? s.dval : s.val;
+  v.empty = s.nslots == 0;
+  return v;
+}
+
+// acc += sum_k v_k * x[c_k] over one row of a SELL triangle, ascending k.
+template <typename T>
+__device__ __forceinline__ T row_accum(const SellView<T>& m, int64_t i, const T* __restrict__ x, T acc) {
+  if (m.empty) return acc;
+  const int64_t s = i >> 5;
+  const int lane = (int)(i & 31);
+  const int64_t p0 = m.sp[s];
+  const int w = (int)((m.sp[s + 1] - p0) >> 5);
+  const int32_t* cp = m.col + p0 + lane;
+  const T* vp = m.val + p0 + lane;
+  for (int j = 0; j < w; ++j) {
+    int32_t c = __ldcs(cp + 32 * j);
+    T v = __ldcs(vp + 32 * j);
+    if (c >= 0) acc = add_rn<T>(acc, mul_rn<T>(v, x[c]));
+  }
+  return acc;
+}
+
+// s -= sum_k v_k * x[c_k] (gs_ordered_sweep form, _kernels.py:31-35)
+template <typename T>
+__device__ __forceinline__ T row_subtract(const SellView<T>& m, int64_t i, const T* x, T s) {
+  if (m.empty) return s;
+  const int64_t sl = i >> 5;
+  const int lane = (int)(i & 31);
+  const int64_t p0 = m.sp[sl];
+  const int w = (int)((m.sp[sl + 1] - p0) >> 5);
+  for (int j = 0; j < w; ++j) {
+    int32_t c = m.col[p0 + 32 * j + lane];
+    if (c >= 0) s = sub_rn<T>(s, mul_rn<T>(m.val[p0 + 32 * j + lane], x[c]));
+  }
+  return s;
+}
+
+enum ResidMode { kSpmv = 0, kResidRd = 1, kJr = 2, kBhat = 3 };
+
+struct Halo {
+  const void* lo;
+  const void* hi;
+};
+
+// Full-row product A x for the local rows: E_lo | L | D | U | E_hi in ascending column order.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256) k_resid(int64_t n, SellView<T> Elo, SellView<T> L, SellView<T> U,
+                                               SellView<T> Ehi, const T* __restrict__ d, const T* __restrict__ x,
+                                               const T* __restrict__ xlo, const T* __restrict__ xhi,
+                                               const T* __restrict__ b, T* __restrict__ out, T w) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  T acc = (T)0;
+  acc = row_accum<T>(Elo, i, xlo, acc);
+  acc = row_accum<T>(L, i, x, acc);
+  const T di = d[i];
+  const T xi = x[i];
+  acc = add_rn<T>(acc, mul_rn<T>(di, xi));
+  acc = row_accum<T>(U, i, x, acc);
+  acc = row_accum<T>(Ehi, i, xhi, acc);
+  if (MODE == kSpmv) {
+    out[i] = acc;
+  } else if (MODE == kResidRd) {
+    out[i] = div_rn<T>(sub_rn<T>(b[i], acc), di);
+  } else if (MODE == kJr) {
+    T g = div_rn<T>(sub_rn<T>(b[i], acc), di);
+    out[i] = add_rn<T>(xi, mul_rn<T>(w, g));
+  }
+}
+
+// bhat = (b - A_full x) + A_pp x   (relax.py:261-264), y and A_pp x from the same row walk
+template <typename T>
+__global__ void __launch_bounds__(256) k_bhat(int64_t n, SellView<T> Elo, SellView<T> L, SellView<T> U,
+                                              SellView<T> Ehi, const T* __restrict__ d, const T* __restrict__ x,
+                                              const T* __restrict__ xlo, const T* __restrict__ xhi,
+                                              const T* __restrict__ b, T* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  T y = row_accum<T>(Elo, i, xlo, (T)0);
+  T s = row_accum<T>(L, i, x, (T)0);
+  y = row_accum<T>(L, i, x, y);
+  T dx = mul_rn<T>(d[i], x[i]);
+  y = add_rn<T>(y, dx);
+  s = add_rn<T>(s, dx);
+  y = row_accum<T>(U, i, x, y);
+  s = row_accum<T>(U, i, x, s);
+  y = row_accum<T>(Ehi, i, xhi, y);
+  out[i] = add_rn<T>(sub_rn<T>(b[i], y), s);
+}
+
+// compact pass 0 (relax.py:200-204): rd = (b - T x - c*(d*x)) / d, T = U (fwd) or L (bwd)
+template <typename T, bool DAMPED>
+__global__ void __launch_bounds__(256) k_compact(int64_t n, SellView<T> Tm, const T* __restrict__ d,
+                                                 const T* __restrict__ x, const T* __restrict__ b,
+                                                 T* __restrict__ rd, T c) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  T t = sub_rn<T>(b[i], row_accum<T>(Tm, i, x, (T)0));
+  const T di = d[i];
+  if (DAMPED) t = sub_rn<T>(t, mul_rn<T>(c, mul_rn<T>(di, x[i])));
+  rd[i] = div_rn<T>(t, di);
+}
+
+// rd = r / d (zero-start first pass: b - A*0 == b)
+template <typename T, typename R>
+__global__ void k_scale_rd(int64_t n, const R* __restrict__ r, const T* __restrict__ d, T* __restrict__ rd,
+                           long long* overflow) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  R rv = r[i];
+  T tv = (T)rv;
+  if (sizeof(T) < sizeof(R) && overflow && isinf((float)tv) && isfinite((double)rv)) atomicMin(overflow, (long long)i);
+  rd[i] = div_rn<T>(tv, d[i]);
+}
+
+enum InnerFinal { kNotFinal = 0, kFinalAdd = 1, kFinalSet = 2 };
+
+// one inner JR step: gout = rd - w*(D^-1T gin)  or damped; last step updates x
+template <typename T, int FINAL, bool GAMMA>
+__global__ void __launch_bounds__(256) k_inner(int64_t n, SellView<T> Tm, const T* __restrict__ rd,
+                                               const T* __restrict__ gin, T* __restrict__ gout, T* __restrict__ x,
+                                               T w, T gm, T gm1) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  T t = row_accum<T>(Tm, i, gin, (T)0);
+  T g = sub_rn<T>(rd[i], mul_rn<T>(w, t));
+  if (GAMMA) g = add_rn<T>(mul_rn<T>(gm1, gin[i]), mul_rn<T>(gm, g));
+  if (FINAL == kNotFinal) gout[i] = g;
+  else if (FINAL == kFinalAdd) x[i] = add_rn<T>(x[i], mul_rn<T>(w, g));
+  else x[i] = mul_rn<T>(w, g);
+}
+
+// n_j == 0 update: x = x + w*rd (non-compact) or x = w*rd (compact)
+template <typename T, bool SET>
+__global__ void k_update(int64_t n, const T* __restrict__ rd, T* __restrict__ x, T w) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  T wg = mul_rn<T>(w, rd[i]);
+  x[i] = SET ? wg : add_rn<T>(x[i], wg);
+}
+
+// in-place GS over one dependency level (gs_ordered_sweep, _kernels.py:24-39):
+// s = b_i - sum_{k != i} a_ik x_k in ascending k (L part first, then U part).
+// Forward: L columns were already visited (new values, xL = x), U columns read
+// the old iterate (xU = x, or a snapshot when the pattern is not structurally
+// symmetric).  Backward swaps the roles.
+template <typename T>
+__global__ void __launch_bounds__(256) k_gs_level(int64_t cnt, const int32_t* __restrict__ rows, SellView<T> L,
+                                                  SellView<T> U, const T* __restrict__ d, const T* __restrict__ b,
+                                                  T* x, const T* xL, const T* xU, T w, T w1, bool damped) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cnt) return;
+  int64_t i = rows[t];
+  T s = b[i];
+  s = row_subtract<T>(L, i, xL, s);
+  s = row_subtract<T>(U, i, xU, s);
+  T q = div_rn<T>(s, d[i]);
+  x[i] = damped ? add_rn<T>(mul_rn<T>(w1, x[i]), mul_rn<T>(w, q)) : q;
+}
+
+// cast_vector(r, "single") (sparse.py:244-257); *flag = min overflowing index
+// (caller initialises it to INT64_MAX)
+__global__ void k_cast_rhs_f32(int64_t n, const double* __restrict__ in, float* __restrict__ out, long long* flag) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double v = in[i];
+  float f = (float)v;
+  out[i] = f;
+  if (flag && isinf(f) && isfinite(v)) atomicMin(flag, (long long)i);
+}
+
+template <typename T>
+__global__ void k_cast(int64_t n, const T* __restrict__ in, double* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (double)in[i];
+}
+
+constexpr int kB = 256;
+
+// ------------------------------------------------------------------ host launchers
+template <typename T>
+struct Ctx {
+  rs_matrix* m;
+  cudaStream_t st;
+  int64_t n;
+  SellView<T> L, U, Lsc, Usc, Elo, Ehi;
+  const T* d;
+  Ctx(rs_matrix* mm, cudaStream_t s) : m(mm), st(s), n(mm->nrows) {
+    L = view(tri<T>(m, 0), false);
+    U = view(tri<T>(m, 1), false);
+    Lsc = view(tri<T>(m, 0), true);
+    Usc = view(tri<T>(m, 1), true);
+    Elo = view(tri<T>(m, 2), false);
+    Ehi = view(tri<T>(m, 3), false);
+    d = (const T*)m->d;
+  }
+  int grid() const { return grid_for(std::max<int64_t>(n, 1), kB); }
+  SellView<T> local_only(SellView<T> v) const { return v; }
+};
+
+template <typename T>
+static SellView<T> none_view() {
+  SellView<T> v;
+  v.sp = nullptr;
+  v.col = nullptr;
+  v.val = nullptr;
+  v.empty = true;
+  return v;
+}
+
+// One inner JR chain from rd; the last step updates x (non-compact add / compact set).
+template <typename T>
+static int inner_chain(Ctx<T>& c, T* rd, T* ga, T* gb, T* x, int n_j, int backward, double omega, double gamma,
+                       bool compact, bool x_zero) {
+  // from a zero iterate x + w*g == w*g exactly (up to the sign of zero), so the
+  // update stores instead of read-modify-write
+  compact = compact || x_zero;
+  T w = (T)omega;
+  SellView<T> Tm = backward ? c.Usc : c.Lsc;
+  const bool damped = gamma != 1.0;
+  T gm = (T)gamma, gm1 = (T)(1.0 - gamma);
+  if (n_j == 0) {
+    if (compact) {
+      k_update<T, true><<<c.grid(), kB, 0, c.st>>>(c.n, rd, x, w);
+      RS_COUNT_LAUNCH();
+    }
+    else {
+      k_update<T, false><<<c.grid(), kB, 0, c.st>>>(c.n, rd, x, w);
+      RS_COUNT_LAUNCH();
+    }
+    return RS_OK;
+  }
+  const T* gin = rd;
+  T* bufs[2] = {ga, gb};
+  for (int j = 0; j < n_j; ++j) {
+    bool last = j == n_j - 1;
+    T* gout = bufs[j & 1];
+    if (!last) {
+      if (damped) {
+        k_inner<T, kNotFinal, true><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1);
+        RS_COUNT_LAUNCH();
+      }
+      else {
+        k_inner<T, kNotFinal, false><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1);
+        RS_COUNT_LAUNCH();
+      }
+    } else if (compact) {
+      if (damped) {
+        k_inner<T, kFinalSet, true><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1);
+        RS_COUNT_LAUNCH();
+      }
+      else {
+        k_inner<T, kFinalSet, false><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1);
+        RS_COUNT_LAUNCH();
+      }
+    } else {
+      if (damped) {
+        k_inner<T, kFinalAdd, true><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1);
+        RS_COUNT_LAUNCH();
+      }
+      else {
+        k_inner<T, kFinalAdd, false><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1);
+        RS_COUNT_LAUNCH();
+      }
+    }
+    gin = gout;
+  }
+  return RS_OK;
+}
+
+// One _two_stage_sweep (relax.py:193-205) on the local block (no halo: E ignored).
+// x_is_zero: the iterate is exactly 0 (zero-start preconditioner) -> pass 0 is rd = b/d.
+template <typename T>
+static int two_stage(Ctx<T>& c, const T* b, T* x, int n_j, int backward, int form, double omega, double gamma,
+                     bool x_is_zero) {
+  T* rd = (T*)c.m->scratch;
+  T* ga = rd + c.n;
+  T* gb = ga + c.n;
+  bool compact = form == RS_COMPACT;
+  if (x_is_zero) {
+    k_scale_rd<T, T><<<c.grid(), kB, 0, c.st>>>(c.n, b, c.d, rd, nullptr);
+    RS_COUNT_LAUNCH();
+  } else if (!compact) {
+    k_resid<T, kResidRd><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x, nullptr,
+                                                     nullptr, b, rd, (T)0);
+    RS_COUNT_LAUNCH();
+  } else {
+    SellView<T> Tm = backward ? c.L : c.U;
+    if (omega != 1.0) {
+      T cc = (T)(1.0 - 1.0 / omega);
+      k_compact<T, true><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, c.d, x, b, rd, cc);
+      RS_COUNT_LAUNCH();
+    } else {
+      k_compact<T, false><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, c.d, x, b, rd, (T)0);
+      RS_COUNT_LAUNCH();
+    }
+  }
+  return inner_chain(c, rd, ga, gb, x, n_j, backward, omega, gamma, compact, x_is_zero);
+}
+
+template <typename T>
+static int gs2_apply_t(rs_matrix* m, const T* b, T* x, const rs_relax_cfg& cfg, cudaStream_t st, bool x_is_zero) {
+  int e;
+  if ((e = ensure_scratch(m))) return e;
+  Ctx<T> c(m, st);
+  bool zero = x_is_zero;
+  for (int t = 0; t < cfg.n_t; ++t)
+    for (int k = 0; k < cfg.n_k; ++k)
+      for (int half = 0; half < 2; ++half) {
+        int bwd = half;
+        if (cfg.direction == RS_FORWARD && bwd) continue;
+        if (cfg.direction == RS_BACKWARD && !bwd) continue;
+        if ((e = two_stage<T>(c, b, x, cfg.n_j, bwd, cfg.form, cfg.omega, cfg.gamma, zero))) return e;
+        zero = false;
+      }
+  RS_CHECK_LAUNCH("gs2_apply");
+  return RS_OK;
+}
+
+// jr_sweeps (relax.py:145-154) with ping-pong iterates: x_next = x + w (b - A x)/d
+template <typename T>
+static int jr_sweeps_t(rs_matrix* m, const T* b, T* x, int sweeps, double omega, cudaStream_t st, bool x_is_zero) {
+  int e;
+  if ((e = ensure_scratch(m))) return e;
+  Ctx<T> c(m, st);
+  T w = (T)omega;
+  T* alt = (T*)m->scratch + 3 * m->nrows;
+  T* cur = x;
+  for (int s = 0; s < sweeps; ++s) {
+    if (s == 0 && x_is_zero) {
+      // x = 0 + w*(b/d): rd into alt then x = w*rd ... done in place on x directly
+      k_scale_rd<T, T><<<c.grid(), kB, 0, c.st>>>(c.n, b, c.d, alt, nullptr);
+      RS_COUNT_LAUNCH();
+      k_update<T, true><<<c.grid(), kB, 0, c.st>>>(c.n, alt, x, w);
+      RS_COUNT_LAUNCH();
+      continue;
+    }
+    T* nxt = cur == x ? alt : x;
+    k_resid<T, kJr><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, cur, nullptr,
+                                               nullptr, b, nxt, w);
+    RS_COUNT_LAUNCH();
+    cur = nxt;
+  }
+  if (cur != x) RS_CUDA(cudaMemcpyAsync(x, cur, sizeof(T) * c.n, cudaMemcpyDeviceToDevice, st));
+  RS_CHECK_LAUNCH("jr_sweeps");
+  return RS_OK;
+}
+
+template <typename T>
+static int gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omega, cudaStream_t st) {
+  int e;
+  if ((e = ensure_scratch(m))) return e;
+  Ctx<T> c(m, st);
+  T w = (T)omega, w1 = (T)(1.0 - omega);
+  bool damped = w != (T)1.0;
+  for (int half = 0; half < 2; ++half) {
+    int bwd = half;
+    if (direction == RS_FORWARD && bwd) continue;
+    if (direction == RS_BACKWARD && !bwd) continue;
+    if ((e = build_levels(m, bwd))) return e;
+    Levels& lv = bwd ? m->bwd : m->fwd;
+    const T* xold = x;
+    if (!m->structurally_symmetric) {
+      // snapshot of the old iterate for the not-yet-visited side
+      T* snap = (T*)m->scratch + 3 * m->nrows;
+      RS_CUDA(cudaMemcpyAsync(snap, x, sizeof(T) * c.n, cudaMemcpyDeviceToDevice, st));
+      xold = snap;
+    }
+    const T* xL = bwd ? xold : x;
+    const T* xU = bwd ? x : xold;
+    for (int64_t l = 0; l < lv.nlevels; ++l) {
+      int64_t lo = lv.level_ptr_host[l], hi = lv.level_ptr_host[l + 1];
+      int64_t cnt = hi - lo;
+      if (!cnt) continue;
+      k_gs_level<T><<<grid_for(cnt, kB), kB, 0, st>>>(cnt, lv.rows + lo, c.L, c.U, c.d, b, x, xL, xU, w, w1, damped);
+      RS_COUNT_LAUNCH();
+    }
+  }
+  RS_CHECK_LAUNCH("gs_sweep");
+  return RS_OK;
+}
+
+}  // namespace rs
+
+namespace rs {
+
+template <typename T>
+static int inner_jr_t(rs_matrix* m, const T* r, T* g, int n_j, int backward, double omega, double gamma,
+                      cudaStream_t st) {
+  int e;
+  if ((e = ensure_scratch(m))) return e;
+  Ctx<T> c(m, st);
+  T* rd = (T*)m->scratch;
+  T* ga = rd + c.n;
+  T* gb = ga + c.n;
+  if (n_j == 0) {
+    k_scale_rd<T, T><<<c.grid(), kB, 0, st>>>(c.n, r, c.d, g, nullptr);
+    RS_COUNT_LAUNCH();
+    RS_CHECK_LAUNCH("inner_jr");
+    return RS_OK;
+  }
+  k_scale_rd<T, T><<<c.grid(), kB, 0, st>>>(c.n, r, c.d, rd, nullptr);
+  RS_COUNT_LAUNCH();
+  T w = (T)omega, gm = (T)gamma, gm1 = (T)(1.0 - gamma);
+  SellView<T> Tm = backward ? c.Usc : c.Lsc;
+  const T* gin = rd;
+  for (int j = 0; j < n_j; ++j) {
+    T* gout = j == n_j - 1 ? g : ((j & 1) ? gb : ga);
+    if (gamma != 1.0) {
+      k_inner<T, kNotFinal, true><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, gout, nullptr, w, gm, gm1);
+      RS_COUNT_LAUNCH();
+    }
+    else {
+      k_inner<T, kNotFinal, false><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, gout, nullptr, w, gm, gm1);
+      RS_COUNT_LAUNCH();
+    }
+    gin = gout;
+  }
+  RS_CHECK_LAUNCH("inner_jr");
+  return RS_OK;
+}
+
+template <typename T>
+static int spmv_t(rs_matrix* m, const T* x, const T* xlo, const T* xhi, T* y, cudaStream_t st) {
+  Ctx<T> c(m, st);
+  if ((!c.Elo.empty && !xlo) || (!c.Ehi.empty && !xhi)) {
+    set_error(RS_ERR_ARG, "halo values required for a row block with off-block couplings");
+    return RS_ERR_ARG;
+  }
+  if (c.n) {
+    k_resid<T, kSpmv><<<c.grid(), kB, 0, st>>>(c.n, c.Elo, c.L, c.U, c.Ehi, c.d, x, xlo, xhi, nullptr, y, (T)0);
+    RS_COUNT_LAUNCH();
+  }
+  RS_CHECK_LAUNCH("spmv");
+  return RS_OK;
+}
+
+template <typename T>
+static int bhat_t(rs_matrix* m, const T* b, const T* x, const T* xlo, const T* xhi, T* out, cudaStream_t st) {
+  Ctx<T> c(m, st);
+  if ((!c.Elo.empty && !xlo) || (!c.Ehi.empty && !xhi)) {
+    set_error(RS_ERR_ARG, "halo values required for a row block with off-block couplings");
+    return RS_ERR_ARG;
+  }
+  if (c.n) {
+    k_bhat<T><<<c.grid(), kB, 0, st>>>(c.n, c.Elo, c.L, c.U, c.Ehi, c.d, x, xlo, xhi, b, out);
+    RS_COUNT_LAUNCH();
+  }
+  RS_CHECK_LAUNCH("hybrid_bhat");
+  return RS_OK;
+}
+
+// Preconditioner.apply (krylov.py:110-137) body in the working dtype, from z = 0.
+template <typename T>
+static int precond_body(rs_matrix* m, int kind, rs_relax_cfg cfg, const T* rhs, T* z, cudaStream_t st) {
+  int sweeps = cfg.n_t * cfg.n_k;
+  if (kind == RS_PC_SGS_SEQ || kind == RS_PC_SGS2) cfg.direction = RS_SYMMETRIC;  // krylov.py:86-87
+  switch (kind) {
+    case RS_PC_JR:
+      return jr_sweeps_t<T>(m, rhs, z, sweeps, cfg.omega, st, true);
+    case RS_PC_GS_SEQ:
+    case RS_PC_SGS_SEQ: {
+      RS_CUDA(cudaMemsetAsync(z, 0, sizeof(T) * m->nrows, st));
+      for (int s = 0; s < sweeps; ++s) {
+        int e = gs_sweep_t<T>(m, rhs, z, cfg.direction, cfg.omega, st);
+        if (e) return e;
+      }
+      return RS_OK;
+    }
+    case RS_PC_GS2:
+    case RS_PC_SGS2:
+      return gs2_apply_t<T>(m, rhs, z, cfg, st, true);
+  }
+  set_error(RS_ERR_ARG, "unknown preconditioner kind");
+  return RS_ERR_ARG;
+}
+
+}  // namespace rs
+
+using namespace rs;
+
+static bool bad_cfg(const rs_relax_cfg* c) {
+  return !c || c->n_t < 1 || c->n_k < 1 || c->n_j < 0 || !(c->omega > 0) || !(c->gamma > 0) || c->direction < 0 ||
+         c->direction > 2 || c->form < 0 || c->form > 1;
+}
+
+#define RS_SET_DEVICE(m)                                              \
+  do {                                                                \
+    if (!(m)) {                                                       \
+      set_error(RS_ERR_ARG, "null matrix handle");                    \
+      return RS_ERR_ARG;                                              \
+    }                                                                 \
+    RS_CUDA(cudaSetDevice((m)->device));                              \
+  } while (0)
+
+extern "C" {
+
+int rs_spmv(rs_matrix_t m, const void* x, const void* x_lo, const void* x_hi, void* y, rs_stream_t stream) {
+  RS_SET_DEVICE(m);
+  cudaStream_t st = (cudaStream_t)stream;
+  return m->dtype == RS_F32 ? spmv_t<float>(m, (const float*)x, (const float*)x_lo, (const float*)x_hi, (float*)y, st)
+                            : spmv_t<double>(m, (const double*)x, (const double*)x_lo, (const double*)x_hi,
+                                             (double*)y, st);
+}
+
+int rs_hybrid_bhat(rs_matrix_t m, const void* b, const void* x, const void* x_lo, const void* x_hi, void* bhat,
+                   rs_stream_t stream) {
+  RS_SET_DEVICE(m);
+  cudaStream_t st = (cudaStream_t)stream;
+  return m->dtype == RS_F32
+             ? bhat_t<float>(m, (const float*)b, (const float*)x, (const float*)x_lo, (const float*)x_hi,
+                             (float*)bhat, st)
+             : bhat_t<double>(m, (const double*)b, (const double*)x, (const double*)x_lo, (const double*)x_hi,
+                              (double*)bhat, st);
+}
+
+int rs_gs_sweep(rs_matrix_t m, const void* b, void* x, int direction, double omega, rs_stream_t stream) {
+  RS_SET_DEVICE(m);
+  if (direction < 0 || direction > 2) {
+    set_error(RS_ERR_ARG, "direction must be forward, backward or symmetric");
+    return RS_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  return m->dtype == RS_F32 ? gs_sweep_t<float>(m, (const float*)b, (float*)x, direction, omega, st)
+                            : gs_sweep_t<double>(m, (const double*)b, (double*)x, direction, omega, st);
+}
+
+int rs_jr_sweeps(rs_matrix_t m, const void* b, void* x, int sweeps, double omega, rs_stream_t stream) {
+  RS_SET_DEVICE(m);
+  if (sweeps < 1) {
+    set_error(RS_ERR_ARG, "sweeps must be >= 1");
+    return RS_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  return m->dtype == RS_F32 ? jr_sweeps_t<float>(m, (const float*)b, (float*)x, sweeps, omega, st, false)
+                            : jr_sweeps_t<double>(m, (const double*)b, (double*)x, sweeps, omega, st, false);
+}
+
+int rs_inner_jr(rs_matrix_t m, const void* r, void* g, int n_j, int backward, double omega, double gamma,
+                rs_stream_t stream) {
+  RS_SET_DEVICE(m);
+  if (n_j < 0) {
+    set_error(RS_ERR_ARG, "n_j must be >= 0");
+    return RS_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  return m->dtype == RS_F32 ? inner_jr_t<float>(m, (const float*)r, (float*)g, n_j, backward, omega, gamma, st)
+                            : inner_jr_t<double>(m, (const double*)r, (double*)g, n_j, backward, omega, gamma, st);
+}
+
+int rs_gs2_apply(rs_matrix_t m, const void* b, void* x, const rs_relax_cfg* cfg, rs_stream_t stream) {
+  RS_SET_DEVICE(m);
+  if (bad_cfg(cfg)) {
+    set_error(RS_ERR_ARG, "invalid relaxation config");
+    return RS_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  return m->dtype == RS_F32 ? gs2_apply_t<float>(m, (const float*)b, (float*)x, *cfg, st, false)
+                            : gs2_apply_t<double>(m, (const double*)b, (double*)x, *cfg, st, false);
+}
+
+int rs_precond_apply(rs_matrix_t m, int kind, const rs_relax_cfg* cfg, const double* r, double* z,
+                     int64_t* overflow_flag, rs_stream_t stream) {
+  RS_SET_DEVICE(m);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (kind == RS_PC_NONE) {
+    RS_CUDA(cudaMemcpyAsync(z, r, sizeof(double) * m->nrows, cudaMemcpyDeviceToDevice, st));
+    return RS_OK;
+  }
+  if (bad_cfg(cfg)) {
+    set_error(RS_ERR_ARG, "invalid relaxation config");
+    return RS_ERR_ARG;
+  }
+  int e;
+  if ((e = ensure_scratch(m))) return e;
+  if (m->dtype == RS_F64) return precond_body<double>(m, kind, *cfg, r, z, st);
+  // single_inside_double (krylov.py:116-118, 135-136): cast r, relax in float32, upcast z
+  float* rhs = (float*)m->scratch + 4 * m->nrows;
+  float* zw = (float*)m->scratch + 5 * m->nrows;
+  int64_t n = m->nrows;
+  if (n) {
+    k_cast_rhs_f32<<<grid_for(n, kB), kB, 0, st>>>(n, r, rhs, (long long*)overflow_flag);
+    RS_COUNT_LAUNCH();
+  }
+  if ((e = precond_body<float>(m, kind, *cfg, rhs, zw, st))) return e;
+  if (n) {
+    k_cast<float><<<grid_for(n, kB), kB, 0, st>>>(n, zw, z);
+    RS_COUNT_LAUNCH();
+  }
+  RS_CHECK_LAUNCH("precond_apply");
+  return RS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,143 @@
+// rs_internal.cuh -- shared internals of libgs2b200 (sm_100a).
+//
+// Device layout of a matrix handle (one GPU, one row block [row0, row0+nrows)):
+//
+//   A = L + D + U  (+ E_lo / E_hi off-block couplings for a distributed slab)
+//
+// Each strict triangle is stored as SELL-32 ("sliced ELL", slice height 32 =
+// one warp): slice s holds rows [32s, 32s+32); entry j of lane r lives at
+// ptr[s] + 32*j + r, so a warp reading entry j of its 32 rows issues one fully
+// coalesced 256 B (fp64) / 128 B (int32 col) request.  Rows keep the
+// reference's ascending column order (sparse.py:195-232 keeps the CSR order);
+// slots past a row's length hold col = -1 and are skipped, so the per-row
+// accumulation is the reference's `acc = 0; acc += v*x` in ascending k
+// (_kernels.py:15-21) bit for bit.
+//
+// For each triangle we keep both the raw values (L, U: residual / compact RHS)
+// and the diagonally prescaled values (D^-1 L, D^-1 U: inner JR sweeps,
+// computed on device as l / d[row] in the working dtype, like sparse.py:227).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/gs2b200.h"
+
+namespace rs {
+
+constexpr int kSlice = 32;
+
+// thread-local error state for rs_last_error()
+void set_error(int code, const std::string& msg, int64_t index = -1);
+int cuda_error(cudaError_t e, const char* where);
+
+#define RS_CUDA(call)                                            \
+  do {                                                           \
+    cudaError_t _e = (call);                                     \
+    if (_e != cudaSuccess) return ::rs::cuda_error(_e, #call);  \
+  } while (0)
+
+// number of kernels this library has launched (rs_launch_count, bench evidence)
+void count_launch();
+#define RS_COUNT_LAUNCH() ::rs::count_launch()
+
+#define RS_CHECK_LAUNCH(where)                                   \
+  do {                                                           \
+    cudaError_t _e = cudaGetLastError();                         \
+    if (_e != cudaSuccess) return ::rs::cuda_error(_e, where);   \
+  } while (0)
+
+// A SELL-32 strict triangle (or off-block coupling block).
+template <typename T>
+struct Sell {
+  int64_t nrows = 0;
+  int64_t nslices = 0;
+  int64_t nnz = 0;        // stored (unpadded) entries
+  int64_t nslots = 0;     // padded slots = slice_ptr[nslices]
+  int64_t* slice_ptr = nullptr;  // [nslices+1], slot offset of each slice
+  int32_t* col = nullptr;        // [nslots], -1 = padding
+  T* val = nullptr;              // [nslots] raw values
+  T* dval = nullptr;             // [nslots] values / d[row] (optional)
+};
+
+struct Levels {
+  // level-scheduled Gauss-Seidel (rows grouped by dependency level)
+  int64_t nlevels = 0;
+  int64_t* level_ptr_host = nullptr;  // [nlevels+1]
+  int32_t* rows = nullptr;            // [nrows] device, rows in level order
+};
+
+}  // namespace rs
+
+// The opaque handle of the C ABI.
+struct rs_matrix {
+  int device = 0;
+  int dtype = RS_F64;
+  int64_t nrows = 0;        // local rows
+  int64_t ncols = 0;        // global columns
+  int64_t row0 = 0;         // first global row of this block
+  int64_t nnz = 0;          // stored entries of the local rows (incl. diagonal, incl. couplings)
+  int structurally_symmetric = 1;
+  void* d = nullptr;        // diagonal [nrows]
+  rs::Sell<double> L64, U64, Elo64, Ehi64;
+  rs::Sell<float> L32, U32, Elo32, Ehi32;
+  int64_t halo_lo = 0;      // #halo entries below row0 (E_lo column space = [row0-halo_lo, row0))
+  int64_t halo_hi = 0;      // #halo entries at/above row0+nrows
+  rs::Levels fwd, bwd;      // lazily built
+  void* scratch = nullptr;  // 3*nrows working dtype (rd, g ping/pong)
+  void* scratch2 = nullptr; // 1*nrows (t)
+  double* red = nullptr;    // reduction partials
+  unsigned int* ticket = nullptr;
+  int64_t red_cap = 0;
+};
+
+namespace rs {
+template <typename T>
+inline Sell<T>& tri(rs_matrix* m, int which);  // 0 L, 1 U, 2 Elo, 3 Ehi
+template <>
+inline Sell<double>& tri<double>(rs_matrix* m, int which) {
+  return which == 0 ? m->L64 : which == 1 ? m->U64 : which == 2 ? m->Elo64 : m->Ehi64;
+}
+template <>
+inline Sell<float>& tri<float>(rs_matrix* m, int which) {
+  return which == 0 ? m->L32 : which == 1 ? m->U32 : which == 2 ? m->Elo32 : m->Ehi32;
+}
+
+inline int grid_for(int64_t n, int block) { return (int)((n + block - 1) / block); }
+
+// exact IEEE operations: no FMA contraction anywhere on the parity path
+template <typename T>
+__device__ __forceinline__ T mul_rn(T a, T b);
+template <>
+__device__ __forceinline__ double mul_rn<double>(double a, double b) { return __dmul_rn(a, b); }
+template <>
+__device__ __forceinline__ float mul_rn<float>(float a, float b) { return __fmul_rn(a, b); }
+template <typename T>
+__device__ __forceinline__ T add_rn(T a, T b);
+template <>
+__device__ __forceinline__ double add_rn<double>(double a, double b) { return __dadd_rn(a, b); }
+template <>
+__device__ __forceinline__ float add_rn<float>(float a, float b) { return __fadd_rn(a, b); }
+template <typename T>
+__device__ __forceinline__ T sub_rn(T a, T b);
+template <>
+__device__ __forceinline__ double sub_rn<double>(double a, double b) { return __dsub_rn(a, b); }
+template <>
+__device__ __forceinline__ float sub_rn<float>(float a, float b) { return __fsub_rn(a, b); }
+template <typename T>
+__device__ __forceinline__ T div_rn(T a, T b);
+template <>
+__device__ __forceinline__ double div_rn<double>(double a, double b) { return __ddiv_rn(a, b); }
+template <>
+__device__ __forceinline__ float div_rn<float>(float a, float b) { return __fdiv_rn(a, b); }
+
+// streaming (read-once) loads for matrix data: keep them out of L1
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T* p) { return __ldcs(p); }
+
+// int status helpers for the host side of each entry point
+int ensure_scratch(rs_matrix* m);
+int ensure_reduction(rs_matrix* m, int64_t n_doubles);
+
+}  // namespace rs

@@ -1,0 +1,318 @@
+"""CUDA parity: the B200 kernels against the reference's golden vectors and the C oracle.
+
+Bar (north_star): bitwise on every sweep / SpMV / splitting / preconditioner
+fixture (the kernels reproduce the reference's exact operation order), per-
+sweep relative error <= 1e-12 (fp64) / 1e-5 (fp32) at larger sizes against the
+oracle (observed: bitwise), identical GMRES iteration counts on
+configurations whose reference count is BLAS-thread independent.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2104_01196_b200 as g2
+from golden_cases import all_cases, inputs, regular_offsets
+from test_oracle import GMRES_FAST, golden_problem, iteration_tolerance, parse_gmres_label
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+
+_MATS = {}
+
+
+def _matrix(golden, case, dtype):
+    key = (case, dtype)
+    if key not in _MATS:
+        rp, ci, v, *_ = inputs(golden, case, dtype)
+        n = len(rp) - 1
+        _MATS[key] = g2.CsrMatrix(n, n, rp, ci, v)
+    return _MATS[key]
+
+
+def _run_gpu(c, golden):
+    rp, ci, v, b, x0, r = inputs(golden, c["case"], c["dtype"])
+    op = c["op"]
+    if op == "prec":
+        a = _matrix(golden, c["case"], "f64")
+        m = g2.Preconditioner(a, c["kind"], g2.RelaxConfig(2, 1, 1), precision=c["precision"])
+        return m.apply(golden[f"{c['case']}__r"])
+    a = _matrix(golden, c["case"], c["dtype"])
+    if op == "spmv":
+        return g2.spmv(a, x0)
+    if op == "d":
+        return g2.extract_splitting(a).d
+    if op == "dinv_l":
+        return g2.extract_splitting(a).dinv_l.values
+    if op == "dinv_u":
+        return g2.extract_splitting(a).dinv_u.values
+    x = x0.copy()
+    om = c.get("omega", 1.0)
+    gm = c.get("gamma", 1.0)
+    s = g2.extract_splitting(a, omega=om, gamma=gm)
+    if op == "jr":
+        g2.jr_sweeps(a, s, b, x, 3)
+    elif op == "gs":
+        g2.gs_sequential_sweep(a, s, b, x, c["direction"])
+    elif op == "inner":
+        return g2.inner_jr_solve(s, r, c["n_j"], c["direction"])
+    elif op == "gs2":
+        g2.gs2_apply(a, s, b, x, g2.RelaxConfig(2, 1, c["n_j"], direction=c["direction"], form=c["form"], omega=om,
+                                                 gamma=gm))
+    elif op == "hybrid":
+        part = g2.BlockPartition(regular_offsets(a.nrows, c["nblocks"]))
+        g2.hybrid_relax(a, part, b, x, g2.RelaxConfig(2, 2, 1), local=c["local"])
+    else:
+        raise KeyError(op)
+    return x
+
+
+def test_bitwise_on_all_reference_fixtures(sweeps_golden):
+    cases = all_cases(sweeps_golden)
+    assert len(cases) > 1000
+    bad = []
+    for c in cases:
+        got = np.asarray(_run_gpu(c, sweeps_golden))
+        want = sweeps_golden[c["key"]]
+        if got.dtype != want.dtype or got.shape != want.shape or not np.array_equal(got, want):
+            bad.append(c["key"])
+    assert not bad, f"{len(bad)}/{len(cases)} mismatches, first: {bad[:8]}"
+
+
+def test_a2_known_answers():
+    a = g2.from_dense([[2.0, -1.0], [-1.0, 2.0]])
+    s = g2.extract_splitting(a)
+    b = np.array([1.0, 1.0])
+    x = np.zeros(2); g2.jr_sweeps(a, s, b, x, 1); assert np.array_equal(x, [0.5, 0.5])
+    x = np.zeros(2); g2.jr_sweeps(a, s, b, x, 2); assert np.array_equal(x, [0.75, 0.75])
+    x = np.ones(2); g2.jr_sweeps(a, s, b, x, 7); assert np.array_equal(x, [1.0, 1.0])
+    x = np.zeros(2); g2.gs_sequential_sweep(a, s, b, x, "forward"); assert np.array_equal(x, [0.5, 0.75])
+    x = np.zeros(2); g2.gs_sequential_sweep(a, s, b, x, "backward"); assert np.array_equal(x, [0.75, 0.5])
+    x = np.zeros(2); g2.gs2_apply(a, s, b, x, g2.RelaxConfig(1, 1, 1)); assert np.array_equal(x, [0.5, 0.75])
+    x = np.zeros(2); g2.gs2_apply(a, s, b, x, g2.RelaxConfig(1, 1, 0)); assert np.array_equal(x, [0.5, 0.5])
+    x = np.zeros(2)
+    g2.gs2_apply(a, s, b, x, g2.RelaxConfig(1, 1, 1, form="compact"))
+    assert np.array_equal(x, [0.5, 0.75])
+    assert np.array_equal(g2.inner_jr_solve(s, b, 0), [0.5, 0.5])
+    assert np.array_equal(g2.inner_jr_solve(s, b, 5), [0.5, 0.75])
+    assert np.array_equal(g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, 1)).apply(b), [0.5, 0.75])
+    assert np.array_equal(g2.Preconditioner(a, "jr", g2.RelaxConfig(1, 1, 0)).apply(b), [0.5, 0.5])
+    z = g2.Preconditioner(a, "none").apply(np.array([3.0, -2.0]))
+    assert np.array_equal(z, [3.0, -2.0])
+    assert np.array_equal(g2.spmv(a, np.array([1.0, 0.0])), [2.0, -1.0])
+
+
+def test_error_conventions():
+    a = g2.from_dense([[2.0, -1.0], [-1.0, 2.0]])
+    s = g2.extract_splitting(a)
+    with pytest.raises(ValueError, match="dtype"):
+        g2.gs2_apply(a, s, np.ones(2, dtype=np.float32), np.zeros(2), g2.RelaxConfig())
+    with pytest.raises(ValueError, match="direction"):
+        g2.gs_sequential_sweep(a, s, np.ones(2), np.zeros(2), "up")
+    with pytest.raises(ValueError):
+        g2.jr_sweeps(a, s, np.ones(2), np.zeros(2), 0)
+    with pytest.raises(ValueError):
+        g2.spmv(a, np.ones(3))
+    z = g2.from_dense([[0.0, 1.0], [1.0, 2.0]])
+    with pytest.raises(ValueError, match="row 0"):
+        g2.extract_splitting(z).dev  # noqa: B018
+    with pytest.raises(ValueError, match="row 1"):
+        g2.CsrMatrix(2, 2, [0, 1, 2], [0, 0], [1.0, 1.0]).device()
+    m = g2.Preconditioner(g2.from_dense(np.diag([2.0, 2.0])), "jr", g2.RelaxConfig(1, 1, 0),
+                          precision="single_inside_double")
+    with pytest.raises(OverflowError):
+        m.apply(np.array([1e39, 0.0]))
+    with pytest.raises(ValueError, match="partition"):
+        g2.hybrid_relax(g2.laplace2d(3), g2.BlockPartition([0, 4]), np.zeros(9), np.zeros(9), g2.RelaxConfig())
+
+
+def test_device_generators_match_host():
+    for make_h, make_d in (
+        (lambda: g2.laplace2d(13, 7), lambda: g2.laplace2d(13, 7, device="cuda")),
+        (lambda: g2.laplace3d(9, 5, 4), lambda: g2.laplace3d(9, 5, 4, device="cuda")),
+        (lambda: g2.convdiff3d(7, (50.0, 25.0, 10.0)), lambda: g2.convdiff3d(7, (50.0, 25.0, 10.0), device="cuda")),
+    ):
+        h, d = make_h(), make_d()
+        back = d.to_csr()
+        assert np.array_equal(back.row_ptr, h.row_ptr)
+        assert np.array_equal(back.col_idx, h.col_idx)
+        assert np.array_equal(back.values, h.values)
+
+
+def test_device_lcg_bitwise():
+    for n, seed in ((1, 0), (1000, 3), (100_003, 12345678901234567), (3_000_000, 1)):
+        got = g2.random_rhs(n, seed, device="cuda").cpu().numpy()
+        assert np.array_equal(got, oracle.random_rhs(n, seed))
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("gen", ["lap3d_40", "ela3d_10", "cd3d_32"])
+def test_per_sweep_parity_vs_oracle(gen, dtype):
+    """Per-sweep relative error vs the oracle on mid-size problems (bar 1e-12 / 1e-5; observed bitwise)."""
+    kind, nx = gen.split("_")
+    nx = int(nx)
+    h = {"lap3d": lambda: g2.laplace3d(nx), "ela3d": lambda: g2.elasticity3d(nx),
+         "cd3d": lambda: g2.convdiff3d(nx, (50.0, 25.0, 10.0))}[kind]()
+    if dtype == np.float32:
+        h = g2.cast_matrix(h, "single")
+    om = oracle.Matrix(h)
+    n = h.nrows
+    b = g2.random_rhs(n, 0).astype(dtype)
+    x0 = g2.random_rhs(n, 1).astype(dtype)
+    tol = 1e-12 if dtype == np.float64 else 1e-5
+    s = g2.extract_splitting(h)
+    for cfg in (g2.RelaxConfig(1, 1, 1), g2.RelaxConfig(1, 1, 3, direction="symmetric"),
+                g2.RelaxConfig(1, 1, 2, form="compact", omega=0.9), g2.RelaxConfig(1, 1, 2, gamma=0.7)):
+        xg = x0.copy()
+        xo = x0.copy()
+        for sweep in range(3):
+            g2.gs2_apply(h, s, b, xg, cfg)
+            oracle.gs2_apply(om, b, xo, cfg)
+            rg = np.linalg.norm(b - g2.spmv(h, xg))
+            ro = np.linalg.norm(b - oracle.spmv(om, xo))
+            assert abs(rg - ro) <= tol * ro, (cfg, sweep)
+            assert np.array_equal(xg, xo), (cfg, sweep)
+    xg = x0.copy()
+    xo = x0.copy()
+    g2.gs_sequential_sweep(h, s, b, xg, "symmetric")
+    oracle.gs_sweep(om, b, xo, "symmetric")
+    assert np.array_equal(xg, xo)
+    xg = x0.copy()
+    xo = x0.copy()
+    g2.jr_sweeps(h, g2.extract_splitting(h, omega=0.7), b, xg, 2)
+    oracle.jr_sweeps(om, b, xo, 2, omega=0.7)
+    assert np.array_equal(xg, xo)
+
+
+def test_nonsymmetric_pattern_level_gs():
+    """Level-scheduled GS on a structurally non-symmetric matrix (snapshot path) == sequential GS."""
+    rng = np.random.default_rng(0)
+    n = 300
+    d = np.zeros((n, n))
+    idx = rng.integers(0, n, size=(1500, 2))
+    d[idx[:, 0], idx[:, 1]] = rng.uniform(-1, 1, 1500)
+    np.fill_diagonal(d, np.abs(d).sum(1) + 1.0)
+    a = g2.from_dense(d)
+    b = rng.standard_normal(n)
+    for direction in ("forward", "backward", "symmetric"):
+        for om in (1.0, 1.3):
+            x = rng.standard_normal(n)
+            xo = x.copy()
+            g2.gs_sequential_sweep(a, g2.extract_splitting(a, omega=om), b, x, direction)
+            oracle.gs_sweep(oracle.Matrix(a), b, xo, direction, omega=om)
+            assert np.array_equal(x, xo)
+
+
+def test_tensor_inputs_in_place():
+    a = g2.laplace3d(16)
+    s = g2.extract_splitting(a)
+    b = g2.random_rhs(a.nrows, 0)
+    x = g2.random_rhs(a.nrows, 1)
+    xt = torch.from_numpy(x.copy()).cuda()
+    bt = torch.from_numpy(b).cuda()
+    g2.gs2_apply(a, s, bt, xt, g2.RelaxConfig(2, 1, 2))
+    g2.gs2_apply(a, s, b, x, g2.RelaxConfig(2, 1, 2))
+    assert np.array_equal(xt.cpu().numpy(), x)
+    m = g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, 1))
+    r = torch.from_numpy(b).cuda()
+    z = m.apply(r)
+    assert z is not r and z.is_cuda
+    assert np.array_equal(z.cpu().numpy(), m.apply(b))
+
+
+@pytest.mark.parametrize("label", GMRES_FAST + ["ela3d_8__m60__gs2_1_1_1", "ela3d_8__m60__gs2_1_1_3",
+                                                "cd3d_16__m60__gs2_1_1_2__same",
+                                                "cd3d_16__m60__gs2_1_1_2__single_inside_double"])
+def test_gmres_iteration_counts(label, gmres_golden):
+    want = gmres_golden["runs"][label]
+    prob, m, kind, (nt, nk, nj), prec, nb = parse_gmres_label(label)
+    a = golden_problem(prob)
+    b = g2.random_rhs(a.nrows, 0)
+    cfg = g2.RelaxConfig(nt, nk, nj)
+    if kind == "hybrid_gs2":
+        part = g2.BlockPartition.regular(a.nrows, nb)
+
+        def pc(r):
+            z = np.zeros(a.nrows)
+            g2.hybrid_relax(a, part, np.asarray(r, dtype=np.float64), z, cfg, local="gs2")
+            return z
+    else:
+        pc = g2.Preconditioner(a, kind, cfg if kind != "none" else None, precision=prec)
+    x, h = g2.gmres(a, b, pc, restart=m, tol=1e-9)
+    assert h.converged == want["converged"]
+    assert abs(h.iterations - want["iterations"]) <= iteration_tolerance(label, gmres_golden), \
+        (h.iterations, want["iterations"])
+    true = np.linalg.norm(b - oracle.spmv(oracle.Matrix(a), x)) / np.linalg.norm(b)
+    assert h.final_rel_res == pytest.approx(true, rel=1e-10, abs=1e-16)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("label", ["lap3d_64__m60__gs2_1_1_0", "lap3d_64__m60__gs2_1_1_1", "lap3d_64__m60__gs2_1_1_2",
+                                   "lap3d_64__m60__gs2_1_1_3", "lap3d_64__m60__gs_seq_1",
+                                   "ela3d_16__m60__gs2_1_1_1", "ela3d_16__m60__gs2_1_1_3",
+                                   "ela3d_16__m60__gs2_1_1_10", "ela3d_16__m60__jr_1", "ela3d_16__m60__gs_seq_1"])
+def test_gmres_iteration_counts_larger(label, gmres_golden):
+    want = gmres_golden["runs"][label]
+    prob, m, kind, (nt, nk, nj), prec, nb = parse_gmres_label(label)
+    if prob.startswith("lap3d"):
+        a = g2.laplace3d(int(prob.split("_")[1]), device="cuda")
+        b = g2.random_rhs(a.nrows, 0, device="cuda")
+    else:
+        a = golden_problem(prob)
+        b = g2.random_rhs(a.nrows, 0)
+    pc = g2.Preconditioner(a, kind, g2.RelaxConfig(nt, nk, nj), precision=prec)
+    _, h = g2.gmres(a, b, pc, restart=m, tol=1e-9)
+    assert h.converged
+    assert h.iterations == want["iterations"]
+    np.testing.assert_allclose(h.rel_res[:50], want["rel_res"][:50], rtol=1e-6)
+
+
+def test_gmres_api_semantics():
+    a = g2.from_dense(np.eye(4))
+    x, h = g2.gmres(a, np.array([4.0, -1.0, 2.0, 0.5]))
+    assert h.converged and h.iterations == 1
+    a2 = g2.from_dense([[2.0, -1.0], [-1.0, 2.0]])
+    x, h = g2.gmres(a2, np.array([1.0, 1.0]), x0=np.array([1.0, 1.0]), tol=1e-12)
+    assert h.converged and h.iterations == 0 and np.array_equal(x, [1.0, 1.0])
+    a = g2.laplace2d(20)
+    _, h = g2.gmres(a, g2.random_rhs(400, 1), tol=1e-14, maxit=5)
+    assert not h.converged and h.iterations == 5
+    _, h = g2.gmres(a, np.zeros(400))
+    assert h.converged and h.iterations == 0
+    with pytest.raises(ValueError):
+        g2.gmres(a2, np.ones(2), tol=0.0)
+    with pytest.raises(ValueError):
+        g2.gmres(a2, np.ones(2), restart=0)
+
+
+def test_reference_seam_callable_preconditioner():
+    """The duck-typed seam (krylov.py:147-154): a host callable drives the GPU gmres."""
+    a = g2.laplace2d(16)
+    b = g2.random_rhs(a.nrows, 2)
+    om = oracle.Precond(a, "gs2", n_t=1, n_k=1, n_j=1)
+    _, h1 = g2.gmres(a, b, om.apply, restart=30)
+    _, h2 = g2.gmres(a, b, g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, 1)), restart=30)
+    assert h1.converged and h2.converged and h1.iterations == h2.iterations
+
+
+def test_stationary_elasticity_pattern(gmres_golden):
+    """Stand-alone smoother (cli.py:136-152): JR diverges, GS2 n_j=3 / SGS2 n_j=10 converge (acceptance 06)."""
+    a = g2.elasticity3d(4)
+    s = g2.extract_splitting(a)
+    b = g2.random_rhs(a.nrows, 31)
+    bn = np.linalg.norm(b)
+    for label, step in (("jr", lambda x: g2.jr_sweeps(a, s, b, x, 1)),
+                        ("gs2_nj3_fwd", lambda x: g2.gs2_apply(a, s, b, x, g2.RelaxConfig(1, 1, 3))),
+                        ("sgs2_nj10", lambda x: g2.gs2_apply(a, s, b, x, g2.RelaxConfig(1, 1, 10,
+                                                                                          direction="symmetric")))):
+        want = gmres_golden["stationary"][f"ela3d_4__{label}"]
+        x = np.zeros(a.nrows)
+        got = []
+        for _ in range(50):
+            step(x)
+            got.append(np.linalg.norm(b - g2.spmv(a, x)) / bn)
+        np.testing.assert_allclose(got, want, rtol=1e-12)
