@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""bench.py -- GS2-preconditioned GMRES(60) on B200 (BASELINE.json metric / configs).
+
+One step = one full GMRES(60) restart cycle (60 Arnoldi iterations, each one
+zero-start GS2(1,1,1) preconditioner application + one SpMV + CGS2
+orthogonalisation, then the cycle-end update and true residual) on the
+synthetic 3D 7-point Laplace problem, right-hand side random_rhs(n, 0):
+
+* N = 1: config C2, laplace3d 256^3 (16.7 M rows) on one B200.
+* N > 1: config C5, laplace3d 512^3 row-partitioned into N z-slabs (one rank
+  per GPU; hybrid block-Jacobi GS2 preconditioner, NCCL halo + allreduce).
+
+``value`` = algorithmic HBM GB/s of the cycle (SURVEY.md §8(d) byte model:
+split-CSR int32 + fp64 per pass, summed over every kernel of the cycle and
+over all ranks) divided by the device time of the step, max over ranks.
+The GS2 sweep figure of the metric (non-zero x, n_j = 1, 2.946 GB at 256^3)
+and the paper's same-device baselines (JR, level-scheduled GS, n_j = 0..3)
+are reported under "sweeps"; time-to-solution of the full solve under "tts".
+
+``--impl reference`` times the reference's CPU algorithm (the C oracle port,
+all host threads) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "GMRES+GS2 time-to-solution & GS2 sweep GB/s vs HBM peak at 1/2/4/8 B200"
+
+
+# ---------------------------------------------------------------- byte model
+class Model:
+    """Algorithmic bytes of each kernel of the path (split-CSR, int32 idx, fp64 values, each operand once)."""
+
+    def __init__(self, n: int, nnz_l: int, nnz_u: int, val_bytes: int = 8):
+        self.n = n
+        self.V = 8 * n
+        self.ML = (4 + val_bytes) * nnz_l + 4 * (n + 1)
+        self.MU = (4 + val_bytes) * nnz_u + 4 * (n + 1)
+
+    def spmv(self):
+        return self.ML + self.MU + 3 * self.V
+
+    def gs2_sweep(self, n_j: int):
+        V, ML, MU = self.V, self.ML, self.MU
+        b = ML + MU + 4 * V
+        if n_j == 1:
+            b += ML + 3 * V
+        elif n_j >= 2:
+            b += (ML + 2 * V) + (n_j - 2) * (ML + 3 * V) + (ML + 4 * V)
+        return b
+
+    def precond_gs2_zero_start(self, n_j: int):
+        """GS2(1,1,n_j) from z = 0: the residual pass is elided (b - A*0 == b)."""
+        V, ML = self.V, self.ML
+        if n_j == 0:
+            return 3 * V
+        if n_j == 1:
+            return ML + 3 * V
+        return (ML + 3 * V) + (n_j - 2) * (ML + 3 * V) + (ML + 4 * V)
+
+    def cgs2(self, k: int):
+        return 2 * (2 * k + 3) * self.V
+
+    def arnoldi_step(self, j: int, n_j: int):
+        return self.precond_gs2_zero_start(n_j) + self.spmv() + self.cgs2(j + 1) + 2 * self.V
+
+    def cycle(self, m: int, n_j: int):
+        steps = sum(self.arnoldi_step(j, n_j) for j in range(m))
+        end = (m + 1) * self.V + self.precond_gs2_zero_start(n_j) + 3 * self.V + self.spmv() + 3 * self.V
+        return steps + end
+
+
+def laplace3d_nnz(nx, ny, nz):
+    n = nx * ny * nz
+    nnz_l = (nx - 1) * ny * nz + nx * (ny - 1) * nz + nx * ny * (nz - 1)
+    return n, nnz_l, nnz_l
+
+
+# ---------------------------------------------------------------- environment helpers
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([c.strip() for c in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        pw = [float(r[3]) for r in self.rows if r[3].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(
+        os.environ.get("LOCAL_RANK", "0"))
+
+
+# ---------------------------------------------------------------- CPU baseline (oracle port)
+def cpu_gmres_sample(nx: int, iters: int, threads: int):
+    """The C oracle (reference algorithm: MGS GMRES, GS2(1,1,1)) on laplace3d nx^3, first `iters` iterations."""
+    import numpy as np
+
+    import oracle
+    from paper_2104_01196_b200 import problems
+
+    oracle.set_threads(threads)
+    a = problems.laplace3d(nx)
+    m = oracle.Matrix(a)
+    m.split()
+    b = oracle.random_rhs(a.nrows, 0)
+    pre = oracle.Precond(m, "gs2", n_t=1, n_k=1, n_j=1)
+    t0 = time.perf_counter()
+    _, hist, _ = oracle.gmres(m, b, pre, restart=60, tol=1e-9, maxit=iters)
+    dt = time.perf_counter() - t0
+    n, nl, nu = laplace3d_nnz(nx, nx, nx)
+    mod = Model(n, nl, nu)
+    k = len(hist) - 1
+    bytes_ = sum(mod.arnoldi_step(j, 1) for j in range(k)) + (k + 1) * mod.V + mod.precond_gs2_zero_start(1) \
+        + 6 * mod.V + mod.spmv()
+    return bytes_ / dt / 1e9, dt, k, np.float64(hist[-1])
+
+
+def reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    nx = 256 if world == 1 else 512
+    iters = args.ref_iters
+    vals = []
+    for s in range(args.warmup + args.steps):
+        gbs, dt, k, _ = cpu_gmres_sample(nx, iters, threads)
+        if s >= args.warmup:
+            vals.append((gbs, dt))
+    v = statistics.median(g for g, _ in vals)
+    ms = statistics.median(d for _, d in vals) * 1e3
+    sample = f"first {iters} GMRES(60)+GS2(1,1,1) iterations of laplace3d {nx}^3 per step (setup excluded)"
+    line = {
+        "metric": METRIC, "value": round(v, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"laplace3d {nx}^3 GMRES(60) + GS2(1,1,1) preconditioner (bounded sample)",
+                   "sample": sample},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- GPU arm
+def ours(args):
+    import numpy as np
+    import torch
+
+    import paper_2104_01196_b200 as g2
+    from paper_2104_01196_b200 import _native
+    from paper_2104_01196_b200.krylov import KernelTimer
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_2104_01196_b200 import distributed as gd
+
+        return gd.bench_rank(args, METRIC, Model, laplace3d_nnz, ClockSampler, peaks)
+
+    lib = _native.load()
+    nx = args.nx or 256
+    n_j = 1
+    m = args.restart
+    a = g2.laplace3d(nx, device=local)
+    n = a.nrows
+    b = g2.random_rhs(n, 0, device=f"cuda:{local}")
+    pc = g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, n_j))
+    mod = Model(n, a.nnz_l, a.nnz_u)
+    cycle_bytes = mod.cycle(m, n_j)
+    hbm, peak_kind = peaks()
+
+    def step():
+        g2.gmres(a, b, pc, restart=m, tol=1e-300, maxit=m)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = lib.rs_launch_count()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+    launches = lib.rs_launch_count() - l0
+    ms = e0.elapsed_time(e1) / args.steps
+    value = cycle_bytes / (ms * 1e-3) / 1e9
+
+    # per-kernel-group attribution inside one more (instrumented) cycle
+    with KernelTimer() as kt:
+        step()
+    ksum = kt.summary()
+    group_bytes = {
+        "precond": (m + 1) * mod.precond_gs2_zero_start(n_j),
+        "spmv": (m + 2) * mod.spmv(),
+        "gemv_t": 2 * sum((k + 1) * mod.V for k in range(1, m + 1)),
+        "gemv_n": 2 * sum((k + 2) * mod.V for k in range(1, m + 1)),
+        "scale": m * 2 * mod.V,
+    }
+    total_ms = sum(t for _, t in ksum.values())
+    kernels = {}
+    for g, (cnt, t) in ksum.items():
+        gb = group_bytes.get(g)
+        kernels[g] = {"launches": cnt, "ms": round(t, 3), "share": round(t / total_ms, 3) if total_ms else None,
+                      "gbs": round(gb / (t * 1e-3) / 1e9, 1) if gb and t else None}
+    dom = max((g for g in kernels if g in group_bytes), key=lambda g: kernels[g]["ms"])
+    traffic = None
+    tfile = ROOT / "profiles" / "traffic.json"
+    if tfile.exists():
+        traffic = json.loads(tfile.read_text()).get(dom)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["gbs"], "peak": hbm, "unit": "GB/s",
+                "frac": round(kernels[dom]["gbs"] / hbm, 3), "traffic": traffic,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}
+
+    # e2e through the public API with host buffers: pinned b in, x out
+    b_host = b.cpu().pin_memory()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        x = g2.gmres(a, b_host, pc, restart=m, tol=1e-300, maxit=m)[0]
+        assert not x.is_cuda
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    e2e = {"value": round(cycle_bytes / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
+           "d2h_bytes_per_step": 8 * n, "ms_per_step": round(e2e_ms, 3)}
+
+    sweeps = sweep_table(g2, torch, a, mod, hbm) if not args.no_sweeps else None
+    tts = None
+    if not args.no_tts:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, h = g2.gmres(a, b, pc, restart=m, tol=1e-9)
+        torch.cuda.synchronize()
+        tts = {"seconds": round(time.perf_counter() - t0, 3), "iterations": h.iterations, "converged": h.converged,
+               "final_rel_res": h.final_rel_res, "preconditioner": "gs2(1,1,1)", "restart": m, "tol": 1e-9}
+    cpu = None
+    if not args.no_cpu_baseline:
+        gbs, dt, k, _ = cpu_gmres_sample(nx, args.cpu_iters, 1)
+        cpu = {"value": round(gbs, 3), "unit": "GB/s", "cores": 1, "kind": "port",
+               "sample": f"C oracle (reference algorithm), first {k} GMRES(60)+GS2(1,1,1) iterations of "
+                         f"laplace3d {nx}^3 on 1 host core, {dt:.1f} s"}
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C2: laplace3d {nx}^3 ({n} rows), one GMRES({m}) cycle with GS2(1,1,1) "
+                               f"zero-start preconditioner, b = random_rhs(n, 0)",
+                   "bytes_per_step": cycle_bytes, "ms_per_iteration": round(ms / m, 4),
+                   "l2": "inputs larger than L2 (V basis 61 x 134 MB, matrix 1.7 GB)", "parallelism": "1 GPU"},
+        "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "clocks": clk.summary(), "sweeps": sweeps, "tts": tts,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def sweep_table(g2, torch, a, mod, hbm, reps: int = 10):
+    """Same-device comparison of the paper's relaxations on x != 0 (b = rhs(0), x = rhs(1))."""
+    n = a.nrows
+    dev = a.torch_device
+    b = g2.random_rhs(n, 0, device=dev)
+    x0 = g2.random_rhs(n, 1, device=dev)
+    s = g2.extract_splitting(a)
+    out = {}
+
+    def timeit(fn, nbytes):
+        x = x0.clone()
+        fn(x)  # warm-up (builds level sets etc.)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn(x)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        r = {"ms": round(ms, 4)}
+        if nbytes:
+            r["gb"] = round(nbytes / 1e9, 4)
+            r["gbs"] = round(nbytes / (ms * 1e-3) / 1e9, 1)
+            r["frac"] = round(nbytes / (ms * 1e-3) / 1e9 / hbm, 3)
+        return r
+
+    for nj in range(4):
+        cfg = g2.RelaxConfig(1, 1, nj)
+        out[f"gs2_nj{nj}"] = timeit(lambda x, cfg=cfg: g2.gs2_apply(a, s, b, x, cfg), mod.gs2_sweep(nj))
+    out["jr"] = timeit(lambda x: g2.jr_sweeps(a, s, b, x, 1), mod.gs2_sweep(0))
+    out["gs_level_sched"] = timeit(lambda x: g2.gs_sequential_sweep(a, s, b, x, "forward"),
+                                   mod.ML + mod.MU + 3 * mod.V)
+    y = torch.empty_like(b)
+    out["spmv"] = timeit(lambda x: y.copy_(g2.spmv(a, x)), mod.spmv())
+    return out
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--nx", type=int, default=0)
+    p.add_argument("--restart", type=int, default=60)
+    p.add_argument("--no-tts", action="store_true")
+    p.add_argument("--no-sweeps", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-iters", type=int, default=8)
+    p.add_argument("--ref-iters", type=int, default=4)
+    args = p.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+    return ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -353,7 +353,7 @@ static int build_split(rs_matrix* m, const Src& src) {
         if (m->nrows > 0) {
           k_cast_diag<T><<<grid_for(m->nrows, B), B>>>(diag, d, m->nrows);
           RS_COUNT_LAUNCH();
-          k_fill<Src, T><<<grid_for(m->nrows, B), B>>>(src, s, out_of(L, 0), out_of(U, 0),
+          k_fill<Src, T><<<grid_for(m->nrows, B), B>>>(src, s, out_of(L, m->row0), out_of(U, m->row0),
                                                          out_of(Elo, m->row0 - m->halo_lo), out_of(Ehi, s.rowe),
                                                          diag);
           RS_COUNT_LAUNCH();
@@ -433,11 +433,13 @@ int build_levels_t(rs_matrix* m, int backward) {
   if ((st = host_tri(oth, sp2, col2))) return st;
   int64_t n = m->nrows;
   std::vector<int32_t> level(n, 0);
+  bool bad_col = false;
   auto row_cols = [&](const std::vector<int64_t>& p, const std::vector<int32_t>& c, int64_t i, auto&& f) {
     int64_t s = i >> 5, lane = i & 31, w = (p[s + 1] - p[s]) / kSlice;
     for (int64_t j = 0; j < w; ++j) {
       int32_t cc = c[p[s] + j * kSlice + lane];
-      if (cc >= 0) f(cc);
+      if (cc >= n) bad_col = true;
+      else if (cc >= 0) f(cc);
     }
   };
   int32_t maxl = 0;
@@ -455,6 +457,10 @@ int build_levels_t(rs_matrix* m, int backward) {
       level[i] = l;
       maxl = std::max(maxl, l);
     }
+  }
+  if (bad_col) {
+    set_error(RS_ERR_ARG, "internal: triangle column outside the local block");
+    return RS_ERR_ARG;
   }
   // structural symmetry: every entry (i, c) of the "other" triangle must appear as (c, i) in dep.
   int sym = 1;

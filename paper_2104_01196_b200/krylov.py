@@ -178,6 +178,54 @@ def _as_operator(m):
     raise ValueError(f"preconditioner must be None, have .apply, or be callable, got {type(m)!r}")
 
 
+class KernelTimer:
+    """Optional CUDA-event timing of the GMRES kernel groups on the launching stream.
+
+    ``with KernelTimer() as kt: gmres(...)`` records an event pair around every
+    group (precond, spmv, gemv_t, gemv_n, scale, vec); ``kt.summary()`` returns
+    {group: (launches, total_ms)}.  Events do not synchronise the stream.
+    """
+
+    _active = None
+
+    def __init__(self):
+        self.events = {}
+
+    def __enter__(self):
+        KernelTimer._active = self
+        return self
+
+    def __exit__(self, *exc):
+        KernelTimer._active = None
+
+    def start(self, name):
+        torch = _torch()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        self.events.setdefault(name, []).append((e0, e1))
+        return e1
+
+    def summary(self):
+        _torch().cuda.synchronize()
+        return {k: (len(v), sum(a.elapsed_time(b) for a, b in v)) for k, v in self.events.items()}
+
+
+class _timed:
+    __slots__ = ("e1",)
+
+    def __init__(self, name):
+        kt = KernelTimer._active
+        self.e1 = kt.start(name) if kt is not None else None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        if self.e1 is not None:
+            self.e1.record()
+
+
 class _Workspace:
     """Device buffers of one GMRES(m) solve (allocated once per solve)."""
 
@@ -224,8 +272,10 @@ def gmres(a, b, m=None, restart: int = 60, tol: float = 1e-9, maxit: int = 10000
         raise ValueError("gmres needs a double-precision matrix")
     n = dm.nrows
     dev = dm.torch_device
-    host_out = not _is_tensor(b)
-    bt = b.to(dev, torch.float64) if _is_tensor(b) else torch.from_numpy(np.ascontiguousarray(b, np.float64)).to(dev)
+    numpy_out = not _is_tensor(b)
+    cpu_tensor_out = _is_tensor(b) and not b.is_cuda
+    bt = (b.to(dev, torch.float64, non_blocking=cpu_tensor_out and b.is_pinned()) if _is_tensor(b)
+          else torch.from_numpy(np.ascontiguousarray(b, np.float64)).to(dev))
     if x0 is None:
         x = torch.zeros(n, dtype=torch.float64, device=dev)
     else:
@@ -233,7 +283,11 @@ def gmres(a, b, m=None, restart: int = 60, tol: float = 1e-9, maxit: int = 10000
              else torch.from_numpy(np.array(x0, dtype=np.float64)).to(dev))
     op = _as_operator(m)
     x, hist, conv = _gmres_device(dm, bt, x, op, restart, tol, maxit)
-    return (x.cpu().numpy() if host_out else x), ConvergenceHistory(np.array(hist), conv)
+    if numpy_out:
+        x = x.cpu().numpy()
+    elif cpu_tensor_out:
+        x = x.cpu()
+    return x, ConvergenceHistory(np.array(hist), conv)
 
 
 def _apply_op(op, v, z, ws):
@@ -270,7 +324,8 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit):
         N.check(s, what)
 
     def spmv(src, dst):
-        chk(lib.rs_spmv(dm.handle, _p(src), None, None, _p(dst), st), "spmv")
+        with _timed("spmv"):
+            chk(lib.rs_spmv(dm.handle, _p(src), None, None, _p(dst), st), "spmv")
 
     def norm_of(vec):
         chk(lib.rs_dot(n, _p(vec), _p(vec), _p(nrm2_slot), _p(work), st), "dot")
@@ -310,15 +365,21 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit):
         while j + 1 < restart and total < maxit:
             j += 1
             total += 1
-            _apply_op(op, V[j], ws.z, ws)
+            with _timed("precond"):
+                _apply_op(op, V[j], ws.z, ws)
             spmv(ws.z, ws.w)
             k = j + 1
             # CGS2: two classical Gram-Schmidt passes (h = h1 + h2), then ||w||
-            chk(lib.rs_gemv_t(_p(V), n, k, n, _p(ws.w), _p(h1), _p(ws.flags), _p(work), st), "gemv_t")
-            chk(lib.rs_gemv_n_update(_p(V), n, k, n, _p(h1), _p(ws.w), None, _p(work), st), "gemv_n")
-            chk(lib.rs_gemv_t(_p(V), n, k, n, _p(ws.w), _p(h2), None, _p(work), st), "gemv_t")
-            chk(lib.rs_gemv_n_update(_p(V), n, k, n, _p(h2), _p(ws.w), _p(nrm2_slot), _p(work), st), "gemv_n")
-            chk(lib.rs_scale_by_norm(n, _p(ws.w), _p(nrm2_slot), _p(V[j + 1]), st), "scale")
+            with _timed("gemv_t"):
+                chk(lib.rs_gemv_t(_p(V), n, k, n, _p(ws.w), _p(h1), _p(ws.flags), _p(work), st), "gemv_t")
+            with _timed("gemv_n"):
+                chk(lib.rs_gemv_n_update(_p(V), n, k, n, _p(h1), _p(ws.w), None, _p(work), st), "gemv_n")
+            with _timed("gemv_t"):
+                chk(lib.rs_gemv_t(_p(V), n, k, n, _p(ws.w), _p(h2), None, _p(work), st), "gemv_t")
+            with _timed("gemv_n"):
+                chk(lib.rs_gemv_n_update(_p(V), n, k, n, _p(h2), _p(ws.w), _p(nrm2_slot), _p(work), st), "gemv_n")
+            with _timed("scale"):
+                chk(lib.rs_scale_by_norm(n, _p(ws.w), _p(nrm2_slot), _p(V[j + 1]), st), "scale")
             ws.pinned.copy_(scal)  # synchronises the stream: one D2H per Arnoldi step
             ws.pinned_flags.copy_(ws.flags)
             hv = ws.pinned.numpy()
