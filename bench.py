@@ -261,8 +261,9 @@ def ours(args):
     group_bytes = {
         "precond": (m + 1) * mod.precond_gs2_zero_start(n_j),
         "spmv": (m + 2) * mod.spmv(),
-        "gemv_t": 2 * sum((k + 1) * mod.V for k in range(1, m + 1)),
-        "gemv_n": 2 * sum((k + 2) * mod.V for k in range(1, m + 1)),
+        "cgs_dots": sum((k + 1) * mod.V for k in range(1, m + 1)),
+        "cgs_update_dots": sum((k + 2) * mod.V for k in range(1, m + 1)),
+        "cgs_update_norm": sum((k + 2) * mod.V for k in range(1, m + 1)),
         "scale": m * 2 * mod.V,
     }
     total_ms = sum(t for _, t in ksum.values())

@@ -167,6 +167,15 @@ int rs_gemv_t(const double *V, int64_t ldv, int k, int64_t n, const double *w, d
 int rs_gemv_n_update(const double *V, int64_t ldv, int k, int64_t n, const double *h, double *w, double *nrm2,
                      double *work, rs_stream_t stream);
 
+/* One fused Gram-Schmidt pass over V (TMA bulk-copy pipeline through shared
+ * memory; V and w read once):  if h_in: w -= V^T-combination h_in;  then if
+ * h_out: h_out = V^T w;  if nrm2: nrm2[0] = w.w.  The CGS2 step of
+ * krylov.py:217-220 is rs_cgs_pass(h_out=h1) ; rs_cgs_pass(h_in=h1, h_out=h2) ;
+ * rs_cgs_pass(h_in=h2, nrm2).  Falls back to the separate kernels for k > 64
+ * or unaligned V / w / odd n. */
+int rs_cgs_pass(const double *V, int64_t ldv, int k, int64_t n, const double *h_in, double *w, double *h_out,
+                double *nrm2, int *nonfinite, double *work, rs_stream_t stream);
+
 /* out[r] = sum_{i<k} y[i] V_i[r]  (krylov.py:244 v[:j+1].T @ y) */
 int rs_gemv_n(const double *V, int64_t ldv, int k, int64_t n, const double *y, double *out, rs_stream_t stream);
 

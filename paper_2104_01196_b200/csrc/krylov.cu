@@ -220,6 +220,154 @@ __global__ void k_cast_up(int64_t n, const float* __restrict__ in, double* __res
   if (i < n) out[i] = (double)in[i];
 }
 
+
+// ------------------------------------------------------------------ fused CGS pass (TMA bulk-copy pipeline)
+// One pass over the Arnoldi basis for a chunk of rows at a time: the k basis
+// segments and w are streamed into shared memory with cp.async.bulk (3-stage
+// ring on mbarriers), then
+//   UPDATE: w[r] -= sum_i h_in[i] V_i[r]           (thread per row, written back)
+//   DOTS:   h_out[i] += sum_r V_i[r] w[r]           (warp per basis vector)
+//   NORM:   nrm2 += w[r]^2
+// so "update + re-orthogonalisation dots" of CGS2 read V once instead of twice.
+constexpr int kCgsThreads = 256;
+constexpr int kCgsWarps = kCgsThreads / 32;
+constexpr int kCgsStages = 3;
+constexpr int kCgsMaxK = 64;
+constexpr int kCgsMaxQ = kCgsMaxK / kCgsWarps;
+constexpr int kCgsStageBytes = 64 * 1024;
+constexpr int kCgsBlocks = 148;
+
+static int cgs_chunk_rows(int k) {
+  int ch = kCgsStageBytes / (8 * (k + 1));
+  ch = std::max(128, std::min(4096, ch)) & ~127;
+  return ch;
+}
+
+static size_t cgs_smem_bytes(int k, int ch) {
+  return (size_t)kCgsStages * (k + 1) * ch * sizeof(double) + kCgsMaxK * sizeof(double) + kCgsStages * 8 + 16;
+}
+
+template <bool UPDATE, bool DOTS, bool NORM>
+__global__ void __launch_bounds__(kCgsThreads, 1)
+    k_cgs(const double* __restrict__ V, int64_t ldv, int k, int64_t n, int ch, int64_t rows_per_blk,
+          const double* __restrict__ h_in, double* __restrict__ w, double* __restrict__ partial, int* nonfinite) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int stage_elems = (k + 1) * ch;
+  double* st = reinterpret_cast<double*>(smraw);
+  double* hs = st + (size_t)kCgsStages * stage_elems;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(hs + kCgsMaxK);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_blk;
+  const int64_t r1 = n < r0 + rows_per_blk ? n : r0 + rows_per_blk;
+  const int nchunks = r1 > r0 ? (int)((r1 - r0 + ch - 1) / ch) : 0;
+  if (UPDATE)
+    for (int i = tid; i < k; i += kCgsThreads) hs[i] = h_in[i];
+  if (tid == 0) {
+    for (int s = 0; s < kCgsStages; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int c) {
+    const int s = c % kCgsStages;
+    const int64_t c0 = r0 + (int64_t)c * ch;
+    const int len = (int)(r1 - c0 < ch ? r1 - c0 : ch);
+    const uint32_t bytes = (uint32_t)len * 8u;
+    double* dst = st + (size_t)s * stage_elems;
+    mbar_expect_tx(&bar[s], (uint32_t)(k + 1) * bytes);
+    for (int i = 0; i < k; ++i) bulk_g2s(dst + (size_t)i * ch, V + (int64_t)i * ldv + c0, bytes, &bar[s]);
+    bulk_g2s(dst + (size_t)k * ch, w + c0, bytes, &bar[s]);
+  };
+  if (tid == 0)
+    for (int c = 0; c < kCgsStages && c < nchunks; ++c) issue(c);
+  double acc[kCgsMaxQ];
+#pragma unroll
+  for (int q = 0; q < kCgsMaxQ; ++q) acc[q] = 0.0;
+  double nrm = 0.0;
+  bool bad = false;
+  for (int c = 0; c < nchunks; ++c) {
+    const int s = c % kCgsStages;
+    mbar_wait(&bar[s], (uint32_t)((c / kCgsStages) & 1));
+    const int64_t c0 = r0 + (int64_t)c * ch;
+    const int len = (int)(r1 - c0 < ch ? r1 - c0 : ch);
+    const double* Vs = st + (size_t)s * stage_elems;
+    double* ws = st + (size_t)s * stage_elems + (size_t)k * ch;
+    if (UPDATE || NORM || nonfinite) {
+      for (int r = tid; r < len; r += kCgsThreads) {
+        double wv = ws[r];
+        if (nonfinite) bad |= !isfinite(wv);
+        if (UPDATE) {
+          double sum = 0.0;
+          int i = 0;
+          for (; i + 4 <= k; i += 4) {
+            sum += hs[i] * Vs[(size_t)i * ch + r];
+            sum += hs[i + 1] * Vs[(size_t)(i + 1) * ch + r];
+            sum += hs[i + 2] * Vs[(size_t)(i + 2) * ch + r];
+            sum += hs[i + 3] * Vs[(size_t)(i + 3) * ch + r];
+          }
+          for (; i < k; ++i) sum += hs[i] * Vs[(size_t)i * ch + r];
+          wv = wv - sum;
+          w[c0 + r] = wv;
+          ws[r] = wv;
+        }
+        if (NORM) nrm += wv * wv;
+      }
+    }
+    if (UPDATE && DOTS) __syncthreads();
+    if (DOTS) {
+#pragma unroll
+      for (int q = 0; q < kCgsMaxQ; ++q) {
+        const int i = warp + q * kCgsWarps;
+        if (i < k) {
+          const double* vi = Vs + (size_t)i * ch;
+          double a0 = 0.0, a1 = 0.0;
+          int r = lane;
+          for (; r + 32 < len; r += 64) {
+            a0 += vi[r] * ws[r];
+            a1 += vi[r + 32] * ws[r + 32];
+          }
+          if (r < len) a0 += vi[r] * ws[r];
+          acc[q] += a0 + a1;
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && c + kCgsStages < nchunks) issue(c + kCgsStages);
+  }
+  const int stride = k + 1;
+  if (DOTS) {
+#pragma unroll
+    for (int q = 0; q < kCgsMaxQ; ++q) {
+      const int i = warp + q * kCgsWarps;
+      if (i < k) {
+        double v = warp_sum(acc[q]);
+        if (lane == 0) partial[(int64_t)blockIdx.x * stride + i] = v;
+      }
+    }
+  }
+  if (NORM) {
+    __shared__ double red[kCgsWarps];
+    nrm = warp_sum(nrm);
+    if (lane == 0) red[warp] = nrm;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int q = 0; q < kCgsWarps; ++q) t += red[q];
+      partial[(int64_t)blockIdx.x * stride + k] = t;
+    }
+  }
+  if (nonfinite && __syncthreads_or(bad) && tid == 0) *nonfinite = 1;
+}
+
+// out[j] = sum_b partial[b*stride + off + j] for j < cnt, b ascending
+__global__ void k_reduce_strided(const double* __restrict__ partial, int nblk, int stride, int off, int cnt,
+                                 double* __restrict__ out) {
+  for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += partial[(int64_t)b * stride + off + j];
+    out[j] = s;
+  }
+}
+
 static int grid_stride_blocks(int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
 }
@@ -230,7 +378,7 @@ using namespace rs;
 
 extern "C" {
 
-int64_t rs_reduce_work_doubles(int k) { return (int64_t)kRedBlocks * std::max(k, 1); }
+int64_t rs_reduce_work_doubles(int k) { return (int64_t)kRedBlocks * (std::max(k, 1) + 2); }
 
 int rs_gemv_t(const double* V, int64_t ldv, int k, int64_t n, const double* w, double* h, int* nonfinite,
               double* work, rs_stream_t stream) {
@@ -269,6 +417,55 @@ int rs_gemv_n_update(const double* V, int64_t ldv, int k, int64_t n, const doubl
     RS_COUNT_LAUNCH();
   }
   RS_CHECK_LAUNCH("rs_gemv_n_update");
+  return RS_OK;
+}
+
+
+int rs_cgs_pass(const double* V, int64_t ldv, int k, int64_t n, const double* h_in, double* w, double* h_out,
+                double* nrm2, int* nonfinite, double* work, rs_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (k < 1 || n < 0 || !work || (!h_out && !nrm2 && !h_in)) {
+    set_error(RS_ERR_ARG, "rs_cgs_pass: bad arguments");
+    return RS_ERR_ARG;
+  }
+  const bool aligned = (ldv % 2 == 0) && (n % 2 == 0) && ((uintptr_t)V % 16 == 0) && ((uintptr_t)w % 16 == 0);
+  if (k > kCgsMaxK || !aligned) {
+    // generic path: separate update / dots / norm kernels
+    int e;
+    if (h_in && (e = rs_gemv_n_update(V, ldv, k, n, h_in, w, h_out ? nullptr : nrm2, work, stream))) return e;
+    if (h_out && (e = rs_gemv_t(V, ldv, k, n, w, h_out, nonfinite, work, stream))) return e;
+    if (h_out && nrm2 && (e = rs_dot(n, w, w, nrm2, work, stream))) return e;
+    if (!h_in && !h_out && nrm2 && (e = rs_dot(n, w, w, nrm2, work, stream))) return e;
+    return RS_OK;
+  }
+  const int ch = cgs_chunk_rows(k);
+  const size_t smem = cgs_smem_bytes(k, ch);
+  int64_t rows = ((n + kCgsBlocks - 1) / kCgsBlocks + ch - 1) / ch * ch;
+  int nblk = (int)std::max<int64_t>(1, (n + rows - 1) / std::max<int64_t>(rows, 1));
+  const bool U = h_in != nullptr, D = h_out != nullptr, Nm = nrm2 != nullptr;
+#define RS_CGS_LAUNCH(u, d, nm)                                                                          \
+  do {                                                                                                   \
+    cudaFuncSetAttribute(k_cgs<u, d, nm>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
+    k_cgs<u, d, nm><<<nblk, kCgsThreads, smem, st>>>(V, ldv, k, n, ch, rows, h_in, w, work, nonfinite); \
+    RS_COUNT_LAUNCH();                                                                                   \
+  } while (0)
+  if (U && D && Nm) RS_CGS_LAUNCH(true, true, true);
+  else if (U && D) RS_CGS_LAUNCH(true, true, false);
+  else if (U && Nm) RS_CGS_LAUNCH(true, false, true);
+  else if (U) RS_CGS_LAUNCH(true, false, false);
+  else if (D && Nm) RS_CGS_LAUNCH(false, true, true);
+  else if (D) RS_CGS_LAUNCH(false, true, false);
+  else RS_CGS_LAUNCH(false, false, true);
+#undef RS_CGS_LAUNCH
+  if (D) {
+    k_reduce_strided<<<1, 64, 0, st>>>(work, nblk, k + 1, 0, k, h_out);
+    RS_COUNT_LAUNCH();
+  }
+  if (Nm) {
+    k_reduce_strided<<<1, 32, 0, st>>>(work, nblk, k + 1, k, 1, nrm2);
+    RS_COUNT_LAUNCH();
+  }
+  RS_CHECK_LAUNCH("rs_cgs_pass");
   return RS_OK;
 }
 

@@ -153,6 +153,69 @@ __global__ void k_scale_rd(int64_t n, const R* __restrict__ r, const T* __restri
   rd[i] = div_rn<T>(tv, d[i]);
 }
 
+
+// Zero-start first inner step (the preconditioner's first half-sweep from z = 0,
+// where b - A*0 == b exactly): g1 = rd - w*(D^-1T rd) with rd_k = (T)r_k / d_k
+// recomputed at every neighbour instead of being stored by a separate pass.
+// r may be float64 while T is float32 (single_inside_double): the cast and its
+// overflow check (own row only) are fused here.  FINAL: z = w*g1 written as O.
+template <typename T, typename R, typename O, bool FINAL, bool GAMMA>
+__global__ void __launch_bounds__(256) k_inner0(int64_t n, SellView<T> Tm, const R* __restrict__ r,
+                                                const T* __restrict__ d, T* __restrict__ rd_out,
+                                                T* __restrict__ gout, O* __restrict__ z, T w, T gm, T gm1,
+                                                long long* overflow) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const R rv = r[i];
+  const T ri = (T)rv;
+  if (sizeof(T) < sizeof(R) && overflow && isinf((float)ri) && isfinite((double)rv)) atomicMin(overflow, (long long)i);
+  const T rdi = div_rn<T>(ri, d[i]);
+  T t = (T)0;
+  if (!Tm.empty) {
+    const int64_t s = i >> 5;
+    const int lane = (int)(i & 31);
+    const int64_t p0 = Tm.sp[s];
+    const int wd = (int)((Tm.sp[s + 1] - p0) >> 5);
+    for (int j = 0; j < wd; ++j) {
+      const int32_t c = __ldcs(Tm.col + p0 + 32 * j + lane);
+      const T v = __ldcs(Tm.val + p0 + 32 * j + lane);
+      if (c >= 0) t = add_rn<T>(t, mul_rn<T>(v, div_rn<T>((T)r[c], d[c])));
+    }
+  }
+  T g = sub_rn<T>(rdi, mul_rn<T>(w, t));
+  if (GAMMA) g = add_rn<T>(mul_rn<T>(gm1, rdi), mul_rn<T>(gm, g));
+  if (FINAL) {
+    z[i] = (O)mul_rn<T>(w, g);
+  } else {
+    gout[i] = g;
+    rd_out[i] = rdi;
+  }
+}
+
+// z = w * (r/d) written as O (zero-start n_j = 0 / one JR sweep)
+template <typename T, typename R, typename O>
+__global__ void k_scale0(int64_t n, const R* __restrict__ r, const T* __restrict__ d, O* __restrict__ z, T w,
+                         long long* overflow) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const R rv = r[i];
+  const T ri = (T)rv;
+  if (sizeof(T) < sizeof(R) && overflow && isinf((float)ri) && isfinite((double)rv)) atomicMin(overflow, (long long)i);
+  z[i] = (O)mul_rn<T>(w, div_rn<T>(ri, d[i]));
+}
+
+// last inner step writing z = w*g as O (generic zero-start chain, n_j >= 2)
+template <typename T, typename O, bool GAMMA>
+__global__ void __launch_bounds__(256) k_inner_out(int64_t n, SellView<T> Tm, const T* __restrict__ rd,
+                                                   const T* __restrict__ gin, O* __restrict__ z, T w, T gm, T gm1) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  T t = row_accum<T>(Tm, i, gin, (T)0);
+  T g = sub_rn<T>(rd[i], mul_rn<T>(w, t));
+  if (GAMMA) g = add_rn<T>(mul_rn<T>(gm1, gin[i]), mul_rn<T>(gm, g));
+  z[i] = (O)mul_rn<T>(w, g);
+}
+
 enum InnerFinal { kNotFinal = 0, kFinalAdd = 1, kFinalSet = 2 };
 
 // one inner JR step: gout = rd - w*(D^-1T gin)  or damped; last step updates x
@@ -490,6 +553,59 @@ static int bhat_t(rs_matrix* m, const T* b, const T* x, const T* xlo, const T* x
   return RS_OK;
 }
 
+
+// Zero-start single half-sweep GS2 preconditioner (kind gs2, n_t*n_k == 1,
+// forward or backward, either form -- from z = 0 both forms give z = w*g):
+//   n_j = 0: one pass z = w*(r/d);  n_j = 1: one pass, M_L + 3V bytes;
+//   n_j >= 2: fused first step, plain middle steps, last step writes z.
+template <typename T, typename R, typename O>
+static int precond_gs2_single(rs_matrix* m, const rs_relax_cfg& cfg, const R* r, O* z, long long* overflow,
+                              cudaStream_t st) {
+  Ctx<T> c(m, st);
+  const bool bwd = cfg.direction == RS_BACKWARD;
+  SellView<T> Tm = bwd ? c.Usc : c.Lsc;
+  const T w = (T)cfg.omega, gm = (T)cfg.gamma, gm1 = (T)(1.0 - cfg.gamma);
+  const bool damped = cfg.gamma != 1.0;
+  if (!c.n) return RS_OK;
+  if (cfg.n_j == 0) {
+    k_scale0<T, R, O><<<c.grid(), kB, 0, st>>>(c.n, r, c.d, z, w, overflow);
+    RS_COUNT_LAUNCH();
+    RS_CHECK_LAUNCH("precond");
+    return RS_OK;
+  }
+  if (cfg.n_j == 1) {
+    if (damped) k_inner0<T, R, O, true, true><<<c.grid(), kB, 0, st>>>(c.n, Tm, r, c.d, nullptr, nullptr, z, w, gm, gm1, overflow);
+    else k_inner0<T, R, O, true, false><<<c.grid(), kB, 0, st>>>(c.n, Tm, r, c.d, nullptr, nullptr, z, w, gm, gm1, overflow);
+    RS_COUNT_LAUNCH();
+    RS_CHECK_LAUNCH("precond");
+    return RS_OK;
+  }
+  T* rd = (T*)m->scratch;
+  T* bufs[2] = {rd + c.n, rd + 2 * c.n};
+  if (damped) k_inner0<T, R, O, false, true><<<c.grid(), kB, 0, st>>>(c.n, Tm, r, c.d, rd, bufs[0], z, w, gm, gm1, overflow);
+  else k_inner0<T, R, O, false, false><<<c.grid(), kB, 0, st>>>(c.n, Tm, r, c.d, rd, bufs[0], z, w, gm, gm1, overflow);
+  RS_COUNT_LAUNCH();
+  const T* gin = bufs[0];
+  for (int j = 1; j < cfg.n_j; ++j) {
+    if (j == cfg.n_j - 1) {
+      if (damped) k_inner_out<T, O, true><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1);
+      else k_inner_out<T, O, false><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1);
+    } else {
+      T* gout = bufs[j & 1];
+      if (damped) k_inner<T, kNotFinal, true><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, gout, nullptr, w, gm, gm1);
+      else k_inner<T, kNotFinal, false><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, gout, nullptr, w, gm, gm1);
+      gin = gout;
+    }
+    RS_COUNT_LAUNCH();
+  }
+  RS_CHECK_LAUNCH("precond");
+  return RS_OK;
+}
+
+static bool single_half_sweep(int kind, const rs_relax_cfg& cfg) {
+  return kind == RS_PC_GS2 && cfg.n_t * cfg.n_k == 1 && cfg.direction != RS_SYMMETRIC;
+}
+
 // Preconditioner.apply (krylov.py:110-137) body in the working dtype, from z = 0.
 template <typename T>
 static int precond_body(rs_matrix* m, int kind, rs_relax_cfg cfg, const T* rhs, T* z, cudaStream_t st) {
@@ -613,6 +729,10 @@ int rs_precond_apply(rs_matrix_t m, int kind, const rs_relax_cfg* cfg, const dou
   }
   int e;
   if ((e = ensure_scratch(m))) return e;
+  if (single_half_sweep(kind, *cfg)) {
+    if (m->dtype == RS_F64) return precond_gs2_single<double, double, double>(m, *cfg, r, z, nullptr, st);
+    return precond_gs2_single<float, double, double>(m, *cfg, r, z, (long long*)overflow_flag, st);
+  }
   if (m->dtype == RS_F64) return precond_body<double>(m, kind, *cfg, r, z, st);
   // single_inside_double (krylov.py:116-118, 135-136): cast r, relax in float32, upcast z
   float* rhs = (float*)m->scratch + 4 * m->nrows;

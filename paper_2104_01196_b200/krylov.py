@@ -232,7 +232,8 @@ class _Workspace:
     def __init__(self, n: int, restart: int, device):
         torch = _torch()
         f64 = dict(dtype=torch.float64, device=device)
-        self.V = torch.empty((restart + 1, n), **f64)
+        self.ldv = n + (n & 1)  # even leading dimension: 16-byte aligned basis rows for the TMA path
+        self.V = torch.empty((restart + 1, self.ldv), **f64)[:, :n]
         self.w = torch.empty(n, **f64)
         self.z = torch.empty(n, **f64)
         self.t = torch.empty(n, **f64)
@@ -369,15 +370,18 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit):
                 _apply_op(op, V[j], ws.z, ws)
             spmv(ws.z, ws.w)
             k = j + 1
-            # CGS2: two classical Gram-Schmidt passes (h = h1 + h2), then ||w||
-            with _timed("gemv_t"):
-                chk(lib.rs_gemv_t(_p(V), n, k, n, _p(ws.w), _p(h1), _p(ws.flags), _p(work), st), "gemv_t")
-            with _timed("gemv_n"):
-                chk(lib.rs_gemv_n_update(_p(V), n, k, n, _p(h1), _p(ws.w), None, _p(work), st), "gemv_n")
-            with _timed("gemv_t"):
-                chk(lib.rs_gemv_t(_p(V), n, k, n, _p(ws.w), _p(h2), None, _p(work), st), "gemv_t")
-            with _timed("gemv_n"):
-                chk(lib.rs_gemv_n_update(_p(V), n, k, n, _p(h2), _p(ws.w), _p(nrm2_slot), _p(work), st), "gemv_n")
+            # CGS2 (krylov.py:217-220 re-designed): h1 = V^T w ; w -= V h1 and h2 = V^T w in ONE
+            # pass over V ; w -= V h2 with ||w||^2 ; h = h1 + h2
+            ldv = ws.ldv
+            with _timed("cgs_dots"):
+                chk(lib.rs_cgs_pass(_p(V), ldv, k, n, None, _p(ws.w), _p(h1), None, _p(ws.flags), _p(work), st),
+                    "cgs_pass")
+            with _timed("cgs_update_dots"):
+                chk(lib.rs_cgs_pass(_p(V), ldv, k, n, _p(h1), _p(ws.w), _p(h2), None, None, _p(work), st),
+                    "cgs_pass")
+            with _timed("cgs_update_norm"):
+                chk(lib.rs_cgs_pass(_p(V), ldv, k, n, _p(h2), _p(ws.w), None, _p(nrm2_slot), None, _p(work), st),
+                    "cgs_pass")
             with _timed("scale"):
                 chk(lib.rs_scale_by_norm(n, _p(ws.w), _p(nrm2_slot), _p(V[j + 1]), st), "scale")
             ws.pinned.copy_(scal)  # synchronises the stream: one D2H per Arnoldi step
@@ -412,7 +416,7 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit):
         for i in range(j, -1, -1):
             y[i] = (g[i] - h[i, i + 1:j + 1] @ y[i + 1:j + 1]) / h[i, i]
         ws.y[: j + 1].copy_(torch.from_numpy(y))
-        chk(lib.rs_gemv_n(_p(V), n, j + 1, n, _p(ws.y), _p(ws.t), st), "gemv_n")
+        chk(lib.rs_gemv_n(_p(V), ws.ldv, j + 1, n, _p(ws.y), _p(ws.t), st), "gemv_n")
         _apply_op(op, ws.t, ws.z, ws)
         chk(lib.rs_axpy1(n, _p(ws.z), _p(x), st), "axpy")
         # true residual (krylov.py:245-249)
