@@ -5,7 +5,12 @@
 // Reductions are deterministic: a fixed grid of kRedBlocks persistent blocks
 // each owns one contiguous row range, writes one partial per output, and a
 // single-block second pass sums the partials in block order.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <cstring>
+#include <mutex>
 
 #include "rs_internal.cuh"
 
@@ -229,18 +234,53 @@ __global__ void k_cast_up(int64_t n, const float* __restrict__ in, double* __res
 //   DOTS:   h_out[i] += sum_r V_i[r] w[r]           (warp per basis vector)
 //   NORM:   nrm2 += w[r]^2
 // so "update + re-orthogonalisation dots" of CGS2 read V once instead of twice.
-constexpr int kCgsThreads = 256;
+constexpr int kCgsThreads = 512;
 constexpr int kCgsWarps = kCgsThreads / 32;
 constexpr int kCgsStages = 3;
 constexpr int kCgsMaxK = 64;
-constexpr int kCgsMaxQ = kCgsMaxK / kCgsWarps;
+constexpr int kCgsMaxQ = kCgsMaxK / kCgsWarps;  // basis vectors per warp in the dots phase
+constexpr int kCgsMaxT = 8;                     // rows per lane in the dots phase (ch <= 256)
 constexpr int kCgsStageBytes = 64 * 1024;
 constexpr int kCgsBlocks = 148;
 
+// k <= kCgsTmapMinK: one 1-D bulk copy per basis row (chunks of >= 7 KB each);
+// larger k: one 2-D tensor-map copy of the k x ch tile per chunk (ch <= 256,
+// the TMA box limit), because a bulk copy costs ~150 cycles of TMA issue time
+// regardless of size (measured: k = 61 with 1 KB row copies reached 2.1 TB/s).
+constexpr int kCgsTmapMinK = 8;
+
 static int cgs_chunk_rows(int k) {
   int ch = kCgsStageBytes / (8 * (k + 1));
+  if (k > kCgsTmapMinK) return std::max(32, std::min(256, ch) & ~31);
   ch = std::max(128, std::min(4096, ch)) & ~127;
   return ch;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D map over the basis: dim0 = rows of the vectors (contiguous), dim1 = basis index
+static bool encode_basis_map(CUtensorMap* map, const double* V, int64_t ldv, int k, int64_t n, int ch) {
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)k};
+  cuuint64_t strides[1] = {(cuuint64_t)ldv * sizeof(double)};
+  cuuint32_t box[2] = {(cuuint32_t)ch, (cuuint32_t)k};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(V), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
 }
 
 static size_t cgs_smem_bytes(int k, int ch) {
@@ -249,9 +289,11 @@ static size_t cgs_smem_bytes(int k, int ch) {
 
 template <bool UPDATE, bool DOTS, bool NORM>
 __global__ void __launch_bounds__(kCgsThreads, 1)
-    k_cgs(const double* __restrict__ V, int64_t ldv, int k, int64_t n, int ch, int64_t rows_per_blk,
-          const double* __restrict__ h_in, double* __restrict__ w, double* __restrict__ partial, int* nonfinite) {
+    k_cgs(const __grid_constant__ CUtensorMap tmap, int use_tmap, const double* __restrict__ V, int64_t ldv, int k,
+          int64_t n, int ch, int64_t rows_per_blk, const double* __restrict__ h_in, double* __restrict__ w,
+          double* __restrict__ partial, int* nonfinite) {
   extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ double red[kCgsThreads];  // update-phase partial sums [split][row]
   const int stage_elems = (k + 1) * ch;
   double* st = reinterpret_cast<double*>(smraw);
   double* hs = st + (size_t)kCgsStages * stage_elems;
@@ -273,12 +315,25 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     const int len = (int)(r1 - c0 < ch ? r1 - c0 : ch);
     const uint32_t bytes = (uint32_t)len * 8u;
     double* dst = st + (size_t)s * stage_elems;
-    mbar_expect_tx(&bar[s], (uint32_t)(k + 1) * bytes);
-    for (int i = 0; i < k; ++i) bulk_g2s(dst + (size_t)i * ch, V + (int64_t)i * ldv + c0, bytes, &bar[s]);
+    if (use_tmap) {
+      // one 2-D tensor copy brings the whole k x ch tile (OOB columns zero-filled)
+      mbar_expect_tx(&bar[s], (uint32_t)k * (uint32_t)ch * 8u + bytes);
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+              "r"(smem_u32(dst)),
+          "l"(reinterpret_cast<uint64_t>(&tmap)), "r"((int)c0), "r"(0), "r"(smem_u32(&bar[s]))
+          : "memory");
+    } else {
+      mbar_expect_tx(&bar[s], (uint32_t)(k + 1) * bytes);
+      for (int i = 0; i < k; ++i) bulk_g2s(dst + (size_t)i * ch, V + (int64_t)i * ldv + c0, bytes, &bar[s]);
+    }
     bulk_g2s(dst + (size_t)k * ch, w + c0, bytes, &bar[s]);
   };
   if (tid == 0)
     for (int c = 0; c < kCgsStages && c < nchunks; ++c) issue(c);
+  // update-phase mapping: each row's basis sum is split over `nsplit` thread groups
+  const int nsplit = ch >= kCgsThreads ? 1 : kCgsThreads / ch;
+  const int urow = tid % ch, usplit = tid / ch;
   double acc[kCgsMaxQ];
 #pragma unroll
   for (int q = 0; q < kCgsMaxQ; ++q) acc[q] = 0.0;
@@ -291,42 +346,85 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     const int len = (int)(r1 - c0 < ch ? r1 - c0 : ch);
     const double* Vs = st + (size_t)s * stage_elems;
     double* ws = st + (size_t)s * stage_elems + (size_t)k * ch;
-    if (UPDATE || NORM || nonfinite) {
+    if (UPDATE) {
+      if (nsplit > 1) {
+        if (usplit < nsplit && urow < len) {
+          double s0 = 0.0, s1 = 0.0;
+          int i = usplit;
+          for (; i + nsplit < k; i += 2 * nsplit) {
+            s0 += hs[i] * Vs[(size_t)i * ch + urow];
+            s1 += hs[i + nsplit] * Vs[(size_t)(i + nsplit) * ch + urow];
+          }
+          if (i < k) s0 += hs[i] * Vs[(size_t)i * ch + urow];
+          red[usplit * ch + urow] = s0 + s1;
+        }
+        __syncthreads();
+      }
+      for (int r = tid; r < len; r += kCgsThreads) {
+        double sum;
+        if (nsplit > 1) {
+          sum = red[r];
+          for (int v = 1; v < nsplit; ++v) sum += red[v * ch + r];
+        } else {
+          double s0 = 0.0, s1 = 0.0;
+          int i = 0;
+          for (; i + 1 < k; i += 2) {
+            s0 += hs[i] * Vs[(size_t)i * ch + r];
+            s1 += hs[i + 1] * Vs[(size_t)(i + 1) * ch + r];
+          }
+          if (i < k) s0 += hs[i] * Vs[(size_t)i * ch + r];
+          sum = s0 + s1;
+        }
+        double wv = ws[r];
+        if (nonfinite) bad |= !isfinite(wv);
+        wv = wv - sum;
+        w[c0 + r] = wv;
+        ws[r] = wv;
+        if (NORM) nrm += wv * wv;
+      }
+      __syncthreads();
+    } else if (NORM || nonfinite) {
       for (int r = tid; r < len; r += kCgsThreads) {
         double wv = ws[r];
         if (nonfinite) bad |= !isfinite(wv);
-        if (UPDATE) {
-          double sum = 0.0;
-          int i = 0;
-          for (; i + 4 <= k; i += 4) {
-            sum += hs[i] * Vs[(size_t)i * ch + r];
-            sum += hs[i + 1] * Vs[(size_t)(i + 1) * ch + r];
-            sum += hs[i + 2] * Vs[(size_t)(i + 2) * ch + r];
-            sum += hs[i + 3] * Vs[(size_t)(i + 3) * ch + r];
-          }
-          for (; i < k; ++i) sum += hs[i] * Vs[(size_t)i * ch + r];
-          wv = wv - sum;
-          w[c0 + r] = wv;
-          ws[r] = wv;
-        }
         if (NORM) nrm += wv * wv;
       }
     }
-    if (UPDATE && DOTS) __syncthreads();
     if (DOTS) {
+      if (ch <= 32 * kCgsMaxT) {
+        // lane owns rows lane + 32 t; w cached in registers; kCgsMaxQ independent chains
+        double wr[kCgsMaxT];
 #pragma unroll
-      for (int q = 0; q < kCgsMaxQ; ++q) {
-        const int i = warp + q * kCgsWarps;
-        if (i < k) {
-          const double* vi = Vs + (size_t)i * ch;
-          double a0 = 0.0, a1 = 0.0;
-          int r = lane;
-          for (; r + 32 < len; r += 64) {
-            a0 += vi[r] * ws[r];
-            a1 += vi[r + 32] * ws[r + 32];
+        for (int t = 0; t < kCgsMaxT; ++t) {
+          const int r = lane + 32 * t;
+          wr[t] = r < len ? ws[r] : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < kCgsMaxT; ++t) {
+          const int r = lane + 32 * t;
+          if (r < ch) {
+#pragma unroll
+            for (int q = 0; q < kCgsMaxQ; ++q) {
+              const int i = warp + q * kCgsWarps;
+              if (i < k) acc[q] += Vs[(size_t)i * ch + r] * wr[t];
+            }
           }
-          if (r < len) a0 += vi[r] * ws[r];
-          acc[q] += a0 + a1;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < kCgsMaxQ; ++q) {
+          const int i = warp + q * kCgsWarps;
+          if (i < k) {
+            const double* vi = Vs + (size_t)i * ch;
+            double a0 = 0.0, a1 = 0.0;
+            int r = lane;
+            for (; r + 32 < len; r += 64) {
+              a0 += vi[r] * ws[r];
+              a1 += vi[r + 32] * ws[r + 32];
+            }
+            if (r < len) a0 += vi[r] * ws[r];
+            acc[q] += a0 + a1;
+          }
         }
       }
     }
@@ -345,8 +443,8 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     }
   }
   if (NORM) {
-    __shared__ double red[kCgsWarps];
     nrm = warp_sum(nrm);
+    __syncthreads();
     if (lane == 0) red[warp] = nrm;
     __syncthreads();
     if (tid == 0) {
@@ -440,13 +538,24 @@ int rs_cgs_pass(const double* V, int64_t ldv, int k, int64_t n, const double* h_
   }
   const int ch = cgs_chunk_rows(k);
   const size_t smem = cgs_smem_bytes(k, ch);
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof(tmap));
+  int use_tmap = 0;
+  if (k > kCgsTmapMinK) {
+    if (!encode_basis_map(&tmap, V, ldv, k, n, ch)) {
+      set_error(RS_ERR_CUDA, "cuTensorMapEncodeTiled failed for the Arnoldi basis");
+      return RS_ERR_CUDA;
+    }
+    use_tmap = 1;
+  }
   int64_t rows = ((n + kCgsBlocks - 1) / kCgsBlocks + ch - 1) / ch * ch;
   int nblk = (int)std::max<int64_t>(1, (n + rows - 1) / std::max<int64_t>(rows, 1));
   const bool U = h_in != nullptr, D = h_out != nullptr, Nm = nrm2 != nullptr;
 #define RS_CGS_LAUNCH(u, d, nm)                                                                          \
   do {                                                                                                   \
     cudaFuncSetAttribute(k_cgs<u, d, nm>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
-    k_cgs<u, d, nm><<<nblk, kCgsThreads, smem, st>>>(V, ldv, k, n, ch, rows, h_in, w, work, nonfinite); \
+    k_cgs<u, d, nm><<<nblk, kCgsThreads, smem, st>>>(tmap, use_tmap, V, ldv, k, n, ch, rows, h_in, w, work, \
+                                                     nonfinite);                                          \
     RS_COUNT_LAUNCH();                                                                                   \
   } while (0)
   if (U && D && Nm) RS_CGS_LAUNCH(true, true, true);

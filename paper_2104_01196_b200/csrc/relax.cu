@@ -17,6 +17,7 @@
 //   k_compact    t = b - U x - (1 - 1/w) d x, scaled by D^-1 (compact pass 0).
 //   k_gs_level   one dependency level of the in-place Gauss-Seidel sweep.
 #include <algorithm>
+#include <cstdlib>
 
 #include "rs_internal.cuh"
 
@@ -43,6 +44,11 @@ static SellView<T> view(const Sell<T>& s, bool scaled) {
 }
 
 // acc += sum_k v_k * x[c_k] over one row of a SELL triangle, ascending k.
+// Entries are fetched in batches of kBatch (columns and values first, then the
+// gathers, then the ordered accumulation) so every thread keeps several
+// independent loads in flight; the summation order is unchanged.
+constexpr int kBatch = 4;
+
 template <typename T>
 __device__ __forceinline__ T row_accum(const SellView<T>& m, int64_t i, const T* __restrict__ x, T acc) {
   if (m.empty) return acc;
@@ -52,10 +58,20 @@ __device__ __forceinline__ T row_accum(const SellView<T>& m, int64_t i, const T*
   const int w = (int)((m.sp[s + 1] - p0) >> 5);
   const int32_t* cp = m.col + p0 + lane;
   const T* vp = m.val + p0 + lane;
-  for (int j = 0; j < w; ++j) {
-    int32_t c = __ldcs(cp + 32 * j);
-    T v = __ldcs(vp + 32 * j);
-    if (c >= 0) acc = add_rn<T>(acc, mul_rn<T>(v, x[c]));
+  for (int j0 = 0; j0 < w; j0 += kBatch) {
+    int32_t c[kBatch];
+    T v[kBatch], xv[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const bool ok = j0 + u < w;
+      c[u] = ok ? __ldcs(cp + 32 * (j0 + u)) : -1;
+      v[u] = ok ? __ldcs(vp + 32 * (j0 + u)) : (T)0;
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) xv[u] = c[u] >= 0 ? x[c[u]] : (T)0;
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u)
+      if (c[u] >= 0) acc = add_rn<T>(acc, mul_rn<T>(v[u], xv[u]));
   }
   return acc;
 }
@@ -176,10 +192,24 @@ __global__ void __launch_bounds__(256) k_inner0(int64_t n, SellView<T> Tm, const
     const int lane = (int)(i & 31);
     const int64_t p0 = Tm.sp[s];
     const int wd = (int)((Tm.sp[s + 1] - p0) >> 5);
-    for (int j = 0; j < wd; ++j) {
-      const int32_t c = __ldcs(Tm.col + p0 + 32 * j + lane);
-      const T v = __ldcs(Tm.val + p0 + 32 * j + lane);
-      if (c >= 0) t = add_rn<T>(t, mul_rn<T>(v, div_rn<T>((T)r[c], d[c])));
+    for (int j0 = 0; j0 < wd; j0 += kBatch) {
+      int32_t c[kBatch];
+      T v[kBatch], dk[kBatch];
+      R rk[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const bool ok = j0 + u < wd;
+        c[u] = ok ? __ldcs(Tm.col + p0 + 32 * (j0 + u) + lane) : -1;
+        v[u] = ok ? __ldcs(Tm.val + p0 + 32 * (j0 + u) + lane) : (T)0;
+      }
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        rk[u] = c[u] >= 0 ? r[c[u]] : (R)0;
+        dk[u] = c[u] >= 0 ? d[c[u]] : (T)1;
+      }
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u)
+        if (c[u] >= 0) t = add_rn<T>(t, mul_rn<T>(v[u], div_rn<T>((T)rk[u], dk[u])));
     }
   }
   T g = sub_rn<T>(rdi, mul_rn<T>(w, t));
@@ -603,7 +633,9 @@ static int precond_gs2_single(rs_matrix* m, const rs_relax_cfg& cfg, const R* r,
 }
 
 static bool single_half_sweep(int kind, const rs_relax_cfg& cfg) {
-  return kind == RS_PC_GS2 && cfg.n_t * cfg.n_k == 1 && cfg.direction != RS_SYMMETRIC;
+  // RS_PRECOND_UNFUSED=1 (tuning / A-B measurements only) forces the generic two-pass path
+  static const bool unfused = getenv("RS_PRECOND_UNFUSED") && atoi(getenv("RS_PRECOND_UNFUSED")) != 0;
+  return !unfused && kind == RS_PC_GS2 && cfg.n_t * cfg.n_k == 1 && cfg.direction != RS_SYMMETRIC;
 }
 
 // Preconditioner.apply (krylov.py:110-137) body in the working dtype, from z = 0.
@@ -729,9 +761,14 @@ int rs_precond_apply(rs_matrix_t m, int kind, const rs_relax_cfg* cfg, const dou
   }
   int e;
   if ((e = ensure_scratch(m))) return e;
+  // Fused zero-start path: always for float32 (the r cast and z upcast fold into
+  // the sweep); for float64 only when n_j == 0 -- with n_j >= 1 the per-neighbour
+  // fp64 divisions r_k/d_k make the single pass latency-bound (ncu: 40% DRAM,
+  // 0.305 ms) and the two-pass rd = r/d ; z = w(rd - w D^-1L rd) is faster
+  // (0.239 ms at 256^3) despite its 2V extra bytes.
   if (single_half_sweep(kind, *cfg)) {
-    if (m->dtype == RS_F64) return precond_gs2_single<double, double, double>(m, *cfg, r, z, nullptr, st);
-    return precond_gs2_single<float, double, double>(m, *cfg, r, z, (long long*)overflow_flag, st);
+    if (m->dtype == RS_F32) return precond_gs2_single<float, double, double>(m, *cfg, r, z, (long long*)overflow_flag, st);
+    if (cfg->n_j == 0) return precond_gs2_single<double, double, double>(m, *cfg, r, z, nullptr, st);
   }
   if (m->dtype == RS_F64) return precond_body<double>(m, kind, *cfg, r, z, st);
   // single_inside_double (krylov.py:116-118, 135-136): cast r, relax in float32, upcast z
