@@ -369,6 +369,7 @@ def main():
     p.add_argument("--nx", type=int, default=0)
     p.add_argument("--restart", type=int, default=60)
     p.add_argument("--no-tts", action="store_true")
+    p.add_argument("--tts", action="store_true", help="also time a full solve at N > 1 (off by default)")
     p.add_argument("--no-sweeps", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-iters", type=int, default=8)

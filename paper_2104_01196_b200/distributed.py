@@ -1,0 +1,421 @@
+"""Multi-GPU hybrid block-Jacobi GS2 + GMRES(m): one process (rank) per GPU.
+
+The matrix rows are split into contiguous blocks by ``BlockPartition.regular``
+(relax.py:89-92) -- for the natural-ordered 3D stencils these are z-slabs.
+Rank p owns rows [lo, hi) as a split handle whose strict triangles are the
+diagonal block A_pp and whose E_lo / E_hi hold the couplings to the rows
+below / above (rs_mat_create_stencil / rs_mat_create_csr with row0).
+
+Collectives:
+* halo exchange of the vector entries E_lo / E_hi read (one plane per
+  neighbour for a 7-point slab) before every residual-forming SpMV and every
+  hybrid round after the first -- NCCL grouped send/recv through
+  torch.distributed;
+* one sum-allreduce per Gram-Schmidt reduction (h1, h2, ||w||^2 + status).
+The zero-start hybrid preconditioner with n_t = 1 needs no exchange at all:
+bhat = r_p, then the local GS2 sweeps of hybrid_relax (relax.py:259-269).
+
+``Comm`` abstracts the collectives: ``TorchComm`` (NCCL or gloo process
+group) for real multi-process runs, ``ThreadComm`` to emulate P ranks as
+threads of one process (tests on one GPU; each rank its own CUDA stream).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from . import _native as N
+from .krylov import ConvergenceHistory, _gmres_device, _p
+from .relax import BlockPartition, RelaxConfig
+from .sparse import CsrMatrix, DeviceMatrix, _torch
+
+
+# ---------------------------------------------------------------- communicators
+class Comm:
+    rank: int = 0
+    size: int = 1
+
+    def allreduce_sum_(self, t):  # in place
+        raise NotImplementedError
+
+    def allreduce_max(self, v: float) -> float:
+        raise NotImplementedError
+
+    def allgather_obj(self, obj) -> list:
+        raise NotImplementedError
+
+    def exchange(self, sends, recvs):
+        """sends: [(peer, tensor)], recvs: [(peer, tensor)] -- at most one message per ordered pair."""
+        raise NotImplementedError
+
+    def barrier(self):
+        raise NotImplementedError
+
+
+class TorchComm(Comm):
+    """torch.distributed process group (NCCL on GPUs; gloo works for CPU tensors)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+
+    def allreduce_sum_(self, t):
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+
+    def allreduce_max(self, v: float) -> float:
+        torch = _torch()
+        dev = torch.device("cuda", torch.cuda.current_device()) if self.dist.get_backend(self.group) == "nccl" \
+            else torch.device("cpu")
+        t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+    def allgather_obj(self, obj) -> list:
+        out = [None] * self.size
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+    def exchange(self, sends, recvs):
+        if not sends and not recvs:
+            return
+        ops = [self.dist.P2POp(self.dist.isend, t, peer, group=self.group) for peer, t in sends]
+        ops += [self.dist.P2POp(self.dist.irecv, t, peer, group=self.group) for peer, t in recvs]
+        for w in self.dist.batch_isend_irecv(ops):
+            w.wait()
+
+    def barrier(self):
+        self.dist.barrier(group=self.group)
+
+
+class _ThreadShared:
+    def __init__(self, size):
+        self.size = size
+        self.bar = threading.Barrier(size)
+        self.slots = [None] * size
+        self.mail = {}
+        self.lock = threading.Lock()
+
+
+class ThreadComm(Comm):
+    """P ranks as P threads of one process (tests).  Reductions sum in rank order."""
+
+    def __init__(self, shared: _ThreadShared, rank: int):
+        self.sh = shared
+        self.rank = rank
+        self.size = shared.size
+
+    @classmethod
+    def group(cls, size: int):
+        sh = _ThreadShared(size)
+        return [cls(sh, r) for r in range(size)]
+
+    def _sync_stream(self):
+        torch = _torch()
+        if torch.cuda.is_available():
+            torch.cuda.current_stream().synchronize()
+
+    def allreduce_sum_(self, t):
+        self._sync_stream()
+        self.sh.slots[self.rank] = t.clone()
+        self.sh.bar.wait()
+        acc = self.sh.slots[0].clone()
+        for r in range(1, self.size):
+            acc += self.sh.slots[r].to(acc.device)
+        self.sh.bar.wait()
+        t.copy_(acc)
+
+    def allreduce_max(self, v: float) -> float:
+        self.sh.slots[self.rank] = float(v)
+        self.sh.bar.wait()
+        m = max(self.sh.slots)
+        self.sh.bar.wait()
+        return m
+
+    def allgather_obj(self, obj) -> list:
+        self.sh.slots[self.rank] = obj
+        self.sh.bar.wait()
+        out = list(self.sh.slots)
+        self.sh.bar.wait()
+        return out
+
+    def exchange(self, sends, recvs):
+        self._sync_stream()
+        with self.sh.lock:
+            for peer, t in sends:
+                self.sh.mail[(self.rank, peer)] = t.clone()
+        self.sh.bar.wait()
+        for peer, t in recvs:
+            t.copy_(self.sh.mail[(peer, self.rank)])
+        self._sync_stream()
+        self.sh.bar.wait()
+        with self.sh.lock:
+            for peer, _ in sends:
+                self.sh.mail.pop((self.rank, peer), None)
+
+    def barrier(self):
+        self._sync_stream()
+        self.sh.bar.wait()
+
+
+# ---------------------------------------------------------------- layout and halo plan
+@dataclass(frozen=True)
+class HaloPlan:
+    """Contiguous segments to send / receive for the E_lo / E_hi couplings of every rank.
+
+    send: [(peer, lo, hi)] -- my rows [lo, hi) (local offsets) go to peer
+    recv: [(peer, buf, lo, hi)] -- buf 'lo' / 'hi' halo buffer slice [lo, hi) comes from peer
+    """
+
+    send: tuple
+    recv: tuple
+
+    @staticmethod
+    def build(rank: int, blocks: list) -> "HaloPlan":
+        """blocks[q] = (lo, hi, halo_lo, halo_hi) of every rank q (global rows)."""
+        lo, hi, _, _ = blocks[rank]
+        send, recv = [], []
+        for q, (qlo, qhi, qhl, qhh) in enumerate(blocks):
+            if q == rank:
+                continue
+            # what q reads from my rows: its low halo [qlo - qhl, qlo) and high halo [qhi, qhi + qhh)
+            for a, b in ((qlo - qhl, qlo), (qhi, qhi + qhh)):
+                s, e = max(a, lo), min(b, hi)
+                if s < e:
+                    send.append((q, s - lo, e - lo))
+        mlo, mhi, mhl, mhh = blocks[rank]
+        for q, (qlo, qhi, _, _) in enumerate(blocks):
+            if q == rank:
+                continue
+            s, e = max(mlo - mhl, qlo), min(mlo, qhi)
+            if s < e:
+                recv.append((q, "lo", s - (mlo - mhl), e - (mlo - mhl)))
+            s, e = max(mhi, qlo), min(mhi + mhh, qhi)
+            if s < e:
+                recv.append((q, "hi", s - mhi, e - mhi))
+        return HaloPlan(tuple(send), tuple(recv))
+
+
+class DistMatrix:
+    """This rank's row block of a distributed matrix plus its halo plan and buffers."""
+
+    def __init__(self, dm: DeviceMatrix, comm: Comm, n_global: int, offsets: np.ndarray):
+        self.dm = dm
+        self.comm = comm
+        self.n_global = n_global
+        self.offsets = offsets
+        self.lo, self.hi = dm.row0, dm.row0 + dm.nrows
+        blocks = comm.allgather_obj((self.lo, self.hi, dm.halo_lo, dm.halo_hi))
+        self.plan = HaloPlan.build(comm.rank, blocks)
+        torch = _torch()
+        f = dict(dtype=dm.torch_dtype, device=dm.torch_device)
+        self.xlo = torch.empty(max(dm.halo_lo, 1), **f)
+        self.xhi = torch.empty(max(dm.halo_hi, 1), **f)
+        self._lib = N.load()
+
+    @property
+    def nrows(self):
+        return self.dm.nrows
+
+    @classmethod
+    def stencil(cls, comm: Comm, kind: str, nx: int, ny=None, nz=None, params=None, dtype=np.float64):
+        ny = nx if ny is None else ny
+        nz = nx if nz is None else nz
+        n = nx * ny * (1 if kind == "laplace2d" else nz)
+        offs = BlockPartition.regular(n, comm.size).offsets
+        lo, hi = int(offs[comm.rank]), int(offs[comm.rank + 1])
+        torch = _torch()
+        dm = DeviceMatrix.stencil(kind, nx, ny, nz, params=params, row0=lo, nrows=hi - lo, dtype=dtype,
+                                  device=torch.cuda.current_device())
+        return cls(dm, comm, n, offs)
+
+    @classmethod
+    def from_csr(cls, comm: Comm, a: CsrMatrix):
+        offs = BlockPartition.regular(a.nrows, comm.size).offsets
+        lo, hi = int(offs[comm.rank]), int(offs[comm.rank + 1])
+        torch = _torch()
+        dm = DeviceMatrix.from_csr(a, device=torch.cuda.current_device(), row0=lo, nrows=hi - lo)
+        return cls(dm, comm, a.nrows, offs)
+
+    def exchange(self, x):
+        """Fill xlo / xhi with the neighbour entries of the local vector x (one grouped send/recv)."""
+        sends = [(peer, x[s:e]) for peer, s, e in self.plan.send]
+        recvs = [(peer, (self.xlo if which == "lo" else self.xhi)[s:e]) for peer, which, s, e in self.plan.recv]
+        self.comm.exchange(sends, recvs)
+
+    def spmv(self, x, y):
+        """y = (A x) for the local rows: halo exchange, then E_lo | L | D | U | E_hi row sums."""
+        self.exchange(x)
+        st = C.c_void_p(_torch().cuda.current_stream().cuda_stream)
+        xlo = _p(self.xlo) if self.dm.halo_lo else None
+        xhi = _p(self.xhi) if self.dm.halo_hi else None
+        N.check(self._lib.rs_spmv(self.dm.handle, _p(x), xlo, xhi, _p(y), st), "spmv")
+
+
+class HybridPreconditioner:
+    """Zero-start hybrid block-Jacobi relaxation (hybrid_relax, relax.py:231-269) as a preconditioner.
+
+    z = 0; per outer round t: bhat_p = (r_p - (A z)_p) + A_pp z_p (halo exchange;
+    round 1 from z = 0 is bhat = r exactly, no exchange); then cfg.n_k local GS2
+    (local="gs2") or GS (local="gs") sweeps on the diagonal block.  With P = 1
+    this is the plain gs2 / sgs2 Preconditioner.
+    """
+
+    def __init__(self, A: DistMatrix, cfg: RelaxConfig, local: str = "gs2", precision: str = "same"):
+        if local not in ("gs", "gs2"):
+            raise ValueError(f"local must be 'gs' or 'gs2', got {local!r}")
+        self.A = A
+        self.cfg = cfg
+        self.local = local
+        self.precision = precision
+        self.dm = A.dm if precision == "same" else A.dm.single()
+        self._local_cfg = N.RelaxCfg.of(replace(cfg, n_t=1))
+        self._lib = N.load()
+        torch = _torch()
+        self._bhat = torch.empty(A.nrows, dtype=torch.float64, device=A.dm.torch_device) if cfg.n_t > 1 else None
+
+    def apply_into(self, r, z, flag=None):
+        lib = self._lib
+        st = C.c_void_p(_torch().cuda.current_stream().cuda_stream)
+        cfg = self.cfg
+        kind = N.PC_KINDS["gs2" if self.local == "gs2" else "gs_seq"]
+        if cfg.n_t == 1:
+            c = self._local_cfg if self.local == "gs2" else N.RelaxCfg.of(replace(cfg, n_t=1))
+            fp = _p(flag) if flag is not None else None
+            N.check(lib.rs_precond_apply(self.dm.handle, kind, C.byref(c), _p(r), _p(z), fp, st), "precond")
+            return
+        if self.precision != "same":
+            raise ValueError("hybrid preconditioner with n_t > 1 supports precision='same' only")
+        # round 1 from zero: bhat = r
+        c = self._local_cfg
+        fp = _p(flag) if flag is not None else None
+        N.check(lib.rs_precond_apply(self.dm.handle, kind, C.byref(c), _p(r), _p(z), fp, st), "precond")
+        A = self.A
+        for _ in range(cfg.n_t - 1):
+            A.exchange(z)
+            xlo = _p(A.xlo) if A.dm.halo_lo else None
+            xhi = _p(A.xhi) if A.dm.halo_hi else None
+            N.check(lib.rs_hybrid_bhat(A.dm.handle, _p(r), _p(z), xlo, xhi, _p(self._bhat), st), "bhat")
+            if self.local == "gs2":
+                N.check(lib.rs_gs2_apply(A.dm.handle, _p(self._bhat), _p(z), C.byref(c), st), "gs2")
+            else:
+                for _ in range(cfg.n_k):
+                    N.check(lib.rs_gs_sweep(A.dm.handle, _p(self._bhat), _p(z), N.DIRECTIONS[cfg.direction],
+                                            float(cfg.omega), st), "gs")
+
+
+def gmres(A: DistMatrix, b_local, m: HybridPreconditioner | None = None, restart: int = 60, tol: float = 1e-9,
+          maxit: int = 10000, x0_local=None):
+    """Distributed GMRES(m): every rank calls it with its local rows; returns (x_local, history)."""
+    if not tol > 0:
+        raise ValueError(f"tol must be positive, got {tol}")
+    if restart < 1:
+        raise ValueError(f"restart must be >= 1, got {restart}")
+    torch = _torch()
+    dm = A.dm
+    dev = dm.torch_device
+    b = b_local.to(dev, torch.float64) if b_local.device != dev else b_local
+    x = torch.zeros(dm.nrows, dtype=torch.float64, device=dev) if x0_local is None else x0_local.clone()
+    x, hist, conv = _gmres_device(dm, b, x, m, restart, tol, maxit, spmv_fn=A.spmv, reduce_fn=A.comm.allreduce_sum_)
+    return x, ConvergenceHistory(np.array(hist), conv)
+
+
+def local_rhs(A: DistMatrix, seed: int = 0):
+    """random_rhs(n_global, seed)[lo:hi] generated on this rank's GPU (LCG jump-ahead to row lo)."""
+    torch = _torch()
+    out = torch.empty(A.nrows, dtype=torch.float64, device=A.dm.torch_device)
+    N.check(N.load().rs_lcg_fill(int(seed) & ((1 << 64) - 1), A.lo, A.nrows, _p(out),
+                                 C.c_void_p(torch.cuda.current_stream().cuda_stream)), "lcg")
+    return out
+
+
+# ---------------------------------------------------------------- bench entry (torchrun, one rank per GPU)
+def bench_rank(args, metric, Model, laplace3d_nnz, ClockSampler, peaks):
+    """Config C5: laplace3d 512^3 in z-slabs, hybrid GS2(1,1,1) preconditioner, one GMRES(60) cycle per step."""
+    import json
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    comm = TorchComm()
+    rank, world = comm.rank, comm.size
+    local = torch.cuda.current_device()
+    lib = N.load()
+    nx = args.nx or 512
+    m = args.restart
+    A = DistMatrix.stencil(comm, "laplace3d", nx)
+    b = local_rhs(A, 0)
+    pc = HybridPreconditioner(A, RelaxConfig(1, 1, 1))
+    n, nl, nu = laplace3d_nnz(nx, nx, nx)
+    mod = Model(n, nl, nu)
+    cycle_bytes = mod.cycle(m, 1)
+
+    def step():
+        gmres(A, b, pc, restart=m, tol=1e-300, maxit=m)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    comm.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = lib.rs_launch_count()
+    with ClockSampler(local) as clk:
+        comm.barrier()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        comm.barrier()
+    launches = lib.rs_launch_count() - l0
+    ms = comm.allreduce_max(e0.elapsed_time(e1) / args.steps)
+    value = cycle_bytes / (ms * 1e-3) / 1e9
+    # e2e: host b in, host x out on every rank
+    b_host = b.cpu().pin_memory()
+    comm.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        x, _ = gmres(A, b_host.to(A.dm.torch_device, non_blocking=True), pc, restart=m, tol=1e-300, maxit=m)
+        x.cpu()
+    e2e_ms = comm.allreduce_max((time.perf_counter() - t0) * 1e3 / args.steps)
+    tts = None
+    if getattr(args, "tts", False):
+        comm.barrier()
+        t0 = time.perf_counter()
+        _, h = gmres(A, b, pc, restart=m, tol=1e-9)
+        torch.cuda.synchronize()
+        secs = comm.allreduce_max(time.perf_counter() - t0)
+        tts = {"seconds": round(secs, 3), "iterations": h.iterations, "converged": h.converged,
+               "final_rel_res": h.final_rel_res, "preconditioner": f"hybrid gs2(1,1,1), {world} z-slabs"}
+    if rank == 0:
+        hbm, kind = peaks()
+        line = {
+            "metric": metric, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C5: laplace3d {nx}^3 ({n} rows) in {world} z-slabs, one GMRES({m}) cycle, "
+                                   f"hybrid block-Jacobi GS2(1,1,1) preconditioner, NCCL halo + allreduce",
+                       "bytes_per_step": cycle_bytes, "ms_per_iteration": round(ms / m, 4),
+                       "l2": "inputs larger than L2", "parallelism": f"{world} ranks x 1 GPU (row blocks)"},
+            "roofline": {"bound": "hbm", "kernel": "whole cycle (per GPU)",
+                         "achieved": round(value / world, 1), "peak": hbm, "unit": "GB/s",
+                         "frac": round(value / world / hbm, 3), "traffic": None,
+                         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({kind})"},
+            "cpu_baseline": None,
+            "e2e": {"value": round(cycle_bytes / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+                    "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
+            "gpu_launches": int(launches), "clocks": clk.summary(), "tts": tts,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0

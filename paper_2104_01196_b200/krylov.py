@@ -169,7 +169,7 @@ def _as_operator(m):
     """The reference's plug-in seam (krylov.py:147-154)."""
     if m is None:
         return None
-    if isinstance(m, Preconditioner):
+    if hasattr(m, "apply_into"):  # device fast path (Preconditioner, distributed HybridPreconditioner)
         return m
     if hasattr(m, "apply"):
         return m.apply
@@ -295,8 +295,8 @@ def _apply_op(op, v, z, ws):
     """z = M v for device vectors, through the fast path or the duck-typed seam."""
     if op is None:
         z.copy_(v)
-    elif isinstance(op, Preconditioner):
-        op.apply_into(v, z, ws.flags[1:2] if op.precision == "single_inside_double" else None)
+    elif hasattr(op, "apply_into"):
+        op.apply_into(v, z, ws.flags[1:2] if getattr(op, "precision", "same") == "single_inside_double" else None)
     else:
         torch = _torch()
         try:
@@ -308,7 +308,14 @@ def _apply_op(op, v, z, ws):
         z.copy_(out)
 
 
-def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit):
+def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None, reduce_fn=None):
+    """GMRES(m) on device vectors of the local rows of ``dm``.
+
+    Single GPU by default.  The distributed solver passes ``spmv_fn(src, dst)``
+    (halo exchange + local SpMV) and ``reduce_fn(tensor)`` (in-place sum over
+    ranks); every dot / norm below is a local partial followed by reduce_fn,
+    so all ranks see bitwise identical scalars and take the same decisions.
+    """
     torch = _torch()
     lib = N.load()
     n = dm.nrows
@@ -317,25 +324,33 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit):
     m1 = ws.m1
     scal, work = ws.scal, ws.work
     nrm2_slot = scal[2 * m1:2 * m1 + 1]
+    status = scal[2 * m1:2 * m1 + 3]  # [nrm2, nonfinite, overflow] reduced together
     h1, h2 = scal[0:m1], scal[m1:2 * m1]
     ws.flags.zero_()
     ws.flags[1] = _I64_MAX
+    reduce_ = reduce_fn if reduce_fn is not None else (lambda t: None)
 
     def chk(s, what):
         N.check(s, what)
 
     def spmv(src, dst):
         with _timed("spmv"):
-            chk(lib.rs_spmv(dm.handle, _p(src), None, None, _p(dst), st), "spmv")
+            if spmv_fn is not None:
+                spmv_fn(src, dst)
+            else:
+                chk(lib.rs_spmv(dm.handle, _p(src), None, None, _p(dst), st), "spmv")
 
     def norm_of(vec):
         chk(lib.rs_dot(n, _p(vec), _p(vec), _p(nrm2_slot), _p(work), st), "dot")
+        reduce_(nrm2_slot)
         return math.sqrt(float(nrm2_slot.item()))
 
     def check_overflow():
         i = int(ws.flags[1].item())
         if i != _I64_MAX:
             raise OverflowError(f"entry {i} overflows single precision")
+        if reduce_fn is not None and float(status[2].item()) > 0:
+            raise OverflowError("an entry overflows single precision on another rank")
 
     bnorm = norm_of(b)
     if bnorm == 0.0:
@@ -343,6 +358,7 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit):
     # r = b - A x (krylov.py:193)
     spmv(x, ws.t)
     chk(lib.rs_sub_norm(n, _p(b), _p(ws.t), _p(ws.r), _p(nrm2_slot), _p(work), st), "sub_norm")
+    reduce_(nrm2_slot)
     rnorm = math.sqrt(float(nrm2_slot.item()))
     hist = [rnorm / bnorm]
     if hist[0] <= tol:
@@ -376,20 +392,26 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit):
             with _timed("cgs_dots"):
                 chk(lib.rs_cgs_pass(_p(V), ldv, k, n, None, _p(ws.w), _p(h1), None, _p(ws.flags), _p(work), st),
                     "cgs_pass")
+            reduce_(h1[:k])
             with _timed("cgs_update_dots"):
                 chk(lib.rs_cgs_pass(_p(V), ldv, k, n, _p(h1), _p(ws.w), _p(h2), None, None, _p(work), st),
                     "cgs_pass")
+            reduce_(h2[:k])
             with _timed("cgs_update_norm"):
                 chk(lib.rs_cgs_pass(_p(V), ldv, k, n, _p(h2), _p(ws.w), None, _p(nrm2_slot), None, _p(work), st),
                     "cgs_pass")
+            if reduce_fn is not None:
+                status[1] = (ws.flags[0] & 0xFFFFFFFF).to(torch.float64)
+                status[2] = (ws.flags[1] != _I64_MAX).to(torch.float64)
+                reduce_(status)
             with _timed("scale"):
                 chk(lib.rs_scale_by_norm(n, _p(ws.w), _p(nrm2_slot), _p(V[j + 1]), st), "scale")
             ws.pinned.copy_(scal)  # synchronises the stream: one D2H per Arnoldi step
             ws.pinned_flags.copy_(ws.flags)
             hv = ws.pinned.numpy()
-            if ws.pinned_flags[0].item() & 0xFFFFFFFF:
+            if (ws.pinned_flags[0].item() & 0xFFFFFFFF) or hv[2 * m1 + 1] > 0:
                 raise DivergenceError(f"non-finite values encountered in Arnoldi iteration {total}")
-            if int(ws.pinned_flags[1].item()) != _I64_MAX:
+            if int(ws.pinned_flags[1].item()) != _I64_MAX or hv[2 * m1 + 2] > 0:
                 check_overflow()
             h[:k, j] = hv[0:k] + hv[m1:m1 + k]
             h[j + 1, j] = math.sqrt(hv[2 * m1])
@@ -422,6 +444,7 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit):
         # true residual (krylov.py:245-249)
         spmv(x, ws.t)
         chk(lib.rs_sub_norm(n, _p(b), _p(ws.t), _p(ws.r), _p(nrm2_slot), _p(work), st), "sub_norm")
+        reduce_(nrm2_slot)
         rnorm = math.sqrt(float(nrm2_slot.item()))
         check_overflow()
         true_rel = rnorm / bnorm
