@@ -132,6 +132,12 @@ int rs_inner_jr(rs_matrix_t m, const void *r, void *g, int n_j, int backward, do
 /* gs2_apply (relax.py:208-220) incl. _two_stage_sweep (193-205): x in place. */
 int rs_gs2_apply(rs_matrix_t m, const void *b, void *x, const rs_relax_cfg *cfg, rs_stream_t stream);
 
+/* One GS2 half-sweep out of place, x_out = GS2(x_in) (cfg: n_t = n_k = 1,
+ * forward or backward, n_j >= 1, either form): the wavefront kernel, one
+ * launch, no copy-back.  Bitwise equal to gs2_apply on a copy of x_in. */
+int rs_gs2_sweep(rs_matrix_t m, const void *b, const void *x_in, void *x_out, const rs_relax_cfg *cfg,
+                 rs_stream_t stream);
+
 /* hybrid_relax right-hand side (relax.py:261-264) for one row block:
  * bhat = (b - A_full x) + A_pp x, with x_lo / x_hi the halo values. */
 int rs_hybrid_bhat(rs_matrix_t m, const void *b, const void *x, const void *x_lo, const void *x_hi, void *bhat,

@@ -381,6 +381,8 @@ static int build_split(rs_matrix* m, const Src& src) {
   return status;
 }
 
+void destroy_wave(void* p);
+
 void destroy(rs_matrix* m) {
   if (!m) return;
   int prev = 0;
@@ -395,6 +397,9 @@ void destroy(rs_matrix* m) {
   cudaFree(m->scratch2);
   cudaFree(m->red);
   cudaFree(m->ticket);
+  destroy_wave(m->wave[0]);
+  destroy_wave(m->wave[1]);
+  cudaFree(m->stage);
   cudaSetDevice(prev);
   delete m;
 }

@@ -24,6 +24,26 @@
 namespace rs {
 
 int build_levels(rs_matrix* m, int backward);
+int wave_enabled();
+template <typename T>
+int wave_half_sweep(rs_matrix* m, const T* b, const T* xin, T* xout, int n_j, int backward, int form, double omega,
+                    double gamma, bool x_zero, cudaStream_t st);
+int wave_precond_f32(rs_matrix* m, const double* r, double* z, int n_j, int backward, double omega, double gamma,
+                     long long* overflow, cudaStream_t st);
+template <typename T>
+int wave_max_width(rs_matrix* m, int backward, int* wmax);
+
+// the skewed-pipeline sweep handles any row width
+template <typename T>
+static bool wave_usable(rs_matrix* m, int direction) {
+  for (int bwd = 0; bwd < 2; ++bwd) {
+    if (direction == RS_FORWARD && bwd) continue;
+    if (direction == RS_BACKWARD && !bwd) continue;
+    int w = 0;
+    if (wave_max_width<T>(m, bwd, &w)) return false;
+  }
+  return true;
+}
 
 template <typename T>
 struct SellView {
@@ -437,6 +457,26 @@ static int gs2_apply_t(rs_matrix* m, const T* b, T* x, const rs_relax_cfg& cfg, 
   if ((e = ensure_scratch(m))) return e;
   Ctx<T> c(m, st);
   bool zero = x_is_zero;
+  if (wave_enabled() && cfg.n_j >= 1 && c.n > 0 && wave_usable<T>(m, cfg.direction)) {
+    // one wavefront launch per half-sweep, ping-pong iterates (the wave reads x_in at
+    // neighbours while writing x_out); the result is copied back only if it ends in alt
+    T* alt = (T*)m->scratch + 3 * c.n;
+    T* cur = x;
+    for (int t = 0; t < cfg.n_t; ++t)
+      for (int k = 0; k < cfg.n_k; ++k)
+        for (int half = 0; half < 2; ++half) {
+          const int bwd = half;
+          if (cfg.direction == RS_FORWARD && bwd) continue;
+          if (cfg.direction == RS_BACKWARD && !bwd) continue;
+          T* nxt = cur == x ? alt : x;
+          if ((e = wave_half_sweep<T>(m, b, cur, nxt, cfg.n_j, bwd, cfg.form, cfg.omega, cfg.gamma, zero, st)))
+            return e;
+          cur = nxt;
+          zero = false;
+        }
+    if (cur != x) RS_CUDA(cudaMemcpyAsync(x, cur, sizeof(T) * c.n, cudaMemcpyDeviceToDevice, st));
+    return RS_OK;
+  }
   for (int t = 0; t < cfg.n_t; ++t)
     for (int k = 0; k < cfg.n_k; ++k)
       for (int half = 0; half < 2; ++half) {
@@ -448,6 +488,20 @@ static int gs2_apply_t(rs_matrix* m, const T* b, T* x, const rs_relax_cfg& cfg, 
       }
   RS_CHECK_LAUNCH("gs2_apply");
   return RS_OK;
+}
+
+// out-of-place single GS2 half-sweep / sweep set: x_out = GS2(x_in) (no copy-back)
+template <typename T>
+static int gs2_sweep_oop_t(rs_matrix* m, const T* b, const T* xin, T* xout, const rs_relax_cfg& cfg,
+                           cudaStream_t st) {
+  if (cfg.n_t * cfg.n_k != 1 || cfg.direction == RS_SYMMETRIC || cfg.n_j < 1) {
+    set_error(RS_ERR_ARG, "rs_gs2_sweep: one forward or backward half-sweep with n_j >= 1");
+    return RS_ERR_ARG;
+  }
+  int e;
+  if ((e = ensure_scratch(m))) return e;
+  return wave_half_sweep<T>(m, b, xin, xout, cfg.n_j, cfg.direction == RS_BACKWARD, cfg.form, cfg.omega, cfg.gamma,
+                            false, st);
 }
 
 // jr_sweeps (relax.py:145-154) with ping-pong iterates: x_next = x + w (b - A x)/d
@@ -747,6 +801,19 @@ int rs_gs2_apply(rs_matrix_t m, const void* b, void* x, const rs_relax_cfg* cfg,
                             : gs2_apply_t<double>(m, (const double*)b, (double*)x, *cfg, st, false);
 }
 
+int rs_gs2_sweep(rs_matrix_t m, const void* b, const void* x_in, void* x_out, const rs_relax_cfg* cfg,
+                 rs_stream_t stream) {
+  RS_SET_DEVICE(m);
+  if (bad_cfg(cfg) || x_in == x_out) {
+    set_error(RS_ERR_ARG, "invalid relaxation config or x_in == x_out");
+    return RS_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  return m->dtype == RS_F32 ? gs2_sweep_oop_t<float>(m, (const float*)b, (const float*)x_in, (float*)x_out, *cfg, st)
+                            : gs2_sweep_oop_t<double>(m, (const double*)b, (const double*)x_in, (double*)x_out, *cfg,
+                                                      st);
+}
+
 int rs_precond_apply(rs_matrix_t m, int kind, const rs_relax_cfg* cfg, const double* r, double* z,
                      int64_t* overflow_flag, rs_stream_t stream) {
   RS_SET_DEVICE(m);
@@ -767,6 +834,15 @@ int rs_precond_apply(rs_matrix_t m, int kind, const rs_relax_cfg* cfg, const dou
   // 0.305 ms) and the two-pass rd = r/d ; z = w(rd - w D^-1L rd) is faster
   // (0.239 ms at 256^3) despite its 2V extra bytes.
   if (single_half_sweep(kind, *cfg)) {
+    const bool wave_ok = m->dtype == RS_F32 ? wave_usable<float>(m, cfg->direction) : wave_usable<double>(m, cfg->direction);
+    if (wave_enabled() && cfg->n_j >= 1 && m->nrows > 0 && wave_ok) {
+      // one wavefront launch: z = GS2 half-sweep from zero (fp32: r cast / z upcast fused)
+      if (m->dtype == RS_F32)
+        return wave_precond_f32(m, r, z, cfg->n_j, cfg->direction == RS_BACKWARD, cfg->omega, cfg->gamma,
+                                (long long*)overflow_flag, st);
+      return wave_half_sweep<double>(m, r, nullptr, z, cfg->n_j, cfg->direction == RS_BACKWARD, cfg->form,
+                                     cfg->omega, cfg->gamma, true, st);
+    }
     if (m->dtype == RS_F32) return precond_gs2_single<float, double, double>(m, *cfg, r, z, (long long*)overflow_flag, st);
     if (cfg->n_j == 0) return precond_gs2_single<double, double, double>(m, *cfg, r, z, nullptr, st);
   }

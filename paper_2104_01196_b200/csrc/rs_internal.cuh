@@ -90,6 +90,9 @@ struct rs_matrix {
   double* red = nullptr;    // reduction partials
   unsigned int* ticket = nullptr;
   int64_t red_cap = 0;
+  void* wave[2] = {nullptr, nullptr};  // wavefront sweep plans (forward / backward)
+  void* stage = nullptr;               // wavefront stage vectors (n_j x nrows)
+  size_t stage_bytes = 0;
 };
 
 namespace rs {

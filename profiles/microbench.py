@@ -42,7 +42,7 @@ def timeit(fn, reps=10):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--nx", type=int, default=256)
-    ap.add_argument("--which", default="cgs,precond,spmv")
+    ap.add_argument("--which", default="cgs,precond,spmv,sweep")
     ap.add_argument("--ks", default="1,8,31,61")
     args = ap.parse_args()
     lib = _native.load()
@@ -76,7 +76,7 @@ def main():
                 print(json.dumps({"kernel": name, "k": k, "ms": round(ms, 4), "gbs": round(by / ms / 1e6, 1)}),
                       flush=True)
         del V
-    if "precond" in which or "spmv" in which:
+    if "precond" in which or "spmv" in which or "sweep" in which:
         a = g2.laplace3d(nx, device="cuda")
         ML = 12 * a.nnz_l + 4 * (n + 1)
         MU = 12 * a.nnz_u + 4 * (n + 1)
@@ -94,6 +94,20 @@ def main():
             ms = timeit(lambda: pc.apply_into(r, z))
             print(json.dumps({"kernel": "precond_gs2_nj1_f32", "ms": round(ms, 4), "gbs": round(by / ms / 1e6, 1)}),
                   flush=True)
+        if "sweep" in which:
+            from paper_2104_01196_b200 import _native as NN
+            b = g2.random_rhs(n, 0, device="cuda")
+            x0 = g2.random_rhs(n, 1, device="cuda")
+            x1 = torch.empty_like(x0)
+            for nj in (1, 2, 3):
+                cfg = NN.RelaxCfg.of(g2.RelaxConfig(1, 1, nj))
+                model = ML + MU + 4 * V8 + (ML + 3 * V8 if nj == 1 else (ML + 2 * V8) + (nj - 2) * (ML + 3 * V8) + (ML + 4 * V8))
+                ms = timeit(lambda: lib.rs_gs2_sweep(a.handle, p(b), p(x0), p(x1), C.byref(cfg), st))
+                print(json.dumps({"kernel": f"gs2_sweep_oop_nj{nj}", "ms": round(ms, 4),
+                                  "model_gbs": round(model / ms / 1e6, 1)}), flush=True)
+                ms = timeit(lambda: lib.rs_gs2_apply(a.handle, p(b), p(x0), C.byref(cfg), st))
+                print(json.dumps({"kernel": f"gs2_apply_inplace_nj{nj}", "ms": round(ms, 4),
+                                  "model_gbs": round(model / ms / 1e6, 1)}), flush=True)
         if "spmv" in which:
             y = torch.empty_like(r)
             ms = timeit(lambda: lib.rs_spmv(a.handle, p(r), None, None, p(y), st))
