@@ -389,8 +389,8 @@ static int launch(rs_matrix* m, WavePlan* p, int fwd, const R* b, const T* xin, 
 // 0.695 ms -- its per-step CTA barriers between stages cap it below the
 // barrier-free thread-per-row passes.  Kept for the fused-sweep work of §8.
 int wave_enabled() {
-  static const int on = getenv("RS_WAVE") && atoi(getenv("RS_WAVE")) != 0;
-  return on;
+  const char* e = getenv("RS_WAVE");
+  return e && atoi(e) != 0;
 }
 
 template <typename T>

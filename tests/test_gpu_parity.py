@@ -316,3 +316,35 @@ def test_stationary_elasticity_pattern(gmres_golden):
             step(x)
             got.append(np.linalg.norm(b - g2.spmv(a, x)) / bn)
         np.testing.assert_allclose(got, want, rtol=1e-12)
+
+
+@pytest.mark.parametrize("gen", ["lap3d_24", "ela3d_6", "rand_300"])
+def test_wavefront_sweep_bitwise(gen, monkeypatch):
+    """The opt-in fused wavefront sweep (RS_WAVE=1) is bitwise the reference arithmetic too."""
+    kind, nx = gen.split("_")
+    nx = int(nx)
+    if kind == "rand":
+        rng = np.random.default_rng(4)
+        d = np.zeros((nx, nx))
+        idx = rng.integers(0, nx, size=(6 * nx, 2))
+        d[idx[:, 0], idx[:, 1]] = rng.uniform(-1, 1, 6 * nx)
+        np.fill_diagonal(d, np.abs(d).sum(1) + 1.0)
+        h = g2.from_dense(d)
+    else:
+        h = {"lap3d": lambda: g2.laplace3d(nx), "ela3d": lambda: g2.elasticity3d(nx)}[kind]()
+    om = oracle.Matrix(h)
+    b = g2.random_rhs(h.nrows, 0)
+    x0 = g2.random_rhs(h.nrows, 1)
+    monkeypatch.setenv("RS_WAVE", "1")
+    s = g2.extract_splitting(h)
+    for cfg in (g2.RelaxConfig(1, 1, 1), g2.RelaxConfig(2, 1, 3, direction="symmetric"),
+                g2.RelaxConfig(1, 1, 2, form="compact", omega=0.9), g2.RelaxConfig(1, 1, 2, gamma=0.7, direction="backward")):
+        xg = x0.copy()
+        xo = x0.copy()
+        g2.gs2_apply(h, s, b, xg, cfg)
+        oracle.gs2_apply(om, b, xo, cfg)
+        assert np.array_equal(xg, xo), cfg
+    for prec in ("same", "single_inside_double"):
+        m = g2.Preconditioner(h, "gs2", g2.RelaxConfig(1, 1, 2), precision=prec)
+        mo = oracle.Precond(h, "gs2", n_j=2, precision=prec)
+        assert np.array_equal(m.apply(b), mo.apply(b)), prec
