@@ -157,7 +157,8 @@ int rs_precond_apply(rs_matrix_t m, int kind, const rs_relax_cfg *cfg, const dou
 /* ---- GMRES building blocks (krylov.py:162-250), float64 ----
  * Reductions are deterministic (fixed block partition, partials summed in
  * block order) and need a caller-owned device workspace of
- * rs_reduce_work_doubles(k) doubles.  V is row-major: Arnoldi vector i is
+ * rs_reduce_work_doubles(k) doubles, zero-filled once before first use
+ * (work[0] is the completion ticket of rs_cgs_pass's in-kernel reduction).  V is row-major: Arnoldi vector i is
  * V + i*ldv.  h / y / nrm2 are device pointers. */
 
 int64_t rs_reduce_work_doubles(int k);

@@ -236,7 +236,8 @@ __global__ void k_cast_up(int64_t n, const float* __restrict__ in, double* __res
 // so "update + re-orthogonalisation dots" of CGS2 read V once instead of twice.
 constexpr int kCgsThreads = 512;
 constexpr int kCgsWarps = kCgsThreads / 32;
-constexpr int kCgsStages = 3;
+constexpr int kCgsMaxStages = 8;
+constexpr int kCgsSmemBudget = 200 * 1024;
 constexpr int kCgsMaxK = 64;
 constexpr int kCgsMaxQ = kCgsMaxK / kCgsWarps;  // basis vectors per warp in the dots phase
 constexpr int kCgsMaxT = 8;                     // rows per lane in the dots phase (ch <= 256)
@@ -251,9 +252,17 @@ constexpr int kCgsTmapMinK = 8;
 
 static int cgs_chunk_rows(int k) {
   int ch = kCgsStageBytes / (8 * (k + 1));
-  if (k > kCgsTmapMinK) return std::max(32, std::min(256, ch) & ~31);
+  // measured: 64-row boxes (512 B rows) halve the TMA throughput; keep rows >= 1 KB
+  if (k > kCgsTmapMinK) return std::max(128, std::min(256, ch) & ~31);
   ch = std::max(128, std::min(4096, ch)) & ~127;
   return ch;
+}
+
+// as many ring stages as fit the shared-memory budget (deeper ring = more bytes in flight
+// while a chunk's update / dots phases run)
+static int cgs_stages(int k, int ch) {
+  const size_t stage = (size_t)(k + 1) * ch * sizeof(double);
+  return (int)std::max<size_t>(2, std::min<size_t>(kCgsMaxStages, kCgsSmemBudget / stage));
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
@@ -283,17 +292,19 @@ static bool encode_basis_map(CUtensorMap* map, const double* V, int64_t ldv, int
   return r == CUDA_SUCCESS;
 }
 
-static size_t cgs_smem_bytes(int k, int ch) {
-  return (size_t)kCgsStages * (k + 1) * ch * sizeof(double) + kCgsMaxK * sizeof(double) + kCgsStages * 8 + 16;
+static size_t cgs_smem_bytes(int k, int ch, int stages) {
+  return (size_t)stages * (k + 1) * ch * sizeof(double) + kCgsMaxK * sizeof(double) + kCgsMaxStages * 8 + 16;
 }
 
 template <bool UPDATE, bool DOTS, bool NORM>
 __global__ void __launch_bounds__(kCgsThreads, 1)
     k_cgs(const __grid_constant__ CUtensorMap tmap, int use_tmap, const double* __restrict__ V, int64_t ldv, int k,
-          int64_t n, int ch, int64_t rows_per_blk, const double* __restrict__ h_in, double* __restrict__ w,
-          double* __restrict__ partial, int* nonfinite) {
+          int64_t n, int ch, int kCgsStages, int64_t rows_per_blk, const double* __restrict__ h_in,
+          double* __restrict__ w, double* __restrict__ partial, int* nonfinite, double* __restrict__ h_out,
+          double* __restrict__ nrm2_out, unsigned int* ticket) {
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ double red[kCgsThreads];  // update-phase partial sums [split][row]
+  __shared__ bool s_last;
   const int stage_elems = (k + 1) * ch;
   double* st = reinterpret_cast<double*>(smraw);
   double* hs = st + (size_t)kCgsStages * stage_elems;
@@ -454,6 +465,26 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     }
   }
   if (nonfinite && __syncthreads_or(bad) && tid == 0) *nonfinite = 1;
+  // the last CTA to finish sums the per-CTA partials in CTA order (deterministic):
+  // one warp per output, lanes over a fixed interleave of CTAs, then a fixed shuffle tree
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int nout = (DOTS ? k : 0) + (NORM ? 1 : 0);
+  for (int o = warp; o < nout; o += kCgsWarps) {
+    const int col = DOTS ? (o < k ? o : k) : k;
+    double a = 0.0;
+    for (int bb = lane; bb < (int)gridDim.x; bb += 32) a += __ldcg(partial + (int64_t)bb * stride + col);
+    a = warp_sum(a);
+    if (lane == 0) {
+      if (DOTS && o < k) h_out[o] = a;
+      else nrm2_out[0] = a;
+    }
+  }
+  if (tid == 0) *ticket = 0;  // reset for the next launch (stream-ordered)
 }
 
 // out[j] = sum_b partial[b*stride + off + j] for j < cnt, b ascending
@@ -476,11 +507,14 @@ using namespace rs;
 
 extern "C" {
 
-int64_t rs_reduce_work_doubles(int k) { return (int64_t)kRedBlocks * (std::max(k, 1) + 2); }
+// one slot for the CGS completion ticket (work[0]) plus partials of kRedBlocks CTAs x (k + 2)
+// outputs; the caller zero-fills the workspace once, the kernel resets the ticket after use
+int64_t rs_reduce_work_doubles(int k) { return (int64_t)kRedBlocks * (std::max(k, 1) + 2) + 1; }
 
 int rs_gemv_t(const double* V, int64_t ldv, int k, int64_t n, const double* w, double* h, int* nonfinite,
               double* work, rs_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  if (work) work += 1;  // work[0] is reserved for the rs_cgs_pass ticket
   if (k < 0 || n < 0 || !work) {
     set_error(RS_ERR_ARG, "rs_gemv_t: bad arguments");
     return RS_ERR_ARG;
@@ -500,6 +534,7 @@ int rs_gemv_t(const double* V, int64_t ldv, int k, int64_t n, const double* w, d
 int rs_gemv_n_update(const double* V, int64_t ldv, int k, int64_t n, const double* h, double* w, double* nrm2,
                      double* work, rs_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  if (work) work += 1;  // work[0] is reserved for the rs_cgs_pass ticket
   if (k < 0 || n < 0 || (nrm2 && !work)) {
     set_error(RS_ERR_ARG, "rs_gemv_n_update: bad arguments");
     return RS_ERR_ARG;
@@ -537,7 +572,8 @@ int rs_cgs_pass(const double* V, int64_t ldv, int k, int64_t n, const double* h_
     return RS_OK;
   }
   const int ch = cgs_chunk_rows(k);
-  const size_t smem = cgs_smem_bytes(k, ch);
+  const int stages = cgs_stages(k, ch);
+  const size_t smem = cgs_smem_bytes(k, ch, stages);
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
   int use_tmap = 0;
@@ -551,11 +587,14 @@ int rs_cgs_pass(const double* V, int64_t ldv, int k, int64_t n, const double* h_
   int64_t rows = ((n + kCgsBlocks - 1) / kCgsBlocks + ch - 1) / ch * ch;
   int nblk = (int)std::max<int64_t>(1, (n + rows - 1) / std::max<int64_t>(rows, 1));
   const bool U = h_in != nullptr, D = h_out != nullptr, Nm = nrm2 != nullptr;
+  // work[0] holds the completion ticket of the in-kernel final reduction; partials follow
+  unsigned int* ticket = reinterpret_cast<unsigned int*>(work);
+  work += 1;
 #define RS_CGS_LAUNCH(u, d, nm)                                                                          \
   do {                                                                                                   \
     cudaFuncSetAttribute(k_cgs<u, d, nm>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
-    k_cgs<u, d, nm><<<nblk, kCgsThreads, smem, st>>>(tmap, use_tmap, V, ldv, k, n, ch, rows, h_in, w, work, \
-                                                     nonfinite);                                          \
+    k_cgs<u, d, nm><<<nblk, kCgsThreads, smem, st>>>(tmap, use_tmap, V, ldv, k, n, ch, stages, rows, h_in, w, \
+                                                     work, nonfinite, h_out, nrm2, ticket);               \
     RS_COUNT_LAUNCH();                                                                                   \
   } while (0)
   if (U && D && Nm) RS_CGS_LAUNCH(true, true, true);
@@ -566,14 +605,6 @@ int rs_cgs_pass(const double* V, int64_t ldv, int k, int64_t n, const double* h_
   else if (D) RS_CGS_LAUNCH(false, true, false);
   else RS_CGS_LAUNCH(false, false, true);
 #undef RS_CGS_LAUNCH
-  if (D) {
-    k_reduce_strided<<<1, 64, 0, st>>>(work, nblk, k + 1, 0, k, h_out);
-    RS_COUNT_LAUNCH();
-  }
-  if (Nm) {
-    k_reduce_strided<<<1, 32, 0, st>>>(work, nblk, k + 1, k, 1, nrm2);
-    RS_COUNT_LAUNCH();
-  }
   RS_CHECK_LAUNCH("rs_cgs_pass");
   return RS_OK;
 }
@@ -601,6 +632,7 @@ int rs_scale_by_norm(int64_t n, const double* w, const double* nrm2, double* out
 int rs_sub_norm(int64_t n, const double* b, const double* y, double* r, double* nrm2, double* work,
                 rs_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  if (work) work += 1;  // work[0] is reserved for the rs_cgs_pass ticket
   k_sub_norm<<<kRedBlocks, 256, 0, st>>>(n, b, y, r, work);
   RS_COUNT_LAUNCH();
   k_reduce_partials<<<1, 32, 0, st>>>(work, kRedBlocks, 1, nrm2, 0);
@@ -611,6 +643,7 @@ int rs_sub_norm(int64_t n, const double* b, const double* y, double* r, double* 
 
 int rs_dot(int64_t n, const double* x, const double* y, double* out, double* work, rs_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  if (work) work += 1;  // work[0] is reserved for the rs_cgs_pass ticket
   k_dot<<<kRedBlocks, 256, 0, st>>>(n, x, y, work);
   RS_COUNT_LAUNCH();
   k_reduce_partials<<<1, 32, 0, st>>>(work, kRedBlocks, 1, out, 0);

@@ -239,7 +239,7 @@ class _Workspace:
         self.t = torch.empty(n, **f64)
         self.r = torch.empty(n, **f64)
         lib = N.load()
-        self.work = torch.empty(int(lib.rs_reduce_work_doubles(max(restart + 1, 1))), **f64)
+        self.work = torch.zeros(int(lib.rs_reduce_work_doubles(max(restart + 2, 1))), **f64)
         # packed scalars: [h1 (m+1) | h2 (m+1) | nrm2 | aux]
         self.m1 = restart + 1
         self.scal = torch.zeros(2 * self.m1 + 4, **f64)

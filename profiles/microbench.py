@@ -59,7 +59,7 @@ def main():
         h = torch.randn(kmax + 1, dtype=torch.float64, device="cuda") * 1e-3
         h2 = torch.empty_like(h)
         nrm = torch.empty(1, dtype=torch.float64, device="cuda")
-        work = torch.empty(int(lib.rs_reduce_work_doubles(kmax + 2)), dtype=torch.float64, device="cuda")
+        work = torch.zeros(int(lib.rs_reduce_work_doubles(kmax + 2)), dtype=torch.float64, device="cuda")
         for k in ks:
             res = {
                 "gemv_t": (timeit(lambda: lib.rs_gemv_t(p(V), n, k, n, p(w), p(h2), None, p(work), st)), (k + 1) * V8),
