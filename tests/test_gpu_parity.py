@@ -348,3 +348,20 @@ def test_wavefront_sweep_bitwise(gen, monkeypatch):
         m = g2.Preconditioner(h, "gs2", g2.RelaxConfig(1, 1, 2), precision=prec)
         mo = oracle.Precond(h, "gs2", n_j=2, precision=prec)
         assert np.array_equal(m.apply(b), mo.apply(b)), prec
+
+
+# Reference GMRES(60) iteration counts at 128^3 (n = 2,097,152) measured by the survey with the
+# reference itself at OPENBLAS_NUM_THREADS=1 (~350 s each on the CPU).
+REF_128 = {("gs2", (1, 1, 0)): 1035, ("gs2", (1, 1, 1)): 858, ("gs2", (1, 1, 2)): 785, ("gs2", (1, 1, 3)): 773,
+           ("gs_seq", (1, 1, 0)): 750, ("jr", (2, 1, 0)): 344, ("jr", (3, 1, 0)): 470,
+           ("sgs2", (1, 1, 1)): 257, ("sgs_seq", (1, 1, 0)): 232}
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("kind,cfg", list(REF_128))
+def test_gmres_iteration_counts_128(kind, cfg):
+    a = g2.laplace3d(128, device="cuda")
+    b = g2.random_rhs(a.nrows, 0, device="cuda")
+    _, h = g2.gmres(a, b, g2.Preconditioner(a, kind, g2.RelaxConfig(*cfg)), restart=60, tol=1e-9)
+    assert h.converged
+    assert h.iterations == REF_128[(kind, cfg)], h.iterations
