@@ -285,10 +285,15 @@ def ours(args):
         kernels[g] = {"launches": cnt, "ms": round(t, 3), "share": round(t / total_ms, 3) if total_ms else None,
                       "gbs": round(gb / (t * 1e-3) / 1e9, 1) if gb and t else None}
     dom = max((g for g in kernels if g in group_bytes), key=lambda g: kernels[g]["ms"])
+    # traffic: ncu DRAM bytes of one launch of the dominant kernel (profiles/traffic.json), scaled to
+    # this cycle's average launch by the measured traffic / algorithmic-bytes ratio of that launch
     traffic = None
     tfile = ROOT / "profiles" / "traffic.json"
     if tfile.exists():
-        traffic = json.loads(tfile.read_text()).get(dom)
+        t = json.loads(tfile.read_text()).get(dom)
+        if t:
+            ratio = (t["dram_read"] + t["dram_write"]) / t["model_bytes"]
+            traffic = round(ratio * group_bytes[dom] / kernels[dom]["launches"])
     roofline = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["gbs"], "peak": hbm, "unit": "GB/s",
                 "frac": round(kernels[dom]["gbs"] / hbm, 3), "traffic": traffic,
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}
