@@ -199,6 +199,11 @@ int rs_dot(int64_t n, const double *x, const double *y, double *out, double *wor
 /* x += z */
 int rs_axpy1(int64_t n, const double *z, double *x, rs_stream_t stream);
 
+/* y = y + a*x and y = x + b*y, each product and sum rounded separately (no FMA):
+ * the CG updates x += alpha p, r -= alpha Ap, p = z + beta p (krylov.py:296-307) */
+int rs_axpy(int64_t n, double a, const double *x, double *y, rs_stream_t stream);
+int rs_xpby(int64_t n, const double *x, double b, double *y, rs_stream_t stream);
+
 /* ---- generators ---- */
 
 /* random_rhs (problems.py:228-242): out[i] = value number (offset+i) of the LCG

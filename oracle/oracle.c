@@ -367,6 +367,61 @@ done:
   return status;
 }
 
+/* ---------------------------------------------------------------- CG (krylov.py:253-309) */
+int orc_cg(const orc_csr *a, const double *b, orc_precond *m, double tol, int maxit, const double *x0, double *x,
+           double *hist, int *iters, int *conv) {
+  int64_t n = a->n;
+  int nh = 0, status = ORC_OK;
+  int64_t ei = 0;
+  *iters = 0;
+  *conv = 0;
+  if (x0) memcpy(x, x0, sizeof(double) * (size_t)n);
+  else memset(x, 0, sizeof(double) * (size_t)n);
+  double bnorm = nrm2(n, b);
+  if (bnorm == 0.0) {
+    memset(x, 0, sizeof(double) * (size_t)n);
+    hist[0] = 0.0;
+    *conv = 1;
+    return ORC_OK;
+  }
+  double *r = (double *)malloc(sizeof(double) * (size_t)n), *t = (double *)malloc(sizeof(double) * (size_t)n);
+  double *z = (double *)malloc(sizeof(double) * (size_t)n), *p = (double *)malloc(sizeof(double) * (size_t)n);
+  double *ap = (double *)malloc(sizeof(double) * (size_t)n);
+  orc_spmv_f64(a, x, t);
+  for (int64_t i = 0; i < n; ++i) r[i] = b[i] - t[i];
+  hist[nh++] = nrm2(n, r) / bnorm;
+  if (hist[0] <= tol) { *conv = 1; goto done; }
+  if (m) { status = orc_precond_apply(m, r, z, &ei); if (status) goto done; }
+  else memcpy(z, r, sizeof(double) * (size_t)n);
+  memcpy(p, z, sizeof(double) * (size_t)n);
+  double rz = orc_dot(n, r, z);
+  for (int it = 0; it < maxit; ++it) {
+    orc_spmv_f64(a, p, ap);
+    double pap = orc_dot(n, p, ap);
+    if (!isfinite(pap)) { status = ORC_EDIVERGE; goto done; }
+    if (pap <= 0.0) { status = ORC_EARG; goto done; } /* not SPD */
+    double alpha = rz / pap;
+    for (int64_t i = 0; i < n; ++i) { double q = alpha * p[i]; x[i] = x[i] + q; }
+    for (int64_t i = 0; i < n; ++i) { double q = alpha * ap[i]; r[i] = r[i] - q; }
+    orc_spmv_f64(a, x, t);
+    for (int64_t i = 0; i < n; ++i) t[i] = b[i] - t[i];
+    double true_rel = nrm2(n, t) / bnorm;
+    if (!isfinite(true_rel)) { status = ORC_EDIVERGE; goto done; }
+    hist[nh++] = true_rel;
+    if (true_rel <= tol) { *conv = 1; break; }
+    if (m) { status = orc_precond_apply(m, r, z, &ei); if (status) goto done; }
+    else memcpy(z, r, sizeof(double) * (size_t)n);
+    double rz_new = orc_dot(n, r, z);
+    double beta = rz_new / rz;
+    for (int64_t i = 0; i < n; ++i) { double q = beta * p[i]; p[i] = z[i] + q; }
+    rz = rz_new;
+  }
+done:
+  *iters = nh - 1;
+  free(r); free(t); free(z); free(p); free(ap);
+  return status;
+}
+
 /* ---------------------------------------------------------------- random_rhs (problems.py:228-242) */
 void orc_random_rhs(int64_t n, uint64_t seed, double *out) {
   uint64_t s = seed;

@@ -105,6 +105,10 @@ int orc_precond_apply(orc_precond *p, const double *r, double *z, int64_t *err_i
 int orc_gmres(const orc_csr *a, const double *b, orc_precond *m, int restart, double tol, int maxit,
               const double *x0, double *x, double *hist, int *iters, int *conv);
 
+/* preconditioned CG (krylov.py:253-309); status ORC_EARG = non-positive curvature (NotSpdError) */
+int orc_cg(const orc_csr *a, const double *b, orc_precond *m, double tol, int maxit, const double *x0, double *x,
+           double *hist, int *iters, int *conv);
+
 void orc_random_rhs(int64_t n, uint64_t seed, double *out);
 double orc_dot(int64_t n, const double *x, const double *y);
 

@@ -175,6 +175,18 @@ __global__ void __launch_bounds__(256) k_dot(int64_t n, const double* __restrict
   }
 }
 
+// y = y + a*x  (CG: x += alpha p, r -= alpha Ap as y + (-alpha)*x, krylov.py:296-297)
+__global__ void k_axpy(int64_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = __dadd_rn(y[i], __dmul_rn(a, x[i]));
+}
+
+// y = x + b*y  (CG: p = z + beta p, krylov.py:307)
+__global__ void k_xpby(int64_t n, const double* __restrict__ x, double b, double* __restrict__ y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = __dadd_rn(x[i], __dmul_rn(b, y[i]));
+}
+
 __global__ void k_axpy1(int64_t n, const double* __restrict__ z, double* __restrict__ x) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     x[i] = x[i] + z[i];
@@ -659,6 +671,26 @@ int rs_axpy1(int64_t n, const double* z, double* x, rs_stream_t stream) {
     RS_COUNT_LAUNCH();
   }
   RS_CHECK_LAUNCH("rs_axpy1");
+  return RS_OK;
+}
+
+int rs_axpy(int64_t n, double a, const double* x, double* y, rs_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n) {
+    k_axpy<<<grid_stride_blocks(n), 256, 0, st>>>(n, a, x, y);
+    RS_COUNT_LAUNCH();
+  }
+  RS_CHECK_LAUNCH("rs_axpy");
+  return RS_OK;
+}
+
+int rs_xpby(int64_t n, const double* x, double b, double* y, rs_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n) {
+    k_xpby<<<grid_stride_blocks(n), 256, 0, st>>>(n, x, b, y);
+    RS_COUNT_LAUNCH();
+  }
+  RS_CHECK_LAUNCH("rs_xpby");
   return RS_OK;
 }
 

@@ -452,3 +452,98 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
         if lucky or true_rel <= tol:
             converged = True
     return x, hist, converged
+
+
+def cg(a, b, m=None, tol: float = 1e-9, maxit: int = 10000, x0=None):
+    """Preconditioned conjugate gradients on the GPU (krylov.py:253-309).
+
+    Same recurrences and history as the reference: the TRUE relative residual
+    ||b - A x|| / ||b|| is recomputed and recorded every iteration; a
+    Preconditioner of a non-symmetric kind is rejected ("symmetric"),
+    non-positive curvature raises NotSpdError, non-finite values
+    DivergenceError.  Scalars (p.Ap, r.z, ||r||) come back to the host once
+    per iteration each; vectors stay in HBM.
+    """
+    if nrows_of(a) != ncols_of(a):
+        raise ValueError(f"square system required, matrix is {nrows_of(a)}x{ncols_of(a)}")
+    if not tol > 0:
+        raise ValueError(f"tol must be positive, got {tol}")
+    if isinstance(m, Preconditioner) and not m.is_symmetric:
+        raise ValueError(f"CG needs a symmetric preconditioner kind, got {m.kind!r} with direction {m.cfg.direction!r}")
+    torch = _torch()
+    lib = N.load()
+    dm = as_device(a)
+    if dm.dtype != np.float64:
+        raise ValueError("cg needs a double-precision matrix")
+    n = dm.nrows
+    dev = dm.torch_device
+    st = stream_ptr(dm.device_index)
+    numpy_out = not _is_tensor(b)
+    bt = b.to(dev, torch.float64) if _is_tensor(b) else torch.from_numpy(np.ascontiguousarray(b, np.float64)).to(dev)
+    x = torch.zeros(n, dtype=torch.float64, device=dev) if x0 is None else (
+        x0.to(dev, torch.float64).clone() if _is_tensor(x0) else torch.from_numpy(np.array(x0, dtype=np.float64)).to(dev))
+    op = _as_operator(m)
+    f64 = dict(dtype=torch.float64, device=dev)
+    r, t, z, p, ap = (torch.empty(n, **f64) for _ in range(5))
+    work = torch.zeros(int(lib.rs_reduce_work_doubles(2)), **f64)
+    sc = torch.zeros(1, **f64)
+
+    class _WS:  # minimal workspace for _apply_op (flags for the fp32 overflow check)
+        flags = torch.full((2,), _I64_MAX, dtype=torch.int64, device=dev)
+
+    def chk(s, what):
+        N.check(s, what)
+
+    def dot(u, v):
+        chk(lib.rs_dot(n, _p(u), _p(v), _p(sc), _p(work), st), "dot")
+        return float(sc.item())
+
+    def finish(xv, hist, conv):
+        out = xv.cpu().numpy() if numpy_out else xv
+        return out, ConvergenceHistory(np.array(hist), conv)
+
+    bnorm = math.sqrt(dot(bt, bt))
+    if bnorm == 0.0:
+        return finish(torch.zeros(n, **f64), [0.0], True)
+    chk(lib.rs_spmv(dm.handle, _p(x), None, None, _p(t), st), "spmv")
+    chk(lib.rs_sub_norm(n, _p(bt), _p(t), _p(r), _p(sc), _p(work), st), "sub_norm")
+    hist = [math.sqrt(float(sc.item())) / bnorm]
+    if hist[0] <= tol:
+        return finish(x, hist, True)
+
+    def precond(src, dst):
+        _WS.flags[1] = _I64_MAX
+        _apply_op(op, src, dst, _WS)
+        if op is not None and getattr(op, "precision", "same") == "single_inside_double":
+            i = int(_WS.flags[1].item())
+            if i != _I64_MAX:
+                raise OverflowError(f"entry {i} overflows single precision")
+
+    precond(r, z)
+    p.copy_(z)
+    rz = dot(r, z)
+    converged = False
+    for _ in range(maxit):
+        chk(lib.rs_spmv(dm.handle, _p(p), None, None, _p(ap), st), "spmv")
+        pap = dot(p, ap)
+        if not math.isfinite(pap):
+            raise DivergenceError("non-finite curvature in CG")
+        if pap <= 0.0:
+            raise NotSpdError(f"non-positive curvature p^T A p = {pap}; matrix is not SPD")
+        alpha = rz / pap
+        chk(lib.rs_axpy(n, alpha, _p(p), _p(x), st), "axpy")
+        chk(lib.rs_axpy(n, -alpha, _p(ap), _p(r), st), "axpy")
+        chk(lib.rs_spmv(dm.handle, _p(x), None, None, _p(t), st), "spmv")
+        chk(lib.rs_sub_norm(n, _p(bt), _p(t), _p(t), _p(sc), _p(work), st), "sub_norm")
+        true_rel = math.sqrt(float(sc.item())) / bnorm
+        if not math.isfinite(true_rel):
+            raise DivergenceError("non-finite residual in CG")
+        hist.append(true_rel)
+        if true_rel <= tol:
+            converged = True
+            break
+        precond(r, z)
+        rz_new = dot(r, z)
+        chk(lib.rs_xpby(n, _p(z), rz_new / rz, _p(p), st), "xpby")
+        rz = rz_new
+    return finish(x, hist, converged)

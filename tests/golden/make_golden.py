@@ -343,7 +343,43 @@ def spread_runs():
     return runs
 
 
+def cg_fixtures():
+    """Preconditioned CG (krylov.py:253-309) histories: paper §9/§10 solver with SGS2."""
+    res = {}
+    P, C = rs.Preconditioner, rs.RelaxConfig
+
+    def run(label, a, b, m, tol=1e-9):
+        t0 = time.perf_counter()
+        _, h = rs.cg(a, b, m, tol=tol)
+        res[label] = {"iterations": int(h.iterations), "converged": bool(h.converged),
+                      "rel_res": [float(v) for v in h.rel_res], "seconds": round(time.perf_counter() - t0, 3)}
+        print(f"{label}: {h.iterations} it, conv={h.converged}", flush=True)
+
+    a = rs.laplace2d(100)
+    b = rs.random_rhs(a.nrows, 51)
+    for spec, kind, cfg, prec in (("sgs_seq", "sgs_seq", C(1, 1, 0), "same"), ("sgs2_1_1_1", "sgs2", C(1, 1, 1), "same"),
+                                  ("sgs2_1_1_2", "sgs2", C(1, 1, 2), "same"), ("jr_1", "jr", C(1, 1, 0), "same"),
+                                  ("none", "none", None, "same"),
+                                  ("sgs2_1_1_1__single", "sgs2", C(1, 1, 1), "single_inside_double")):
+        run(f"cg__lap2d_100__{spec}", a, b, P(a, kind, cfg, precision=prec))
+    a = rs.laplace3d(32)
+    b = rs.random_rhs(a.nrows, 0)
+    for spec, kind, cfg, prec in (("sgs2_1_1_1", "sgs2", C(1, 1, 1), "same"), ("sgs_seq", "sgs_seq", C(1, 1, 0), "same"),
+                                  ("sgs2_1_1_1__single", "sgs2", C(1, 1, 1), "single_inside_double")):
+        run(f"cg__lap3d_32__{spec}", a, b, P(a, kind, cfg, precision=prec))
+    a = rs.elasticity3d(8)
+    b = rs.random_rhs(a.nrows, 0)
+    run("cg__ela3d_8__sgs2_1_1_3", a, b, P(a, "sgs2", C(1, 1, 3)))
+    return res
+
+
 def main():
+    if "--cg" in sys.argv:
+        path = HERE / "gmres.json"
+        data = json.loads(path.read_text())
+        data["cg"] = cg_fixtures()
+        path.write_text(json.dumps(data, indent=1))
+        return
     if "--spread" in sys.argv:
         path = HERE / "gmres.json"
         data = json.loads(path.read_text())
@@ -367,9 +403,9 @@ def main():
         old = json.loads(path.read_text()).get("runs", {})
         old.update(gm)
         gm = old
-    spread = json.loads(path.read_text()).get("spread", {}) if path.exists() else {}
-    path.write_text(json.dumps({"meta": meta, "runs": gm, "stationary": stationary_fixtures(), "spread": spread},
-                               indent=1))
+    old = json.loads(path.read_text()) if path.exists() else {}
+    path.write_text(json.dumps({"meta": meta, "runs": gm, "stationary": stationary_fixtures(),
+                                "spread": old.get("spread", {}), "cg": old.get("cg", {})}, indent=1))
     print(f"all done in {time.perf_counter() - t0:.1f}s")
 
 

@@ -365,3 +365,35 @@ def test_gmres_iteration_counts_128(kind, cfg):
     _, h = g2.gmres(a, b, g2.Preconditioner(a, kind, g2.RelaxConfig(*cfg)), restart=60, tol=1e-9)
     assert h.converged
     assert h.iterations == REF_128[(kind, cfg)], h.iterations
+
+
+from test_oracle import CG_LABELS, parse_cg_label  # noqa: E402
+
+
+@pytest.mark.parametrize("label", CG_LABELS)
+def test_cg_iteration_counts(label, gmres_golden):
+    """PCG (krylov.py:253-309) with SGS2 / SGS / JR: reference iteration counts and true-residual history."""
+    want = gmres_golden["cg"][label]
+    prob, seed, kind, cfg, prec = parse_cg_label(label)
+    a = golden_problem(prob)
+    b = g2.random_rhs(a.nrows, seed)
+    m = g2.Preconditioner(a, kind, g2.RelaxConfig(*cfg) if kind != "none" else None, precision=prec)
+    x, h = g2.cg(a, b, m, tol=1e-9)
+    assert h.converged and h.iterations == want["iterations"], (h.iterations, want["iterations"])
+    np.testing.assert_allclose(h.rel_res, want["rel_res"], rtol=1e-6)
+
+
+def test_cg_api_semantics():
+    a2 = g2.from_dense([[2.0, -1.0], [-1.0, 2.0]])
+    with pytest.raises(ValueError, match="symmetric"):
+        g2.cg(a2, np.ones(2), g2.Preconditioner(a2, "gs_seq", g2.RelaxConfig(1, 1, 0)))
+    with pytest.raises(g2.NotSpdError):
+        g2.cg(g2.from_dense(np.diag([1.0, -1.0])), np.array([1.0, 1.0]))
+    x, h = g2.cg(g2.from_dense(np.diag([1.0, 2.0, 3.0, 4.0])), np.ones(4),
+                 g2.Preconditioner(g2.from_dense(np.diag([1.0, 2.0, 3.0, 4.0])), "jr", g2.RelaxConfig(1, 1, 0)))
+    assert h.converged and h.iterations == 1
+    np.testing.assert_allclose(x, [1.0, 0.5, 1.0 / 3.0, 0.25], rtol=1e-12)
+    a = g2.laplace3d(24, device="cuda")
+    b = g2.random_rhs(a.nrows, 3, device="cuda")
+    x, h = g2.cg(a, b, g2.Preconditioner(a, "sgs2", g2.RelaxConfig(1, 1, 1)))
+    assert h.converged and x.is_cuda

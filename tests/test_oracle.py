@@ -171,3 +171,36 @@ def test_oracle_gmres_iteration_counts(label, gmres_golden):
     # the trajectories agree closely: dot-product rounding (OpenBLAS vs a fixed
     # chunked order) only perturbs the late estimates at the 1e-3 level
     assert np.max(np.abs(hist - ref) / np.maximum(ref, 1e-300)) < 5e-2
+
+
+CG_LABELS = ["cg__lap2d_100__sgs_seq", "cg__lap2d_100__sgs2_1_1_1", "cg__lap2d_100__sgs2_1_1_2", "cg__lap2d_100__jr_1",
+             "cg__lap2d_100__none", "cg__lap2d_100__sgs2_1_1_1__single", "cg__lap3d_32__sgs2_1_1_1",
+             "cg__lap3d_32__sgs_seq", "cg__lap3d_32__sgs2_1_1_1__single", "cg__ela3d_8__sgs2_1_1_3"]
+
+
+def parse_cg_label(label):
+    """'cg__lap2d_100__sgs2_1_1_1__single' -> (problem, rhs seed, kind, (n_t, n_k, n_j), precision)"""
+    parts = label.split("__")
+    prob, spec = parts[1], parts[2]
+    prec = "single_inside_double" if len(parts) > 3 and parts[3] == "single" else "same"
+    seed = 51 if prob == "lap2d_100" else 0
+    toks = spec.split("_")
+    if spec == "none":
+        return prob, seed, "none", (1, 1, 1), prec
+    if toks[1] == "seq":
+        return prob, seed, toks[0] + "_seq", (1, 1, 0), prec
+    if toks[0] == "jr":
+        return prob, seed, "jr", (int(toks[1]), 1, 0), prec
+    return prob, seed, toks[0], tuple(int(t) for t in toks[1:]), prec
+
+
+@pytest.mark.parametrize("label", CG_LABELS)
+def test_oracle_cg_iteration_counts(label, gmres_golden):
+    want = gmres_golden["cg"][label]
+    prob, seed, kind, (nt, nk, nj), prec = parse_cg_label(label)
+    a = golden_problem(prob)
+    b = oracle.random_rhs(a.nrows, seed)
+    pre = oracle.Precond(a, kind, n_t=nt, n_k=nk, n_j=nj, precision=prec)
+    _, hist, conv = oracle.cg(a, b, pre, tol=1e-9)
+    assert conv and len(hist) - 1 == want["iterations"]
+    np.testing.assert_allclose(hist, want["rel_res"], rtol=1e-6)
