@@ -238,6 +238,9 @@ static void free_sell(Sell<T>& s) {
 static void free_levels(Levels& l) {
   free(l.level_ptr_host);
   cudaFree(l.rows);
+  cudaFree(l.done);
+  cudaFree(l.level_ptr_dev);
+  cudaFree(l.barrier);
   l = Levels();
 }
 

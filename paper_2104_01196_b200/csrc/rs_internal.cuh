@@ -66,6 +66,12 @@ struct Levels {
   int64_t nlevels = 0;
   int64_t* level_ptr_host = nullptr;  // [nlevels+1]
   int32_t* rows = nullptr;            // [nrows] device, rows in level order
+  unsigned int* done = nullptr;       // [nrows] per-row done flags of the sync-free sweep (epoch-tagged)
+  unsigned int epoch = 0;
+  int64_t* level_ptr_dev = nullptr;   // [nlevels+1] device (level-synchronous sweep)
+  unsigned int* barrier = nullptr;    // grid-barrier words (count, generation)
+  int coop_grid = -1;                 // CTAs of the cooperative sweeps (0: unsupported, -1: not probed)
+  int level_grid = 0;
 };
 
 }  // namespace rs
