@@ -254,6 +254,25 @@ def gmres_fixtures(slow=False):
 def stationary_fixtures():
     """Stand-alone smoother mode (cli.py:136-152 semantics): rel. residual per application."""
     res = {}
+    # config C3 pattern (SURVEY.md App. A4) at 16^3: JR with damping 1 diverges, GS2 converges as n_j grows
+    a = rs.elasticity3d(16)
+    s = rs.extract_splitting(a)
+    b = rs.random_rhs(a.nrows, 0)
+    bn = np.linalg.norm(b)
+    runs = [("jr", lambda x: rs.jr_sweeps(a, s, b, x, 1)),
+            ("gs_fwd", lambda x: rs.gs_sequential_sweep(a, s, b, x, "forward"))]
+    for nj in (1, 2, 3, 5, 10):
+        for d in ("forward", "symmetric"):
+            cfg = rs.RelaxConfig(1, 1, nj, direction=d)
+            runs.append((f"gs2_nj{nj}_{d}", lambda x, cfg=cfg: rs.gs2_apply(a, s, b, x, cfg)))
+    for label, fn in runs:
+        x = np.zeros(a.nrows)
+        hist = []
+        for _ in range(50):
+            fn(x)
+            hist.append(float(np.linalg.norm(rs.residual(a, b, x)) / bn))
+        res[f"ela3d_16__{label}"] = hist
+        print(f"stationary ela3d_16 {label}: {hist[-1]:.3e}", flush=True)
     a = rs.elasticity3d(4)
     s = rs.extract_splitting(a)
     b = rs.random_rhs(a.nrows, 31)
@@ -374,6 +393,12 @@ def cg_fixtures():
 
 
 def main():
+    if "--stationary" in sys.argv:
+        path = HERE / "gmres.json"
+        data = json.loads(path.read_text())
+        data["stationary"] = stationary_fixtures()
+        path.write_text(json.dumps(data, indent=1))
+        return
     if "--cg" in sys.argv:
         path = HERE / "gmres.json"
         data = json.loads(path.read_text())

@@ -397,3 +397,34 @@ def test_cg_api_semantics():
     b = g2.random_rhs(a.nrows, 3, device="cuda")
     x, h = g2.cg(a, b, g2.Preconditioner(a, "sgs2", g2.RelaxConfig(1, 1, 1)))
     assert h.converged and x.is_cuda
+
+
+@pytest.mark.parametrize("label", ["jr", "gs_fwd"] + [f"gs2_nj{nj}_{d}" for nj in (1, 2, 3, 5, 10)
+                                                      for d in ("forward", "symmetric")])
+def test_c3_elasticity_smoother_pattern(label, gmres_golden):
+    """Config C3 pattern at 16^3 (reference histories, 50 applications): JR(w=1) diverges to 1.4e9,
+    GS2 converges once n_j >= 3, SGS2 needs n_j >= 3; every residual matches the reference run."""
+    want = gmres_golden["stationary"][f"ela3d_16__{label}"]
+    a = _ELA16.get("a")
+    if a is None:
+        a = _ELA16["a"] = g2.elasticity3d(16)
+    s = g2.extract_splitting(a)
+    b = torch.from_numpy(g2.random_rhs(a.nrows, 0)).cuda()
+    x = torch.zeros_like(b)
+    if label == "jr":
+        step = lambda: g2.jr_sweeps(a, s, b, x, 1)  # noqa: E731
+    elif label == "gs_fwd":
+        step = lambda: g2.gs_sequential_sweep(a, s, b, x, "forward")  # noqa: E731
+    else:
+        nj, d = label[6:].split("_")
+        cfg = g2.RelaxConfig(1, 1, int(nj), direction=d)
+        step = lambda: g2.gs2_apply(a, s, b, x, cfg)  # noqa: E731
+    bn = float(torch.linalg.norm(b))
+    got = []
+    for _ in range(50):
+        step()
+        got.append(float(torch.linalg.norm(b - g2.spmv(a, x))) / bn)
+    np.testing.assert_allclose(got, want, rtol=1e-9)
+
+
+_ELA16 = {}
