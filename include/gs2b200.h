@@ -46,13 +46,15 @@ extern "C" {
 #define RS_NON_COMPACT 0
 #define RS_COMPACT 1
 
-/* preconditioner kinds (krylov.py:24 PRECOND_KINDS; mt_* are not on this path) */
+/* preconditioner kinds (krylov.py:24 PRECOND_KINDS) */
 #define RS_PC_NONE 0
 #define RS_PC_JR 1
 #define RS_PC_GS_SEQ 2
 #define RS_PC_SGS_SEQ 3
 #define RS_PC_GS2 4
 #define RS_PC_SGS2 5
+#define RS_PC_MT_GS 6
+#define RS_PC_MT_SGS 7
 
 /* stencil generators for rs_mat_create_stencil */
 #define RS_STENCIL_LAPLACE2D 0  /* problems.py:58-73, params unused */
@@ -108,6 +110,14 @@ int rs_mat_info(rs_matrix_t m, int64_t *info8, int *dtype);
 int rs_mat_export_tri(rs_matrix_t m, int which, int64_t *row_ptr, int64_t *col_idx, void *values, void *dvalues);
 int rs_mat_export_diag(rs_matrix_t m, void *d);
 
+/* greedy_color (coloring.py:33-63): rows ascending, smallest color unused by a
+ * neighbour in the symmetrized pattern; computed once per handle (host).
+ * color_out: host int64[nrows] (may be NULL).  Synchronises. */
+int rs_mat_coloring(rs_matrix_t m, int64_t *color_out, int64_t *ncolors);
+
+/* install a caller-supplied coloring (Coloring argument of mt_gs_sweep); colors in [0, ncolors) */
+int rs_mat_set_coloring(rs_matrix_t m, const int64_t *color, int64_t ncolors);
+
 /* ---- kernels of the numba ABI (_kernels.py) ---- */
 
 /* csr_matvec (_kernels.py:15-21) / spmv (sparse.py:179-184): y = A x.
@@ -118,6 +128,11 @@ int rs_spmv(rs_matrix_t m, const void *x, const void *x_lo, const void *x_hi, vo
  * level-scheduled: rows of one dependency level run in parallel, x in place.
  * Bitwise equal to the sequential natural-order sweep. */
 int rs_gs_sweep(rs_matrix_t m, const void *b, void *x, int direction, double omega, rs_stream_t stream);
+
+/* mt_gs_sweep (coloring.py:66-88): multicolor GS, colors in order (reversed
+ * backward), rows of one color in parallel, x in place; bitwise the reference
+ * visit of the concatenated color classes. */
+int rs_mt_gs_sweep(rs_matrix_t m, const void *b, void *x, int direction, double omega, rs_stream_t stream);
 
 /* ---- relaxation (relax.py) ---- */
 

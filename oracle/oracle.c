@@ -117,9 +117,74 @@ int orc_hybrid_relax(const orc_csr *a, int is_f32, const int64_t *off, int nb, c
   return st;
 }
 
+/* ---------------------------------------------------------------- multicolor GS (coloring.py:33-88) */
+/* greedy_color: rows ascending, smallest color not used by a neighbour in the symmetrized pattern */
+int orc_greedy_color(const orc_csr *a, int64_t *color, int64_t *ncolors) {
+  int64_t n = a->n;
+  int64_t *deg = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t k = a->row_ptr[i]; k < a->row_ptr[i + 1]; ++k) {
+      int64_t j = a->col_idx[k];
+      if (j != i) { deg[i + 1]++; deg[j + 1]++; }
+    }
+  for (int64_t i = 0; i < n; ++i) deg[i + 1] += deg[i];
+  int64_t *adj = (int64_t *)malloc(sizeof(int64_t) * (size_t)(deg[n] ? deg[n] : 1));
+  int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n ? n : 1));
+  for (int64_t i = 0; i < n; ++i) fill[i] = deg[i];
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t k = a->row_ptr[i]; k < a->row_ptr[i + 1]; ++k) {
+      int64_t j = a->col_idx[k];
+      if (j != i) { adj[fill[i]++] = j; adj[fill[j]++] = i; }
+    }
+  int64_t *mark = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  for (int64_t i = 0; i <= n; ++i) mark[i] = -1;
+  for (int64_t i = 0; i < n; ++i) color[i] = -1;
+  int64_t nc = n ? 0 : 1;
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t q = deg[i]; q < deg[i + 1]; ++q) {
+      int64_t c = color[adj[q]];
+      if (c >= 0) mark[c] = i;
+    }
+    int64_t c = 0;
+    while (mark[c] == i) ++c;
+    color[i] = c;
+    if (c + 1 > nc) nc = c + 1;
+  }
+  *ncolors = nc;
+  free(deg); free(adj); free(fill); free(mark);
+  return ORC_OK;
+}
+
+/* rows grouped by color, ascending within a color; colors ascending (forward) or descending (backward) */
+static int64_t *color_order(const int64_t *color, int64_t n, int64_t nc, int backward) {
+  int64_t *order = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n ? n : 1));
+  int64_t q = 0;
+  for (int64_t cc = 0; cc < nc; ++cc) {
+    int64_t c = backward ? nc - 1 - cc : cc;
+    for (int64_t i = 0; i < n; ++i)
+      if (color[i] == c) order[q++] = i;
+  }
+  return order;
+}
+
+int orc_mt_gs_sweep(const orc_csr *a, const orc_split *s, const int64_t *color, int64_t nc, const void *b, void *x,
+                    int direction, double omega) {
+  for (int pass = 0; pass < 2; ++pass) {
+    int bwd = pass == 1;
+    if (direction == 0 && bwd) continue;
+    if (direction == 1 && !bwd) continue;
+    int64_t *order = color_order(color, a->n, nc, bwd);
+    if (s->is_f32) gs_sweep_order_f32(a, (const float *)s->d, (const float *)b, (float *)x, order, a->n, omega);
+    else gs_sweep_order_f64(a, (const double *)s->d, (const double *)b, (double *)x, order, a->n, omega);
+    free(order);
+  }
+  return ORC_OK;
+}
+
 /* ---------------------------------------------------------------- preconditioner (krylov.py:59-137) */
 struct orc_precond {
   int kind, single, nblocks;
+  int64_t *color, ncolors;
   orc_cfg cfg;
   orc_csr a64, a32;
   float *v32;
@@ -142,7 +207,7 @@ orc_precond *orc_precond_create(const orc_csr *a64, int kind, const orc_cfg *cfg
   p->a64 = *a64;
   p->nblocks = nblocks;
   /* symmetric kinds force the symmetric direction (krylov.py:86-87) */
-  if (kind == ORC_SGS_SEQ || kind == ORC_SGS2) p->cfg.direction = 2;
+  if (kind == ORC_SGS_SEQ || kind == ORC_SGS2 || kind == ORC_MT_SGS) p->cfg.direction = 2;
   *status = ORC_OK;
   if (kind == ORC_NONE) return p;
   int64_t nnz = a64->row_ptr[n];
@@ -169,6 +234,10 @@ orc_precond *orc_precond_create(const orc_csr *a64, int kind, const orc_cfg *cfg
   } else {
     *status = orc_split_build(aw, single, single ? &p->s32 : &p->s64, err_index);
   }
+  if (kind == ORC_MT_GS || kind == ORC_MT_SGS) {
+    p->color = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n ? n : 1));
+    orc_greedy_color(a64, p->color, &p->ncolors);
+  }
   size_t es = single ? sizeof(float) : sizeof(double);
   p->work = malloc(es * 8 * (size_t)(n ? n : 1));
   p->rhs = malloc(es * (size_t)(n ? n : 1));
@@ -183,7 +252,7 @@ void orc_precond_free(orc_precond *p) {
   if (p->s32.d) orc_split_free(&p->s32);
   if (p->blk64) { blocks_free_f64(p->blk64, p->nblocks); free(p->blk64); }
   if (p->blk32) { blocks_free_f32(p->blk32, p->nblocks); free(p->blk32); }
-  free(p->work); free(p->rhs); free(p->z);
+  free(p->work); free(p->rhs); free(p->z); free(p->color);
   free(p);
 }
 
@@ -200,6 +269,11 @@ void orc_precond_free(orc_precond *p) {
           if (p->cfg.direction != 1) gs_sweep_dir_##SFX(aw, (const T *)(sw)->d, rhs, z, 0, p->cfg.omega); \
           if (p->cfg.direction != 0) gs_sweep_dir_##SFX(aw, (const T *)(sw)->d, rhs, z, 1, p->cfg.omega); \
         }                                                                                       \
+        break;                                                                                  \
+      case ORC_MT_GS:                                                                           \
+      case ORC_MT_SGS:                                                                          \
+        for (int it = 0; it < sweeps; ++it)                                                     \
+          orc_mt_gs_sweep(aw, sw, p->color, p->ncolors, rhs, z, p->cfg.direction, p->cfg.omega); \
         break;                                                                                  \
       case ORC_GS2:                                                                             \
       case ORC_SGS2: gs2_apply_##SFX(aw, sw, rhs, z, &p->cfg, w); break;                        \

@@ -72,7 +72,8 @@ typedef struct {
 } orc_cfg;
 
 /* preconditioner kinds (krylov.py:24) */
-enum { ORC_NONE = 0, ORC_JR = 1, ORC_GS_SEQ = 2, ORC_SGS_SEQ = 3, ORC_GS2 = 4, ORC_SGS2 = 5, ORC_HYBRID_GS2 = 6, ORC_HYBRID_GS = 7 };
+enum { ORC_NONE = 0, ORC_JR = 1, ORC_GS_SEQ = 2, ORC_SGS_SEQ = 3, ORC_GS2 = 4, ORC_SGS2 = 5, ORC_HYBRID_GS2 = 6, ORC_HYBRID_GS = 7,
+       ORC_MT_GS = 8, ORC_MT_SGS = 9 };
 
 typedef struct orc_precond orc_precond;
 
@@ -90,6 +91,11 @@ int orc_jr_sweeps(const orc_csr *a, const orc_split *s, const void *b, void *x, 
 int orc_gs_sweep(const orc_csr *a, const orc_split *s, const void *b, void *x, int direction, double omega);
 int orc_inner_jr(const orc_split *s, const void *r, int n_j, int backward, double omega, double gamma, void *g_out);
 int orc_gs2_apply(const orc_csr *a, const orc_split *s, const void *b, void *x, const orc_cfg *cfg);
+/* greedy_color (coloring.py:49-63) and mt_gs_sweep (coloring.py:66-88) */
+int orc_greedy_color(const orc_csr *a, int64_t *color, int64_t *ncolors);
+int orc_mt_gs_sweep(const orc_csr *a, const orc_split *s, const int64_t *color, int64_t ncolors, const void *b, void *x,
+                    int direction, double omega);
+
 /* hybrid block Jacobi: offsets[nblocks+1]; local: 0 gs, 1 gs2 */
 int orc_hybrid_relax(const orc_csr *a, int is_f32, const int64_t *offsets, int nblocks, const void *b, void *x,
                      const orc_cfg *cfg, int local, int64_t *err_index);

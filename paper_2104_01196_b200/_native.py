@@ -25,7 +25,7 @@ RS_ERR_UNSUPPORTED = -7
 RS_F64, RS_F32 = 0, 1
 DIRECTIONS = {"forward": 0, "backward": 1, "symmetric": 2}
 FORMS = {"non_compact": 0, "compact": 1}
-PC_KINDS = {"none": 0, "jr": 1, "gs_seq": 2, "sgs_seq": 3, "gs2": 4, "sgs2": 5}
+PC_KINDS = {"none": 0, "jr": 1, "gs_seq": 2, "sgs_seq": 3, "gs2": 4, "sgs2": 5, "mt_gs": 6, "mt_sgs": 7}
 STENCILS = {"laplace2d": 0, "laplace3d": 1, "convdiff3d": 2}
 
 
@@ -57,6 +57,9 @@ _SIGS = {
     "rs_mat_info": ([_P, _P, C.POINTER(C.c_int)], C.c_int),
     "rs_mat_export_tri": ([_P, C.c_int, _P, _P, _P, _P], C.c_int),
     "rs_mat_export_diag": ([_P, _P], C.c_int),
+    "rs_mat_coloring": ([_P, _P, C.POINTER(C.c_int64)], C.c_int),
+    "rs_mat_set_coloring": ([_P, _P, C.c_int64], C.c_int),
+    "rs_mt_gs_sweep": ([_P, _P, _P, C.c_int, C.c_double, _P], C.c_int),
     "rs_spmv": ([_P, _P, _P, _P, _P, _P], C.c_int),
     "rs_gs_sweep": ([_P, _P, _P, C.c_int, C.c_double, _P], C.c_int),
     "rs_jr_sweeps": ([_P, _P, _P, C.c_int, C.c_double, _P], C.c_int),

@@ -396,6 +396,8 @@ void destroy(rs_matrix* m) {
   free_sell(m->L32); free_sell(m->U32); free_sell(m->Elo32); free_sell(m->Ehi32);
   free_levels(m->fwd);
   free_levels(m->bwd);
+  free_levels(m->mt);
+  free(m->color);
   cudaFree(m->scratch);
   cudaFree(m->scratch2);
   cudaFree(m->red);
@@ -491,6 +493,81 @@ int build_levels_t(rs_matrix* m, int backward) {
   RS_CUDA(cudaMalloc(&lv.rows, sizeof(int32_t) * std::max<int64_t>(n, 1)));
   RS_CUDA(cudaMemcpy(lv.rows, rows.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
   return RS_OK;
+}
+
+// ------------------------------------------------------------------ multicolor GS coloring (host)
+// greedy_color (coloring.py:33-63): rows ascending, smallest color not used by a
+// neighbour of the symmetrized stored pattern (L and U of the local block, both
+// directions).  Installs rows-by-color in m->mt.
+static int install_coloring(rs_matrix* m, const int64_t* color, int64_t nc) {
+  const int64_t n = m->nrows;
+  Levels& lv = m->mt;
+  free(lv.level_ptr_host);
+  cudaFree(lv.rows);
+  lv = Levels();
+  lv.nlevels = nc;
+  lv.level_ptr_host = (int64_t*)calloc(nc + 1, sizeof(int64_t));
+  for (int64_t i = 0; i < n; ++i) lv.level_ptr_host[color[i] + 1]++;
+  for (int64_t c = 0; c < nc; ++c) lv.level_ptr_host[c + 1] += lv.level_ptr_host[c];
+  std::vector<int64_t> fillp(lv.level_ptr_host, lv.level_ptr_host + nc);
+  std::vector<int32_t> rows(std::max<int64_t>(n, 1));
+  for (int64_t i = 0; i < n; ++i) rows[fillp[color[i]]++] = (int32_t)i;
+  RS_CUDA(cudaMalloc(&lv.rows, sizeof(int32_t) * std::max<int64_t>(n, 1)));
+  if (n) RS_CUDA(cudaMemcpy(lv.rows, rows.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  if (m->color != color) {
+    free(m->color);
+    m->color = (int64_t*)malloc(sizeof(int64_t) * std::max<int64_t>(n, 1));
+    memcpy(m->color, color, sizeof(int64_t) * n);
+  }
+  return RS_OK;
+}
+
+template <typename T>
+static int build_coloring_t(rs_matrix* m) {
+  if (m->color) return RS_OK;
+  const int64_t n = m->nrows;
+  std::vector<int64_t> deg(n + 1, 0);
+  std::vector<int32_t> adj;
+  std::vector<int64_t> sp[2];
+  std::vector<int32_t> col[2];
+  int st;
+  for (int w = 0; w < 2; ++w)
+    if ((st = host_tri(tri<T>(m, w), sp[w], col[w]))) return st;
+  auto each = [&](auto&& f) {
+    for (int w = 0; w < 2; ++w)
+      for (int64_t i = 0; i < n; ++i) {
+        const int64_t s = i >> 5, lane = i & 31, wd = (sp[w][s + 1] - sp[w][s]) / kSlice;
+        for (int64_t j = 0; j < wd; ++j) {
+          const int32_t c = col[w][sp[w][s] + j * kSlice + lane];
+          if (c >= 0) f(i, (int64_t)c);
+        }
+      }
+  };
+  each([&](int64_t i, int64_t c) { deg[i + 1]++; deg[c + 1]++; });
+  for (int64_t i = 0; i < n; ++i) deg[i + 1] += deg[i];
+  adj.resize(std::max<int64_t>(deg[n], 1));
+  std::vector<int64_t> fill(deg.begin(), deg.end() - 1);
+  each([&](int64_t i, int64_t c) { adj[fill[i]++] = (int32_t)c; adj[fill[c]++] = (int32_t)i; });
+  int64_t* color = (int64_t*)malloc(sizeof(int64_t) * std::max<int64_t>(n, 1));
+  std::vector<int64_t> mark(n + 1, -1);
+  int64_t nc = n ? 0 : 1;
+  for (int64_t i = 0; i < n; ++i) color[i] = -1;
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t q = deg[i]; q < deg[i + 1]; ++q) {
+      const int64_t c = color[adj[q]];
+      if (c >= 0) mark[c] = i;
+    }
+    int64_t c = 0;
+    while (mark[c] == i) ++c;
+    color[i] = c;
+    nc = std::max(nc, c + 1);
+  }
+  m->color = color;
+  return install_coloring(m, color, nc);
+}
+
+int build_coloring(rs_matrix* m) {
+  return m->dtype == RS_F32 ? build_coloring_t<float>(m) : build_coloring_t<double>(m);
 }
 
 int build_levels(rs_matrix* m, int backward) {
@@ -765,6 +842,33 @@ int rs_mat_export_tri(rs_matrix_t m, int which, int64_t* row_ptr, int64_t* col_i
   RS_CUDA(cudaDeviceSynchronize());
   return m->dtype == RS_F32 ? export_tri_t<float>(m, which, row_ptr, col_idx, values, dvalues)
                             : export_tri_t<double>(m, which, row_ptr, col_idx, values, dvalues);
+}
+
+int rs_mat_coloring(rs_matrix_t m, int64_t* color_out, int64_t* ncolors) {
+  if (!m) {
+    set_error(RS_ERR_ARG, "null matrix handle");
+    return RS_ERR_ARG;
+  }
+  RS_CUDA(cudaSetDevice(m->device));
+  int st = build_coloring(m);
+  if (st) return st;
+  if (color_out) memcpy(color_out, m->color, sizeof(int64_t) * m->nrows);
+  if (ncolors) *ncolors = m->mt.nlevels;
+  return RS_OK;
+}
+
+int rs_mat_set_coloring(rs_matrix_t m, const int64_t* color, int64_t ncolors) {
+  if (!m || !color || ncolors < 1) {
+    set_error(RS_ERR_ARG, "rs_mat_set_coloring: bad arguments");
+    return RS_ERR_ARG;
+  }
+  for (int64_t i = 0; i < m->nrows; ++i)
+    if (color[i] < 0 || color[i] >= ncolors) {
+      set_error(RS_ERR_ARG, "coloring: color out of range", i);
+      return RS_ERR_ARG;
+    }
+  RS_CUDA(cudaSetDevice(m->device));
+  return install_coloring(m, color, ncolors);
 }
 
 int rs_mat_export_diag(rs_matrix_t m, void* d) {

@@ -25,6 +25,7 @@
 namespace rs {
 
 int build_levels(rs_matrix* m, int backward);
+int build_coloring(rs_matrix* m);
 int wave_enabled();
 template <typename T>
 int wave_half_sweep(rs_matrix* m, const T* b, const T* xin, T* xout, int n_j, int backward, int form, double omega,
@@ -608,6 +609,34 @@ static int gs2_apply_t(rs_matrix* m, const T* b, T* x, const rs_relax_cfg& cfg, 
   return RS_OK;
 }
 
+// mt_gs_sweep (coloring.py:66-88): colors in order (reversed for backward), the rows
+// of a color in parallel; same-color rows are uncoupled, so reading x in place gives
+// new values for earlier colors and old values for later ones, as the sequential
+// visit of the concatenated color classes does.
+template <typename T>
+static int mt_gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omega, cudaStream_t st) {
+  int e;
+  if ((e = build_coloring(m))) return e;
+  Ctx<T> c(m, st);
+  T w = (T)omega, w1 = (T)(1.0 - omega);
+  const bool damped = w != (T)1.0;
+  Levels& lv = m->mt;
+  for (int half = 0; half < 2; ++half) {
+    const int bwd = half;
+    if (direction == RS_FORWARD && bwd) continue;
+    if (direction == RS_BACKWARD && !bwd) continue;
+    for (int64_t q = 0; q < lv.nlevels; ++q) {
+      const int64_t col = bwd ? lv.nlevels - 1 - q : q;
+      const int64_t lo = lv.level_ptr_host[col], cnt = lv.level_ptr_host[col + 1] - lo;
+      if (!cnt) continue;
+      k_gs_level<T><<<grid_for(cnt, kB), kB, 0, st>>>(cnt, lv.rows + lo, c.L, c.U, c.d, b, x, x, x, w, w1, damped);
+      RS_COUNT_LAUNCH();
+    }
+  }
+  RS_CHECK_LAUNCH("mt_gs_sweep");
+  return RS_OK;
+}
+
 // out-of-place single GS2 half-sweep / sweep set: x_out = GS2(x_in) (no copy-back)
 template <typename T>
 static int gs2_sweep_oop_t(rs_matrix* m, const T* b, const T* xin, T* xout, const rs_relax_cfg& cfg,
@@ -878,7 +907,7 @@ static bool single_half_sweep(int kind, const rs_relax_cfg& cfg) {
 template <typename T>
 static int precond_body(rs_matrix* m, int kind, rs_relax_cfg cfg, const T* rhs, T* z, cudaStream_t st) {
   int sweeps = cfg.n_t * cfg.n_k;
-  if (kind == RS_PC_SGS_SEQ || kind == RS_PC_SGS2) cfg.direction = RS_SYMMETRIC;  // krylov.py:86-87
+  if (kind == RS_PC_SGS_SEQ || kind == RS_PC_SGS2 || kind == RS_PC_MT_SGS) cfg.direction = RS_SYMMETRIC;
   switch (kind) {
     case RS_PC_JR:
       return jr_sweeps_t<T>(m, rhs, z, sweeps, cfg.omega, st, true);
@@ -894,6 +923,15 @@ static int precond_body(rs_matrix* m, int kind, rs_relax_cfg cfg, const T* rhs, 
     case RS_PC_GS2:
     case RS_PC_SGS2:
       return gs2_apply_t<T>(m, rhs, z, cfg, st, true);
+    case RS_PC_MT_GS:
+    case RS_PC_MT_SGS: {
+      RS_CUDA(cudaMemsetAsync(z, 0, sizeof(T) * m->nrows, st));
+      for (int s = 0; s < sweeps; ++s) {
+        int e = mt_gs_sweep_t<T>(m, rhs, z, cfg.direction, cfg.omega, st);
+        if (e) return e;
+      }
+      return RS_OK;
+    }
   }
   set_error(RS_ERR_ARG, "unknown preconditioner kind");
   return RS_ERR_ARG;
@@ -947,6 +985,17 @@ int rs_gs_sweep(rs_matrix_t m, const void* b, void* x, int direction, double ome
   cudaStream_t st = (cudaStream_t)stream;
   return m->dtype == RS_F32 ? gs_sweep_t<float>(m, (const float*)b, (float*)x, direction, omega, st)
                             : gs_sweep_t<double>(m, (const double*)b, (double*)x, direction, omega, st);
+}
+
+int rs_mt_gs_sweep(rs_matrix_t m, const void* b, void* x, int direction, double omega, rs_stream_t stream) {
+  RS_SET_DEVICE(m);
+  if (direction < 0 || direction > 2) {
+    set_error(RS_ERR_ARG, "direction must be forward, backward or symmetric");
+    return RS_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  return m->dtype == RS_F32 ? mt_gs_sweep_t<float>(m, (const float*)b, (float*)x, direction, omega, st)
+                            : mt_gs_sweep_t<double>(m, (const double*)b, (double*)x, direction, omega, st);
 }
 
 int rs_jr_sweeps(rs_matrix_t m, const void* b, void* x, int sweeps, double omega, rs_stream_t stream) {

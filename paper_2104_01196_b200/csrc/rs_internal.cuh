@@ -91,6 +91,8 @@ struct rs_matrix {
   int64_t halo_lo = 0;      // #halo entries below row0 (E_lo column space = [row0-halo_lo, row0))
   int64_t halo_hi = 0;      // #halo entries at/above row0+nrows
   rs::Levels fwd, bwd;      // lazily built
+  rs::Levels mt;            // multicolor GS: "levels" = colors, rows ascending within a color
+  int64_t* color = nullptr; // host, per-row color of the multicolor sweep
   void* scratch = nullptr;  // 3*nrows working dtype (rd, g ping/pong)
   void* scratch2 = nullptr; // 1*nrows (t)
   double* red = nullptr;    // reduction partials

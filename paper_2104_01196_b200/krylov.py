@@ -76,8 +76,6 @@ class Preconditioner:
             raise ValueError(f"unknown preconditioner kind {kind!r}; expected one of {PRECOND_KINDS}")
         if precision not in ("same", "single_inside_double"):
             raise ValueError(f"unknown precision mode {precision!r}")
-        if kind in _MT_KINDS:
-            raise ValueError(f"preconditioner kind {kind!r} (multicolor GS) is not on the GS2 path of this build")
         cfg = cfg if cfg is not None else RelaxConfig()
         if kind in _SYMMETRIC_DIRECTION_KINDS:
             cfg = replace(cfg, direction="symmetric")
@@ -94,6 +92,10 @@ class Preconditioner:
         if kind != "none":
             self.splitting = extract_splitting(a, cfg.omega, cfg.gamma)
             dm = as_device(a)
+            if kind in _MT_KINDS:
+                from .coloring import greedy_color
+
+                self.coloring = greedy_color(dm)
             if dm.dtype != np.float64:
                 raise ValueError("the preconditioner's matrix must be double precision")
             self._dev = dm.single() if precision == "single_inside_double" else dm

@@ -134,6 +134,16 @@ def sweep_fixtures():
                     x = x0.copy()
                     rs.gs_sequential_sweep(a, s, b, x, d)
                     put(out, f"{pre}__gs__{d}__w{om}", x)
+            # multicolor GS (coloring.py:66-88) on the reference's greedy coloring
+            col = rs.greedy_color(a)
+            if tag == "f64":
+                put(out, f"{name}__colors", col.color)
+            for om in (1.0, 1.3):
+                s = rs.extract_splitting(a, omega=om)
+                for d in ("forward", "backward", "symmetric"):
+                    x = x0.copy()
+                    rs.mt_gs_sweep(a, s, col, b, x, d)
+                    put(out, f"{pre}__mt__{d}__w{om}", x)
             # inner JR
             for om, gm in ((1.0, 1.0), (0.9, 0.6)):
                 s = rs.extract_splitting(a, omega=om, gamma=gm)
@@ -162,7 +172,7 @@ def sweep_fixtures():
                     rs.hybrid_relax(a, part, b, x, rs.RelaxConfig(2, 2, 1), local=local)
                     put(out, f"{pre}__hybrid__P{nb}__{local}", x)
         # preconditioner applications (r is float64; single_inside_double casts inside)
-        for kind in ("jr", "gs_seq", "sgs_seq", "gs2", "sgs2"):
+        for kind in ("jr", "gs_seq", "sgs_seq", "gs2", "sgs2", "mt_gs", "mt_sgs"):
             for prec in ("same", "single_inside_double"):
                 m = rs.Preconditioner(a64, kind, rs.RelaxConfig(2, 1, 1), precision=prec)
                 put(out, f"{name}__prec__{kind}__{prec}", m.apply(r64))
@@ -221,6 +231,8 @@ def gmres_fixtures(slow=False):
     run_gmres("lap3d_32__m60__gs_seq_1", a, b, P(a, "gs_seq", C(1, 1, 0)), 60, res)
     run_gmres("lap3d_32__m60__jr_2", a, b, P(a, "jr", C(2, 1, 0)), 60, res)
     run_gmres("lap3d_32__m60__sgs2_1_1_1", a, b, P(a, "sgs2", C(1, 1, 1)), 60, res)
+    run_gmres("lap3d_32__m60__mt_gs_1", a, b, P(a, "mt_gs", C(1, 1, 0)), 60, res)
+    run_gmres("lap3d_32__m60__mt_sgs_1", a, b, P(a, "mt_sgs", C(1, 1, 0)), 60, res)
     run_gmres("lap3d_32__m60__gs2_1_1_1__single", a, b, P(a, "gs2", C(1, 1, 1), precision="single_inside_double"), 60, res)
     for nparts in (1, 2, 4, 8):
         run_gmres(f"lap3d_32__m60__hybrid_gs2_1_1_1__P{nparts}", a, b, hybrid_precond(a, nparts, C(1, 1, 1)), 60, res)
@@ -389,6 +401,15 @@ def cg_fixtures():
     a = rs.elasticity3d(8)
     b = rs.random_rhs(a.nrows, 0)
     run("cg__ela3d_8__sgs2_1_1_3", a, b, P(a, "sgs2", C(1, 1, 3)))
+    # acceptance 08 ordering (test_acceptance.py:162-170): SGS <= SGS2 <= MT-SGS at n_x = 200
+    a = rs.laplace2d(200)
+    b = rs.random_rhs(a.nrows, 51)
+    run("cg__lap2d_200__sgs_seq", a, b, P(a, "sgs_seq", C(1, 1, 0)))
+    run("cg__lap2d_200__sgs2_1_1_1", a, b, P(a, "sgs2", C(1, 1, 1)))
+    run("cg__lap2d_200__mt_sgs", a, b, P(a, "mt_sgs", C(1, 1, 0)))
+    a = rs.laplace3d(32)
+    b = rs.random_rhs(a.nrows, 0)
+    run("cg__lap3d_32__mt_sgs", a, b, P(a, "mt_sgs", C(1, 1, 0)))
     return res
 
 

@@ -19,7 +19,7 @@ def _num(tok: str, prefix: str) -> float:
 def decode(key: str):
     parts = key.split("__")
     case = parts[0]
-    if len(parts) == 2 and parts[1] in INPUT_SUFFIXES:
+    if len(parts) == 2 and (parts[1] in INPUT_SUFFIXES or parts[1] == "colors"):
         return None
     if parts[1] == "prec":
         return dict(key=key, case=case, dtype="f64", op="prec", kind=parts[2], precision=parts[3])
@@ -30,7 +30,7 @@ def decode(key: str):
         pass
     elif op == "jr":
         d["omega"] = _num(rest[0], "w")
-    elif op == "gs":
+    elif op in ("gs", "mt"):
         d["direction"] = rest[0]
         d["omega"] = _num(rest[1], "w")
     elif op == "inner":

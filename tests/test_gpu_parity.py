@@ -58,6 +58,8 @@ def _run_gpu(c, golden):
         g2.jr_sweeps(a, s, b, x, 3)
     elif op == "gs":
         g2.gs_sequential_sweep(a, s, b, x, c["direction"])
+    elif op == "mt":
+        g2.mt_gs_sweep(a, s, g2.greedy_color(a), b, x, c["direction"])
     elif op == "inner":
         return g2.inner_jr_solve(s, r, c["n_j"], c["direction"])
     elif op == "gs2":
@@ -81,6 +83,41 @@ def test_bitwise_on_all_reference_fixtures(sweeps_golden):
         if got.dtype != want.dtype or got.shape != want.shape or not np.array_equal(got, want):
             bad.append(c["key"])
     assert not bad, f"{len(bad)}/{len(cases)} mismatches, first: {bad[:8]}"
+
+
+def test_greedy_color_matches_reference(sweeps_golden):
+    for k, want in sweeps_golden.items():
+        if k.endswith("__colors"):
+            case = k[: -len("__colors")]
+            col = g2.greedy_color(_matrix(sweeps_golden, case, "f64"))
+            assert np.array_equal(col.color, want), case
+            assert col.num_colors == want.max() + 1
+    # test_coloring.py cases
+    assert np.array_equal(g2.greedy_color(g2.from_dense([[2.0, -1.0], [-1.0, 2.0]])).color, [0, 1])
+    assert g2.greedy_color(g2.from_dense(np.diag([1.0, 2.0, 3.0]))).num_colors == 1
+    c = g2.greedy_color(g2.from_dense([[1.0, 1.0], [0.0, 1.0]]))
+    assert c.color[0] != c.color[1]
+
+
+def test_mt_sweep_invariant_under_intra_color_shuffle_and_custom_coloring():
+    rng = np.random.default_rng(3)
+    a = g2.laplace2d(9)
+    s = g2.extract_splitting(a)
+    b = g2.random_rhs(a.nrows, 1)
+    c = g2.greedy_color(a)
+    x1 = np.zeros(a.nrows)
+    g2.mt_gs_sweep(a, s, c, b, x1)
+    shuffled = g2.Coloring(c.color, c.num_colors, [rng.permutation(r) for r in c.rows_by_color])
+    x2 = np.zeros(a.nrows)
+    g2.mt_gs_sweep(a, s, shuffled, b, x2)
+    assert np.array_equal(x1, x2)
+    # n colors in natural order == sequential GS bitwise (coloring.py:76-78)
+    natural = g2.Coloring(np.arange(a.nrows), a.nrows, [np.array([i]) for i in range(a.nrows)])
+    x3 = np.zeros(a.nrows)
+    g2.mt_gs_sweep(a, s, natural, b, x3)
+    x4 = np.zeros(a.nrows)
+    g2.gs_sequential_sweep(a, s, b, x4)
+    assert np.array_equal(x3, x4)
 
 
 def test_a2_known_answers():

@@ -35,6 +35,8 @@ def _run_oracle(c, golden):
         oracle.jr_sweeps(a, b, x, 3, omega=c["omega"])
     elif op == "gs":
         oracle.gs_sweep(a, b, x, c["direction"], omega=c["omega"])
+    elif op == "mt":
+        oracle.mt_gs_sweep(a, b, x, c["direction"], omega=c["omega"])
     elif op == "inner":
         return oracle.inner_jr(a, r, c["n_j"], c["direction"], omega=c["omega"], gamma=c["gamma"])
     elif op == "gs2":
@@ -57,6 +59,16 @@ def test_oracle_bitwise_on_all_sweep_fixtures(sweeps_golden):
         if got.dtype != want.dtype or not np.array_equal(got, want):
             bad.append(c["key"])
     assert not bad, f"{len(bad)} mismatches, first: {bad[:5]}"
+
+
+def test_oracle_greedy_color_matches_reference(sweeps_golden):
+    for k, want in sweeps_golden.items():
+        if k.endswith("__colors"):
+            case = k[: -len("__colors")]
+            rp, ci, v, *_ = inputs(sweeps_golden, case, "f64")
+            color, nc = oracle.greedy_color(_Csr(rp, ci, v))
+            assert np.array_equal(color, want), case
+            assert nc == want.max() + 1
 
 
 def test_lcg_known_answers(generators_golden):
@@ -96,7 +108,8 @@ GMRES_FAST = [
     "lap2d_128__m30__gs2_2_1_1__single", "lap2d_128__m30__gs_seq_2__single",
     "lap3d_32__m60__gs2_1_1_0", "lap3d_32__m60__gs2_1_1_1", "lap3d_32__m60__gs2_1_1_2", "lap3d_32__m60__gs2_1_1_3",
     "lap3d_32__m60__gs_seq_1", "lap3d_32__m60__jr_2", "lap3d_32__m60__sgs2_1_1_1",
-    "lap3d_32__m60__gs2_1_1_1__single", "lap3d_32__m60__hybrid_gs2_1_1_1__P2",
+    "lap3d_32__m60__gs2_1_1_1__single", "lap3d_32__m60__hybrid_gs2_1_1_1__P2", "lap3d_32__m60__mt_gs_1",
+    "lap3d_32__m60__mt_sgs_1",
     "lap3d_32__m60__hybrid_gs2_1_1_1__P8",
 ]
 
@@ -117,6 +130,9 @@ def parse_gmres_label(label):
         nums = tuple(int(t) for t in toks[2:])
     elif toks[0] in ("gs", "sgs") and toks[1] == "seq":
         kind = toks[0] + "_seq"
+        nums = (int(toks[2]), 1, 0)
+    elif toks[0] == "mt":
+        kind = "mt_" + toks[1]
         nums = (int(toks[2]), 1, 0)
     elif toks[0] == "jr":
         kind = "jr"
@@ -173,7 +189,8 @@ def test_oracle_gmres_iteration_counts(label, gmres_golden):
     assert np.max(np.abs(hist - ref) / np.maximum(ref, 1e-300)) < 5e-2
 
 
-CG_LABELS = ["cg__lap2d_100__sgs_seq", "cg__lap2d_100__sgs2_1_1_1", "cg__lap2d_100__sgs2_1_1_2", "cg__lap2d_100__jr_1",
+CG_LABELS = ["cg__lap2d_200__sgs_seq", "cg__lap2d_200__sgs2_1_1_1", "cg__lap2d_200__mt_sgs", "cg__lap3d_32__mt_sgs",
+             "cg__lap2d_100__sgs_seq", "cg__lap2d_100__sgs2_1_1_1", "cg__lap2d_100__sgs2_1_1_2", "cg__lap2d_100__jr_1",
              "cg__lap2d_100__none", "cg__lap2d_100__sgs2_1_1_1__single", "cg__lap3d_32__sgs2_1_1_1",
              "cg__lap3d_32__sgs_seq", "cg__lap3d_32__sgs2_1_1_1__single", "cg__ela3d_8__sgs2_1_1_3"]
 
@@ -183,10 +200,12 @@ def parse_cg_label(label):
     parts = label.split("__")
     prob, spec = parts[1], parts[2]
     prec = "single_inside_double" if len(parts) > 3 and parts[3] == "single" else "same"
-    seed = 51 if prob == "lap2d_100" else 0
+    seed = 51 if prob in ("lap2d_100", "lap2d_200") else 0
     toks = spec.split("_")
     if spec == "none":
         return prob, seed, "none", (1, 1, 1), prec
+    if toks[0] == "mt":
+        return prob, seed, "mt_" + toks[1], (1, 1, 0), prec
     if toks[1] == "seq":
         return prob, seed, toks[0] + "_seq", (1, 1, 0), prec
     if toks[0] == "jr":
