@@ -314,14 +314,27 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
           int64_t n, int ch, int kCgsStages, int64_t rows_per_blk, const double* __restrict__ h_in,
           double* __restrict__ w, double* __restrict__ partial, int* nonfinite, double* __restrict__ h_out,
           double* __restrict__ nrm2_out, unsigned int* ticket) {
+  // Two warp groups ping-pong the chunks of this CTA's row range (group g takes
+  // chunks c = g, g+2, ...), each synchronising on its own named barrier, so one
+  // group's update / dots compute overlaps the other's; the TMA ring is shared.
+  constexpr int kGroups = 2;
+  constexpr int kGT = kCgsThreads / kGroups;  // threads per group
+  constexpr int kGW = kGT / 32;               // warps per group
+  constexpr int kQ = (kCgsMaxK + kGW - 1) / kGW;
   extern __shared__ __align__(128) unsigned char smraw[];
-  __shared__ double red[kCgsThreads];  // update-phase partial sums [split][row]
+  __shared__ double red[kCgsThreads];         // update-phase partial sums [group][split][row]
+  __shared__ double comb[kGroups][kCgsMaxK];  // per-group dot partials
+  // issue round of every ring stage: a group may only wait on chunk c after the TMA for
+  // chunk c was issued (round c / stages), otherwise mbarrier parity would alias to an
+  // older completed phase of that stage
+  __shared__ int s_issued[kCgsMaxStages];
   __shared__ bool s_last;
   const int stage_elems = (k + 1) * ch;
   double* st = reinterpret_cast<double*>(smraw);
   double* hs = st + (size_t)kCgsStages * stage_elems;
   uint64_t* bar = reinterpret_cast<uint64_t*>(hs + kCgsMaxK);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int grp = warp / kGW, gtid = tid % kGT, gwarp = warp % kGW;
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_blk;
   const int64_t r1 = n < r0 + rows_per_blk ? n : r0 + rows_per_blk;
   const int nchunks = r1 > r0 ? (int)((r1 - r0 + ch - 1) / ch) : 0;
@@ -329,9 +342,11 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     for (int i = tid; i < k; i += kCgsThreads) hs[i] = h_in[i];
   if (tid == 0) {
     for (int s = 0; s < kCgsStages; ++s) mbar_init(&bar[s], 1);
+    for (int s = 0; s < kCgsMaxStages; ++s) s_issued[s] = 0;
     fence_mbar_init();
   }
   __syncthreads();
+  auto group_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(kGT) : "memory"); };
   auto issue = [&](int c) {
     const int s = c % kCgsStages;
     const int64_t c0 = r0 + (int64_t)c * ch;
@@ -351,19 +366,24 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
       for (int i = 0; i < k; ++i) bulk_g2s(dst + (size_t)i * ch, V + (int64_t)i * ldv + c0, bytes, &bar[s]);
     }
     bulk_g2s(dst + (size_t)k * ch, w + c0, bytes, &bar[s]);
+    __threadfence_block();
+    *(volatile int*)&s_issued[s] = c / kCgsStages + 1;
   };
   if (tid == 0)
     for (int c = 0; c < kCgsStages && c < nchunks; ++c) issue(c);
-  // update-phase mapping: each row's basis sum is split over `nsplit` thread groups
-  const int nsplit = ch >= kCgsThreads ? 1 : kCgsThreads / ch;
-  const int urow = tid % ch, usplit = tid / ch;
-  double acc[kCgsMaxQ];
+  // update-phase mapping inside a group: each row's basis sum split over `nsplit` thread sets
+  const int nsplit = ch >= kGT ? 1 : kGT / ch;
+  const int urow = gtid % ch, usplit = gtid / ch;
+  double* gred = red + grp * kGT;
+  double acc[kQ];
 #pragma unroll
-  for (int q = 0; q < kCgsMaxQ; ++q) acc[q] = 0.0;
+  for (int q = 0; q < kQ; ++q) acc[q] = 0.0;
   double nrm = 0.0;
   bool bad = false;
-  for (int c = 0; c < nchunks; ++c) {
+  for (int c = grp; c < nchunks; c += kGroups) {
     const int s = c % kCgsStages;
+    while (*(volatile int*)&s_issued[s] < c / kCgsStages + 1) {
+    }
     mbar_wait(&bar[s], (uint32_t)((c / kCgsStages) & 1));
     const int64_t c0 = r0 + (int64_t)c * ch;
     const int len = (int)(r1 - c0 < ch ? r1 - c0 : ch);
@@ -379,15 +399,15 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
             s1 += hs[i + nsplit] * Vs[(size_t)(i + nsplit) * ch + urow];
           }
           if (i < k) s0 += hs[i] * Vs[(size_t)i * ch + urow];
-          red[usplit * ch + urow] = s0 + s1;
+          gred[usplit * ch + urow] = s0 + s1;
         }
-        __syncthreads();
+        group_sync();
       }
-      for (int r = tid; r < len; r += kCgsThreads) {
+      for (int r = gtid; r < len; r += kGT) {
         double sum;
         if (nsplit > 1) {
-          sum = red[r];
-          for (int v = 1; v < nsplit; ++v) sum += red[v * ch + r];
+          sum = gred[r];
+          for (int v = 1; v < nsplit; ++v) sum += gred[v * ch + r];
         } else {
           double s0 = 0.0, s1 = 0.0;
           int i = 0;
@@ -405,9 +425,9 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
         ws[r] = wv;
         if (NORM) nrm += wv * wv;
       }
-      __syncthreads();
+      group_sync();
     } else if (NORM || nonfinite) {
-      for (int r = tid; r < len; r += kCgsThreads) {
+      for (int r = gtid; r < len; r += kGT) {
         double wv = ws[r];
         if (nonfinite) bad |= !isfinite(wv);
         if (NORM) nrm += wv * wv;
@@ -415,7 +435,7 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     }
     if (DOTS) {
       if (ch <= 32 * kCgsMaxT) {
-        // lane owns rows lane + 32 t; w cached in registers; kCgsMaxQ independent chains
+        // lane owns rows lane + 32 t; w cached in registers; kQ independent chains
         double wr[kCgsMaxT];
 #pragma unroll
         for (int t = 0; t < kCgsMaxT; ++t) {
@@ -427,16 +447,16 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
           const int r = lane + 32 * t;
           if (r < ch) {
 #pragma unroll
-            for (int q = 0; q < kCgsMaxQ; ++q) {
-              const int i = warp + q * kCgsWarps;
+            for (int q = 0; q < kQ; ++q) {
+              const int i = gwarp + q * kGW;
               if (i < k) acc[q] += Vs[(size_t)i * ch + r] * wr[t];
             }
           }
         }
       } else {
 #pragma unroll
-        for (int q = 0; q < kCgsMaxQ; ++q) {
-          const int i = warp + q * kCgsWarps;
+        for (int q = 0; q < kQ; ++q) {
+          const int i = gwarp + q * kGW;
           if (i < k) {
             const double* vi = Vs + (size_t)i * ch;
             double a0 = 0.0, a1 = 0.0;
@@ -451,19 +471,21 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
         }
       }
     }
-    __syncthreads();
-    if (tid == 0 && c + kCgsStages < nchunks) issue(c + kCgsStages);
+    group_sync();
+    if (gtid == 0 && c + kCgsStages < nchunks) issue(c + kCgsStages);
   }
   const int stride = k + 1;
   if (DOTS) {
 #pragma unroll
-    for (int q = 0; q < kCgsMaxQ; ++q) {
-      const int i = warp + q * kCgsWarps;
+    for (int q = 0; q < kQ; ++q) {
+      const int i = gwarp + q * kGW;
       if (i < k) {
-        double v = warp_sum(acc[q]);
-        if (lane == 0) partial[(int64_t)blockIdx.x * stride + i] = v;
+        const double v = warp_sum(acc[q]);
+        if (lane == 0) comb[grp][i] = v;
       }
     }
+    __syncthreads();
+    for (int i = tid; i < k; i += kCgsThreads) partial[(int64_t)blockIdx.x * stride + i] = comb[0][i] + comb[1][i];
   }
   if (NORM) {
     nrm = warp_sum(nrm);
