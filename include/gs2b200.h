@@ -198,6 +198,13 @@ int rs_gemv_n_update(const double *V, int64_t ldv, int k, int64_t n, const doubl
 int rs_cgs_pass(const double *V, int64_t ldv, int k, int64_t n, const double *h_in, double *w, double *h_out,
                 double *nrm2, int *nonfinite, double *work, rs_stream_t stream);
 
+/* One modified Gram-Schmidt step of the reference's loop (krylov.py:217-219):
+ * if v_prev: w -= h_prev[0] * v_prev (product and difference rounded separately);
+ * then out[0] = v_cur . w, or w . w when v_cur is NULL (krylov.py:220).  One
+ * launch, deterministic in-kernel reduction (work as for rs_cgs_pass). */
+int rs_mgs_step(int64_t n, const double *v_prev, const double *h_prev, const double *v_cur, double *w, double *out,
+                double *work, rs_stream_t stream);
+
 /* out[r] = sum_{i<k} y[i] V_i[r]  (krylov.py:244 v[:j+1].T @ y) */
 int rs_gemv_n(const double *V, int64_t ldv, int k, int64_t n, const double *y, double *out, rs_stream_t stream);
 

@@ -73,6 +73,7 @@ _SIGS = {
     "rs_gemv_n_update": ([_P, _I64, C.c_int, _I64, _P, _P, _P, _P, _P], C.c_int),
     "rs_gemv_n": ([_P, _I64, C.c_int, _I64, _P, _P, _P], C.c_int),
     "rs_cgs_pass": ([_P, _I64, C.c_int, _I64, _P, _P, _P, _P, _P, _P, _P], C.c_int),
+    "rs_mgs_step": ([_I64, _P, _P, _P, _P, _P, _P, _P], C.c_int),
     "rs_scale_by_norm": ([_I64, _P, _P, _P, _P], C.c_int),
     "rs_sub_norm": ([_I64, _P, _P, _P, _P, _P, _P], C.c_int),
     "rs_dot": ([_I64, _P, _P, _P, _P, _P], C.c_int),

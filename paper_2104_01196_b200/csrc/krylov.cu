@@ -521,6 +521,50 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
   if (tid == 0) *ticket = 0;  // reset for the next launch (stream-ordered)
 }
 
+// One modified Gram-Schmidt step (krylov.py:217-219): w -= hprev[0] * v_prev (when
+// v_prev != NULL; product and difference rounded separately like the reference's
+// numpy `w -= h * v`), then out[0] = v_cur . w  (or w . w when v_cur == NULL).
+// Deterministic: per-CTA partials, the last CTA sums them in CTA order.
+__global__ void __launch_bounds__(256) k_mgs(int64_t n, const double* __restrict__ vprev,
+                                             const double* __restrict__ hprev, const double* __restrict__ vcur,
+                                             double* __restrict__ w, double* __restrict__ partial,
+                                             double* __restrict__ out, unsigned int* ticket) {
+  __shared__ double red[8];
+  __shared__ bool s_last;
+  const double h = vprev ? hprev[0] : 0.0;
+  double acc = 0.0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    double wv = w[r];
+    if (vprev) {
+      wv = __dsub_rn(wv, __dmul_rn(h, vprev[r]));
+      w[r] = wv;
+    }
+    acc += (vcur ? vcur[r] : wv) * wv;
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q];
+    partial[blockIdx.x] = t;
+    __threadfence();
+    s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x < 32) {
+    double a = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) a += __ldcg(partial + b);
+    a = warp_sum(a);
+    if (threadIdx.x == 0) {
+      out[0] = a;
+      *ticket = 0;
+    }
+  }
+}
+
 // out[j] = sum_b partial[b*stride + off + j] for j < cnt, b ascending
 __global__ void k_reduce_strided(const double* __restrict__ partial, int nblk, int stride, int off, int cnt,
                                  double* __restrict__ out) {
@@ -693,6 +737,20 @@ int rs_axpy1(int64_t n, const double* z, double* x, rs_stream_t stream) {
     RS_COUNT_LAUNCH();
   }
   RS_CHECK_LAUNCH("rs_axpy1");
+  return RS_OK;
+}
+
+int rs_mgs_step(int64_t n, const double* v_prev, const double* h_prev, const double* v_cur, double* w, double* out,
+                double* work, rs_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n < 0 || !work || !out || (v_prev && !h_prev)) {
+    set_error(RS_ERR_ARG, "rs_mgs_step: bad arguments");
+    return RS_ERR_ARG;
+  }
+  unsigned int* ticket = reinterpret_cast<unsigned int*>(work);
+  k_mgs<<<kRedBlocks, 256, 0, st>>>(n, v_prev, h_prev, v_cur, w, work + 1, out, ticket);
+  RS_COUNT_LAUNCH();
+  RS_CHECK_LAUNCH("rs_mgs_step");
   return RS_OK;
 }
 

@@ -255,8 +255,15 @@ def _p(t):
     return C.c_void_p(t.data_ptr())
 
 
-def gmres(a, b, m=None, restart: int = 60, tol: float = 1e-9, maxit: int = 10000, x0=None):
+def gmres(a, b, m=None, restart: int = 60, tol: float = 1e-9, maxit: int = 10000, x0=None, ortho: str = "cgs2"):
     """Restarted right-preconditioned GMRES(m) (krylov.py:162-250) on the GPU.
+
+    ``ortho="cgs2"`` (default, north_star item 4): classical Gram-Schmidt with
+    one re-orthogonalisation, three fused passes over the basis per step.
+    ``ortho="mgs"``: the reference's modified Gram-Schmidt loop
+    (krylov.py:217-219), one fused update+dot launch per basis vector -- the
+    reference-faithful mode (same iteration counts where the reference's are
+    dot-order stable), ~1.3x the basis traffic of CGS2.
 
     Returns ``(x, ConvergenceHistory)``; ``x`` is a numpy array when ``b`` is
     numpy, a CUDA tensor when ``b`` is a CUDA tensor.  History: the Arnoldi
@@ -284,8 +291,10 @@ def gmres(a, b, m=None, restart: int = 60, tol: float = 1e-9, maxit: int = 10000
     else:
         x = (x0.to(dev, torch.float64).clone() if _is_tensor(x0)
              else torch.from_numpy(np.array(x0, dtype=np.float64)).to(dev))
+    if ortho not in ("cgs2", "mgs"):
+        raise ValueError(f"ortho must be 'cgs2' or 'mgs', got {ortho!r}")
     op = _as_operator(m)
-    x, hist, conv = _gmres_device(dm, bt, x, op, restart, tol, maxit)
+    x, hist, conv = _gmres_device(dm, bt, x, op, restart, tol, maxit, ortho=ortho)
     if numpy_out:
         x = x.cpu().numpy()
     elif cpu_tensor_out:
@@ -310,7 +319,7 @@ def _apply_op(op, v, z, ws):
         z.copy_(out)
 
 
-def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None, reduce_fn=None):
+def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None, reduce_fn=None, ortho="cgs2"):
     """GMRES(m) on device vectors of the local rows of ``dm``.
 
     Single GPU by default.  The distributed solver passes ``spmv_fn(src, dst)``
@@ -388,20 +397,31 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
                 _apply_op(op, V[j], ws.z, ws)
             spmv(ws.z, ws.w)
             k = j + 1
-            # CGS2 (krylov.py:217-220 re-designed): h1 = V^T w ; w -= V h1 and h2 = V^T w in ONE
-            # pass over V ; w -= V h2 with ||w||^2 ; h = h1 + h2
             ldv = ws.ldv
-            with _timed("cgs_dots"):
-                chk(lib.rs_cgs_pass(_p(V), ldv, k, n, None, _p(ws.w), _p(h1), None, _p(ws.flags), _p(work), st),
-                    "cgs_pass")
-            reduce_(h1[:k])
-            with _timed("cgs_update_dots"):
-                chk(lib.rs_cgs_pass(_p(V), ldv, k, n, _p(h1), _p(ws.w), _p(h2), None, None, _p(work), st),
-                    "cgs_pass")
-            reduce_(h2[:k])
-            with _timed("cgs_update_norm"):
-                chk(lib.rs_cgs_pass(_p(V), ldv, k, n, _p(h2), _p(ws.w), None, _p(nrm2_slot), None, _p(work), st),
-                    "cgs_pass")
+            if ortho == "mgs" and reduce_fn is None:
+                # MGS (krylov.py:217-220): h_i = v_i . w ; w -= h_i v_i, one fused launch per i
+                h2.zero_()
+                with _timed("mgs"):
+                    for i in range(k + 1):
+                        vp = _p(V[i - 1]) if i > 0 else None
+                        hp = _p(h1[i - 1:i]) if i > 0 else None
+                        out = _p(h1[i:i + 1]) if i < k else _p(nrm2_slot)
+                        vc = _p(V[i]) if i < k else None
+                        chk(lib.rs_mgs_step(n, vp, hp, vc, _p(ws.w), out, _p(work), st), "mgs")
+            else:
+                # CGS2 (krylov.py:217-220 re-designed): h1 = V^T w ; w -= V h1 and h2 = V^T w in ONE
+                # pass over V ; w -= V h2 with ||w||^2 ; h = h1 + h2
+                with _timed("cgs_dots"):
+                    chk(lib.rs_cgs_pass(_p(V), ldv, k, n, None, _p(ws.w), _p(h1), None, _p(ws.flags), _p(work),
+                                        st), "cgs_pass")
+                reduce_(h1[:k])
+                with _timed("cgs_update_dots"):
+                    chk(lib.rs_cgs_pass(_p(V), ldv, k, n, _p(h1), _p(ws.w), _p(h2), None, None, _p(work), st),
+                        "cgs_pass")
+                reduce_(h2[:k])
+                with _timed("cgs_update_norm"):
+                    chk(lib.rs_cgs_pass(_p(V), ldv, k, n, _p(h2), _p(ws.w), None, _p(nrm2_slot), None, _p(work),
+                                        st), "cgs_pass")
             if reduce_fn is not None:
                 status[1] = (ws.flags[0] & 0xFFFFFFFF).to(torch.float64)
                 status[2] = (ws.flags[1] != _I64_MAX).to(torch.float64)

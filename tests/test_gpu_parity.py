@@ -465,3 +465,15 @@ def test_c3_elasticity_smoother_pattern(label, gmres_golden):
 
 
 _ELA16 = {}
+
+
+@pytest.mark.parametrize("label", ["lap2d_128__m30__gs2_2_1_1", "lap2d_128__m30__gs_seq_2", "lap3d_32__m60__gs2_1_1_1",
+                                   "lap3d_32__m60__sgs2_1_1_1", "lap3d_64__m60__gs2_1_1_1"])
+def test_gmres_mgs_mode_counts(label, gmres_golden):
+    """ortho='mgs' runs the reference's modified Gram-Schmidt loop on the GPU: same counts."""
+    want = gmres_golden["runs"][label]
+    prob, m, kind, cfg, prec, nb = parse_gmres_label(label)
+    a = golden_problem(prob) if not prob.startswith("lap3d_64") else g2.laplace3d(64, device="cuda")
+    b = g2.random_rhs(a.nrows, 0) if not prob.startswith("lap3d_64") else g2.random_rhs(a.nrows, 0, device="cuda")
+    _, h = g2.gmres(a, b, g2.Preconditioner(a, kind, g2.RelaxConfig(*cfg)), restart=m, tol=1e-9, ortho="mgs")
+    assert h.converged and h.iterations == want["iterations"]
