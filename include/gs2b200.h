@@ -34,6 +34,7 @@ extern "C" {
 #define RS_ERR_NONFINITE (-5) /* non-finite values (DivergenceError, krylov.py:157-159) */
 #define RS_ERR_SHAPE (-6)     /* dimension mismatch (sparse.py:172-176, relax.py:95-103) */
 #define RS_ERR_UNSUPPORTED (-7)
+#define RS_ERR_PARSE (-8)     /* malformed MatrixMarket entry; index = 1-based line number (mmio.py:69-94) */
 
 /* value dtypes (sparse.py:25 PRECISION_DTYPES) */
 #define RS_F64 0
@@ -236,6 +237,28 @@ int rs_lcg_fill(uint64_t seed, int64_t offset, int64_t n, double *out, rs_stream
 int rs_cast_f64_f32(int64_t n, const double *in, float *out, int64_t *overflow_flag /* INT64_MAX-initialised */,
                     rs_stream_t stream);
 int rs_cast_f32_f64(int64_t n, const float *in, double *out, rs_stream_t stream);
+
+/* ---- MatrixMarket input (mmio.py:27-106) ---- */
+
+/* Parse the entry section of a MatrixMarket coordinate file (the bytes after
+ * the size line; mmio.py:69-94) into 0-based COO triplets, multi-threaded on
+ * the host.  `first_line` = 1-based number of the first line in `buf`;
+ * `with_values` = 0 for the pattern field (values 1.0); `capacity` = length of
+ * rows / cols / vals (>= min(entries, declared)).  Entry k of the file lands at
+ * index k.  *count_out = entries stored, *last_line_out = number of the last
+ * line (the reference's len(lines)).  RS_ERR_PARSE: the first offending line
+ * (extra entry, token count, int()/float() syntax, index bounds) is
+ * rs_last_error_index().  nthreads <= 0: all hardware threads.  Host memory. */
+int rs_mm_parse_entries(const char *buf, int64_t len, int64_t first_line, int64_t declared, int with_values,
+                        int64_t nrows, int64_t ncols, int64_t capacity, int64_t *rows, int64_t *cols, double *vals,
+                        int64_t *count_out, int64_t *last_line_out, int nthreads);
+
+/* from_coo ordering (sparse.py:133-160): perm[nnz] = the stable (row, col)
+ * order of the triplets (== np.lexsort((cols, rows))) and row_ptr[nrows+1] =
+ * the row counts' prefix sum before duplicate merging.  Host memory; rows must
+ * lie in [0, nrows) (RS_ERR_ARG, index = entry). */
+int rs_coo_sort(int64_t nnz, int64_t nrows, const int64_t *rows, const int64_t *cols, int64_t *perm, int64_t *row_ptr,
+                int nthreads);
 
 #ifdef __cplusplus
 }

@@ -21,6 +21,7 @@ RS_ERR_OVERFLOW = -4
 RS_ERR_NONFINITE = -5
 RS_ERR_SHAPE = -6
 RS_ERR_UNSUPPORTED = -7
+RS_ERR_PARSE = -8
 
 RS_F64, RS_F32 = 0, 1
 DIRECTIONS = {"forward": 0, "backward": 1, "symmetric": 2}
@@ -83,6 +84,9 @@ _SIGS = {
     "rs_lcg_fill": ([C.c_uint64, _I64, _I64, _P, _P], C.c_int),
     "rs_cast_f64_f32": ([_I64, _P, _P, _P, _P], C.c_int),
     "rs_cast_f32_f64": ([_I64, _P, _P, _P], C.c_int),
+    "rs_mm_parse_entries": ([_P, _I64, _I64, _I64, C.c_int, _I64, _I64, _I64, _P, _P, _P, C.POINTER(_I64),
+                             C.POINTER(_I64), C.c_int], C.c_int),
+    "rs_coo_sort": ([_I64, _I64, _P, _P, _P, _P, C.c_int], C.c_int),
 }
 
 _lib = None

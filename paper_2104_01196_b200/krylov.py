@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import threading
 from dataclasses import dataclass, replace
 
 import numpy as np
@@ -229,7 +230,21 @@ class _timed:
 
 
 class _Workspace:
-    """Device buffers of one GMRES(m) solve (allocated once per solve)."""
+    """Device buffers of one GMRES(m) solve.  Kept per thread for the last (n, restart, device), so
+    back-to-back solves of the same size do not re-allocate the (m+1) x n basis; see release_workspace()."""
+
+    _tls = threading.local()
+
+    @classmethod
+    def get(cls, n: int, restart: int, device):
+        key = (n, restart, str(device))
+        ws = getattr(cls._tls, "ws", None)
+        if ws is None or ws.key != key:
+            cls._tls.ws = None  # free the old basis before allocating the new one
+            ws = cls(n, restart, device)
+            ws.key = key
+            cls._tls.ws = ws
+        return ws
 
     def __init__(self, n: int, restart: int, device):
         torch = _torch()
@@ -247,8 +262,8 @@ class _Workspace:
         self.scal = torch.zeros(2 * self.m1 + 4, **f64)
         self.flags = torch.zeros(2, dtype=torch.int64, device=device)  # [nonfinite(int32 in int64 slot), overflow]
         self.y = torch.empty(restart + 1, **f64)
-        self.pinned = torch.empty(2 * self.m1 + 4, dtype=torch.float64, pin_memory=True)
-        self.pinned_flags = torch.empty(2, dtype=torch.int64, pin_memory=True)
+        self.pinned = torch.empty((2, 2 * self.m1 + 4), dtype=torch.float64, pin_memory=True)
+        self.pinned_flags = torch.empty((2, 2), dtype=torch.int64, pin_memory=True)
 
 
 def _p(t):
@@ -295,11 +310,17 @@ def gmres(a, b, m=None, restart: int = 60, tol: float = 1e-9, maxit: int = 10000
         raise ValueError(f"ortho must be 'cgs2' or 'mgs', got {ortho!r}")
     op = _as_operator(m)
     x, hist, conv = _gmres_device(dm, bt, x, op, restart, tol, maxit, ortho=ortho)
-    if numpy_out:
-        x = x.cpu().numpy()
-    elif cpu_tensor_out:
-        x = x.cpu()
+    if numpy_out or cpu_tensor_out:
+        # D2H through page-locked memory (torch's caching host allocator): DMA-speed read-back
+        host = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        host.copy_(x)
+        x = host.numpy() if numpy_out else host
     return x, ConvergenceHistory(np.array(hist), conv)
+
+
+def release_workspace() -> None:
+    """Free this thread's cached GMRES basis (the next solve re-allocates it)."""
+    _Workspace._tls.ws = None
 
 
 def _apply_op(op, v, z, ws):
@@ -331,7 +352,7 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
     lib = N.load()
     n = dm.nrows
     st = stream_ptr(dm.device_index)
-    ws = _Workspace(n, restart, dm.torch_device)
+    ws = _Workspace.get(n, restart, dm.torch_device)
     m1 = ws.m1
     scal, work = ws.scal, ws.work
     nrm2_slot = scal[2 * m1:2 * m1 + 1]
@@ -379,6 +400,52 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
     converged = False
     breakdown_tol = BREAKDOWN_RTOL * bnorm
     V = ws.V
+    ldv = ws.ldv
+
+    def enqueue_step(jj):
+        """GPU work of Arnoldi step jj (z = M v_jj, w = A z, orthogonalise, v_jj+1 = w/||w||), then an
+        async copy of its scalars into pinned slot jj % 2; returns the completion event."""
+        with _timed("precond"):
+            _apply_op(op, V[jj], ws.z, ws)
+        spmv(ws.z, ws.w)
+        k = jj + 1
+        if ortho == "mgs" and reduce_fn is None:
+            # MGS (krylov.py:217-220): h_i = v_i . w ; w -= h_i v_i, one fused launch per i
+            h2.zero_()
+            with _timed("mgs"):
+                for i in range(k + 1):
+                    vp = _p(V[i - 1]) if i > 0 else None
+                    hp = _p(h1[i - 1:i]) if i > 0 else None
+                    out = _p(h1[i:i + 1]) if i < k else _p(nrm2_slot)
+                    vc = _p(V[i]) if i < k else None
+                    chk(lib.rs_mgs_step(n, vp, hp, vc, _p(ws.w), out, _p(work), st), "mgs")
+        else:
+            # CGS2 (krylov.py:217-220 re-designed): h1 = V^T w ; w -= V h1 and h2 = V^T w in ONE
+            # pass over V ; w -= V h2 with ||w||^2 ; h = h1 + h2
+            with _timed("cgs_dots"):
+                chk(lib.rs_cgs_pass(_p(V), ldv, k, n, None, _p(ws.w), _p(h1), None, _p(ws.flags), _p(work), st),
+                    "cgs_pass")
+            reduce_(h1[:k])
+            with _timed("cgs_update_dots"):
+                chk(lib.rs_cgs_pass(_p(V), ldv, k, n, _p(h1), _p(ws.w), _p(h2), None, None, _p(work), st),
+                    "cgs_pass")
+            reduce_(h2[:k])
+            with _timed("cgs_update_norm"):
+                chk(lib.rs_cgs_pass(_p(V), ldv, k, n, _p(h2), _p(ws.w), None, _p(nrm2_slot), None, _p(work), st),
+                    "cgs_pass")
+        if reduce_fn is not None:
+            status[1] = (ws.flags[0] & 0xFFFFFFFF).to(torch.float64)
+            status[2] = (ws.flags[1] != _I64_MAX).to(torch.float64)
+            reduce_(status)
+        with _timed("scale"):
+            chk(lib.rs_scale_by_norm(n, _p(ws.w), _p(nrm2_slot), _p(V[jj + 1]), st), "scale")
+        slot = jj % 2
+        ws.pinned[slot].copy_(scal, non_blocking=True)
+        ws.pinned_flags[slot].copy_(ws.flags, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        return ev
+
     while total < maxit and not converged:
         beta = rnorm
         h = np.zeros((restart + 1, restart))
@@ -390,51 +457,26 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
         g[0] = beta
         j = -1
         lucky = False
-        while j + 1 < restart and total < maxit:
+        # Software pipeline: step j+1 is enqueued before the host waits for step j's scalars, so
+        # the host-side Givens update (exactly the reference's numpy arithmetic) overlaps GPU
+        # work.  A speculative step past convergence is discarded (its results are never read).
+        ev_next = enqueue_step(0)
+        speculated = False
+        while True:
             j += 1
             total += 1
-            with _timed("precond"):
-                _apply_op(op, V[j], ws.z, ws)
-            spmv(ws.z, ws.w)
-            k = j + 1
-            ldv = ws.ldv
-            if ortho == "mgs" and reduce_fn is None:
-                # MGS (krylov.py:217-220): h_i = v_i . w ; w -= h_i v_i, one fused launch per i
-                h2.zero_()
-                with _timed("mgs"):
-                    for i in range(k + 1):
-                        vp = _p(V[i - 1]) if i > 0 else None
-                        hp = _p(h1[i - 1:i]) if i > 0 else None
-                        out = _p(h1[i:i + 1]) if i < k else _p(nrm2_slot)
-                        vc = _p(V[i]) if i < k else None
-                        chk(lib.rs_mgs_step(n, vp, hp, vc, _p(ws.w), out, _p(work), st), "mgs")
-            else:
-                # CGS2 (krylov.py:217-220 re-designed): h1 = V^T w ; w -= V h1 and h2 = V^T w in ONE
-                # pass over V ; w -= V h2 with ||w||^2 ; h = h1 + h2
-                with _timed("cgs_dots"):
-                    chk(lib.rs_cgs_pass(_p(V), ldv, k, n, None, _p(ws.w), _p(h1), None, _p(ws.flags), _p(work),
-                                        st), "cgs_pass")
-                reduce_(h1[:k])
-                with _timed("cgs_update_dots"):
-                    chk(lib.rs_cgs_pass(_p(V), ldv, k, n, _p(h1), _p(ws.w), _p(h2), None, None, _p(work), st),
-                        "cgs_pass")
-                reduce_(h2[:k])
-                with _timed("cgs_update_norm"):
-                    chk(lib.rs_cgs_pass(_p(V), ldv, k, n, _p(h2), _p(ws.w), None, _p(nrm2_slot), None, _p(work),
-                                        st), "cgs_pass")
-            if reduce_fn is not None:
-                status[1] = (ws.flags[0] & 0xFFFFFFFF).to(torch.float64)
-                status[2] = (ws.flags[1] != _I64_MAX).to(torch.float64)
-                reduce_(status)
-            with _timed("scale"):
-                chk(lib.rs_scale_by_norm(n, _p(ws.w), _p(nrm2_slot), _p(V[j + 1]), st), "scale")
-            ws.pinned.copy_(scal)  # synchronises the stream: one D2H per Arnoldi step
-            ws.pinned_flags.copy_(ws.flags)
-            hv = ws.pinned.numpy()
-            if (ws.pinned_flags[0].item() & 0xFFFFFFFF) or hv[2 * m1 + 1] > 0:
+            ev = ev_next
+            ev_next = None
+            if j + 1 < restart and total < maxit:
+                ev_next = enqueue_step(j + 1)
+            ev.synchronize()
+            hv = ws.pinned[j % 2].numpy()
+            fl = ws.pinned_flags[j % 2]
+            if (int(fl[0]) & 0xFFFFFFFF) or hv[2 * m1 + 1] > 0:
                 raise DivergenceError(f"non-finite values encountered in Arnoldi iteration {total}")
-            if int(ws.pinned_flags[1].item()) != _I64_MAX or hv[2 * m1 + 2] > 0:
-                check_overflow()
+            if int(fl[1]) != _I64_MAX or hv[2 * m1 + 2] > 0:
+                raise OverflowError(f"an entry overflows single precision (Arnoldi iteration {total})")
+            k = j + 1
             h[:k, j] = hv[0:k] + hv[m1:m1 + k]
             h[j + 1, j] = math.sqrt(hv[2 * m1])
             lucky = h[j + 1, j] < breakdown_tol
@@ -453,8 +495,14 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
             if not np.isfinite(est):
                 raise DivergenceError(f"residual estimate became non-finite at iteration {total}")
             hist.append(est)
-            if est <= tol or lucky:
+            if est <= tol or lucky or ev_next is None:
+                speculated = ev_next is not None
                 break
+        if speculated:
+            # the discarded speculative step may have raised device flags; clear them
+            ws.flags.zero_()
+            ws.flags[1] = _I64_MAX
+            status[1:3].zero_()
         # least squares + update (krylov.py:241-244)
         y = np.zeros(j + 1)
         for i in range(j, -1, -1):

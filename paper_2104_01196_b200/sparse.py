@@ -468,7 +468,13 @@ def from_coo(nrows, ncols, rows, cols, vals, dtype=None) -> CsrMatrix:
             raise ValueError("row index out of range")
         if cols.min() < 0 or cols.max() >= ncols:
             raise ValueError("column index out of range")
-    perm = np.lexsort((cols, rows))
+    # the stable (row, col) order of np.lexsort((cols, rows)), by the library's threaded host sort
+    rows = np.ascontiguousarray(rows)
+    cols = np.ascontiguousarray(cols)
+    perm = np.empty(rows.size, dtype=np.int64)
+    counts = np.empty(int(nrows) + 1, dtype=np.int64)
+    N.check(N.load().rs_coo_sort(rows.size, int(nrows), rows.ctypes.data, cols.ctypes.data, perm.ctypes.data,
+                                 counts.ctypes.data, 0), "from_coo")
     rows, cols, vals = rows[perm], cols[perm], vals[perm]
     if rows.size:
         head = np.empty(rows.size, dtype=bool)
