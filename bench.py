@@ -8,7 +8,9 @@ synthetic 3D 7-point Laplace problem, right-hand side random_rhs(n, 0):
 
 * N = 1: config C2, laplace3d 256^3 (16.7 M rows) on one B200.
 * N > 1: config C5, laplace3d 512^3 row-partitioned into N z-slabs (one rank
-  per GPU; hybrid block-Jacobi GS2 preconditioner, NCCL halo + allreduce).
+  per GPU; hybrid block-Jacobi GS2 preconditioner; halo exchange and the
+  Gram-Schmidt allreduces over NVLink peer memory, the allreduces fused into
+  the CGS kernels -- ``--comm nccl`` for the NCCL baseline).
 
 ``value`` = algorithmic HBM GB/s of the cycle (SURVEY.md §8(d) byte model:
 split-CSR int32 + fp64 per pass, summed over every kernel of the cycle and
@@ -388,6 +390,8 @@ def main():
     p.add_argument("--no-tts", action="store_true")
     p.add_argument("--tts", action="store_true", help="also time a full solve at N > 1 (off by default)")
     p.add_argument("--no-sweeps", action="store_true")
+    p.add_argument("--comm", default="peer", choices=["peer", "nccl"],
+                   help="N > 1 collectives: NVLink peer-memory kernels (default) or NCCL")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-iters", type=int, default=8)
     p.add_argument("--ref-iters", type=int, default=3)

@@ -238,6 +238,53 @@ int rs_cast_f64_f32(int64_t n, const double *in, float *out, int64_t *overflow_f
                     rs_stream_t stream);
 int rs_cast_f32_f64(int64_t n, const float *in, double *out, rs_stream_t stream);
 
+/* ---- multi-GPU: NVLink peer-memory collectives ----
+ *
+ * Replaces the reference's distributed halo exchange / dot allreduce seam
+ * (hybrid_relax's coupling rounds, relax.py:259-269, and the GMRES dots,
+ * krylov.py:217-220, once rows are split over ranks) with one mailbox per rank
+ * in device memory, mapped into every peer process by CUDA IPC.  Protocol and
+ * layout: paper_2104_01196_b200/csrc/peer.cuh.  Every collective carries an
+ * epoch: a per-communicator counter starting at 1 that all ranks advance
+ * identically (one per collective call).  Results are identical on all ranks
+ * (rank-order sums).  A peer that never arrives makes the waiting kernel give
+ * up after 20 s and set an error flag (rs_peer_error) instead of hanging. */
+#define RS_IPC_HANDLE_BYTES 64
+typedef struct rs_peer rs_peer;
+
+/* allocate this rank's mailbox: reduce payload capacity `rcap` doubles, halo
+ * buffers of halo_lo / halo_hi entries (double-buffered by epoch parity) */
+int rs_peer_create(int rank, int nranks, int64_t rcap, int64_t halo_lo, int64_t halo_hi, rs_peer **out);
+/* RS_IPC_HANDLE_BYTES bytes naming this rank's mailbox for the other processes */
+int rs_peer_ipc_handle(rs_peer *p, void *handle);
+/* map the peers' mailboxes: handles = nranks * RS_IPC_HANDLE_BYTES bytes in rank order */
+int rs_peer_connect(rs_peer *p, const void *handles);
+/* same, for ranks that are threads of one process (peers = all ranks' handles) */
+int rs_peer_connect_local(rs_peer *p, rs_peer *const *peers);
+/* halo plan: nseg segments of 5 int64 {peer, src_off, len, dst_word, parity_stride}: my local
+ * entries x[src_off, +len) go to word dst_word (+ parity * parity_stride) of peer's mailbox;
+ * src[nsrc] = the ranks I receive from */
+int rs_peer_set_halo(rs_peer *p, int nseg, const int64_t *seg, int nsrc, const int32_t *src);
+/* word offset of the halo buffers in every mailbox and the mailbox size in words */
+int rs_peer_layout(rs_peer *p, int64_t *off_halo, int64_t *words);
+/* this rank's halo buffers of one parity (NULL for an empty side): the xlo / xhi of rs_spmv */
+int rs_peer_halo(rs_peer *p, int parity, double **lo, double **hi);
+/* push my boundary entries of x into the peers' halo buffers (NVLink stores) and wait for
+ * mine; after it completes in stream order, rs_peer_halo(p, epoch & 1) holds the halo */
+int rs_halo_exchange(rs_peer *p, const double *x, uint64_t epoch, rs_stream_t stream);
+/* a[0..n) = sum over ranks (in place); with flags ([nonfinite, overflow] as in
+ * rs_cgs_pass), status_out[0..1] = #ranks with a non-finite / overflow flag */
+int rs_peer_allreduce(rs_peer *p, double *a, int n, const int64_t *flags, double *status_out, uint64_t epoch,
+                      rs_stream_t stream);
+/* rs_cgs_pass with the allreduce of its outputs (h_out, nrm2 and the optional
+ * status from flags) fused into the kernel's final reduction: one collective */
+int rs_cgs_pass_peer(const double *V, int64_t ldv, int k, int64_t n, const double *h_in, double *w, double *h_out,
+                     double *nrm2, int *nonfinite, double *work, rs_peer *peer, uint64_t epoch,
+                     const int64_t *flags, double *status_out, rs_stream_t stream);
+/* *timed_out = 1 if a wait of this rank gave up (synchronous) */
+int rs_peer_error(rs_peer *p, int *timed_out);
+int rs_peer_destroy(rs_peer *p);
+
 /* ---- MatrixMarket input (mmio.py:27-106) ---- */
 
 /* Parse the entry section of a MatrixMarket coordinate file (the bytes after

@@ -87,7 +87,20 @@ _SIGS = {
     "rs_mm_parse_entries": ([_P, _I64, _I64, _I64, C.c_int, _I64, _I64, _I64, _P, _P, _P, C.POINTER(_I64),
                              C.POINTER(_I64), C.c_int], C.c_int),
     "rs_coo_sort": ([_I64, _I64, _P, _P, _P, _P, C.c_int], C.c_int),
+    "rs_peer_create": ([C.c_int, C.c_int, _I64, _I64, _I64, C.POINTER(_P)], C.c_int),
+    "rs_peer_ipc_handle": ([_P, _P], C.c_int),
+    "rs_peer_connect": ([_P, _P], C.c_int),
+    "rs_peer_connect_local": ([_P, _P], C.c_int),
+    "rs_peer_set_halo": ([_P, C.c_int, _P, C.c_int, _P], C.c_int),
+    "rs_peer_layout": ([_P, C.POINTER(_I64), C.POINTER(_I64)], C.c_int),
+    "rs_peer_halo": ([_P, C.c_int, C.POINTER(_P), C.POINTER(_P)], C.c_int),
+    "rs_halo_exchange": ([_P, _P, C.c_uint64, _P], C.c_int),
+    "rs_peer_allreduce": ([_P, _P, C.c_int, _P, _P, C.c_uint64, _P], C.c_int),
+    "rs_cgs_pass_peer": ([_P, _I64, C.c_int, _I64, _P, _P, _P, _P, _P, _P, _P, C.c_uint64, _P, _P, _P], C.c_int),
+    "rs_peer_error": ([_P, C.POINTER(C.c_int)], C.c_int),
+    "rs_peer_destroy": ([_P], C.c_int),
 }
+RS_IPC_HANDLE_BYTES = 64
 
 _lib = None
 _lock = threading.Lock()

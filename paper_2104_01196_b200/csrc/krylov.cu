@@ -12,6 +12,7 @@
 #include <cstring>
 #include <mutex>
 
+#include "peer.cuh"
 #include "rs_internal.cuh"
 
 namespace rs {
@@ -313,7 +314,8 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     k_cgs(const __grid_constant__ CUtensorMap tmap, int use_tmap, const double* __restrict__ V, int64_t ldv, int k,
           int64_t n, int ch, int kCgsStages, int64_t rows_per_blk, const double* __restrict__ h_in,
           double* __restrict__ w, double* __restrict__ partial, int* nonfinite, double* __restrict__ h_out,
-          double* __restrict__ nrm2_out, unsigned int* ticket) {
+          double* __restrict__ nrm2_out, unsigned int* ticket, const PeerArgs pa, const int64_t* flags_in,
+          double* status_out) {
   // Two warp groups ping-pong the chunks of this CTA's row range (group g takes
   // chunks c = g, g+2, ...), each synchronising on its own named barrier, so one
   // group's update / dots compute overlaps the other's; the TMA ring is shared.
@@ -508,14 +510,38 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
   if (!s_last) return;
   __threadfence();
   const int nout = (DOTS ? k : 0) + (NORM ? 1 : 0);
+  double* s_pay = comb[0];  // the dot partials are consumed; reuse as the allreduce payload
   for (int o = warp; o < nout; o += kCgsWarps) {
     const int col = DOTS ? (o < k ? o : k) : k;
     double a = 0.0;
     for (int bb = lane; bb < (int)gridDim.x; bb += 32) a += __ldcg(partial + (int64_t)bb * stride + col);
     a = warp_sum(a);
     if (lane == 0) {
-      if (DOTS && o < k) h_out[o] = a;
+      if (pa.boxes) s_pay[o] = a;
+      else if (DOTS && o < k) h_out[o] = a;
       else nrm2_out[0] = a;
+    }
+  }
+  if (pa.boxes) {
+    // multi-GPU: the sum over ranks happens here, through NVLink peer memory (peer.cuh),
+    // instead of a separate NCCL allreduce launch after this kernel
+    int cnt = nout;
+    if (flags_in) {
+      if (tid == 0) {
+        s_pay[nout] = (flags_in[0] & 0xffffffffll) != 0 ? 1.0 : 0.0;
+        s_pay[nout + 1] = flags_in[1] != INT64_MAX ? 1.0 : 0.0;
+      }
+      cnt += 2;
+    }
+    __syncthreads();
+    peer_allreduce_cta(pa, s_pay, cnt);
+    for (int o = tid; o < nout; o += kCgsThreads) {
+      if (DOTS && o < k) h_out[o] = s_pay[o];
+      else nrm2_out[0] = s_pay[o];
+    }
+    if (flags_in && tid == 0) {
+      status_out[0] = s_pay[nout];
+      status_out[1] = s_pay[nout + 1];
     }
   }
   if (tid == 0) *ticket = 0;  // reset for the next launch (stream-ordered)
@@ -632,22 +658,27 @@ int rs_gemv_n_update(const double* V, int64_t ldv, int k, int64_t n, const doubl
 }
 
 
-int rs_cgs_pass(const double* V, int64_t ldv, int k, int64_t n, const double* h_in, double* w, double* h_out,
-                double* nrm2, int* nonfinite, double* work, rs_stream_t stream) {
-  cudaStream_t st = (cudaStream_t)stream;
-  if (k < 1 || n < 0 || !work || (!h_out && !nrm2 && !h_in)) {
-    set_error(RS_ERR_ARG, "rs_cgs_pass: bad arguments");
-    return RS_ERR_ARG;
-  }
+static int cgs_pass(const double* V, int64_t ldv, int k, int64_t n, const double* h_in, double* w, double* h_out,
+                    double* nrm2, int* nonfinite, double* work, cudaStream_t st, const rs_peer* peer, uint64_t epoch,
+                    const int64_t* flags_in, double* status_out) {
+  rs_stream_t stream = (rs_stream_t)st;
   const bool aligned = (ldv % 2 == 0) && (n % 2 == 0) && ((uintptr_t)V % 16 == 0) && ((uintptr_t)w % 16 == 0);
   if (k > kCgsMaxK || !aligned) {
-    // generic path: separate update / dots / norm kernels
+    // generic path: separate update / dots / norm kernels (+ one peer allreduce launch)
     int e;
     if (h_in && (e = rs_gemv_n_update(V, ldv, k, n, h_in, w, h_out ? nullptr : nrm2, work, stream))) return e;
     if (h_out && (e = rs_gemv_t(V, ldv, k, n, w, h_out, nonfinite, work, stream))) return e;
     if (h_out && nrm2 && (e = rs_dot(n, w, w, nrm2, work, stream))) return e;
     if (!h_in && !h_out && nrm2 && (e = rs_dot(n, w, w, nrm2, work, stream))) return e;
+    if (peer && (e = peer_allreduce_launch(peer, epoch, h_out, h_out ? k : 0, nrm2, nrm2 ? 1 : 0, flags_in,
+                                           status_out, st)))
+      return e;
     return RS_OK;
+  }
+  const PeerArgs pa = peer_args(peer, epoch);
+  if (peer && (h_out ? k : 0) + (nrm2 ? 1 : 0) + (flags_in ? 2 : 0) > std::min<int64_t>(peer->rcap, 2 * kCgsMaxK)) {
+    set_error(RS_ERR_ARG, "rs_cgs_pass_peer: payload exceeds the mailbox capacity");
+    return RS_ERR_ARG;
   }
   const int ch = cgs_chunk_rows(k);
   const int stages = cgs_stages(k, ch);
@@ -672,7 +703,8 @@ int rs_cgs_pass(const double* V, int64_t ldv, int k, int64_t n, const double* h_
   do {                                                                                                   \
     cudaFuncSetAttribute(k_cgs<u, d, nm>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
     k_cgs<u, d, nm><<<nblk, kCgsThreads, smem, st>>>(tmap, use_tmap, V, ldv, k, n, ch, stages, rows, h_in, w, \
-                                                     work, nonfinite, h_out, nrm2, ticket);               \
+                                                     work, nonfinite, h_out, nrm2, ticket, pa, flags_in,  \
+                                                     status_out);                                         \
     RS_COUNT_LAUNCH();                                                                                   \
   } while (0)
   if (U && D && Nm) RS_CGS_LAUNCH(true, true, true);
@@ -685,6 +717,27 @@ int rs_cgs_pass(const double* V, int64_t ldv, int k, int64_t n, const double* h_
 #undef RS_CGS_LAUNCH
   RS_CHECK_LAUNCH("rs_cgs_pass");
   return RS_OK;
+}
+
+int rs_cgs_pass(const double* V, int64_t ldv, int k, int64_t n, const double* h_in, double* w, double* h_out,
+                double* nrm2, int* nonfinite, double* work, rs_stream_t stream) {
+  if (k < 1 || n < 0 || !work || (!h_out && !nrm2 && !h_in)) {
+    set_error(RS_ERR_ARG, "rs_cgs_pass: bad arguments");
+    return RS_ERR_ARG;
+  }
+  return cgs_pass(V, ldv, k, n, h_in, w, h_out, nrm2, nonfinite, work, (cudaStream_t)stream, nullptr, 0, nullptr,
+                  nullptr);
+}
+
+int rs_cgs_pass_peer(const double* V, int64_t ldv, int k, int64_t n, const double* h_in, double* w, double* h_out,
+                     double* nrm2, int* nonfinite, double* work, rs_peer* peer, uint64_t epoch,
+                     const int64_t* flags, double* status_out, rs_stream_t stream) {
+  if (k < 1 || n < 0 || !work || !peer || epoch == 0 || (!h_out && !nrm2) || (flags && (!nrm2 || !status_out))) {
+    set_error(RS_ERR_ARG, "rs_cgs_pass_peer: bad arguments");
+    return RS_ERR_ARG;
+  }
+  return cgs_pass(V, ldv, k, n, h_in, w, h_out, nrm2, nonfinite, work, (cudaStream_t)stream, peer, epoch, flags,
+                  status_out);
 }
 
 int rs_gemv_n(const double* V, int64_t ldv, int k, int64_t n, const double* y, double* out, rs_stream_t stream) {

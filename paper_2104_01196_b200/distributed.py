@@ -95,6 +95,88 @@ class TorchComm(Comm):
         self.dist.barrier(group=self.group)
 
 
+class PeerComm(TorchComm):
+    """TorchComm whose data-path collectives run over NVLink peer memory (csrc/peer.cu).
+
+    The process group (NCCL or gloo) is only used at setup (exchanging the CUDA
+    IPC handles of the mailboxes, barriers).  A DistMatrix built on a PeerComm
+    owns a ``PeerMailbox``: its halo exchange is one push-and-wait kernel over
+    NVLink instead of an NCCL send/recv group, and the GMRES reductions run
+    inside the CGS kernels (rs_cgs_pass_peer) instead of separate NCCL
+    allreduce launches.
+    """
+
+    peer = True
+
+
+class PeerMailbox:
+    """This rank's mailbox (rs_peer) plus the epoch counters of its two collective kinds."""
+
+    def __init__(self, comm: Comm, halo_lo: int, halo_hi: int, rcap: int = 256, local_group=None):
+        lib = N.load()
+        self._lib = lib
+        self.comm = comm
+        self.rcap = int(rcap)
+        h = C.c_void_p()
+        N.check(lib.rs_peer_create(comm.rank, comm.size, self.rcap, int(halo_lo), int(halo_hi), C.byref(h)), "peer")
+        self.handle = h
+        if local_group is not None:  # ranks are threads of this process: share raw pointers
+            allh = comm.allgather_obj(h.value)
+            arr = (C.c_void_p * comm.size)(*allh)
+            N.check(lib.rs_peer_connect_local(h, arr), "peer connect")
+        else:
+            buf = C.create_string_buffer(N.RS_IPC_HANDLE_BYTES)
+            N.check(lib.rs_peer_ipc_handle(h, buf), "peer ipc handle")
+            allh = comm.allgather_obj(buf.raw)
+            joined = b"".join(allh)
+            N.check(lib.rs_peer_connect(h, C.c_char_p(joined)), "peer connect")
+        off, words = C.c_int64(), C.c_int64()
+        N.check(lib.rs_peer_layout(h, C.byref(off), C.byref(words)), "peer layout")
+        self.off_halo = int(off.value)
+        self.r_epoch = 0
+        self.h_epoch = 0
+        self._closed = False
+
+    def next_reduce_epoch(self) -> int:
+        self.r_epoch += 1
+        return self.r_epoch
+
+    def set_halo(self, segs, srcs):
+        seg = np.ascontiguousarray(np.asarray(segs, dtype=np.int64).reshape(-1, 5))
+        src = np.ascontiguousarray(np.asarray(srcs, dtype=np.int32))
+        N.check(self._lib.rs_peer_set_halo(self.handle, len(seg), seg.ctypes.data if len(seg) else None,
+                                           len(src), src.ctypes.data if len(src) else None), "peer halo plan")
+
+    def exchange(self, x, stream):
+        """Push my boundary entries of x, wait for my halo; returns the (lo, hi) halo pointers."""
+        self.h_epoch += 1
+        N.check(self._lib.rs_halo_exchange(self.handle, _p(x), self.h_epoch, stream), "halo exchange")
+        lo, hi = C.c_void_p(), C.c_void_p()
+        N.check(self._lib.rs_peer_halo(self.handle, self.h_epoch & 1, C.byref(lo), C.byref(hi)), "peer halo")
+        return lo, hi
+
+    def allreduce_(self, t):
+        """In-place sum over ranks of a float64 device tensor (one-CTA peer-memory kernel)."""
+        st = C.c_void_p(_torch().cuda.current_stream().cuda_stream)
+        N.check(self._lib.rs_peer_allreduce(self.handle, _p(t), t.numel(), None, None, self.next_reduce_epoch(), st),
+                "peer allreduce")
+
+    def check(self):
+        bad = C.c_int(0)
+        N.check(self._lib.rs_peer_error(self.handle, C.byref(bad)), "peer error")
+        if bad.value:
+            raise RuntimeError("a peer-memory collective timed out (a rank stopped participating)")
+
+    def close(self):
+        """Collective: wait for every rank, then unmap and free the mailbox."""
+        if self._closed:
+            return
+        _torch().cuda.synchronize()
+        self.comm.barrier()
+        self._lib.rs_peer_destroy(self.handle)
+        self._closed = True
+
+
 class _ThreadShared:
     def __init__(self, size):
         self.size = size
@@ -219,6 +301,30 @@ class DistMatrix:
         self.xlo = torch.empty(max(dm.halo_lo, 1), **f)
         self.xhi = torch.empty(max(dm.halo_hi, 1), **f)
         self._lib = N.load()
+        self.mailbox = None
+        if getattr(comm, "peer", False):
+            self.mailbox = PeerMailbox(comm, dm.halo_lo, dm.halo_hi, local_group=getattr(comm, "local_group", None))
+            segs, srcs = self.peer_segments(comm.rank, blocks, self.mailbox.off_halo)
+            self.mailbox.set_halo(segs, srcs)
+
+    @staticmethod
+    def peer_segments(rank: int, blocks: list, off_halo: int):
+        """Halo push segments {peer, src_off, len, dst_word, parity_stride} and the ranks I receive from.
+
+        What q reads from my rows lands in q's mailbox: its low halo [qlo - qhl, qlo) at words
+        off_halo + [0, qhl), its high halo [qhi, qhi + qhh) at off_halo + qhl + [0, qhh); the
+        second parity buffer follows at + (qhl + qhh)."""
+        lo, hi, _, _ = blocks[rank]
+        segs = []
+        for q, (qlo, qhi, qhl, qhh) in enumerate(blocks):
+            if q == rank:
+                continue
+            for a, b, base in ((qlo - qhl, qlo, off_halo), (qhi, qhi + qhh, off_halo + qhl)):
+                s0, e0 = max(a, lo), min(b, hi)
+                if s0 < e0:
+                    segs.append((q, s0 - lo, e0 - s0, base + (s0 - a), qhl + qhh))
+        srcs = sorted({peer for peer, _, _, _ in HaloPlan.build(rank, blocks).recv})
+        return segs, srcs
 
     @property
     def nrows(self):
@@ -245,18 +351,34 @@ class DistMatrix:
         return cls(dm, comm, a.nrows, offs)
 
     def exchange(self, x):
-        """Fill xlo / xhi with the neighbour entries of the local vector x (one grouped send/recv)."""
+        """Gather the neighbour entries of the local vector x; returns the (xlo, xhi) halo pointers.
+
+        PeerComm: one push-and-wait kernel over NVLink into double-buffered mailbox halos.
+        Otherwise: one grouped NCCL / gloo send/recv into xlo / xhi."""
+        if self.mailbox is not None:
+            return self.mailbox.exchange(x, C.c_void_p(_torch().cuda.current_stream().cuda_stream))
         sends = [(peer, x[s:e]) for peer, s, e in self.plan.send]
         recvs = [(peer, (self.xlo if which == "lo" else self.xhi)[s:e]) for peer, which, s, e in self.plan.recv]
         self.comm.exchange(sends, recvs)
+        return (_p(self.xlo) if self.dm.halo_lo else None), (_p(self.xhi) if self.dm.halo_hi else None)
 
     def spmv(self, x, y):
         """y = (A x) for the local rows: halo exchange, then E_lo | L | D | U | E_hi row sums."""
-        self.exchange(x)
+        xlo, xhi = self.exchange(x)
         st = C.c_void_p(_torch().cuda.current_stream().cuda_stream)
-        xlo = _p(self.xlo) if self.dm.halo_lo else None
-        xhi = _p(self.xhi) if self.dm.halo_hi else None
         N.check(self._lib.rs_spmv(self.dm.handle, _p(x), xlo, xhi, _p(y), st), "spmv")
+
+    def allreduce_(self, t):
+        """In-place sum over ranks (peer-memory kernel on a PeerComm, else the comm's allreduce)."""
+        if self.mailbox is not None:
+            self.mailbox.allreduce_(t)
+        else:
+            self.comm.allreduce_sum_(t)
+
+    def close(self):
+        if self.mailbox is not None:
+            self.mailbox.close()
+            self.mailbox = None
 
 
 class HybridPreconditioner:
@@ -299,9 +421,7 @@ class HybridPreconditioner:
         N.check(lib.rs_precond_apply(self.dm.handle, kind, C.byref(c), _p(r), _p(z), fp, st), "precond")
         A = self.A
         for _ in range(cfg.n_t - 1):
-            A.exchange(z)
-            xlo = _p(A.xlo) if A.dm.halo_lo else None
-            xhi = _p(A.xhi) if A.dm.halo_hi else None
+            xlo, xhi = A.exchange(z)
             N.check(lib.rs_hybrid_bhat(A.dm.handle, _p(r), _p(z), xlo, xhi, _p(self._bhat), st), "bhat")
             if self.local == "gs2":
                 N.check(lib.rs_gs2_apply(A.dm.handle, _p(self._bhat), _p(z), C.byref(c), st), "gs2")
@@ -323,7 +443,10 @@ def gmres(A: DistMatrix, b_local, m: HybridPreconditioner | None = None, restart
     dev = dm.torch_device
     b = b_local.to(dev, torch.float64) if b_local.device != dev else b_local
     x = torch.zeros(dm.nrows, dtype=torch.float64, device=dev) if x0_local is None else x0_local.clone()
-    x, hist, conv = _gmres_device(dm, b, x, m, restart, tol, maxit, spmv_fn=A.spmv, reduce_fn=A.comm.allreduce_sum_)
+    x, hist, conv = _gmres_device(dm, b, x, m, restart, tol, maxit, spmv_fn=A.spmv, reduce_fn=A.allreduce_,
+                                  peer=A.mailbox)
+    if A.mailbox is not None:
+        A.mailbox.check()
     return x, ConvergenceHistory(np.array(hist), conv)
 
 
@@ -345,7 +468,8 @@ def bench_rank(args, metric, Model, laplace3d_nnz, ClockSampler, peaks):
     import torch
     import torch.distributed as dist
 
-    comm = TorchComm()
+    use_peer = getattr(args, "comm", "peer") == "peer"
+    comm = PeerComm() if use_peer else TorchComm()
     rank, world = comm.rank, comm.size
     local = torch.cuda.current_device()
     lib = N.load()
@@ -403,7 +527,9 @@ def bench_rank(args, metric, Model, laplace3d_nnz, ClockSampler, peaks):
             "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"C5: laplace3d {nx}^3 ({n} rows) in {world} z-slabs, one GMRES({m}) cycle, "
-                                   f"hybrid block-Jacobi GS2(1,1,1) preconditioner, NCCL halo + allreduce",
+                                   f"hybrid block-Jacobi GS2(1,1,1) preconditioner, "
+                                   + ("halo + allreduce over NVLink peer memory (fused into the CGS kernels)"
+                                      if use_peer else "NCCL halo + allreduce"),
                        "bytes_per_step": cycle_bytes, "ms_per_iteration": round(ms / m, 4),
                        "l2": "inputs larger than L2", "parallelism": f"{world} ranks x 1 GPU (row blocks)"},
             "roofline": {"bound": "hbm", "kernel": "whole cycle (per GPU)",
@@ -416,6 +542,7 @@ def bench_rank(args, metric, Model, laplace3d_nnz, ClockSampler, peaks):
             "gpu_launches": int(launches), "clocks": clk.summary(), "tts": tts,
         }
         print(json.dumps(line), flush=True)
+    A.close()
     dist.barrier()
     dist.destroy_process_group()
     return 0

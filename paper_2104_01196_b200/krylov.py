@@ -340,13 +340,17 @@ def _apply_op(op, v, z, ws):
         z.copy_(out)
 
 
-def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None, reduce_fn=None, ortho="cgs2"):
+def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None, reduce_fn=None, ortho="cgs2",
+                  peer=None):
     """GMRES(m) on device vectors of the local rows of ``dm``.
 
     Single GPU by default.  The distributed solver passes ``spmv_fn(src, dst)``
     (halo exchange + local SpMV) and ``reduce_fn(tensor)`` (in-place sum over
     ranks); every dot / norm below is a local partial followed by reduce_fn,
     so all ranks see bitwise identical scalars and take the same decisions.
+    ``peer`` (a distributed.PeerMailbox) moves the three per-step reductions
+    into the CGS kernels themselves (rs_cgs_pass_peer: NVLink peer-memory
+    allreduce in the kernel's final reduction).
     """
     torch = _torch()
     lib = N.load()
@@ -419,6 +423,18 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
                     out = _p(h1[i:i + 1]) if i < k else _p(nrm2_slot)
                     vc = _p(V[i]) if i < k else None
                     chk(lib.rs_mgs_step(n, vp, hp, vc, _p(ws.w), out, _p(work), st), "mgs")
+        elif peer is not None:
+            # CGS2 with the sum over ranks fused into each pass (one collective per pass, no extra launch)
+            ph = peer.handle
+            with _timed("cgs_dots"):
+                chk(lib.rs_cgs_pass_peer(_p(V), ldv, k, n, None, _p(ws.w), _p(h1), None, _p(ws.flags), _p(work), ph,
+                                         peer.next_reduce_epoch(), None, None, st), "cgs_pass")
+            with _timed("cgs_update_dots"):
+                chk(lib.rs_cgs_pass_peer(_p(V), ldv, k, n, _p(h1), _p(ws.w), _p(h2), None, None, _p(work), ph,
+                                         peer.next_reduce_epoch(), None, None, st), "cgs_pass")
+            with _timed("cgs_update_norm"):
+                chk(lib.rs_cgs_pass_peer(_p(V), ldv, k, n, _p(h2), _p(ws.w), None, _p(nrm2_slot), None, _p(work), ph,
+                                         peer.next_reduce_epoch(), _p(ws.flags), _p(status[1:3]), st), "cgs_pass")
         else:
             # CGS2 (krylov.py:217-220 re-designed): h1 = V^T w ; w -= V h1 and h2 = V^T w in ONE
             # pass over V ; w -= V h2 with ||w||^2 ; h = h1 + h2
@@ -433,7 +449,7 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
             with _timed("cgs_update_norm"):
                 chk(lib.rs_cgs_pass(_p(V), ldv, k, n, _p(h2), _p(ws.w), None, _p(nrm2_slot), None, _p(work), st),
                     "cgs_pass")
-        if reduce_fn is not None:
+        if reduce_fn is not None and peer is None:
             status[1] = (ws.flags[0] & 0xFFFFFFFF).to(torch.float64)
             status[2] = (ws.flags[1] != _I64_MAX).to(torch.float64)
             reduce_(status)
