@@ -302,6 +302,8 @@ def ours(args):
 
     # e2e through the public API with host buffers: pinned b in, x out
     b_host = b.cpu().pin_memory()
+    for _ in range(args.warmup):  # untimed: first-touch of the pinned output staging
+        g2.gmres(a, b_host, pc, restart=m, tol=1e-300, maxit=m)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(args.steps):
