@@ -9,6 +9,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -263,7 +264,15 @@ constexpr int kCgsBlocks = 148;
 // regardless of size (measured: k = 61 with 1 KB row copies reached 2.1 TB/s).
 constexpr int kCgsTmapMinK = 8;
 
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
 static int cgs_chunk_rows(int k) {
+  // tuning override (profiles/cgs_tune.py): RS_CGS_CH = rows per chunk for the tensor-map path
+  const int force = env_int("RS_CGS_CH", 0);
+  if (force > 0 && k > kCgsTmapMinK) return std::max(32, std::min(256, force) & ~31);
   int ch = kCgsStageBytes / (8 * (k + 1));
   // measured: 64-row boxes (512 B rows) halve the TMA throughput; keep rows >= 1 KB
   if (k > kCgsTmapMinK) return std::max(128, std::min(256, ch) & ~31);
@@ -275,7 +284,8 @@ static int cgs_chunk_rows(int k) {
 // while a chunk's update / dots phases run)
 static int cgs_stages(int k, int ch) {
   const size_t stage = (size_t)(k + 1) * ch * sizeof(double);
-  return (int)std::max<size_t>(2, std::min<size_t>(kCgsMaxStages, kCgsSmemBudget / stage));
+  const size_t budget = (size_t)env_int("RS_CGS_SMEM_KB", kCgsSmemBudget / 1024) * 1024;
+  return (int)std::max<size_t>(2, std::min<size_t>(kCgsMaxStages, std::min<size_t>(budget, 220 * 1024) / stage));
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
@@ -303,6 +313,33 @@ static bool encode_basis_map(CUtensorMap* map, const double* V, int64_t ldv, int
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+// 3-D view of the basis for small k: (256 rows, n/256 row blocks, k vectors).  A box of
+// (256, ch/256, k) lands in shared memory as [k][ch] -- the same tile layout as the 2-D map --
+// but with up to 1024 rows per chunk (the 2-D box is limited to 256 rows), so small-k passes
+// move >= 32 KB per TMA copy instead of paying the per-chunk overheads 2-4x as often.
+static bool encode_basis_map3(CUtensorMap* map, const double* V, int64_t ldv, int k, int64_t n, int ch) {
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {256, (cuuint64_t)(n / 256), (cuuint64_t)k};
+  cuuint64_t strides[2] = {256 * sizeof(double), (cuuint64_t)ldv * sizeof(double)};
+  cuuint32_t box[3] = {256, (cuuint32_t)(ch / 256), (cuuint32_t)k};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(V), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// rows per chunk of the 3-D path (multiple of 256), 0 = use the 2-D path
+static int cgs_chunk_rows3(int k, int64_t n) {
+  if (k <= kCgsTmapMinK || n % 256 != 0 || !env_int("RS_CGS_3D", 1)) return 0;
+  const int force = env_int("RS_CGS_CH3", 0);
+  int ch = force > 0 ? force : (kCgsStageBytes / (8 * (k + 1))) & ~255;
+  ch = std::min(1024, ch & ~255);
+  if (ch <= 256 && force <= 0) return 0;  // the 2-D box already covers it
+  return ch >= 256 ? ch : 0;
 }
 
 static size_t cgs_smem_bytes(int k, int ch, int stages) {
@@ -355,7 +392,15 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     const int len = (int)(r1 - c0 < ch ? r1 - c0 : ch);
     const uint32_t bytes = (uint32_t)len * 8u;
     double* dst = st + (size_t)s * stage_elems;
-    if (use_tmap) {
+    if (use_tmap == 2) {
+      // one 3-D tensor copy: (256 rows) x (ch/256 row blocks) x (k vectors) -> [k][ch]
+      mbar_expect_tx(&bar[s], (uint32_t)k * (uint32_t)ch * 8u + bytes);
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+          "[%5];" ::"r"(smem_u32(dst)),
+          "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(0), "r"((int)(c0 >> 8)), "r"(0), "r"(smem_u32(&bar[s]))
+          : "memory");
+    } else if (use_tmap) {
       // one 2-D tensor copy brings the whole k x ch tile (OOB columns zero-filled)
       mbar_expect_tx(&bar[s], (uint32_t)k * (uint32_t)ch * 8u + bytes);
       asm volatile(
@@ -680,13 +725,20 @@ static int cgs_pass(const double* V, int64_t ldv, int k, int64_t n, const double
     set_error(RS_ERR_ARG, "rs_cgs_pass_peer: payload exceeds the mailbox capacity");
     return RS_ERR_ARG;
   }
-  const int ch = cgs_chunk_rows(k);
+  const int ch3 = cgs_chunk_rows3(k, n);
+  const int ch = ch3 ? ch3 : cgs_chunk_rows(k);
   const int stages = cgs_stages(k, ch);
   const size_t smem = cgs_smem_bytes(k, ch, stages);
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
   int use_tmap = 0;
-  if (k > kCgsTmapMinK) {
+  if (ch3) {
+    if (!encode_basis_map3(&tmap, V, ldv, k, n, ch)) {
+      set_error(RS_ERR_CUDA, "cuTensorMapEncodeTiled (3-D) failed for the Arnoldi basis");
+      return RS_ERR_CUDA;
+    }
+    use_tmap = 2;
+  } else if (k > kCgsTmapMinK) {
     if (!encode_basis_map(&tmap, V, ldv, k, n, ch)) {
       set_error(RS_ERR_CUDA, "cuTensorMapEncodeTiled failed for the Arnoldi basis");
       return RS_ERR_CUDA;

@@ -28,7 +28,9 @@ def p(t):
 
 
 def timeit(fn, reps=10):
-    fn()
+    st = fn()
+    if isinstance(st, int):
+        _native.check(st, "microbench")
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
