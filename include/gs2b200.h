@@ -238,6 +238,32 @@ int rs_cast_f64_f32(int64_t n, const double *in, float *out, int64_t *overflow_f
                     rs_stream_t stream);
 int rs_cast_f32_f64(int64_t n, const float *in, double *out, rs_stream_t stream);
 
+/* ---- DCGS2: classical Gram-Schmidt with DELAYED re-orthogonalisation ----
+ *
+ * The same projections as CGS2 (krylov.py:217-220 re-designed; exact-arithmetic
+ * equal, same iteration counts in tests) in TWO passes over the basis per
+ * Arnoldi step instead of three: the re-orthogonalisation of v_j is folded into
+ * step j's first pass.  Step j with k = j+1 basis rows, u = row j
+ * (once-orthogonalised, tentative), w = A M u:
+ *   rs_dcgs2_dots   out[0,k) = V^T w, out[k,2k) = V^T u        (one pass)
+ *   rs_dcgs2_coef   finalises Hessenberg column j-1 and the tentative column j in
+ *                   H (raw, column-major, ldh rows), fills the coefficient block
+ *                   coef (2*64+2 doubles)                       (one thread)
+ *   rs_dcgs2_update row j <- v_j = (u - Q s)/rho, row j+1 <- u' = (w - Q a - gamma v_j)/rho,
+ *                   nrm2 = ||u'||^2                             (one pass)
+ * With last = 1, rs_dcgs2_coef only finalises column k-2 from out = V^T u (k values,
+ * e.g. rs_cgs_pass dots with w = row k-1).  peer != NULL: the sums over ranks run
+ * inside the passes (see rs_cgs_pass_peer; flags -> status_out in the update).
+ * k <= 64, n even, 16-byte aligned rows. */
+typedef struct rs_peer rs_peer;
+int rs_dcgs2_dots(const double *V, int64_t ldv, int k, int64_t n, const double *w, double *out, int *nonfinite,
+                  double *work, rs_peer *peer, uint64_t epoch, rs_stream_t stream);
+int rs_dcgs2_coef(int k, const double *dots, double *H, int ldh, double *coef, const double *nrm2_prev, int last,
+                  rs_stream_t stream);
+int rs_dcgs2_update(const double *V, int64_t ldv, int k, int64_t n, const double *coef, const double *w,
+                    double *vrow, double *urow, double *nrm2, double *work, rs_peer *peer, uint64_t epoch,
+                    const int64_t *flags, double *status_out, rs_stream_t stream);
+
 /* ---- multi-GPU: NVLink peer-memory collectives ----
  *
  * Replaces the reference's distributed halo exchange / dot allreduce seam
@@ -250,7 +276,6 @@ int rs_cast_f32_f64(int64_t n, const float *in, double *out, rs_stream_t stream)
  * (rank-order sums).  A peer that never arrives makes the waiting kernel give
  * up after 20 s and set an error flag (rs_peer_error) instead of hanging. */
 #define RS_IPC_HANDLE_BYTES 64
-typedef struct rs_peer rs_peer;
 
 /* allocate this rank's mailbox: reduce payload capacity `rcap` doubles, halo
  * buffers of halo_lo / halo_hi entries (double-buffered by epoch parity) */

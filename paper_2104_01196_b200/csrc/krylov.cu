@@ -342,17 +342,29 @@ static int cgs_chunk_rows3(int k, int64_t n) {
   return ch >= 256 ? ch : 0;
 }
 
+// coefficient block of a DCGS2 update pass (see rs_dcgs2_*): s at [0, k-1), a at
+// [kDcgsA, kDcgsA + k-1), 1/rho at kDcgsRho, gamma at kDcgsRho + 1
+constexpr int kDcgsA = kCgsMaxK;
+constexpr int kDcgsRho = 2 * kCgsMaxK;
+constexpr int kDcgsCoef = 2 * kCgsMaxK + 2;
+
 static size_t cgs_smem_bytes(int k, int ch, int stages) {
-  return (size_t)stages * (k + 1) * ch * sizeof(double) + kCgsMaxK * sizeof(double) + kCgsMaxStages * 8 + 16;
+  return (size_t)stages * (k + 1) * ch * sizeof(double) + kDcgsCoef * sizeof(double) + kCgsMaxStages * 8 + 16;
 }
 
-template <bool UPDATE, bool DOTS, bool NORM>
+// DCGS (delayed classical Gram-Schmidt with re-orthogonalisation, rs_dcgs2_*):
+//  DOTS  : dual dots of the tile against w AND against its last basis row u:
+//          h_out[0, k) = V^T w, h_out[k, 2k) = V^T u (one collective of 2k values)
+//  UPDATE: with Q = rows [0, k-1), u = row k-1, coefficients (s, a, 1/rho, gamma):
+//          v = (u - Q s) / rho -> vrow,  u' = (w - Q a - gamma v) / rho -> urow
+//          (+ NORM: ||u'||^2)
+template <bool UPDATE, bool DOTS, bool NORM, bool DCGS = false>
 __global__ void __launch_bounds__(kCgsThreads, 1)
     k_cgs(const __grid_constant__ CUtensorMap tmap, int use_tmap, const double* __restrict__ V, int64_t ldv, int k,
           int64_t n, int ch, int kCgsStages, int64_t rows_per_blk, const double* __restrict__ h_in,
           double* __restrict__ w, double* __restrict__ partial, int* nonfinite, double* __restrict__ h_out,
           double* __restrict__ nrm2_out, unsigned int* ticket, const PeerArgs pa, const int64_t* flags_in,
-          double* status_out) {
+          double* status_out, double* __restrict__ vout, double* __restrict__ uout) {
   // Two warp groups ping-pong the chunks of this CTA's row range (group g takes
   // chunks c = g, g+2, ...), each synchronising on its own named barrier, so one
   // group's update / dots compute overlaps the other's; the TMA ring is shared.
@@ -362,7 +374,8 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
   constexpr int kQ = (kCgsMaxK + kGW - 1) / kGW;
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ double red[kCgsThreads];         // update-phase partial sums [group][split][row]
-  __shared__ double comb[kGroups][kCgsMaxK];  // per-group dot partials
+  __shared__ double comb[kGroups][2 * kCgsMaxK + 4];  // per-group dot partials (+ allreduce payload)
+  __shared__ double red2[(DCGS && UPDATE) ? kCgsThreads : 1];  // second update sum of a DCGS pass
   // issue round of every ring stage: a group may only wait on chunk c after the TMA for
   // chunk c was issued (round c / stages), otherwise mbarrier parity would alias to an
   // older completed phase of that stage
@@ -371,14 +384,16 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
   const int stage_elems = (k + 1) * ch;
   double* st = reinterpret_cast<double*>(smraw);
   double* hs = st + (size_t)kCgsStages * stage_elems;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(hs + kCgsMaxK);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(hs + kDcgsCoef);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int grp = warp / kGW, gtid = tid % kGT, gwarp = warp % kGW;
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_blk;
   const int64_t r1 = n < r0 + rows_per_blk ? n : r0 + rows_per_blk;
   const int nchunks = r1 > r0 ? (int)((r1 - r0 + ch - 1) / ch) : 0;
-  if (UPDATE)
+  if (UPDATE && !DCGS)
     for (int i = tid; i < k; i += kCgsThreads) hs[i] = h_in[i];
+  if (UPDATE && DCGS)
+    for (int i = tid; i < kDcgsCoef; i += kCgsThreads) hs[i] = h_in[i];
   if (tid == 0) {
     for (int s = 0; s < kCgsStages; ++s) mbar_init(&bar[s], 1);
     for (int s = 0; s < kCgsMaxStages; ++s) s_issued[s] = 0;
@@ -422,9 +437,12 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
   const int nsplit = ch >= kGT ? 1 : kGT / ch;
   const int urow = gtid % ch, usplit = gtid / ch;
   double* gred = red + grp * kGT;
-  double acc[kQ];
+  double* gred2 = red2 + ((DCGS && UPDATE) ? grp * kGT : 0);
+  double acc[kQ], acc2[DCGS ? kQ : 1];
 #pragma unroll
   for (int q = 0; q < kQ; ++q) acc[q] = 0.0;
+#pragma unroll
+  for (int q = 0; q < (DCGS ? kQ : 1); ++q) acc2[q] = 0.0;
   double nrm = 0.0;
   bool bad = false;
   for (int c = grp; c < nchunks; c += kGroups) {
@@ -436,7 +454,62 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     const int len = (int)(r1 - c0 < ch ? r1 - c0 : ch);
     const double* Vs = st + (size_t)s * stage_elems;
     double* ws = st + (size_t)s * stage_elems + (size_t)k * ch;
-    if (UPDATE) {
+    if (UPDATE && DCGS) {
+      // v = (u - Q s) / rho, u' = (w - Q a - gamma v) / rho over the Q rows [0, k-1)
+      const int kq = k - 1;
+      const double* ha = hs + kDcgsA;
+      const double irho = hs[kDcgsRho], gam = hs[kDcgsRho + 1];
+      if (nsplit > 1) {
+        if (usplit < nsplit && urow < len) {
+          double s0 = 0.0, s1 = 0.0;
+          for (int i = usplit; i < kq; i += nsplit) {
+            const double q = Vs[(size_t)i * ch + urow];
+            s0 += hs[i] * q;
+            s1 += ha[i] * q;
+          }
+          gred[usplit * ch + urow] = s0;
+          gred2[usplit * ch + urow] = s1;
+        }
+        group_sync();
+      }
+      for (int r = gtid; r < len; r += kGT) {
+        double sq, sa;
+        if (nsplit > 1) {
+          sq = gred[r];
+          sa = gred2[r];
+          for (int v = 1; v < nsplit; ++v) {
+            sq += gred[v * ch + r];
+            sa += gred2[v * ch + r];
+          }
+        } else {
+          double q0 = 0.0, q1 = 0.0, a0 = 0.0, a1 = 0.0;
+          int i = 0;
+          for (; i + 1 < kq; i += 2) {
+            const double x0 = Vs[(size_t)i * ch + r], x1 = Vs[(size_t)(i + 1) * ch + r];
+            q0 += hs[i] * x0;
+            a0 += ha[i] * x0;
+            q1 += hs[i + 1] * x1;
+            a1 += ha[i + 1] * x1;
+          }
+          if (i < kq) {
+            const double x0 = Vs[(size_t)i * ch + r];
+            q0 += hs[i] * x0;
+            a0 += ha[i] * x0;
+          }
+          sq = q0 + q1;
+          sa = a0 + a1;
+        }
+        const double u = Vs[(size_t)kq * ch + r];
+        const double wv = ws[r];
+        if (nonfinite) bad |= !isfinite(wv);
+        const double v = (u - sq) * irho;
+        const double up = (wv - sa - gam * v) * irho;
+        vout[c0 + r] = v;
+        uout[c0 + r] = up;
+        if (NORM) nrm += up * up;
+      }
+      group_sync();
+    } else if (UPDATE) {
       if (nsplit > 1) {
         if (usplit < nsplit && urow < len) {
           double s0 = 0.0, s1 = 0.0;
@@ -480,7 +553,25 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
         if (NORM) nrm += wv * wv;
       }
     }
-    if (DOTS) {
+    if (DOTS && DCGS) {
+      // dual dots against w and against the tile's last basis row u (both from shared memory)
+      const double* us = Vs + (size_t)(k - 1) * ch;
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const int i = gwarp + q * kGW;
+        if (i < k) {
+          const double* vi = Vs + (size_t)i * ch;
+          double a0 = 0.0, b0 = 0.0;
+          for (int r = lane; r < len; r += 32) {
+            const double x = vi[r];
+            a0 += x * ws[r];
+            b0 += x * us[r];
+          }
+          acc[q] += a0;
+          acc2[q] += b0;
+        }
+      }
+    } else if (DOTS) {
       if (ch <= 32 * kCgsMaxT) {
         // lane owns rows lane + 32 t; w cached in registers; kQ independent chains
         double wr[kCgsMaxT];
@@ -521,7 +612,8 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     group_sync();
     if (gtid == 0 && c + kCgsStages < nchunks) issue(c + kCgsStages);
   }
-  const int stride = k + 1;
+  const int nd = DOTS ? (DCGS ? 2 * k : k) : 0;  // dot outputs: V^T w (+ V^T u for DCGS)
+  const int stride = nd + 1;
   if (DOTS) {
 #pragma unroll
     for (int q = 0; q < kQ; ++q) {
@@ -529,10 +621,14 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
       if (i < k) {
         const double v = warp_sum(acc[q]);
         if (lane == 0) comb[grp][i] = v;
+        if (DCGS) {
+          const double v2 = warp_sum(acc2[DCGS ? q : 0]);
+          if (lane == 0) comb[grp][k + i] = v2;
+        }
       }
     }
     __syncthreads();
-    for (int i = tid; i < k; i += kCgsThreads) partial[(int64_t)blockIdx.x * stride + i] = comb[0][i] + comb[1][i];
+    for (int i = tid; i < nd; i += kCgsThreads) partial[(int64_t)blockIdx.x * stride + i] = comb[0][i] + comb[1][i];
   }
   if (NORM) {
     nrm = warp_sum(nrm);
@@ -542,7 +638,7 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     if (tid == 0) {
       double t = 0.0;
       for (int q = 0; q < kCgsWarps; ++q) t += red[q];
-      partial[(int64_t)blockIdx.x * stride + k] = t;
+      partial[(int64_t)blockIdx.x * stride + nd] = t;
     }
   }
   if (nonfinite && __syncthreads_or(bad) && tid == 0) *nonfinite = 1;
@@ -554,16 +650,16 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  const int nout = (DOTS ? k : 0) + (NORM ? 1 : 0);
+  const int nout = nd + (NORM ? 1 : 0);
   double* s_pay = comb[0];  // the dot partials are consumed; reuse as the allreduce payload
   for (int o = warp; o < nout; o += kCgsWarps) {
-    const int col = DOTS ? (o < k ? o : k) : k;
+    const int col = o;
     double a = 0.0;
     for (int bb = lane; bb < (int)gridDim.x; bb += 32) a += __ldcg(partial + (int64_t)bb * stride + col);
     a = warp_sum(a);
     if (lane == 0) {
       if (pa.boxes) s_pay[o] = a;
-      else if (DOTS && o < k) h_out[o] = a;
+      else if (o < nd) h_out[o] = a;
       else nrm2_out[0] = a;
     }
   }
@@ -581,7 +677,7 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     __syncthreads();
     peer_allreduce_cta(pa, s_pay, cnt);
     for (int o = tid; o < nout; o += kCgsThreads) {
-      if (DOTS && o < k) h_out[o] = s_pay[o];
+      if (o < nd) h_out[o] = s_pay[o];
       else nrm2_out[0] = s_pay[o];
     }
     if (flags_in && tid == 0) {
@@ -705,7 +801,8 @@ int rs_gemv_n_update(const double* V, int64_t ldv, int k, int64_t n, const doubl
 
 static int cgs_pass(const double* V, int64_t ldv, int k, int64_t n, const double* h_in, double* w, double* h_out,
                     double* nrm2, int* nonfinite, double* work, cudaStream_t st, const rs_peer* peer, uint64_t epoch,
-                    const int64_t* flags_in, double* status_out) {
+                    const int64_t* flags_in, double* status_out, bool dcgs = false, double* vrow = nullptr,
+                    double* urow = nullptr) {
   rs_stream_t stream = (rs_stream_t)st;
   const bool aligned = (ldv % 2 == 0) && (n % 2 == 0) && ((uintptr_t)V % 16 == 0) && ((uintptr_t)w % 16 == 0);
   if (k > kCgsMaxK || !aligned) {
@@ -721,7 +818,8 @@ static int cgs_pass(const double* V, int64_t ldv, int k, int64_t n, const double
     return RS_OK;
   }
   const PeerArgs pa = peer_args(peer, epoch);
-  if (peer && (h_out ? k : 0) + (nrm2 ? 1 : 0) + (flags_in ? 2 : 0) > std::min<int64_t>(peer->rcap, 2 * kCgsMaxK)) {
+  if (peer && (h_out ? (dcgs ? 2 * k : k) : 0) + (nrm2 ? 1 : 0) + (flags_in ? 2 : 0) >
+                  std::min<int64_t>(peer->rcap, 2 * kCgsMaxK + 4)) {
     set_error(RS_ERR_ARG, "rs_cgs_pass_peer: payload exceeds the mailbox capacity");
     return RS_ERR_ARG;
   }
@@ -751,21 +849,24 @@ static int cgs_pass(const double* V, int64_t ldv, int k, int64_t n, const double
   // work[0] holds the completion ticket of the in-kernel final reduction; partials follow
   unsigned int* ticket = reinterpret_cast<unsigned int*>(work);
   work += 1;
-#define RS_CGS_LAUNCH(u, d, nm)                                                                          \
-  do {                                                                                                   \
-    cudaFuncSetAttribute(k_cgs<u, d, nm>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
-    k_cgs<u, d, nm><<<nblk, kCgsThreads, smem, st>>>(tmap, use_tmap, V, ldv, k, n, ch, stages, rows, h_in, w, \
-                                                     work, nonfinite, h_out, nrm2, ticket, pa, flags_in,  \
-                                                     status_out);                                         \
-    RS_COUNT_LAUNCH();                                                                                   \
+#define RS_CGS_LAUNCH(u, d, nm, dc)                                                                          \
+  do {                                                                                                       \
+    cudaFuncSetAttribute(k_cgs<u, d, nm, dc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
+    k_cgs<u, d, nm, dc><<<nblk, kCgsThreads, smem, st>>>(tmap, use_tmap, V, ldv, k, n, ch, stages, rows, h_in, \
+                                                         w, work, nonfinite, h_out, nrm2, ticket, pa, flags_in, \
+                                                         status_out, vrow, urow);                             \
+    RS_COUNT_LAUNCH();                                                                                       \
   } while (0)
-  if (U && D && Nm) RS_CGS_LAUNCH(true, true, true);
-  else if (U && D) RS_CGS_LAUNCH(true, true, false);
-  else if (U && Nm) RS_CGS_LAUNCH(true, false, true);
-  else if (U) RS_CGS_LAUNCH(true, false, false);
-  else if (D && Nm) RS_CGS_LAUNCH(false, true, true);
-  else if (D) RS_CGS_LAUNCH(false, true, false);
-  else RS_CGS_LAUNCH(false, false, true);
+  if (dcgs) {
+    if (U) RS_CGS_LAUNCH(true, false, true, true);
+    else RS_CGS_LAUNCH(false, true, false, true);
+  } else if (U && D && Nm) RS_CGS_LAUNCH(true, true, true, false);
+  else if (U && D) RS_CGS_LAUNCH(true, true, false, false);
+  else if (U && Nm) RS_CGS_LAUNCH(true, false, true, false);
+  else if (U) RS_CGS_LAUNCH(true, false, false, false);
+  else if (D && Nm) RS_CGS_LAUNCH(false, true, true, false);
+  else if (D) RS_CGS_LAUNCH(false, true, false, false);
+  else RS_CGS_LAUNCH(false, false, true, false);
 #undef RS_CGS_LAUNCH
   RS_CHECK_LAUNCH("rs_cgs_pass");
   return RS_OK;
@@ -790,6 +891,100 @@ int rs_cgs_pass_peer(const double* V, int64_t ldv, int k, int64_t n, const doubl
   }
   return cgs_pass(V, ldv, k, n, h_in, w, h_out, nrm2, nonfinite, work, (cudaStream_t)stream, peer, epoch, flags,
                   status_out);
+}
+
+// ---------------------------------------------------------------- DCGS2 Arnoldi (delayed re-orthogonalisation)
+namespace rs {
+// Host-free coefficient step between the two DCGS2 passes of Arnoldi step j = k-1
+// (one thread; j <= 63).  H is the raw (unrotated) Hessenberg, column-major, ldh rows.
+//   dots = [V^T w | V^T u] (2k) from rs_dcgs2_dots, or V^T u (k) when `last`
+//   j == 0: v_0 is final; coef = (s = [], a = [], 1/rho = 1, gamma = v_0.w); H[0,0] = gamma
+//   j >= 1: s = Q^T u, rho = sqrt(u.u - s.s), beta = sqrt(*nrm2_prev) (tentative H[j,j-1]);
+//           final column j-1: H[0:j, j-1] += beta s, H[j, j-1] = beta rho;
+//           gamma = (u.w - s.a) / rho; tentative column j: H[0:j, j] = (a - H[0:j,0:j] s) / rho,
+//           H[j, j] = (gamma - H[j, j-1] s[j-1]) / rho;  coef = (s, a, 1/rho, gamma)
+__global__ void k_dcgs2_coef(int k, const double* __restrict__ dots, double* __restrict__ H, int ldh,
+                             double* __restrict__ coef, const double* __restrict__ nrm2_prev, int last) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int j = k - 1;
+  const double* aw = dots;
+  const double* au = last ? dots : dots + k;
+  if (j == 0) {
+    if (last) return;
+    coef[kDcgsRho] = 1.0;
+    coef[kDcgsRho + 1] = aw[0];
+    H[0] = aw[0];
+    return;
+  }
+  double ss = 0.0;
+  for (int i = 0; i < j; ++i) ss += au[i] * au[i];
+  const double rho = sqrt(au[j] - ss);
+  const double beta = sqrt(*nrm2_prev);
+  double* hc = H + (int64_t)(j - 1) * ldh;
+  for (int i = 0; i < j; ++i) hc[i] += beta * au[i];
+  hc[j] = beta * rho;
+  if (last) return;
+  double sa = 0.0;
+  for (int i = 0; i < j; ++i) sa += au[i] * aw[i];
+  const double gam = (aw[j] - sa) / rho;
+  double* hn = H + (int64_t)j * ldh;
+  for (int i = 0; i < j; ++i) {
+    double t = 0.0;
+    for (int c = (i > 0 ? i - 1 : 0); c < j; ++c) t += H[i + (int64_t)c * ldh] * au[c];
+    hn[i] = (aw[i] - t) / rho;
+    coef[i] = au[i];
+    coef[kDcgsA + i] = aw[i];
+  }
+  hn[j] = (gam - hc[j] * au[j - 1]) / rho;
+  coef[kDcgsRho] = 1.0 / rho;
+  coef[kDcgsRho + 1] = gam;
+}
+}  // namespace rs
+
+static bool dcgs_ok(const double* V, int64_t ldv, int k, int64_t n, const double* w, const char* who) {
+  const bool aligned = (ldv % 2 == 0) && (n % 2 == 0) && ((uintptr_t)V % 16 == 0) && (!w || (uintptr_t)w % 16 == 0);
+  if (k < 1 || k > kCgsMaxK || n < 0 || !aligned) {
+    set_error(RS_ERR_ARG, std::string(who) + ": needs 1 <= k <= 64 basis vectors, an even row count and "
+                                             "16-byte aligned rows");
+    return false;
+  }
+  return true;
+}
+
+int rs_dcgs2_dots(const double* V, int64_t ldv, int k, int64_t n, const double* w, double* out, int* nonfinite,
+                  double* work, rs_peer* peer, uint64_t epoch, rs_stream_t stream) {
+  if (!dcgs_ok(V, ldv, k, n, w, "rs_dcgs2_dots")) return RS_ERR_ARG;
+  if (!w || !out || !work || (peer && epoch == 0)) {
+    set_error(RS_ERR_ARG, "rs_dcgs2_dots: bad arguments");
+    return RS_ERR_ARG;
+  }
+  return cgs_pass(V, ldv, k, n, nullptr, const_cast<double*>(w), out, nullptr, nonfinite, work, (cudaStream_t)stream,
+                  peer, epoch, nullptr, nullptr, true);
+}
+
+int rs_dcgs2_coef(int k, const double* dots, double* H, int ldh, double* coef, const double* nrm2_prev, int last,
+                  rs_stream_t stream) {
+  if (k < 1 || k > kCgsMaxK || !dots || !H || ldh < k || (!last && !coef) || (k > 1 && !nrm2_prev)) {
+    set_error(RS_ERR_ARG, "rs_dcgs2_coef: bad arguments");
+    return RS_ERR_ARG;
+  }
+  k_dcgs2_coef<<<1, 32, 0, (cudaStream_t)stream>>>(k, dots, H, ldh, coef, nrm2_prev, last);
+  RS_COUNT_LAUNCH();
+  RS_CHECK_LAUNCH("rs_dcgs2_coef");
+  return RS_OK;
+}
+
+int rs_dcgs2_update(const double* V, int64_t ldv, int k, int64_t n, const double* coef, const double* w,
+                    double* vrow, double* urow, double* nrm2, double* work, rs_peer* peer, uint64_t epoch,
+                    const int64_t* flags, double* status_out, rs_stream_t stream) {
+  if (!dcgs_ok(V, ldv, k, n, w, "rs_dcgs2_update")) return RS_ERR_ARG;
+  if (!coef || !w || !vrow || !urow || !nrm2 || !work || (peer && epoch == 0) || (flags && !status_out) ||
+      (flags && !peer)) {
+    set_error(RS_ERR_ARG, "rs_dcgs2_update: bad arguments");
+    return RS_ERR_ARG;
+  }
+  return cgs_pass(V, ldv, k, n, coef, const_cast<double*>(w), nullptr, nrm2, nullptr, work, (cudaStream_t)stream,
+                  peer, epoch, flags, status_out, true, vrow, urow);
 }
 
 int rs_gemv_n(const double* V, int64_t ldv, int k, int64_t n, const double* y, double* out, rs_stream_t stream) {

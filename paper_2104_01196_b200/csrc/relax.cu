@@ -98,6 +98,55 @@ __device__ __forceinline__ T row_accum(const SellView<T>& m, int64_t i, const T*
   return acc;
 }
 
+// One row of a SELL triangle, fetched in batches (see row_accum).  Splitting the
+// fetch from the accumulation lets a kernel issue the slice pointers, the first
+// column / value batch and the gathers of BOTH triangles before it accumulates
+// either, so a row costs ~3 dependent memory latencies instead of ~6; the
+// accumulation order (L ascending, diagonal, U ascending) is unchanged.
+template <typename T>
+struct RowFetch {
+  int32_t c[kBatch];
+  T v[kBatch], xv[kBatch];
+  const int32_t* cp = nullptr;
+  const T* vp = nullptr;
+  int w = 0;
+  __device__ __forceinline__ void start(const SellView<T>& m, int64_t i) {
+    if (m.empty) return;
+    const int64_t s = i >> 5;
+    const int64_t p0 = m.sp[s];
+    w = (int)((m.sp[s + 1] - p0) >> 5);
+    cp = m.col + p0 + (i & 31);
+    vp = m.val + p0 + (i & 31);
+  }
+  __device__ __forceinline__ void load(int j0) {
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const bool ok = j0 + u < w;
+      c[u] = ok ? __ldcs(cp + 32 * (j0 + u)) : -1;
+      v[u] = ok ? __ldcs(vp + 32 * (j0 + u)) : (T)0;
+    }
+  }
+  __device__ __forceinline__ void gather(const T* __restrict__ x) {
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) xv[u] = c[u] >= 0 ? x[c[u]] : (T)0;
+  }
+  __device__ __forceinline__ T accum(T acc) const {
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u)
+      if (c[u] >= 0) acc = add_rn<T>(acc, mul_rn<T>(v[u], xv[u]));
+    return acc;
+  }
+  // remaining batches after the first one
+  __device__ __forceinline__ T rest(const T* __restrict__ x, T acc) {
+    for (int j0 = kBatch; j0 < w; j0 += kBatch) {
+      load(j0);
+      gather(x);
+      acc = accum(acc);
+    }
+    return acc;
+  }
+};
+
 // s -= sum_k v_k * x[c_k] (gs_ordered_sweep form, _kernels.py:31-35)
 template <typename T>
 __device__ __forceinline__ T row_subtract(const SellView<T>& m, int64_t i, const T* x, T s) {
@@ -121,6 +170,10 @@ struct Halo {
 };
 
 // Full-row product A x for the local rows: E_lo | L | D | U | E_hi in ascending column order.
+// (A one-shot prefetch of both triangles' slice pointers / first batches / gathers
+// before accumulating -- RowFetch -- was measured slower here: 0.37-0.72 ms vs
+// 0.31 ms for the 256^3 SpMV, the extra registers cost more occupancy than the
+// shorter dependency chain gains; profiles/resid_tune.sh.)
 template <typename T, int MODE>
 __global__ void __launch_bounds__(256) k_resid(int64_t n, SellView<T> Elo, SellView<T> L, SellView<T> U,
                                                SellView<T> Ehi, const T* __restrict__ d, const T* __restrict__ x,
@@ -262,9 +315,15 @@ __global__ void __launch_bounds__(256) k_inner_out(int64_t n, SellView<T> Tm, co
                                                    const T* __restrict__ gin, O* __restrict__ z, T w, T gm, T gm1) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  T t = row_accum<T>(Tm, i, gin, (T)0);
-  T g = sub_rn<T>(rd[i], mul_rn<T>(w, t));
-  if (GAMMA) g = add_rn<T>(mul_rn<T>(gm1, gin[i]), mul_rn<T>(gm, g));
+  RowFetch<T> ft;
+  ft.start(Tm, i);
+  const T rdi = rd[i];
+  const T gi = GAMMA ? gin[i] : (T)0;
+  ft.load(0);
+  ft.gather(gin);
+  T t = ft.rest(gin, ft.accum((T)0));
+  T g = sub_rn<T>(rdi, mul_rn<T>(w, t));
+  if (GAMMA) g = add_rn<T>(mul_rn<T>(gm1, gi), mul_rn<T>(gm, g));
   z[i] = (O)mul_rn<T>(w, g);
 }
 
@@ -277,11 +336,18 @@ __global__ void __launch_bounds__(256) k_inner(int64_t n, SellView<T> Tm, const 
                                                T w, T gm, T gm1) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  T t = row_accum<T>(Tm, i, gin, (T)0);
-  T g = sub_rn<T>(rd[i], mul_rn<T>(w, t));
-  if (GAMMA) g = add_rn<T>(mul_rn<T>(gm1, gin[i]), mul_rn<T>(gm, g));
+  RowFetch<T> ft;
+  ft.start(Tm, i);
+  const T rdi = rd[i];
+  const T gi = GAMMA ? gin[i] : (T)0;
+  const T xi0 = FINAL == kFinalAdd ? x[i] : (T)0;
+  ft.load(0);
+  ft.gather(gin);
+  T t = ft.rest(gin, ft.accum((T)0));
+  T g = sub_rn<T>(rdi, mul_rn<T>(w, t));
+  if (GAMMA) g = add_rn<T>(mul_rn<T>(gm1, gi), mul_rn<T>(gm, g));
   if (FINAL == kNotFinal) gout[i] = g;
-  else if (FINAL == kFinalAdd) x[i] = add_rn<T>(x[i], mul_rn<T>(w, g));
+  else if (FINAL == kFinalAdd) x[i] = add_rn<T>(xi0, mul_rn<T>(w, g));
   else x[i] = mul_rn<T>(w, g);
 }
 

@@ -7,9 +7,12 @@
 * ``gmres`` (krylov.py:162-250): same control flow, history and stopping
   rules as the reference; the Arnoldi basis V lives in HBM and is
   orthogonalised by classical Gram-Schmidt with one re-orthogonalisation
-  (CGS2) as tall-skinny GEMV kernels instead of the reference's MGS loop
-  (north_star item 4).  Givens rotations and the least-squares solve stay on
-  the host (O(m^2) scalars): one (j+3)-double D2H copy per Arnoldi step.
+  (CGS2) as fused tall-skinny GEMV kernels instead of the reference's MGS
+  loop (north_star item 4) -- by default with the re-orthogonalisation of
+  v_j delayed into step j+1's first basis pass (DCGS2: two passes over the
+  basis per step instead of three).  Givens rotations and the least-squares
+  solve stay on the host (O(m^2) scalars), one small D2H copy per Arnoldi
+  step, software-pipelined so the host never stalls the GPU.
 
 ``m`` may be None, a :class:`Preconditioner` (device fast path), or -- the
 reference's duck-typed seam (krylov.py:147-154) -- any object with
@@ -229,6 +232,9 @@ class _timed:
             self.e1.record()
 
 
+_DCGS_COEF = 2 * 64 + 2  # rs_dcgs2_* coefficient block (include/gs2b200.h)
+
+
 class _Workspace:
     """Device buffers of one GMRES(m) solve.  Kept per thread for the last (n, restart, device), so
     back-to-back solves of the same size do not re-allocate the (m+1) x n basis; see release_workspace()."""
@@ -264,17 +270,27 @@ class _Workspace:
         self.y = torch.empty(restart + 1, **f64)
         self.pinned = torch.empty((2, 2 * self.m1 + 4), dtype=torch.float64, pin_memory=True)
         self.pinned_flags = torch.empty((2, 2), dtype=torch.int64, pin_memory=True)
+        # DCGS2: raw Hessenberg (column-major, m+1 rows), dual dots, coefficient block
+        self.H = torch.zeros(restart * self.m1, **f64)
+        self.dots = torch.zeros(2 * self.m1, **f64)
+        self.coef = torch.zeros(_DCGS_COEF, **f64)
 
 
 def _p(t):
     return C.c_void_p(t.data_ptr())
 
 
-def gmres(a, b, m=None, restart: int = 60, tol: float = 1e-9, maxit: int = 10000, x0=None, ortho: str = "cgs2"):
+def gmres(a, b, m=None, restart: int = 60, tol: float = 1e-9, maxit: int = 10000, x0=None, ortho: str = "auto"):
     """Restarted right-preconditioned GMRES(m) (krylov.py:162-250) on the GPU.
 
-    ``ortho="cgs2"`` (default, north_star item 4): classical Gram-Schmidt with
-    one re-orthogonalisation, three fused passes over the basis per step.
+    ``ortho="auto"`` (default): "dcgs2" when restart <= 63 and the row count is
+    even, else "cgs2".
+    ``ortho="cgs2"`` (north_star item 4): classical Gram-Schmidt with one
+    re-orthogonalisation, three fused passes over the basis per step.
+    ``ortho="dcgs2"``: the same CGS2 projections with the re-orthogonalisation
+    of v_j delayed into step j+1's first pass (two passes over the basis per
+    step instead of three; column j of the Hessenberg is final one step later).
+    Equal to CGS2 in exact arithmetic; restart <= 63, even row count.
     ``ortho="mgs"``: the reference's modified Gram-Schmidt loop
     (krylov.py:217-219), one fused update+dot launch per basis vector -- the
     reference-faithful mode (same iteration counts where the reference's are
@@ -306,8 +322,7 @@ def gmres(a, b, m=None, restart: int = 60, tol: float = 1e-9, maxit: int = 10000
     else:
         x = (x0.to(dev, torch.float64).clone() if _is_tensor(x0)
              else torch.from_numpy(np.array(x0, dtype=np.float64)).to(dev))
-    if ortho not in ("cgs2", "mgs"):
-        raise ValueError(f"ortho must be 'cgs2' or 'mgs', got {ortho!r}")
+    ortho = _check_ortho(ortho, n, restart)
     op = _as_operator(m)
     x, hist, conv = _gmres_device(dm, bt, x, op, restart, tol, maxit, ortho=ortho)
     if numpy_out or cpu_tensor_out:
@@ -321,6 +336,18 @@ def gmres(a, b, m=None, restart: int = 60, tol: float = 1e-9, maxit: int = 10000
 def release_workspace() -> None:
     """Free this thread's cached GMRES basis (the next solve re-allocates it)."""
     _Workspace._tls.ws = None
+
+
+def _check_ortho(ortho, n, restart):
+    """Validate / resolve the orthogonalisation mode ("auto" -> "dcgs2" where it applies)."""
+    if ortho not in ("auto", "cgs2", "mgs", "dcgs2"):
+        raise ValueError(f"ortho must be 'auto', 'cgs2', 'dcgs2' or 'mgs', got {ortho!r}")
+    dcgs_ok = restart <= 63 and n % 2 == 0
+    if ortho == "auto":
+        return "dcgs2" if dcgs_ok else "cgs2"
+    if ortho == "dcgs2" and not dcgs_ok:
+        raise ValueError("ortho='dcgs2' needs restart <= 63 and an even number of rows (fused basis passes)")
+    return ortho
 
 
 def _apply_op(op, v, z, ws):
@@ -338,6 +365,23 @@ def _apply_op(op, v, z, ws):
         if not _is_tensor(out):
             out = torch.from_numpy(np.ascontiguousarray(np.asarray(out, dtype=np.float64)))
         z.copy_(out)
+
+
+def _givens_step(h, cs, sn, g, j):
+    """Apply the previous rotations to column j, form rotation j, update g (krylov.py:224-234);
+    returns |g[j+1]| (the unscaled residual estimate)."""
+    for i in range(j):
+        hi = cs[i] * h[i, j] + sn[i] * h[i + 1, j]
+        h[i + 1, j] = -sn[i] * h[i, j] + cs[i] * h[i + 1, j]
+        h[i, j] = hi
+    denom = float(np.hypot(h[j, j], h[j + 1, j]))
+    cs[j] = h[j, j] / denom
+    sn[j] = h[j + 1, j] / denom
+    h[j, j] = denom
+    h[j + 1, j] = 0.0
+    g[j + 1] = -sn[j] * g[j]
+    g[j] = cs[j] * g[j]
+    return abs(g[j + 1])
 
 
 def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None, reduce_fn=None, ortho="cgs2",
@@ -462,6 +506,68 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
         ev.record()
         return ev
 
+    ph = peer.handle if peer is not None else None
+    ldh = m1
+
+    def stage_column(jj, before):
+        """Pinned slot jj % 2 gets, for Hessenberg column c = jj-1: before the coefficient kernel the
+        tentative column (rows 0..c, at m1), ||u'||^2 of step c (at 2 m1, the tentative subdiagonal
+        squared), the status and the flags; after it the final column (rows 0..c+1, at 0)."""
+        if jj < 1:
+            return
+        slot, c = jj % 2, jj - 1
+        if before:
+            ws.pinned[slot, m1:m1 + c + 1].copy_(ws.H[c * ldh:c * ldh + c + 1], non_blocking=True)
+            ws.pinned[slot, 2 * m1:2 * m1 + 3].copy_(status, non_blocking=True)
+            ws.pinned_flags[slot].copy_(ws.flags, non_blocking=True)
+        else:
+            ws.pinned[slot, :c + 2].copy_(ws.H[c * ldh:c * ldh + c + 2], non_blocking=True)
+
+    def enqueue_dcgs(jj):
+        """DCGS2 step jj: w = A M u_jj, dual dots, coefficients (finalises Hessenberg column jj-1),
+        v_jj = reorthogonalised u_jj, u_jj+1 = next tentative vector; jj == restart only finalises
+        the last column.  Column jj-1 (rows 0..jj) goes to pinned slot jj % 2."""
+        ep = (lambda: peer.next_reduce_epoch()) if peer is not None else (lambda: 0)
+        if jj < restart:
+            with _timed("precond"):
+                _apply_op(op, V[jj], ws.z, ws)
+            spmv(ws.z, ws.w)
+            k = jj + 1
+            with _timed("dcgs_dots"):
+                chk(lib.rs_dcgs2_dots(_p(V), ldv, k, n, _p(ws.w), _p(ws.dots), _p(ws.flags), _p(work), ph, ep(),
+                                      st), "dcgs2_dots")
+            if peer is None:
+                reduce_(ws.dots[:2 * k])
+            stage_column(jj, before=True)
+            chk(lib.rs_dcgs2_coef(k, _p(ws.dots), _p(ws.H), ldh, _p(ws.coef), _p(nrm2_slot), 0, st), "dcgs2_coef")
+            stage_column(jj, before=False)
+            with _timed("dcgs_update"):
+                chk(lib.rs_dcgs2_update(_p(V), ldv, k, n, _p(ws.coef), _p(ws.w), _p(V[jj]), _p(V[jj + 1]),
+                                        _p(nrm2_slot), _p(work), ph, ep(), _p(ws.flags) if ph else None,
+                                        _p(status[1:3]) if ph else None, st), "dcgs2_update")
+            if reduce_fn is not None and peer is None:
+                status[1] = (ws.flags[0] & 0xFFFFFFFF).to(torch.float64)
+                status[2] = (ws.flags[1] != _I64_MAX).to(torch.float64)
+                reduce_(status)
+            with _timed("scale"):
+                chk(lib.rs_scale_by_norm(n, _p(V[jj + 1]), _p(nrm2_slot), _p(V[jj + 1]), st), "scale")
+        else:
+            k = restart + 1
+            with _timed("dcgs_dots"):
+                if ph:
+                    chk(lib.rs_cgs_pass_peer(_p(V), ldv, k, n, None, _p(V[restart]), _p(ws.dots), None, None,
+                                             _p(work), ph, ep(), None, None, st), "cgs_pass")
+                else:
+                    chk(lib.rs_cgs_pass(_p(V), ldv, k, n, None, _p(V[restart]), _p(ws.dots), None, None, _p(work),
+                                        st), "cgs_pass")
+                    reduce_(ws.dots[:k])
+            stage_column(jj, before=True)
+            chk(lib.rs_dcgs2_coef(k, _p(ws.dots), _p(ws.H), ldh, None, _p(nrm2_slot), 1, st), "dcgs2_coef")
+            stage_column(jj, before=False)
+        ev = torch.cuda.Event()
+        ev.record()
+        return ev
+
     while total < maxit and not converged:
         beta = rnorm
         h = np.zeros((restart + 1, restart))
@@ -473,52 +579,85 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
         g[0] = beta
         j = -1
         lucky = False
-        # Software pipeline: step j+1 is enqueued before the host waits for step j's scalars, so
-        # the host-side Givens update (exactly the reference's numpy arithmetic) overlaps GPU
-        # work.  A speculative step past convergence is discarded (its results are never read).
-        ev_next = enqueue_step(0)
-        speculated = False
-        while True:
-            j += 1
-            total += 1
-            ev = ev_next
-            ev_next = None
-            if j + 1 < restart and total < maxit:
-                ev_next = enqueue_step(j + 1)
-            ev.synchronize()
-            hv = ws.pinned[j % 2].numpy()
-            fl = ws.pinned_flags[j % 2]
-            if (int(fl[0]) & 0xFFFFFFFF) or hv[2 * m1 + 1] > 0:
-                raise DivergenceError(f"non-finite values encountered in Arnoldi iteration {total}")
-            if int(fl[1]) != _I64_MAX or hv[2 * m1 + 2] > 0:
-                raise OverflowError(f"an entry overflows single precision (Arnoldi iteration {total})")
-            k = j + 1
-            h[:k, j] = hv[0:k] + hv[m1:m1 + k]
-            h[j + 1, j] = math.sqrt(hv[2 * m1])
-            lucky = h[j + 1, j] < breakdown_tol
-            for i in range(j):  # Givens (krylov.py:224-227)
-                hi = cs[i] * h[i, j] + sn[i] * h[i + 1, j]
-                h[i + 1, j] = -sn[i] * h[i, j] + cs[i] * h[i + 1, j]
-                h[i, j] = hi
-            denom = float(np.hypot(h[j, j], h[j + 1, j]))
-            cs[j] = h[j, j] / denom
-            sn[j] = h[j + 1, j] / denom
-            h[j, j] = denom
-            h[j + 1, j] = 0.0
-            g[j + 1] = -sn[j] * g[j]
-            g[j] = cs[j] * g[j]
-            est = abs(g[j + 1]) / bnorm
-            if not np.isfinite(est):
-                raise DivergenceError(f"residual estimate became non-finite at iteration {total}")
-            hist.append(est)
-            if est <= tol or lucky or ev_next is None:
-                speculated = ev_next is not None
-                break
-        if speculated:
-            # the discarded speculative step may have raised device flags; clear them
-            ws.flags.zero_()
-            ws.flags[1] = _I64_MAX
+        if ortho == "dcgs2":
+            # Column c of the Hessenberg is final after step c+1 (delayed re-orthogonalisation), so
+            # the pipeline runs one step ahead: steps c+1 (and speculatively c+2) are on the GPU
+            # while the host applies the Givens rotations to column c.
             status[1:3].zero_()
+            enqueue_dcgs(0)
+            ev_next = enqueue_dcgs(1)
+            speculated = False
+            while True:
+                j += 1
+                total += 1
+                ev = ev_next
+                ev_next = None
+                if j + 2 <= restart and total < maxit:
+                    ev_next = enqueue_dcgs(j + 2)
+                ev.synchronize()
+                hv = ws.pinned[(j + 1) % 2].numpy()
+                fl = ws.pinned_flags[(j + 1) % 2]
+                if int(fl[1]) != _I64_MAX or hv[2 * m1 + 2] > 0:
+                    raise OverflowError(f"an entry overflows single precision (Arnoldi iteration {total})")
+                beta_t = math.sqrt(hv[2 * m1]) if hv[2 * m1] >= 0 else float("nan")
+                if beta_t < breakdown_tol:
+                    # lucky breakdown on the tentative vector (u_j+1 ~ 0): its re-orthogonalisation
+                    # is meaningless (and may be NaN); close the column with the CGS1 projection
+                    h[:j + 1, j] = hv[m1:m1 + j + 1]
+                    h[j + 1, j] = beta_t
+                    lucky = True
+                else:
+                    if (int(fl[0]) & 0xFFFFFFFF) or hv[2 * m1 + 1] > 0:
+                        raise DivergenceError(f"non-finite values encountered in Arnoldi iteration {total}")
+                    h[:j + 2, j] = hv[:j + 2]
+                    lucky = h[j + 1, j] < breakdown_tol
+                est = _givens_step(h, cs, sn, g, j) / bnorm
+                if not np.isfinite(est):
+                    raise DivergenceError(f"residual estimate became non-finite at iteration {total}")
+                hist.append(est)
+                if est <= tol or lucky or ev_next is None:
+                    speculated = ev_next is not None
+                    break
+            if speculated:
+                ws.flags.zero_()
+                ws.flags[1] = _I64_MAX
+                status[1:3].zero_()
+        else:
+            # Software pipeline: step j+1 is enqueued before the host waits for step j's scalars, so
+            # the host-side Givens update (exactly the reference's numpy arithmetic) overlaps GPU
+            # work.  A speculative step past convergence is discarded (its results are never read).
+            ev_next = enqueue_step(0)
+            speculated = False
+            while True:
+                j += 1
+                total += 1
+                ev = ev_next
+                ev_next = None
+                if j + 1 < restart and total < maxit:
+                    ev_next = enqueue_step(j + 1)
+                ev.synchronize()
+                hv = ws.pinned[j % 2].numpy()
+                fl = ws.pinned_flags[j % 2]
+                if (int(fl[0]) & 0xFFFFFFFF) or hv[2 * m1 + 1] > 0:
+                    raise DivergenceError(f"non-finite values encountered in Arnoldi iteration {total}")
+                if int(fl[1]) != _I64_MAX or hv[2 * m1 + 2] > 0:
+                    raise OverflowError(f"an entry overflows single precision (Arnoldi iteration {total})")
+                k = j + 1
+                h[:k, j] = hv[0:k] + hv[m1:m1 + k]
+                h[j + 1, j] = math.sqrt(hv[2 * m1])
+                lucky = h[j + 1, j] < breakdown_tol
+                est = _givens_step(h, cs, sn, g, j) / bnorm
+                if not np.isfinite(est):
+                    raise DivergenceError(f"residual estimate became non-finite at iteration {total}")
+                hist.append(est)
+                if est <= tol or lucky or ev_next is None:
+                    speculated = ev_next is not None
+                    break
+            if speculated:
+                # the discarded speculative step may have raised device flags; clear them
+                ws.flags.zero_()
+                ws.flags[1] = _I64_MAX
+                status[1:3].zero_()
         # least squares + update (krylov.py:241-244)
         y = np.zeros(j + 1)
         for i in range(j, -1, -1):

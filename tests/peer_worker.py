@@ -73,6 +73,11 @@ def main():
     _, h_n = gd.gmres(A_n, b, pc_n, restart=60, tol=1e-9)
     x_p, h_p = gd.gmres(A_p, b, pc_p, restart=60, tol=1e-9)
     out["its_nccl"], out["its_peer"] = h_n.iterations, h_p.iterations
+    # the three-pass CGS2 mode over both communicators as well (default above is DCGS2)
+    _, hc_n = gd.gmres(A_n, b, pc_n, restart=60, tol=1e-9, ortho="cgs2")
+    _, hc_p = gd.gmres(A_p, b, pc_p, restart=60, tol=1e-9, ortho="cgs2")
+    out["its_cgs2_nccl"], out["its_cgs2_peer"] = hc_n.iterations, hc_p.iterations
+    out["history_cgs2_bitwise"] = bool(np.array_equal(hc_n.rel_res, hc_p.rel_res))
     out["history_bitwise"] = bool(np.array_equal(h_n.rel_res, h_p.rel_res))
     out["converged"] = bool(h_p.converged)
     # n_t = 2: hybrid rounds with halo exchanges inside the preconditioner
@@ -113,8 +118,9 @@ def main():
 
     ok = out["spmv_bitwise"] and out["allreduce_rank_order"] and out["converged"]
     ok &= out["its_peer"] == out["its_nccl"] if world <= 2 else abs(out["its_peer"] - out["its_nccl"]) <= 2
+    ok &= abs(out["its_cgs2_peer"] - out["its_peer"]) <= 2
     if world <= 2:
-        ok &= out["history_bitwise"] and out["history_nt2_bitwise"]
+        ok &= out["history_bitwise"] and out["history_nt2_bitwise"] and out["history_cgs2_bitwise"]
     if out["its_reference"] is not None:
         ok &= abs(out["its_peer"] - out["its_reference"]) <= 1
     out["ok"] = bool(ok)

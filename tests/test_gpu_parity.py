@@ -264,7 +264,8 @@ def test_tensor_inputs_in_place():
 @pytest.mark.parametrize("label", GMRES_FAST + ["ela3d_8__m60__gs2_1_1_1", "ela3d_8__m60__gs2_1_1_3",
                                                 "cd3d_16__m60__gs2_1_1_2__same",
                                                 "cd3d_16__m60__gs2_1_1_2__single_inside_double"])
-def test_gmres_iteration_counts(label, gmres_golden):
+@pytest.mark.parametrize("ortho", ["cgs2", "auto"])
+def test_gmres_iteration_counts(label, ortho, gmres_golden):
     want = gmres_golden["runs"][label]
     prob, m, kind, (nt, nk, nj), prec, nb = parse_gmres_label(label)
     a = golden_problem(prob)
@@ -279,7 +280,7 @@ def test_gmres_iteration_counts(label, gmres_golden):
             return z
     else:
         pc = g2.Preconditioner(a, kind, cfg if kind != "none" else None, precision=prec)
-    x, h = g2.gmres(a, b, pc, restart=m, tol=1e-9)
+    x, h = g2.gmres(a, b, pc, restart=m, tol=1e-9, ortho=ortho)
     assert h.converged == want["converged"]
     assert abs(h.iterations - want["iterations"]) <= iteration_tolerance(label, gmres_golden), \
         (h.iterations, want["iterations"])
@@ -477,3 +478,62 @@ def test_gmres_mgs_mode_counts(label, gmres_golden):
     b = g2.random_rhs(a.nrows, 0) if not prob.startswith("lap3d_64") else g2.random_rhs(a.nrows, 0, device="cuda")
     _, h = g2.gmres(a, b, g2.Preconditioner(a, kind, g2.RelaxConfig(*cfg)), restart=m, tol=1e-9, ortho="mgs")
     assert h.converged and h.iterations == want["iterations"]
+
+
+@pytest.mark.parametrize("label", GMRES_FAST + ["ela3d_8__m60__gs2_1_1_3", "cd3d_16__m60__gs2_1_1_2__single_inside_double",
+                                                "lap3d_64__m60__gs2_1_1_1", "lap3d_64__m60__gs2_1_1_3"])
+def test_gmres_dcgs2_mode_counts(label, gmres_golden):
+    """ortho='dcgs2' (re-orthogonalisation delayed into the next step's first basis pass): the
+    reference's iteration counts, a true final residual, and bitwise run-to-run reproducibility."""
+    want = gmres_golden["runs"][label]
+    prob, m, kind, (nt, nk, nj), prec, nb = parse_gmres_label(label)
+    if kind == "hybrid_gs2":
+        pytest.skip("host-callable hybrid preconditioner: covered by the CGS2 test")
+    if prob.startswith("lap3d_64"):
+        a = g2.laplace3d(64, device="cuda")
+        b = g2.random_rhs(a.nrows, 0, device="cuda")
+    else:
+        a = golden_problem(prob)
+        b = g2.random_rhs(a.nrows, 0)
+    if a.nrows % 2:
+        pytest.skip("odd row count")
+    pc = g2.Preconditioner(a, kind, g2.RelaxConfig(nt, nk, nj) if kind != "none" else None, precision=prec)
+    x, h = g2.gmres(a, b, pc, restart=m, tol=1e-9, ortho="dcgs2")
+    assert h.converged == want["converged"]
+    assert abs(h.iterations - want["iterations"]) <= iteration_tolerance(label, gmres_golden), \
+        (h.iterations, want["iterations"])
+    xn = x.cpu().numpy() if hasattr(x, "cpu") else x
+    bn = b.cpu().numpy() if hasattr(b, "cpu") else b
+    am = oracle.Matrix(a if not hasattr(a, "to_csr") else a.to_csr())
+    true = np.linalg.norm(bn - oracle.spmv(am, xn)) / np.linalg.norm(bn)
+    assert h.final_rel_res == pytest.approx(true, rel=1e-10, abs=1e-16)
+    _, h2 = g2.gmres(a, b, pc, restart=m, tol=1e-9, ortho="dcgs2")
+    assert np.array_equal(h.rel_res, h2.rel_res)
+
+
+def test_gmres_dcgs2_edge_cases():
+    a = g2.laplace3d(8)
+    b = g2.random_rhs(a.nrows, 0)
+    pc = g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, 1))
+    # restart 1 and 2, maxit cut inside a cycle, x0 = exact solution (no iteration)
+    for m, maxit in ((1, 40), (2, 7), (5, 13)):
+        _, h = g2.gmres(a, b, pc, restart=m, tol=1e-9, maxit=maxit, ortho="dcgs2")
+        _, hc = g2.gmres(a, b, pc, restart=m, tol=1e-9, maxit=maxit, ortho="cgs2")
+        assert h.iterations == hc.iterations == maxit
+        np.testing.assert_allclose(h.rel_res, hc.rel_res, rtol=1e-8)
+    x, h = g2.gmres(a, b, pc, restart=30, tol=1e-9, ortho="dcgs2")
+    _, h0 = g2.gmres(a, b, pc, restart=30, tol=1e-9, x0=x, ortho="dcgs2")
+    assert h0.iterations == 0 or h0.rel_res[0] <= 1e-9
+    with pytest.raises(ValueError, match="restart <= 63"):
+        g2.gmres(a, b, pc, restart=64, ortho="dcgs2")
+    odd = g2.laplace2d(5)
+    with pytest.raises(ValueError, match="even number of rows"):
+        g2.gmres(odd, g2.random_rhs(odd.nrows, 0), restart=10, ortho="dcgs2")
+
+
+@pytest.mark.slow
+def test_gmres_dcgs2_128():
+    a = g2.laplace3d(128, device="cuda")
+    b = g2.random_rhs(a.nrows, 0, device="cuda")
+    _, h = g2.gmres(a, b, g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, 1)), restart=60, tol=1e-9, ortho="dcgs2")
+    assert h.converged and h.iterations == REF_128[("gs2", (1, 1, 1))], h.iterations
