@@ -903,41 +903,60 @@ namespace rs {
 //           final column j-1: H[0:j, j-1] += beta s, H[j, j-1] = beta rho;
 //           gamma = (u.w - s.a) / rho; tentative column j: H[0:j, j] = (a - H[0:j,0:j] s) / rho,
 //           H[j, j] = (gamma - H[j, j-1] s[j-1]) / rho;  coef = (s, a, 1/rho, gamma)
-__global__ void k_dcgs2_coef(int k, const double* __restrict__ dots, double* __restrict__ H, int ldh,
-                             double* __restrict__ coef, const double* __restrict__ nrm2_prev, int last) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__global__ void __launch_bounds__(64) k_dcgs2_coef(int k, const double* __restrict__ dots, double* __restrict__ H,
+                                                   int ldh, double* __restrict__ coef,
+                                                   const double* __restrict__ nrm2_prev, int last) {
+  // 64 threads: thread i owns Hessenberg row i; the two length-j sums are taken by thread 0 in
+  // ascending order from shared memory (deterministic)
+  __shared__ double s_au[kCgsMaxK], s_aw[kCgsMaxK];
+  __shared__ double s_rho, s_beta, s_gam;
+  const int t = threadIdx.x;
   const int j = k - 1;
   const double* aw = dots;
   const double* au = last ? dots : dots + k;
   if (j == 0) {
-    if (last) return;
+    if (last || t != 0) return;
     coef[kDcgsRho] = 1.0;
     coef[kDcgsRho + 1] = aw[0];
     H[0] = aw[0];
     return;
   }
-  double ss = 0.0;
-  for (int i = 0; i < j; ++i) ss += au[i] * au[i];
-  const double rho = sqrt(au[j] - ss);
-  const double beta = sqrt(*nrm2_prev);
-  double* hc = H + (int64_t)(j - 1) * ldh;
-  for (int i = 0; i < j; ++i) hc[i] += beta * au[i];
-  hc[j] = beta * rho;
-  if (last) return;
-  double sa = 0.0;
-  for (int i = 0; i < j; ++i) sa += au[i] * aw[i];
-  const double gam = (aw[j] - sa) / rho;
-  double* hn = H + (int64_t)j * ldh;
-  for (int i = 0; i < j; ++i) {
-    double t = 0.0;
-    for (int c = (i > 0 ? i - 1 : 0); c < j; ++c) t += H[i + (int64_t)c * ldh] * au[c];
-    hn[i] = (aw[i] - t) / rho;
-    coef[i] = au[i];
-    coef[kDcgsA + i] = aw[i];
+  if (t < k) {
+    s_au[t] = au[t];
+    s_aw[t] = last ? 0.0 : aw[t];
   }
-  hn[j] = (gam - hc[j] * au[j - 1]) / rho;
-  coef[kDcgsRho] = 1.0 / rho;
-  coef[kDcgsRho + 1] = gam;
+  __syncthreads();
+  if (t == 0) {
+    double ss = 0.0, sa = 0.0;
+    for (int i = 0; i < j; ++i) {
+      ss += s_au[i] * s_au[i];
+      sa += s_au[i] * s_aw[i];
+    }
+    const double rho = sqrt(s_au[j] - ss);
+    s_rho = rho;
+    s_beta = sqrt(*nrm2_prev);
+    s_gam = (s_aw[j] - sa) / rho;
+  }
+  __syncthreads();
+  const double rho = s_rho, beta = s_beta;
+  double* hc = H + (int64_t)(j - 1) * ldh;
+  if (t < j) hc[t] += beta * s_au[t];
+  if (t == j) hc[j] = beta * rho;
+  if (last) return;
+  __syncthreads();  // column j-1 final before it enters H s below
+  double* hn = H + (int64_t)j * ldh;
+  if (t < j) {
+    double acc = 0.0;
+    for (int c = (t > 0 ? t - 1 : 0); c < j; ++c) acc += H[t + (int64_t)c * ldh] * s_au[c];
+    hn[t] = (s_aw[t] - acc) / rho;
+    coef[t] = s_au[t];
+    coef[kDcgsA + t] = s_aw[t];
+  }
+  if (t == 0) {
+    hn[j] = (s_gam - beta * rho * s_au[j - 1]) / rho;
+    coef[kDcgsRho] = 1.0 / rho;
+    coef[kDcgsRho + 1] = s_gam;
+  }
 }
 }  // namespace rs
 
@@ -968,7 +987,7 @@ int rs_dcgs2_coef(int k, const double* dots, double* H, int ldh, double* coef, c
     set_error(RS_ERR_ARG, "rs_dcgs2_coef: bad arguments");
     return RS_ERR_ARG;
   }
-  k_dcgs2_coef<<<1, 32, 0, (cudaStream_t)stream>>>(k, dots, H, ldh, coef, nrm2_prev, last);
+  k_dcgs2_coef<<<1, 64, 0, (cudaStream_t)stream>>>(k, dots, H, ldh, coef, nrm2_prev, last);
   RS_COUNT_LAUNCH();
   RS_CHECK_LAUNCH("rs_dcgs2_coef");
   return RS_OK;
