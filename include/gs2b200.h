@@ -258,8 +258,12 @@ int rs_cast_f32_f64(int64_t n, const float *in, double *out, rs_stream_t stream)
 typedef struct rs_peer rs_peer;
 int rs_dcgs2_dots(const double *V, int64_t ldv, int k, int64_t n, const double *w, double *out, int *nonfinite,
                   double *work, rs_peer *peer, uint64_t epoch, rs_stream_t stream);
+/* stage (nullable; pinned host memory is fine -- written zero-copy): host-visible record of column
+ * c = k-2 for the host's Givens: [0, c+2) final column, [stage_ld, stage_ld+c+1) tentative column,
+ * [2 stage_ld] *nrm2_prev, [2 stage_ld + 1, +3) status[0..1], [2 stage_ld + 3] local non-finite
+ * flag, [2 stage_ld + 4] local overflow flag (flags as in rs_cgs_pass; status / flags nullable) */
 int rs_dcgs2_coef(int k, const double *dots, double *H, int ldh, double *coef, const double *nrm2_prev, int last,
-                  rs_stream_t stream);
+                  double *stage, int stage_ld, const double *status, const int64_t *flags, rs_stream_t stream);
 int rs_dcgs2_update(const double *V, int64_t ldv, int k, int64_t n, const double *coef, const double *w,
                     double *vrow, double *urow, double *nrm2, double *work, rs_peer *peer, uint64_t epoch,
                     const int64_t *flags, double *status_out, rs_stream_t stream);

@@ -134,11 +134,30 @@ __global__ void __launch_bounds__(256) k_gemv_n(const double* __restrict__ V, in
   }
 }
 
-__global__ void k_scale_by_norm(int64_t n, const double* __restrict__ w, const double* __restrict__ nrm2,
-                                double* __restrict__ out) {
+// out = w / sqrt(nrm2) (out may alias w: each element is read and written by one thread)
+__global__ void k_scale_by_norm(int64_t n, const double* w, const double* __restrict__ nrm2, double* out) {
   const double h = sqrt(nrm2[0]);
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
     out[r] = w[r] / h;
+}
+
+// the same on 16-byte aligned data: double2 accesses, four independent loads in flight per thread
+__global__ void __launch_bounds__(256) k_scale_by_norm2(int64_t n2, const double2* w, const double* __restrict__ nrm2,
+                                                        double2* out) {
+  const double h = sqrt(nrm2[0]);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; r + 3 * stride < n2; r += 4 * stride) {
+    double2 a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = __ldcs(w + r + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) out[r + u * stride] = make_double2(a[u].x / h, a[u].y / h);
+  }
+  for (; r < n2; r += stride) {
+    const double2 a = __ldcs(w + r);
+    out[r] = make_double2(a.x / h, a.y / h);
+  }
 }
 
 // r = b - y; partial of r.r
@@ -905,7 +924,9 @@ namespace rs {
 //           H[j, j] = (gamma - H[j, j-1] s[j-1]) / rho;  coef = (s, a, 1/rho, gamma)
 __global__ void __launch_bounds__(64) k_dcgs2_coef(int k, const double* __restrict__ dots, double* __restrict__ H,
                                                    int ldh, double* __restrict__ coef,
-                                                   const double* __restrict__ nrm2_prev, int last) {
+                                                   const double* __restrict__ nrm2_prev, int last, double* stage,
+                                                   int stage_ld, const double* __restrict__ status,
+                                                   const int64_t* __restrict__ flags) {
   // 64 threads: thread i owns Hessenberg row i; the two length-j sums are taken by thread 0 in
   // ascending order from shared memory (deterministic)
   __shared__ double s_au[kCgsMaxK], s_aw[kCgsMaxK];
@@ -920,6 +941,20 @@ __global__ void __launch_bounds__(64) k_dcgs2_coef(int k, const double* __restri
     coef[kDcgsRho + 1] = aw[0];
     H[0] = aw[0];
     return;
+  }
+  if (stage) {
+    // host-visible record of Hessenberg column c = j-1 (pinned host memory, zero-copy):
+    // [m, m + c + 1) tentative column, [2m] ||u'||^2 of step c (tentative subdiagonal^2),
+    // [2m+1, 2m+3) reduced status, [2m+3] local non-finite flag, [2m+4] local overflow flag
+    const double* hcol = H + (int64_t)(j - 1) * ldh;
+    if (t < j) stage[stage_ld + t] = hcol[t];
+    if (t == 0) {
+      stage[2 * stage_ld] = *nrm2_prev;
+      stage[2 * stage_ld + 1] = status ? status[0] : 0.0;
+      stage[2 * stage_ld + 2] = status ? status[1] : 0.0;
+      stage[2 * stage_ld + 3] = (flags && (flags[0] & 0xffffffffll)) ? 1.0 : 0.0;
+      stage[2 * stage_ld + 4] = (flags && flags[1] != INT64_MAX) ? 1.0 : 0.0;
+    }
   }
   if (t < k) {
     s_au[t] = au[t];
@@ -942,6 +977,7 @@ __global__ void __launch_bounds__(64) k_dcgs2_coef(int k, const double* __restri
   double* hc = H + (int64_t)(j - 1) * ldh;
   if (t < j) hc[t] += beta * s_au[t];
   if (t == j) hc[j] = beta * rho;
+  if (stage && t <= j) stage[t] = hc[t];  // the final column
   if (last) return;
   __syncthreads();  // column j-1 final before it enters H s below
   double* hn = H + (int64_t)j * ldh;
@@ -982,12 +1018,14 @@ int rs_dcgs2_dots(const double* V, int64_t ldv, int k, int64_t n, const double* 
 }
 
 int rs_dcgs2_coef(int k, const double* dots, double* H, int ldh, double* coef, const double* nrm2_prev, int last,
-                  rs_stream_t stream) {
-  if (k < 1 || k > kCgsMaxK || !dots || !H || ldh < k || (!last && !coef) || (k > 1 && !nrm2_prev)) {
+                  double* stage, int stage_ld, const double* status, const int64_t* flags, rs_stream_t stream) {
+  if (k < 1 || k > kCgsMaxK || !dots || !H || ldh < k || (!last && !coef) || (k > 1 && !nrm2_prev) ||
+      (stage && stage_ld < k)) {
     set_error(RS_ERR_ARG, "rs_dcgs2_coef: bad arguments");
     return RS_ERR_ARG;
   }
-  k_dcgs2_coef<<<1, 64, 0, (cudaStream_t)stream>>>(k, dots, H, ldh, coef, nrm2_prev, last);
+  k_dcgs2_coef<<<1, 64, 0, (cudaStream_t)stream>>>(k, dots, H, ldh, coef, nrm2_prev, last, k > 1 ? stage : nullptr,
+                                                   stage_ld, status, flags);
   RS_COUNT_LAUNCH();
   RS_CHECK_LAUNCH("rs_dcgs2_coef");
   return RS_OK;
@@ -1018,7 +1056,11 @@ int rs_gemv_n(const double* V, int64_t ldv, int k, int64_t n, const double* y, d
 
 int rs_scale_by_norm(int64_t n, const double* w, const double* nrm2, double* out, rs_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  if (n) {
+  if (n && n % 2 == 0 && (uintptr_t)w % 16 == 0 && (uintptr_t)out % 16 == 0) {
+    k_scale_by_norm2<<<148 * 4, 256, 0, st>>>(n / 2, reinterpret_cast<const double2*>(w), nrm2,
+                                              reinterpret_cast<double2*>(out));
+    RS_COUNT_LAUNCH();
+  } else if (n) {
     k_scale_by_norm<<<grid_stride_blocks(n), 256, 0, st>>>(n, w, nrm2, out);
     RS_COUNT_LAUNCH();
   }

@@ -274,6 +274,9 @@ class _Workspace:
         self.H = torch.zeros(restart * self.m1, **f64)
         self.dots = torch.zeros(2 * self.m1, **f64)
         self.coef = torch.zeros(_DCGS_COEF, **f64)
+        # per-step record of the Hessenberg column the coefficient kernel writes straight into
+        # page-locked host memory (zero-copy; two slots for the one-step-ahead pipeline)
+        self.stage = torch.zeros((2, 2 * self.m1 + 8), dtype=torch.float64, pin_memory=True)
 
 
 def _p(t):
@@ -509,19 +512,8 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
     ph = peer.handle if peer is not None else None
     ldh = m1
 
-    def stage_column(jj, before):
-        """Pinned slot jj % 2 gets, for Hessenberg column c = jj-1: before the coefficient kernel the
-        tentative column (rows 0..c, at m1), ||u'||^2 of step c (at 2 m1, the tentative subdiagonal
-        squared), the status and the flags; after it the final column (rows 0..c+1, at 0)."""
-        if jj < 1:
-            return
-        slot, c = jj % 2, jj - 1
-        if before:
-            ws.pinned[slot, m1:m1 + c + 1].copy_(ws.H[c * ldh:c * ldh + c + 1], non_blocking=True)
-            ws.pinned[slot, 2 * m1:2 * m1 + 3].copy_(status, non_blocking=True)
-            ws.pinned_flags[slot].copy_(ws.flags, non_blocking=True)
-        else:
-            ws.pinned[slot, :c + 2].copy_(ws.H[c * ldh:c * ldh + c + 2], non_blocking=True)
+    def stage_ptr(jj):
+        return C.c_void_p(ws.stage[jj % 2].data_ptr()) if jj >= 1 else None
 
     def enqueue_dcgs(jj):
         """DCGS2 step jj: w = A M u_jj, dual dots, coefficients (finalises Hessenberg column jj-1),
@@ -538,9 +530,8 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
                                       st), "dcgs2_dots")
             if peer is None:
                 reduce_(ws.dots[:2 * k])
-            stage_column(jj, before=True)
-            chk(lib.rs_dcgs2_coef(k, _p(ws.dots), _p(ws.H), ldh, _p(ws.coef), _p(nrm2_slot), 0, st), "dcgs2_coef")
-            stage_column(jj, before=False)
+            chk(lib.rs_dcgs2_coef(k, _p(ws.dots), _p(ws.H), ldh, _p(ws.coef), _p(nrm2_slot), 0, stage_ptr(jj),
+                                  m1, _p(status[1:3]), _p(ws.flags), st), "dcgs2_coef")
             with _timed("dcgs_update"):
                 chk(lib.rs_dcgs2_update(_p(V), ldv, k, n, _p(ws.coef), _p(ws.w), _p(V[jj]), _p(V[jj + 1]),
                                         _p(nrm2_slot), _p(work), ph, ep(), _p(ws.flags) if ph else None,
@@ -561,9 +552,8 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
                     chk(lib.rs_cgs_pass(_p(V), ldv, k, n, None, _p(V[restart]), _p(ws.dots), None, None, _p(work),
                                         st), "cgs_pass")
                     reduce_(ws.dots[:k])
-            stage_column(jj, before=True)
-            chk(lib.rs_dcgs2_coef(k, _p(ws.dots), _p(ws.H), ldh, None, _p(nrm2_slot), 1, st), "dcgs2_coef")
-            stage_column(jj, before=False)
+            chk(lib.rs_dcgs2_coef(k, _p(ws.dots), _p(ws.H), ldh, None, _p(nrm2_slot), 1, stage_ptr(jj), m1,
+                                  _p(status[1:3]), _p(ws.flags), st), "dcgs2_coef")
         ev = torch.cuda.Event()
         ev.record()
         return ev
@@ -595,9 +585,8 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
                 if j + 2 <= restart and total < maxit:
                     ev_next = enqueue_dcgs(j + 2)
                 ev.synchronize()
-                hv = ws.pinned[(j + 1) % 2].numpy()
-                fl = ws.pinned_flags[(j + 1) % 2]
-                if int(fl[1]) != _I64_MAX or hv[2 * m1 + 2] > 0:
+                hv = ws.stage[(j + 1) % 2].numpy()
+                if hv[2 * m1 + 4] > 0 or hv[2 * m1 + 2] > 0:
                     raise OverflowError(f"an entry overflows single precision (Arnoldi iteration {total})")
                 beta_t = math.sqrt(hv[2 * m1]) if hv[2 * m1] >= 0 else float("nan")
                 if beta_t < breakdown_tol:
@@ -607,7 +596,7 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
                     h[j + 1, j] = beta_t
                     lucky = True
                 else:
-                    if (int(fl[0]) & 0xFFFFFFFF) or hv[2 * m1 + 1] > 0:
+                    if hv[2 * m1 + 3] > 0 or hv[2 * m1 + 1] > 0:
                         raise DivergenceError(f"non-finite values encountered in Arnoldi iteration {total}")
                     h[:j + 2, j] = hv[:j + 2]
                     lucky = h[j + 1, j] < breakdown_tol
