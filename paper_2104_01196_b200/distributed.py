@@ -120,16 +120,24 @@ class PeerMailbox:
         h = C.c_void_p()
         N.check(lib.rs_peer_create(comm.rank, comm.size, self.rcap, int(halo_lo), int(halo_hi), C.byref(h)), "peer")
         self.handle = h
+        err = None
         if local_group is not None:  # ranks are threads of this process: share raw pointers
             allh = comm.allgather_obj(h.value)
             arr = (C.c_void_p * comm.size)(*allh)
-            N.check(lib.rs_peer_connect_local(h, arr), "peer connect")
+            st = lib.rs_peer_connect_local(h, arr)
         else:
             buf = C.create_string_buffer(N.RS_IPC_HANDLE_BYTES)
-            N.check(lib.rs_peer_ipc_handle(h, buf), "peer ipc handle")
-            allh = comm.allgather_obj(buf.raw)
-            joined = b"".join(allh)
-            N.check(lib.rs_peer_connect(h, C.c_char_p(joined)), "peer connect")
+            st = lib.rs_peer_ipc_handle(h, buf)
+            allh = comm.allgather_obj(buf.raw if st == 0 else b"")
+            st = st or lib.rs_peer_connect(h, C.c_char_p(b"".join(allh)))
+        if st:
+            err = lib.rs_last_error().decode(errors="replace")
+        # agree on success before anyone uses the mailboxes (a rank that failed to map a peer
+        # must not leave the others spinning on it)
+        if comm.allreduce_max(1.0 if err else 0.0) > 0:
+            lib.rs_peer_destroy(h)
+            raise RuntimeError(f"peer-memory mailboxes unavailable on at least one rank"
+                               + (f" (this rank: {err})" if err else ""))
         off, words = C.c_int64(), C.c_int64()
         N.check(lib.rs_peer_layout(h, C.byref(off), C.byref(words)), "peer layout")
         self.off_halo = int(off.value)
@@ -484,7 +492,20 @@ def bench_rank(args, metric, Model, laplace3d_nnz, ClockSampler, peaks):
     lib = N.load()
     nx = args.nx or 512
     m = args.restart
-    A = DistMatrix.stencil(comm, "laplace3d", nx)
+    peer_note = None
+    try:
+        A = DistMatrix.stencil(comm, "laplace3d", nx)
+    except Exception as e:  # noqa: BLE001 -- e.g. no NVLink peer access on this box
+        if not use_peer:
+            raise
+        # every rank fails the same collective setup step, so all switch together
+        peer_note = f"peer-memory setup failed ({type(e).__name__}: {e}); NCCL collectives used instead"
+        import sys as _sys
+
+        print(f"[bench rank {rank}] {peer_note}", file=_sys.stderr, flush=True)
+        use_peer = False
+        comm = TorchComm()
+        A = DistMatrix.stencil(comm, "laplace3d", nx)
     b = local_rhs(A, 0)
     pc = HybridPreconditioner(A, RelaxConfig(1, 1, 1))
     n, nl, nu = laplace3d_nnz(nx, nx, nx)
@@ -552,7 +573,8 @@ def bench_rank(args, metric, Model, laplace3d_nnz, ClockSampler, peaks):
                        "bytes_per_step": cycle_bytes, "ms_per_iteration": round(ms / m, 4),
                        "bytes_note": "value = SURVEY §8(d) byte model of the whole cycle (a fixed amount of "
                                      "work) / device time; roofline = the kernels' own algorithmic bytes",
-                       "ortho": "dcgs2",
+                       "ortho": "dcgs2", "collectives": "nvlink-peer" if use_peer else "nccl",
+                       **({"collectives_note": peer_note} if peer_note else {}),
                        "l2": "inputs larger than L2", "parallelism": f"{world} ranks x 1 GPU (row blocks)"},
             "roofline": {"bound": "hbm", "kernel": "whole cycle (per GPU, algorithmic bytes of the launched "
                                                   "kernels on the local slab)",
