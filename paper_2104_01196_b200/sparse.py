@@ -365,15 +365,23 @@ def _check_vector(a, v, what: str):
 
 
 # ---------------------------------------------------------------- spmv / residual (sparse.py:179-192)
-def spmv(a, x):
-    """y = A x on the GPU (csr_matvec, _kernels.py:15-21): bitwise the reference row sums."""
+def spmv(a, x, out=None):
+    """y = A x on the GPU (csr_matvec, _kernels.py:15-21): bitwise the reference row sums.
+
+    ``out`` (extension): a preallocated device tensor of the matrix dtype to write y into."""
     dm = as_device(a)
     if not _is_tensor(x):
         x = np.asarray(x, dtype=dm.dtype)
     _check_vector(dm, x, "x")
     xv = _Vec(x, dm.dtype, dm.device_index, "x")
     torch = _torch()
-    y = torch.empty(dm.nrows, dtype=dm.torch_dtype, device=dm.torch_device)
+    if out is not None:
+        if not (_is_tensor(out) and out.is_cuda and out.dtype == dm.torch_dtype and out.is_contiguous()
+                and out.shape == (dm.nrows,)):
+            raise ValueError("out must be a contiguous CUDA tensor of the matrix dtype and length nrows")
+        y = out
+    else:
+        y = torch.empty(dm.nrows, dtype=dm.torch_dtype, device=dm.torch_device)
     if dm.halo_lo or dm.halo_hi:
         raise ValueError("spmv of a distributed row block needs halo values; use the distributed API")
     N.call("rs_spmv", dm.handle, xv.ptr, None, None, C.c_void_p(y.data_ptr()), stream_ptr(dm.device_index))
