@@ -200,6 +200,28 @@ class CpuSample:
         n, nl, nu = laplace3d_nnz(nx, nx, nx)
         self.mod = Model(n, nl, nu)
 
+    def sweeps(self, reps: int = 2):
+        """Per-sweep ms of the reference's relaxations (a6-a8) on b = rhs(0), x = rhs(1): the
+        SURVEY §8(d) CPU timing (median of reps, 1 application each)."""
+        o, m = self.oracle, self.m
+        x1 = o.random_rhs(m.n, 1)
+        out = {}
+
+        def med(fn):
+            ts = []
+            for _ in range(reps):
+                x = x1.copy()
+                t0 = time.perf_counter()
+                fn(x)
+                ts.append((time.perf_counter() - t0) * 1e3)
+            return round(statistics.median(ts), 1)
+
+        out["gs2_nj1_ms"] = med(lambda x: o.gs2_apply(m, self.b, x, n_t=1, n_k=1, n_j=1))
+        out["jr_ms"] = med(lambda x: o.jr_sweeps(m, self.b, x, 1))
+        out["gs_seq_ms"] = med(lambda x: o.gs_sweep(m, self.b, x, "forward"))
+        out["spmv_ms"] = med(lambda x: o.spmv(m, x))
+        return out
+
     def run(self, iters: int):
         """First `iters` Arnoldi iterations (+ cycle end); returns (GB/s, seconds, iterations)."""
         t0 = time.perf_counter()
@@ -354,10 +376,12 @@ def ours(args):
                "final_rel_res": h.final_rel_res, "preconditioner": "gs2(1,1,1)", "restart": m, "tol": 1e-9}
     cpu = None
     if not args.no_cpu_baseline:
-        gbs, dt, k = CpuSample(nx, 1).run(args.cpu_iters)
+        cs = CpuSample(nx, 1)
+        gbs, dt, k = cs.run(args.cpu_iters)
         cpu = {"value": round(gbs, 3), "unit": "GB/s", "cores": 1, "kind": "port",
                "sample": f"C oracle (reference algorithm), first {k} GMRES(60)+GS2(1,1,1) iterations of "
-                         f"laplace3d {nx}^3 on 1 host core, {dt:.1f} s"}
+                         f"laplace3d {nx}^3 on 1 host core, {dt:.1f} s",
+               "per_sweep_ms_1core": cs.sweeps()}
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
