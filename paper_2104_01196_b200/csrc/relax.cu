@@ -949,6 +949,31 @@ static int precond_gs2_single(rs_matrix* m, const rs_relax_cfg& cfg, const R* r,
     RS_CHECK_LAUNCH("precond");
     return RS_OK;
   }
+  // two-pass first step (rd = (T)r / d stored, then the inner step gathers rd) instead of k_inner0's
+  // per-neighbour divisions: RS_PRECOND_TWOPASS = 1 / 0 forces it on / off (default: on for fp32)
+  static const int twopass_env = getenv("RS_PRECOND_TWOPASS") ? atoi(getenv("RS_PRECOND_TWOPASS")) : -1;
+  const bool twopass = twopass_env >= 0 ? twopass_env != 0 : sizeof(T) == 4;
+  if (twopass) {
+    T* rd = (T*)m->scratch;
+    T* bufs[2] = {rd + c.n, rd + 2 * c.n};
+    k_scale_rd<T, R><<<c.grid(), kB, 0, st>>>(c.n, r, c.d, rd, overflow);
+    RS_COUNT_LAUNCH();
+    const T* gin = rd;
+    for (int j = 0; j < cfg.n_j; ++j) {
+      if (j == cfg.n_j - 1) {
+        if (damped) k_inner_out<T, O, true><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1);
+        else k_inner_out<T, O, false><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1);
+      } else {
+        T* gout = bufs[j & 1];
+        if (damped) k_inner<T, kNotFinal, true><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, gout, nullptr, w, gm, gm1);
+        else k_inner<T, kNotFinal, false><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, gout, nullptr, w, gm, gm1);
+        gin = gout;
+      }
+      RS_COUNT_LAUNCH();
+    }
+    RS_CHECK_LAUNCH("precond");
+    return RS_OK;
+  }
   if (cfg.n_j == 1) {
     if (damped) k_inner0<T, R, O, true, true><<<c.grid(), kB, 0, st>>>(c.n, Tm, r, c.d, nullptr, nullptr, z, w, gm, gm1, overflow);
     else k_inner0<T, R, O, true, false><<<c.grid(), kB, 0, st>>>(c.n, Tm, r, c.d, nullptr, nullptr, z, w, gm, gm1, overflow);
