@@ -226,6 +226,12 @@ int rs_axpy1(int64_t n, const double *z, double *x, rs_stream_t stream);
  * the CG updates x += alpha p, r -= alpha Ap, p = z + beta p (krylov.py:296-307) */
 int rs_axpy(int64_t n, double a, const double *x, double *y, rs_stream_t stream);
 int rs_xpby(int64_t n, const double *x, double b, double *y, rs_stream_t stream);
+/* the same CG updates with their scalars on the device (no host round trip per iteration):
+ * rs_cg_update: alpha = rz[0] / pap[0]; x_out = x + alpha p; r = r - alpha ap (krylov.py:295-297)
+ * rs_xpby_dev:  y = x + (num[0] / den[0]) y                               (krylov.py:307) */
+int rs_cg_update(int64_t n, const double *rz, const double *pap, const double *x, const double *p, double *x_out,
+                 double *r, const double *ap, rs_stream_t stream);
+int rs_xpby_dev(int64_t n, const double *x, const double *num, const double *den, double *y, rs_stream_t stream);
 
 /* ---- generators ---- */
 

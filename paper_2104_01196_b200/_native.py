@@ -81,6 +81,8 @@ _SIGS = {
     "rs_axpy1": ([_I64, _P, _P, _P], C.c_int),
     "rs_axpy": ([_I64, C.c_double, _P, _P, _P], C.c_int),
     "rs_xpby": ([_I64, _P, C.c_double, _P, _P], C.c_int),
+    "rs_cg_update": ([_I64, _P, _P, _P, _P, _P, _P, _P, _P], C.c_int),
+    "rs_xpby_dev": ([_I64, _P, _P, _P, _P, _P], C.c_int),
     "rs_lcg_fill": ([C.c_uint64, _I64, _I64, _P, _P], C.c_int),
     "rs_cast_f64_f32": ([_I64, _P, _P, _P, _P], C.c_int),
     "rs_cast_f32_f64": ([_I64, _P, _P, _P], C.c_int),

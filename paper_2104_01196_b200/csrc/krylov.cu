@@ -208,6 +208,27 @@ __global__ void k_xpby(int64_t n, const double* __restrict__ x, double b, double
     y[i] = __dadd_rn(x[i], __dmul_rn(b, y[i]));
 }
 
+// CG step with device scalars (no host round trip): alpha = rz / pap;
+// x_out = x + alpha p ; r = r - alpha ap  (krylov.py:295-297, same roundings as k_axpy)
+__global__ void k_cg_update(int64_t n, const double* __restrict__ rz, const double* __restrict__ pap,
+                            const double* __restrict__ x, const double* __restrict__ p, double* __restrict__ x_out,
+                            double* __restrict__ r, const double* __restrict__ ap) {
+  const double alpha = __ddiv_rn(rz[0], pap[0]);
+  const double nalpha = -alpha;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x_out[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+    r[i] = __dadd_rn(r[i], __dmul_rn(nalpha, ap[i]));
+  }
+}
+
+// p = z + (rz_new / rz) p with device scalars (krylov.py:307)
+__global__ void k_xpby_dev(int64_t n, const double* __restrict__ x, const double* __restrict__ num,
+                           const double* __restrict__ den, double* __restrict__ y) {
+  const double b = __ddiv_rn(num[0], den[0]);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = __dadd_rn(x[i], __dmul_rn(b, y[i]));
+}
+
 __global__ void k_axpy1(int64_t n, const double* __restrict__ z, double* __restrict__ x) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     x[i] = x[i] + z[i];
@@ -1122,6 +1143,35 @@ int rs_axpy(int64_t n, double a, const double* x, double* y, rs_stream_t stream)
     RS_COUNT_LAUNCH();
   }
   RS_CHECK_LAUNCH("rs_axpy");
+  return RS_OK;
+}
+
+int rs_cg_update(int64_t n, const double* rz, const double* pap, const double* x, const double* p, double* x_out,
+                 double* r, const double* ap, rs_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n < 0 || !rz || !pap || (n && (!x || !p || !x_out || !r || !ap))) {
+    set_error(RS_ERR_ARG, "rs_cg_update: bad arguments");
+    return RS_ERR_ARG;
+  }
+  if (n) {
+    k_cg_update<<<grid_stride_blocks(n), 256, 0, st>>>(n, rz, pap, x, p, x_out, r, ap);
+    RS_COUNT_LAUNCH();
+  }
+  RS_CHECK_LAUNCH("rs_cg_update");
+  return RS_OK;
+}
+
+int rs_xpby_dev(int64_t n, const double* x, const double* num, const double* den, double* y, rs_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n < 0 || !num || !den || (n && (!x || !y))) {
+    set_error(RS_ERR_ARG, "rs_xpby_dev: bad arguments");
+    return RS_ERR_ARG;
+  }
+  if (n) {
+    k_xpby_dev<<<grid_stride_blocks(n), 256, 0, st>>>(n, x, num, den, y);
+    RS_COUNT_LAUNCH();
+  }
+  RS_CHECK_LAUNCH("rs_xpby_dev");
   return RS_OK;
 }
 

@@ -743,11 +743,12 @@ static int jr_sweeps_t(rs_matrix* m, const T* b, T* x, int sweeps, double omega,
   T* cur = x;
   for (int s = 0; s < sweeps; ++s) {
     if (s == 0 && x_is_zero) {
-      // x = 0 + w*(b/d): rd into alt then x = w*rd ... done in place on x directly
-      k_scale_rd<T, T><<<c.grid(), kB, 0, c.st>>>(c.n, b, c.d, alt, nullptr);
+      // from zero the first sweep is pointwise, x1 = w*(b/d) (one pass); write it into the buffer
+      // that makes the remaining ping-pong sweeps end in x, so no copy-back is needed
+      T* dst = ((sweeps - 1) % 2 == 0) ? x : alt;
+      k_scale0<T, T, T><<<c.grid(), kB, 0, c.st>>>(c.n, b, c.d, dst, w, nullptr);
       RS_COUNT_LAUNCH();
-      k_update<T, true><<<c.grid(), kB, 0, c.st>>>(c.n, alt, x, w);
-      RS_COUNT_LAUNCH();
+      cur = dst;
       continue;
     }
     T* nxt = cur == x ? alt : x;

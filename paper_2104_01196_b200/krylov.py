@@ -675,8 +675,10 @@ def cg(a, b, m=None, tol: float = 1e-9, maxit: int = 10000, x0=None):
     ||b - A x|| / ||b|| is recomputed and recorded every iteration; a
     Preconditioner of a non-symmetric kind is rejected ("symmetric"),
     non-positive curvature raises NotSpdError, non-finite values
-    DivergenceError.  Scalars (p.Ap, r.z, ||r||) come back to the host once
-    per iteration each; vectors stay in HBM.
+    DivergenceError.  Scalars stay on the device (alpha and beta are formed
+    inside the update kernels); the host reads p.Ap and the true residual once
+    per iteration from a pinned mirror, one iteration behind the GPU
+    (software pipeline), so it never stalls the stream.
     """
     if nrows_of(a) != ncols_of(a):
         raise ValueError(f"square system required, matrix is {nrows_of(a)}x{ncols_of(a)}")
@@ -735,29 +737,61 @@ def cg(a, b, m=None, tol: float = 1e-9, maxit: int = 10000, x0=None):
 
     precond(r, z)
     p.copy_(z)
-    rz = dot(r, z)
-    converged = False
-    for _ in range(maxit):
+    # device scalars: [pap, ||b - A x||^2, rz (two slots: iteration parity)]; pinned mirror per
+    # iteration slot: [pap, res2, overflow-flag-as-double]
+    ds = torch.zeros(4, **f64)
+    pap_s, res_s = ds[0:1], ds[1:2]
+    rz_s = (ds[2:3], ds[3:4])
+    chk(lib.rs_dot(n, _p(r), _p(z), _p(rz_s[0]), _p(work), st), "dot")
+    xs = (x, torch.empty_like(x))  # x ping-pong: a speculative iteration never overwrites the answer
+    stage = torch.full((2, 3), -1.0, dtype=torch.float64, pin_memory=True)
+    fp32 = op is not None and getattr(op, "precision", "same") == "single_inside_double"
+
+    def enqueue(k):
+        """CG iteration k entirely on the device (krylov.py:288-308), scalars staged to pinned slot k%2."""
+        xin, xout = xs[k % 2], xs[(k + 1) % 2]
         chk(lib.rs_spmv(dm.handle, _p(p), None, None, _p(ap), st), "spmv")
-        pap = dot(p, ap)
+        chk(lib.rs_dot(n, _p(p), _p(ap), _p(pap_s), _p(work), st), "dot")
+        chk(lib.rs_cg_update(n, _p(rz_s[k % 2]), _p(pap_s), _p(xin), _p(p), _p(xout), _p(r), _p(ap), st), "cg")
+        chk(lib.rs_spmv(dm.handle, _p(xout), None, None, _p(t), st), "spmv")
+        chk(lib.rs_sub_norm(n, _p(bt), _p(t), _p(t), _p(res_s), _p(work), st), "sub_norm")
+        if fp32:
+            _WS.flags[1] = _I64_MAX
+        _apply_op(op, r, z, _WS)
+        stage[k % 2, 0:2].copy_(ds[0:2], non_blocking=True)
+        if fp32:  # overflowing entry index (INT64_MAX: none), exact in a double below 2^53
+            stage[k % 2, 2:3].copy_(torch.where(_WS.flags[1:2] == _I64_MAX, -1, _WS.flags[1:2]).to(torch.float64),
+                                    non_blocking=True)
+        chk(lib.rs_dot(n, _p(r), _p(z), _p(rz_s[(k + 1) % 2]), _p(work), st), "dot")
+        chk(lib.rs_xpby_dev(n, _p(z), _p(rz_s[(k + 1) % 2]), _p(rz_s[k % 2]), _p(p), st), "xpby")
+        ev = torch.cuda.Event()
+        ev.record()
+        return ev
+
+    # Software pipeline as in gmres: iteration k+1 is enqueued before the host checks iteration k's
+    # scalars; a speculative iteration past convergence (or past an error) is never read.
+    converged = False
+    k_last = -1
+    ev_next = enqueue(0) if maxit > 0 else None
+    for k in range(maxit):
+        ev = ev_next
+        ev_next = enqueue(k + 1) if k + 1 < maxit else None
+        ev.synchronize()
+        pap, res2, ovf = (float(v) for v in stage[k % 2])
         if not math.isfinite(pap):
             raise DivergenceError("non-finite curvature in CG")
         if pap <= 0.0:
             raise NotSpdError(f"non-positive curvature p^T A p = {pap}; matrix is not SPD")
-        alpha = rz / pap
-        chk(lib.rs_axpy(n, alpha, _p(p), _p(x), st), "axpy")
-        chk(lib.rs_axpy(n, -alpha, _p(ap), _p(r), st), "axpy")
-        chk(lib.rs_spmv(dm.handle, _p(x), None, None, _p(t), st), "spmv")
-        chk(lib.rs_sub_norm(n, _p(bt), _p(t), _p(t), _p(sc), _p(work), st), "sub_norm")
-        true_rel = math.sqrt(float(sc.item())) / bnorm
+        true_rel = math.sqrt(res2) / bnorm
         if not math.isfinite(true_rel):
             raise DivergenceError("non-finite residual in CG")
         hist.append(true_rel)
+        k_last = k
         if true_rel <= tol:
             converged = True
             break
-        precond(r, z)
-        rz_new = dot(r, z)
-        chk(lib.rs_xpby(n, _p(z), rz_new / rz, _p(p), st), "xpby")
-        rz = rz_new
+        if ovf >= 0:
+            raise OverflowError(f"entry {int(ovf)} overflows single precision")
+    if k_last >= 0:
+        x = xs[(k_last + 1) % 2]
     return finish(x, hist, converged)
