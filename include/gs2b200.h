@@ -268,8 +268,11 @@ int rs_dcgs2_dots(const double *V, int64_t ldv, int k, int64_t n, const double *
  * c = k-2 for the host's Givens: [0, c+2) final column, [stage_ld, stage_ld+c+1) tentative column,
  * [2 stage_ld] *nrm2_prev, [2 stage_ld + 1, +3) status[0..1], [2 stage_ld + 3] local non-finite
  * flag, [2 stage_ld + 4] local overflow flag (flags as in rs_cgs_pass; status / flags nullable) */
+/* unnormalized = 1: row k-1 holds u' itself (norm sqrt(*nrm2_prev)) rather than u'/||u'|| -- the
+ * caller skipped the scaling pass; s, rho then already carry the norm (beta = 1 below) */
 int rs_dcgs2_coef(int k, const double *dots, double *H, int ldh, double *coef, const double *nrm2_prev, int last,
-                  double *stage, int stage_ld, const double *status, const int64_t *flags, rs_stream_t stream);
+                  double *stage, int stage_ld, const double *status, const int64_t *flags, int unnormalized,
+                  rs_stream_t stream);
 int rs_dcgs2_update(const double *V, int64_t ldv, int k, int64_t n, const double *coef, const double *w,
                     double *vrow, double *urow, double *nrm2, double *work, rs_peer *peer, uint64_t epoch,
                     const int64_t *flags, double *status_out, rs_stream_t stream);

@@ -947,7 +947,7 @@ __global__ void __launch_bounds__(64) k_dcgs2_coef(int k, const double* __restri
                                                    int ldh, double* __restrict__ coef,
                                                    const double* __restrict__ nrm2_prev, int last, double* stage,
                                                    int stage_ld, const double* __restrict__ status,
-                                                   const int64_t* __restrict__ flags) {
+                                                   const int64_t* __restrict__ flags, int unnormalized) {
   // 64 threads: thread i owns Hessenberg row i; the two length-j sums are taken by thread 0 in
   // ascending order from shared memory (deterministic)
   __shared__ double s_au[kCgsMaxK], s_aw[kCgsMaxK];
@@ -990,7 +990,8 @@ __global__ void __launch_bounds__(64) k_dcgs2_coef(int k, const double* __restri
     }
     const double rho = sqrt(s_au[j] - ss);
     s_rho = rho;
-    s_beta = sqrt(*nrm2_prev);
+    // unnormalized: u is ||u'|| times the unit tentative vector, so s, rho already carry beta
+    s_beta = unnormalized ? 1.0 : sqrt(*nrm2_prev);
     s_gam = (s_aw[j] - sa) / rho;
   }
   __syncthreads();
@@ -1039,14 +1040,15 @@ int rs_dcgs2_dots(const double* V, int64_t ldv, int k, int64_t n, const double* 
 }
 
 int rs_dcgs2_coef(int k, const double* dots, double* H, int ldh, double* coef, const double* nrm2_prev, int last,
-                  double* stage, int stage_ld, const double* status, const int64_t* flags, rs_stream_t stream) {
+                  double* stage, int stage_ld, const double* status, const int64_t* flags, int unnormalized,
+                  rs_stream_t stream) {
   if (k < 1 || k > kCgsMaxK || !dots || !H || ldh < k || (!last && !coef) || (k > 1 && !nrm2_prev) ||
       (stage && stage_ld < k)) {
     set_error(RS_ERR_ARG, "rs_dcgs2_coef: bad arguments");
     return RS_ERR_ARG;
   }
   k_dcgs2_coef<<<1, 64, 0, (cudaStream_t)stream>>>(k, dots, H, ldh, coef, nrm2_prev, last, k > 1 ? stage : nullptr,
-                                                   stage_ld, status, flags);
+                                                   stage_ld, status, flags, unnormalized);
   RS_COUNT_LAUNCH();
   RS_CHECK_LAUNCH("rs_dcgs2_coef");
   return RS_OK;

@@ -233,6 +233,7 @@ class _timed:
 
 
 _DCGS_COEF = 2 * 64 + 2  # rs_dcgs2_* coefficient block (include/gs2b200.h)
+_DEFER_NORM = __import__("os").environ.get("RS_DEFER_NORM", "1") != "0"  # A/B switch (profiles/ortho_probe.py)
 
 
 class _Workspace:
@@ -512,6 +513,13 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
     ph = peer.handle if peer is not None else None
     ldh = m1
 
+    # The tentative vector u' can stay unnormalised (no scaling pass): the next step's dots and
+    # re-orthogonalisation absorb its norm, provided the preconditioner is linear and exact in
+    # scale -- true for this library's fp64 Preconditioner kinds (zero-start relaxations), not for
+    # an arbitrary callable or the fp32-inside mode (whose overflow check must see the unit vector).
+    defer_norm = (ortho == "dcgs2" and (op is None or (isinstance(op, Preconditioner) and op.precision == "same"))
+                  and _DEFER_NORM)
+
     def stage_ptr(jj):
         return C.c_void_p(ws.stage[jj % 2].data_ptr()) if jj >= 1 else None
 
@@ -531,7 +539,7 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
             if peer is None:
                 reduce_(ws.dots[:2 * k])
             chk(lib.rs_dcgs2_coef(k, _p(ws.dots), _p(ws.H), ldh, _p(ws.coef), _p(nrm2_slot), 0, stage_ptr(jj),
-                                  m1, _p(status[1:3]), _p(ws.flags), st), "dcgs2_coef")
+                                  m1, _p(status[1:3]), _p(ws.flags), int(defer_norm and jj >= 1), st), "dcgs2_coef")
             with _timed("dcgs_update"):
                 chk(lib.rs_dcgs2_update(_p(V), ldv, k, n, _p(ws.coef), _p(ws.w), _p(V[jj]), _p(V[jj + 1]),
                                         _p(nrm2_slot), _p(work), ph, ep(), _p(ws.flags) if ph else None,
@@ -540,8 +548,9 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
                 status[1] = (ws.flags[0] & 0xFFFFFFFF).to(torch.float64)
                 status[2] = (ws.flags[1] != _I64_MAX).to(torch.float64)
                 reduce_(status)
-            with _timed("scale"):
-                chk(lib.rs_scale_by_norm(n, _p(V[jj + 1]), _p(nrm2_slot), _p(V[jj + 1]), st), "scale")
+            if not defer_norm:
+                with _timed("scale"):
+                    chk(lib.rs_scale_by_norm(n, _p(V[jj + 1]), _p(nrm2_slot), _p(V[jj + 1]), st), "scale")
         else:
             k = restart + 1
             with _timed("dcgs_dots"):
@@ -553,7 +562,7 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
                                         st), "cgs_pass")
                     reduce_(ws.dots[:k])
             chk(lib.rs_dcgs2_coef(k, _p(ws.dots), _p(ws.H), ldh, None, _p(nrm2_slot), 1, stage_ptr(jj), m1,
-                                  _p(status[1:3]), _p(ws.flags), st), "dcgs2_coef")
+                                  _p(status[1:3]), _p(ws.flags), int(defer_norm), st), "dcgs2_coef")
         ev = torch.cuda.Event()
         ev.record()
         return ev
