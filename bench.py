@@ -436,6 +436,9 @@ def sweep_table(g2, torch, a, mod, hbm, reps: int = 10):
     out["jr"] = timeit(lambda x: g2.jr_sweeps(a, s, b, x, 1), mod.gs2_sweep(0))
     out["gs_level_sched"] = timeit(lambda x: g2.gs_sequential_sweep(a, s, b, x, "forward"),
                                    mod.ML + mod.MU + 3 * mod.V)
+    coloring = g2.greedy_color(a)
+    out["mt_gs"] = timeit(lambda x: g2.mt_gs_sweep(a, s, coloring, b, x, "forward"), mod.ML + mod.MU + 3 * mod.V)
+    out["mt_gs"]["colors"] = coloring.num_colors
     y = torch.empty_like(b)
     out["spmv"] = timeit(lambda x: g2.spmv(a, x, out=y), mod.spmv())
     return out

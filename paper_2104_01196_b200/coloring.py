@@ -56,12 +56,16 @@ def mt_gs_sweep(a, s: Splitting, coloring: Coloring, b, x, direction: str = "for
     if coloring.color.shape[0] != nrows_of(a):
         raise ValueError(f"coloring covers {coloring.color.shape[0]} rows, matrix has {nrows_of(a)}")
     dm = as_device(a)
-    cur = np.empty(max(dm.nrows, 1), dtype=np.int64)
-    nc = C.c_int64(0)
-    N.call("rs_mat_coloring", dm.handle, cur.ctypes.data, C.byref(nc))
-    col = np.ascontiguousarray(coloring.color, dtype=np.int64)
-    if int(nc.value) != coloring.num_colors or not np.array_equal(cur[: dm.nrows], col):
-        N.call("rs_mat_set_coloring", dm.handle, col.ctypes.data, int(coloring.num_colors))
+    # the handle's installed coloring is re-checked only when a different Coloring object arrives
+    # (exporting and comparing n colors on the host costs far more than the sweep itself)
+    if getattr(dm, "_mt_coloring", None) is not coloring:
+        cur = np.empty(max(dm.nrows, 1), dtype=np.int64)
+        nc = C.c_int64(0)
+        N.call("rs_mat_coloring", dm.handle, cur.ctypes.data, C.byref(nc))
+        col = np.ascontiguousarray(coloring.color, dtype=np.int64)
+        if int(nc.value) != coloring.num_colors or not np.array_equal(cur[: dm.nrows], col):
+            N.call("rs_mat_set_coloring", dm.handle, col.ctypes.data, int(coloring.num_colors))
+        dm._mt_coloring = coloring
     bv, xv = _vectors(dm, b, x)
     N.call("rs_mt_gs_sweep", dm.handle, bv.ptr, xv.ptr, N.DIRECTIONS[direction], float(s.omega),
            stream_ptr(dm.device_index))
