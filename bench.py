@@ -459,7 +459,7 @@ def main():
     p.add_argument("--nx", type=int, default=0)
     p.add_argument("--restart", type=int, default=60)
     p.add_argument("--no-tts", action="store_true")
-    p.add_argument("--tts", action="store_true", help="also time a full solve at N > 1 (off by default)")
+    p.add_argument("--tts", action="store_true", help="(default now) time a full solve at N > 1 as well")
     p.add_argument("--no-sweeps", action="store_true")
     p.add_argument("--comm", default="peer", choices=["peer", "nccl"],
                    help="N > 1 collectives: NVLink peer-memory kernels (default) or NCCL")

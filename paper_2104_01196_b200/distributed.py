@@ -552,7 +552,7 @@ def bench_rank(args, metric, Model, laplace3d_nnz, ClockSampler, peaks):
         e2e_step()
     e2e_ms = comm.allreduce_max((time.perf_counter() - t0) * 1e3 / args.steps)
     tts = None
-    if getattr(args, "tts", False):
+    if not getattr(args, "no_tts", False):
         comm.barrier()
         t0 = time.perf_counter()
         _, h = gmres(A, b, pc, restart=m, tol=1e-9)
