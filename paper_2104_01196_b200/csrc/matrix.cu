@@ -235,6 +235,13 @@ static void free_sell(Sell<T>& s) {
   s = Sell<T>();
 }
 
+void free_mt_sell(rs_matrix* m) {
+  free_sell(m->MT64);
+  free_sell(m->MT32);
+  free(m->mt_slice_base);
+  m->mt_slice_base = nullptr;
+}
+
 static void free_levels(Levels& l) {
   free(l.level_ptr_host);
   cudaFree(l.rows);
@@ -397,6 +404,7 @@ void destroy(rs_matrix* m) {
   free_levels(m->fwd);
   free_levels(m->bwd);
   free_levels(m->mt);
+  free_mt_sell(m);
   free(m->color);
   cudaFree(m->scratch);
   cudaFree(m->scratch2);
@@ -505,6 +513,7 @@ static int install_coloring(rs_matrix* m, const int64_t* color, int64_t nc) {
   free(lv.level_ptr_host);
   cudaFree(lv.rows);
   lv = Levels();
+  free_mt_sell(m);
   lv.nlevels = nc;
   lv.level_ptr_host = (int64_t*)calloc(nc + 1, sizeof(int64_t));
   for (int64_t i = 0; i < n; ++i) lv.level_ptr_host[color[i] + 1]++;

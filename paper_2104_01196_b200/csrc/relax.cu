@@ -20,12 +20,15 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <vector>
+
 #include "rs_internal.cuh"
 
 namespace rs {
 
 int build_levels(rs_matrix* m, int backward);
 int build_coloring(rs_matrix* m);
+void free_mt_sell(rs_matrix* m);
 int wave_enabled();
 template <typename T>
 int wave_half_sweep(rs_matrix* m, const T* b, const T* xin, T* xout, int n_j, int backward, int form, double omega,
@@ -694,6 +697,159 @@ static int gs2_apply_t(rs_matrix* m, const T* b, T* x, const rs_relax_cfg& cfg, 
 // of a color in parallel; same-color rows are uncoupled, so reading x in place gives
 // new values for earlier colors and old values for later ones, as the sequential
 // visit of the concatenated color classes does.
+// ---- multicolor GS on color-ordered slices (see rs_matrix::MT64)
+// off-diagonal slot count of row i in one SELL triangle
+template <typename T>
+__device__ __forceinline__ int sell_row_count(const SellView<T>& m, int64_t i) {
+  if (m.empty) return 0;
+  const int64_t s = i >> 5, p0 = m.sp[s];
+  const int w = (int)((m.sp[s + 1] - p0) >> 5);
+  int c = 0;
+  for (int j = 0; j < w; ++j) c += m.col[p0 + 32 * j + (i & 31)] >= 0;
+  return c;
+}
+
+template <typename T>
+__global__ void k_mt_len(int64_t n, const int32_t* __restrict__ rows, SellView<T> L, SellView<T> U,
+                         int32_t* __restrict__ len) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int64_t i = rows[t];
+  len[t] = sell_row_count(L, i) + sell_row_count(U, i);
+}
+
+// one thread per slice of one color: width = max row length of its (up to) 32 rows
+__global__ void k_mt_width(int64_t nsl, int64_t cnt, const int32_t* __restrict__ len, int64_t* __restrict__ width) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nsl) return;
+  int w = 0;
+  for (int64_t t = q * 32; t < cnt && t < q * 32 + 32; ++t) w = max(w, len[t]);
+  width[q] = w;
+}
+
+// row t of a color: its L entries then its U entries (ascending columns), padded with col = -1
+template <typename T>
+__global__ void k_mt_fill(int64_t cnt, const int32_t* __restrict__ rows, const int64_t* __restrict__ sp,
+                          SellView<T> L, SellView<T> U, int32_t* __restrict__ col, T* __restrict__ val) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cnt) return;
+  const int64_t i = rows[t];
+  const int64_t base = sp[t >> 5] + (t & 31);
+  const int w = (int)((sp[(t >> 5) + 1] - sp[t >> 5]) >> 5);
+  int k = 0;
+  for (int tri = 0; tri < 2; ++tri) {
+    const SellView<T>& m = tri == 0 ? L : U;
+    if (m.empty) continue;
+    const int64_t s = i >> 5, p0 = m.sp[s];
+    const int mw = (int)((m.sp[s + 1] - p0) >> 5);
+    for (int j = 0; j < mw; ++j) {
+      const int32_t c = m.col[p0 + 32 * j + (i & 31)];
+      if (c < 0) continue;
+      col[base + 32 * k] = c;
+      val[base + 32 * k] = m.val[p0 + 32 * j + (i & 31)];
+      ++k;
+    }
+  }
+  for (; k < w; ++k) {
+    col[base + 32 * k] = -1;
+    val[base + 32 * k] = (T)0;
+  }
+}
+
+// GS update of the rows of one color (gs_ordered_sweep arithmetic, _kernels.py:24-39):
+// s = b_i - sum_k a_ik x_k in ascending k over the merged L|U entries; x_i = s/d_i (damped form)
+template <typename T>
+__global__ void __launch_bounds__(256) k_mt_color(int64_t cnt, const int32_t* __restrict__ rows,
+                                                  const int64_t* __restrict__ sp, const int32_t* __restrict__ col,
+                                                  const T* __restrict__ val, const T* __restrict__ d,
+                                                  const T* __restrict__ b, T* x, T w, T w1, bool damped) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cnt) return;
+  const int64_t i = rows[t];
+  const int64_t p0 = sp[t >> 5];
+  const int wd = (int)((sp[(t >> 5) + 1] - p0) >> 5);
+  const int32_t* cp = col + p0 + (t & 31);
+  const T* vp = val + p0 + (t & 31);
+  T s = b[i];
+  const T di = d[i];
+  const T xi = damped ? x[i] : (T)0;
+  for (int j0 = 0; j0 < wd; j0 += kBatch) {
+    int32_t c[kBatch];
+    T v[kBatch], xv[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const bool ok = j0 + u < wd;
+      c[u] = ok ? __ldcs(cp + 32 * (j0 + u)) : -1;
+      v[u] = ok ? __ldcs(vp + 32 * (j0 + u)) : (T)0;
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) xv[u] = c[u] >= 0 ? x[c[u]] : (T)0;
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u)
+      if (c[u] >= 0) s = sub_rn<T>(s, mul_rn<T>(v[u], xv[u]));
+  }
+  const T q = div_rn<T>(s, di);
+  x[i] = damped ? add_rn<T>(mul_rn<T>(w1, xi), mul_rn<T>(w, q)) : q;
+}
+
+template <typename T>
+static Sell<T>& mt_sell(rs_matrix* m);
+template <>
+Sell<double>& mt_sell<double>(rs_matrix* m) { return m->MT64; }
+template <>
+Sell<float>& mt_sell<float>(rs_matrix* m) { return m->MT32; }
+
+// build the color-ordered slices once per installed coloring
+template <typename T>
+static int build_mt_sell(rs_matrix* m, Ctx<T>& c, cudaStream_t st) {
+  Sell<T>& S = mt_sell<T>(m);
+  if (S.slice_ptr || m->nrows == 0) return RS_OK;
+  Levels& lv = m->mt;
+  const int64_t n = m->nrows, nc = lv.nlevels;
+  std::vector<int64_t> base(nc + 1, 0);
+  for (int64_t q = 0; q < nc; ++q) base[q + 1] = base[q] + (lv.level_ptr_host[q + 1] - lv.level_ptr_host[q] + 31) / 32;
+  const int64_t nsl = base[nc];
+  int32_t* len = nullptr;
+  int64_t* width = nullptr;
+  RS_CUDA(cudaMalloc(&len, sizeof(int32_t) * n));
+  RS_CUDA(cudaMalloc(&width, sizeof(int64_t) * std::max<int64_t>(nsl, 1)));
+  k_mt_len<T><<<grid_for(n, kB), kB, 0, st>>>(n, lv.rows, c.L, c.U, len);
+  RS_COUNT_LAUNCH();
+  for (int64_t q = 0; q < nc; ++q) {
+    const int64_t lo = lv.level_ptr_host[q], cnt = lv.level_ptr_host[q + 1] - lo, ns = base[q + 1] - base[q];
+    if (ns) {
+      k_mt_width<<<grid_for(ns, kB), kB, 0, st>>>(ns, cnt, len + lo, width + base[q]);
+      RS_COUNT_LAUNCH();
+    }
+  }
+  std::vector<int64_t> w(std::max<int64_t>(nsl, 1));
+  RS_CUDA(cudaMemcpyAsync(w.data(), width, sizeof(int64_t) * nsl, cudaMemcpyDeviceToHost, st));
+  RS_CUDA(cudaStreamSynchronize(st));
+  std::vector<int64_t> sp(nsl + 1, 0);
+  for (int64_t q = 0; q < nsl; ++q) sp[q + 1] = sp[q] + 32 * w[q];
+  S.nrows = n;
+  S.nslices = nsl;
+  S.nslots = sp[nsl];
+  RS_CUDA(cudaMalloc(&S.slice_ptr, sizeof(int64_t) * (nsl + 1)));
+  RS_CUDA(cudaMalloc(&S.col, sizeof(int32_t) * std::max<int64_t>(S.nslots, 1)));
+  RS_CUDA(cudaMalloc(&S.val, sizeof(T) * std::max<int64_t>(S.nslots, 1)));
+  RS_CUDA(cudaMemcpyAsync(S.slice_ptr, sp.data(), sizeof(int64_t) * (nsl + 1), cudaMemcpyHostToDevice, st));
+  for (int64_t q = 0; q < nc; ++q) {
+    const int64_t lo = lv.level_ptr_host[q], cnt = lv.level_ptr_host[q + 1] - lo;
+    if (cnt) {
+      k_mt_fill<T><<<grid_for(cnt, kB), kB, 0, st>>>(cnt, lv.rows + lo, S.slice_ptr + base[q], c.L, c.U, S.col, S.val);
+      RS_COUNT_LAUNCH();
+    }
+  }
+  RS_CUDA(cudaStreamSynchronize(st));
+  cudaFree(len);
+  cudaFree(width);
+  m->mt_slice_base = (int64_t*)malloc(sizeof(int64_t) * (nc + 1));
+  memcpy(m->mt_slice_base, base.data(), sizeof(int64_t) * (nc + 1));
+  RS_CHECK_LAUNCH("build multicolor slices");
+  return RS_OK;
+}
+
 template <typename T>
 static int mt_gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omega, cudaStream_t st) {
   int e;
@@ -702,6 +858,8 @@ static int mt_gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double o
   T w = (T)omega, w1 = (T)(1.0 - omega);
   const bool damped = w != (T)1.0;
   Levels& lv = m->mt;
+  if ((e = build_mt_sell<T>(m, c, st))) return e;
+  const Sell<T>& S = mt_sell<T>(m);
   for (int half = 0; half < 2; ++half) {
     const int bwd = half;
     if (direction == RS_FORWARD && bwd) continue;
@@ -710,7 +868,8 @@ static int mt_gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double o
       const int64_t col = bwd ? lv.nlevels - 1 - q : q;
       const int64_t lo = lv.level_ptr_host[col], cnt = lv.level_ptr_host[col + 1] - lo;
       if (!cnt) continue;
-      k_gs_level<T><<<grid_for(cnt, kB), kB, 0, st>>>(cnt, lv.rows + lo, c.L, c.U, c.d, b, x, x, x, w, w1, damped);
+      k_mt_color<T><<<grid_for(cnt, kB), kB, 0, st>>>(cnt, lv.rows + lo, S.slice_ptr + m->mt_slice_base[col],
+                                                      S.col, S.val, c.d, b, x, w, w1, damped);
       RS_COUNT_LAUNCH();
     }
   }

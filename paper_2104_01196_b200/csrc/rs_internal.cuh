@@ -93,6 +93,13 @@ struct rs_matrix {
   rs::Levels fwd, bwd;      // lazily built
   rs::Levels mt;            // multicolor GS: "levels" = colors, rows ascending within a color
   int64_t* color = nullptr; // host, per-row color of the multicolor sweep
+  // multicolor GS: the off-diagonal entries (L then U, ascending columns) of the rows of each
+  // color, stored as SELL-32 slices in color order (row t of color c = mt.rows[lo_c + t]), so a
+  // color sweep reads coalesced slices instead of every other row's slots; mt_slice_base[c] =
+  // first slice of color c (host, ncolors + 1 entries)
+  rs::Sell<double> MT64;
+  rs::Sell<float> MT32;
+  int64_t* mt_slice_base = nullptr;
   void* scratch = nullptr;  // 3*nrows working dtype (rd, g ping/pong)
   void* scratch2 = nullptr; // 1*nrows (t)
   double* red = nullptr;    // reduction partials
