@@ -392,6 +392,7 @@ static int build_split(rs_matrix* m, const Src& src) {
 }
 
 void destroy_wave(void* p);
+void destroy_pipe(void* p);
 
 void destroy(rs_matrix* m) {
   if (!m) return;
@@ -412,6 +413,7 @@ void destroy(rs_matrix* m) {
   cudaFree(m->ticket);
   destroy_wave(m->wave[0]);
   destroy_wave(m->wave[1]);
+  destroy_pipe(m->pipe);
   cudaFree(m->stage);
   cudaSetDevice(prev);
   delete m;

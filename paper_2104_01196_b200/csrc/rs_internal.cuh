@@ -107,6 +107,7 @@ struct rs_matrix {
   int64_t red_cap = 0;
   void* wave[2] = {nullptr, nullptr};  // wavefront sweep plans (forward / backward)
   void* stage = nullptr;               // wavefront stage vectors (n_j x nrows)
+  void* pipe = nullptr;                // window-pipelined sweep plan (relax.cu PipePlan)
   size_t stage_bytes = 0;
 };
 

@@ -62,7 +62,7 @@ def _run(nproc: int, nx: int = 32):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("nproc", [1, 2, 4])
+@pytest.mark.parametrize("nproc", [1, 2, 4, 8])
 def test_peer_collectives_match_nccl(nproc):
     if not torch.cuda.is_available() or torch.cuda.device_count() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
