@@ -8,6 +8,7 @@
 // (2) exclusive-scan the slice widths and scatter every row into its SELL-32
 // slots, keeping ascending column order and padding with col = -1.
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_reduce.cuh>
 
 #include <algorithm>
 #include <atomic>
@@ -151,6 +152,11 @@ __global__ void k_count(Src src, BuildShape s, CountOut o) {
   }
 }
 
+__global__ void k_uniform_slots(int64_t* sp, int64_t ns, int64_t per) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s <= ns) sp[s] = s * per;
+}
+
 __global__ void k_widths_to_slots(const int32_t* w, int64_t* slots, int64_t ns) {
   int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s < ns) slots[s] = (int64_t)w[s] * kSlice;
@@ -271,6 +277,33 @@ static int alloc_sell(Sell<T>& s, int64_t nrows, int64_t nnz, const int32_t* d_w
   RS_CUDA(cudaMemcpy(&s.nslots, s.slice_ptr + s.nslices, sizeof(int64_t), cudaMemcpyDeviceToHost));
   cudaFree(tbuf);
   cudaFree(tmp);
+  // Uniform width: when padding every slice to the widest one costs <= 5% more slots (stencil
+  // matrices: only boundary rows are shorter), store it that way -- slice s then starts at
+  // 32*uw*s, so the sweep kernels compute the slice bounds instead of loading them (one
+  // dependent memory round trip less per row); slice_ptr stays valid for every other user.
+  s.uw = -1;
+  if (s.nslots > 0 && s.nslices > 0) {
+    int32_t* dmax = nullptr;
+    RS_CUDA(cudaMalloc(&dmax, sizeof(int32_t)));
+    size_t rb = 0;
+    RS_CUDA(cub::DeviceReduce::Max(nullptr, rb, d_width, dmax, s.nslices));
+    void* rbuf = nullptr;
+    RS_CUDA(cudaMalloc(&rbuf, std::max<size_t>(rb, 1)));
+    RS_CUDA(cub::DeviceReduce::Max(rbuf, rb, d_width, dmax, s.nslices));
+    int32_t wmax = 0;
+    RS_CUDA(cudaMemcpy(&wmax, dmax, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    cudaFree(rbuf);
+    cudaFree(dmax);
+    const int64_t uslots = (int64_t)wmax * kSlice * s.nslices;
+    static const bool no_uniform = getenv("RS_SELL_UNIFORM") && atoi(getenv("RS_SELL_UNIFORM")) == 0;
+    if (!no_uniform && wmax > 0 && (uslots - s.nslots) * 20 <= s.nslots) {
+      k_uniform_slots<<<grid_for(s.nslices + 1, 256), 256>>>(s.slice_ptr, s.nslices, (int64_t)wmax * kSlice);
+      RS_COUNT_LAUNCH();
+      RS_CHECK_LAUNCH("k_uniform_slots");
+      s.nslots = uslots;
+      s.uw = wmax;
+    }
+  }
   size_t ns = (size_t)std::max<int64_t>(s.nslots, 1);
   RS_CUDA(cudaMalloc(&s.col, sizeof(int32_t) * ns));
   RS_CUDA(cudaMalloc(&s.val, sizeof(T) * ns));
@@ -642,6 +675,7 @@ static int cast_sell(const Sell<double>& a, Sell<float>& b, long long* bad, cons
   b.nslices = a.nslices;
   b.nnz = a.nnz;
   b.nslots = a.nslots;
+  b.uw = a.uw;
   size_t ns = (size_t)std::max<int64_t>(a.nslots, 1);
   RS_CUDA(cudaMalloc(&b.slice_ptr, sizeof(int64_t) * (a.nslices + 1)));
   RS_CUDA(cudaMemcpy(b.slice_ptr, a.slice_ptr, sizeof(int64_t) * (a.nslices + 1), cudaMemcpyDeviceToDevice));

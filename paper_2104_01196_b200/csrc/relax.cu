@@ -57,7 +57,20 @@ struct SellView {
   const int32_t* __restrict__ col;
   const T* __restrict__ val;
   bool empty;
+  int uw;  // uniform slice width (Sell::uw) or -1
 };
+
+// first slot and width of slice s: computed for a uniform-width triangle, loaded otherwise
+template <typename T>
+__device__ __forceinline__ void slice_bounds(const SellView<T>& m, int64_t s, int64_t& p0, int& w) {
+  if (m.uw >= 0) {
+    p0 = s * (int64_t)(32 * m.uw);
+    w = m.uw;
+  } else {
+    p0 = m.sp[s];
+    w = (int)((m.sp[s + 1] - p0) >> 5);
+  }
+}
 
 template <typename T>
 static SellView<T> view(const Sell<T>& s, bool scaled) {
@@ -66,6 +79,7 @@ static SellView<T> view(const Sell<T>& s, bool scaled) {
   v.col = s.col;
   v.val = scaled ? s.dval : s.val;
   v.empty = s.nslots == 0;
+  v.uw = s.uw;
   return v;
 }
 
@@ -82,9 +96,10 @@ __device__ __forceinline__ T row_accum_p(const SellView<T>& m, int64_t p0, int w
 template <typename T>
 __device__ __forceinline__ T row_accum(const SellView<T>& m, int64_t i, const T* __restrict__ x, T acc) {
   if (m.empty) return acc;
-  const int64_t s = i >> 5;
-  const int64_t p0 = m.sp[s];
-  return row_accum_p<T>(m, p0, (int)((m.sp[s + 1] - p0) >> 5), i, x, acc);
+  int64_t p0;
+  int w;
+  slice_bounds<T>(m, i >> 5, p0, w);
+  return row_accum_p<T>(m, p0, w, i, x, acc);
 }
 
 // row_accum with the slice bounds already loaded (p0 = first slot, w = slots per lane)
@@ -127,9 +142,8 @@ struct RowFetch {
   int w = 0;
   __device__ __forceinline__ void start(const SellView<T>& m, int64_t i) {
     if (m.empty) return;
-    const int64_t s = i >> 5;
-    const int64_t p0 = m.sp[s];
-    w = (int)((m.sp[s + 1] - p0) >> 5);
+    int64_t p0;
+    slice_bounds<T>(m, i >> 5, p0, w);
     cp = m.col + p0 + (i & 31);
     vp = m.val + p0 + (i & 31);
   }
@@ -197,16 +211,16 @@ __global__ void __launch_bounds__(256) k_resid(int64_t n, SellView<T> Elo, SellV
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   // the U slice bounds and the row's own operands do not depend on the L walk: fetch them first
-  const int64_t s = i >> 5;
-  const int64_t pu0 = U.empty ? 0 : U.sp[s];
-  const int64_t pu1 = U.empty ? 0 : U.sp[s + 1];
+  int64_t pu0 = 0;
+  int uwd = 0;
+  if (!U.empty) slice_bounds<T>(U, i >> 5, pu0, uwd);
   const T di = d[i];
   const T xi = x[i];
   T acc = (T)0;
   acc = row_accum<T>(Elo, i, xlo, acc);
   acc = row_accum<T>(L, i, x, acc);
   acc = add_rn<T>(acc, mul_rn<T>(di, xi));
-  acc = row_accum_p<T>(U, pu0, (int)((pu1 - pu0) >> 5), i, x, acc);
+  acc = row_accum_p<T>(U, pu0, uwd, i, x, acc);
   acc = row_accum<T>(Ehi, i, xhi, acc);
   if (MODE == kSpmv) {
     out[i] = acc;
@@ -282,10 +296,10 @@ __global__ void __launch_bounds__(256) k_inner0(int64_t n, SellView<T> Tm, const
   const T rdi = div_rn<T>(ri, d[i]);
   T t = (T)0;
   if (!Tm.empty) {
-    const int64_t s = i >> 5;
     const int lane = (int)(i & 31);
-    const int64_t p0 = Tm.sp[s];
-    const int wd = (int)((Tm.sp[s + 1] - p0) >> 5);
+    int64_t p0;
+    int wd;
+    slice_bounds<T>(Tm, i >> 5, p0, wd);
     for (int j0 = 0; j0 < wd; j0 += kBatch) {
       int32_t c[kBatch];
       T v[kBatch], dk[kBatch];
@@ -669,10 +683,10 @@ __global__ void __launch_bounds__(256) k_gs2_pipe(PipeSched p, SellView<T> L, Se
           const T xi0 = (s == p.n_j && MODE == kPipeResid) ? x[i] : (T)0;
           T acc = (T)0;
           if (!Tsc.empty) {
-            const int64_t sl = i >> 5;
             const int lane = (int)(i & 31);
-            const int64_t p0 = Tsc.sp[sl];
-            const int wd = (int)((Tsc.sp[sl + 1] - p0) >> 5);
+            int64_t p0;
+            int wd;
+            slice_bounds<T>(Tsc, i >> 5, p0, wd);
             for (int j0 = 0; j0 < wd; j0 += kBatch) {
               int32_t cl[kBatch];
               T vv[kBatch], gv[kBatch];
@@ -989,6 +1003,7 @@ static SellView<T> none_view() {
   v.col = nullptr;
   v.val = nullptr;
   v.empty = true;
+  v.uw = -1;
   return v;
 }
 

@@ -59,6 +59,7 @@ struct Sell {
   int32_t* col = nullptr;        // [nslots], -1 = padding
   T* val = nullptr;              // [nslots] raw values
   T* dval = nullptr;             // [nslots] values / d[row] (optional)
+  int uw = -1;                   // every slice has this width (slice_ptr[s] = 32*uw*s), else -1
 };
 
 struct Levels {
