@@ -360,6 +360,61 @@ __global__ void __launch_bounds__(256) k_inner_out(int64_t n, SellView<T> Tm, co
   z[i] = (O)mul_rn<T>(w, g);
 }
 
+// k_inner_out with NR rows per thread (rows i, i+256, ... of a 256*NR-row tile): the loads of
+// all NR rows are issued before any is consumed.  For float32 a thread-per-row pass keeps only
+// half the bytes of the float64 pass in flight and is latency-bound; NR = 2 doubles them.
+template <typename T, typename O, bool GAMMA, int NR>
+__global__ void __launch_bounds__(256) k_inner_out_nr(int64_t n, SellView<T> Tm, const T* __restrict__ rd,
+                                                      const T* __restrict__ gin, O* __restrict__ z, T w, T gm,
+                                                      T gm1) {
+  const int64_t base = (int64_t)blockIdx.x * (256 * NR) + threadIdx.x;
+  RowFetch<T> ft[NR];
+  T rdi[NR], gi[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int64_t i = base + 256 * r;
+    rdi[r] = gi[r] = (T)0;
+    if (i < n) {
+      ft[r].start(Tm, i);
+      rdi[r] = rd[i];
+      if (GAMMA) gi[r] = gin[i];
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < NR; ++r) ft[r].load(0);
+#pragma unroll
+  for (int r = 0; r < NR; ++r) ft[r].gather(gin);
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int64_t i = base + 256 * r;
+    T t = ft[r].rest(gin, ft[r].accum((T)0));
+    T g = sub_rn<T>(rdi[r], mul_rn<T>(w, t));
+    if (GAMMA) g = add_rn<T>(mul_rn<T>(gm1, gi[r]), mul_rn<T>(gm, g));
+    if (i < n) z[i] = (O)mul_rn<T>(w, g);
+  }
+}
+
+// k_scale_rd for a float32 working dtype, two entries per thread (float2 / double2 accesses)
+__global__ void k_scale_rd_f32x2(int64_t n, const double* __restrict__ r, const float* __restrict__ d,
+                                 float* __restrict__ rd, long long* overflow) {
+  const int64_t i = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  if (i + 1 < n) {
+    const double2 rv = *reinterpret_cast<const double2*>(r + i);
+    const float2 dv = *reinterpret_cast<const float2*>(d + i);
+    const float t0 = (float)rv.x, t1 = (float)rv.y;
+    if (overflow) {
+      if (isinf(t0) && isfinite(rv.x)) atomicMin(overflow, (long long)i);
+      if (isinf(t1) && isfinite(rv.y)) atomicMin(overflow, (long long)(i + 1));
+    }
+    *reinterpret_cast<float2*>(rd + i) = make_float2(__fdiv_rn(t0, dv.x), __fdiv_rn(t1, dv.y));
+  } else if (i < n) {
+    const double rv = r[i];
+    const float t0 = (float)rv;
+    if (overflow && isinf(t0) && isfinite(rv)) atomicMin(overflow, (long long)i);
+    rd[i] = __fdiv_rn(t0, d[i]);
+  }
+}
+
 enum InnerFinal { kNotFinal = 0, kFinalAdd = 1, kFinalSet = 2 };
 
 // one inner JR step: gout = rd - w*(D^-1T gin)  or damped; last step updates x
@@ -1579,11 +1634,31 @@ static int precond_gs2_single(rs_matrix* m, const rs_relax_cfg& cfg, const R* r,
   if (twopass) {
     T* rd = (T*)m->scratch;
     T* bufs[2] = {rd + c.n, rd + 2 * c.n};
-    k_scale_rd<T, R><<<c.grid(), kB, 0, st>>>(c.n, r, c.d, rd, overflow);
+    // fp32 (single_inside_double): wide scale pass and 2 rows per thread in the final step
+    // (RS_F32_NR=1 restores the one-row kernels for A/B runs)
+    static const int nr_env = getenv("RS_F32_NR") ? atoi(getenv("RS_F32_NR")) : 2;
+    static const int nr64_env = getenv("RS_F64_NR") ? atoi(getenv("RS_F64_NR")) : 1;
+    const int nr = sizeof(T) == 4 ? nr_env : nr64_env;
+    const bool wide = sizeof(T) == 4 && sizeof(R) == 8 && nr >= 2 && ((uintptr_t)r % 16 == 0) &&
+                      ((uintptr_t)c.d % 8 == 0) && ((uintptr_t)rd % 8 == 0);
+    if (wide) {
+      k_scale_rd_f32x2<<<grid_for((c.n + 1) / 2, kB), kB, 0, st>>>(c.n, (const double*)r, (const float*)c.d,
+                                                                 (float*)rd, overflow);
+    } else {
+      k_scale_rd<T, R><<<c.grid(), kB, 0, st>>>(c.n, r, c.d, rd, overflow);
+    }
     RS_COUNT_LAUNCH();
     const T* gin = rd;
     for (int j = 0; j < cfg.n_j; ++j) {
-      if (j == cfg.n_j - 1) {
+      if (j == cfg.n_j - 1 && nr == 4) {
+        const int g4 = grid_for(c.n, 4 * kB);
+        if (damped) k_inner_out_nr<T, O, true, 4><<<g4, kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1);
+        else k_inner_out_nr<T, O, false, 4><<<g4, kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1);
+      } else if (j == cfg.n_j - 1 && nr >= 2) {
+        const int g2 = grid_for(c.n, 2 * kB);
+        if (damped) k_inner_out_nr<T, O, true, 2><<<g2, kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1);
+        else k_inner_out_nr<T, O, false, 2><<<g2, kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1);
+      } else if (j == cfg.n_j - 1) {
         if (damped) k_inner_out<T, O, true><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1);
         else k_inner_out<T, O, false><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1);
       } else {
