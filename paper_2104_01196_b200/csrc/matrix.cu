@@ -152,6 +152,14 @@ __global__ void k_count(Src src, BuildShape s, CountOut o) {
   }
 }
 
+__global__ void k_slice_range(const int32_t* w, int64_t ns, long long* rng) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < ns && w[s] > 0) {
+    atomicMin(rng, (long long)s);
+    atomicMax(rng + 1, (long long)s);
+  }
+}
+
 __global__ void k_uniform_slots(int64_t* sp, int64_t ns, int64_t per) {
   int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s <= ns) sp[s] = s * per;
@@ -282,6 +290,25 @@ static int alloc_sell(Sell<T>& s, int64_t nrows, int64_t nnz, const int32_t* d_w
   // 32*uw*s, so the sweep kernels compute the slice bounds instead of loading them (one
   // dependent memory round trip less per row); slice_ptr stays valid for every other user.
   s.uw = -1;
+  s.s_lo = 0;
+  s.s_hi = s.nslices;
+  if (s.nslots > 0 && s.nslices > 0) {
+    // range of non-empty slices: the off-block couplings of a row block live in its first / last
+    // planes only, and the sweep kernels skip every other row without touching slice_ptr
+    long long* rng = nullptr;
+    RS_CUDA(cudaMalloc(&rng, 2 * sizeof(long long)));
+    long long init[2] = {LLONG_MAX, -1};
+    RS_CUDA(cudaMemcpy(rng, init, sizeof(init), cudaMemcpyHostToDevice));
+    k_slice_range<<<grid_for(s.nslices, 256), 256>>>(d_width, s.nslices, rng);
+    RS_COUNT_LAUNCH();
+    long long hr[2];
+    RS_CUDA(cudaMemcpy(hr, rng, sizeof(hr), cudaMemcpyDeviceToHost));
+    cudaFree(rng);
+    if (hr[1] >= 0) {
+      s.s_lo = hr[0];
+      s.s_hi = hr[1] + 1;
+    }
+  }
   if (s.nslots > 0 && s.nslices > 0) {
     int32_t* dmax = nullptr;
     RS_CUDA(cudaMalloc(&dmax, sizeof(int32_t)));
@@ -676,6 +703,8 @@ static int cast_sell(const Sell<double>& a, Sell<float>& b, long long* bad, cons
   b.nnz = a.nnz;
   b.nslots = a.nslots;
   b.uw = a.uw;
+  b.s_lo = a.s_lo;
+  b.s_hi = a.s_hi;
   size_t ns = (size_t)std::max<int64_t>(a.nslots, 1);
   RS_CUDA(cudaMalloc(&b.slice_ptr, sizeof(int64_t) * (a.nslices + 1)));
   RS_CUDA(cudaMemcpy(b.slice_ptr, a.slice_ptr, sizeof(int64_t) * (a.nslices + 1), cudaMemcpyDeviceToDevice));

@@ -58,6 +58,7 @@ struct SellView {
   const T* __restrict__ val;
   bool empty;
   int uw;  // uniform slice width (Sell::uw) or -1
+  int64_t s_lo, s_hi;  // non-empty slice range
 };
 
 // first slot and width of slice s: computed for a uniform-width triangle, loaded otherwise
@@ -66,6 +67,9 @@ __device__ __forceinline__ void slice_bounds(const SellView<T>& m, int64_t s, in
   if (m.uw >= 0) {
     p0 = s * (int64_t)(32 * m.uw);
     w = m.uw;
+  } else if (s < m.s_lo || s >= m.s_hi) {
+    p0 = 0;
+    w = 0;
   } else {
     p0 = m.sp[s];
     w = (int)((m.sp[s + 1] - p0) >> 5);
@@ -80,6 +84,8 @@ static SellView<T> view(const Sell<T>& s, bool scaled) {
   v.val = scaled ? s.dval : s.val;
   v.empty = s.nslots == 0;
   v.uw = s.uw;
+  v.s_lo = s.s_lo;
+  v.s_hi = s.s_hi < 0 ? s.nslices : s.s_hi;
   return v;
 }
 
@@ -363,7 +369,8 @@ __global__ void __launch_bounds__(256) k_inner_out(int64_t n, SellView<T> Tm, co
 // k_inner_out with NR rows per thread (rows i, i+256, ... of a 256*NR-row tile): the loads of
 // all NR rows are issued before any is consumed.  For float32 a thread-per-row pass keeps only
 // half the bytes of the float64 pass in flight and is latency-bound; NR = 2 doubles them.
-template <typename T, typename O, bool GAMMA, int NR>
+// (MID: a middle inner step, z = g written in the working dtype; else the last one, z = w*g)
+template <typename T, typename O, bool GAMMA, int NR, bool MID = false>
 __global__ void __launch_bounds__(256) k_inner_out_nr(int64_t n, SellView<T> Tm, const T* __restrict__ rd,
                                                       const T* __restrict__ gin, O* __restrict__ z, T w, T gm,
                                                       T gm1) {
@@ -390,7 +397,7 @@ __global__ void __launch_bounds__(256) k_inner_out_nr(int64_t n, SellView<T> Tm,
     T t = ft[r].rest(gin, ft[r].accum((T)0));
     T g = sub_rn<T>(rdi[r], mul_rn<T>(w, t));
     if (GAMMA) g = add_rn<T>(mul_rn<T>(gm1, gi[r]), mul_rn<T>(gm, g));
-    if (i < n) z[i] = (O)mul_rn<T>(w, g);
+    if (i < n) z[i] = MID ? (O)g : (O)mul_rn<T>(w, g);
   }
 }
 
@@ -1059,6 +1066,8 @@ static SellView<T> none_view() {
   v.val = nullptr;
   v.empty = true;
   v.uw = -1;
+  v.s_lo = 0;
+  v.s_hi = 0;
   return v;
 }
 
@@ -1661,6 +1670,12 @@ static int precond_gs2_single(rs_matrix* m, const rs_relax_cfg& cfg, const R* r,
       } else if (j == cfg.n_j - 1) {
         if (damped) k_inner_out<T, O, true><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1);
         else k_inner_out<T, O, false><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1);
+      } else if (nr >= 2) {
+        T* gout = bufs[j & 1];
+        const int g2 = grid_for(c.n, 2 * kB);
+        if (damped) k_inner_out_nr<T, T, true, 2, true><<<g2, kB, 0, st>>>(c.n, Tm, rd, gin, gout, w, gm, gm1);
+        else k_inner_out_nr<T, T, false, 2, true><<<g2, kB, 0, st>>>(c.n, Tm, rd, gin, gout, w, gm, gm1);
+        gin = gout;
       } else {
         T* gout = bufs[j & 1];
         if (damped) k_inner<T, kNotFinal, true><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, gout, nullptr, w, gm, gm1);

@@ -91,11 +91,12 @@ def main():
                 ms = timeit(lambda: pc.apply_into(r, z))
                 print(json.dumps({"kernel": f"precond_gs2_nj{nj}", "ms": round(ms, 4), "gbs": round(by / ms / 1e6, 1)}),
                       flush=True)
-            pc = g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, 1), precision="single_inside_double")
-            by = 4 * a.nnz_l * 2 + 4 * (n + 1) + 8 * n + 4 * n + 8 * n
-            ms = timeit(lambda: pc.apply_into(r, z))
-            print(json.dumps({"kernel": "precond_gs2_nj1_f32", "ms": round(ms, 4), "gbs": round(by / ms / 1e6, 1)}),
-                  flush=True)
+            for nj in (1, 2):
+                pc = g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, nj), precision="single_inside_double")
+                by = nj * (4 * a.nnz_l * 2 + 4 * (n + 1)) + 8 * n + 4 * n + 8 * n
+                ms = timeit(lambda: pc.apply_into(r, z))
+                print(json.dumps({"kernel": f"precond_gs2_nj{nj}_f32", "ms": round(ms, 4),
+                                  "gbs": round(by / ms / 1e6, 1)}), flush=True)
         if "sweep" in which:
             from paper_2104_01196_b200 import _native as NN
             b = g2.random_rhs(n, 0, device="cuda")
