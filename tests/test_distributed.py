@@ -225,3 +225,71 @@ def test_hybrid_nt2_matches_reference_fixture(sweeps_golden):
     res = _run_ranks(3, fn)
     z = np.concatenate([t[1] for t in sorted(res, key=lambda t: t[0])])
     assert np.array_equal(z, z_ref)
+
+
+class _ThreadPeerComm(ThreadComm):
+    """Thread ranks whose halo exchange and Gram-Schmidt reductions run through the peer-memory
+    mailboxes (rs_peer_connect_local: the ranks share one process, so raw pointers are exchanged)."""
+
+    peer = True
+    local_group = True
+
+
+def _run_ranks_cls(nranks, fn, cls):
+    import threading
+
+    comms = [cls(c.sh, c.rank) for c in ThreadComm.group(nranks)]
+    res, errs = [None] * nranks, []
+
+    def run(c):
+        try:
+            torch.cuda.set_device(0)
+            with torch.cuda.stream(torch.cuda.Stream()):
+                res[c.rank] = fn(c)
+                torch.cuda.current_stream().synchronize()
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+            c.sh.bar.abort()
+
+    ths = [threading.Thread(target=run, args=(c,)) for c in comms]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    if errs:
+        raise errs[0]
+    return res
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nparts", [3, 8])
+def test_peer_mailboxes_thread_ranks_bitwise(nparts, gmres_golden):
+    """P ranks as threads on one GPU: the NVLink-peer code path (mailbox halo push / wait kernel,
+    allreduces fused into the DCGS2 kernels) at P = 3 and 8 -- the 8-rank layout the 8-GPU box
+    runs -- gives histories bitwise equal to the host rank-order reductions of ThreadComm, and
+    the reference hybrid_relax count."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2104_01196_b200 as g2
+    from paper_2104_01196_b200 import distributed as gd
+
+    a = g2.laplace3d(32)
+
+    def fn(comm):
+        A = gd.DistMatrix.from_csr(comm, a)
+        assert (A.mailbox is not None) == bool(getattr(comm, "peer", False))
+        b = gd.local_rhs(A, 0)
+        pc = gd.HybridPreconditioner(A, g2.RelaxConfig(1, 1, 1))
+        x, h = gd.gmres(A, b, pc, restart=60, tol=1e-9)
+        out = (np.asarray(h.rel_res), x.cpu().numpy())
+        A.close()
+        return out
+
+    host = _run_ranks_cls(nparts, fn, ThreadComm)
+    peer = _run_ranks_cls(nparts, fn, _ThreadPeerComm)
+    for r in range(nparts):
+        assert np.array_equal(host[r][0], peer[r][0]), f"rank {r}: histories differ"
+        assert np.array_equal(host[r][1], peer[r][1]), f"rank {r}: iterates differ"
+    key = f"lap3d_32__m60__hybrid_gs2_1_1_1__P{nparts}"
+    if key in gmres_golden["runs"]:
+        assert abs(len(peer[0][0]) - 1 - gmres_golden["runs"][key]["iterations"]) <= 1
