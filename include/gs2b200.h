@@ -125,6 +125,13 @@ int rs_mat_set_coloring(rs_matrix_t m, const int64_t *color, int64_t ncolors);
  * x_lo / x_hi: halo values below / above the block (NULL when halo is empty). */
 int rs_spmv(rs_matrix_t m, const void *x, const void *x_lo, const void *x_hi, void *y, rs_stream_t stream);
 
+/* CG's SpMV fused with the reduction that follows it (krylov.py:289-298; float64, a matrix
+ * without off-block couplings): rs_spmv_dot: y = A x and *xdoty = x.y (p^T A p);
+ * rs_resid_norm2: *nrm2 = ||b - A x||^2 without storing the residual.  Scalars stay on the
+ * device (stream-ordered); the row sums are rs_spmv's, the reductions fixed-order trees. */
+int rs_spmv_dot(rs_matrix_t m, const double *x, double *y, double *xdoty, rs_stream_t stream);
+int rs_resid_norm2(rs_matrix_t m, const double *b, const double *x, double *nrm2, rs_stream_t stream);
+
 /* gs_sequential_sweep (relax.py:177-190) / gs_ordered_sweep (_kernels.py:24-39),
  * level-scheduled: rows of one dependency level run in parallel, x in place.
  * Bitwise equal to the sequential natural-order sweep. */

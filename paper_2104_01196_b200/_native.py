@@ -62,6 +62,8 @@ _SIGS = {
     "rs_mat_set_coloring": ([_P, _P, C.c_int64], C.c_int),
     "rs_mt_gs_sweep": ([_P, _P, _P, C.c_int, C.c_double, _P], C.c_int),
     "rs_spmv": ([_P, _P, _P, _P, _P, _P], C.c_int),
+    "rs_spmv_dot": ([_P, _P, _P, _P, _P], C.c_int),
+    "rs_resid_norm2": ([_P, _P, _P, _P, _P], C.c_int),
     "rs_gs_sweep": ([_P, _P, _P, C.c_int, C.c_double, _P], C.c_int),
     "rs_jr_sweeps": ([_P, _P, _P, C.c_int, C.c_double, _P], C.c_int),
     "rs_inner_jr": ([_P, _P, _P, C.c_int, C.c_int, C.c_double, C.c_double, _P], C.c_int),

@@ -479,6 +479,16 @@ void destroy(rs_matrix* m) {
   delete m;
 }
 
+int ensure_reduction(rs_matrix* m, int64_t n_doubles) {
+  if (m->red && m->red_cap >= n_doubles) return RS_OK;
+  cudaFree(m->red);
+  m->red = nullptr;
+  m->red_cap = 0;
+  RS_CUDA(cudaMalloc(&m->red, sizeof(double) * std::max<int64_t>(n_doubles, 1)));
+  m->red_cap = n_doubles;
+  return RS_OK;
+}
+
 int ensure_scratch(rs_matrix* m) {
   if (m->scratch) return RS_OK;
   size_t es = m->dtype == RS_F32 ? 4 : 8;

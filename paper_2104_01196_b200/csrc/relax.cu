@@ -238,6 +238,62 @@ __global__ void __launch_bounds__(256) k_resid(int64_t n, SellView<T> Elo, SellV
   }
 }
 
+// SpMV fused with the reduction CG takes right after it (krylov.py:289-298), per-block partials:
+//   RED_DOT:  y = A x, partial = sum_i x_i y_i          (p^T A p)
+//   RED_NORM: partial = sum_i (b_i - (A x)_i)^2          (||b - A x||^2, nothing stored)
+// The row sums are k_resid's (bitwise the reference SpMV); the reductions are fixed-order trees.
+enum RedMode { kRedDot = 0, kRedNorm = 1 };
+template <int MODE>
+__global__ void __launch_bounds__(256) k_spmv_red(int64_t n, SellView<double> L, SellView<double> U,
+                                                  const double* __restrict__ d, const double* __restrict__ x,
+                                                  const double* __restrict__ b, double* __restrict__ y,
+                                                  double* __restrict__ partial) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double v = 0.0;
+  if (i < n) {
+    int64_t pu0 = 0;
+    int uwd = 0;
+    if (!U.empty) slice_bounds<double>(U, i >> 5, pu0, uwd);
+    const double di = d[i];
+    const double xi = x[i];
+    double acc = row_accum<double>(L, i, x, 0.0);
+    acc = add_rn<double>(acc, mul_rn<double>(di, xi));
+    acc = row_accum_p<double>(U, pu0, uwd, i, x, acc);
+    if (MODE == kRedDot) {
+      y[i] = acc;
+      v = xi * acc;
+    } else {
+      const double t = sub_rn<double>(b[i], acc);
+      v = t * t;
+    }
+  }
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __shared__ double red[8];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < 8; ++q) t += red[q];
+    partial[blockIdx.x] = t;
+  }
+}
+
+// out = sum of nblk partials, one 1024-thread block, fixed order (deterministic)
+__global__ void __launch_bounds__(1024) k_reduce_many(const double* __restrict__ partial, int64_t nblk,
+                                                      double* __restrict__ out) {
+  double v = 0.0;
+  for (int64_t b = threadIdx.x; b < nblk; b += 1024) v += partial[b];
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < 32; ++q) t += red[q];
+    *out = t;
+  }
+}
+
 // bhat = (b - A_full x) + A_pp x   (relax.py:261-264), y and A_pp x from the same row walk
 template <typename T>
 __global__ void __launch_bounds__(256) k_bhat(int64_t n, SellView<T> Elo, SellView<T> L, SellView<T> U,
@@ -1782,6 +1838,43 @@ int rs_spmv(rs_matrix_t m, const void* x, const void* x_lo, const void* x_hi, vo
   return m->dtype == RS_F32 ? spmv_t<float>(m, (const float*)x, (const float*)x_lo, (const float*)x_hi, (float*)y, st)
                             : spmv_t<double>(m, (const double*)x, (const double*)x_lo, (const double*)x_hi,
                                              (double*)y, st);
+}
+
+static int spmv_red(rs_matrix_t m, int mode, const double* x, const double* b, double* y, double* out,
+                    rs_stream_t stream) {
+  if (!m || !x || !out || (mode == kRedDot && !y) || (mode == kRedNorm && !b)) {
+    set_error(RS_ERR_ARG, "rs_spmv_dot / rs_resid_norm2: bad arguments");
+    return RS_ERR_ARG;
+  }
+  RS_CUDA(cudaSetDevice(m->device));
+  if (m->dtype != RS_F64 || m->Elo64.nslots || m->Ehi64.nslots) {
+    set_error(RS_ERR_UNSUPPORTED, "rs_spmv_dot / rs_resid_norm2: float64 matrix without off-block couplings");
+    return RS_ERR_UNSUPPORTED;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = m->nrows;
+  const int64_t nblk = std::max<int64_t>(grid_for(std::max<int64_t>(n, 1), kB), 1);
+  int e;
+  if ((e = ensure_reduction(m, nblk))) return e;
+  SellView<double> Lv = view(m->L64, false), Uv = view(m->U64, false);
+  const double* d = (const double*)m->d;
+  if (mode == kRedDot)
+    k_spmv_red<kRedDot><<<nblk, kB, 0, st>>>(n, Lv, Uv, d, x, b, y, m->red);
+  else
+    k_spmv_red<kRedNorm><<<nblk, kB, 0, st>>>(n, Lv, Uv, d, x, b, y, m->red);
+  RS_COUNT_LAUNCH();
+  k_reduce_many<<<1, 1024, 0, st>>>(m->red, nblk, out);
+  RS_COUNT_LAUNCH();
+  RS_CHECK_LAUNCH("spmv_red");
+  return RS_OK;
+}
+
+int rs_spmv_dot(rs_matrix_t m, const double* x, double* y, double* xdoty, rs_stream_t stream) {
+  return spmv_red(m, kRedDot, x, nullptr, y, xdoty, stream);
+}
+
+int rs_resid_norm2(rs_matrix_t m, const double* b, const double* x, double* nrm2, rs_stream_t stream) {
+  return spmv_red(m, kRedNorm, x, b, nullptr, nrm2, stream);
 }
 
 int rs_hybrid_bhat(rs_matrix_t m, const void* b, const void* x, const void* x_lo, const void* x_hi, void* bhat,

@@ -759,11 +759,10 @@ def cg(a, b, m=None, tol: float = 1e-9, maxit: int = 10000, x0=None):
     def enqueue(k):
         """CG iteration k entirely on the device (krylov.py:288-308), scalars staged to pinned slot k%2."""
         xin, xout = xs[k % 2], xs[(k + 1) % 2]
-        chk(lib.rs_spmv(dm.handle, _p(p), None, None, _p(ap), st), "spmv")
-        chk(lib.rs_dot(n, _p(p), _p(ap), _p(pap_s), _p(work), st), "dot")
+        # SpMV fused with p^T A p, and the true residual norm without storing b - A x
+        chk(lib.rs_spmv_dot(dm.handle, _p(p), _p(ap), _p(pap_s), st), "spmv_dot")
         chk(lib.rs_cg_update(n, _p(rz_s[k % 2]), _p(pap_s), _p(xin), _p(p), _p(xout), _p(r), _p(ap), st), "cg")
-        chk(lib.rs_spmv(dm.handle, _p(xout), None, None, _p(t), st), "spmv")
-        chk(lib.rs_sub_norm(n, _p(bt), _p(t), _p(t), _p(res_s), _p(work), st), "sub_norm")
+        chk(lib.rs_resid_norm2(dm.handle, _p(bt), _p(xout), _p(res_s), st), "resid_norm2")
         if fp32:
             _WS.flags[1] = _I64_MAX
         _apply_op(op, r, z, _WS)
