@@ -537,3 +537,34 @@ def test_gmres_dcgs2_128():
     b = g2.random_rhs(a.nrows, 0, device="cuda")
     _, h = g2.gmres(a, b, g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, 1)), restart=60, tol=1e-9, ortho="dcgs2")
     assert h.converged and h.iterations == REF_128[("gs2", (1, 1, 1))], h.iterations
+
+
+@pytest.mark.parametrize("shape", [(20, 17, 9), (33, 33, 33)])
+def test_fused_spmv_reductions(shape):
+    """rs_spmv_dot / rs_resid_norm2 (CG's fused SpMV + reduction): the product is bitwise rs_spmv's
+    (the reference csr_matvec), the scalars match the oracle's to 1e-13."""
+    import ctypes as C
+
+    from paper_2104_01196_b200 import _native
+
+    lib = _native.load()
+    a = g2.laplace3d(*shape)
+    dm = a.device(0)
+    n = a.nrows
+    x = torch.from_numpy(g2.random_rhs(n, 1)).cuda()
+    b = torch.from_numpy(g2.random_rhs(n, 0)).cuda()
+    y, y2 = torch.empty_like(x), torch.empty_like(x)
+    sc = torch.zeros(2, dtype=torch.float64, device="cuda")
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    _native.check(lib.rs_spmv(dm.handle, p(x), None, None, p(y), st), "spmv")
+    _native.check(lib.rs_spmv_dot(dm.handle, p(x), p(y2), p(sc[0:1]), st), "spmv_dot")
+    _native.check(lib.rs_resid_norm2(dm.handle, p(b), p(x), p(sc[1:2]), st), "resid_norm2")
+    torch.cuda.synchronize()
+    assert torch.equal(y, y2)
+    yo = oracle.spmv(oracle.Matrix(a), x.cpu().numpy())
+    assert np.array_equal(y.cpu().numpy(), yo)
+    want_dot = float(np.dot(x.cpu().numpy(), yo))
+    want_res = float(np.dot(b.cpu().numpy() - yo, b.cpu().numpy() - yo))
+    assert abs(float(sc[0]) - want_dot) <= 1e-13 * abs(want_dot)
+    assert abs(float(sc[1]) - want_res) <= 1e-13 * abs(want_res)
