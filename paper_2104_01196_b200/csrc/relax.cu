@@ -76,6 +76,41 @@ __device__ __forceinline__ void slice_bounds(const SellView<T>& m, int64_t s, in
   }
 }
 
+// Software L2 prefetch for the row-per-thread passes: every warp prefetches the lines the warp
+// handling rows D ahead will read (its slice of each uniform-width triangle and the dense row
+// vectors), one line per lane.  A prefetch holds no register, so it raises the bytes in flight
+// without costing occupancy; RS_PF_DIST = D in rows (0 disables; read once per process).
+static int pf_dist_host() {
+  static const int v = getenv("RS_PF_DIST") ? atoi(getenv("RS_PF_DIST")) : 65536;
+  return v;
+}
+__device__ __forceinline__ void pf_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+// lane `q` (0-based within the warp's prefetch set) prefetches one line of slice s of triangle m
+// (columns: uw lines of 128 B, values: uw * sizeof(T) / 4 lines); returns the number of lines
+template <typename T>
+__device__ __forceinline__ int pf_sell(const SellView<T>& m, int64_t s, int q) {
+  if (m.empty || m.uw <= 0) return 0;
+  const int vl = (int)(sizeof(T) / 4);  // value lines per slot row (32 values)
+  const int64_t base = s * (int64_t)(32 * m.uw);
+  const int nl = m.uw * (1 + vl);
+  if (q >= 0 && q < nl) {
+    if (q < m.uw) pf_l2(m.col + base + 32 * q);
+    else {
+      const int r = q - m.uw;
+      pf_l2(m.val + base + 32 * (r / vl) + (32 / vl) * (r % vl));
+    }
+  }
+  return nl;
+}
+// one line per lane of the slice's 32 entries of a dense vector (1 or 2 lines)
+template <typename T>
+__device__ __forceinline__ int pf_vec(const T* v, int64_t s, int q) {
+  const int vl = (int)(sizeof(T) / 4);
+  if (v && q >= 0 && q < vl) pf_l2(v + s * 32 + (32 / vl) * q);
+  return v ? vl : 0;
+}
+
 template <typename T>
 static SellView<T> view(const Sell<T>& s, bool scaled) {
   SellView<T> v;
@@ -213,8 +248,17 @@ template <typename T, int MODE>
 __global__ void __launch_bounds__(256) k_resid(int64_t n, SellView<T> Elo, SellView<T> L, SellView<T> U,
                                                SellView<T> Ehi, const T* __restrict__ d, const T* __restrict__ x,
                                                const T* __restrict__ xlo, const T* __restrict__ xhi,
-                                               const T* __restrict__ b, T* __restrict__ out, T w) {
+                                               const T* __restrict__ b, T* __restrict__ out, T w, int pf) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pf && i + pf < n) {
+    const int64_t s2 = (i + pf) >> 5;
+    int q = (int)(i & 31);
+    q -= pf_sell<T>(L, s2, q);
+    q -= pf_sell<T>(U, s2, q);
+    q -= pf_vec<T>(d, s2, q);
+    q -= pf_vec<T>(x, s2, q);
+    if (MODE != kSpmv) q -= pf_vec<T>(b, s2, q);
+  }
   if (i >= n) return;
   // the U slice bounds and the row's own operands do not depend on the L walk: fetch them first
   int64_t pu0 = 0;
@@ -247,8 +291,17 @@ template <int MODE>
 __global__ void __launch_bounds__(256) k_spmv_red(int64_t n, SellView<double> L, SellView<double> U,
                                                   const double* __restrict__ d, const double* __restrict__ x,
                                                   const double* __restrict__ b, double* __restrict__ y,
-                                                  double* __restrict__ partial) {
+                                                  double* __restrict__ partial, int pf) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pf && i + pf < n) {
+    const int64_t s2 = (i + pf) >> 5;
+    int q = (int)(i & 31);
+    q -= pf_sell<double>(L, s2, q);
+    q -= pf_sell<double>(U, s2, q);
+    q -= pf_vec<double>(d, s2, q);
+    q -= pf_vec<double>(x, s2, q);
+    if (MODE == kRedNorm) q -= pf_vec<double>(b, s2, q);
+  }
   double v = 0.0;
   if (i < n) {
     int64_t pu0 = 0;
@@ -318,8 +371,16 @@ __global__ void __launch_bounds__(256) k_bhat(int64_t n, SellView<T> Elo, SellVi
 template <typename T, bool DAMPED>
 __global__ void __launch_bounds__(256) k_compact(int64_t n, SellView<T> Tm, const T* __restrict__ d,
                                                  const T* __restrict__ x, const T* __restrict__ b,
-                                                 T* __restrict__ rd, T c) {
+                                                 T* __restrict__ rd, T c, int pf) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pf && i + pf < n) {
+    const int64_t s2 = (i + pf) >> 5;
+    int q = (int)(i & 31);
+    q -= pf_sell<T>(Tm, s2, q);
+    q -= pf_vec<T>(d, s2, q);
+    q -= pf_vec<T>(x, s2, q);
+    q -= pf_vec<T>(b, s2, q);
+  }
   if (i >= n) return;
   T t = sub_rn<T>(b[i], row_accum<T>(Tm, i, x, (T)0));
   const T di = d[i];
@@ -407,8 +468,16 @@ __global__ void k_scale0(int64_t n, const R* __restrict__ r, const T* __restrict
 // last inner step writing z = w*g as O (generic zero-start chain, n_j >= 2)
 template <typename T, typename O, bool GAMMA>
 __global__ void __launch_bounds__(256) k_inner_out(int64_t n, SellView<T> Tm, const T* __restrict__ rd,
-                                                   const T* __restrict__ gin, O* __restrict__ z, T w, T gm, T gm1) {
+                                                   const T* __restrict__ gin, O* __restrict__ z, T w, T gm, T gm1,
+                                                   int pf) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pf && i + pf < n) {
+    const int64_t s2 = (i + pf) >> 5;
+    int q = (int)(i & 31);
+    q -= pf_sell<T>(Tm, s2, q);
+    q -= pf_vec<T>(rd, s2, q);
+    if (GAMMA && gin != rd) q -= pf_vec<T>(gin, s2, q);
+  }
   if (i >= n) return;
   RowFetch<T> ft;
   ft.start(Tm, i);
@@ -429,8 +498,20 @@ __global__ void __launch_bounds__(256) k_inner_out(int64_t n, SellView<T> Tm, co
 template <typename T, typename O, bool GAMMA, int NR, bool MID = false>
 __global__ void __launch_bounds__(256) k_inner_out_nr(int64_t n, SellView<T> Tm, const T* __restrict__ rd,
                                                       const T* __restrict__ gin, O* __restrict__ z, T w, T gm,
-                                                      T gm1) {
+                                                      T gm1, int pf) {
   const int64_t base = (int64_t)blockIdx.x * (256 * NR) + threadIdx.x;
+  if (pf) {
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int64_t i2 = base + 256 * r + pf;
+      if (i2 < n) {
+        int q = (int)(threadIdx.x & 31);
+        q -= pf_sell<T>(Tm, i2 >> 5, q);
+        q -= pf_vec<T>(rd, i2 >> 5, q);
+        if (GAMMA && gin != rd) q -= pf_vec<T>(gin, i2 >> 5, q);
+      }
+    }
+  }
   RowFetch<T> ft[NR];
   T rdi[NR], gi[NR];
 #pragma unroll
@@ -484,8 +565,16 @@ enum InnerFinal { kNotFinal = 0, kFinalAdd = 1, kFinalSet = 2 };
 template <typename T, int FINAL, bool GAMMA>
 __global__ void __launch_bounds__(256) k_inner(int64_t n, SellView<T> Tm, const T* __restrict__ rd,
                                                const T* __restrict__ gin, T* __restrict__ gout, T* __restrict__ x,
-                                               T w, T gm, T gm1) {
+                                               T w, T gm, T gm1, int pf) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pf && i + pf < n) {
+    const int64_t s2 = (i + pf) >> 5;
+    int q = (int)(i & 31);
+    q -= pf_sell<T>(Tm, s2, q);
+    q -= pf_vec<T>(rd, s2, q);
+    if (GAMMA && gin != rd) q -= pf_vec<T>(gin, s2, q);
+    if (FINAL == kFinalAdd) q -= pf_vec<T>(x, s2, q);
+  }
   if (i >= n) return;
   RowFetch<T> ft;
   ft.start(Tm, i);
@@ -1156,29 +1245,29 @@ static int inner_chain(Ctx<T>& c, T* rd, T* ga, T* gb, T* x, int n_j, int backwa
     T* gout = bufs[j & 1];
     if (!last) {
       if (damped) {
-        k_inner<T, kNotFinal, true><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1);
+        k_inner<T, kNotFinal, true><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1, pf_dist_host());
         RS_COUNT_LAUNCH();
       }
       else {
-        k_inner<T, kNotFinal, false><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1);
+        k_inner<T, kNotFinal, false><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1, pf_dist_host());
         RS_COUNT_LAUNCH();
       }
     } else if (compact) {
       if (damped) {
-        k_inner<T, kFinalSet, true><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1);
+        k_inner<T, kFinalSet, true><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1, pf_dist_host());
         RS_COUNT_LAUNCH();
       }
       else {
-        k_inner<T, kFinalSet, false><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1);
+        k_inner<T, kFinalSet, false><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1, pf_dist_host());
         RS_COUNT_LAUNCH();
       }
     } else {
       if (damped) {
-        k_inner<T, kFinalAdd, true><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1);
+        k_inner<T, kFinalAdd, true><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1, pf_dist_host());
         RS_COUNT_LAUNCH();
       }
       else {
-        k_inner<T, kFinalAdd, false><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1);
+        k_inner<T, kFinalAdd, false><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1, pf_dist_host());
         RS_COUNT_LAUNCH();
       }
     }
@@ -1201,7 +1290,7 @@ static int two_stage(Ctx<T>& c, const T* b, T* x, int n_j, int backward, int for
     // bitwise): one fused pass into the spare buffer + copy-back instead of rd pass + update pass
     T* alt = rd + 3 * c.n;
     k_resid<T, kJr><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x, nullptr,
-                                               nullptr, b, alt, (T)omega);
+                                               nullptr, b, alt, (T)omega, pf_dist_host());
     RS_COUNT_LAUNCH();
     RS_CUDA(cudaMemcpyAsync(x, alt, sizeof(T) * c.n, cudaMemcpyDeviceToDevice, c.st));
     return RS_OK;
@@ -1216,16 +1305,16 @@ static int two_stage(Ctx<T>& c, const T* b, T* x, int n_j, int backward, int for
     RS_COUNT_LAUNCH();
   } else if (!compact) {
     k_resid<T, kResidRd><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x, nullptr,
-                                                     nullptr, b, rd, (T)0);
+                                                     nullptr, b, rd, (T)0, pf_dist_host());
     RS_COUNT_LAUNCH();
   } else {
     SellView<T> Tm = backward ? c.L : c.U;
     if (omega != 1.0) {
       T cc = (T)(1.0 - 1.0 / omega);
-      k_compact<T, true><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, c.d, x, b, rd, cc);
+      k_compact<T, true><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, c.d, x, b, rd, cc, pf_dist_host());
       RS_COUNT_LAUNCH();
     } else {
-      k_compact<T, false><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, c.d, x, b, rd, (T)0);
+      k_compact<T, false><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, c.d, x, b, rd, (T)0, pf_dist_host());
       RS_COUNT_LAUNCH();
     }
   }
@@ -1490,7 +1579,7 @@ static int jr_sweeps_t(rs_matrix* m, const T* b, T* x, int sweeps, double omega,
     }
     T* nxt = cur == x ? alt : x;
     k_resid<T, kJr><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, cur, nullptr,
-                                               nullptr, b, nxt, w);
+                                               nullptr, b, nxt, w, pf_dist_host());
     RS_COUNT_LAUNCH();
     cur = nxt;
   }
@@ -1624,11 +1713,11 @@ static int inner_jr_t(rs_matrix* m, const T* r, T* g, int n_j, int backward, dou
   for (int j = 0; j < n_j; ++j) {
     T* gout = j == n_j - 1 ? g : ((j & 1) ? gb : ga);
     if (gamma != 1.0) {
-      k_inner<T, kNotFinal, true><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, gout, nullptr, w, gm, gm1);
+      k_inner<T, kNotFinal, true><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, gout, nullptr, w, gm, gm1, pf_dist_host());
       RS_COUNT_LAUNCH();
     }
     else {
-      k_inner<T, kNotFinal, false><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, gout, nullptr, w, gm, gm1);
+      k_inner<T, kNotFinal, false><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, gout, nullptr, w, gm, gm1, pf_dist_host());
       RS_COUNT_LAUNCH();
     }
     gin = gout;
@@ -1645,7 +1734,7 @@ static int spmv_t(rs_matrix* m, const T* x, const T* xlo, const T* xhi, T* y, cu
     return RS_ERR_ARG;
   }
   if (c.n) {
-    k_resid<T, kSpmv><<<c.grid(), kB, 0, st>>>(c.n, c.Elo, c.L, c.U, c.Ehi, c.d, x, xlo, xhi, nullptr, y, (T)0);
+    k_resid<T, kSpmv><<<c.grid(), kB, 0, st>>>(c.n, c.Elo, c.L, c.U, c.Ehi, c.d, x, xlo, xhi, nullptr, y, (T)0, pf_dist_host());
     RS_COUNT_LAUNCH();
   }
   RS_CHECK_LAUNCH("spmv");
@@ -1717,25 +1806,25 @@ static int precond_gs2_single(rs_matrix* m, const rs_relax_cfg& cfg, const R* r,
     for (int j = 0; j < cfg.n_j; ++j) {
       if (j == cfg.n_j - 1 && nr == 4) {
         const int g4 = grid_for(c.n, 4 * kB);
-        if (damped) k_inner_out_nr<T, O, true, 4><<<g4, kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1);
-        else k_inner_out_nr<T, O, false, 4><<<g4, kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1);
+        if (damped) k_inner_out_nr<T, O, true, 4><<<g4, kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1, pf_dist_host());
+        else k_inner_out_nr<T, O, false, 4><<<g4, kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1, pf_dist_host());
       } else if (j == cfg.n_j - 1 && nr >= 2) {
         const int g2 = grid_for(c.n, 2 * kB);
-        if (damped) k_inner_out_nr<T, O, true, 2><<<g2, kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1);
-        else k_inner_out_nr<T, O, false, 2><<<g2, kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1);
+        if (damped) k_inner_out_nr<T, O, true, 2><<<g2, kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1, pf_dist_host());
+        else k_inner_out_nr<T, O, false, 2><<<g2, kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1, pf_dist_host());
       } else if (j == cfg.n_j - 1) {
-        if (damped) k_inner_out<T, O, true><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1);
-        else k_inner_out<T, O, false><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1);
+        if (damped) k_inner_out<T, O, true><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1, pf_dist_host());
+        else k_inner_out<T, O, false><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1, pf_dist_host());
       } else if (nr >= 2) {
         T* gout = bufs[j & 1];
         const int g2 = grid_for(c.n, 2 * kB);
-        if (damped) k_inner_out_nr<T, T, true, 2, true><<<g2, kB, 0, st>>>(c.n, Tm, rd, gin, gout, w, gm, gm1);
-        else k_inner_out_nr<T, T, false, 2, true><<<g2, kB, 0, st>>>(c.n, Tm, rd, gin, gout, w, gm, gm1);
+        if (damped) k_inner_out_nr<T, T, true, 2, true><<<g2, kB, 0, st>>>(c.n, Tm, rd, gin, gout, w, gm, gm1, pf_dist_host());
+        else k_inner_out_nr<T, T, false, 2, true><<<g2, kB, 0, st>>>(c.n, Tm, rd, gin, gout, w, gm, gm1, pf_dist_host());
         gin = gout;
       } else {
         T* gout = bufs[j & 1];
-        if (damped) k_inner<T, kNotFinal, true><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, gout, nullptr, w, gm, gm1);
-        else k_inner<T, kNotFinal, false><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, gout, nullptr, w, gm, gm1);
+        if (damped) k_inner<T, kNotFinal, true><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, gout, nullptr, w, gm, gm1, pf_dist_host());
+        else k_inner<T, kNotFinal, false><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, gout, nullptr, w, gm, gm1, pf_dist_host());
         gin = gout;
       }
       RS_COUNT_LAUNCH();
@@ -1758,12 +1847,12 @@ static int precond_gs2_single(rs_matrix* m, const rs_relax_cfg& cfg, const R* r,
   const T* gin = bufs[0];
   for (int j = 1; j < cfg.n_j; ++j) {
     if (j == cfg.n_j - 1) {
-      if (damped) k_inner_out<T, O, true><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1);
-      else k_inner_out<T, O, false><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1);
+      if (damped) k_inner_out<T, O, true><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1, pf_dist_host());
+      else k_inner_out<T, O, false><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1, pf_dist_host());
     } else {
       T* gout = bufs[j & 1];
-      if (damped) k_inner<T, kNotFinal, true><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, gout, nullptr, w, gm, gm1);
-      else k_inner<T, kNotFinal, false><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, gout, nullptr, w, gm, gm1);
+      if (damped) k_inner<T, kNotFinal, true><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, gout, nullptr, w, gm, gm1, pf_dist_host());
+      else k_inner<T, kNotFinal, false><<<c.grid(), kB, 0, st>>>(c.n, Tm, rd, gin, gout, nullptr, w, gm, gm1, pf_dist_host());
       gin = gout;
     }
     RS_COUNT_LAUNCH();
@@ -1859,9 +1948,9 @@ static int spmv_red(rs_matrix_t m, int mode, const double* x, const double* b, d
   SellView<double> Lv = view(m->L64, false), Uv = view(m->U64, false);
   const double* d = (const double*)m->d;
   if (mode == kRedDot)
-    k_spmv_red<kRedDot><<<nblk, kB, 0, st>>>(n, Lv, Uv, d, x, b, y, m->red);
+    k_spmv_red<kRedDot><<<nblk, kB, 0, st>>>(n, Lv, Uv, d, x, b, y, m->red, pf_dist_host());
   else
-    k_spmv_red<kRedNorm><<<nblk, kB, 0, st>>>(n, Lv, Uv, d, x, b, y, m->red);
+    k_spmv_red<kRedNorm><<<nblk, kB, 0, st>>>(n, Lv, Uv, d, x, b, y, m->red, pf_dist_host());
   RS_COUNT_LAUNCH();
   k_reduce_many<<<1, 1024, 0, st>>>(m->red, nblk, out);
   RS_COUNT_LAUNCH();
