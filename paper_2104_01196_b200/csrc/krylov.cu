@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
           int64_t n, int ch, int kCgsStages, int64_t rows_per_blk, const double* __restrict__ h_in,
           double* __restrict__ w, double* __restrict__ partial, int* nonfinite, double* __restrict__ h_out,
           double* __restrict__ nrm2_out, unsigned int* ticket, const PeerArgs pa, const int64_t* flags_in,
-          double* status_out, double* __restrict__ vout, double* __restrict__ uout) {
+          double* status_out, double* __restrict__ vout, double* __restrict__ uout, int opts) {
   // Two warp groups ping-pong the chunks of this CTA's row range (group g takes
   // chunks c = g, g+2, ...), each synchronising on its own named barrier, so one
   // group's update / dots compute overlaps the other's; the TMA ring is shared.
@@ -596,19 +596,51 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     if (DOTS && DCGS) {
       // dual dots against w and against the tile's last basis row u (both from shared memory)
       const double* us = Vs + (size_t)(k - 1) * ch;
+      if ((opts & 1) && ch <= 32 * kCgsMaxT) {
+        // w and u of the lane's rows cached in registers: one shared-memory load per basis
+        // element for the two FMAs instead of three (the pass is close to the shared-memory
+        // bandwidth, which scales with the power-capped SM clock); same summation order
+        double wr[kCgsMaxT], ur[kCgsMaxT];
 #pragma unroll
-      for (int q = 0; q < kQ; ++q) {
-        const int i = gwarp + q * kGW;
-        if (i < k) {
-          const double* vi = Vs + (size_t)i * ch;
-          double a0 = 0.0, b0 = 0.0;
-          for (int r = lane; r < len; r += 32) {
-            const double x = vi[r];
-            a0 += x * ws[r];
-            b0 += x * us[r];
+        for (int t = 0; t < kCgsMaxT; ++t) {
+          const int r = lane + 32 * t;
+          wr[t] = r < len ? ws[r] : 0.0;
+          ur[t] = r < len ? us[r] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+          const int i = gwarp + q * kGW;
+          if (i < k) {
+            const double* vi = Vs + (size_t)i * ch;
+            double a0 = 0.0, b0 = 0.0;
+#pragma unroll
+            for (int t = 0; t < kCgsMaxT; ++t) {
+              const int r = lane + 32 * t;
+              if (r < len) {
+                const double x = vi[r];
+                a0 += x * wr[t];
+                b0 += x * ur[t];
+              }
+            }
+            acc[q] += a0;
+            acc2[q] += b0;
           }
-          acc[q] += a0;
-          acc2[q] += b0;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+          const int i = gwarp + q * kGW;
+          if (i < k) {
+            const double* vi = Vs + (size_t)i * ch;
+            double a0 = 0.0, b0 = 0.0;
+            for (int r = lane; r < len; r += 32) {
+              const double x = vi[r];
+              a0 += x * ws[r];
+              b0 += x * us[r];
+            }
+            acc[q] += a0;
+            acc2[q] += b0;
+          }
         }
       }
     } else if (DOTS) {
@@ -889,12 +921,14 @@ static int cgs_pass(const double* V, int64_t ldv, int k, int64_t n, const double
   // work[0] holds the completion ticket of the in-kernel final reduction; partials follow
   unsigned int* ticket = reinterpret_cast<unsigned int*>(work);
   work += 1;
+  // RS_DCGS_REGDOTS=0: the DCGS2 dual dots read w / u from shared memory per basis element (A/B)
+  static const int opts = env_int("RS_DCGS_REGDOTS", 1) ? 1 : 0;
 #define RS_CGS_LAUNCH(u, d, nm, dc)                                                                          \
   do {                                                                                                       \
     cudaFuncSetAttribute(k_cgs<u, d, nm, dc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
     k_cgs<u, d, nm, dc><<<nblk, kCgsThreads, smem, st>>>(tmap, use_tmap, V, ldv, k, n, ch, stages, rows, h_in, \
                                                          w, work, nonfinite, h_out, nrm2, ticket, pa, flags_in, \
-                                                         status_out, vrow, urow);                             \
+                                                         status_out, vrow, urow, opts);                       \
     RS_COUNT_LAUNCH();                                                                                       \
   } while (0)
   if (dcgs) {
