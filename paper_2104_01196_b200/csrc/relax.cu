@@ -401,6 +401,19 @@ __global__ void k_scale_rd(int64_t n, const R* __restrict__ r, const T* __restri
 }
 
 
+// rd = r / d, float64, two entries per thread (double2 accesses; 16-byte aligned r, d, rd)
+__global__ void k_scale_rd_f64x2(int64_t n, const double* __restrict__ r, const double* __restrict__ d,
+                                 double* __restrict__ rd) {
+  const int64_t i = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  if (i + 1 < n) {
+    const double2 rv = __ldcs(reinterpret_cast<const double2*>(r + i));
+    const double2 dv = *reinterpret_cast<const double2*>(d + i);
+    *reinterpret_cast<double2*>(rd + i) = make_double2(__ddiv_rn(rv.x, dv.x), __ddiv_rn(rv.y, dv.y));
+  } else if (i < n) {
+    rd[i] = __ddiv_rn(r[i], d[i]);
+  }
+}
+
 // Zero-start first inner step (the preconditioner's first half-sweep from z = 0,
 // where b - A*0 == b exactly): g1 = rd - w*(D^-1T rd) with rd_k = (T)r_k / d_k
 // recomputed at every neighbour instead of being stored by a separate pass.
@@ -1301,7 +1314,12 @@ static int two_stage(Ctx<T>& c, const T* b, T* x, int n_j, int backward, int for
     if (e != RS_ERR_UNSUPPORTED) return e;
   }
   if (x_is_zero) {
-    k_scale_rd<T, T><<<c.grid(), kB, 0, c.st>>>(c.n, b, c.d, rd, nullptr);
+    static const bool x2 = !getenv("RS_SCALE_X2") || atoi(getenv("RS_SCALE_X2")) != 0;
+    if (sizeof(T) == 8 && x2 && (uintptr_t)b % 16 == 0 && (uintptr_t)c.d % 16 == 0 && (uintptr_t)rd % 16 == 0)
+      k_scale_rd_f64x2<<<grid_for((c.n + 1) / 2, kB), kB, 0, c.st>>>(c.n, (const double*)b, (const double*)c.d,
+                                                                    (double*)rd);
+    else
+      k_scale_rd<T, T><<<c.grid(), kB, 0, c.st>>>(c.n, b, c.d, rd, nullptr);
     RS_COUNT_LAUNCH();
   } else if (!compact) {
     k_resid<T, kResidRd><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x, nullptr,
