@@ -277,6 +277,14 @@ int rs_dcgs2_dots(const double *V, int64_t ldv, int k, int64_t n, const double *
  * flag, [2 stage_ld + 4] local overflow flag (flags as in rs_cgs_pass; status / flags nullable) */
 /* unnormalized = 1: row k-1 holds u' itself (norm sqrt(*nrm2_prev)) rather than u'/||u'|| -- the
  * caller skipped the scaling pass; s, rho then already carry the norm (beta = 1 below) */
+/* rs_dcgs2_dots followed by rs_dcgs2_coef in ONE launch: the CTA that finishes the dots
+ * reduction (after the peer-memory allreduce when peer != NULL) runs the coefficient step.
+ * Same arguments and results as the two calls (last = 0). */
+int rs_dcgs2_dots_coef(const double *V, int64_t ldv, int k, int64_t n, const double *w, double *out,
+                       int *nonfinite, double *work, rs_peer *peer, uint64_t epoch, double *H, int ldh,
+                       double *coef, const double *nrm2_prev, double *stage, int stage_ld, const double *status,
+                       const int64_t *flags, int unnormalized, rs_stream_t stream);
+
 int rs_dcgs2_coef(int k, const double *dots, double *H, int ldh, double *coef, const double *nrm2_prev, int last,
                   double *stage, int stage_ld, const double *status, const int64_t *flags, int unnormalized,
                   rs_stream_t stream);

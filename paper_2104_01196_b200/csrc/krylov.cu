@@ -398,13 +398,108 @@ static size_t cgs_smem_bytes(int k, int ch, int stages) {
 //  UPDATE: with Q = rows [0, k-1), u = row k-1, coefficients (s, a, 1/rho, gamma):
 //          v = (u - Q s) / rho -> vrow,  u' = (w - Q a - gamma v) / rho -> urow
 //          (+ NORM: ||u'||^2)
+// Host-free coefficient step between the two DCGS2 passes of Arnoldi step j = k-1
+// (one thread; j <= 63).  H is the raw (unrotated) Hessenberg, column-major, ldh rows.
+//   dots = [V^T w | V^T u] (2k) from rs_dcgs2_dots, or V^T u (k) when `last`
+//   j == 0: v_0 is final; coef = (s = [], a = [], 1/rho = 1, gamma = v_0.w); H[0,0] = gamma
+//   j >= 1: s = Q^T u, rho = sqrt(u.u - s.s), beta = sqrt(*nrm2_prev) (tentative H[j,j-1]);
+//           final column j-1: H[0:j, j-1] += beta s, H[j, j-1] = beta rho;
+//           gamma = (u.w - s.a) / rho; tentative column j: H[0:j, j] = (a - H[0:j,0:j] s) / rho,
+//           H[j, j] = (gamma - H[j, j-1] s[j-1]) / rho;  coef = (s, a, 1/rho, gamma)
+__device__ __forceinline__ void dcgs2_coef_dev(int k, const double* __restrict__ dots, double* __restrict__ H,
+                                                   int ldh, double* __restrict__ coef,
+                                                   const double* __restrict__ nrm2_prev, int last, double* stage,
+                                                   int stage_ld, const double* __restrict__ status,
+                                                   const int64_t* __restrict__ flags, int unnormalized) {
+  // 64 threads: thread i owns Hessenberg row i; the two length-j sums are taken by thread 0 in
+  // ascending order from shared memory (deterministic)
+  __shared__ double s_au[kCgsMaxK], s_aw[kCgsMaxK];
+  __shared__ double s_rho, s_beta, s_gam;
+  const int t = threadIdx.x;
+  const int j = k - 1;
+  const double* aw = dots;
+  const double* au = last ? dots : dots + k;
+  if (j == 0) {
+    if (last || t != 0) return;
+    coef[kDcgsRho] = 1.0;
+    coef[kDcgsRho + 1] = aw[0];
+    H[0] = aw[0];
+    return;
+  }
+  if (stage) {
+    // host-visible record of Hessenberg column c = j-1 (pinned host memory, zero-copy):
+    // [m, m + c + 1) tentative column, [2m] ||u'||^2 of step c (tentative subdiagonal^2),
+    // [2m+1, 2m+3) reduced status, [2m+3] local non-finite flag, [2m+4] local overflow flag
+    const double* hcol = H + (int64_t)(j - 1) * ldh;
+    if (t < j) stage[stage_ld + t] = hcol[t];
+    if (t == 0) {
+      stage[2 * stage_ld] = *nrm2_prev;
+      stage[2 * stage_ld + 1] = status ? status[0] : 0.0;
+      stage[2 * stage_ld + 2] = status ? status[1] : 0.0;
+      stage[2 * stage_ld + 3] = (flags && (flags[0] & 0xffffffffll)) ? 1.0 : 0.0;
+      stage[2 * stage_ld + 4] = (flags && flags[1] != INT64_MAX) ? 1.0 : 0.0;
+    }
+  }
+  if (t < k) {
+    s_au[t] = au[t];
+    s_aw[t] = last ? 0.0 : aw[t];
+  }
+  __syncthreads();
+  if (t == 0) {
+    double ss = 0.0, sa = 0.0;
+    for (int i = 0; i < j; ++i) {
+      ss += s_au[i] * s_au[i];
+      sa += s_au[i] * s_aw[i];
+    }
+    const double rho = sqrt(s_au[j] - ss);
+    s_rho = rho;
+    // unnormalized: u is ||u'|| times the unit tentative vector, so s, rho already carry beta
+    s_beta = unnormalized ? 1.0 : sqrt(*nrm2_prev);
+    s_gam = (s_aw[j] - sa) / rho;
+  }
+  __syncthreads();
+  const double rho = s_rho, beta = s_beta;
+  double* hc = H + (int64_t)(j - 1) * ldh;
+  if (t < j) hc[t] += beta * s_au[t];
+  if (t == j) hc[j] = beta * rho;
+  if (stage && t <= j) stage[t] = hc[t];  // the final column
+  if (last) return;
+  __syncthreads();  // column j-1 final before it enters H s below
+  double* hn = H + (int64_t)j * ldh;
+  if (t < j) {
+    double acc = 0.0;
+    for (int c = (t > 0 ? t - 1 : 0); c < j; ++c) acc += H[t + (int64_t)c * ldh] * s_au[c];
+    hn[t] = (s_aw[t] - acc) / rho;
+    coef[t] = s_au[t];
+    coef[kDcgsA + t] = s_aw[t];
+  }
+  if (t == 0) {
+    hn[j] = (s_gam - beta * rho * s_au[j - 1]) / rho;
+    coef[kDcgsRho] = 1.0 / rho;
+    coef[kDcgsRho + 1] = s_gam;
+  }
+}
+
+// DCGS2 coefficient step fused into the dual-dots pass: the last CTA, having the reduced
+// (and, multi-GPU, rank-summed) dots, runs dcgs2_coef_dev instead of a separate 64-thread launch
+struct CoefArgs {
+  double* H = nullptr;
+  const double* nrm2_prev = nullptr;
+  double* coef = nullptr;
+  double* stage = nullptr;
+  const double* status = nullptr;
+  const int64_t* flags = nullptr;
+  int ldh = 0, stage_ld = 0, unnormalized = 0, on = 0;
+};
+
 template <bool UPDATE, bool DOTS, bool NORM, bool DCGS = false>
 __global__ void __launch_bounds__(kCgsThreads, 1)
     k_cgs(const __grid_constant__ CUtensorMap tmap, int use_tmap, const double* __restrict__ V, int64_t ldv, int k,
           int64_t n, int ch, int kCgsStages, int64_t rows_per_blk, const double* __restrict__ h_in,
           double* __restrict__ w, double* __restrict__ partial, int* nonfinite, double* __restrict__ h_out,
           double* __restrict__ nrm2_out, unsigned int* ticket, const PeerArgs pa, const int64_t* flags_in,
-          double* status_out, double* __restrict__ vout, double* __restrict__ uout, int opts) {
+          double* status_out, double* __restrict__ vout, double* __restrict__ uout, int opts,
+          const CoefArgs ca) {
   // Two warp groups ping-pong the chunks of this CTA's row range (group g takes
   // chunks c = g, g+2, ...), each synchronising on its own named barrier, so one
   // group's update / dots compute overlaps the other's; the TMA ring is shared.
@@ -757,6 +852,11 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
       status_out[1] = s_pay[nout + 1];
     }
   }
+  if (DCGS && DOTS && ca.on) {
+    __syncthreads();  // h_out (written above by this CTA) complete
+    dcgs2_coef_dev(k, h_out, ca.H, ca.ldh, ca.coef, ca.nrm2_prev, 0, k > 1 ? ca.stage : nullptr, ca.stage_ld,
+                   ca.status, ca.flags, ca.unnormalized);
+  }
   if (tid == 0) *ticket = 0;  // reset for the next launch (stream-ordered)
 }
 
@@ -874,7 +974,8 @@ int rs_gemv_n_update(const double* V, int64_t ldv, int k, int64_t n, const doubl
 static int cgs_pass(const double* V, int64_t ldv, int k, int64_t n, const double* h_in, double* w, double* h_out,
                     double* nrm2, int* nonfinite, double* work, cudaStream_t st, const rs_peer* peer, uint64_t epoch,
                     const int64_t* flags_in, double* status_out, bool dcgs = false, double* vrow = nullptr,
-                    double* urow = nullptr) {
+                    double* urow = nullptr, const CoefArgs* cap = nullptr) {
+  const CoefArgs ca = cap ? *cap : CoefArgs();
   rs_stream_t stream = (rs_stream_t)st;
   const bool aligned = (ldv % 2 == 0) && (n % 2 == 0) && ((uintptr_t)V % 16 == 0) && ((uintptr_t)w % 16 == 0);
   if (k > kCgsMaxK || !aligned) {
@@ -928,7 +1029,7 @@ static int cgs_pass(const double* V, int64_t ldv, int k, int64_t n, const double
     cudaFuncSetAttribute(k_cgs<u, d, nm, dc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
     k_cgs<u, d, nm, dc><<<nblk, kCgsThreads, smem, st>>>(tmap, use_tmap, V, ldv, k, n, ch, stages, rows, h_in, \
                                                          w, work, nonfinite, h_out, nrm2, ticket, pa, flags_in, \
-                                                         status_out, vrow, urow, opts);                       \
+                                                         status_out, vrow, urow, opts, ca);                   \
     RS_COUNT_LAUNCH();                                                                                       \
   } while (0)
   if (dcgs) {
@@ -969,86 +1070,12 @@ int rs_cgs_pass_peer(const double* V, int64_t ldv, int k, int64_t n, const doubl
 
 // ---------------------------------------------------------------- DCGS2 Arnoldi (delayed re-orthogonalisation)
 namespace rs {
-// Host-free coefficient step between the two DCGS2 passes of Arnoldi step j = k-1
-// (one thread; j <= 63).  H is the raw (unrotated) Hessenberg, column-major, ldh rows.
-//   dots = [V^T w | V^T u] (2k) from rs_dcgs2_dots, or V^T u (k) when `last`
-//   j == 0: v_0 is final; coef = (s = [], a = [], 1/rho = 1, gamma = v_0.w); H[0,0] = gamma
-//   j >= 1: s = Q^T u, rho = sqrt(u.u - s.s), beta = sqrt(*nrm2_prev) (tentative H[j,j-1]);
-//           final column j-1: H[0:j, j-1] += beta s, H[j, j-1] = beta rho;
-//           gamma = (u.w - s.a) / rho; tentative column j: H[0:j, j] = (a - H[0:j,0:j] s) / rho,
-//           H[j, j] = (gamma - H[j, j-1] s[j-1]) / rho;  coef = (s, a, 1/rho, gamma)
 __global__ void __launch_bounds__(64) k_dcgs2_coef(int k, const double* __restrict__ dots, double* __restrict__ H,
                                                    int ldh, double* __restrict__ coef,
                                                    const double* __restrict__ nrm2_prev, int last, double* stage,
                                                    int stage_ld, const double* __restrict__ status,
                                                    const int64_t* __restrict__ flags, int unnormalized) {
-  // 64 threads: thread i owns Hessenberg row i; the two length-j sums are taken by thread 0 in
-  // ascending order from shared memory (deterministic)
-  __shared__ double s_au[kCgsMaxK], s_aw[kCgsMaxK];
-  __shared__ double s_rho, s_beta, s_gam;
-  const int t = threadIdx.x;
-  const int j = k - 1;
-  const double* aw = dots;
-  const double* au = last ? dots : dots + k;
-  if (j == 0) {
-    if (last || t != 0) return;
-    coef[kDcgsRho] = 1.0;
-    coef[kDcgsRho + 1] = aw[0];
-    H[0] = aw[0];
-    return;
-  }
-  if (stage) {
-    // host-visible record of Hessenberg column c = j-1 (pinned host memory, zero-copy):
-    // [m, m + c + 1) tentative column, [2m] ||u'||^2 of step c (tentative subdiagonal^2),
-    // [2m+1, 2m+3) reduced status, [2m+3] local non-finite flag, [2m+4] local overflow flag
-    const double* hcol = H + (int64_t)(j - 1) * ldh;
-    if (t < j) stage[stage_ld + t] = hcol[t];
-    if (t == 0) {
-      stage[2 * stage_ld] = *nrm2_prev;
-      stage[2 * stage_ld + 1] = status ? status[0] : 0.0;
-      stage[2 * stage_ld + 2] = status ? status[1] : 0.0;
-      stage[2 * stage_ld + 3] = (flags && (flags[0] & 0xffffffffll)) ? 1.0 : 0.0;
-      stage[2 * stage_ld + 4] = (flags && flags[1] != INT64_MAX) ? 1.0 : 0.0;
-    }
-  }
-  if (t < k) {
-    s_au[t] = au[t];
-    s_aw[t] = last ? 0.0 : aw[t];
-  }
-  __syncthreads();
-  if (t == 0) {
-    double ss = 0.0, sa = 0.0;
-    for (int i = 0; i < j; ++i) {
-      ss += s_au[i] * s_au[i];
-      sa += s_au[i] * s_aw[i];
-    }
-    const double rho = sqrt(s_au[j] - ss);
-    s_rho = rho;
-    // unnormalized: u is ||u'|| times the unit tentative vector, so s, rho already carry beta
-    s_beta = unnormalized ? 1.0 : sqrt(*nrm2_prev);
-    s_gam = (s_aw[j] - sa) / rho;
-  }
-  __syncthreads();
-  const double rho = s_rho, beta = s_beta;
-  double* hc = H + (int64_t)(j - 1) * ldh;
-  if (t < j) hc[t] += beta * s_au[t];
-  if (t == j) hc[j] = beta * rho;
-  if (stage && t <= j) stage[t] = hc[t];  // the final column
-  if (last) return;
-  __syncthreads();  // column j-1 final before it enters H s below
-  double* hn = H + (int64_t)j * ldh;
-  if (t < j) {
-    double acc = 0.0;
-    for (int c = (t > 0 ? t - 1 : 0); c < j; ++c) acc += H[t + (int64_t)c * ldh] * s_au[c];
-    hn[t] = (s_aw[t] - acc) / rho;
-    coef[t] = s_au[t];
-    coef[kDcgsA + t] = s_aw[t];
-  }
-  if (t == 0) {
-    hn[j] = (s_gam - beta * rho * s_au[j - 1]) / rho;
-    coef[kDcgsRho] = 1.0 / rho;
-    coef[kDcgsRho + 1] = s_gam;
-  }
+  dcgs2_coef_dev(k, dots, H, ldh, coef, nrm2_prev, last, stage, stage_ld, status, flags, unnormalized);
 }
 }  // namespace rs
 
@@ -1071,6 +1098,31 @@ int rs_dcgs2_dots(const double* V, int64_t ldv, int k, int64_t n, const double* 
   }
   return cgs_pass(V, ldv, k, n, nullptr, const_cast<double*>(w), out, nullptr, nonfinite, work, (cudaStream_t)stream,
                   peer, epoch, nullptr, nullptr, true);
+}
+
+int rs_dcgs2_dots_coef(const double* V, int64_t ldv, int k, int64_t n, const double* w, double* out, int* nonfinite,
+                       double* work, rs_peer* peer, uint64_t epoch, double* H, int ldh, double* coef,
+                       const double* nrm2_prev, double* stage, int stage_ld, const double* status,
+                       const int64_t* flags, int unnormalized, rs_stream_t stream) {
+  if (!dcgs_ok(V, ldv, k, n, w, "rs_dcgs2_dots_coef")) return RS_ERR_ARG;
+  if (!w || !out || !work || (peer && epoch == 0) || !H || ldh < k || !coef || (k > 1 && !nrm2_prev) ||
+      (stage && stage_ld < k)) {
+    set_error(RS_ERR_ARG, "rs_dcgs2_dots_coef: bad arguments");
+    return RS_ERR_ARG;
+  }
+  CoefArgs ca;
+  ca.H = H;
+  ca.ldh = ldh;
+  ca.coef = coef;
+  ca.nrm2_prev = nrm2_prev;
+  ca.stage = stage;
+  ca.stage_ld = stage_ld;
+  ca.status = status;
+  ca.flags = flags;
+  ca.unnormalized = unnormalized;
+  ca.on = 1;
+  return cgs_pass(V, ldv, k, n, nullptr, const_cast<double*>(w), out, nullptr, nonfinite, work, (cudaStream_t)stream,
+                  peer, epoch, nullptr, nullptr, true, nullptr, nullptr, &ca);
 }
 
 int rs_dcgs2_coef(int k, const double* dots, double* H, int ldh, double* coef, const double* nrm2_prev, int last,

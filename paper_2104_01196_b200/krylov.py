@@ -234,6 +234,7 @@ class _timed:
 
 _DCGS_COEF = 2 * 64 + 2  # rs_dcgs2_* coefficient block (include/gs2b200.h)
 _DEFER_NORM = __import__("os").environ.get("RS_DEFER_NORM", "1") != "0"  # A/B switch (profiles/ortho_probe.py)
+_FUSE_COEF = __import__("os").environ.get("RS_DCGS_FUSE_COEF", "1") != "0"  # A/B switch
 
 
 class _Workspace:
@@ -520,6 +521,10 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
     defer_norm = (ortho == "dcgs2" and (op is None or (isinstance(op, Preconditioner) and op.precision == "same"))
                   and _DEFER_NORM)
 
+    # the coefficient step runs inside the dots kernel unless a host-side (NCCL / gloo) reduction
+    # has to happen between the two (RS_DCGS_FUSE_COEF=0 keeps them separate for A/B runs)
+    fuse_coef = (peer is not None or reduce_fn is None) and _FUSE_COEF
+
     def stage_ptr(jj):
         return C.c_void_p(ws.stage[jj % 2].data_ptr()) if jj >= 1 else None
 
@@ -533,13 +538,20 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
                 _apply_op(op, V[jj], ws.z, ws)
             spmv(ws.z, ws.w)
             k = jj + 1
-            with _timed("dcgs_dots"):
-                chk(lib.rs_dcgs2_dots(_p(V), ldv, k, n, _p(ws.w), _p(ws.dots), _p(ws.flags), _p(work), ph, ep(),
-                                      st), "dcgs2_dots")
-            if peer is None:
-                reduce_(ws.dots[:2 * k])
-            chk(lib.rs_dcgs2_coef(k, _p(ws.dots), _p(ws.H), ldh, _p(ws.coef), _p(nrm2_slot), 0, stage_ptr(jj),
-                                  m1, _p(status[1:3]), _p(ws.flags), int(defer_norm and jj >= 1), st), "dcgs2_coef")
+            unnorm = int(defer_norm and jj >= 1)
+            if fuse_coef:  # one launch: dots (+ in-kernel rank sum) and the coefficient step
+                with _timed("dcgs_dots"):
+                    chk(lib.rs_dcgs2_dots_coef(_p(V), ldv, k, n, _p(ws.w), _p(ws.dots), _p(ws.flags), _p(work), ph,
+                                               ep(), _p(ws.H), ldh, _p(ws.coef), _p(nrm2_slot), stage_ptr(jj), m1,
+                                               _p(status[1:3]), _p(ws.flags), unnorm, st), "dcgs2_dots_coef")
+            else:
+                with _timed("dcgs_dots"):
+                    chk(lib.rs_dcgs2_dots(_p(V), ldv, k, n, _p(ws.w), _p(ws.dots), _p(ws.flags), _p(work), ph,
+                                          ep(), st), "dcgs2_dots")
+                if peer is None:
+                    reduce_(ws.dots[:2 * k])
+                chk(lib.rs_dcgs2_coef(k, _p(ws.dots), _p(ws.H), ldh, _p(ws.coef), _p(nrm2_slot), 0, stage_ptr(jj),
+                                      m1, _p(status[1:3]), _p(ws.flags), unnorm, st), "dcgs2_coef")
             with _timed("dcgs_update"):
                 chk(lib.rs_dcgs2_update(_p(V), ldv, k, n, _p(ws.coef), _p(ws.w), _p(V[jj]), _p(V[jj + 1]),
                                         _p(nrm2_slot), _p(work), ph, ep(), _p(ws.flags) if ph else None,
