@@ -461,7 +461,7 @@ def gmres(A: DistMatrix, b_local, m: HybridPreconditioner | None = None, restart
     b = b_local.to(dev, torch.float64) if b_local.device != dev else b_local
     x = torch.zeros(dm.nrows, dtype=torch.float64, device=dev) if x0_local is None else x0_local.clone()
     x, hist, conv = _gmres_device(dm, b, x, m, restart, tol, maxit, spmv_fn=A.spmv, reduce_fn=A.allreduce_,
-                                  ortho=ortho, peer=A.mailbox)
+                                  ortho=ortho, peer=A.mailbox, x_zero=x0_local is None)
     if A.mailbox is not None:
         A.mailbox.check()
     return x, ConvergenceHistory(np.array(hist), conv)

@@ -329,7 +329,7 @@ def gmres(a, b, m=None, restart: int = 60, tol: float = 1e-9, maxit: int = 10000
              else torch.from_numpy(np.array(x0, dtype=np.float64)).to(dev))
     ortho = _check_ortho(ortho, n, restart)
     op = _as_operator(m)
-    x, hist, conv = _gmres_device(dm, bt, x, op, restart, tol, maxit, ortho=ortho)
+    x, hist, conv = _gmres_device(dm, bt, x, op, restart, tol, maxit, ortho=ortho, x_zero=x0 is None)
     if numpy_out or cpu_tensor_out:
         # D2H through page-locked memory (torch's caching host allocator): DMA-speed read-back
         host = torch.empty(n, dtype=torch.float64, pin_memory=True)
@@ -390,7 +390,7 @@ def _givens_step(h, cs, sn, g, j):
 
 
 def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None, reduce_fn=None, ortho="cgs2",
-                  peer=None):
+                  peer=None, x_zero=False):
     """GMRES(m) on device vectors of the local rows of ``dm``.
 
     Single GPU by default.  The distributed solver passes ``spmv_fn(src, dst)``
@@ -440,11 +440,17 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
     bnorm = norm_of(b)
     if bnorm == 0.0:
         return torch.zeros(n, dtype=torch.float64, device=b.device), [0.0], True
-    # r = b - A x (krylov.py:193)
-    spmv(x, ws.t)
-    chk(lib.rs_sub_norm(n, _p(b), _p(ws.t), _p(ws.r), _p(nrm2_slot), _p(work), st), "sub_norm")
-    reduce_(nrm2_slot)
-    rnorm = math.sqrt(float(nrm2_slot.item()))
+    # r = b - A x (krylov.py:193).  From x = 0 the product is all (+-)0, so r = b bit for bit and
+    # ||r|| = ||b|| (the same dot): skip the SpMV, the subtraction and a host round trip.
+    r0 = ws.r
+    if x_zero:
+        r0 = b
+        rnorm = bnorm
+    else:
+        spmv(x, ws.t)
+        chk(lib.rs_sub_norm(n, _p(b), _p(ws.t), _p(ws.r), _p(nrm2_slot), _p(work), st), "sub_norm")
+        reduce_(nrm2_slot)
+        rnorm = math.sqrt(float(nrm2_slot.item()))
     hist = [rnorm / bnorm]
     if hist[0] <= tol:
         return x, hist, True
@@ -586,7 +592,7 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
         sn = np.zeros(restart)
         g = np.zeros(restart + 1)
         # v0 = r / beta (krylov.py:208)
-        chk(lib.rs_scale_by_norm(n, _p(ws.r), _p(nrm2_slot), _p(V[0]), st), "scale")
+        chk(lib.rs_scale_by_norm(n, _p(r0), _p(nrm2_slot), _p(V[0]), st), "scale")
         g[0] = beta
         j = -1
         lucky = False
@@ -680,6 +686,7 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
         spmv(x, ws.t)
         chk(lib.rs_sub_norm(n, _p(b), _p(ws.t), _p(ws.r), _p(nrm2_slot), _p(work), st), "sub_norm")
         reduce_(nrm2_slot)
+        r0 = ws.r
         rnorm = math.sqrt(float(nrm2_slot.item()))
         check_overflow()
         true_rel = rnorm / bnorm
