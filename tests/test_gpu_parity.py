@@ -568,3 +568,26 @@ def test_fused_spmv_reductions(shape):
     want_res = float(np.dot(b.cpu().numpy() - yo, b.cpu().numpy() - yo))
     assert abs(float(sc[0]) - want_dot) <= 1e-13 * abs(want_dot)
     assert abs(float(sc[1]) - want_res) <= 1e-13 * abs(want_res)
+
+
+def test_gmres_iteration_count_256_vs_reference():
+    """Config C2 at full size: GS2(1,1,1)-GMRES(60) on laplace3d 256^3 against the reference's own run
+    (tests/golden/ref_lap3d_256.json, relaxsolve with OPENBLAS_NUM_THREADS=1: 2635 iterations,
+    3 h 3 min on one core).  Exact equality is not a meaningful bar at this size: the count moves
+    with the last-bit rounding of the Gram-Schmidt dot products (the C oracle -- the reference
+    algorithm with bitwise-reference sweeps and SpMV but its own dot summation order -- gives
+    2591, and the reference itself moves by up to 5% with the BLAS thread count on config 1), so
+    the bar is 1%.  Observed: 2628 (DCGS2, default), 2629 (MGS)."""
+    import json
+    from pathlib import Path
+
+    want = json.loads((Path(__file__).parent / "golden" / "ref_lap3d_256.json").read_text())["iterations"]
+    a = g2.laplace3d(256, device="cuda")
+    b = g2.random_rhs(a.nrows, 0, device="cuda")
+    _, h = g2.gmres(a, b, g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, 1)), restart=60, tol=1e-9)
+    assert h.converged and h.final_rel_res <= 1e-9
+    assert abs(h.iterations - want) <= 0.01 * want, (h.iterations, want)
+    # the true residuals recorded at the first restarts agree closely (the preconditioner and SpMV
+    # are bitwise the reference's; only the dot-product rounding differs)
+    ref_hist = json.loads((Path(__file__).parent / "golden" / "ref_lap3d_256.json").read_text())["rel_res_every_60"]
+    np.testing.assert_allclose(np.asarray(h.rel_res)[:300:60], ref_hist[:5], rtol=1e-8)
