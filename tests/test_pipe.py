@@ -1,4 +1,6 @@
-"""The window-pipelined one-launch GS2 sweep (relax.cu k_gs2_pipe) against the multi-pass sweep.
+"""The window-pipelined one-launch GS2 sweep (relax.cu k_gs2_pipe) against the multi-pass sweep,
+and the multi-pass sweep with its layout / prefetch switches off (variable-width SELL slices, no
+software L2 prefetch, one-row fp32 kernels, scalar scale pass) against the default.
 
 Both paths keep the reference's operation forms, so every iterate must be bitwise equal:
 GS2 n_j 1/2/3/5, forward / backward / symmetric, non-compact / compact, omega / gamma != 1,
@@ -42,10 +44,14 @@ def runs(tmp_path_factory):
         "multipass": _run(tmp, "multipass", RS_PIPE="0"),
         "pipe_small": _run(tmp, "pipe_small", RS_PIPE="1", RS_PIPE_WS="5"),
         "pipe_default": _run(tmp, "pipe_default", RS_PIPE="1"),
+        # layout / prefetch switches of the default path: variable-width slices (loaded bounds),
+        # no software L2 prefetch, one-row fp32 preconditioner kernels
+        "varwidth_nopf": _run(tmp, "varwidth_nopf", RS_PIPE="0", RS_SELL_UNIFORM="0", RS_PF_DIST="0",
+                              RS_F32_NR="1", RS_SCALE_X2="0"),
     }
 
 
-@pytest.mark.parametrize("variant", ["pipe_small", "pipe_default"])
+@pytest.mark.parametrize("variant", ["pipe_small", "pipe_default", "varwidth_nopf"])
 def test_pipe_bitwise_equals_multipass(runs, variant):
     ref, got = runs["multipass"], runs[variant]
     keys = [k for k in ref if not k.startswith("launches:")]
