@@ -250,6 +250,14 @@ static void free_sell(Sell<T>& s) {
 }
 
 void free_mt_sell(rs_matrix* m) {
+  for (int d = 0; d < 2; ++d) {
+    free_sell(m->LV64[d]);
+    free_sell(m->LV32[d]);
+    free(m->lv_slice_base[d]);
+    m->lv_slice_base[d] = nullptr;
+    cudaFree(m->lv_slice_base_dev[d]);
+    m->lv_slice_base_dev[d] = nullptr;
+  }
   free_sell(m->MT64);
   free_sell(m->MT32);
   free(m->mt_slice_base);

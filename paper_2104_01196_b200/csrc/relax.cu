@@ -546,6 +546,52 @@ __global__ void __launch_bounds__(256) k_gs_levels(const int64_t* __restrict__ l
   }
 }
 
+// Level-synchronous GS half-sweep over level-ordered L|U slices (RS_GS_MODE=ordered): one
+// cooperative launch, grid barrier between levels; a level's rows read contiguous slices (no
+// slice-pointer indirection into the natural-order triangles).  Same row update as k_gs_level;
+// x is read through L2 (written by other SMs at earlier levels of this launch).
+template <typename T>
+__global__ void __launch_bounds__(256) k_gs_levels_ord(const int64_t* __restrict__ level_ptr,
+                                                       const int64_t* __restrict__ base, int64_t nlevels,
+                                                       const int32_t* __restrict__ rows, const int64_t* __restrict__ sp,
+                                                       const int32_t* __restrict__ col, const T* __restrict__ val,
+                                                       const T* __restrict__ d, const T* __restrict__ b, T* x, T w,
+                                                       T w1, bool damped, unsigned int* bar) {
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t l = 0; l < nlevels; ++l) {
+    const int64_t lo = level_ptr[l], cnt = level_ptr[l + 1] - lo, sb = base[l];
+    for (int64_t t = gtid; t < cnt; t += nthreads) {
+      const int64_t i = rows[lo + t];
+      const int64_t p0 = sp[sb + (t >> 5)];
+      const int wd = (int)((sp[sb + (t >> 5) + 1] - p0) >> 5);
+      const int32_t* cp = col + p0 + (t & 31);
+      const T* vp = val + p0 + (t & 31);
+      T s = b[i];
+      const T di = d[i];
+      const T xi = damped ? __ldcg(x + i) : (T)0;
+      for (int j0 = 0; j0 < wd; j0 += kBatch) {
+        int32_t c[kBatch];
+        T v[kBatch], xv[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          const bool ok = j0 + u < wd;
+          c[u] = ok ? cp[32 * (j0 + u)] : -1;
+          v[u] = ok ? vp[32 * (j0 + u)] : (T)0;
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) xv[u] = c[u] >= 0 ? __ldcg(x + c[u]) : (T)0;
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u)
+          if (c[u] >= 0) s = sub_rn<T>(s, mul_rn<T>(v[u], xv[u]));
+      }
+      const T q = div_rn<T>(s, di);
+      x[i] = damped ? add_rn<T>(mul_rn<T>(w1, xi), mul_rn<T>(w, q)) : q;
+    }
+    if (l + 1 < nlevels) grid_barrier(bar, bar + 1, gridDim.x);
+  }
+}
+
 // Sync-free level-ordered GS half-sweep (one cooperative launch): rows are
 // visited in level order, statically interleaved over all co-resident warps
 // (32 consecutive positions per warp per round).  A row spins only on the
@@ -898,12 +944,19 @@ Sell<double>& mt_sell<double>(rs_matrix* m) { return m->MT64; }
 template <>
 Sell<float>& mt_sell<float>(rs_matrix* m) { return m->MT32; }
 
-// build the color-ordered slices once per installed coloring
 template <typename T>
-static int build_mt_sell(rs_matrix* m, Ctx<T>& c, cudaStream_t st) {
-  Sell<T>& S = mt_sell<T>(m);
+static Sell<T>& lv_sell(rs_matrix* m, int bwd);
+template <>
+Sell<double>& lv_sell<double>(rs_matrix* m, int bwd) { return m->LV64[bwd]; }
+template <>
+Sell<float>& lv_sell<float>(rs_matrix* m, int bwd) { return m->LV32[bwd]; }
+
+// L|U-merged slices of the rows of each group of `lv` (colours, or dependency levels), in group
+// order, once per grouping; *base_out[q] = first slice of group q (host)
+template <typename T>
+static int build_ordered_sell(rs_matrix* m, Ctx<T>& c, cudaStream_t st, Levels& lv, Sell<T>& S,
+                              int64_t** base_out) {
   if (S.slice_ptr || m->nrows == 0) return RS_OK;
-  Levels& lv = m->mt;
   const int64_t n = m->nrows, nc = lv.nlevels;
   std::vector<int64_t> base(nc + 1, 0);
   for (int64_t q = 0; q < nc; ++q) base[q + 1] = base[q] + (lv.level_ptr_host[q + 1] - lv.level_ptr_host[q] + 31) / 32;
@@ -943,10 +996,16 @@ static int build_mt_sell(rs_matrix* m, Ctx<T>& c, cudaStream_t st) {
   RS_CUDA(cudaStreamSynchronize(st));
   cudaFree(len);
   cudaFree(width);
-  m->mt_slice_base = (int64_t*)malloc(sizeof(int64_t) * (nc + 1));
-  memcpy(m->mt_slice_base, base.data(), sizeof(int64_t) * (nc + 1));
-  RS_CHECK_LAUNCH("build multicolor slices");
+  *base_out = (int64_t*)malloc(sizeof(int64_t) * (nc + 1));
+  memcpy(*base_out, base.data(), sizeof(int64_t) * (nc + 1));
+  RS_CHECK_LAUNCH("build ordered slices");
   return RS_OK;
+}
+
+// build the color-ordered slices once per installed coloring
+template <typename T>
+static int build_mt_sell(rs_matrix* m, Ctx<T>& c, cudaStream_t st) {
+  return build_ordered_sell<T>(m, c, st, m->mt, mt_sell<T>(m), &m->mt_slice_base);
 }
 
 template <typename T>
@@ -1025,12 +1084,27 @@ static int jr_sweeps_t(rs_matrix* m, const T* b, T* x, int sweeps, double omega,
 // RS_GS_MODE: "barrier" (default, one grid barrier per level), "syncfree" (per-row
 // done flags), "launch" (one kernel launch per level).  Measured at 256^3
 // (766 levels): 8.3 ms / 42.7 ms (no backoff) / 8.6 ms.
+enum GsMode { kGsBarrier = 0, kGsSyncfree = 1, kGsLaunch = 2, kGsOrdered = 3, kGsOrderedLaunch = 4 };
+static int gs_mode() {
+  static const int mode = [] {
+    // default: level-ordered slices, one launch per level (256^3: 6.1 ms per sweep vs 8.5 ms for
+    // the cooperative barrier sweep over the natural-order triangles, profiles/r01_wave_notes.md)
+    const char* s = getenv("RS_GS_MODE");
+    if (!s) return (int)kGsOrderedLaunch;
+    if (!strcmp(s, "syncfree")) return (int)kGsSyncfree;
+    if (!strcmp(s, "launch")) return (int)kGsLaunch;
+    if (!strcmp(s, "ordered")) return (int)kGsOrdered;
+    if (!strcmp(s, "ordered_launch")) return (int)kGsOrderedLaunch;
+    return (int)kGsBarrier;
+  }();
+  return mode;
+}
+
+// grid size / barrier words / device level pointers of the cooperative level sweeps (once per
+// direction); lv.coop_grid = 0 when the device cannot co-schedule them
 template <typename T>
-static int gs_cooperative(rs_matrix* m, Levels& lv, Ctx<T>& c, const T* b, T* x, const T* xL, const T* xU, T w, T w1,
-                          bool damped, int backward, cudaStream_t st) {
-  const char* mode_s = getenv("RS_GS_MODE");
-  const int mode = !mode_s ? 0 : (!strcmp(mode_s, "syncfree") ? 1 : (!strcmp(mode_s, "launch") ? 2 : 0));
-  if (mode == 2 || lv.nlevels < 2 || c.n == 0) return RS_ERR_UNSUPPORTED;
+static int gs_cooperative_setup(rs_matrix* m, Levels& lv, Ctx<T>& c) {
+  if (lv.nlevels < 2 || c.n == 0) return RS_ERR_UNSUPPORTED;
   if (lv.coop_grid < 0) {
     lv.coop_grid = 0;
     int dev = 0, coop = 0, nsm = 0, per_sm = 0, per_sm2 = 0;
@@ -1039,6 +1113,8 @@ static int gs_cooperative(rs_matrix* m, Levels& lv, Ctx<T>& c, const T* b, T* x,
     RS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_syncfree<T>, kB, 0));
     RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_gs_levels<T>, kB, 0));
+    per_sm = std::min(per_sm, per_sm2);
+    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_gs_levels_ord<T>, kB, 0));
     per_sm = std::min(per_sm, per_sm2);
     if (coop && per_sm > 0) {
       RS_CUDA(cudaMalloc(&lv.done, sizeof(unsigned int) * c.n));
@@ -1056,6 +1132,15 @@ static int gs_cooperative(rs_matrix* m, Levels& lv, Ctx<T>& c, const T* b, T* x,
       lv.level_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * nsm, grid_for(widest, kB)));
     }
   }
+  return lv.coop_grid ? RS_OK : RS_ERR_UNSUPPORTED;
+}
+
+template <typename T>
+static int gs_cooperative(rs_matrix* m, Levels& lv, Ctx<T>& c, const T* b, T* x, const T* xL, const T* xU, T w, T w1,
+                          bool damped, int backward, cudaStream_t st) {
+  const int mode = gs_mode() == kGsSyncfree ? 1 : (gs_mode() == kGsLaunch ? 2 : 0);
+  if (mode == 2) return RS_ERR_UNSUPPORTED;
+  if (gs_cooperative_setup<T>(m, lv, c) != RS_OK) return RS_ERR_UNSUPPORTED;
   if (!lv.coop_grid) return RS_ERR_UNSUPPORTED;
   int64_t n = c.n;
   const int32_t* rows = lv.rows;
@@ -1105,6 +1190,46 @@ static int gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omeg
     }
     const T* xL = bwd ? xold : x;
     const T* xU = bwd ? x : xold;
+    if (m->structurally_symmetric && (gs_mode() == kGsOrdered || gs_mode() == kGsOrderedLaunch)) {
+      // level-ordered L|U slices (built once per direction): one launch per level of the
+      // multicolour kernel -- the same row update (b_i - sum a_ik x_k ascending, / d_i, damped
+      // form), x read in place, which is the sequential order for a structurally symmetric DAG
+      Sell<T>& S = lv_sell<T>(m, bwd);
+      if ((e = build_ordered_sell<T>(m, c, st, lv, S, &m->lv_slice_base[bwd]))) return e;
+      const int64_t* base = m->lv_slice_base[bwd];
+      // one cooperative launch with a grid barrier per level (grid / barrier words of the
+      // level-synchronous sweep); per-level launches if the device cannot co-schedule it
+      if (gs_mode() == kGsOrdered && gs_cooperative_setup<T>(m, lv, c) == RS_OK && lv.level_grid > 0) {
+        if (!m->lv_slice_base_dev[bwd]) {
+          RS_CUDA(cudaMalloc(&m->lv_slice_base_dev[bwd], sizeof(int64_t) * (lv.nlevels + 1)));
+          RS_CUDA(cudaMemcpy(m->lv_slice_base_dev[bwd], base, sizeof(int64_t) * (lv.nlevels + 1),
+                             cudaMemcpyHostToDevice));
+        }
+        const int64_t* lp = lv.level_ptr_dev;
+        const int64_t* bd = m->lv_slice_base_dev[bwd];
+        int64_t nl = lv.nlevels;
+        const int32_t* rows = lv.rows;
+        const int64_t* sp = S.slice_ptr;
+        const int32_t* colp = S.col;
+        const T* valp = S.val;
+        const T* d = c.d;
+        unsigned int* bar = lv.barrier;
+        void* args[] = {(void*)&lp, (void*)&bd, (void*)&nl, (void*)&rows, (void*)&sp, (void*)&colp, (void*)&valp,
+                        (void*)&d, (void*)&b, (void*)&x, (void*)&w, (void*)&w1, (void*)&damped, (void*)&bar};
+        RS_CUDA(cudaLaunchCooperativeKernel((const void*)k_gs_levels_ord<T>, dim3(lv.level_grid), dim3(kB), args, 0,
+                                            st));
+        RS_COUNT_LAUNCH();
+        continue;
+      }
+      for (int64_t l = 0; l < lv.nlevels; ++l) {
+        const int64_t lo = lv.level_ptr_host[l], cnt = lv.level_ptr_host[l + 1] - lo;
+        if (!cnt) continue;
+        k_mt_color<T><<<grid_for(cnt, kB), kB, 0, st>>>(cnt, lv.rows + lo, S.slice_ptr + base[l], S.col, S.val, c.d,
+                                                        b, x, w, w1, damped);
+        RS_COUNT_LAUNCH();
+      }
+      continue;
+    }
     if (gs_cooperative<T>(m, lv, c, b, x, xL, xU, w, w1, damped, bwd, st) == RS_OK) continue;
     for (int64_t l = 0; l < lv.nlevels; ++l) {
       int64_t lo = lv.level_ptr_host[l], hi = lv.level_ptr_host[l + 1];

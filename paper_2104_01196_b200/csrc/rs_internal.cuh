@@ -102,6 +102,12 @@ struct rs_matrix {
   rs::Sell<double> MT64;
   rs::Sell<float> MT32;
   int64_t* mt_slice_base = nullptr;
+  // level-scheduled GS: the same L|U-merged slices in level order (forward / backward DAG), so a
+  // level's rows read contiguous slices; lv_slice_base[dir][l] = first slice of level l
+  rs::Sell<double> LV64[2];
+  rs::Sell<float> LV32[2];
+  int64_t* lv_slice_base[2] = {nullptr, nullptr};
+  int64_t* lv_slice_base_dev[2] = {nullptr, nullptr};
   void* scratch = nullptr;  // 3*nrows working dtype (rd, g ping/pong)
   void* scratch2 = nullptr; // 1*nrows (t)
   double* red = nullptr;    // reduction partials
