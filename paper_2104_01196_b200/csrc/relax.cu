@@ -937,6 +937,56 @@ __global__ void __launch_bounds__(256) k_mt_color(int64_t cnt, const int32_t* __
   x[i] = damped ? add_rn<T>(mul_rn<T>(w1, xi), mul_rn<T>(w, q)) : q;
 }
 
+// k_mt_color for a chain of dependent launches with programmatic dependent launch (PDL): the grid
+// lets its dependent start at once; everything that does not depend on the previous level --
+// row ids, the row's slice (columns, values), b_i, d_i -- is loaded BEFORE griddepcontrol.wait,
+// which returns once the previous level's grid has completed and its writes are visible; only
+// the x gathers, the update and the store follow it.  Same arithmetic as k_mt_color.
+template <typename T>
+__global__ void __launch_bounds__(256) k_mt_color_pdl(int64_t cnt, const int32_t* __restrict__ rows,
+                                                      const int64_t* __restrict__ sp, const int32_t* __restrict__ col,
+                                                      const T* __restrict__ val, const T* __restrict__ d,
+                                                      const T* __restrict__ b, T* x, T w, T w1, bool damped) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  constexpr int kW = 8;  // entries held before the wait (wider rows continue after it)
+  int32_t c[kW];
+  T v[kW];
+  int64_t i = 0, p0 = 0;
+  int wd = 0;
+  T s = (T)0, di = (T)1;
+  if (t < cnt) {
+    i = rows[t];
+    p0 = sp[t >> 5];
+    wd = (int)((sp[(t >> 5) + 1] - p0) >> 5);
+    s = b[i];
+    di = d[i];
+#pragma unroll
+    for (int u = 0; u < kW; ++u) {
+      const bool ok = u < wd;
+      c[u] = ok ? __ldcs(col + p0 + (t & 31) + 32 * u) : -1;
+      v[u] = ok ? __ldcs(val + p0 + (t & 31) + 32 * u) : (T)0;
+    }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (t >= cnt) return;
+  // x through L2 (.cg): this grid may have started before the previous level finished, so no
+  // L1 copy of x from before the wait may be trusted
+  const T xi = damped ? __ldcg(x + i) : (T)0;
+  T xv[kW];
+#pragma unroll
+  for (int u = 0; u < kW; ++u) xv[u] = c[u] >= 0 ? __ldcg(x + c[u]) : (T)0;
+#pragma unroll
+  for (int u = 0; u < kW; ++u)
+    if (c[u] >= 0) s = sub_rn<T>(s, mul_rn<T>(v[u], xv[u]));
+  for (int j = kW; j < wd; ++j) {
+    const int32_t cc = col[p0 + (t & 31) + 32 * j];
+    if (cc >= 0) s = sub_rn<T>(s, mul_rn<T>(val[p0 + (t & 31) + 32 * j], __ldcg(x + cc)));
+  }
+  const T q = div_rn<T>(s, di);
+  x[i] = damped ? add_rn<T>(mul_rn<T>(w1, xi), mul_rn<T>(w, q)) : q;
+}
+
 template <typename T>
 static Sell<T>& mt_sell(rs_matrix* m);
 template <>
@@ -1221,11 +1271,29 @@ static int gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omeg
         RS_COUNT_LAUNCH();
         continue;
       }
+      static const bool pdl = !getenv("RS_GS_PDL") || atoi(getenv("RS_GS_PDL")) != 0;
       for (int64_t l = 0; l < lv.nlevels; ++l) {
         const int64_t lo = lv.level_ptr_host[l], cnt = lv.level_ptr_host[l + 1] - lo;
         if (!cnt) continue;
-        k_mt_color<T><<<grid_for(cnt, kB), kB, 0, st>>>(cnt, lv.rows + lo, S.slice_ptr + base[l], S.col, S.val, c.d,
-                                                        b, x, w, w1, damped);
+        if (pdl) {
+          // programmatic dependent launch: level l+1's grid starts while level l drains and
+          // prefetches its rows' matrix data before waiting on level l (k_mt_color_pdl)
+          cudaLaunchConfig_t cfgl = {};
+          cfgl.gridDim = dim3(grid_for(cnt, kB));
+          cfgl.blockDim = dim3(kB);
+          cfgl.stream = st;
+          cudaLaunchAttribute at[1];
+          at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+          at[0].val.programmaticStreamSerializationAllowed = 1;
+          cfgl.attrs = at;
+          cfgl.numAttrs = 1;
+          RS_CUDA(cudaLaunchKernelEx(&cfgl, k_mt_color_pdl<T>, cnt, (const int32_t*)(lv.rows + lo),
+                                     (const int64_t*)(S.slice_ptr + base[l]), (const int32_t*)S.col, (const T*)S.val,
+                                     c.d, b, x, w, w1, damped));
+        } else {
+          k_mt_color<T><<<grid_for(cnt, kB), kB, 0, st>>>(cnt, lv.rows + lo, S.slice_ptr + base[l], S.col, S.val,
+                                                          c.d, b, x, w, w1, damped);
+        }
         RS_COUNT_LAUNCH();
       }
       continue;
