@@ -385,6 +385,34 @@ def ours(args):
         torch.cuda.synchronize()
         tts = {"seconds": round(time.perf_counter() - t0, 3), "iterations": h.iterations, "converged": h.converged,
                "final_rel_res": h.final_rel_res, "preconditioner": "gs2(1,1,1)", "restart": m, "tol": 1e-9}
+    # C5 on ONE GPU: the 512^3 cycle, the strong-scaling reference for the N > 1 lines (which run
+    # 512^3 in z-slabs); the 256^3 workspace is released first (512^3 basis: 65.5 GB)
+    c5 = None
+    if not args.no_c5 and (args.nx or 256) == 256:
+        from paper_2104_01196_b200 import krylov as gk
+
+        del a, pc
+        gk.release_workspace()
+        torch.cuda.empty_cache()
+        a5 = g2.laplace3d(512, device=local)
+        b5 = g2.random_rhs(a5.nrows, 0, device=f"cuda:{local}")
+        pc5 = g2.Preconditioner(a5, "gs2", g2.RelaxConfig(1, 1, n_j))
+        mod5 = Model(a5.nrows, a5.nnz_l, a5.nnz_u)
+        g2.gmres(a5, b5, pc5, restart=m, tol=1e-300, maxit=m)
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(2):
+            g2.gmres(a5, b5, pc5, restart=m, tol=1e-300, maxit=m)
+        f1.record()
+        torch.cuda.synchronize()
+        ms5 = f0.elapsed_time(f1) / 2
+        c5 = {"workload": "C5 laplace3d 512^3 on ONE GPU, one GMRES(60) cycle (strong-scaling reference of the "
+                          "N > 1 lines)", "ms_per_step": round(ms5, 3),
+              "value": round(mod5.cycle(m, n_j) / (ms5 * 1e-3) / 1e9, 3), "unit": "GB/s"}
+        del a5, b5, pc5
+        gk.release_workspace()
+        torch.cuda.empty_cache()
     cpu = None
     if not args.no_cpu_baseline:
         cs = CpuSample(nx, 1)
@@ -408,7 +436,7 @@ def ours(args):
                    "ms_per_iteration": round(ms / m, 4),
                    "l2": "inputs larger than L2 (V basis 61 x 134 MB, matrix 1.7 GB)", "parallelism": "1 GPU"},
         "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-        "clocks": clk.summary(), "sweeps": sweeps, "tts": tts,
+        "clocks": clk.summary(), "sweeps": sweeps, "tts": tts, "c5_one_gpu": c5,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -469,6 +497,7 @@ def main():
     p.add_argument("--comm", default="peer", choices=["peer", "nccl"],
                    help="N > 1 collectives: NVLink peer-memory kernels (default) or NCCL")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-c5", action="store_true", help="skip the 512^3 one-GPU cycle (strong-scaling reference)")
     p.add_argument("--cpu-iters", type=int, default=8)
     p.add_argument("--ref-iters", type=int, default=3)
     args = p.parse_args()
