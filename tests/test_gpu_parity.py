@@ -591,3 +591,39 @@ def test_gmres_iteration_count_256_vs_reference():
     # are bitwise the reference's; only the dot-product rounding differs)
     ref_hist = json.loads((Path(__file__).parent / "golden" / "ref_lap3d_256.json").read_text())["rel_res_every_60"]
     np.testing.assert_allclose(np.asarray(h.rel_res)[:300:60], ref_hist[:5], rtol=1e-8)
+
+
+def test_sweeps_bitwise_at_full_c2_size():
+    """Config C2 at full size (laplace3d 256^3, 16.7 M rows): one GS2 sweep for n_j = 1 and 2, one
+    damped JR sweep, one sequential (level-scheduled) GS sweep, the zero-start GS2(1,1,1)
+    preconditioner and the SpMV are bitwise the oracle's (the north-star bar is 1e-12 relative
+    per sweep) -- the production layout at this size (uniform-width slices, L2 prefetch,
+    level-ordered slices) is the one measured by bench.py."""
+    h = g2.laplace3d(256)
+    dev = g2.laplace3d(256, device="cuda")
+    om = oracle.Matrix(h)
+    n = h.nrows
+    b = g2.random_rhs(n, 0)
+    x0 = g2.random_rhs(n, 1)
+    bt = torch.from_numpy(b).cuda()
+    s = g2.extract_splitting(dev)
+    for cfg in (g2.RelaxConfig(1, 1, 1), g2.RelaxConfig(1, 1, 2, omega=0.9)):
+        xt = torch.from_numpy(x0).cuda()
+        g2.gs2_apply(dev, s, bt, xt, cfg)
+        xo = x0.copy()
+        oracle.gs2_apply(om, b, xo, cfg)
+        assert np.array_equal(xt.cpu().numpy(), xo), cfg
+    xt = torch.from_numpy(x0).cuda()
+    g2.jr_sweeps(dev, g2.extract_splitting(dev, omega=0.7), bt, xt, 1)
+    xo = x0.copy()
+    oracle.jr_sweeps(om, b, xo, 1, omega=0.7)
+    assert np.array_equal(xt.cpu().numpy(), xo)
+    xt = torch.from_numpy(x0).cuda()
+    g2.gs_sequential_sweep(dev, s, bt, xt, "forward")
+    xo = x0.copy()
+    oracle.gs_sweep(om, b, xo, "forward")
+    assert np.array_equal(xt.cpu().numpy(), xo)
+    y = g2.spmv(dev, torch.from_numpy(x0).cuda())
+    assert np.array_equal(y.cpu().numpy(), oracle.spmv(om, x0))
+    z = g2.Preconditioner(dev, "gs2", g2.RelaxConfig(1, 1, 1)).apply(bt)
+    assert np.array_equal(z.cpu().numpy(), oracle.Precond(om, "gs2", n_j=1).apply(b))
