@@ -19,6 +19,9 @@ The GS2 sweep figure of the metric (non-zero x, n_j = 1, 2.946 GB at 256^3)
 and the paper's same-device baselines (JR, level-scheduled GS, n_j = 0..3)
 are reported under "sweeps"; time-to-solution of the full solve under "tts".
 
+``c5_one_gpu`` (N = 1 only): the 512^3 cycle on one GPU, the strong-scaling reference of the
+N > 1 lines (``--no-c5`` skips it).
+
 ``--impl reference`` times the reference's CPU algorithm (the C oracle port,
 all host threads) on a bounded sample of the same workload.
 """
