@@ -279,6 +279,8 @@ class _Workspace:
         # per-step record of the Hessenberg column the coefficient kernel writes straight into
         # page-locked host memory (zero-copy; two slots for the one-step-ahead pipeline)
         self.stage = torch.zeros((2, 2 * self.m1 + 8), dtype=torch.float64, pin_memory=True)
+        # ||b||^2, ||r||^2 of a deferred GMRES start (read with the first Arnoldi step)
+        self.start_pin = torch.zeros(2, dtype=torch.float64, pin_memory=True)
 
 
 def _p(t):
@@ -437,27 +439,47 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
         if reduce_fn is not None and float(status[2].item()) > 0:
             raise OverflowError("an entry overflows single precision on another rank")
 
-    bnorm = norm_of(b)
-    if bnorm == 0.0:
-        return torch.zeros(n, dtype=torch.float64, device=b.device), [0.0], True
     # r = b - A x (krylov.py:193).  From x = 0 the product is all (+-)0, so r = b bit for bit and
     # ||r|| = ||b|| (the same dot): skip the SpMV, the subtraction and a host round trip.
     r0 = ws.r
-    if x_zero:
-        r0 = b
-        rnorm = bnorm
-    else:
-        spmv(x, ws.t)
-        chk(lib.rs_sub_norm(n, _p(b), _p(ws.t), _p(ws.r), _p(nrm2_slot), _p(work), st), "sub_norm")
+    # DCGS2: ||b|| and ||r|| stay on the device at first (v0 = r / ||r|| is scaled there); the host
+    # reads them with the first Arnoldi step's scalars, so the GPU starts the cycle without
+    # waiting for a host round trip (the early exits -- b = 0, r already small -- are taken then,
+    # discarding the speculative steps)
+    defer_start = ortho == "dcgs2" and maxit > 0
+    if defer_start:
+        chk(lib.rs_dot(n, _p(b), _p(b), _p(nrm2_slot), _p(work), st), "dot")
         reduce_(nrm2_slot)
-        rnorm = math.sqrt(float(nrm2_slot.item()))
-    hist = [rnorm / bnorm]
-    if hist[0] <= tol:
-        return x, hist, True
+        ws.start_pin[0:1].copy_(nrm2_slot, non_blocking=True)
+        if x_zero:
+            r0 = b
+        else:
+            spmv(x, ws.t)
+            chk(lib.rs_sub_norm(n, _p(b), _p(ws.t), _p(ws.r), _p(nrm2_slot), _p(work), st), "sub_norm")
+            reduce_(nrm2_slot)
+        ws.start_pin[1:2].copy_(nrm2_slot, non_blocking=True)
+        bnorm = rnorm = None
+        hist = []
+        breakdown_tol = 0.0
+    else:
+        bnorm = norm_of(b)
+        if bnorm == 0.0:
+            return torch.zeros(n, dtype=torch.float64, device=b.device), [0.0], True
+        if x_zero:
+            r0 = b
+            rnorm = bnorm
+        else:
+            spmv(x, ws.t)
+            chk(lib.rs_sub_norm(n, _p(b), _p(ws.t), _p(ws.r), _p(nrm2_slot), _p(work), st), "sub_norm")
+            reduce_(nrm2_slot)
+            rnorm = math.sqrt(float(nrm2_slot.item()))
+        hist = [rnorm / bnorm]
+        if hist[0] <= tol:
+            return x, hist, True
+        breakdown_tol = BREAKDOWN_RTOL * bnorm
 
     total = 0
     converged = False
-    breakdown_tol = BREAKDOWN_RTOL * bnorm
     V = ws.V
     ldv = ws.ldv
 
@@ -593,7 +615,7 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
         g = np.zeros(restart + 1)
         # v0 = r / beta (krylov.py:208)
         chk(lib.rs_scale_by_norm(n, _p(r0), _p(nrm2_slot), _p(V[0]), st), "scale")
-        g[0] = beta
+        g[0] = beta if beta is not None else 0.0
         j = -1
         lucky = False
         if ortho == "dcgs2":
@@ -612,6 +634,18 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
                 if j + 2 <= restart and total < maxit:
                     ev_next = enqueue_dcgs(j + 2)
                 ev.synchronize()
+                if bnorm is None:  # deferred start (see defer_start): ||b||, ||r|| are on the host now
+                    bn2, rn2 = (float(v) for v in ws.start_pin)
+                    bnorm = math.sqrt(bn2)
+                    if bnorm == 0.0:
+                        return torch.zeros(n, dtype=torch.float64, device=b.device), [0.0], True
+                    rnorm = math.sqrt(rn2)
+                    hist = [rnorm / bnorm]
+                    if hist[0] <= tol:
+                        return x, hist, True
+                    breakdown_tol = BREAKDOWN_RTOL * bnorm
+                    beta = rnorm
+                    g[0] = beta
                 hv = ws.stage[(j + 1) % 2].numpy()
                 if hv[2 * m1 + 4] > 0 or hv[2 * m1 + 2] > 0:
                     raise OverflowError(f"an entry overflows single precision (Arnoldi iteration {total})")
