@@ -1058,8 +1058,22 @@ static int build_mt_sell(rs_matrix* m, Ctx<T>& c, cudaStream_t st) {
   return build_ordered_sell<T>(m, c, st, m->mt, mt_sell<T>(m), &m->mt_slice_base);
 }
 
+// first colour of a multicolour sweep from x = 0 (the zero-start preconditioner): every
+// neighbour of the colour's rows is still 0, so b_i - sum a_ik * 0 = b_i (up to the sign of zero)
+// and the row update is x_i = b_i / d_i (damped: (1-w)*0 + w*(b_i/d_i)) -- no matrix reads
 template <typename T>
-static int mt_gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omega, cudaStream_t st) {
+__global__ void k_mt_first(int64_t cnt, const int32_t* __restrict__ rows, const T* __restrict__ d,
+                           const T* __restrict__ b, T* __restrict__ x, T w, T w1, bool damped) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cnt) return;
+  const int64_t i = rows[t];
+  const T q = div_rn<T>(b[i], d[i]);
+  x[i] = damped ? add_rn<T>(mul_rn<T>(w1, (T)0), mul_rn<T>(w, q)) : q;
+}
+
+template <typename T>
+static int mt_gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omega, cudaStream_t st,
+                         bool x_zero = false) {
   int e;
   if ((e = build_coloring(m))) return e;
   Ctx<T> c(m, st);
@@ -1076,8 +1090,13 @@ static int mt_gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double o
       const int64_t col = bwd ? lv.nlevels - 1 - q : q;
       const int64_t lo = lv.level_ptr_host[col], cnt = lv.level_ptr_host[col + 1] - lo;
       if (!cnt) continue;
-      k_mt_color<T><<<grid_for(cnt, kB), kB, 0, st>>>(cnt, lv.rows + lo, S.slice_ptr + m->mt_slice_base[col],
-                                                      S.col, S.val, c.d, b, x, w, w1, damped);
+      if (x_zero) {
+        k_mt_first<T><<<grid_for(cnt, kB), kB, 0, st>>>(cnt, lv.rows + lo, c.d, b, x, w, w1, damped);
+        x_zero = false;
+      } else {
+        k_mt_color<T><<<grid_for(cnt, kB), kB, 0, st>>>(cnt, lv.rows + lo, S.slice_ptr + m->mt_slice_base[col],
+                                                        S.col, S.val, c.d, b, x, w, w1, damped);
+      }
       RS_COUNT_LAUNCH();
     }
   }
@@ -1516,7 +1535,7 @@ static int precond_body(rs_matrix* m, int kind, rs_relax_cfg cfg, const T* rhs, 
     case RS_PC_MT_SGS: {
       RS_CUDA(cudaMemsetAsync(z, 0, sizeof(T) * m->nrows, st));
       for (int s = 0; s < sweeps; ++s) {
-        int e = mt_gs_sweep_t<T>(m, rhs, z, cfg.direction, cfg.omega, st);
+        int e = mt_gs_sweep_t<T>(m, rhs, z, cfg.direction, cfg.omega, st, s == 0);
         if (e) return e;
       }
       return RS_OK;
