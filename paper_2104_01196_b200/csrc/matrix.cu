@@ -246,6 +246,7 @@ static void free_sell(Sell<T>& s) {
   cudaFree(s.col);
   cudaFree(s.val);
   cudaFree(s.dval);
+  cudaFree(s.dord);
   s = Sell<T>();
 }
 

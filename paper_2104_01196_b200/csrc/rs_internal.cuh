@@ -59,6 +59,7 @@ struct Sell {
   int32_t* col = nullptr;        // [nslots], -1 = padding
   T* val = nullptr;              // [nslots] raw values
   T* dval = nullptr;             // [nslots] values / d[row] (optional)
+  T* dord = nullptr;             // [nrows] d[rows[t]] of group-ordered slices (MT / LV), else null
   int uw = -1;                   // every slice has this width (slice_ptr[s] = 32*uw*s), else -1
   int64_t s_lo = 0, s_hi = -1;   // slices outside [s_lo, s_hi) are empty (-1: not computed = all)
 };
