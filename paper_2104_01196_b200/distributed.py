@@ -29,7 +29,7 @@ from dataclasses import dataclass, replace
 import numpy as np
 
 from . import _native as N
-from .krylov import ConvergenceHistory, _check_ortho, _gmres_device, _p
+from .krylov import ConvergenceHistory, _Workspace, _check_ortho, _gmres_device, _p
 from .relax import BlockPartition, RelaxConfig
 from .sparse import CsrMatrix, DeviceMatrix, _torch
 
@@ -411,6 +411,14 @@ class HybridPreconditioner:
         torch = _torch()
         self._bhat = torch.empty(A.nrows, dtype=torch.float64, device=A.dm.torch_device) if cfg.n_t > 1 else None
 
+    def prepare(self, r_zero, z):
+        """Create the local relaxation's lazily allocated device buffers now (one local zero-start
+        apply of r = 0, no exchange): see _settle_before_collectives."""
+        c = self._local_cfg if self.local == "gs2" else N.RelaxCfg.of(replace(self.cfg, n_t=1))
+        st = C.c_void_p(_torch().cuda.current_stream().cuda_stream)
+        N.check(self._lib.rs_precond_apply(self.dm.handle, N.PC_KINDS["gs2" if self.local == "gs2" else "gs_seq"],
+                                           C.byref(c), _p(r_zero), _p(z), None, st), "precond")
+
     def apply_into(self, r, z, flag=None):
         lib = self._lib
         st = C.c_void_p(_torch().cuda.current_stream().cuda_stream)
@@ -439,6 +447,23 @@ class HybridPreconditioner:
                                             float(cfg.omega), st), "gs")
 
 
+def _settle_before_collectives(A: DistMatrix, m, restart: int) -> None:
+    """Peer-memory collectives spin on the device until every rank has arrived.  A rank that is
+    still making a lazy allocation (cudaMalloc, page-locked host memory: both may implicitly
+    synchronise the device) while another rank's collective spins on the SAME device -- thread
+    ranks sharing a GPU -- waits for that kernel, which waits for the rank: a deadlock broken only
+    by the collective's timeout.  So the solve's lazily allocated resources (GMRES workspace,
+    the preconditioner's scratch) are created first, and the ranks meet on the host before the
+    first collective is launched."""
+    torch = _torch()
+    ws = _Workspace.get(A.dm.nrows, restart, A.dm.torch_device)
+    if isinstance(m, HybridPreconditioner):
+        ws.z.zero_()
+        m.prepare(ws.z, ws.t)
+    torch.cuda.current_stream().synchronize()
+    A.comm.barrier()
+
+
 def gmres(A: DistMatrix, b_local, m: HybridPreconditioner | None = None, restart: int = 60, tol: float = 1e-9,
           maxit: int = 10000, x0_local=None, ortho: str = "auto"):
     """Distributed GMRES(m): every rank calls it with its local rows; returns (x_local, history).
@@ -460,6 +485,8 @@ def gmres(A: DistMatrix, b_local, m: HybridPreconditioner | None = None, restart
     dev = dm.torch_device
     b = b_local.to(dev, torch.float64) if b_local.device != dev else b_local
     x = torch.zeros(dm.nrows, dtype=torch.float64, device=dev) if x0_local is None else x0_local.clone()
+    if A.mailbox is not None:
+        _settle_before_collectives(A, m, restart)
     x, hist, conv = _gmres_device(dm, b, x, m, restart, tol, maxit, spmv_fn=A.spmv, reduce_fn=A.allreduce_,
                                   ortho=ortho, peer=A.mailbox, x_zero=x0_local is None)
     if A.mailbox is not None:

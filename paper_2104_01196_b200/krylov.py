@@ -235,6 +235,7 @@ class _timed:
 _DCGS_COEF = 2 * 64 + 2  # rs_dcgs2_* coefficient block (include/gs2b200.h)
 _DEFER_NORM = __import__("os").environ.get("RS_DEFER_NORM", "1") != "0"  # A/B switch (profiles/ortho_probe.py)
 _FUSE_COEF = __import__("os").environ.get("RS_DCGS_FUSE_COEF", "1") != "0"  # A/B switch
+_DEFER_START = __import__("os").environ.get("RS_DEFER_START", "1") != "0"  # A/B switch (deferred GMRES start)
 
 
 class _Workspace:
@@ -446,7 +447,7 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
     # reads them with the first Arnoldi step's scalars, so the GPU starts the cycle without
     # waiting for a host round trip (the early exits -- b = 0, r already small -- are taken then,
     # discarding the speculative steps)
-    defer_start = ortho == "dcgs2" and maxit > 0
+    defer_start = ortho == "dcgs2" and maxit > 0 and _DEFER_START
     if defer_start:
         chk(lib.rs_dot(n, _p(b), _p(b), _p(nrm2_slot), _p(work), st), "dot")
         reduce_(nrm2_slot)
