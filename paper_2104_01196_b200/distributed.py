@@ -410,6 +410,7 @@ class HybridPreconditioner:
         self._lib = N.load()
         torch = _torch()
         self._bhat = torch.empty(A.nrows, dtype=torch.float64, device=A.dm.torch_device) if cfg.n_t > 1 else None
+        self._prepared = False  # lazy device buffers created (see prepare)
 
     def prepare(self, r_zero, z):
         """Create the local relaxation's lazily allocated device buffers now (one local zero-start
@@ -457,9 +458,10 @@ def _settle_before_collectives(A: DistMatrix, m, restart: int) -> None:
     first collective is launched."""
     torch = _torch()
     ws = _Workspace.get(A.dm.nrows, restart, A.dm.torch_device)
-    if isinstance(m, HybridPreconditioner):
+    if isinstance(m, HybridPreconditioner) and not m._prepared:
         ws.z.zero_()
         m.prepare(ws.z, ws.t)
+        m._prepared = True
     torch.cuda.current_stream().synchronize()
     A.comm.barrier()
 
@@ -487,8 +489,15 @@ def gmres(A: DistMatrix, b_local, m: HybridPreconditioner | None = None, restart
     x = torch.zeros(dm.nrows, dtype=torch.float64, device=dev) if x0_local is None else x0_local.clone()
     if A.mailbox is not None:
         _settle_before_collectives(A, m, restart)
-    x, hist, conv = _gmres_device(dm, b, x, m, restart, tol, maxit, spmv_fn=A.spmv, reduce_fn=A.allreduce_,
-                                  ortho=ortho, peer=A.mailbox, x_zero=x0_local is None)
+    try:
+        x, hist, conv = _gmres_device(dm, b, x, m, restart, tol, maxit, spmv_fn=A.spmv, reduce_fn=A.allreduce_,
+                                      ortho=ortho, peer=A.mailbox, x_zero=x0_local is None)
+    except (ArithmeticError, N.DivergenceError):
+        # a timed-out peer collective leaves garbage behind it: report the timeout, not its symptom
+        if A.mailbox is not None:
+            _torch().cuda.current_stream().synchronize()
+            A.mailbox.check()
+        raise
     if A.mailbox is not None:
         A.mailbox.check()
     return x, ConvergenceHistory(np.array(hist), conv)
