@@ -1003,6 +1003,89 @@ Sell<double>& lv_sell<double>(rs_matrix* m, int bwd) { return m->LV64[bwd]; }
 template <>
 Sell<float>& lv_sell<float>(rs_matrix* m, int bwd) { return m->LV32[bwd]; }
 
+// Consecutive SMALL levels (at most blockDim rows each) of the level-scheduled GS in ONE CTA: the
+// levels at both ends of a stencil's DAG hold few rows (level l of a 3D 7-point grid has ~l^2/2;
+// every level of a 2D 128^2 grid <= 128), where a launch per level (~4 us even with PDL) costs far
+// more than its rows.  Thread t owns row t of each level; what does not depend on x (row id, b_i,
+// d_i, the row's first kW slots) is loaded for level l+1 BEFORE the __syncthreads() that ends
+// level l, so a level costs one x gather + store + barrier.  x is read through L2 (.cg), never
+// from a stale L1 line.  Same row update, entry order and arithmetic as k_mt_color_pdl; chained
+// with PDL like it.
+template <typename T>
+struct CtaRow {
+  static constexpr int kW = 8;
+  int64_t i;
+  int64_t q0;
+  int wd;
+  bool on;
+  T s, di;
+  int32_t c[kW];
+  T v[kW];
+};
+
+template <typename T>
+__device__ __forceinline__ void cta_row_load(CtaRow<T>& r, int64_t l, const int64_t* __restrict__ lp,
+                                             const int64_t* __restrict__ base, const int32_t* __restrict__ rows,
+                                             const int64_t* __restrict__ sp, const int32_t* __restrict__ col,
+                                             const T* __restrict__ val, const T* __restrict__ d,
+                                             const T* __restrict__ b) {
+  const int64_t t = threadIdx.x;
+  const int64_t lo = lp[l], cnt = lp[l + 1] - lo;
+  r.on = t < cnt;
+  r.wd = 0;
+  if (r.on) {
+    const int64_t* spl = sp + base[l];
+    r.i = rows[lo + t];
+    const int64_t p0 = spl[t >> 5];
+    r.wd = (int)((spl[(t >> 5) + 1] - p0) >> 5);
+    r.q0 = p0 + (t & 31);
+    r.s = b[r.i];
+    r.di = d[r.i];
+  }
+#pragma unroll
+  for (int u = 0; u < CtaRow<T>::kW; ++u) {
+    const bool ok = u < r.wd;
+    r.c[u] = ok ? col[r.q0 + 32 * u] : -1;
+    r.v[u] = ok ? val[r.q0 + 32 * u] : (T)0;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024) k_gs_levels_cta(int64_t l0, int64_t l1, const int64_t* __restrict__ lp,
+                                                        const int64_t* __restrict__ base,
+                                                        const int32_t* __restrict__ rows,
+                                                        const int64_t* __restrict__ sp,
+                                                        const int32_t* __restrict__ col, const T* __restrict__ val,
+                                                        const T* __restrict__ d, const T* __restrict__ b, T* x, T w,
+                                                        T w1, bool damped) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  constexpr int kW = CtaRow<T>::kW;
+  CtaRow<T> cur, nxt;
+  cta_row_load<T>(cur, l0, lp, base, rows, sp, col, val, d, b);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  for (int64_t l = l0; l < l1; ++l) {
+    if (cur.on) {
+      const T xi = damped ? __ldcg(x + cur.i) : (T)0;
+      T xv[kW];
+#pragma unroll
+      for (int u = 0; u < kW; ++u) xv[u] = cur.c[u] >= 0 ? __ldcg(x + cur.c[u]) : (T)0;
+      T s = cur.s;
+#pragma unroll
+      for (int u = 0; u < kW; ++u)
+        if (cur.c[u] >= 0) s = sub_rn<T>(s, mul_rn<T>(cur.v[u], xv[u]));
+      for (int j = kW; j < cur.wd; ++j) {
+        const int32_t cc = col[cur.q0 + 32 * j];
+        if (cc >= 0) s = sub_rn<T>(s, mul_rn<T>(val[cur.q0 + 32 * j], __ldcg(x + cc)));
+      }
+      const T q = div_rn<T>(s, cur.di);
+      x[cur.i] = damped ? add_rn<T>(mul_rn<T>(w1, xi), mul_rn<T>(w, q)) : q;
+    }
+    if (l + 1 < l1) cta_row_load<T>(nxt, l + 1, lp, base, rows, sp, col, val, d, b);
+    __syncthreads();
+    cur = nxt;
+  }
+}
+
 // out[t] = v[rows[t]]: the diagonal in group order (Sell::dord)
 template <typename T>
 __global__ void k_gather_rows(int64_t n, const int32_t* __restrict__ rows, const T* __restrict__ v, T* __restrict__ out) {
@@ -1303,9 +1386,44 @@ static int gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omeg
         continue;
       }
       static const bool pdl = !getenv("RS_GS_PDL") || atoi(getenv("RS_GS_PDL")) != 0;
+      // runs of consecutive levels of at most cta_rows rows go to one single-CTA launch
+      // (k_gs_levels_cta); RS_GS_CTA_ROWS=0 switches that off
+      static const int64_t cta_rows =
+          std::min<int64_t>(1024, getenv("RS_GS_CTA_ROWS") ? atoll(getenv("RS_GS_CTA_ROWS")) : 256);
+      auto lcount = [&](int64_t l) { return lv.level_ptr_host[l + 1] - lv.level_ptr_host[l]; };
       for (int64_t l = 0; l < lv.nlevels; ++l) {
         const int64_t lo = lv.level_ptr_host[l], cnt = lv.level_ptr_host[l + 1] - lo;
         if (!cnt) continue;
+        if (pdl && cta_rows > 0 && cnt <= cta_rows && l + 1 < lv.nlevels && lcount(l + 1) <= cta_rows) {
+          int64_t l2 = l + 1;
+          while (l2 < lv.nlevels && lcount(l2) <= cta_rows) ++l2;
+          if (!lv.level_ptr_dev) {
+            RS_CUDA(cudaMalloc(&lv.level_ptr_dev, sizeof(int64_t) * (lv.nlevels + 1)));
+            RS_CUDA(cudaMemcpy(lv.level_ptr_dev, lv.level_ptr_host, sizeof(int64_t) * (lv.nlevels + 1),
+                               cudaMemcpyHostToDevice));
+          }
+          if (!m->lv_slice_base_dev[bwd]) {
+            RS_CUDA(cudaMalloc(&m->lv_slice_base_dev[bwd], sizeof(int64_t) * (lv.nlevels + 1)));
+            RS_CUDA(cudaMemcpy(m->lv_slice_base_dev[bwd], base, sizeof(int64_t) * (lv.nlevels + 1),
+                               cudaMemcpyHostToDevice));
+          }
+          cudaLaunchConfig_t cfgl = {};
+          cfgl.gridDim = dim3(1);
+          cfgl.blockDim = dim3(1024);
+          cfgl.stream = st;
+          cudaLaunchAttribute at[1];
+          at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+          at[0].val.programmaticStreamSerializationAllowed = 1;
+          cfgl.attrs = at;
+          cfgl.numAttrs = 1;
+          RS_CUDA(cudaLaunchKernelEx(&cfgl, k_gs_levels_cta<T>, l, l2, (const int64_t*)lv.level_ptr_dev,
+                                     (const int64_t*)m->lv_slice_base_dev[bwd], (const int32_t*)lv.rows,
+                                     (const int64_t*)S.slice_ptr, (const int32_t*)S.col, (const T*)S.val, c.d, b, x,
+                                     w, w1, damped));
+          RS_COUNT_LAUNCH();
+          l = l2 - 1;
+          continue;
+        }
         if (pdl) {
           // programmatic dependent launch: level l+1's grid starts while level l drains and
           // prefetches its rows' matrix data before waiting on level l (k_mt_color_pdl)
