@@ -1003,6 +1003,8 @@ Sell<double>& lv_sell<double>(rs_matrix* m, int bwd) { return m->LV64[bwd]; }
 template <>
 Sell<float>& lv_sell<float>(rs_matrix* m, int bwd) { return m->LV32[bwd]; }
 
+constexpr size_t kGsSmemBytes = 200 * 1024;  // x staged in shared memory up to this size
+
 // Consecutive SMALL levels (at most blockDim rows each) of the level-scheduled GS in ONE CTA: the
 // levels at both ends of a stencil's DAG hold few rows (level l of a 3D 7-point grid has ~l^2/2;
 // every level of a 2D 128^2 grid <= 128), where a launch per level (~4 us even with PDL) costs far
@@ -1050,40 +1052,53 @@ __device__ __forceinline__ void cta_row_load(CtaRow<T>& r, int64_t l, const int6
   }
 }
 
-template <typename T>
+// SMEM: the run is the whole half-sweep and x (n entries) fits in shared memory -- x is staged in
+// shared memory for all levels and written back once (every gather an on-chip load).
+template <typename T, bool SMEM>
 __global__ void __launch_bounds__(1024) k_gs_levels_cta(int64_t l0, int64_t l1, const int64_t* __restrict__ lp,
                                                         const int64_t* __restrict__ base,
                                                         const int32_t* __restrict__ rows,
                                                         const int64_t* __restrict__ sp,
                                                         const int32_t* __restrict__ col, const T* __restrict__ val,
                                                         const T* __restrict__ d, const T* __restrict__ b, T* x, T w,
-                                                        T w1, bool damped) {
+                                                        T w1, bool damped, int64_t n) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int kW = CtaRow<T>::kW;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* xs = reinterpret_cast<T*>(smem_raw);
+  auto xload = [&](int64_t k) -> T { return SMEM ? xs[k] : __ldcg(x + k); };
   CtaRow<T> cur, nxt;
   cta_row_load<T>(cur, l0, lp, base, rows, sp, col, val, d, b);
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (SMEM) {
+    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) xs[k] = __ldcg(x + k);
+    __syncthreads();
+  }
   for (int64_t l = l0; l < l1; ++l) {
     if (cur.on) {
-      const T xi = damped ? __ldcg(x + cur.i) : (T)0;
+      const T xi = damped ? xload(cur.i) : (T)0;
       T xv[kW];
 #pragma unroll
-      for (int u = 0; u < kW; ++u) xv[u] = cur.c[u] >= 0 ? __ldcg(x + cur.c[u]) : (T)0;
+      for (int u = 0; u < kW; ++u) xv[u] = cur.c[u] >= 0 ? xload(cur.c[u]) : (T)0;
       T s = cur.s;
 #pragma unroll
       for (int u = 0; u < kW; ++u)
         if (cur.c[u] >= 0) s = sub_rn<T>(s, mul_rn<T>(cur.v[u], xv[u]));
       for (int j = kW; j < cur.wd; ++j) {
         const int32_t cc = col[cur.q0 + 32 * j];
-        if (cc >= 0) s = sub_rn<T>(s, mul_rn<T>(val[cur.q0 + 32 * j], __ldcg(x + cc)));
+        if (cc >= 0) s = sub_rn<T>(s, mul_rn<T>(val[cur.q0 + 32 * j], xload(cc)));
       }
       const T q = div_rn<T>(s, cur.di);
-      x[cur.i] = damped ? add_rn<T>(mul_rn<T>(w1, xi), mul_rn<T>(w, q)) : q;
+      const T xn = damped ? add_rn<T>(mul_rn<T>(w1, xi), mul_rn<T>(w, q)) : q;
+      if (SMEM) xs[cur.i] = xn;
+      else x[cur.i] = xn;
     }
     if (l + 1 < l1) cta_row_load<T>(nxt, l + 1, lp, base, rows, sp, col, val, d, b);
     __syncthreads();
     cur = nxt;
   }
+  if (SMEM)
+    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) x[k] = xs[k];
 }
 
 // out[t] = v[rows[t]]: the diagonal in group order (Sell::dord)
@@ -1407,19 +1422,37 @@ static int gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omeg
             RS_CUDA(cudaMemcpy(m->lv_slice_base_dev[bwd], base, sizeof(int64_t) * (lv.nlevels + 1),
                                cudaMemcpyHostToDevice));
           }
+          // the whole half-sweep in one CTA with x resident in shared memory when it fits
+          static const bool smem_ok = !getenv("RS_GS_SMEM") || atoi(getenv("RS_GS_SMEM")) != 0;
+          const size_t xbytes = sizeof(T) * (size_t)c.n;
+          const bool in_smem = smem_ok && l == 0 && l2 == lv.nlevels && xbytes <= kGsSmemBytes;
           cudaLaunchConfig_t cfgl = {};
           cfgl.gridDim = dim3(1);
           cfgl.blockDim = dim3(1024);
+          cfgl.dynamicSmemBytes = in_smem ? xbytes : 0;
           cfgl.stream = st;
           cudaLaunchAttribute at[1];
           at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
           at[0].val.programmaticStreamSerializationAllowed = 1;
           cfgl.attrs = at;
           cfgl.numAttrs = 1;
-          RS_CUDA(cudaLaunchKernelEx(&cfgl, k_gs_levels_cta<T>, l, l2, (const int64_t*)lv.level_ptr_dev,
-                                     (const int64_t*)m->lv_slice_base_dev[bwd], (const int32_t*)lv.rows,
-                                     (const int64_t*)S.slice_ptr, (const int32_t*)S.col, (const T*)S.val, c.d, b, x,
-                                     w, w1, damped));
+          if (in_smem) {
+            static bool attr_set = false;
+            if (!attr_set) {
+              RS_CUDA(cudaFuncSetAttribute(k_gs_levels_cta<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)kGsSmemBytes));
+              attr_set = true;
+            }
+            RS_CUDA(cudaLaunchKernelEx(&cfgl, k_gs_levels_cta<T, true>, l, l2, (const int64_t*)lv.level_ptr_dev,
+                                       (const int64_t*)m->lv_slice_base_dev[bwd], (const int32_t*)lv.rows,
+                                       (const int64_t*)S.slice_ptr, (const int32_t*)S.col, (const T*)S.val, c.d, b,
+                                       x, w, w1, damped, (int64_t)c.n));
+          } else {
+            RS_CUDA(cudaLaunchKernelEx(&cfgl, k_gs_levels_cta<T, false>, l, l2, (const int64_t*)lv.level_ptr_dev,
+                                       (const int64_t*)m->lv_slice_base_dev[bwd], (const int32_t*)lv.rows,
+                                       (const int64_t*)S.slice_ptr, (const int32_t*)S.col, (const T*)S.val, c.d, b,
+                                       x, w, w1, damped, (int64_t)c.n));
+          }
           RS_COUNT_LAUNCH();
           l = l2 - 1;
           continue;
