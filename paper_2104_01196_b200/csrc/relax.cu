@@ -1003,7 +1003,8 @@ Sell<double>& lv_sell<double>(rs_matrix* m, int bwd) { return m->LV64[bwd]; }
 template <>
 Sell<float>& lv_sell<float>(rs_matrix* m, int bwd) { return m->LV32[bwd]; }
 
-constexpr size_t kGsSmemBytes = 200 * 1024;  // x staged in shared memory up to this size
+constexpr size_t kGsSmemBytes = 192 * 1024;  // x staged in shared memory up to this size
+constexpr int64_t kGsMaxRun = 2047;           // levels per single-CTA run (their bounds staged in smem)
 
 // Consecutive SMALL levels (at most blockDim rows each) of the level-scheduled GS in ONE CTA: the
 // levels at both ends of a stencil's DAG hold few rows (level l of a 3D 7-point grid has ~l^2/2;
@@ -1064,17 +1065,27 @@ __global__ void __launch_bounds__(1024) k_gs_levels_cta(int64_t l0, int64_t l1, 
                                                         T w1, bool damped, int64_t n) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int kW = CtaRow<T>::kW;
+  // shared memory: the run's level bounds and slice bases (one dependent global hop less per
+  // level), then x (SMEM)
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* xs = reinterpret_cast<T*>(smem_raw);
+  const int64_t nl = l1 - l0;
+  int64_t* lps = reinterpret_cast<int64_t*>(smem_raw);
+  int64_t* bss = lps + (nl + 1);
+  T* xs = reinterpret_cast<T*>(bss + (nl + 1));
   auto xload = [&](int64_t k) -> T { return SMEM ? xs[k] : __ldcg(x + k); };
+  for (int64_t k = threadIdx.x; k <= nl; k += blockDim.x) {
+    lps[k] = lp[l0 + k];
+    bss[k] = base[l0 + k];
+  }
+  __syncthreads();
   CtaRow<T> cur, nxt;
-  cta_row_load<T>(cur, l0, lp, base, rows, sp, col, val, d, b);
+  cta_row_load<T>(cur, 0, lps, bss, rows, sp, col, val, d, b);
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (SMEM) {
     for (int64_t k = threadIdx.x; k < n; k += blockDim.x) xs[k] = __ldcg(x + k);
     __syncthreads();
   }
-  for (int64_t l = l0; l < l1; ++l) {
+  for (int64_t l = 0; l < nl; ++l) {
     if (cur.on) {
       const T xi = damped ? xload(cur.i) : (T)0;
       T xv[kW];
@@ -1093,7 +1104,7 @@ __global__ void __launch_bounds__(1024) k_gs_levels_cta(int64_t l0, int64_t l1, 
       if (SMEM) xs[cur.i] = xn;
       else x[cur.i] = xn;
     }
-    if (l + 1 < l1) cta_row_load<T>(nxt, l + 1, lp, base, rows, sp, col, val, d, b);
+    if (l + 1 < nl) cta_row_load<T>(nxt, l + 1, lps, bss, rows, sp, col, val, d, b);
     __syncthreads();
     cur = nxt;
   }
@@ -1411,7 +1422,7 @@ static int gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omeg
         if (!cnt) continue;
         if (pdl && cta_rows > 0 && cnt <= cta_rows && l + 1 < lv.nlevels && lcount(l + 1) <= cta_rows) {
           int64_t l2 = l + 1;
-          while (l2 < lv.nlevels && lcount(l2) <= cta_rows) ++l2;
+          while (l2 < lv.nlevels && lcount(l2) <= cta_rows && l2 - l < kGsMaxRun) ++l2;
           if (!lv.level_ptr_dev) {
             RS_CUDA(cudaMalloc(&lv.level_ptr_dev, sizeof(int64_t) * (lv.nlevels + 1)));
             RS_CUDA(cudaMemcpy(lv.level_ptr_dev, lv.level_ptr_host, sizeof(int64_t) * (lv.nlevels + 1),
@@ -1429,7 +1440,7 @@ static int gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omeg
           cudaLaunchConfig_t cfgl = {};
           cfgl.gridDim = dim3(1);
           cfgl.blockDim = dim3(1024);
-          cfgl.dynamicSmemBytes = in_smem ? xbytes : 0;
+          cfgl.dynamicSmemBytes = sizeof(int64_t) * 2 * (size_t)(l2 - l + 1) + (in_smem ? xbytes : 0);
           cfgl.stream = st;
           cudaLaunchAttribute at[1];
           at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1440,7 +1451,7 @@ static int gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omeg
             static bool attr_set = false;
             if (!attr_set) {
               RS_CUDA(cudaFuncSetAttribute(k_gs_levels_cta<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)kGsSmemBytes));
+                                           (int)(kGsSmemBytes + sizeof(int64_t) * 2 * (kGsMaxRun + 1))));
               attr_set = true;
             }
             RS_CUDA(cudaLaunchKernelEx(&cfgl, k_gs_levels_cta<T, true>, l, l2, (const int64_t*)lv.level_ptr_dev,
