@@ -1423,6 +1423,11 @@ static int gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omeg
         if (pdl && cta_rows > 0 && cnt <= cta_rows && l + 1 < lv.nlevels && lcount(l + 1) <= cta_rows) {
           int64_t l2 = l + 1;
           while (l2 < lv.nlevels && lcount(l2) <= cta_rows && l2 - l < kGsMaxRun) ++l2;
+          // one thread per row of the widest level of the run (fewer warps per barrier)
+          static const bool fit = !getenv("RS_GS_CTA_FIT") || atoi(getenv("RS_GS_CTA_FIT")) != 0;
+          int64_t widest = 1;
+          for (int64_t q = l; q < l2; ++q) widest = std::max<int64_t>(widest, lcount(q));
+          const unsigned cta_threads = fit ? (unsigned)std::min<int64_t>(1024, (widest + 31) / 32 * 32) : 1024u;
           if (!lv.level_ptr_dev) {
             RS_CUDA(cudaMalloc(&lv.level_ptr_dev, sizeof(int64_t) * (lv.nlevels + 1)));
             RS_CUDA(cudaMemcpy(lv.level_ptr_dev, lv.level_ptr_host, sizeof(int64_t) * (lv.nlevels + 1),
@@ -1439,7 +1444,7 @@ static int gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omeg
           const bool in_smem = smem_ok && l == 0 && l2 == lv.nlevels && xbytes <= kGsSmemBytes;
           cudaLaunchConfig_t cfgl = {};
           cfgl.gridDim = dim3(1);
-          cfgl.blockDim = dim3(1024);
+          cfgl.blockDim = dim3(cta_threads);
           cfgl.dynamicSmemBytes = sizeof(int64_t) * 2 * (size_t)(l2 - l + 1) + (in_smem ? xbytes : 0);
           cfgl.stream = st;
           cudaLaunchAttribute at[1];
