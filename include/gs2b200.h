@@ -229,6 +229,23 @@ int rs_dot(int64_t n, const double *x, const double *y, double *out, double *wor
 /* x += z */
 int rs_axpy1(int64_t n, const double *z, double *x, rs_stream_t stream);
 
+/* ---- the reference's BLAS summation orders (blasorder.cu; ortho="mgs_ref") ----
+ * numpy -> OpenBLAS 0.3.30 (core SkylakeX, 1 thread) is what rounds the reference's GMRES / CG
+ * scalars: `v[i] @ w`, `np.linalg.norm(w)` (ddot; krylov.py:190, 194, 218, 220, 246) and
+ * `v[:j+1].T @ y` (dgemv 'N'; krylov.py:244).  These entry points reproduce those orders bit for
+ * bit (order restated in oracle/oracle.c), so the GMRES history is the reference's own.  A ddot
+ * is 32 sequential FMA chains of n/32 steps: latency-bound, a parity mode. */
+/* out[0] = ddot(x, y) (sqrt of it when sqrt_out) */
+int rs_dot_blas(int64_t n, const double *x, const double *y, double *out, int sqrt_out, rs_stream_t stream);
+/* rs_mgs_step with the dot in ddot order (krylov.py:217-220) */
+int rs_mgs_step_blas(int64_t n, const double *v_prev, const double *h_prev, const double *v_cur, double *w,
+                     double *out, rs_stream_t stream);
+/* out[r] = sum_{i<k} V_i[r] y[i] in dgemv_n order (krylov.py:244) */
+int rs_gemv_n_blas(const double *V, int64_t ldv, int k, int64_t n, const double *y, double *out,
+                   rs_stream_t stream);
+/* host ddot in the same order (back substitution `h[i, i+1:j+1] @ y[i+1:j+1]`, krylov.py:243) */
+double rs_host_ddot_blas(int64_t n, const double *x, const double *y);
+
 /* y = y + a*x and y = x + b*y, each product and sum rounded separately (no FMA):
  * the CG updates x += alpha p, r -= alpha Ap, p = z + beta p (krylov.py:296-307) */
 int rs_axpy(int64_t n, double a, const double *x, double *y, rs_stream_t stream);

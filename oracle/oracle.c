@@ -304,26 +304,94 @@ int orc_precond_apply(orc_precond *p, const double *r, double *zout, int64_t *er
 }
 
 /* ---------------------------------------------------------------- BLAS-1 */
-#define DOT_CHUNK 4096
-double orc_dot(int64_t n, const double *x, const double *y) {
-  int64_t nc = (n + DOT_CHUNK - 1) / DOT_CHUNK;
-  if (nc <= 1) {
-    double s = 0.0;
-    for (int64_t i = 0; i < n; ++i) { double p = x[i] * y[i]; s = s + p; }
-    return s;
+/* ---------------------------------------------------------------- BLAS-1/2 in the reference's order
+ * The reference's dots / norms / basis combination are numpy calls into OpenBLAS (krylov.py:190, 194,
+ * 202, 218, 220, 243, 244, 246: `np.linalg.norm(v)` = sqrt(ddot(v, v)), `v[i] @ w` = ddot,
+ * `v[:j+1].T @ y` = dgemv 'N' on the column-major n x (j+1) view).  OpenBLAS is a third-party
+ * dependency not vendored under /root/reference; the version the reference ran with here is
+ * OpenBLAS 0.3.30 (scipy-openblas64 wheel of numpy 2.3.5, DYNAMIC_ARCH, core "SkylakeX" on this
+ * container's Xeon), OPENBLAS_NUM_THREADS=1.  Its summation orders, restated below,
+ * were determined by bitwise experiments against np.dot / np.matmul on random vectors (n = 1..200,
+ * 1000, 4097, 65549, 100003, 262144, 2097169, 256^3; gemv n x k, k = 1..9, 13, 33, 60, 61):
+ *
+ * ddot (kernel/x86_64/ddot.c + ddot_microk_skylakex-2.c): n1 = n & -16 elements go through the kernel:
+ *   32-element blocks into 4 x 8 fused-multiply-add accumulators acc[a][l] (element 8a+l of the block),
+ *   each folded to 4 x 4 as acc[a][l] + acc[a][l+4]; a remaining 16-element block (n1 % 32 == 16) is
+ *   FMA-accumulated into the folded acc[a][l] (element 4a+l); then s_l = ((acc0+acc1)+acc2)+acc3,
+ *   dot = (s0+s2) + (s1+s3).  The n - n1 < 16 tail elements follow as dot = fma(y_i, x_i, dot).
+ * dgemv_n (kernel/x86_64/dgemv_n_4.c): rows below m & ~3: for each group of 4 columns c..c+3,
+ *   t = a_{c+1} x_{c+1}; t = fma(a_c, x_c, t); t = fma(a_{c+2}, x_{c+2}, t); t = fma(a_{c+3}, x_{c+3}, t);
+ *   y = y + t; then 2 leftover columns t = fma(a_c, x_c, a_{c+1} x_{c+1}), y = y + t; then 1 leftover
+ *   column y = y + a_c x_c (rounded product).  The last m & 3 rows: t = 0, t = fma(a_c, x_c, t) over all
+ *   columns in order, y = 0 + t.  (numpy passes beta = 0, alpha = 1, so y starts at 0.)
+ * These are the reference's exact roundings on this container, which is what lets the GMRES / CG
+ * histories be checked bitwise (tests/test_oracle.py::test_gmres_histories_bitwise).  fma() is the
+ * correctly rounded C99 fused multiply-add. */
+#if defined(__x86_64__) && defined(__GNUC__)
+#define ORC_FMA_TARGET __attribute__((target("fma")))
+#else
+#define ORC_FMA_TARGET
+#endif
+
+ORC_FMA_TARGET static double blas_ddot(int64_t n, const double *x, const double *y) {
+  int64_t n1 = n & ~(int64_t)15, n32 = n1 & ~(int64_t)31, i = 0;
+  double dot = 0.0;
+  if (n1 > 0) {
+    double a5[4][8] = {{0}}, a4[4][4];
+    for (; i < n32; i += 32)
+      for (int a = 0; a < 4; ++a)
+        for (int l = 0; l < 8; ++l) a5[a][l] = fma(x[i + 8 * a + l], y[i + 8 * a + l], a5[a][l]);
+    for (int a = 0; a < 4; ++a)
+      for (int l = 0; l < 4; ++l) a4[a][l] = a5[a][l] + a5[a][l + 4];
+    for (; i < n1; i += 16)
+      for (int a = 0; a < 4; ++a)
+        for (int l = 0; l < 4; ++l) a4[a][l] = fma(x[i + 4 * a + l], y[i + 4 * a + l], a4[a][l]);
+    double s[4];
+    for (int l = 0; l < 4; ++l) s[l] = ((a4[0][l] + a4[1][l]) + a4[2][l]) + a4[3][l];
+    dot = (s[0] + s[2]) + (s[1] + s[3]);
   }
-  double *part = (double *)malloc(sizeof(double) * (size_t)nc);
+  for (; i < n; ++i) dot = fma(y[i], x[i], dot);
+  return dot;
+}
+
+/* out[r] = sum_c v[c * ldv + r] * y[c], c < k: `v[:k].T @ y` (krylov.py:244) in dgemv_n order */
+ORC_FMA_TARGET static void blas_dgemv_t_rows(int64_t n, int k, const double *v, int64_t ldv, const double *y,
+                                             double *out) {
+  int64_t mm = n & ~(int64_t)3;
 #pragma omp parallel for schedule(static) if (n > 65536)
-  for (int64_t c = 0; c < nc; ++c) {
-    int64_t lo = c * DOT_CHUNK, hi = lo + DOT_CHUNK < n ? lo + DOT_CHUNK : n;
-    double s = 0.0;
-    for (int64_t i = lo; i < hi; ++i) { double p = x[i] * y[i]; s = s + p; }
-    part[c] = s;
+  for (int64_t r = 0; r < n; ++r) {
+    double acc = 0.0;
+    if (r < mm) {
+      int c = 0;
+      for (; c + 4 <= k; c += 4) {
+        double t = v[(size_t)(c + 1) * ldv + r] * y[c + 1];
+        t = fma(v[(size_t)c * ldv + r], y[c], t);
+        t = fma(v[(size_t)(c + 2) * ldv + r], y[c + 2], t);
+        t = fma(v[(size_t)(c + 3) * ldv + r], y[c + 3], t);
+        acc = acc + t;
+      }
+      if (k - c >= 2) {
+        double t = fma(v[(size_t)c * ldv + r], y[c], v[(size_t)(c + 1) * ldv + r] * y[c + 1]);
+        acc = acc + t;
+        c += 2;
+      }
+      if (k - c >= 1) {
+        double t = v[(size_t)c * ldv + r] * y[c];
+        acc = acc + t;
+      }
+    } else {
+      double t = 0.0;
+      for (int c = 0; c < k; ++c) t = fma(v[(size_t)c * ldv + r], y[c], t);
+      acc = acc + t;
+    }
+    out[r] = acc;
   }
-  double s = 0.0;
-  for (int64_t c = 0; c < nc; ++c) s = s + part[c];
-  free(part);
-  return s;
+}
+
+double orc_dot(int64_t n, const double *x, const double *y) { return blas_ddot(n, x, y); }
+
+void orc_gemv_t_rows(int64_t n, int k, const double *v, int64_t ldv, const double *y, double *out) {
+  blas_dgemv_t_rows(n, k, v, ldv, y, out);
 }
 
 static double nrm2(int64_t n, const double *x) { return sqrt(orc_dot(n, x, x)); }
@@ -415,15 +483,11 @@ int orc_gmres(const orc_csr *a, const double *b, orc_precond *m, int restart, do
       if (est <= tol || lucky) break;
     }
     for (int i = j; i >= 0; --i) { /* back substitution (krylov.py:241-243) */
-      double s = 0.0;
-      for (int k = i + 1; k <= j; ++k) { double p = H(i, k) * y[k]; s = s + p; }
+      /* h[i, i+1:j+1] @ y[i+1:j+1]: a ddot of length j - i (row i of h is contiguous) */
+      double s = blas_ddot(j - i, &H(i, i + 1), y + i + 1);
       y[i] = (g[i] - s) / H(i, i);
     }
-    for (int64_t k = 0; k < n; ++k) { /* V^T y (krylov.py:244) */
-      double s = 0.0;
-      for (int i = 0; i <= j; ++i) { double p = v[(size_t)i * n + k] * y[i]; s = s + p; }
-      t[k] = s;
-    }
+    blas_dgemv_t_rows(n, j + 1, v, n, y, t); /* V^T y (krylov.py:244) */
     if (m) { status = orc_precond_apply(m, t, z, &ei); if (status) goto done; }
     else memcpy(z, t, sizeof(double) * (size_t)n);
     for (int64_t k = 0; k < n; ++k) x[k] = x[k] + z[k];

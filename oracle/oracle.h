@@ -116,7 +116,9 @@ int orc_cg(const orc_csr *a, const double *b, orc_precond *m, double tol, int ma
            double *hist, int *iters, int *conv);
 
 void orc_random_rhs(int64_t n, uint64_t seed, double *out);
-double orc_dot(int64_t n, const double *x, const double *y);
+double orc_dot(int64_t n, const double *x, const double *y);  /* OpenBLAS 0.3.30 SkylakeX ddot order */
+/* out[r] = sum_{c<k} v[c*ldv + r] y[c] in OpenBLAS dgemv_n order (`v[:k].T @ y`, krylov.py:244) */
+void orc_gemv_t_rows(int64_t n, int k, const double *v, int64_t ldv, const double *y, double *out);
 
 #ifdef __cplusplus
 }

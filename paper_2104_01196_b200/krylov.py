@@ -303,6 +303,11 @@ def gmres(a, b, m=None, restart: int = 60, tol: float = 1e-9, maxit: int = 10000
     (krylov.py:217-219), one fused update+dot launch per basis vector -- the
     reference-faithful mode (same iteration counts where the reference's are
     dot-order stable), ~1.3x the basis traffic of CGS2.
+    ``ortho="mgs_ref"``: the same MGS loop with every dot, norm and basis
+    combination summed in the reference's own BLAS order (OpenBLAS 0.3.30
+    ddot / dgemv_n, blasorder.cu; back substitution likewise on the host):
+    the history is bitwise the reference's.  Each dot is a latency-bound
+    32-chain FMA recurrence (~n/32 dependent steps) -- a parity mode.
 
     Returns ``(x, ConvergenceHistory)``; ``x`` is a numpy array when ``b`` is
     numpy, a CUDA tensor when ``b`` is a CUDA tensor.  History: the Arnoldi
@@ -348,8 +353,8 @@ def release_workspace() -> None:
 
 def _check_ortho(ortho, n, restart):
     """Validate / resolve the orthogonalisation mode ("auto" -> "dcgs2" where it applies)."""
-    if ortho not in ("auto", "cgs2", "mgs", "dcgs2"):
-        raise ValueError(f"ortho must be 'auto', 'cgs2', 'dcgs2' or 'mgs', got {ortho!r}")
+    if ortho not in ("auto", "cgs2", "mgs", "mgs_ref", "dcgs2"):
+        raise ValueError(f"ortho must be 'auto', 'cgs2', 'dcgs2', 'mgs' or 'mgs_ref', got {ortho!r}")
     dcgs_ok = restart <= 63 and n % 2 == 0
     if ortho == "auto":
         return "dcgs2" if dcgs_ok else "cgs2"
@@ -428,8 +433,25 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
             else:
                 chk(lib.rs_spmv(dm.handle, _p(src), None, None, _p(dst), st), "spmv")
 
+    blas_order = ortho == "mgs_ref"
+    if blas_order and reduce_fn is not None:
+        raise ValueError("ortho='mgs_ref' (the reference's BLAS summation order) is single-GPU only")
+
+    def norm2_into(vec):
+        """nrm2_slot = vec . vec (np.linalg.norm(vec)**2 before the sqrt, krylov.py:190)"""
+        if blas_order:
+            chk(lib.rs_dot_blas(n, _p(vec), _p(vec), _p(nrm2_slot), 0, st), "dot_blas")
+        else:
+            chk(lib.rs_dot(n, _p(vec), _p(vec), _p(nrm2_slot), _p(work), st), "dot")
+
+    def sub_norm(dst):
+        """dst = b - t and nrm2_slot = dst . dst (krylov.py:193-194, 245-246)"""
+        chk(lib.rs_sub_norm(n, _p(b), _p(ws.t), _p(dst), _p(nrm2_slot), _p(work), st), "sub_norm")
+        if blas_order:
+            norm2_into(dst)
+
     def norm_of(vec):
-        chk(lib.rs_dot(n, _p(vec), _p(vec), _p(nrm2_slot), _p(work), st), "dot")
+        norm2_into(vec)
         reduce_(nrm2_slot)
         return math.sqrt(float(nrm2_slot.item()))
 
@@ -471,7 +493,7 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
             rnorm = bnorm
         else:
             spmv(x, ws.t)
-            chk(lib.rs_sub_norm(n, _p(b), _p(ws.t), _p(ws.r), _p(nrm2_slot), _p(work), st), "sub_norm")
+            sub_norm(ws.r)
             reduce_(nrm2_slot)
             rnorm = math.sqrt(float(nrm2_slot.item()))
         hist = [rnorm / bnorm]
@@ -491,7 +513,17 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
             _apply_op(op, V[jj], ws.z, ws)
         spmv(ws.z, ws.w)
         k = jj + 1
-        if ortho == "mgs" and reduce_fn is None:
+        if blas_order:
+            # the reference's MGS loop with its OpenBLAS ddot order (blasorder.cu)
+            h2.zero_()
+            with _timed("mgs"):
+                for i in range(k + 1):
+                    vp = _p(V[i - 1]) if i > 0 else None
+                    hp = _p(h1[i - 1:i]) if i > 0 else None
+                    out = _p(h1[i:i + 1]) if i < k else _p(nrm2_slot)
+                    vc = _p(V[i]) if i < k else None
+                    chk(lib.rs_mgs_step_blas(n, vp, hp, vc, _p(ws.w), out, st), "mgs_blas")
+        elif ortho == "mgs" and reduce_fn is None:
             # MGS (krylov.py:217-220): h_i = v_i . w ; w -= h_i v_i, one fused launch per i
             h2.zero_()
             with _timed("mgs"):
@@ -711,15 +743,23 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
                 status[1:3].zero_()
         # least squares + update (krylov.py:241-244)
         y = np.zeros(j + 1)
-        for i in range(j, -1, -1):
-            y[i] = (g[i] - h[i, i + 1:j + 1] @ y[i + 1:j + 1]) / h[i, i]
+        if blas_order:  # `h[i, i+1:j+1] @ y[i+1:j+1]` in the reference's ddot order, host-independent
+            hp, yp = h.ctypes.data, y.ctypes.data
+            for i in range(j, -1, -1):
+                s = lib.rs_host_ddot_blas(j - i, C.c_void_p(hp + 8 * (i * restart + i + 1)),
+                                          C.c_void_p(yp + 8 * (i + 1)))
+                y[i] = (g[i] - s) / h[i, i]
+        else:
+            for i in range(j, -1, -1):
+                y[i] = (g[i] - h[i, i + 1:j + 1] @ y[i + 1:j + 1]) / h[i, i]
         ws.y[: j + 1].copy_(torch.from_numpy(y))
-        chk(lib.rs_gemv_n(_p(V), ws.ldv, j + 1, n, _p(ws.y), _p(ws.t), st), "gemv_n")
+        gemv = lib.rs_gemv_n_blas if blas_order else lib.rs_gemv_n
+        chk(gemv(_p(V), ws.ldv, j + 1, n, _p(ws.y), _p(ws.t), st), "gemv_n")
         _apply_op(op, ws.t, ws.z, ws)
         chk(lib.rs_axpy1(n, _p(ws.z), _p(x), st), "axpy")
         # true residual (krylov.py:245-249)
         spmv(x, ws.t)
-        chk(lib.rs_sub_norm(n, _p(b), _p(ws.t), _p(ws.r), _p(nrm2_slot), _p(work), st), "sub_norm")
+        sub_norm(ws.r)
         reduce_(nrm2_slot)
         r0 = ws.r
         rnorm = math.sqrt(float(nrm2_slot.item()))

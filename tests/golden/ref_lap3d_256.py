@@ -5,7 +5,13 @@ Test infrastructure: pins the C2 iteration count on the reference itself (the C 
 Multi-hour single-core run; progress (preconditioner applications) goes to stderr.
 
     OPENBLAS_NUM_THREADS=1 NUMBA_NUM_THREADS=1 NUMBA_CACHE_DIR=/tmp/numba_cache \
-        python tests/golden/ref_lap3d_256.py [nx]
+        python tests/golden/ref_lap3d_256.py [nx] [--tag T] [--dots pairwise]
+
+Spread runs (VERDICT r1 "pin C2 parity"): the same run with another OPENBLAS_NUM_THREADS
+(``--tag t8``), or with the MGS dot ``v[i] @ w`` (krylov.py:218) replaced by numpy's pairwise
+``np.add.reduce(v[i] * w)`` in a scratch copy of the reference under /tmp (``--dots pairwise``),
+measure how far the reference's OWN count moves with the dot-product summation order.
+Outputs ``ref_lap3d_<nx>[_<tag>].json``.
 """
 
 from __future__ import annotations
@@ -21,7 +27,26 @@ import sys
 import time
 from pathlib import Path
 
-sys.path.insert(0, "/root/reference/pkg/src")
+import argparse  # noqa: E402
+import shutil  # noqa: E402
+
+_ap = argparse.ArgumentParser()
+_ap.add_argument("nx", nargs="?", type=int, default=256)
+_ap.add_argument("--tag", default="")
+_ap.add_argument("--dots", choices=("blas", "pairwise"), default="blas")
+ARGS = _ap.parse_args()
+
+if ARGS.dots == "pairwise":
+    # scratch copy of the reference package with only the MGS dot's summation order changed
+    _dst = Path(f"/tmp/ref_pairwise_{os.getpid()}")
+    shutil.copytree("/root/reference/pkg/src/relaxsolve", _dst / "relaxsolve")
+    _k = _dst / "relaxsolve" / "krylov.py"
+    _src = _k.read_text()
+    assert _src.count("h[i, j] = v[i] @ w") == 1
+    _k.write_text(_src.replace("h[i, j] = v[i] @ w", "h[i, j] = np.add.reduce(v[i] * w)"))
+    sys.path.insert(0, str(_dst))
+else:
+    sys.path.insert(0, "/root/reference/pkg/src")
 
 import numpy as np  # noqa: E402
 
@@ -31,7 +56,7 @@ HERE = Path(__file__).parent
 
 
 def main() -> None:
-    nx = int(sys.argv[1]) if len(sys.argv) > 1 else 256
+    nx = ARGS.nx
     t0 = time.time()
     a = rs.laplace3d(nx)
     b = rs.random_rhs(a.nrows, 0)
@@ -51,7 +76,10 @@ def main() -> None:
     t_solve = time.time() - t1
     res = np.asarray(h.rel_res)
     out = {
-        "label": f"lap3d_{nx}__m60__gs2_1_1_1 (reference relaxsolve, OPENBLAS_NUM_THREADS=1)",
+        "label": f"lap3d_{nx}__m60__gs2_1_1_1 (reference relaxsolve, "
+        f"OPENBLAS_NUM_THREADS={os.environ['OPENBLAS_NUM_THREADS']}, dots={ARGS.dots})",
+        "openblas_num_threads": int(os.environ["OPENBLAS_NUM_THREADS"]),
+        "dots": ARGS.dots,
         "iterations": int(h.iterations),
         "converged": bool(h.converged),
         "final_rel_res": float(res[-1]),
@@ -60,7 +88,8 @@ def main() -> None:
         "solve_seconds": t_solve,
         "numpy": np.__version__,
     }
-    (HERE / f"ref_lap3d_{nx}.json").write_text(json.dumps(out, indent=1) + "\n")
+    tag = f"_{ARGS.tag}" if ARGS.tag else ""
+    (HERE / f"ref_lap3d_{nx}{tag}.json").write_text(json.dumps(out, indent=1) + "\n")
     print(json.dumps({k: out[k] for k in ("iterations", "converged", "final_rel_res", "solve_seconds")}))
 
 

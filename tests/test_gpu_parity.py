@@ -627,3 +627,75 @@ def test_sweeps_bitwise_at_full_c2_size():
     assert np.array_equal(y.cpu().numpy(), oracle.spmv(om, x0))
     z = g2.Preconditioner(dev, "gs2", g2.RelaxConfig(1, 1, 1)).apply(bt)
     assert np.array_equal(z.cpu().numpy(), oracle.Precond(om, "gs2", n_j=1).apply(b))
+
+
+def test_blas_order_kernels_bitwise():
+    """rs_dot_blas / rs_mgs_step_blas / rs_gemv_n_blas / rs_host_ddot_blas reproduce the reference's
+    OpenBLAS summation orders (restated and pinned against numpy in oracle.c) bit for bit, on every
+    branch: n % 32 >= 16, the < 16 tail, tiny n, unaligned vectors (direct-load kernel), k % 4."""
+    import ctypes
+
+    from paper_2104_01196_b200 import _native
+
+    lib = _native.load()
+    st = None
+    rng = np.random.default_rng(11)
+    out = torch.zeros(4, dtype=torch.float64, device="cuda")
+    for n in [0, 1, 5, 15, 16, 17, 31, 32, 33, 47, 48, 63, 64, 65, 100, 1000, 2047, 2048, 2049, 4097, 12288 + 16,
+              65549, (1 << 20) + 19, 3_000_001]:
+        x = rng.standard_normal(n + 1)
+        y = rng.uniform(-1, 1, n + 1)
+        xt, yt = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+        want = oracle.dot(x[:n], y[:n])
+        _native.check(lib.rs_dot_blas(n, xt.data_ptr(), yt.data_ptr(), out.data_ptr(), 0, st))
+        _native.check(lib.rs_dot_blas(n, xt[1:].data_ptr(), yt[1:].data_ptr(), out[1:].data_ptr(), 0, st))
+        _native.check(lib.rs_dot_blas(n, xt.data_ptr(), xt.data_ptr(), out[2:].data_ptr(), 1, st))
+        o = out.cpu().numpy()
+        assert o[0] == want, n
+        assert o[1] == oracle.dot(x[1:], y[1:]), n
+        assert o[2] == np.sqrt(oracle.dot(x[:n], x[:n])), n
+        assert lib.rs_host_ddot_blas(n, ctypes.c_void_p(x.ctypes.data), ctypes.c_void_p(y.ctypes.data)) == want
+    # MGS step: w -= h v_prev ; out = v_cur . w
+    n = 100003
+    vp, vc, w = (rng.standard_normal(n) for _ in range(3))
+    hh = np.array([0.37])
+    wt = torch.from_numpy(w.copy()).cuda()
+    vpt, vct, ht = (torch.from_numpy(a).cuda() for a in (vp, vc, hh))
+    _native.check(lib.rs_mgs_step_blas(n, vpt.data_ptr(), ht.data_ptr(), vct.data_ptr(), wt.data_ptr(),
+                                       out.data_ptr(), st))
+    w2 = w - hh[0] * vp
+    assert np.array_equal(wt.cpu().numpy(), w2)
+    assert float(out[0]) == oracle.dot(vc, w2)
+    for n, k in [(1000, 1), (1001, 2), (1002, 3), (1003, 4), (999, 5), (64, 6), (77, 7), (4096, 13), (513, 61),
+                 (262146, 60)]:
+        V = rng.standard_normal((k, n))
+        yk = rng.standard_normal(k)
+        Vt, yt = torch.from_numpy(V).cuda(), torch.from_numpy(yk).cuda()
+        o = torch.empty(n, dtype=torch.float64, device="cuda")
+        _native.check(lib.rs_gemv_n_blas(Vt.data_ptr(), n, k, n, yt.data_ptr(), o.data_ptr(), st))
+        assert np.array_equal(o.cpu().numpy(), oracle.gemv_t_rows(V, yk)), (n, k)
+
+
+MGS_REF_LABELS = [lb for lb in GMRES_FAST if "hybrid" not in lb] + [
+    "lap2d_128__m30__none", "ela3d_8__m60__gs2_1_1_1", "ela3d_8__m60__gs2_1_1_3", "ela3d_8__m60__jr_1",
+    "cd3d_16__m60__gs2_1_1_2__same", "cd3d_16__m60__gs2_1_1_2__single_inside_double",
+    "ela3d_16__m60__gs2_1_1_1", "ela3d_16__m60__gs_seq_1", "lap3d_64__m60__gs2_1_1_1", "lap3d_64__m60__gs_seq_1"]
+
+
+@pytest.mark.parametrize("label", MGS_REF_LABELS)
+def test_gmres_mgs_ref_bitwise(label, gmres_golden):
+    """ortho="mgs_ref": the reference's MGS loop with its own OpenBLAS summation order for every dot,
+    norm and basis combination -- the GPU GMRES history equals the reference's recorded history
+    bit for bit (every Arnoldi estimate and every restart's true residual), not just the count."""
+    want = gmres_golden["runs"][label]
+    prob, m, kind, (nt, nk, nj), prec, nb = parse_gmres_label(label)
+    if prob.startswith("lap3d"):
+        a = g2.laplace3d(int(prob.split("_")[1]), device="cuda")
+    else:
+        a = golden_problem(prob)
+    b = g2.random_rhs(a.nrows, 0)
+    pc = g2.Preconditioner(a, kind, g2.RelaxConfig(nt, nk, nj) if kind != "none" else None, precision=prec)
+    _, h = g2.gmres(a, b, pc, restart=m, tol=1e-9, ortho="mgs_ref")
+    assert h.converged == want["converged"]
+    assert h.iterations == want["iterations"]
+    assert np.array_equal(np.asarray(h.rel_res), np.array(want["rel_res"]))

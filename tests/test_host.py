@@ -117,7 +117,7 @@ class TestRelaxConfig:
 
 def _header_symbols():
     txt = (ROOT / "include" / "gs2b200.h").read_text()
-    return sorted(set(re.findall(r"^(?:int|int64_t|const char \*)\s*(rs_\w+)\(", txt, re.M)))
+    return sorted(set(re.findall(r"^(?:int|int64_t|double|const char \*)\s*(rs_\w+)\(", txt, re.M)))
 
 
 def test_library_builds_and_exports_every_header_symbol():
