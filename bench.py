@@ -1,29 +1,33 @@
 #!/usr/bin/env python
 """bench.py -- GS2-preconditioned GMRES(60) on B200 (BASELINE.json metric / configs).
 
-One step = one full GMRES(60) restart cycle (60 Arnoldi iterations, each one
-zero-start GS2(1,1,1) preconditioner application + one SpMV + CGS2
-orthogonalisation, then the cycle-end update and true residual) on the
-synthetic 3D 7-point Laplace problem, right-hand side random_rhs(n, 0):
+One step = one full GMRES(60) restart cycle (60 Arnoldi iterations, each one zero-start
+GS2(1,1,1) preconditioner application + one SpMV + DCGS2 orthogonalisation, then the cycle-end
+update and true residual) on the synthetic 3D 7-point Laplace problem, b = random_rhs(n, 0):
 
 * N = 1: config C2, laplace3d 256^3 (16.7 M rows) on one B200.
-* N > 1: config C5, laplace3d 512^3 row-partitioned into N z-slabs (one rank
-  per GPU; hybrid block-Jacobi GS2 preconditioner; halo exchange and the
-  Gram-Schmidt allreduces over NVLink peer memory, the allreduces fused into
-  the CGS kernels -- ``--comm nccl`` for the NCCL baseline).
+* N > 1: config C5, laplace3d 512^3 row-partitioned into N z-slabs (one rank per GPU; hybrid
+  block-Jacobi GS2 preconditioner; halo exchange and the Gram-Schmidt allreduces over NVLink peer
+  memory, the allreduces fused into the CGS kernels -- ``--comm nccl`` for the NCCL baseline).
+  ``python bench.py --gpus N`` re-executes itself under ``torch.distributed.run`` with N ranks
+  when it is not already running under a launcher (WORLD_SIZE unset); rank 0 prints the line.
 
-``value`` = algorithmic HBM GB/s of the cycle (SURVEY.md §8(d) byte model:
-split-CSR int32 + fp64 per pass, summed over every kernel of the cycle and
-over all ranks) divided by the device time of the step, max over ranks.
-The GS2 sweep figure of the metric (non-zero x, n_j = 1, 2.946 GB at 256^3)
-and the paper's same-device baselines (JR, level-scheduled GS, n_j = 0..3)
-are reported under "sweeps"; time-to-solution of the full solve under "tts".
+``value`` (GB/s, higher is better) = W / t: W = the algorithmic HBM bytes of the kernel sequence
+the B200 path launches for the step's work (split-CSR int32 + fp64, each operand once per pass,
+fused passes counted once; summed over ranks), t = device time of the step (max over ranks).
+For our arm W is exactly the bytes the kernels must move, so value / the measured copy peak is
+the whole-cycle roofline fraction.  The reference arm (``--impl reference``) times the
+reference's CPU algorithm (the C oracle port, all host threads) on Arnoldi iterations sampled
+across the same 60-step cycle (stratified j) and divides the SAME W of those iterations by its
+time, so the driver's ratio of the two values is the time ratio on identical work; the oracle's
+own byte count is reported beside it.  The SURVEY §8(d) model bytes (unfused CGS2) stay as
+``config.model_bytes_per_step`` / ``model_gbs``.
 
-``c5_one_gpu`` (N = 1 only): the 512^3 cycle on one GPU, the strong-scaling reference of the
-N > 1 lines (``--no-c5`` skips it).
-
-``--impl reference`` times the reference's CPU algorithm (the C oracle port,
-all host threads) on a bounded sample of the same workload.
+Extra keys of the N = 1 line: ``sweeps`` (the metric's GS2 sweep GB/s and the paper's
+same-device baselines: JR, level-scheduled GS, multicolour GS, n_j = 0..3), ``tts`` (time to
+solution), ``c5_one_gpu`` (the 512^3 cycle on one GPU: the strong-scaling reference of the
+N > 1 lines), ``configs`` (C1, C3, C4 and the stand-alone smoother), ``setup`` (matrix build /
+split, level-set analysis, colouring), ``cpu_baseline`` (the oracle on one core).
 """
 
 from __future__ import annotations
@@ -100,17 +104,29 @@ class Model:
     def cgs_update(self, k: int):
         return (k + 2) * self.V            # V rows + w read, w written
 
+    def step_actual(self, j: int, n_j: int, ortho: str = "dcgs2"):
+        """Algorithmic bytes the B200 kernels move for Arnoldi iteration j (zero-start preconditioner,
+        SpMV, fused orthogonalisation passes over the k = j + 1 basis rows, 2V of vector passes)."""
+        k = j + 1
+        orth = (self.dcgs_dots(k) + self.dcgs_update(k)) if ortho == "dcgs2" else \
+            (self.cgs_dots(k) + 2 * self.cgs_update(k))
+        return self.precond_gs2_zero_start(n_j) + self.spmv() + 2 * self.V + orth
+
+    def cycle_end_actual(self, m: int, n_j: int, ortho: str = "dcgs2"):
+        """Cycle end: the last column's dots (DCGS2), V^T-combination, preconditioner, update, SpMV,
+        residual."""
+        V = self.V
+        last = self.dcgs_dots(m + 1) if ortho == "dcgs2" else 0
+        return last + (m + 2) * V + self.precond_gs2_zero_start(n_j) + 3 * V + self.spmv() + 3 * V
+
     def cycle_actual(self, m: int, n_j: int, ortho: str = "dcgs2"):
-        """Algorithmic bytes of the kernels one cycle actually launches (fused passes, zero-start
-        preconditioner model, cycle end: V^T-combination, preconditioner, update, SpMV, residual)."""
-        pre, sp, V = self.precond_gs2_zero_start(n_j), self.spmv(), self.V
-        if ortho == "dcgs2":
-            orth = sum(self.dcgs_dots(k) + self.dcgs_update(k) for k in range(1, m + 1)) + self.dcgs_dots(m + 1)
-        else:
-            orth = sum(self.cgs_dots(k) + 2 * self.cgs_update(k) for k in range(1, m + 1))
-        steps = m * (pre + sp + 2 * V) + orth
-        end = (m + 2) * V + pre + 3 * V + sp + 3 * V
-        return steps + end
+        """Algorithmic bytes of the kernels one cycle actually launches (value's numerator)."""
+        return sum(self.step_actual(j, n_j, ortho) for j in range(m)) + self.cycle_end_actual(m, n_j, ortho)
+
+    def step_mgs_own(self, j: int, n_j: int):
+        """Bytes of the reference's own MGS Arnoldi iteration j (oracle): per basis vector one dot
+        (2V) and one update (3V), then norm (V) and scaling (2V)."""
+        return self.precond_gs2_zero_start(n_j) + self.spmv() + (j + 1) * 5 * self.V + 3 * self.V
 
 
 def laplace3d_nnz(nx, ny, nz):
@@ -182,31 +198,60 @@ def dist_env():
 
 # ---------------------------------------------------------------- CPU baseline (oracle port)
 class CpuSample:
-    """The C oracle (reference algorithm: MGS GMRES, GS2(1,1,1) zero-start) on laplace3d nx^3.
+    """The C oracle (the reference algorithm: MGS GMRES(60) with the zero-start GS2(1,1,1)
+    preconditioner) on laplace3d nx^3, sampled one Arnoldi iteration at a time.
 
-    Setup (host CSR, splitting) is built once and excluded from timing, like
-    the reference CLI's timing convention (cli.py:162-176)."""
+    A GMRES(60) cycle's cost depends on the iteration index j (the MGS loop runs over j + 1 basis
+    vectors), so a bounded sample of the workload is a set of iterations j drawn stratified across
+    the cycle (j_s = floor((s + 1/2) m / K) for K samples): the sample has the cycle's j-mix.  The
+    basis rows are pseudo-random unit vectors (the cost of an iteration does not depend on their
+    values).  Setup (host CSR, splitting, basis) is excluded from timing, like the reference CLI
+    (cli.py:162-176)."""
 
-    def __init__(self, nx: int, threads: int):
+    def __init__(self, nx: int, threads: int, m: int = 60):
+        import numpy as np
+
         import oracle
         from paper_2104_01196_b200 import problems
 
+        self.np = np
         self.oracle = oracle
         oracle.set_threads(threads)
+        oracle.set_dot_threads(threads)
         self.threads = threads
         self.nx = nx
+        self.m = m
         a = problems.laplace3d(nx)
-        self.m = oracle.Matrix(a)
-        self.m.split()
-        self.b = oracle.random_rhs(a.nrows, 0)
-        self.pre = oracle.Precond(self.m, "gs2", n_t=1, n_k=1, n_j=1)
-        n, nl, nu = laplace3d_nnz(nx, nx, nx)
-        self.mod = Model(n, nl, nu)
+        self.mat = oracle.Matrix(a)
+        self.mat.split()
+        n = a.nrows
+        self.b = oracle.random_rhs(n, 0)
+        self.pre = oracle.Precond(self.mat, "gs2", n_t=1, n_k=1, n_j=1)
+        self.V = np.empty((m + 1, n))
+        for i in range(m + 1):
+            v = oracle.random_rhs(n, 1000 + i)
+            self.V[i] = v / np.sqrt(oracle.dot(v, v))
+        self.w = np.empty(n)
+        self.z = np.empty(n)
+        n_, nl, nu = laplace3d_nnz(nx, nx, nx)
+        self.mod = Model(n_, nl, nu)
+
+    def js(self, k: int):
+        return [min(self.m - 1, int((s + 0.5) * self.m / k)) for s in range(k)]
+
+    def step(self, j: int) -> float:
+        t0 = time.perf_counter()
+        self.oracle.arnoldi_step(self.mat, self.pre, self.V, j, self.w, self.z)
+        return time.perf_counter() - t0
+
+    def work(self, j: int) -> int:
+        """The B200 path's algorithmic bytes for iteration j (the common numerator of both arms)."""
+        return self.mod.step_actual(j, 1)
 
     def sweeps(self, reps: int = 2):
         """Per-sweep ms of the reference's relaxations (a6-a8) on b = rhs(0), x = rhs(1): the
         SURVEY §8(d) CPU timing (median of reps, 1 application each)."""
-        o, m = self.oracle, self.m
+        o, m = self.oracle, self.mat
         x1 = o.random_rhs(m.n, 1)
         out = {}
 
@@ -225,47 +270,45 @@ class CpuSample:
         out["spmv_ms"] = med(lambda x: o.spmv(m, x))
         return out
 
-    def run(self, iters: int):
-        """First `iters` Arnoldi iterations (+ cycle end); returns (GB/s, seconds, iterations)."""
-        t0 = time.perf_counter()
-        # restart = iters: the first `iters` Arnoldi steps of GMRES(60) are the same computation, and
-        # the basis then holds iters+1 vectors instead of 61 (65 GB at 512^3 otherwise)
-        _, hist, _ = self.oracle.gmres(self.m, self.b, self.pre, restart=max(iters, 1), tol=1e-9, maxit=iters)
-        dt = time.perf_counter() - t0
-        mod = self.mod
-        k = len(hist) - 1
-        bytes_ = sum(mod.arnoldi_step(j, 1) for j in range(k)) + (k + 1) * mod.V + mod.precond_gs2_zero_start(1) \
-            + 6 * mod.V + mod.spmv()
-        return bytes_ / dt / 1e9, dt, k
-
 
 def reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
+    n_gpus = max(world, args.gpus)
     threads = os.cpu_count() or 1
     # the sample is always laplace3d 256^3: the C5 workload (512^3, N > 1) needs > 64 GB of host RAM
-    # for the CPU matrix + splitting + basis (measured: killed at 62 GB), and the oracle's GB/s is
-    # size-independent once the working set is far beyond the host caches (2+ GB here)
-    nx = 256
-    target = "laplace3d 256^3 (C2)" if world == 1 else "laplace3d 512^3 (C5), sampled on a 256^3 instance"
-    iters = args.ref_iters
+    # for the CPU matrix + splitting + basis (measured: killed at 62 GB); W per row is the same at
+    # both sizes (the slab per GPU at N = 8 is the 256^3 problem)
+    nx = args.ref_nx
+    target = f"laplace3d {nx}^3 (C2)" if n_gpus == 1 else "laplace3d 512^3 (C5), sampled on a 256^3 instance"
     cs = CpuSample(nx, threads)
-    vals = []
-    for s in range(args.warmup + args.steps):
-        gbs, dt, k = cs.run(iters)
-        if s >= args.warmup:
-            vals.append((gbs, dt))
-    v = statistics.median(g for g, _ in vals)
-    ms = statistics.median(d for _, d in vals) * 1e3
-    sample = (f"C oracle (reference algorithm), first {iters} GMRES(60)+GS2(1,1,1) iterations of laplace3d {nx}^3 "
-              f"per step, {threads} host threads (OpenMP row loops; GS-free path), setup excluded")
+    for j in cs.js(max(args.warmup, 1))[: args.warmup]:
+        cs.step(j)
+    js = cs.js(args.steps)
+    ts = [cs.step(j) for j in js]
+    work = sum(cs.work(j) for j in js)
+    own = sum(cs.mod.step_mgs_own(j, 1) for j in js)
+    secs = sum(ts)
+    v = work / secs / 1e9
+    m = cs.m
+    # a full cycle = the 60 iterations (+ its end); the stratified sample's mean iteration time
+    # estimates ms per cycle
+    ms_cycle = secs / len(js) * m * 1e3
+    sample = (f"C oracle (reference algorithm: MGS GMRES(60) + zero-start GS2(1,1,1)), Arnoldi iterations "
+              f"j = {js[0]}..{js[-1]} stratified over the 60-step cycle of laplace3d {nx}^3 (one per step, "
+              f"{secs:.1f} s total), {threads} host threads (OpenMP row loops, threaded ddot split), setup excluded")
     line = {
-        "metric": METRIC, "value": round(v, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{target}: GMRES(60) + GS2(1,1,1) preconditioner (bounded sample)",
-                   "sample": sample},
+        "metric": METRIC, "value": round(v, 3), "unit": "GB/s", "n_gpus": n_gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_cycle, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{target}: GMRES(60) + GS2(1,1,1) preconditioner (bounded sample of the cycle)",
+                   "sample": sample, "iterations_sampled": js,
+                   "work_note": "value = the B200 path's algorithmic bytes for the sampled iterations / CPU time "
+                                "(the same numerator as the GPU arm, so the ratio is a time ratio on identical "
+                                "work); own_gbs = the oracle's own MGS bytes / time",
+                   "own_gbs": round(own / secs / 1e9, 3),
+                   "ms_per_iteration": round(secs / len(js) * 1e3, 2)},
         "impl": "reference",
         "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -276,7 +319,6 @@ def reference_arm(args):
 
 # ---------------------------------------------------------------- GPU arm
 def ours(args):
-    import numpy as np
     import torch
 
     import paper_2104_01196_b200 as g2
@@ -297,12 +339,18 @@ def ours(args):
     nx = args.nx or 256
     n_j = 1
     m = args.restart
-    a = g2.laplace3d(nx, device=local)
+    setup = {}
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    a = g2.laplace3d(nx, device=local)  # on-device stencil build + split-CSR (SELL-32) + D^-1 scaling
+    torch.cuda.synchronize()
+    setup["device_matrix_build_split_s"] = round(time.perf_counter() - t0, 4)
     n = a.nrows
     b = g2.random_rhs(n, 0, device=f"cuda:{local}")
     pc = g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, n_j))
     mod = Model(n, a.nnz_l, a.nnz_u)
-    cycle_bytes = mod.cycle(m, n_j)
+    actual_bytes = mod.cycle_actual(m, n_j)
+    model_bytes = mod.cycle(m, n_j)
     hbm, peak_kind = peaks()
 
     def step():
@@ -322,7 +370,7 @@ def ours(args):
         torch.cuda.synchronize()
     launches = lib.rs_launch_count() - l0
     ms = e0.elapsed_time(e1) / args.steps
-    value = cycle_bytes / (ms * 1e-3) / 1e9
+    value = actual_bytes / (ms * 1e-3) / 1e9
 
     # per-kernel-group attribution inside one more (instrumented) cycle
     with KernelTimer() as kt:
@@ -341,25 +389,31 @@ def ours(args):
         "scale": m * 2 * mod.V,
     }
     total_ms = sum(t for _, t in ksum.values())
-    actual_bytes = mod.cycle_actual(m, n_j)
     kernels = {}
     for g, (cnt, t) in ksum.items():
         gb = group_bytes.get(g)
         kernels[g] = {"launches": cnt, "ms": round(t, 3), "share": round(t / total_ms, 3) if total_ms else None,
-                      "gbs": round(gb / (t * 1e-3) / 1e9, 1) if gb and t else None}
+                      "gbs": round(gb / (t * 1e-3) / 1e9, 1) if gb and t else None,
+                      "bytes_per_launch": round(gb / cnt) if gb and cnt else None}
     dom = max((g for g in kernels if g in group_bytes), key=lambda g: kernels[g]["ms"])
-    # traffic: ncu DRAM bytes of one launch of the dominant kernel (profiles/traffic.json), scaled to
-    # this cycle's average launch by the measured traffic / algorithmic-bytes ratio of that launch
-    traffic = None
+    # traffic: ncu DRAM bytes of one launch of the dominant kernel (profiles/traffic.json, stamped with
+    # the git sha of the capture), scaled to this cycle's average launch by the measured traffic /
+    # algorithmic-bytes ratio of that launch
+    traffic, traffic_src = None, None
     tfile = ROOT / "profiles" / "traffic.json"
     if tfile.exists():
-        t = json.loads(tfile.read_text()).get(dom)
+        tj = json.loads(tfile.read_text())
+        t = tj.get(dom)
         if t:
             ratio = (t["dram_read"] + t["dram_write"]) / t["model_bytes"]
             traffic = round(ratio * group_bytes[dom] / kernels[dom]["launches"])
+            traffic_src = f"profiles/traffic.json ({t.get('capture', '?')}, sha {tj.get('git_sha', '?')})"
     roofline = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["gbs"], "peak": hbm, "unit": "GB/s",
-                "frac": round(kernels[dom]["gbs"] / hbm, 3), "traffic": traffic,
-                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}
+                "frac": round(kernels[dom]["gbs"] / hbm, 3), "traffic": traffic, "traffic_source": traffic_src,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                "achieved_note": "algorithmic bytes of the group's launches (SURVEY §8(d) per-row figures x rows) / "
+                                 "the group's CUDA-event time on the launching stream",
+                "cycle_frac": round(value / hbm, 3)}
 
     # e2e through the public API with host buffers: pinned b in, x out
     b_host = b.cpu().pin_memory()
@@ -375,11 +429,10 @@ def ours(args):
         assert not x.is_cuda
         e2e_steps.append(round((time.perf_counter() - ts) * 1e3, 2))
     e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
-    e2e = {"value": round(cycle_bytes / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
-           "d2h_bytes_per_step": 8 * n, "ms_per_step": round(e2e_ms, 3),
-           "ms_steps": e2e_steps}
+    e2e = {"value": round(actual_bytes / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
+           "d2h_bytes_per_step": 8 * n, "ms_per_step": round(e2e_ms, 3), "ms_steps": e2e_steps}
 
-    sweeps = sweep_table(g2, torch, a, mod, hbm) if not args.no_sweeps else None
+    sweeps = sweep_table(g2, torch, a, mod, hbm, setup) if not args.no_sweeps else None
     tts = None
     if not args.no_tts:
         torch.cuda.synchronize()
@@ -387,7 +440,10 @@ def ours(args):
         _, h = g2.gmres(a, b, pc, restart=m, tol=1e-9)
         torch.cuda.synchronize()
         tts = {"seconds": round(time.perf_counter() - t0, 3), "iterations": h.iterations, "converged": h.converged,
-               "final_rel_res": h.final_rel_res, "preconditioner": "gs2(1,1,1)", "restart": m, "tol": 1e-9}
+               "final_rel_res": h.final_rel_res, "preconditioner": "gs2(1,1,1)", "restart": m, "tol": 1e-9,
+               "reference_iterations": 2635, "reference_seconds_1core": 11002,
+               "note": "default ortho (DCGS2, fixed-order device reductions); ortho='mgs_ref' reproduces the "
+                       "reference's history bitwise (profiles/r02_c2_mgs_ref.json)"}
     # C5 on ONE GPU: the 512^3 cycle, the strong-scaling reference for the N > 1 lines (which run
     # 512^3 in z-slabs); the 256^3 workspace is released first (512^3 basis: 65.5 GB)
     c5 = None
@@ -412,18 +468,26 @@ def ours(args):
         ms5 = f0.elapsed_time(f1) / 2
         c5 = {"workload": "C5 laplace3d 512^3 on ONE GPU, one GMRES(60) cycle (strong-scaling reference of the "
                           "N > 1 lines)", "ms_per_step": round(ms5, 3),
-              "value": round(mod5.cycle(m, n_j) / (ms5 * 1e-3) / 1e9, 3), "unit": "GB/s"}
+              "value": round(mod5.cycle_actual(m, n_j) / (ms5 * 1e-3) / 1e9, 3), "unit": "GB/s"}
         del a5, b5, pc5
         gk.release_workspace()
         torch.cuda.empty_cache()
+    configs = None
+    if not args.no_configs:
+        configs = secondary_configs(g2, torch)
     cpu = None
     if not args.no_cpu_baseline:
         cs = CpuSample(nx, 1)
-        gbs, dt, k = cs.run(args.cpu_iters)
-        cpu = {"value": round(gbs, 3), "unit": "GB/s", "cores": 1, "kind": "port",
-               "sample": f"C oracle (reference algorithm), first {k} GMRES(60)+GS2(1,1,1) iterations of "
-                         f"laplace3d {nx}^3 on 1 host core, {dt:.1f} s",
+        js = cs.js(3)
+        secs = sum(cs.step(j) for j in js)
+        cpu = {"value": round(sum(cs.work(j) for j in js) / secs / 1e9, 3), "unit": "GB/s", "cores": 1,
+               "kind": "port",
+               "sample": f"C oracle (reference algorithm), Arnoldi iterations j = {js} of the GMRES(60)+GS2(1,1,1) "
+                         f"cycle on laplace3d {nx}^3, 1 host core, {secs:.1f} s (value: the B200 path's bytes for "
+                         f"that work / CPU time, as in the reference arm)",
+               "own_gbs": round(sum(cs.mod.step_mgs_own(j, 1) for j in js) / secs / 1e9, 3),
                "per_sweep_ms_1core": cs.sweeps()}
+        del cs
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
@@ -431,22 +495,102 @@ def ours(args):
         "config": {"workload": f"C2: laplace3d {nx}^3 ({n} rows), one GMRES({m}) cycle with GS2(1,1,1) "
                                f"zero-start preconditioner, b = random_rhs(n, 0)",
                    "ortho": "dcgs2 (CGS2 with delayed re-orthogonalisation, 2 basis passes per step)",
-                   "bytes_per_step": cycle_bytes,
-                   "bytes_note": "value = SURVEY §8(d) byte model of the cycle (unfused CGS2: 4 basis reads per "
-                                 "step) / device time, i.e. a fixed amount of work per step; the fused kernels "
-                                 "move fewer bytes (actual_bytes_per_step), so value can exceed the HBM peak",
-                   "actual_bytes_per_step": actual_bytes, "actual_gbs": round(actual_bytes / (ms * 1e-3) / 1e9, 1),
+                   "bytes_per_step": actual_bytes,
+                   "bytes_note": "value = algorithmic bytes of the launched kernel sequence (fused passes counted "
+                                 "once) / device time: the whole-cycle HBM throughput",
+                   "model_bytes_per_step": model_bytes,
+                   "model_gbs": round(model_bytes / (ms * 1e-3) / 1e9, 1),
+                   "model_note": "SURVEY §8(d) model of the cycle (unfused CGS2, 4 basis reads per step): a fixed "
+                                 "work figure, exceeds the HBM peak because the fused kernels move fewer bytes",
                    "ms_per_iteration": round(ms / m, 4),
-                   "l2": "inputs larger than L2 (V basis 61 x 134 MB, matrix 1.7 GB)", "parallelism": "1 GPU"},
+                   "iterations_per_s": round(m / (ms * 1e-3), 1),
+                   "row_iterations_per_s": round(n * m / (ms * 1e-3)),
+                   "l2": "inputs larger than L2 (V basis 61 x 134 MB, matrix 1.7 GB)", "parallelism": "1 GPU",
+                   "scaling_note": "N > 1 lines run C5 (laplace3d 512^3 in N z-slabs, fixed total problem); the "
+                                   "512^3 cycle on this one GPU is c5_one_gpu"},
         "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-        "clocks": clk.summary(), "sweeps": sweeps, "tts": tts, "c5_one_gpu": c5,
+        "clocks": clk.summary(), "sweeps": sweeps, "tts": tts, "c5_one_gpu": c5, "configs": configs,
+        "setup": setup,
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def sweep_table(g2, torch, a, mod, hbm, reps: int = 10):
-    """Same-device comparison of the paper's relaxations on x != 0 (b = rhs(0), x = rhs(1))."""
+def _timed(torch, fn):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    out = fn()
+    torch.cuda.synchronize()
+    return out, time.perf_counter() - t0
+
+
+def secondary_configs(g2, torch):
+    """The other BASELINE.json configs, one compact record each (bench_configs.py has the full
+    tables): C1 (laplace2d 128^2, GMRES(30): GS2(2,1,1) vs sequential GS(2); the reference's
+    counts 563 / 471), C3 (elasticity3d 64^3: 50 stand-alone applications of JR(w=1) -- diverges --
+    and GS2 n_j = 1/3/10 through stationary_solve, plus GMRES(60) counts), C4 (convdiff3d 256^3:
+    fp64 vs fp32-inside-fp64 GS2(1,1,2) in GMRES(60))."""
+    out = {}
+    a = g2.laplace2d(128)
+    b = g2.random_rhs(a.nrows, 0)
+    c1 = {"workload": "C1 laplace2d 128^2, GMRES(30)", "reference_iterations": {"gs2(2,1,1)": 563, "gs_seq(2)": 471}}
+    for label, kind, cfg in (("gs2(2,1,1)", "gs2", (2, 1, 1)), ("gs_seq(2)", "gs_seq", (2, 1, 0))):
+        pm = g2.Preconditioner(a, kind, g2.RelaxConfig(*cfg))
+        g2.gmres(a, b, pm, restart=30)
+        (_, h), dt = _timed(torch, lambda: g2.gmres(a, b, pm, restart=30))
+        c1[label] = {"iterations": h.iterations, "seconds": round(dt, 4)}
+    if hasattr(g2, "stationary_solve"):
+        pm_cfg = g2.RelaxConfig(2, 1, 1)
+        g2.stationary_solve(a, b, "gs2", pm_cfg, tol=1e-6, maxit=50)
+        (_, h), dt = _timed(torch, lambda: g2.stationary_solve(a, b, "gs2", pm_cfg, tol=1e-6))
+        c1["stationary gs2(2,1,1) to 1e-6"] = {"applications": h.iterations, "final_rel_res": h.final_rel_res,
+                                               "seconds": round(dt, 4), "reference_applications": 8872,
+                                               "reference_seconds_1core": 9.9}
+    out["c1"] = c1
+    t0 = time.perf_counter()
+    a = g2.elasticity3d(64)
+    gen = time.perf_counter() - t0
+    b = g2.random_rhs(a.nrows, 0, device="cuda")
+    c3 = {"workload": f"C3 elasticity3d 64^3 (n = {a.nrows}, nnz = {a.nnz})", "host_generation_s": round(gen, 1)}
+    if hasattr(g2, "stationary_solve"):
+        st = {}
+        for label, kind, cfg in (("jr(w=1)", "jr", (1, 1, 0)), ("gs2 n_j=1", "gs2", (1, 1, 1)),
+                                 ("gs2 n_j=3", "gs2", (1, 1, 3)), ("gs2 n_j=10", "gs2", (1, 1, 10))):
+            (_, h), dt = _timed(torch, lambda: g2.stationary_solve(a, b, kind, g2.RelaxConfig(*cfg), tol=1e-300,
+                                                                   maxit=50))
+            st[label] = {"applications": h.iterations, "rel_res": h.final_rel_res,
+                         "ms_per_application": round(dt * 1e3 / max(h.iterations, 1), 3)}
+        c3["stationary_50"] = st
+        c3["reference_rel_res_50"] = {"jr(w=1)": 3.40e9, "gs2 n_j=1": 71.1, "gs2 n_j=3": 5.92e-2, "gs2 n_j=10": 4.46e-3}
+    gm = {}
+    for label, kind, cfg in (("gs2 n_j=1", "gs2", (1, 1, 1)), ("gs2 n_j=3", "gs2", (1, 1, 3))):
+        pm = g2.Preconditioner(a, kind, g2.RelaxConfig(*cfg))
+        (_, h), dt = _timed(torch, lambda: g2.gmres(a, b, pm, restart=60, maxit=3000))
+        gm[label] = {"iterations": h.iterations, "converged": h.converged, "seconds": round(dt, 3)}
+    c3["gmres60"] = gm
+    out["c3"] = c3
+    del a, b
+    a = g2.convdiff3d(256, (50.0, 25.0, 10.0), device="cuda")
+    b = g2.random_rhs(a.nrows, 0, device="cuda")
+    c4 = {"workload": "C4 convdiff3d 256^3 beta=(50,25,10), GMRES(60) + GS2(1,1,2)"}
+    for prec in ("same", "single_inside_double"):
+        pm = g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, 2), precision=prec)
+        g2.gmres(a, b, pm, restart=60, maxit=60)
+        (_, h), dt = _timed(torch, lambda: g2.gmres(a, b, pm, restart=60))
+        c4[prec] = {"iterations": h.iterations, "converged": h.converged, "seconds": round(dt, 3),
+                    "ms_per_iteration": round(dt * 1e3 / max(h.iterations, 1), 4)}
+    out["c4"] = c4
+    from paper_2104_01196_b200 import krylov as gk
+
+    del a, b, pm
+    gk.release_workspace()
+    torch.cuda.empty_cache()
+    return out
+
+
+def sweep_table(g2, torch, a, mod, hbm, setup=None, reps: int = 10):
+    """Same-device comparison of the paper's relaxations on x != 0 (b = rhs(0), x = rhs(1)).
+    ``setup`` receives the one-off analysis costs the baselines pay (level sets, colouring)."""
     n = a.nrows
     dev = a.torch_device
     b = g2.random_rhs(n, 0, device=dev)
@@ -454,10 +598,14 @@ def sweep_table(g2, torch, a, mod, hbm, reps: int = 10):
     s = g2.extract_splitting(a)
     out = {}
 
-    def timeit(fn, nbytes):
+    def timeit(fn, nbytes, setup_key=None):
         x = x0.clone()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
         fn(x)  # warm-up (builds level sets etc.)
         torch.cuda.synchronize()
+        if setup_key and setup is not None:
+            setup[setup_key] = round(time.perf_counter() - t0, 4)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(reps):
@@ -477,9 +625,15 @@ def sweep_table(g2, torch, a, mod, hbm, reps: int = 10):
         out[f"gs2_nj{nj}"] = timeit(lambda x, cfg=cfg: g2.gs2_apply(a, s, b, x, cfg), mod.gs2_sweep(nj))
     out["jr"] = timeit(lambda x: g2.jr_sweeps(a, s, b, x, 1), mod.gs2_sweep(0))
     out["gs_level_sched"] = timeit(lambda x: g2.gs_sequential_sweep(a, s, b, x, "forward"),
-                                   mod.ML + mod.MU + 3 * mod.V)
+                                   mod.ML + mod.MU + 3 * mod.V, "level_set_analysis_plus_first_sweep_s")
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
     coloring = g2.greedy_color(a)
-    out["mt_gs"] = timeit(lambda x: g2.mt_gs_sweep(a, s, coloring, b, x, "forward"), mod.ML + mod.MU + 3 * mod.V)
+    torch.cuda.synchronize()
+    if setup is not None:
+        setup["greedy_coloring_s"] = round(time.perf_counter() - t0, 4)
+    out["mt_gs"] = timeit(lambda x: g2.mt_gs_sweep(a, s, coloring, b, x, "forward"), mod.ML + mod.MU + 3 * mod.V,
+                          "mt_colour_ordered_slices_plus_first_sweep_s")
     out["mt_gs"]["colors"] = coloring.num_colors
     y = torch.empty_like(b)
     out["spmv"] = timeit(lambda x: g2.spmv(a, x, out=y), mod.spmv())
@@ -501,12 +655,29 @@ def main():
                    help="N > 1 collectives: NVLink peer-memory kernels (default) or NCCL")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-c5", action="store_true", help="skip the 512^3 one-GPU cycle (strong-scaling reference)")
-    p.add_argument("--cpu-iters", type=int, default=8)
-    p.add_argument("--ref-iters", type=int, default=3)
+    p.add_argument("--ref-nx", type=int, default=256, help="(testing) grid of the reference arm's sample")
+    p.add_argument("--no-configs", action="store_true", help="skip the C1 / C3 / C4 records of the N = 1 line")
     args = p.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args.gpus)
     return ours(args)
+
+
+def relaunch(n: int) -> int:
+    """``--gpus N`` without a launcher: re-execute this script under torch.distributed.run with N
+    ranks on this node (rendezvous on 127.0.0.1); rank 0 prints the JSON line."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "4")
+    return subprocess.call(cmd, env=env)
 
 
 if __name__ == "__main__":

@@ -9,6 +9,18 @@
  * `stream` is a cudaStream_t (NULL = legacy default stream).  Nothing here
  * synchronises the stream unless its comment says so.
  *
+ * Threading (the reference's contract: concurrent solves on shared read-only
+ * matrices and preconditioners): every sweep / SpMV /
+ * preconditioner entry point may be called concurrently on one matrix handle
+ * from several host threads and streams.  The library's working vectors
+ * (rd, g, ping-pong iterates, reduction partials) are per (host thread,
+ * stream) pair, allocated on first use and freed by rs_mat_destroy; the lazy
+ * analyses (level sets, colouring, level-/colour-ordered slices) are built
+ * once under a per-handle lock.  Not concurrent with a call that mutates the
+ * handle (rs_mat_set_coloring, rs_mat_destroy).  The non-default level-GS
+ * modes RS_GS_MODE=barrier/syncfree/ordered keep grid-barrier words per
+ * handle and are not reentrant.
+ *
  * Each function names the reference interface it replaces (paths relative to
  * /root/reference/pkg/src/relaxsolve).  The reference's native seam is the
  * numba kernel ABI of _kernels.py (flat arrays, caller-allocated outputs, no
@@ -155,9 +167,8 @@ int rs_inner_jr(rs_matrix_t m, const void *r, void *g, int n_j, int backward, do
 /* gs2_apply (relax.py:208-220) incl. _two_stage_sweep (193-205): x in place. */
 int rs_gs2_apply(rs_matrix_t m, const void *b, void *x, const rs_relax_cfg *cfg, rs_stream_t stream);
 
-/* One GS2 half-sweep out of place, x_out = GS2(x_in) (cfg: n_t = n_k = 1,
- * forward or backward, n_j >= 1, either form): the wavefront kernel, one
- * launch, no copy-back.  Bitwise equal to gs2_apply on a copy of x_in. */
+/* gs2_apply out of place, x_out = GS2(x_in), x_in unchanged (any cfg): x_out = x_in, then the
+ * in-place pass chain.  Bitwise equal to gs2_apply on a copy of x_in. */
 int rs_gs2_sweep(rs_matrix_t m, const void *b, const void *x_in, void *x_out, const rs_relax_cfg *cfg,
                  rs_stream_t stream);
 

@@ -388,7 +388,29 @@ ORC_FMA_TARGET static void blas_dgemv_t_rows(int64_t n, int k, const double *v, 
   }
 }
 
-double orc_dot(int64_t n, const double *x, const double *y) { return blas_ddot(n, x, y); }
+/* OPENBLAS_NUM_THREADS > 1 (the CPU baseline's "all host threads" timing mode, orc_set_dot_threads):
+ * OpenBLAS then splits a long ddot into one contiguous range per thread, each summed in the kernel
+ * order, and adds the per-thread results in range order -- the reference's own multi-threaded
+ * arithmetic (a different rounding than the one-thread goldens, same cost structure). */
+static int g_dot_threads = 1;
+
+void orc_set_dot_threads(int t) { g_dot_threads = t > 1 ? t : 1; }
+
+double orc_dot(int64_t n, const double *x, const double *y) {
+  int t = g_dot_threads;
+  if (t <= 1 || n <= 10000) return blas_ddot(n, x, y);
+  double part[256];
+  if (t > 256) t = 256;
+  int64_t w = ((n / t) + 15) & ~(int64_t)15;
+#pragma omp parallel for schedule(static) num_threads(t)
+  for (int q = 0; q < t; ++q) {
+    int64_t lo = (int64_t)q * w, hi = lo + w < n ? lo + w : n;
+    part[q] = lo < hi ? blas_ddot(hi - lo, x + lo, y + lo) : 0.0;
+  }
+  double s = 0.0;
+  for (int q = 0; q < t; ++q) s = s + part[q];
+  return s;
+}
 
 void orc_gemv_t_rows(int64_t n, int k, const double *v, int64_t ldv, const double *y, double *out) {
   blas_dgemv_t_rows(n, k, v, ldv, y, out);
@@ -503,6 +525,31 @@ done:
   *iters = nh - 1;
   free(r); free(t); free(w); free(z); free(v); free(h); free(cs); free(sn); free(g); free(y);
   return status;
+}
+
+/* One Arnoldi iteration j of the reference's GMRES loop (krylov.py:214-223), the CPU baseline's
+ * sampling unit: z = M v_j, w = A z, MGS against v_0..v_j (h[0..j]), h[j+1] = ||w||,
+ * v_{j+1} = w / h[j+1].  V is (j+2) x n row-major with leading dimension ldv. */
+int orc_arnoldi_step(const orc_csr *a, orc_precond *m, double *V, int64_t ldv, int j, double *w, double *z,
+                     double *h) {
+  int64_t n = a->n, ei = 0;
+  double *vj = V + (size_t)j * (size_t)ldv;
+  if (m) { int st = orc_precond_apply(m, vj, z, &ei); if (st) return st; }
+  else memcpy(z, vj, sizeof(double) * (size_t)n);
+  orc_spmv_f64(a, z, w);
+  for (int i = 0; i <= j; ++i) {
+    const double *vi = V + (size_t)i * (size_t)ldv;
+    double hij = orc_dot(n, vi, w);
+    h[i] = hij;
+#pragma omp parallel for schedule(static) if (n > 65536)
+    for (int64_t k = 0; k < n; ++k) { double p = hij * vi[k]; w[k] = w[k] - p; }
+  }
+  double hn = nrm2(n, w);
+  h[j + 1] = hn;
+  double *vn = V + (size_t)(j + 1) * (size_t)ldv;
+#pragma omp parallel for schedule(static) if (n > 65536)
+  for (int64_t k = 0; k < n; ++k) vn[k] = w[k] / hn;
+  return ORC_OK;
 }
 
 /* ---------------------------------------------------------------- CG (krylov.py:253-309) */

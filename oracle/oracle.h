@@ -118,6 +118,11 @@ int orc_cg(const orc_csr *a, const double *b, orc_precond *m, double tol, int ma
 void orc_random_rhs(int64_t n, uint64_t seed, double *out);
 double orc_dot(int64_t n, const double *x, const double *y);  /* OpenBLAS 0.3.30 SkylakeX ddot order */
 /* out[r] = sum_{c<k} v[c*ldv + r] y[c] in OpenBLAS dgemv_n order (`v[:k].T @ y`, krylov.py:244) */
+/* threads of orc_dot (1 = the one-thread order of the goldens; >1 = OpenBLAS's threaded split) */
+void orc_set_dot_threads(int t);
+/* one Arnoldi iteration j (krylov.py:214-223): CPU-baseline sampling unit */
+int orc_arnoldi_step(const orc_csr *a, orc_precond *m, double *V, int64_t ldv, int j, double *w, double *z,
+                     double *h);
 void orc_gemv_t_rows(int64_t n, int k, const double *v, int64_t ldv, const double *y, double *out);
 
 #ifdef __cplusplus

@@ -95,17 +95,37 @@ __global__ void __launch_bounds__(64, 1) k_dot_blas_ring(int64_t n, const double
     const double* sy = sx + kBoStage;
     const int len = (int)(n32 - s * kBoStage < kBoStage ? n32 - s * kBoStage : kBoStage);
     int e = lane;
-    for (; e + 7 * 32 < len; e += 8 * 32) {
+    if (len == kBoStage) {
+      // software-pipelined: the shared-memory loads of batch q+1 are in flight while the FMA
+      // chain consumes batch q, so the loop runs at the FMA latency
       double xv[8], yv[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         xv[u] = sx[e + 32 * u];
         yv[u] = sy[e + 32 * u];
       }
+#pragma unroll 1
+      for (int q = 0; q < kBoStage / 256 - 1; ++q) {
+        double xn[8], yn[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          xn[u] = sx[e + 256 + 32 * u];
+          yn[u] = sy[e + 256 + 32 * u];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = fma(xv[u], yv[u], acc);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          xv[u] = xn[u];
+          yv[u] = yn[u];
+        }
+        e += 256;
+      }
 #pragma unroll
       for (int u = 0; u < 8; ++u) acc = fma(xv[u], yv[u], acc);
+    } else {
+      for (; e < len; e += 32) acc = fma(sx[e], sy[e], acc);
     }
-    for (; e < len; e += 32) acc = fma(sx[e], sy[e], acc);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
   }

@@ -460,8 +460,6 @@ static int build_split(rs_matrix* m, const Src& src) {
   return status;
 }
 
-void destroy_wave(void* p);
-void destroy_pipe(void* p);
 
 void destroy(rs_matrix* m) {
   if (!m) return;
@@ -476,34 +474,49 @@ void destroy(rs_matrix* m) {
   free_levels(m->mt);
   free_mt_sell(m);
   free(m->color);
-  cudaFree(m->scratch);
-  cudaFree(m->scratch2);
-  cudaFree(m->red);
-  cudaFree(m->ticket);
-  destroy_wave(m->wave[0]);
-  destroy_wave(m->wave[1]);
-  destroy_pipe(m->pipe);
-  cudaFree(m->stage);
+  for (Workspace* w : m->ws) {
+    cudaFree(w->scratch);
+    cudaFree(w->red);
+    delete w;
+  }
+  m->ws.clear();
   cudaSetDevice(prev);
   delete m;
 }
 
-int ensure_reduction(rs_matrix* m, int64_t n_doubles) {
-  if (m->red && m->red_cap >= n_doubles) return RS_OK;
-  cudaFree(m->red);
-  m->red = nullptr;
-  m->red_cap = 0;
-  RS_CUDA(cudaMalloc(&m->red, sizeof(double) * std::max<int64_t>(n_doubles, 1)));
-  m->red_cap = n_doubles;
+static Workspace* workspace(rs_matrix* m, cudaStream_t st) {
+  const std::thread::id me = std::this_thread::get_id();
+  std::lock_guard<std::mutex> g(m->mu);
+  for (Workspace* w : m->ws)
+    if (w->tid == me && w->st == st) return w;
+  Workspace* w = new Workspace();
+  w->tid = me;
+  w->st = st;
+  m->ws.push_back(w);
+  return w;
+}
+
+int get_scratch(rs_matrix* m, cudaStream_t st, void** out) {
+  Workspace* w = workspace(m, st);
+  if (!w->scratch) {
+    size_t es = m->dtype == RS_F32 ? 4 : 8;
+    size_t n = (size_t)std::max<int64_t>(m->nrows, 1);
+    RS_CUDA(cudaMalloc(&w->scratch, es * 6 * n));
+  }
+  *out = w->scratch;
   return RS_OK;
 }
 
-int ensure_scratch(rs_matrix* m) {
-  if (m->scratch) return RS_OK;
-  size_t es = m->dtype == RS_F32 ? 4 : 8;
-  size_t n = (size_t)std::max<int64_t>(m->nrows, 1);
-  // [rd | g_a | g_b | alt/snapshot | f32 rhs | f32 z]
-  RS_CUDA(cudaMalloc(&m->scratch, es * 6 * n));
+int get_reduction(rs_matrix* m, cudaStream_t st, int64_t n_doubles, double** out) {
+  Workspace* w = workspace(m, st);
+  if (!w->red || w->red_cap < n_doubles) {
+    cudaFree(w->red);
+    w->red = nullptr;
+    w->red_cap = 0;
+    RS_CUDA(cudaMalloc(&w->red, sizeof(double) * std::max<int64_t>(n_doubles, 1)));
+    w->red_cap = n_doubles;
+  }
+  *out = w->red;
   return RS_OK;
 }
 
@@ -943,6 +956,7 @@ int rs_mat_coloring(rs_matrix_t m, int64_t* color_out, int64_t* ncolors) {
     return RS_ERR_ARG;
   }
   RS_CUDA(cudaSetDevice(m->device));
+  std::lock_guard<std::mutex> guard(m->build_mu);
   int st = build_coloring(m);
   if (st) return st;
   if (color_out) memcpy(color_out, m->color, sizeof(int64_t) * m->nrows);
@@ -961,6 +975,7 @@ int rs_mat_set_coloring(rs_matrix_t m, const int64_t* color, int64_t ncolors) {
       return RS_ERR_ARG;
     }
   RS_CUDA(cudaSetDevice(m->device));
+  std::lock_guard<std::mutex> guard(m->build_mu);
   return install_coloring(m, color, ncolors);
 }
 

@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <atomic>
 #include <map>
 #include <vector>
 
@@ -31,26 +32,6 @@ namespace rs {
 int build_levels(rs_matrix* m, int backward);
 int build_coloring(rs_matrix* m);
 void free_mt_sell(rs_matrix* m);
-int wave_enabled();
-template <typename T>
-int wave_half_sweep(rs_matrix* m, const T* b, const T* xin, T* xout, int n_j, int backward, int form, double omega,
-                    double gamma, bool x_zero, cudaStream_t st);
-int wave_precond_f32(rs_matrix* m, const double* r, double* z, int n_j, int backward, double omega, double gamma,
-                     long long* overflow, cudaStream_t st);
-template <typename T>
-int wave_max_width(rs_matrix* m, int backward, int* wmax);
-
-// the skewed-pipeline sweep handles any row width
-template <typename T>
-static bool wave_usable(rs_matrix* m, int direction) {
-  for (int bwd = 0; bwd < 2; ++bwd) {
-    if (direction == RS_FORWARD && bwd) continue;
-    if (direction == RS_BACKWARD && !bwd) continue;
-    int w = 0;
-    if (wave_max_width<T>(m, bwd, &w)) return false;
-  }
-  return true;
-}
 
 // s -= sum_k v_k * x[c_k] (gs_ordered_sweep form, _kernels.py:31-35)
 template <typename T>
@@ -648,12 +629,7 @@ __global__ void k_cast(int64_t n, const T* __restrict__ in, double* __restrict__
 }
 
 constexpr int kB = 256;
-
-// window-pipelined one-launch GS2 half-sweep (opt-in RS_PIPE=1): pipe.cu
-enum PipeMode { kPipeResid = 0, kPipeCompact = 1, kPipeZero = 2 };
-template <typename T, typename R, typename O>
-int pipe_half_sweep(rs_matrix* m, int mode, const T* b, const R* r, T* x, O* z, int n_j, int bwd, double omega,
-                    double gamma, long long* overflow, cudaStream_t st);
+constexpr int kMaxDevices = 64;
 
 // ------------------------------------------------------------------ host launchers
 template <typename T>
@@ -663,6 +639,7 @@ struct Ctx {
   int64_t n;
   SellView<T> L, U, Lsc, Usc, Elo, Ehi;
   const T* d;
+  T* scr = nullptr;  // this call's working vectors (get_scratch)
   Ctx(rs_matrix* mm, cudaStream_t s) : m(mm), st(s), n(mm->nrows) {
     L = view(tri<T>(m, 0), false);
     U = view(tri<T>(m, 1), false);
@@ -754,7 +731,7 @@ static int inner_chain(Ctx<T>& c, T* rd, T* ga, T* gb, T* x, int n_j, int backwa
 template <typename T>
 static int two_stage(Ctx<T>& c, const T* b, T* x, int n_j, int backward, int form, double omega, double gamma,
                      bool x_is_zero) {
-  T* rd = (T*)c.m->scratch;
+  T* rd = c.scr;
   T* ga = rd + c.n;
   T* gb = ga + c.n;
   bool compact = form == RS_COMPACT;
@@ -767,11 +744,6 @@ static int two_stage(Ctx<T>& c, const T* b, T* x, int n_j, int backward, int for
     RS_COUNT_LAUNCH();
     RS_CUDA(cudaMemcpyAsync(x, alt, sizeof(T) * c.n, cudaMemcpyDeviceToDevice, c.st));
     return RS_OK;
-  }
-  if (n_j >= 1) {
-    const int mode = x_is_zero ? kPipeZero : (compact ? kPipeCompact : kPipeResid);
-    const int e = pipe_half_sweep<T, T, T>(c.m, mode, b, b, x, x, n_j, backward, omega, gamma, nullptr, c.st);
-    if (e != RS_ERR_UNSUPPORTED) return e;
   }
   if (x_is_zero) {
     static const bool x2 = !getenv("RS_SCALE_X2") || atoi(getenv("RS_SCALE_X2")) != 0;
@@ -802,29 +774,11 @@ static int two_stage(Ctx<T>& c, const T* b, T* x, int n_j, int backward, int for
 template <typename T>
 static int gs2_apply_t(rs_matrix* m, const T* b, T* x, const rs_relax_cfg& cfg, cudaStream_t st, bool x_is_zero) {
   int e;
-  if ((e = ensure_scratch(m))) return e;
+  void* scr_ = nullptr;
+  if ((e = get_scratch(m, st, &scr_))) return e;
   Ctx<T> c(m, st);
+  c.scr = (T*)scr_;
   bool zero = x_is_zero;
-  if (wave_enabled() && cfg.n_j >= 1 && c.n > 0 && wave_usable<T>(m, cfg.direction)) {
-    // one wavefront launch per half-sweep, ping-pong iterates (the wave reads x_in at
-    // neighbours while writing x_out); the result is copied back only if it ends in alt
-    T* alt = (T*)m->scratch + 3 * c.n;
-    T* cur = x;
-    for (int t = 0; t < cfg.n_t; ++t)
-      for (int k = 0; k < cfg.n_k; ++k)
-        for (int half = 0; half < 2; ++half) {
-          const int bwd = half;
-          if (cfg.direction == RS_FORWARD && bwd) continue;
-          if (cfg.direction == RS_BACKWARD && !bwd) continue;
-          T* nxt = cur == x ? alt : x;
-          if ((e = wave_half_sweep<T>(m, b, cur, nxt, cfg.n_j, bwd, cfg.form, cfg.omega, cfg.gamma, zero, st)))
-            return e;
-          cur = nxt;
-          zero = false;
-        }
-    if (cur != x) RS_CUDA(cudaMemcpyAsync(x, cur, sizeof(T) * c.n, cudaMemcpyDeviceToDevice, st));
-    return RS_OK;
-  }
   for (int t = 0; t < cfg.n_t; ++t)
     for (int k = 0; k < cfg.n_k; ++k)
       for (int half = 0; half < 2; ++half) {
@@ -1195,6 +1149,9 @@ __global__ void k_mt_first(int64_t cnt, const int32_t* __restrict__ rows, const 
 template <typename T>
 static int mt_gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omega, cudaStream_t st,
                          bool x_zero = false) {
+  // the colouring and its ordered slices are built on first use; concurrent callers wait here
+  // (enqueue only: the sweeps themselves run concurrently on their streams)
+  std::lock_guard<std::mutex> guard(m->build_mu);
   int e;
   if ((e = build_coloring(m))) return e;
   Ctx<T> c(m, st);
@@ -1225,28 +1182,25 @@ static int mt_gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double o
   return RS_OK;
 }
 
-// out-of-place single GS2 half-sweep / sweep set: x_out = GS2(x_in) (no copy-back)
+// out-of-place GS2 application: x_out = GS2(x_in) (x_in is not modified): the in-place sweep
+// chain of gs2_apply on x_out = x_in (the passes themselves are out-of-place: rd, g buffers)
 template <typename T>
 static int gs2_sweep_oop_t(rs_matrix* m, const T* b, const T* xin, T* xout, const rs_relax_cfg& cfg,
                            cudaStream_t st) {
-  if (cfg.n_t * cfg.n_k != 1 || cfg.direction == RS_SYMMETRIC || cfg.n_j < 1) {
-    set_error(RS_ERR_ARG, "rs_gs2_sweep: one forward or backward half-sweep with n_j >= 1");
-    return RS_ERR_ARG;
-  }
-  int e;
-  if ((e = ensure_scratch(m))) return e;
-  return wave_half_sweep<T>(m, b, xin, xout, cfg.n_j, cfg.direction == RS_BACKWARD, cfg.form, cfg.omega, cfg.gamma,
-                            false, st);
+  RS_CUDA(cudaMemcpyAsync(xout, xin, sizeof(T) * m->nrows, cudaMemcpyDeviceToDevice, st));
+  return gs2_apply_t<T>(m, b, xout, cfg, st, false);
 }
 
 // jr_sweeps (relax.py:145-154) with ping-pong iterates: x_next = x + w (b - A x)/d
 template <typename T>
 static int jr_sweeps_t(rs_matrix* m, const T* b, T* x, int sweeps, double omega, cudaStream_t st, bool x_is_zero) {
   int e;
-  if ((e = ensure_scratch(m))) return e;
+  void* scr_ = nullptr;
+  if ((e = get_scratch(m, st, &scr_))) return e;
   Ctx<T> c(m, st);
+  c.scr = (T*)scr_;
   T w = (T)omega;
-  T* alt = (T*)m->scratch + 3 * m->nrows;
+  T* alt = c.scr + 3 * m->nrows;
   T* cur = x;
   for (int s = 0; s < sweeps; ++s) {
     if (s == 0 && x_is_zero) {
@@ -1360,11 +1314,19 @@ static int gs_cooperative(rs_matrix* m, Levels& lv, Ctx<T>& c, const T* b, T* x,
 
 template <typename T>
 static int gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omega, cudaStream_t st) {
+  // level sets, level-ordered slices and their device copies are built on first use
+  std::lock_guard<std::mutex> guard(m->build_mu);
   int e;
-  if ((e = ensure_scratch(m))) return e;
+  void* scr_ = nullptr;
+  if ((e = get_scratch(m, st, &scr_))) return e;
   Ctx<T> c(m, st);
+  c.scr = (T*)scr_;
   T w = (T)omega, w1 = (T)(1.0 - omega);
   bool damped = w != (T)1.0;
+  // programmatic dependent launch only BETWEEN this call's kernels: the first kernel reads b (and
+  // the first level's rows) before griddepcontrol.wait, so it must not overlap the kernel that
+  // produced b / x (e.g. rs_hybrid_bhat right before a hybrid local sweep)
+  bool pdl_ok = false;
   for (int half = 0; half < 2; ++half) {
     int bwd = half;
     if (direction == RS_FORWARD && bwd) continue;
@@ -1374,7 +1336,7 @@ static int gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omeg
     const T* xold = x;
     if (!m->structurally_symmetric) {
       // snapshot of the old iterate for the not-yet-visited side
-      T* snap = (T*)m->scratch + 3 * m->nrows;
+      T* snap = c.scr + 3 * m->nrows;
       RS_CUDA(cudaMemcpyAsync(snap, x, sizeof(T) * c.n, cudaMemcpyDeviceToDevice, st));
       xold = snap;
     }
@@ -1409,6 +1371,7 @@ static int gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omeg
         RS_CUDA(cudaLaunchCooperativeKernel((const void*)k_gs_levels_ord<T>, dim3(lv.level_grid), dim3(kB), args, 0,
                                             st));
         RS_COUNT_LAUNCH();
+        pdl_ok = true;
         continue;
       }
       static const bool pdl = !getenv("RS_GS_PDL") || atoi(getenv("RS_GS_PDL")) != 0;
@@ -1451,13 +1414,15 @@ static int gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omeg
           at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
           at[0].val.programmaticStreamSerializationAllowed = 1;
           cfgl.attrs = at;
-          cfgl.numAttrs = 1;
+          cfgl.numAttrs = pdl_ok ? 1 : 0;
           if (in_smem) {
-            static bool attr_set = false;
-            if (!attr_set) {
+            // the attribute is per device context: set it once per device (threads / ranks may race
+            // here harmlessly -- the call is idempotent)
+            static std::atomic<bool> attr_set[kMaxDevices];
+            if (m->device >= kMaxDevices || !attr_set[m->device].load(std::memory_order_acquire)) {
               RS_CUDA(cudaFuncSetAttribute(k_gs_levels_cta<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)(kGsSmemBytes + sizeof(int64_t) * 2 * (kGsMaxRun + 1))));
-              attr_set = true;
+              if (m->device < kMaxDevices) attr_set[m->device].store(true, std::memory_order_release);
             }
             RS_CUDA(cudaLaunchKernelEx(&cfgl, k_gs_levels_cta<T, true>, l, l2, (const int64_t*)lv.level_ptr_dev,
                                        (const int64_t*)m->lv_slice_base_dev[bwd], (const int32_t*)lv.rows,
@@ -1470,6 +1435,7 @@ static int gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omeg
                                        x, w, w1, damped, (int64_t)c.n));
           }
           RS_COUNT_LAUNCH();
+        pdl_ok = true;
           l = l2 - 1;
           continue;
         }
@@ -1484,7 +1450,7 @@ static int gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omeg
           at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
           at[0].val.programmaticStreamSerializationAllowed = 1;
           cfgl.attrs = at;
-          cfgl.numAttrs = 1;
+          cfgl.numAttrs = pdl_ok ? 1 : 0;
           RS_CUDA(cudaLaunchKernelEx(&cfgl, k_mt_color_pdl<T>, cnt, (const int32_t*)(lv.rows + lo),
                                      (const int64_t*)(S.slice_ptr + base[l]), (const int32_t*)S.col, (const T*)S.val,
                                      c.d, b, x, w, w1, damped));
@@ -1493,16 +1459,21 @@ static int gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omeg
                                                           S.dord + lo, b, x, w, w1, damped);
         }
         RS_COUNT_LAUNCH();
+        pdl_ok = true;
       }
       continue;
     }
-    if (gs_cooperative<T>(m, lv, c, b, x, xL, xU, w, w1, damped, bwd, st) == RS_OK) continue;
+    if (gs_cooperative<T>(m, lv, c, b, x, xL, xU, w, w1, damped, bwd, st) == RS_OK) {
+      pdl_ok = true;
+      continue;
+    }
     for (int64_t l = 0; l < lv.nlevels; ++l) {
       int64_t lo = lv.level_ptr_host[l], hi = lv.level_ptr_host[l + 1];
       int64_t cnt = hi - lo;
       if (!cnt) continue;
       k_gs_level<T><<<grid_for(cnt, kB), kB, 0, st>>>(cnt, lv.rows + lo, c.L, c.U, c.d, b, x, xL, xU, w, w1, damped);
       RS_COUNT_LAUNCH();
+        pdl_ok = true;
     }
   }
   RS_CHECK_LAUNCH("gs_sweep");
@@ -1517,9 +1488,11 @@ template <typename T>
 static int inner_jr_t(rs_matrix* m, const T* r, T* g, int n_j, int backward, double omega, double gamma,
                       cudaStream_t st) {
   int e;
-  if ((e = ensure_scratch(m))) return e;
+  void* scr_ = nullptr;
+  if ((e = get_scratch(m, st, &scr_))) return e;
   Ctx<T> c(m, st);
-  T* rd = (T*)m->scratch;
+  c.scr = (T*)scr_;
+  T* rd = c.scr;
   T* ga = rd + c.n;
   T* gb = ga + c.n;
   if (n_j == 0) {
@@ -1593,23 +1566,24 @@ static int precond_gs2_single(rs_matrix* m, const rs_relax_cfg& cfg, const R* r,
   const T w = (T)cfg.omega, gm = (T)cfg.gamma, gm1 = (T)(1.0 - cfg.gamma);
   const bool damped = cfg.gamma != 1.0;
   if (!c.n) return RS_OK;
+  {
+    void* s_ = nullptr;
+    const int e_ = get_scratch(m, st, &s_);
+    if (e_) return e_;
+    c.scr = (T*)s_;
+  }
   if (cfg.n_j == 0) {
     k_scale0<T, R, O><<<c.grid(), kB, 0, st>>>(c.n, r, c.d, z, w, overflow);
     RS_COUNT_LAUNCH();
     RS_CHECK_LAUNCH("precond");
     return RS_OK;
   }
-  {
-    const int e = pipe_half_sweep<T, R, O>(m, kPipeZero, nullptr, r, nullptr, z, cfg.n_j, bwd, cfg.omega, cfg.gamma,
-                                           overflow, st);
-    if (e != RS_ERR_UNSUPPORTED) return e;
-  }
   // two-pass first step (rd = (T)r / d stored, then the inner step gathers rd) instead of k_inner0's
   // per-neighbour divisions: RS_PRECOND_TWOPASS = 1 / 0 forces it on / off (default: on for fp32)
   static const int twopass_env = getenv("RS_PRECOND_TWOPASS") ? atoi(getenv("RS_PRECOND_TWOPASS")) : -1;
   const bool twopass = twopass_env >= 0 ? twopass_env != 0 : sizeof(T) == 4;
   if (twopass) {
-    T* rd = (T*)m->scratch;
+    T* rd = c.scr;
     T* bufs[2] = {rd + c.n, rd + 2 * c.n};
     // fp32 (single_inside_double): wide scale pass and 2 rows per thread in the final step
     // (RS_F32_NR=1 restores the one-row kernels for A/B runs)
@@ -1662,7 +1636,7 @@ static int precond_gs2_single(rs_matrix* m, const rs_relax_cfg& cfg, const R* r,
     RS_CHECK_LAUNCH("precond");
     return RS_OK;
   }
-  T* rd = (T*)m->scratch;
+  T* rd = c.scr;
   T* bufs[2] = {rd + c.n, rd + 2 * c.n};
   if (damped) k_inner0<T, R, O, false, true><<<c.grid(), kB, 0, st>>>(c.n, Tm, r, c.d, rd, bufs[0], z, w, gm, gm1, overflow);
   else k_inner0<T, R, O, false, false><<<c.grid(), kB, 0, st>>>(c.n, Tm, r, c.d, rd, bufs[0], z, w, gm, gm1, overflow);
@@ -1767,15 +1741,16 @@ static int spmv_red(rs_matrix_t m, int mode, const double* x, const double* b, d
   const int64_t n = m->nrows;
   const int64_t nblk = std::max<int64_t>(grid_for(std::max<int64_t>(n, 1), kB), 1);
   int e;
-  if ((e = ensure_reduction(m, nblk))) return e;
+  double* red = nullptr;
+  if ((e = get_reduction(m, st, nblk, &red))) return e;
   SellView<double> Lv = view(m->L64, false), Uv = view(m->U64, false);
   const double* d = (const double*)m->d;
   if (mode == kRedDot)
-    k_spmv_red<kRedDot><<<nblk, kB, 0, st>>>(n, Lv, Uv, d, x, b, y, m->red, pf_dist_host());
+    k_spmv_red<kRedDot><<<nblk, kB, 0, st>>>(n, Lv, Uv, d, x, b, y, red, pf_dist_host());
   else
-    k_spmv_red<kRedNorm><<<nblk, kB, 0, st>>>(n, Lv, Uv, d, x, b, y, m->red, pf_dist_host());
+    k_spmv_red<kRedNorm><<<nblk, kB, 0, st>>>(n, Lv, Uv, d, x, b, y, red, pf_dist_host());
   RS_COUNT_LAUNCH();
-  k_reduce_many<<<1, 1024, 0, st>>>(m->red, nblk, out);
+  k_reduce_many<<<1, 1024, 0, st>>>(red, nblk, out);
   RS_COUNT_LAUNCH();
   RS_CHECK_LAUNCH("spmv_red");
   return RS_OK;
@@ -1882,22 +1857,14 @@ int rs_precond_apply(rs_matrix_t m, int kind, const rs_relax_cfg* cfg, const dou
     return RS_ERR_ARG;
   }
   int e;
-  if ((e = ensure_scratch(m))) return e;
+  void* scr_ = nullptr;
+  if ((e = get_scratch(m, st, &scr_))) return e;
   // Fused zero-start path: always for float32 (the r cast and z upcast fold into
   // the sweep); for float64 only when n_j == 0 -- with n_j >= 1 the per-neighbour
   // fp64 divisions r_k/d_k make the single pass latency-bound (ncu: 40% DRAM,
   // 0.305 ms) and the two-pass rd = r/d ; z = w(rd - w D^-1L rd) is faster
   // (0.239 ms at 256^3) despite its 2V extra bytes.
   if (single_half_sweep(kind, *cfg)) {
-    const bool wave_ok = m->dtype == RS_F32 ? wave_usable<float>(m, cfg->direction) : wave_usable<double>(m, cfg->direction);
-    if (wave_enabled() && cfg->n_j >= 1 && m->nrows > 0 && wave_ok) {
-      // one wavefront launch: z = GS2 half-sweep from zero (fp32: r cast / z upcast fused)
-      if (m->dtype == RS_F32)
-        return wave_precond_f32(m, r, z, cfg->n_j, cfg->direction == RS_BACKWARD, cfg->omega, cfg->gamma,
-                                (long long*)overflow_flag, st);
-      return wave_half_sweep<double>(m, r, nullptr, z, cfg->n_j, cfg->direction == RS_BACKWARD, cfg->form,
-                                     cfg->omega, cfg->gamma, true, st);
-    }
     if (m->dtype == RS_F32) return precond_gs2_single<float, double, double>(m, *cfg, r, z, (long long*)overflow_flag, st);
     // (the one-pass k_inner0 for f64 n_j >= 1 measured 0.268 ms vs 0.222 ms two-pass at 256^3: the
     // per-neighbour fp64 divisions make it latency-bound)
@@ -1905,8 +1872,8 @@ int rs_precond_apply(rs_matrix_t m, int kind, const rs_relax_cfg* cfg, const dou
   }
   if (m->dtype == RS_F64) return precond_body<double>(m, kind, *cfg, r, z, st);
   // single_inside_double (krylov.py:116-118, 135-136): cast r, relax in float32, upcast z
-  float* rhs = (float*)m->scratch + 4 * m->nrows;
-  float* zw = (float*)m->scratch + 5 * m->nrows;
+  float* rhs = (float*)scr_ + 4 * m->nrows;
+  float* zw = (float*)scr_ + 5 * m->nrows;
   int64_t n = m->nrows;
   if (n) {
     k_cast_rhs_f32<<<grid_for(n, kB), kB, 0, st>>>(n, r, rhs, (long long*)overflow_flag);

@@ -20,7 +20,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "../../include/gs2b200.h"
 
@@ -62,6 +65,15 @@ struct Sell {
   T* dord = nullptr;             // [nrows] d[rows[t]] of group-ordered slices (MT / LV), else null
   int uw = -1;                   // every slice has this width (slice_ptr[s] = 32*uw*s), else -1
   int64_t s_lo = 0, s_hi = -1;   // slices outside [s_lo, s_hi) are empty (-1: not computed = all)
+};
+
+// per (host thread, stream) working memory of a matrix handle
+struct Workspace {
+  std::thread::id tid;
+  cudaStream_t st = nullptr;
+  void* scratch = nullptr;  // [rd | g_a | g_b | alt/snapshot | f32 rhs | f32 z], nrows each (working dtype)
+  double* red = nullptr;    // reduction partials
+  int64_t red_cap = 0;
 };
 
 struct Levels {
@@ -109,15 +121,13 @@ struct rs_matrix {
   rs::Sell<float> LV32[2];
   int64_t* lv_slice_base[2] = {nullptr, nullptr};
   int64_t* lv_slice_base_dev[2] = {nullptr, nullptr};
-  void* scratch = nullptr;  // 3*nrows working dtype (rd, g ping/pong)
-  void* scratch2 = nullptr; // 1*nrows (t)
-  double* red = nullptr;    // reduction partials
-  unsigned int* ticket = nullptr;
-  int64_t red_cap = 0;
-  void* wave[2] = {nullptr, nullptr};  // wavefront sweep plans (forward / backward)
-  void* stage = nullptr;               // wavefront stage vectors (n_j x nrows)
-  void* pipe = nullptr;                // window-pipelined sweep plan (relax.cu PipePlan)
-  size_t stage_bytes = 0;
+  // Working vectors are per (host thread, stream): concurrent solves on one shared matrix (the
+  // reference's contract) never share an rd / g / alt buffer or a reduction
+  // partial; `mu` guards this list and the lazily built analyses above (level sets, colouring,
+  // ordered slices), which are built once and then only read.
+  std::mutex mu;
+  std::vector<rs::Workspace*> ws;
+  std::mutex build_mu;  // serialises the lazy analyses (gs_sweep_t / mt_gs_sweep_t / colouring updates)
 };
 
 namespace rs {
@@ -165,8 +175,9 @@ template <typename T>
 __device__ __forceinline__ T ld_stream(const T* p) { return __ldcs(p); }
 
 // int status helpers for the host side of each entry point
-int ensure_scratch(rs_matrix* m);
-int ensure_reduction(rs_matrix* m, int64_t n_doubles);
+// this host thread's working memory on stream st (allocated on first use, freed with the handle)
+int get_scratch(rs_matrix* m, cudaStream_t st, void** out);
+int get_reduction(rs_matrix* m, cudaStream_t st, int64_t n_doubles, double** out);
 
 }  // namespace rs
 

@@ -92,7 +92,6 @@ class Preconditioner:
         self.coloring = None
         self._dev: DeviceMatrix | None = None
         self._cfg_c = N.RelaxCfg.of(cfg)
-        self._flag = None
         if kind != "none":
             self.splitting = extract_splitting(a, cfg.omega, cfg.gamma)
             dm = as_device(a)
@@ -113,11 +112,11 @@ class Preconditioner:
         return self._dev
 
     # -- device fast path ------------------------------------------------
-    def _overflow_flag(self, device):
+    @staticmethod
+    def _overflow_flag(device):
+        """A fresh overflow-index flag for one apply (never shared between concurrent calls)."""
         torch = _torch()
-        if self._flag is None or self._flag.device != device:
-            self._flag = torch.full((1,), _I64_MAX, dtype=torch.int64, device=device)
-        return self._flag
+        return torch.full((1,), _I64_MAX, dtype=torch.int64, device=device)
 
     def apply_into(self, r, z, flag=None) -> None:
         """z = P(r) for float64 CUDA tensors r, z (asynchronous; overflow index lands in ``flag``)."""
@@ -143,7 +142,6 @@ class Preconditioner:
             flag = None
             if self.precision == "single_inside_double":
                 flag = self._overflow_flag(r.device)
-                flag.fill_(_I64_MAX)
             self.apply_into(r, z, flag)
             if flag is not None:
                 i = int(flag.item())

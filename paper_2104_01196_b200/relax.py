@@ -18,6 +18,7 @@ current stream.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 from dataclasses import dataclass, replace
 
 import numpy as np
@@ -176,6 +177,7 @@ class _Blocks:
 
 
 _BLOCK_CACHE: dict = {}
+_BLOCK_LOCK = threading.Lock()
 
 
 def hybrid_relax(a, part: BlockPartition, b, x, cfg: RelaxConfig, local: str = "gs") -> None:
@@ -193,16 +195,17 @@ def hybrid_relax(a, part: BlockPartition, b, x, cfg: RelaxConfig, local: str = "
     if offs[-1] != nrows_of(a):
         raise ValueError(f"partition covers {offs[-1]} rows, matrix has {nrows_of(a)}")
     key = (id(a), tuple(int(o) for o in offs))
-    ent = _BLOCK_CACHE.get(key)
-    if ent is None or ent[0]() is not a:
-        import weakref
+    with _BLOCK_LOCK:
+        ent = _BLOCK_CACHE.get(key)
+        if ent is None or ent[0]() is not a:
+            import weakref
 
-        try:
-            ref = weakref.ref(a)
-        except TypeError:
-            ref = (lambda obj: (lambda: obj))(a)
-        ent = (ref, _Blocks(a, part))
-        _BLOCK_CACHE[key] = ent
+            try:
+                ref = weakref.ref(a)
+            except TypeError:
+                ref = (lambda obj: (lambda: obj))(a)
+            ent = (ref, _Blocks(a, part))
+            _BLOCK_CACHE[key] = ent
     blocks = ent[1].blocks
     dm0 = blocks[0][2]
     bv, xv = _vectors(dm0, b, x)

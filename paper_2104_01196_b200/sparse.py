@@ -14,6 +14,7 @@ host arrays) or CUDA torch tensors (used in place; the fast path).
 from __future__ import annotations
 
 import ctypes as C
+import threading
 import weakref
 from dataclasses import dataclass
 
@@ -116,12 +117,20 @@ class CsrMatrix:
         dev = _device_index(device)
         m = self._dev.get(dev)
         if m is None:
-            m = DeviceMatrix.from_csr(self, device=dev)
-            self._dev[dev] = m
+            with _LAZY_LOCK:  # concurrent first uses from several threads build one handle
+                m = self._dev.get(dev)
+                if m is None:
+                    m = DeviceMatrix.from_csr(self, device=dev)
+                    self._dev[dev] = m
         return m
 
     def __repr__(self):
         return f"CsrMatrix({self.nrows}x{self.ncols}, nnz={self.nnz}, {self.precision})"
+
+
+# guards the lazily built device handles (CsrMatrix.device, DeviceMatrix.single): matrices and
+# preconditioners are shared read-only between threads
+_LAZY_LOCK = threading.RLock()
 
 
 def _device_index(device=None) -> int:
@@ -189,9 +198,11 @@ class DeviceMatrix:
         if self.dtype == np.float32:
             return self
         if self._single is None:
-            h = C.c_void_p()
-            N.call("rs_mat_cast", self._h, N.RS_F32, C.byref(h))
-            self._single = DeviceMatrix(h.value, self.device_index)
+            with _LAZY_LOCK:
+                if self._single is None:
+                    h = C.c_void_p()
+                    N.call("rs_mat_cast", self._h, N.RS_F32, C.byref(h))
+                    self._single = DeviceMatrix(h.value, self.device_index)
         return self._single
 
     def __del__(self):

@@ -357,8 +357,13 @@ def test_stationary_elasticity_pattern(gmres_golden):
 
 
 @pytest.mark.parametrize("gen", ["lap3d_24", "ela3d_6", "rand_300"])
-def test_wavefront_sweep_bitwise(gen, monkeypatch):
-    """The opt-in fused wavefront sweep (RS_WAVE=1) is bitwise the reference arithmetic too."""
+def test_gs2_sweep_out_of_place_bitwise(gen):
+    """rs_gs2_sweep (x_out = GS2(x_in), x_in untouched) is bitwise the reference's in-place
+    gs2_apply, for every form / direction / damping combination."""
+    import ctypes
+
+    from paper_2104_01196_b200 import _native
+
     kind, nx = gen.split("_")
     nx = int(nx)
     if kind == "rand":
@@ -373,19 +378,21 @@ def test_wavefront_sweep_bitwise(gen, monkeypatch):
     om = oracle.Matrix(h)
     b = g2.random_rhs(h.nrows, 0)
     x0 = g2.random_rhs(h.nrows, 1)
-    monkeypatch.setenv("RS_WAVE", "1")
-    s = g2.extract_splitting(h)
+    from paper_2104_01196_b200.sparse import as_device
+
+    dm = as_device(h)
+    lib = _native.load()
+    bt, xin = torch.from_numpy(b).cuda(), torch.from_numpy(x0).cuda()
     for cfg in (g2.RelaxConfig(1, 1, 1), g2.RelaxConfig(2, 1, 3, direction="symmetric"),
                 g2.RelaxConfig(1, 1, 2, form="compact", omega=0.9), g2.RelaxConfig(1, 1, 2, gamma=0.7, direction="backward")):
-        xg = x0.copy()
+        xout = torch.empty_like(xin)
+        c = _native.RelaxCfg.of(cfg)
+        _native.check(lib.rs_gs2_sweep(dm.handle, bt.data_ptr(), xin.data_ptr(), xout.data_ptr(), ctypes.byref(c),
+                                       None))
         xo = x0.copy()
-        g2.gs2_apply(h, s, b, xg, cfg)
         oracle.gs2_apply(om, b, xo, cfg)
-        assert np.array_equal(xg, xo), cfg
-    for prec in ("same", "single_inside_double"):
-        m = g2.Preconditioner(h, "gs2", g2.RelaxConfig(1, 1, 2), precision=prec)
-        mo = oracle.Precond(h, "gs2", n_j=2, precision=prec)
-        assert np.array_equal(m.apply(b), mo.apply(b)), prec
+        assert np.array_equal(xout.cpu().numpy(), xo), cfg
+        assert np.array_equal(xin.cpu().numpy(), x0)
 
 
 # Reference GMRES(60) iteration counts at 128^3 (n = 2,097,152) measured by the survey with the
@@ -571,26 +578,59 @@ def test_fused_spmv_reductions(shape):
 
 
 def test_gmres_iteration_count_256_vs_reference():
-    """Config C2 at full size: GS2(1,1,1)-GMRES(60) on laplace3d 256^3 against the reference's own run
-    (tests/golden/ref_lap3d_256.json, relaxsolve with OPENBLAS_NUM_THREADS=1: 2635 iterations,
-    3 h 3 min on one core).  Exact equality is not a meaningful bar at this size: the count moves
-    with the last-bit rounding of the Gram-Schmidt dot products (the C oracle -- the reference
-    algorithm with bitwise-reference sweeps and SpMV but its own dot summation order -- gives
-    2591, and the reference itself moves by up to 5% with the BLAS thread count on config 1), so
-    the bar is 1%.  Observed: 2628 (DCGS2, default), 2629 (MGS)."""
+    """Config C2 at full size with the default (fast) orthogonalisation: GS2(1,1,1)-GMRES(60) on
+    laplace3d 256^3 against the reference's own run (tests/golden/ref_lap3d_256.json, relaxsolve
+    with OPENBLAS_NUM_THREADS=1: 2635 iterations, 3 h 3 min on one core).  DCGS2 sums its dots in
+    fixed-order device trees, so its count can only be compared within the reference's own
+    dot-order spread at this size (the reference re-run with other BLAS thread counts and with
+    numpy's pairwise dot, tests/golden/ref_lap3d_256_*.json -- `spread_band_256`); the
+    reference-order mode ortho="mgs_ref" reproduces 2635 and the whole history bit for bit
+    (profiles/r02_c2_mgs_ref.json; test_gmres_mgs_ref_256_prefix).  Observed: 2628."""
     import json
     from pathlib import Path
 
     want = json.loads((Path(__file__).parent / "golden" / "ref_lap3d_256.json").read_text())["iterations"]
+    lo, hi = spread_band_256()
     a = g2.laplace3d(256, device="cuda")
     b = g2.random_rhs(a.nrows, 0, device="cuda")
     _, h = g2.gmres(a, b, g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, 1)), restart=60, tol=1e-9)
     assert h.converged and h.final_rel_res <= 1e-9
-    assert abs(h.iterations - want) <= 0.01 * want, (h.iterations, want)
+    assert lo <= h.iterations <= hi, (h.iterations, want, (lo, hi))
     # the true residuals recorded at the first restarts agree closely (the preconditioner and SpMV
     # are bitwise the reference's; only the dot-product rounding differs)
     ref_hist = json.loads((Path(__file__).parent / "golden" / "ref_lap3d_256.json").read_text())["rel_res_every_60"]
     np.testing.assert_allclose(np.asarray(h.rel_res)[:300:60], ref_hist[:5], rtol=1e-8)
+
+
+def spread_band_256():
+    """[min, max] of the reference algorithm's 256^3 counts over the dot-product summation orders it
+    was run with: the reference itself at OPENBLAS_NUM_THREADS = 1 / 2 / 8 and with numpy's pairwise
+    sum for the MGS dot (tests/golden/ref_lap3d_256*.json, tests/golden/ref_lap3d_256.py), and the
+    same MGS algorithm with bitwise-reference sweeps / SpMV but a chunked dot order (the pre-round-2
+    C oracle, tests/golden/oracle_lap3d_256.json)."""
+    import json
+    from pathlib import Path
+
+    g = Path(__file__).parent / "golden"
+    files = sorted(g.glob("ref_lap3d_256*.json")) + [g / "oracle_lap3d_256.json"]
+    counts = [json.loads(f.read_text())["iterations"] for f in files if f.exists()]
+    return min(counts), max(counts)
+
+
+def test_gmres_mgs_ref_256_prefix():
+    """C2 at full size in the reference's summation order (ortho="mgs_ref"): the first five
+    GMRES(60) cycles' true residuals are bitwise the reference's recorded ones (the full solve --
+    2635 iterations, final residual bit-identical -- is profiles/r02_c2_mgs_ref.json, 7 min)."""
+    import json
+    from pathlib import Path
+
+    ref = json.loads((Path(__file__).parent / "golden" / "ref_lap3d_256.json").read_text())
+    a = g2.laplace3d(256, device="cuda")
+    b = g2.random_rhs(a.nrows, 0, device="cuda")
+    _, h = g2.gmres(a, b, g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, 1)), restart=60, tol=1e-9, maxit=300,
+                    ortho="mgs_ref")
+    got = [float(v) for v in np.asarray(h.rel_res)[::60]]
+    assert got == ref["rel_res_every_60"][:6]
 
 
 def test_sweeps_bitwise_at_full_c2_size():
@@ -699,3 +739,65 @@ def test_gmres_mgs_ref_bitwise(label, gmres_golden):
     assert h.converged == want["converged"]
     assert h.iterations == want["iterations"]
     assert np.array_equal(np.asarray(h.rel_res), np.array(want["rel_res"]))
+
+
+def test_concurrent_solves_share_matrix_and_preconditioner():
+    """The reference's contract (the threaded sweep-study, cli.py:230-241): solves
+    may run concurrently on shared read-only matrices and preconditioners.  Four host threads, each
+    on its own CUDA stream, share one DeviceMatrix and one Preconditioner of every kind (working
+    vectors are per (thread, stream) inside the library, lazy analyses are built under a lock, the
+    fp32 overflow flag is per call); every result is bitwise the serial one."""
+    import threading
+
+    a = g2.laplace3d(40, device="cuda")
+    n = a.nrows
+    pcs = {
+        "gs2": g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, 2)),
+        "sgs2": g2.Preconditioner(a, "sgs2", g2.RelaxConfig(1, 1, 1)),
+        "gs2_f32": g2.Preconditioner(a, "gs2", g2.RelaxConfig(2, 1, 1), precision="single_inside_double"),
+        "jr": g2.Preconditioner(a, "jr", g2.RelaxConfig(2, 1, 0)),
+        "gs_seq": g2.Preconditioner(a, "gs_seq", g2.RelaxConfig(1, 1, 0)),
+        "mt_sgs": g2.Preconditioner(a, "mt_sgs", g2.RelaxConfig(1, 1, 0)),
+    }
+    s = g2.extract_splitting(a)
+    rhs = [g2.random_rhs(n, 10 + i, device="cuda") for i in range(4)]
+    x0 = g2.random_rhs(n, 99, device="cuda")
+
+    def work(i):
+        out = {}
+        for k, pc in pcs.items():
+            out[k] = pc.apply(rhs[i])
+        x = x0.clone()
+        g2.gs2_apply(a, s, rhs[i], x, g2.RelaxConfig(1, 1, 3, direction="symmetric"))
+        out["gs2_apply"] = x
+        out["spmv"] = g2.spmv(a, rhs[i])
+        xs, h = g2.gmres(a, rhs[i], pcs["gs2"], restart=20, tol=1e-7)
+        out["gmres"] = xs
+        out["hist"] = torch.tensor(h.rel_res)
+        return out
+
+    serial = [work(i) for i in range(4)]
+    torch.cuda.synchronize()
+    got = [None] * 4
+    errs = []
+
+    def worker(i):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                res = [work(i) for _ in range(2)]
+            st.synchronize()
+            got[i] = res
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    ths = [threading.Thread(target=worker, args=(i,)) for i in range(4)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not errs, errs
+    for i in range(4):
+        for res in got[i]:
+            for k, v in serial[i].items():
+                assert torch.equal(res[k].cpu(), v.cpu()), (i, k)
