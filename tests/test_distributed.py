@@ -293,3 +293,81 @@ def test_peer_mailboxes_thread_ranks_bitwise(nparts, gmres_golden):
     key = f"lap3d_32__m60__hybrid_gs2_1_1_1__P{nparts}"
     if key in gmres_golden["runs"]:
         assert abs(len(peer[0][0]) - 1 - gmres_golden["runs"][key]["iterations"]) <= 1
+
+
+def _slab_blocks(n, plane, world):
+    """(lo, hi, halo_lo, halo_hi) of the C5 z-slab partition (BlockPartition.regular, relax.py:89-92)
+    of a grid with `plane` rows per z-plane: one plane of halo per neighbour (7-point stencil)."""
+    from paper_2104_01196_b200 import BlockPartition
+
+    offs = [int(o) for o in BlockPartition.regular(n, world).offsets]
+    return [(offs[r], offs[r + 1], plane if r > 0 else 0, plane if r < world - 1 else 0) for r in range(world)]
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_halo_plan_c5_512_slabs(world):
+    """Config C5 (laplace3d 512^3, 2/4/8 z-slabs): every rank sends its first / last plane (512^2 rows
+    = 2 MiB fp64) to each neighbour and receives one plane per side -- no other traffic."""
+    n, plane = 512 ** 3, 512 ** 2
+    blocks = _slab_blocks(n, plane, world)
+    assert all(hi - lo == n // world for lo, hi, _, _ in blocks)
+    for r in range(world):
+        p = HaloPlan.build(r, blocks)
+        lo, hi = blocks[r][:2]
+        want_send, want_recv = set(), set()
+        if r > 0:
+            want_send.add((r - 1, 0, plane))
+            want_recv.add((r - 1, "lo", 0, plane))
+        if r < world - 1:
+            want_send.add((r + 1, hi - lo - plane, hi - lo))
+            want_recv.add((r + 1, "hi", 0, plane))
+        assert set(p.send) == want_send and set(p.recv) == want_recv, r
+        assert sum(e - s for _, s, e in p.send) * 8 == 2 * 2 ** 20 * (2 if 0 < r < world - 1 else 1)
+
+
+def _gloo_slab_worker(rank, world, port, q, nxy, nz):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = TorchComm()
+        plane = nxy * nxy
+        n = plane * nz
+        lo, hi, halo_lo, halo_hi = _slab_blocks(n, plane, world)[rank]
+        blocks = comm.allgather_obj((lo, hi, halo_lo, halo_hi))
+        plan = HaloPlan.build(rank, blocks)
+        x = torch.arange(lo, hi, dtype=torch.float64) * 0.5 - 3.0  # x_global[i] = 0.5 i - 3
+        xlo = torch.full((max(halo_lo, 1),), -1.0, dtype=torch.float64)
+        xhi = torch.full((max(halo_hi, 1),), -1.0, dtype=torch.float64)
+        sends = [(peer, x[s:e].contiguous()) for peer, s, e in plan.send]
+        recvs = [(peer, (xlo if w == "lo" else xhi)[s:e]) for peer, w, s, e in plan.recv]
+        comm.exchange(sends, recvs)
+        ok = True
+        if halo_lo:
+            ok &= torch.equal(xlo[:halo_lo], torch.arange(lo - halo_lo, lo, dtype=torch.float64) * 0.5 - 3.0)
+        if halo_hi:
+            ok &= torch.equal(xhi[:halo_hi], torch.arange(hi, hi + halo_hi, dtype=torch.float64) * 0.5 - 3.0)
+        # the Gram-Schmidt reductions: 2 x (j+1) <= 122 doubles summed over ranks, same bits everywhere
+        t = torch.arange(122, dtype=torch.float64) * (rank + 1)
+        comm.allreduce_sum_(t)
+        ok &= torch.equal(t, torch.arange(122, dtype=torch.float64) * (world * (world + 1) / 2))
+        ok &= comm.allreduce_max(float(rank)) == float(world - 1)
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_gloo_c5_slab_exchange_and_reductions(world):
+    """world_size 4 and 8 (gloo, CPU): the C5 z-slab halo plan (scaled grid 16 x 16 x 64) exchanges
+    exactly the neighbours' boundary planes, and the reductions agree on every rank."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_slab_worker, args=(r, world, port, q, 16, 64)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {r: True for r in range(world)}
