@@ -167,6 +167,14 @@ int rs_inner_jr(rs_matrix_t m, const void *r, void *g, int n_j, int backward, do
 /* gs2_apply (relax.py:208-220) incl. _two_stage_sweep (193-205): x in place. */
 int rs_gs2_apply(rs_matrix_t m, const void *b, void *x, const rs_relax_cfg *cfg, rs_stream_t stream);
 
+/* Stand-alone smoother (_run_stationary / _stationary_apply, cli.py:118-152): napps applications
+ * of `kind` (RS_PC_JR: n_t*n_k damped-JR sweeps; GS_SEQ / SGS_SEQ, MT_GS / MT_SGS: n_t*n_k sweeps;
+ * GS2 / SGS2: one gs2_apply) to x in place, float64.  norm2 (device, napps+1 doubles, may be NULL):
+ * norm2[k] = ||b - A x_k||^2, x_0 = x on entry -- for GS2 / SGS2 (non-compact) and JR taken from the
+ * next application's own residual pass (fixed-order tree sum), else one fused SpMV + norm each. */
+int rs_stationary_batch(rs_matrix_t m, int kind, const rs_relax_cfg *cfg, const double *b, double *x, int napps,
+                        double *norm2, rs_stream_t stream);
+
 /* gs2_apply out of place, x_out = GS2(x_in), x_in unchanged (any cfg): x_out = x_in, then the
  * in-place pass chain.  Bitwise equal to gs2_apply on a copy of x_in. */
 int rs_gs2_sweep(rs_matrix_t m, const void *b, const void *x_in, void *x_out, const rs_relax_cfg *cfg,

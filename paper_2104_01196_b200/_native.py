@@ -69,6 +69,7 @@ _SIGS = {
     "rs_inner_jr": ([_P, _P, _P, C.c_int, C.c_int, C.c_double, C.c_double, _P], C.c_int),
     "rs_gs2_apply": ([_P, _P, _P, C.POINTER(RelaxCfg), _P], C.c_int),
     "rs_gs2_sweep": ([_P, _P, _P, _P, C.POINTER(RelaxCfg), _P], C.c_int),
+    "rs_stationary_batch": ([_P, C.c_int, C.POINTER(RelaxCfg), _P, _P, C.c_int, _P, _P], C.c_int),
     "rs_hybrid_bhat": ([_P, _P, _P, _P, _P, _P, _P], C.c_int),
     "rs_precond_apply": ([_P, C.c_int, C.POINTER(RelaxCfg), _P, _P, _P, _P], C.c_int),
     "rs_reduce_work_doubles": ([C.c_int], C.c_int64),

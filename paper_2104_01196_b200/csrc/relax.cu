@@ -60,11 +60,15 @@ struct Halo {
 // before accumulating -- RowFetch -- was measured slower here: 0.37-0.72 ms vs
 // 0.31 ms for the 256^3 SpMV, the extra registers cost more occupancy than the
 // shorter dependency chain gains; profiles/resid_tune.sh.)
-template <typename T, int MODE>
+// NORM (kResidRd / kJr): also the block's partial of ||b - A x||^2 into partial[blockIdx.x] -- the
+// stand-alone smoother's residual history (cli.py:140-152) taken from the residual pass the next
+// application computes anyway, instead of an extra SpMV + norm.
+template <typename T, int MODE, bool NORM = false>
 __global__ void __launch_bounds__(256) k_resid(int64_t n, SellView<T> Elo, SellView<T> L, SellView<T> U,
                                                SellView<T> Ehi, const T* __restrict__ d, const T* __restrict__ x,
                                                const T* __restrict__ xlo, const T* __restrict__ xhi,
-                                               const T* __restrict__ b, T* __restrict__ out, T w, int pf) {
+                                               const T* __restrict__ b, T* __restrict__ out, T w, int pf,
+                                               double* __restrict__ partial = nullptr) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (pf && i + pf < n) {
     const int64_t s2 = (i + pf) >> 5;
@@ -75,26 +79,44 @@ __global__ void __launch_bounds__(256) k_resid(int64_t n, SellView<T> Elo, SellV
     q -= pf_vec<T>(x, s2, q);
     if (MODE != kSpmv) q -= pf_vec<T>(b, s2, q);
   }
-  if (i >= n) return;
-  // the U slice bounds and the row's own operands do not depend on the L walk: fetch them first
-  int64_t pu0 = 0;
-  int uwd = 0;
-  if (!U.empty) slice_bounds<T>(U, i >> 5, pu0, uwd);
-  const T di = d[i];
-  const T xi = x[i];
-  T acc = (T)0;
-  acc = row_accum<T>(Elo, i, xlo, acc);
-  acc = row_accum<T>(L, i, x, acc);
-  acc = add_rn<T>(acc, mul_rn<T>(di, xi));
-  acc = row_accum_p<T>(U, pu0, uwd, i, x, acc);
-  acc = row_accum<T>(Ehi, i, xhi, acc);
-  if (MODE == kSpmv) {
-    out[i] = acc;
-  } else if (MODE == kResidRd) {
-    out[i] = div_rn<T>(sub_rn<T>(b[i], acc), di);
-  } else if (MODE == kJr) {
-    T g = div_rn<T>(sub_rn<T>(b[i], acc), di);
-    out[i] = add_rn<T>(xi, mul_rn<T>(w, g));
+  if (!NORM && i >= n) return;
+  double v2 = 0.0;
+  if (i < n) {
+    // the U slice bounds and the row's own operands do not depend on the L walk: fetch them first
+    int64_t pu0 = 0;
+    int uwd = 0;
+    if (!U.empty) slice_bounds<T>(U, i >> 5, pu0, uwd);
+    const T di = d[i];
+    const T xi = x[i];
+    T acc = (T)0;
+    acc = row_accum<T>(Elo, i, xlo, acc);
+    acc = row_accum<T>(L, i, x, acc);
+    acc = add_rn<T>(acc, mul_rn<T>(di, xi));
+    acc = row_accum_p<T>(U, pu0, uwd, i, x, acc);
+    acc = row_accum<T>(Ehi, i, xhi, acc);
+    if (MODE == kSpmv) {
+      out[i] = acc;
+    } else if (MODE == kResidRd) {
+      const T r = sub_rn<T>(b[i], acc);
+      out[i] = div_rn<T>(r, di);
+      if (NORM) v2 = (double)r * (double)r;
+    } else if (MODE == kJr) {
+      const T r = sub_rn<T>(b[i], acc);
+      T g = div_rn<T>(r, di);
+      out[i] = add_rn<T>(xi, mul_rn<T>(w, g));
+      if (NORM) v2 = (double)r * (double)r;
+    }
+  }
+  if (NORM) {
+    for (int o = 16; o; o >>= 1) v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+    __shared__ double red[8];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v2;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int q = 0; q < 8; ++q) t += red[q];
+      partial[blockIdx.x] = t;
+    }
   }
 }
 
@@ -640,6 +662,10 @@ struct Ctx {
   SellView<T> L, U, Lsc, Usc, Elo, Ehi;
   const T* d;
   T* scr = nullptr;  // this call's working vectors (get_scratch)
+  // norm sink (stand-alone smoother): when set, the next residual pass (k_resid kResidRd / kJr) also
+  // writes ||b - A x||^2 of the iterate it reads into *norm_out (partials in norm_red), then clears it
+  double* norm_out = nullptr;
+  double* norm_red = nullptr;
   Ctx(rs_matrix* mm, cudaStream_t s) : m(mm), st(s), n(mm->nrows) {
     L = view(tri<T>(m, 0), false);
     U = view(tri<T>(m, 1), false);
@@ -739,8 +765,16 @@ static int two_stage(Ctx<T>& c, const T* b, T* x, int n_j, int backward, int for
     // x + w*((b - A x)/d) is exactly the damped-JR update (test_relax.py:198-208: n_j = 0 == JR
     // bitwise): one fused pass into the spare buffer + copy-back instead of rd pass + update pass
     T* alt = rd + 3 * c.n;
-    k_resid<T, kJr><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x, nullptr,
-                                               nullptr, b, alt, (T)omega, pf_dist_host());
+    if (c.norm_out) {
+      k_resid<T, kJr, true><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x,
+                                                       nullptr, nullptr, b, alt, (T)omega, pf_dist_host(), c.norm_red);
+      RS_COUNT_LAUNCH();
+      k_reduce_many<<<1, 1024, 0, c.st>>>(c.norm_red, c.grid(), c.norm_out);
+      c.norm_out = nullptr;
+    } else {
+      k_resid<T, kJr><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x, nullptr,
+                                                 nullptr, b, alt, (T)omega, pf_dist_host());
+    }
     RS_COUNT_LAUNCH();
     RS_CUDA(cudaMemcpyAsync(x, alt, sizeof(T) * c.n, cudaMemcpyDeviceToDevice, c.st));
     return RS_OK;
@@ -754,8 +788,16 @@ static int two_stage(Ctx<T>& c, const T* b, T* x, int n_j, int backward, int for
       k_scale_rd<T, T><<<c.grid(), kB, 0, c.st>>>(c.n, b, c.d, rd, nullptr);
     RS_COUNT_LAUNCH();
   } else if (!compact) {
-    k_resid<T, kResidRd><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x, nullptr,
-                                                     nullptr, b, rd, (T)0, pf_dist_host());
+    if (c.norm_out) {
+      k_resid<T, kResidRd, true><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x,
+                                                            nullptr, nullptr, b, rd, (T)0, pf_dist_host(), c.norm_red);
+      RS_COUNT_LAUNCH();
+      k_reduce_many<<<1, 1024, 0, c.st>>>(c.norm_red, c.grid(), c.norm_out);
+      c.norm_out = nullptr;
+    } else {
+      k_resid<T, kResidRd><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x, nullptr,
+                                                       nullptr, b, rd, (T)0, pf_dist_host());
+    }
     RS_COUNT_LAUNCH();
   } else {
     SellView<T> Tm = backward ? c.L : c.U;
@@ -772,12 +814,15 @@ static int two_stage(Ctx<T>& c, const T* b, T* x, int n_j, int backward, int for
 }
 
 template <typename T>
-static int gs2_apply_t(rs_matrix* m, const T* b, T* x, const rs_relax_cfg& cfg, cudaStream_t st, bool x_is_zero) {
+static int gs2_apply_t(rs_matrix* m, const T* b, T* x, const rs_relax_cfg& cfg, cudaStream_t st, bool x_is_zero,
+                       double* norm_out = nullptr, double* norm_red = nullptr) {
   int e;
   void* scr_ = nullptr;
   if ((e = get_scratch(m, st, &scr_))) return e;
   Ctx<T> c(m, st);
   c.scr = (T*)scr_;
+  c.norm_out = x_is_zero ? nullptr : norm_out;
+  c.norm_red = norm_red;
   bool zero = x_is_zero;
   for (int t = 0; t < cfg.n_t; ++t)
     for (int k = 0; k < cfg.n_k; ++k)
@@ -1193,7 +1238,8 @@ static int gs2_sweep_oop_t(rs_matrix* m, const T* b, const T* xin, T* xout, cons
 
 // jr_sweeps (relax.py:145-154) with ping-pong iterates: x_next = x + w (b - A x)/d
 template <typename T>
-static int jr_sweeps_t(rs_matrix* m, const T* b, T* x, int sweeps, double omega, cudaStream_t st, bool x_is_zero) {
+static int jr_sweeps_t(rs_matrix* m, const T* b, T* x, int sweeps, double omega, cudaStream_t st, bool x_is_zero,
+                       double* norm_out = nullptr, double* norm_red = nullptr) {
   int e;
   void* scr_ = nullptr;
   if ((e = get_scratch(m, st, &scr_))) return e;
@@ -1213,8 +1259,15 @@ static int jr_sweeps_t(rs_matrix* m, const T* b, T* x, int sweeps, double omega,
       continue;
     }
     T* nxt = cur == x ? alt : x;
-    k_resid<T, kJr><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, cur, nullptr,
-                                               nullptr, b, nxt, w, pf_dist_host());
+    if (s == 0 && norm_out) {  // the first sweep's residual pass is ||b - A x_in||
+      k_resid<T, kJr, true><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, cur,
+                                                       nullptr, nullptr, b, nxt, w, pf_dist_host(), norm_red);
+      RS_COUNT_LAUNCH();
+      k_reduce_many<<<1, 1024, 0, c.st>>>(norm_red, c.grid(), norm_out);
+    } else {
+      k_resid<T, kJr><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, cur, nullptr,
+                                                 nullptr, b, nxt, w, pf_dist_host());
+    }
     RS_COUNT_LAUNCH();
     cur = nxt;
   }
@@ -1885,6 +1938,63 @@ int rs_precond_apply(rs_matrix_t m, int kind, const rs_relax_cfg* cfg, const dou
     RS_COUNT_LAUNCH();
   }
   RS_CHECK_LAUNCH("precond_apply");
+  return RS_OK;
+}
+
+// Stand-alone smoother (the reference's _run_stationary / _stationary_apply, cli.py:118-152):
+// napps applications of `kind` to x in place; if norm2 != NULL, norm2[k] = ||b - A x_k||^2 for
+// k = 0..napps (x_0 = x on entry).  For GS2 / SGS2 in the non-compact form and for JR the norm of
+// x_k is taken from application k+1's own residual pass (k_resid NORM variant), so a history costs
+// one extra fused SpMV + norm per batch; other kinds / the compact form pay one per application.
+int rs_stationary_batch(rs_matrix_t m, int kind, const rs_relax_cfg* cfg, const double* b, double* x, int napps,
+                        double* norm2, rs_stream_t stream) {
+  RS_SET_DEVICE(m);
+  if (m->dtype != RS_F64) {
+    set_error(RS_ERR_UNSUPPORTED, "rs_stationary_batch: the smoother runs on the float64 matrix (cli.py:138)");
+    return RS_ERR_UNSUPPORTED;
+  }
+  if (bad_cfg(cfg) || napps < 0 || !b || !x) {
+    set_error(RS_ERR_ARG, "rs_stationary_batch: bad arguments");
+    return RS_ERR_ARG;
+  }
+  if (kind < RS_PC_JR || kind > RS_PC_MT_SGS) {
+    set_error(RS_ERR_ARG, "kind cannot run as a stationary solver");
+    return RS_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  rs_relax_cfg c = *cfg;
+  const int sweeps = c.n_t * c.n_k;
+  if (kind == RS_PC_SGS_SEQ || kind == RS_PC_SGS2 || kind == RS_PC_MT_SGS) c.direction = RS_SYMMETRIC;
+  const bool gs2 = kind == RS_PC_GS2 || kind == RS_PC_SGS2;
+  const bool fused = norm2 && m->nrows > 0 && ((gs2 && c.form == RS_NON_COMPACT) || kind == RS_PC_JR);
+  double* red = nullptr;
+  int e;
+  if (fused && (e = get_reduction(m, st, grid_for(m->nrows, kB), &red))) return e;
+  if (norm2 && !fused && (e = spmv_red(m, kRedNorm, x, b, nullptr, norm2, stream))) return e;
+  for (int k = 0; k < napps; ++k) {
+    double* nk = fused ? norm2 + k : nullptr;
+    switch (kind) {
+      case RS_PC_JR:
+        e = jr_sweeps_t<double>(m, b, x, sweeps, c.omega, st, false, nk, red);
+        break;
+      case RS_PC_GS_SEQ:
+      case RS_PC_SGS_SEQ:
+        e = RS_OK;
+        for (int q = 0; q < sweeps && !e; ++q) e = gs_sweep_t<double>(m, b, x, c.direction, c.omega, st);
+        break;
+      case RS_PC_MT_GS:
+      case RS_PC_MT_SGS:
+        e = RS_OK;
+        for (int q = 0; q < sweeps && !e; ++q) e = mt_gs_sweep_t<double>(m, b, x, c.direction, c.omega, st);
+        break;
+      default:
+        e = gs2_apply_t<double>(m, b, x, c, st, false, nk, red);
+    }
+    if (e) return e;
+    if (norm2 && !fused && (e = spmv_red(m, kRedNorm, x, b, nullptr, norm2 + k + 1, stream))) return e;
+  }
+  if (fused && (e = spmv_red(m, kRedNorm, x, b, nullptr, norm2 + napps, stream))) return e;
+  RS_CHECK_LAUNCH("stationary_batch");
   return RS_OK;
 }
 

@@ -43,3 +43,8 @@ def gmres_golden():
 
 
 SWEEP_CASES = ("lap2d_12", "lap3d_8", "lap3d_6x5x4", "ela3d_3", "rand_80", "spd_50", "cd3d_6")
+
+
+@pytest.fixture(scope="session")
+def stationary_golden():
+    return json.loads((GOLDEN / "stationary.json").read_text())

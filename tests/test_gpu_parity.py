@@ -801,3 +801,51 @@ def test_concurrent_solves_share_matrix_and_preconditioner():
         for res in got[i]:
             for k, v in serial[i].items():
                 assert torch.equal(res[k].cpu(), v.cpu()), (i, k)
+
+
+@pytest.mark.parametrize("label", ["lap2d_128__gs2_2_1_1__tol1e-6", "lap2d_32__jr_1", "lap2d_32__jr_2__w0.8",
+                                   "lap2d_32__gs_seq_1", "lap2d_32__sgs_seq_1", "lap2d_32__mt_gs_1",
+                                   "lap2d_32__mt_sgs_2", "lap2d_32__sgs2_1_1_1", "lap2d_32__gs2_1_2_2__compact_w0.9",
+                                   "lap3d_12__gs2_1_1_3__gamma0.7_bwd", "ela3d_6__jr_1__diverges",
+                                   "ela3d_6__gs2_1_1_3"])
+@pytest.mark.parametrize("exact", [True, False])
+def test_stationary_solve_reference_histories(label, exact, stationary_golden):
+    """Row a14 (the smoother mode, cli.py:118-152): stationary_solve reproduces the reference's own
+    _run_stationary -- same number of applications, same stop (tol / > 1e12), and the residual
+    history bit for bit with exact_norms (reference ddot order), to 1e-12 with the fused
+    device-resident norms (C1: gs2(2,1,1) to 1e-6 in 8,872 applications)."""
+    from test_oracle import _stationary_problem
+
+    want = stationary_golden["runs"][label]
+    a = _stationary_problem(label)
+    b = g2.random_rhs(a.nrows, want["seed"])
+    nt, nk, nj = want["cfg"]
+    cfg = g2.RelaxConfig(nt, nk, nj, **want["cfg_kw"])
+    x, h = g2.stationary_solve(a, b, want["kind"], cfg, tol=want["tol"], maxit=want["maxit"], exact_norms=exact)
+    assert h.converged == want["converged"]
+    assert h.iterations == want["applications"]
+    if exact:
+        assert list(np.asarray(h.rel_res)) == want["rel_res"]
+    else:
+        np.testing.assert_allclose(h.rel_res, want["rel_res"], rtol=1e-12)
+    assert isinstance(x, np.ndarray) and x.shape == (a.nrows,)
+
+
+def test_stationary_solve_device_and_rollback():
+    """Device tensors in / out, x0, maxit, and the batch rollback: the iterate returned at the stop is
+    bitwise the one of exactly `applications` single applications (gs2_apply in a loop)."""
+    a = g2.laplace3d(20, device="cuda")
+    b = g2.random_rhs(a.nrows, 0, device="cuda")
+    x0 = g2.random_rhs(a.nrows, 4, device="cuda") * 0.1
+    cfg = g2.RelaxConfig(1, 1, 2)
+    x, h = g2.stationary_solve(a, b, "gs2", cfg, tol=1e-7, x0=x0)
+    assert x.is_cuda and h.converged and h.final_rel_res <= 1e-7
+    s = g2.extract_splitting(a)
+    xr = x0.clone()
+    for _ in range(h.iterations):
+        g2.gs2_apply(a, s, b, xr, cfg)
+    assert torch.equal(x, xr)
+    x2, h2 = g2.stationary_solve(a, b, "gs2", cfg, tol=1e-30, maxit=37)
+    assert h2.iterations == 37 and not h2.converged
+    with pytest.raises(ValueError, match="stationary"):
+        g2.stationary_solve(a, b, "none", cfg)

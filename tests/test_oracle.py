@@ -253,3 +253,66 @@ def test_blas_order_restatement_matches_numpy():
             V = rng.standard_normal((k + 2, n))
             yk = rng.standard_normal(k)
             assert np.array_equal(oracle.gemv_t_rows(V[:k], yk), V[:k].T @ yk), (n, k)
+
+
+def _stationary_problem(label):
+    from paper_2104_01196_b200 import problems
+
+    kind, size = label.split("__")[0].split("_")
+    nx = int(size)
+    return {"lap2d": problems.laplace2d, "lap3d": problems.laplace3d, "ela3d": problems.elasticity3d}[kind](nx)
+
+
+STATIONARY_ORACLE = ["lap2d_32__jr_1", "lap2d_32__jr_2__w0.8", "lap2d_32__gs_seq_1", "lap2d_32__sgs_seq_1",
+                     "lap2d_32__mt_gs_1", "lap2d_32__mt_sgs_2", "lap2d_32__sgs2_1_1_1",
+                     "lap2d_32__gs2_1_2_2__compact_w0.9", "lap3d_12__gs2_1_1_3__gamma0.7_bwd",
+                     "ela3d_6__jr_1__diverges", "ela3d_6__gs2_1_1_3", "lap2d_128__gs2_2_1_1__tol1e-6"]
+
+
+@pytest.mark.parametrize("label", STATIONARY_ORACLE)
+def test_oracle_stationary_histories(label, stationary_golden):
+    """The reference's stand-alone smoother (cli.py:138-152) restated with the oracle's sweeps and
+    its OpenBLAS-order norm: every recorded residual is the reference's, bit for bit."""
+    want = stationary_golden["runs"][label]
+    a = _stationary_problem(label)
+    m = oracle.Matrix(a)
+    b = oracle.random_rhs(a.nrows, want["seed"])
+    nt, nk, nj = want["cfg"]
+    kw = want["cfg_kw"]
+    om = kw.get("omega", 1.0)
+    kind = want["kind"]
+    bn = np.sqrt(oracle.dot(b, b))
+
+    def rel(x):
+        r = b - oracle.spmv(m, x)
+        v = np.sqrt(oracle.dot(r, r)) / bn
+        return v if np.isfinite(v) else np.inf
+
+    def step(x):
+        if kind == "jr":
+            oracle.jr_sweeps(m, b, x, nt * nk, omega=om)
+        elif kind in ("gs_seq", "sgs_seq"):
+            for _ in range(nt * nk):
+                oracle.gs_sweep(m, b, x, "symmetric" if kind == "sgs_seq" else kw.get("direction", "forward"), omega=om)
+        elif kind in ("mt_gs", "mt_sgs"):
+            for _ in range(nt * nk):
+                oracle.mt_gs_sweep(m, b, x, "symmetric" if kind == "mt_sgs" else kw.get("direction", "forward"),
+                                   omega=om)
+        else:
+            d = "symmetric" if kind == "sgs2" else kw.get("direction", "forward")
+            oracle.gs2_apply(m, b, x, n_t=nt, n_k=nk, n_j=nj, direction=d, form=kw.get("form", "non_compact"),
+                             omega=om, gamma=kw.get("gamma", 1.0))
+
+    x = np.zeros(a.nrows)
+    hist = [rel(x)]
+    conv = hist[0] <= want["tol"]
+    for _ in range(want["maxit"]):
+        if conv:
+            break
+        step(x)
+        hist.append(rel(x))
+        if not np.isfinite(hist[-1]) or hist[-1] > 1e12:
+            break
+        conv = hist[-1] <= want["tol"]
+    assert conv == want["converged"]
+    assert hist == want["rel_res"]
