@@ -256,30 +256,59 @@ class _Workspace:
     def __init__(self, n: int, restart: int, device):
         torch = _torch()
         f64 = dict(dtype=torch.float64, device=device)
+        self._guards = []
         self.ldv = n + (n & 1)  # even leading dimension: 16-byte aligned basis rows for the TMA path
-        self.V = torch.empty((restart + 1, self.ldv), **f64)[:, :n]
-        self.w = torch.empty(n, **f64)
-        self.z = torch.empty(n, **f64)
-        self.t = torch.empty(n, **f64)
-        self.r = torch.empty(n, **f64)
+        self.V = self._alloc((restart + 1) * self.ldv, device).view(restart + 1, self.ldv)[:, :n]
+        self.w = self._alloc(n, device)
+        self.z = self._alloc(n, device)
+        self.t = self._alloc(n, device)
+        self.r = self._alloc(n, device)
         lib = N.load()
-        self.work = torch.zeros(int(lib.rs_reduce_work_doubles(max(restart + 2, 1))), **f64)
+        self.work = self._alloc(int(lib.rs_reduce_work_doubles(max(restart + 2, 1))), device, zero=True)
         # packed scalars: [h1 (m+1) | h2 (m+1) | nrm2 | aux]
         self.m1 = restart + 1
-        self.scal = torch.zeros(2 * self.m1 + 4, **f64)
+        self.scal = self._alloc(2 * self.m1 + 4, device, zero=True)
         self.flags = torch.zeros(2, dtype=torch.int64, device=device)  # [nonfinite(int32 in int64 slot), overflow]
-        self.y = torch.empty(restart + 1, **f64)
+        self.y = self._alloc(restart + 1, device)
         self.pinned = torch.empty((2, 2 * self.m1 + 4), dtype=torch.float64, pin_memory=True)
         self.pinned_flags = torch.empty((2, 2), dtype=torch.int64, pin_memory=True)
         # DCGS2: raw Hessenberg (column-major, m+1 rows), dual dots, coefficient block
-        self.H = torch.zeros(restart * self.m1, **f64)
-        self.dots = torch.zeros(2 * self.m1, **f64)
-        self.coef = torch.zeros(_DCGS_COEF, **f64)
+        self.H = self._alloc(restart * self.m1, device, zero=True)
+        self.dots = self._alloc(2 * self.m1, device, zero=True)
+        self.coef = self._alloc(_DCGS_COEF, device, zero=True)
         # per-step record of the Hessenberg column the coefficient kernel writes straight into
         # page-locked host memory (zero-copy; two slots for the one-step-ahead pipeline)
         self.stage = torch.zeros((2, 2 * self.m1 + 8), dtype=torch.float64, pin_memory=True)
         # ||b||^2, ||r||^2 of a deferred GMRES start (read with the first Arnoldi step)
         self.start_pin = torch.zeros(2, dtype=torch.float64, pin_memory=True)
+
+
+    # Guard mode (debug / tests; compute-sanitizer is unavailable on the GPU pool): every device
+    # buffer of the workspace is allocated with GUARD_ELEMS sentinel doubles on each side, and
+    # guards_intact() reports whether any kernel wrote outside its buffer.
+    GUARD_ELEMS = 0
+    _SENTINEL = -0x5EADBEEF0BADF00D  # int64 bit pattern of the guard doubles (a NaN payload)
+
+    def _alloc(self, count: int, device, zero: bool = False):
+        torch = _torch()
+        g = int(_Workspace.GUARD_ELEMS)
+        if g <= 0:
+            return (torch.zeros if zero else torch.empty)(count, dtype=torch.float64, device=device)
+        buf = torch.empty(count + 2 * g, dtype=torch.float64, device=device)
+        buf.view(torch.int64).fill_(_Workspace._SENTINEL)
+        inner = buf[g:g + count]
+        if zero:
+            inner.zero_()
+        self._guards.append((buf, g, count))
+        return inner
+
+    def guards_intact(self) -> bool:
+        for buf, g, count in self._guards:
+            bits = buf.view(_torch().int64)
+            if not (bool((bits[:g] == _Workspace._SENTINEL).all()) and
+                    bool((bits[g + count:] == _Workspace._SENTINEL).all())):
+                return False
+        return True
 
 
 def _p(t):
