@@ -149,10 +149,19 @@ int rs_resid_norm2(rs_matrix_t m, const double *b, const double *x, double *nrm2
  * Bitwise equal to the sequential natural-order sweep. */
 int rs_gs_sweep(rs_matrix_t m, const void *b, void *x, int direction, double omega, rs_stream_t stream);
 
+/* the numba-ABI form of rs_gs_sweep (gs_ordered_sweep, _kernels.py:24-39 called from relax.py:171-174):
+ * omega and one_minus_omega are already rounded to the matrix dtype by the caller and used as given
+ * (for float32, (float)(1 - (double)(float)w) can differ from the caller's _scalar(1 - w)). */
+int rs_gs_sweep_w(rs_matrix_t m, const void *b, void *x, int direction, double omega, double one_minus_omega,
+                  rs_stream_t stream);
+
 /* mt_gs_sweep (coloring.py:66-88): multicolor GS, colors in order (reversed
  * backward), rows of one color in parallel, x in place; bitwise the reference
  * visit of the concatenated color classes. */
 int rs_mt_gs_sweep(rs_matrix_t m, const void *b, void *x, int direction, double omega, rs_stream_t stream);
+/* numba-ABI form (pre-cast omega / one_minus_omega), as rs_gs_sweep_w */
+int rs_mt_gs_sweep_w(rs_matrix_t m, const void *b, void *x, int direction, double omega, double one_minus_omega,
+                     rs_stream_t stream);
 
 /* ---- relaxation (relax.py) ---- */
 

@@ -65,6 +65,8 @@ _SIGS = {
     "rs_spmv_dot": ([_P, _P, _P, _P, _P], C.c_int),
     "rs_resid_norm2": ([_P, _P, _P, _P, _P], C.c_int),
     "rs_gs_sweep": ([_P, _P, _P, C.c_int, C.c_double, _P], C.c_int),
+    "rs_gs_sweep_w": ([_P, _P, _P, C.c_int, C.c_double, C.c_double, _P], C.c_int),
+    "rs_mt_gs_sweep_w": ([_P, _P, _P, C.c_int, C.c_double, C.c_double, _P], C.c_int),
     "rs_jr_sweeps": ([_P, _P, _P, C.c_int, C.c_double, _P], C.c_int),
     "rs_inner_jr": ([_P, _P, _P, C.c_int, C.c_int, C.c_double, C.c_double, _P], C.c_int),
     "rs_gs2_apply": ([_P, _P, _P, C.POINTER(RelaxCfg), _P], C.c_int),

@@ -17,6 +17,7 @@
 //   k_compact    t = b - U x - (1 - 1/w) d x, scaled by D^-1 (compact pass 0).
 //   k_gs_level   one dependency level of the in-place Gauss-Seidel sweep.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 
@@ -1193,14 +1194,16 @@ __global__ void k_mt_first(int64_t cnt, const int32_t* __restrict__ rows, const 
 
 template <typename T>
 static int mt_gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omega, cudaStream_t st,
-                         bool x_zero = false) {
+                         bool x_zero = false, double one_minus_omega = NAN) {
   // the colouring and its ordered slices are built on first use; concurrent callers wait here
   // (enqueue only: the sweeps themselves run concurrently on their streams)
   std::lock_guard<std::mutex> guard(m->build_mu);
   int e;
   if ((e = build_coloring(m))) return e;
   Ctx<T> c(m, st);
-  T w = (T)omega, w1 = (T)(1.0 - omega);
+  // (1 - w) in the working dtype: _scalar(dtype, 1.0 - omega) (relax.py:171-174), or the caller's
+  // pre-cast value (the numba ABI passes omega and one_minus_omega already in the dtype)
+  T w = (T)omega, w1 = std::isnan(one_minus_omega) ? (T)(1.0 - omega) : (T)one_minus_omega;
   const bool damped = w != (T)1.0;
   Levels& lv = m->mt;
   if ((e = build_mt_sell<T>(m, c, st))) return e;
@@ -1366,7 +1369,8 @@ static int gs_cooperative(rs_matrix* m, Levels& lv, Ctx<T>& c, const T* b, T* x,
 }
 
 template <typename T>
-static int gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omega, cudaStream_t st) {
+static int gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omega, cudaStream_t st,
+                      double one_minus_omega = NAN) {
   // level sets, level-ordered slices and their device copies are built on first use
   std::lock_guard<std::mutex> guard(m->build_mu);
   int e;
@@ -1374,7 +1378,9 @@ static int gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omeg
   if ((e = get_scratch(m, st, &scr_))) return e;
   Ctx<T> c(m, st);
   c.scr = (T*)scr_;
-  T w = (T)omega, w1 = (T)(1.0 - omega);
+  // (1 - w) in the working dtype: _scalar(dtype, 1.0 - omega) (relax.py:171-174), or the caller's
+  // pre-cast value (the numba ABI passes omega and one_minus_omega already in the dtype)
+  T w = (T)omega, w1 = std::isnan(one_minus_omega) ? (T)(1.0 - omega) : (T)one_minus_omega;
   bool damped = w != (T)1.0;
   // programmatic dependent launch only BETWEEN this call's kernels: the first kernel reads b (and
   // the first level's rows) before griddepcontrol.wait, so it must not overlap the kernel that
@@ -1848,6 +1854,34 @@ int rs_mt_gs_sweep(rs_matrix_t m, const void* b, void* x, int direction, double 
   cudaStream_t st = (cudaStream_t)stream;
   return m->dtype == RS_F32 ? mt_gs_sweep_t<float>(m, (const float*)b, (float*)x, direction, omega, st)
                             : mt_gs_sweep_t<double>(m, (const double*)b, (double*)x, direction, omega, st);
+}
+
+// the numba-ABI forms (gs_ordered_sweep, _kernels.py:24-39): omega and one_minus_omega arrive
+// already rounded to the matrix dtype (relax.py:171-174) and are used as given
+int rs_gs_sweep_w(rs_matrix_t m, const void* b, void* x, int direction, double omega, double one_minus_omega,
+                  rs_stream_t stream) {
+  RS_SET_DEVICE(m);
+  if (direction < 0 || direction > 2 || std::isnan(one_minus_omega)) {
+    set_error(RS_ERR_ARG, "direction must be forward, backward or symmetric");
+    return RS_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  return m->dtype == RS_F32
+             ? gs_sweep_t<float>(m, (const float*)b, (float*)x, direction, omega, st, one_minus_omega)
+             : gs_sweep_t<double>(m, (const double*)b, (double*)x, direction, omega, st, one_minus_omega);
+}
+
+int rs_mt_gs_sweep_w(rs_matrix_t m, const void* b, void* x, int direction, double omega, double one_minus_omega,
+                     rs_stream_t stream) {
+  RS_SET_DEVICE(m);
+  if (direction < 0 || direction > 2 || std::isnan(one_minus_omega)) {
+    set_error(RS_ERR_ARG, "direction must be forward, backward or symmetric");
+    return RS_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  return m->dtype == RS_F32
+             ? mt_gs_sweep_t<float>(m, (const float*)b, (float*)x, direction, omega, st, false, one_minus_omega)
+             : mt_gs_sweep_t<double>(m, (const double*)b, (double*)x, direction, omega, st, false, one_minus_omega);
 }
 
 int rs_jr_sweeps(rs_matrix_t m, const void* b, void* x, int sweeps, double omega, rs_stream_t stream) {
