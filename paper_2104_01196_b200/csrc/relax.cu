@@ -109,15 +109,10 @@ __global__ void __launch_bounds__(256) k_resid(int64_t n, SellView<T> Elo, SellV
     }
   }
   if (NORM) {
+    // one partial per warp (no block barrier: a CTA's warps retire independently, as in the plain
+    // pass); k_reduce_many sums them in warp order -- deterministic
     for (int o = 16; o; o >>= 1) v2 += __shfl_xor_sync(0xffffffffu, v2, o);
-    __shared__ double red[8];
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v2;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int q = 0; q < 8; ++q) t += red[q];
-      partial[blockIdx.x] = t;
-    }
+    if ((threadIdx.x & 31) == 0) partial[((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5] = v2;
   }
 }
 
@@ -770,7 +765,7 @@ static int two_stage(Ctx<T>& c, const T* b, T* x, int n_j, int backward, int for
       k_resid<T, kJr, true><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x,
                                                        nullptr, nullptr, b, alt, (T)omega, pf_dist_host(), c.norm_red);
       RS_COUNT_LAUNCH();
-      k_reduce_many<<<1, 1024, 0, c.st>>>(c.norm_red, c.grid(), c.norm_out);
+      k_reduce_many<<<1, 1024, 0, c.st>>>(c.norm_red, (int64_t)c.grid() * (kB / 32), c.norm_out);
       c.norm_out = nullptr;
     } else {
       k_resid<T, kJr><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x, nullptr,
@@ -793,7 +788,7 @@ static int two_stage(Ctx<T>& c, const T* b, T* x, int n_j, int backward, int for
       k_resid<T, kResidRd, true><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x,
                                                             nullptr, nullptr, b, rd, (T)0, pf_dist_host(), c.norm_red);
       RS_COUNT_LAUNCH();
-      k_reduce_many<<<1, 1024, 0, c.st>>>(c.norm_red, c.grid(), c.norm_out);
+      k_reduce_many<<<1, 1024, 0, c.st>>>(c.norm_red, (int64_t)c.grid() * (kB / 32), c.norm_out);
       c.norm_out = nullptr;
     } else {
       k_resid<T, kResidRd><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x, nullptr,
@@ -1266,7 +1261,7 @@ static int jr_sweeps_t(rs_matrix* m, const T* b, T* x, int sweeps, double omega,
       k_resid<T, kJr, true><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, cur,
                                                        nullptr, nullptr, b, nxt, w, pf_dist_host(), norm_red);
       RS_COUNT_LAUNCH();
-      k_reduce_many<<<1, 1024, 0, c.st>>>(norm_red, c.grid(), norm_out);
+      k_reduce_many<<<1, 1024, 0, c.st>>>(norm_red, (int64_t)c.grid() * (kB / 32), norm_out);
     } else {
       k_resid<T, kJr><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, cur, nullptr,
                                                  nullptr, b, nxt, w, pf_dist_host());
@@ -2003,7 +1998,7 @@ int rs_stationary_batch(rs_matrix_t m, int kind, const rs_relax_cfg* cfg, const 
   const bool fused = norm2 && m->nrows > 0 && ((gs2 && c.form == RS_NON_COMPACT) || kind == RS_PC_JR);
   double* red = nullptr;
   int e;
-  if (fused && (e = get_reduction(m, st, grid_for(m->nrows, kB), &red))) return e;
+  if (fused && (e = get_reduction(m, st, (int64_t)grid_for(m->nrows, kB) * (kB / 32), &red))) return e;
   if (norm2 && !fused && (e = spmv_red(m, kRedNorm, x, b, nullptr, norm2, stream))) return e;
   for (int k = 0; k < napps; ++k) {
     double* nk = fused ? norm2 + k : nullptr;
