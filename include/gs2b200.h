@@ -230,7 +230,9 @@ int rs_gemv_n_update(const double *V, int64_t ldv, int k, int64_t n, const doubl
  * h_out: h_out = V^T w;  if nrm2: nrm2[0] = w.w.  The CGS2 step of
  * krylov.py:217-220 is rs_cgs_pass(h_out=h1) ; rs_cgs_pass(h_in=h1, h_out=h2) ;
  * rs_cgs_pass(h_in=h2, nrm2).  Falls back to the separate kernels for k > 64
- * or unaligned V / w / odd n. */
+ * or unaligned V / w.  Odd n: w and every basis row must have one readable
+ * element past n (the copies move whole 16-byte units; the extra element is
+ * never used) -- an even ldv provides it for the rows. */
 int rs_cgs_pass(const double *V, int64_t ldv, int k, int64_t n, const double *h_in, double *w, double *h_out,
                 double *nrm2, int *nonfinite, double *work, rs_stream_t stream);
 
@@ -312,7 +314,7 @@ int rs_cast_f32_f64(int64_t n, const float *in, double *out, rs_stream_t stream)
  * With last = 1, rs_dcgs2_coef only finalises column k-2 from out = V^T u (k values,
  * e.g. rs_cgs_pass dots with w = row k-1).  peer != NULL: the sums over ranks run
  * inside the passes (see rs_cgs_pass_peer; flags -> status_out in the update).
- * k <= 64, n even, 16-byte aligned rows. */
+ * k <= 64, even ldv, 16-byte aligned rows (odd n: as rs_cgs_pass). */
 typedef struct rs_peer rs_peer;
 int rs_dcgs2_dots(const double *V, int64_t ldv, int k, int64_t n, const double *w, double *out, int *nonfinite,
                   double *work, rs_peer *peer, uint64_t epoch, rs_stream_t stream);

@@ -540,7 +540,10 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     const int s = c % kCgsStages;
     const int64_t c0 = r0 + (int64_t)c * ch;
     const int len = (int)(r1 - c0 < ch ? r1 - c0 : ch);
-    const uint32_t bytes = (uint32_t)len * 8u;
+    // bulk copies move whole 16-byte units: an odd last chunk (odd n) copies one element past n,
+    // which the caller guarantees is readable (the ldv padding of a basis row; the padded w of
+    // the GMRES workspace) and which no phase below uses (every loop stops at len)
+    const uint32_t bytes = (uint32_t)((len + 1) & ~1) * 8u;
     double* dst = st + (size_t)s * stage_elems;
     if (use_tmap == 2) {
       // one 3-D tensor copy: (256 rows) x (ch/256 row blocks) x (k vectors) -> [k][ch]
@@ -977,7 +980,8 @@ static int cgs_pass(const double* V, int64_t ldv, int k, int64_t n, const double
                     double* urow = nullptr, const CoefArgs* cap = nullptr) {
   const CoefArgs ca = cap ? *cap : CoefArgs();
   rs_stream_t stream = (rs_stream_t)st;
-  const bool aligned = (ldv % 2 == 0) && (n % 2 == 0) && ((uintptr_t)V % 16 == 0) && ((uintptr_t)w % 16 == 0);
+  // odd n: see issue() in k_cgs (w and the basis rows must have one readable element past n)
+  const bool aligned = (ldv % 2 == 0) && ((uintptr_t)V % 16 == 0) && ((uintptr_t)w % 16 == 0);
   if (k > kCgsMaxK || !aligned) {
     // generic path: separate update / dots / norm kernels (+ one peer allreduce launch)
     int e;
@@ -1080,9 +1084,9 @@ __global__ void __launch_bounds__(64) k_dcgs2_coef(int k, const double* __restri
 }  // namespace rs
 
 static bool dcgs_ok(const double* V, int64_t ldv, int k, int64_t n, const double* w, const char* who) {
-  const bool aligned = (ldv % 2 == 0) && (n % 2 == 0) && ((uintptr_t)V % 16 == 0) && (!w || (uintptr_t)w % 16 == 0);
+  const bool aligned = (ldv % 2 == 0) && ((uintptr_t)V % 16 == 0) && (!w || (uintptr_t)w % 16 == 0);
   if (k < 1 || k > kCgsMaxK || n < 0 || !aligned) {
-    set_error(RS_ERR_ARG, std::string(who) + ": needs 1 <= k <= 64 basis vectors, an even row count and "
+    set_error(RS_ERR_ARG, std::string(who) + ": needs 1 <= k <= 64 basis vectors, an even leading dimension and "
                                              "16-byte aligned rows");
     return false;
   }

@@ -259,7 +259,8 @@ class _Workspace:
         self._guards = []
         self.ldv = n + (n & 1)  # even leading dimension: 16-byte aligned basis rows for the TMA path
         self.V = self._alloc((restart + 1) * self.ldv, device).view(restart + 1, self.ldv)[:, :n]
-        self.w = self._alloc(n, device)
+        # w: one readable element past n when n is odd (the fused passes copy whole 16-byte units)
+        self.w = self._alloc(n + (n & 1), device, zero=True)[:n]
         self.z = self._alloc(n, device)
         self.t = self._alloc(n, device)
         self.r = self._alloc(n, device)
@@ -318,14 +319,13 @@ def _p(t):
 def gmres(a, b, m=None, restart: int = 60, tol: float = 1e-9, maxit: int = 10000, x0=None, ortho: str = "auto"):
     """Restarted right-preconditioned GMRES(m) (krylov.py:162-250) on the GPU.
 
-    ``ortho="auto"`` (default): "dcgs2" when restart <= 63 and the row count is
-    even, else "cgs2".
+    ``ortho="auto"`` (default): "dcgs2" when restart <= 63, else "cgs2".
     ``ortho="cgs2"`` (north_star item 4): classical Gram-Schmidt with one
     re-orthogonalisation, three fused passes over the basis per step.
     ``ortho="dcgs2"``: the same CGS2 projections with the re-orthogonalisation
     of v_j delayed into step j+1's first pass (two passes over the basis per
     step instead of three; column j of the Hessenberg is final one step later).
-    Equal to CGS2 in exact arithmetic; restart <= 63, even row count.
+    Equal to CGS2 in exact arithmetic; restart <= 63.
     ``ortho="mgs"``: the reference's modified Gram-Schmidt loop
     (krylov.py:217-219), one fused update+dot launch per basis vector -- the
     reference-faithful mode (same iteration counts where the reference's are
@@ -382,11 +382,11 @@ def _check_ortho(ortho, n, restart):
     """Validate / resolve the orthogonalisation mode ("auto" -> "dcgs2" where it applies)."""
     if ortho not in ("auto", "cgs2", "mgs", "mgs_ref", "dcgs2"):
         raise ValueError(f"ortho must be 'auto', 'cgs2', 'dcgs2', 'mgs' or 'mgs_ref', got {ortho!r}")
-    dcgs_ok = restart <= 63 and n % 2 == 0
+    dcgs_ok = restart <= 63
     if ortho == "auto":
         return "dcgs2" if dcgs_ok else "cgs2"
     if ortho == "dcgs2" and not dcgs_ok:
-        raise ValueError("ortho='dcgs2' needs restart <= 63 and an even number of rows (fused basis passes)")
+        raise ValueError("ortho='dcgs2' needs restart <= 63 (fused basis passes of at most 64 vectors)")
     return ortho
 
 

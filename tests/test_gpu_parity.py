@@ -502,8 +502,6 @@ def test_gmres_dcgs2_mode_counts(label, gmres_golden):
     else:
         a = golden_problem(prob)
         b = g2.random_rhs(a.nrows, 0)
-    if a.nrows % 2:
-        pytest.skip("odd row count")
     pc = g2.Preconditioner(a, kind, g2.RelaxConfig(nt, nk, nj) if kind != "none" else None, precision=prec)
     x, h = g2.gmres(a, b, pc, restart=m, tol=1e-9, ortho="dcgs2")
     assert h.converged == want["converged"]
@@ -533,9 +531,15 @@ def test_gmres_dcgs2_edge_cases():
     assert h0.iterations == 0 or h0.rel_res[0] <= 1e-9
     with pytest.raises(ValueError, match="restart <= 63"):
         g2.gmres(a, b, pc, restart=64, ortho="dcgs2")
-    odd = g2.laplace2d(5)
-    with pytest.raises(ValueError, match="even number of rows"):
-        g2.gmres(odd, g2.random_rhs(odd.nrows, 0), restart=10, ortho="dcgs2")
+    # odd row counts take the fused DCGS2 passes too (one padded element per copied row)
+    for shape in ((5, 5), (15, 15, 15), (33, 31, 29)):
+        odd = g2.laplace2d(*shape) if len(shape) == 2 else g2.laplace3d(*shape)
+        bo = g2.random_rhs(odd.nrows, 0)
+        po = g2.Preconditioner(odd, "gs2", g2.RelaxConfig(1, 1, 1))
+        _, hd = g2.gmres(odd, bo, po, restart=30, tol=1e-9, ortho="dcgs2")
+        _, hc = g2.gmres(odd, bo, po, restart=30, tol=1e-9, ortho="cgs2")
+        ref = oracle.gmres(odd, bo, oracle.Precond(odd, "gs2", n_j=1), restart=30, tol=1e-9)[1]
+        assert hd.converged and hd.iterations == hc.iterations == len(ref) - 1, shape
 
 
 @pytest.mark.slow
