@@ -9,6 +9,7 @@
 // slots, keeping ascending column order and padding with col = -1.
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_reduce.cuh>
+#include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
 #include <atomic>
@@ -532,10 +533,241 @@ static int host_tri(const Sell<T>& s, std::vector<int64_t>& sp, std::vector<int3
   return RS_OK;
 }
 
+// ------------------------------------------------------------------ level sets / colouring on the device
+// The analyses the level-scheduled and multicolour GS baselines need, computed on the GPU for a
+// structurally symmetric pattern (every matrix of the paper's configs): a Kahn wavefront over the
+// dependency DAG (level(i) = 1 + max level of the rows i depends on), a stable radix sort of the
+// rows by level (rows ascending within a level, as the host version), and the greedy colouring
+// level by level (colour(i) = smallest colour not used by a lower neighbour -- the reference's
+// sequential greedy_color, coloring.py:33-63, whose "already coloured" neighbours of row i are
+// exactly its lower neighbours).  Other patterns keep the host algorithms below.
+struct RowsView {
+  const int64_t* sp;
+  const int32_t* col;
+};
+template <typename T>
+static RowsView rows_view(const Sell<T>& s) {
+  return RowsView{s.slice_ptr, s.col};
+}
+
+__device__ __forceinline__ void row_span(const RowsView& v, int64_t i, int64_t& p0, int& w) {
+  const int64_t sl = i >> 5;
+  p0 = v.sp[sl] + (i & 31);
+  w = (int)((v.sp[sl + 1] - v.sp[sl]) >> 5);
+}
+
+// every entry (i, c) of A has (c, i) in B
+__global__ void k_transpose_contained(int64_t n, RowsView A, RowsView B, int* ok) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t p, q;
+  int w, wb;
+  row_span(A, i, p, w);
+  for (int j = 0; j < w; ++j) {
+    const int32_t c = A.col[p + 32 * j];
+    if (c < 0) continue;
+    row_span(B, c, q, wb);
+    bool found = false;
+    for (int k = 0; k < wb && !found; ++k) found = B.col[q + 32 * k] == (int32_t)i;
+    if (!found) atomicExch(ok, 0);
+  }
+}
+
+__global__ void k_row_count(int64_t n, RowsView A, int* deg) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t p;
+  int w, c = 0;
+  row_span(A, i, p, w);
+  for (int j = 0; j < w; ++j) c += A.col[p + 32 * j] >= 0;
+  deg[i] = c;
+}
+
+__global__ void k_level0(int64_t n, const int* deg, int32_t* order, unsigned long long* tail, int32_t* level) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || deg[i]) return;
+  level[i] = 0;
+  order[atomicAdd(tail, 1ull)] = (int32_t)i;
+}
+
+// one wavefront: every successor whose last dependency this level satisfies joins level l
+__global__ void k_level_step(const int32_t* __restrict__ front, int64_t nf, RowsView succ, int* deg, int32_t* order,
+                             unsigned long long* tail, int32_t* level, int32_t l) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nf) return;
+  const int32_t j = front[t];
+  int64_t p;
+  int w;
+  row_span(succ, j, p, w);
+  for (int k = 0; k < w; ++k) {
+    const int32_t s = succ.col[p + 32 * k];
+    if (s >= 0 && atomicSub(&deg[s], 1) == 1) {
+      level[s] = l;
+      order[atomicAdd(tail, 1ull)] = s;
+    }
+  }
+}
+
+// bounds[c] = first position of colour c in the sorted keys (bounds[nc] = n); every colour occurs
+__global__ void k_color_bounds(int64_t n, const int32_t* __restrict__ keys, int64_t* bounds, int64_t nc) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (i == 0) {
+    bounds[0] = 0;
+    bounds[nc] = n;
+  }
+  if (i > 0 && keys[i] != keys[i - 1])
+    for (int32_t c = keys[i - 1] + 1; c <= keys[i]; ++c) bounds[c] = i;
+}
+
+__global__ void k_iota32(int64_t n, int32_t* v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (int32_t)i;
+}
+
+// greedy colour of the rows of one level: smallest colour unused by the row's lower neighbours
+__global__ void k_color_level(const int32_t* __restrict__ rows, int64_t cnt, RowsView lower, int32_t* color) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cnt) return;
+  const int32_t i = rows[t];
+  int64_t p;
+  int w;
+  row_span(lower, i, p, w);
+  unsigned long long used = 0ull;
+  bool big = false;
+  for (int k = 0; k < w; ++k) {
+    const int32_t c = lower.col[p + 32 * k];
+    if (c < 0) continue;
+    const int32_t cc = color[c];
+    if (cc < 64) used |= 1ull << cc;
+    else big = true;
+  }
+  int32_t mex = used == ~0ull ? 64 : __ffsll((long long)~used) - 1;
+  if (big || mex == 64) {  // rare: colours beyond 63 -- test candidates one by one
+    for (mex = 0;; ++mex) {
+      bool taken = false;
+      for (int k = 0; k < w && !taken; ++k) {
+        const int32_t c = lower.col[p + 32 * k];
+        taken = c >= 0 && color[c] == mex;
+      }
+      if (!taken) break;
+    }
+  }
+  color[i] = mex;
+}
+
+// 1 = both triangles are transposes of each other's pattern (fills m->structurally_symmetric)
+template <typename T>
+static int device_symmetry(rs_matrix* m, int* sym) {
+  const int64_t n = m->nrows;
+  int* ok = nullptr;
+  RS_CUDA(cudaMalloc(&ok, sizeof(int)));
+  const int one = 1;
+  RS_CUDA(cudaMemcpy(ok, &one, sizeof(int), cudaMemcpyHostToDevice));
+  if (n) {
+    const RowsView L = rows_view(tri<T>(m, 0)), U = rows_view(tri<T>(m, 1));
+    k_transpose_contained<<<grid_for(n, 256), 256>>>(n, L, U, ok);
+    k_transpose_contained<<<grid_for(n, 256), 256>>>(n, U, L, ok);
+  }
+  int h = 0;
+  RS_CUDA(cudaMemcpy(&h, ok, sizeof(int), cudaMemcpyDeviceToHost));
+  cudaFree(ok);
+  *sym = h;
+  return RS_OK;
+}
+
+// level sets on the device (structurally symmetric pattern); *done = false -> use the host path
+template <typename T>
+static int device_levels(rs_matrix* m, int backward, bool* done) {
+  *done = false;
+  Levels& lv = backward ? m->bwd : m->fwd;
+  const int64_t n = m->nrows;
+  if (n == 0 || n >= INT32_MAX) return RS_OK;
+  int sym = 0;
+  int e;
+  if ((e = device_symmetry<T>(m, &sym))) return e;
+  if (!sym) return RS_OK;
+  m->structurally_symmetric = 1;
+  const RowsView dep = rows_view(tri<T>(m, backward ? 1 : 0));   // rows i depends on
+  const RowsView succ = rows_view(tri<T>(m, backward ? 0 : 1));  // = the rows depending on j
+  int* deg = nullptr;
+  int32_t *order = nullptr, *level = nullptr, *keys = nullptr, *rows = nullptr, *iota = nullptr;
+  unsigned long long* tail = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  int status = RS_OK;
+  std::vector<int64_t> ptr(1, 0);
+  auto fail = [&](cudaError_t err, const char* where) { status = cuda_error(err, where); };
+  cudaError_t ce = cudaSuccess;
+  if ((ce = cudaMalloc(&deg, sizeof(int) * n)) || (ce = cudaMalloc(&order, sizeof(int32_t) * n)) ||
+      (ce = cudaMalloc(&level, sizeof(int32_t) * n)) || (ce = cudaMalloc(&keys, sizeof(int32_t) * n)) ||
+      (ce = cudaMalloc(&rows, sizeof(int32_t) * n)) || (ce = cudaMalloc(&iota, sizeof(int32_t) * n)) ||
+      (ce = cudaMalloc(&tail, sizeof(unsigned long long)))) {
+    fail(ce, "device_levels alloc");
+  } else {
+    const int gb = grid_for(n, 256);
+    k_row_count<<<gb, 256>>>(n, dep, deg);
+    cudaMemset(tail, 0, sizeof(unsigned long long));
+    k_level0<<<gb, 256>>>(n, deg, order, tail, level);
+    unsigned long long t = 0, prev = 0;
+    cudaMemcpy(&t, tail, sizeof(t), cudaMemcpyDeviceToHost);
+    ptr.push_back((int64_t)t);
+    for (int32_t l = 1; t < (unsigned long long)n; ++l) {
+      const int64_t nf = (int64_t)(t - prev);
+      if (nf <= 0) {  // no progress: not a DAG (cannot happen for a strict triangle)
+        set_error(RS_ERR_ARG, "internal: level analysis made no progress");
+        status = RS_ERR_ARG;
+        break;
+      }
+      k_level_step<<<grid_for(nf, 256), 256>>>(order + prev, nf, succ, deg, order, tail, level, l);
+      prev = t;
+      if ((ce = cudaMemcpy(&t, tail, sizeof(t), cudaMemcpyDeviceToHost))) {
+        fail(ce, "device_levels step");
+        break;
+      }
+      ptr.push_back((int64_t)t);
+    }
+    if (status == RS_OK) {
+      // stable sort of the rows by level: rows ascending inside each level
+      int bits = 1;
+      while ((1ll << bits) < (int64_t)ptr.size()) ++bits;
+      k_iota32<<<gb, 256>>>(n, iota);
+      cub::DeviceRadixSort::SortPairs(nullptr, tb, level, keys, iota, rows, (int)n, 0, bits);
+      if ((ce = cudaMalloc(&tmp, std::max<size_t>(tb, 1))) ||
+          (ce = cub::DeviceRadixSort::SortPairs(tmp, tb, level, keys, iota, rows, (int)n, 0, bits)) ||
+          (ce = cudaDeviceSynchronize()))
+        fail(ce, "device_levels sort");
+    }
+  }
+  if (status == RS_OK) {
+    lv.nlevels = (int64_t)ptr.size() - 1;
+    lv.level_ptr_host = (int64_t*)malloc(sizeof(int64_t) * ptr.size());
+    memcpy(lv.level_ptr_host, ptr.data(), sizeof(int64_t) * ptr.size());
+    lv.rows = rows;
+    rows = nullptr;
+    *done = true;
+  }
+  cudaFree(deg);
+  cudaFree(order);
+  cudaFree(level);
+  cudaFree(keys);
+  cudaFree(rows);
+  cudaFree(iota);
+  cudaFree(tail);
+  cudaFree(tmp);
+  return status;
+}
+
 template <typename T>
 int build_levels_t(rs_matrix* m, int backward) {
   Levels& lv = backward ? m->bwd : m->fwd;
   if (lv.rows) return RS_OK;
+  static const bool dev_ok = !getenv("RS_HOST_ANALYSIS") || atoi(getenv("RS_HOST_ANALYSIS")) == 0;
+  if (dev_ok) {
+    bool done = false;
+    const int e = device_levels<T>(m, backward, &done);
+    if (e || done) return e;
+  }
   const Sell<T>& dep = backward ? tri<T>(m, 1) : tri<T>(m, 0);
   const Sell<T>& oth = backward ? tri<T>(m, 0) : tri<T>(m, 1);
   std::vector<int64_t> sp, sp2;
@@ -626,8 +858,88 @@ static int install_coloring(rs_matrix* m, const int64_t* color, int64_t nc) {
 }
 
 template <typename T>
+int build_levels_t(rs_matrix* m, int backward);
+
+// greedy colouring level by level on the device (structurally symmetric pattern)
+template <typename T>
+static int device_coloring(rs_matrix* m, bool* done) {
+  *done = false;
+  const int64_t n = m->nrows;
+  if (n == 0) return RS_OK;
+  int e;
+  if ((e = build_levels_t<T>(m, 0))) return e;
+  if (!m->structurally_symmetric || !m->fwd.rows) return RS_OK;
+  const Levels& lv = m->fwd;
+  const RowsView lower = rows_view(tri<T>(m, 0));
+  int32_t* color = nullptr;
+  RS_CUDA(cudaMalloc(&color, sizeof(int32_t) * n));
+  for (int64_t l = 0; l < lv.nlevels; ++l) {
+    const int64_t lo = lv.level_ptr_host[l], cnt = lv.level_ptr_host[l + 1] - lo;
+    if (cnt) k_color_level<<<grid_for(cnt, 256), 256>>>(lv.rows + lo, cnt, lower, color);
+  }
+  // rows by colour on the device: stable radix sort of (colour, row) -> rows ascending per colour
+  int32_t *keys = nullptr, *iota = nullptr, *rows = nullptr;
+  int64_t* bounds = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  cudaError_t ce = cudaSuccess;
+  std::vector<int32_t> hc(n);
+  int64_t nc = 1;
+  if (!(ce = cudaMemcpy(hc.data(), color, sizeof(int32_t) * n, cudaMemcpyDeviceToHost))) {
+    for (int64_t i = 0; i < n; ++i) nc = std::max<int64_t>(nc, hc[i] + 1);
+    int bits = 1;
+    while ((1ll << bits) < nc) ++bits;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, color, keys, iota, rows, (int)n, 0, bits);
+    if (!(ce = cudaMalloc(&keys, sizeof(int32_t) * n)) && !(ce = cudaMalloc(&iota, sizeof(int32_t) * n)) &&
+        !(ce = cudaMalloc(&rows, sizeof(int32_t) * n)) && !(ce = cudaMalloc(&bounds, sizeof(int64_t) * (nc + 1))) &&
+        !(ce = cudaMalloc(&tmp, std::max<size_t>(tb, 1)))) {
+      k_iota32<<<grid_for(n, 256), 256>>>(n, iota);
+      ce = cub::DeviceRadixSort::SortPairs(tmp, tb, color, keys, iota, rows, (int)n, 0, bits);
+      if (!ce) {
+        k_color_bounds<<<grid_for(n, 256), 256>>>(n, keys, bounds, nc);
+        ce = cudaDeviceSynchronize();
+      }
+    }
+  }
+  int status = ce ? cuda_error(ce, "device_coloring") : RS_OK;
+  if (!status) {
+    Levels& mt = m->mt;
+    free(mt.level_ptr_host);
+    cudaFree(mt.rows);
+    mt = Levels();
+    free_mt_sell(m);
+    mt.nlevels = nc;
+    mt.level_ptr_host = (int64_t*)malloc(sizeof(int64_t) * (nc + 1));
+    if ((ce = cudaMemcpy(mt.level_ptr_host, bounds, sizeof(int64_t) * (nc + 1), cudaMemcpyDeviceToHost))) {
+      status = cuda_error(ce, "device_coloring");
+    } else {
+      mt.rows = rows;
+      rows = nullptr;
+      int64_t* c64 = (int64_t*)malloc(sizeof(int64_t) * n);
+      for (int64_t i = 0; i < n; ++i) c64[i] = hc[i];
+      free(m->color);
+      m->color = c64;
+      *done = true;
+    }
+  }
+  cudaFree(color);
+  cudaFree(keys);
+  cudaFree(iota);
+  cudaFree(rows);
+  cudaFree(bounds);
+  cudaFree(tmp);
+  return status;
+}
+
+template <typename T>
 static int build_coloring_t(rs_matrix* m) {
   if (m->color) return RS_OK;
+  static const bool dev_ok = !getenv("RS_HOST_ANALYSIS") || atoi(getenv("RS_HOST_ANALYSIS")) == 0;
+  if (dev_ok) {
+    bool done = false;
+    const int e = device_coloring<T>(m, &done);
+    if (e || done) return e;
+  }
   const int64_t n = m->nrows;
   std::vector<int64_t> deg(n + 1, 0);
   std::vector<int32_t> adj;

@@ -853,3 +853,36 @@ def test_stationary_solve_device_and_rollback():
     assert h2.iterations == 37 and not h2.converged
     with pytest.raises(ValueError, match="stationary"):
         g2.stationary_solve(a, b, "none", cfg)
+
+
+@pytest.mark.parametrize("gen", ["lap3d_64", "lap2d_200", "ela3d_6", "cd3d_20", "spd_rand"])
+def test_device_analysis_equals_reference_greedy_and_sequential_gs(gen):
+    """The level sets and the greedy colouring are computed on the GPU (Kahn wavefronts + radix sort;
+    colour = smallest colour unused by the lower neighbours, level by level).  The colouring is the
+    reference's sequential greedy_color (coloring.py:33-63, via the oracle) and the level-scheduled
+    sweep the sequential GS, bitwise; a non-symmetric pattern takes the host analysis."""
+    if gen == "spd_rand":
+        rng = np.random.default_rng(9)
+        n = 400
+        d = np.zeros((n, n))
+        idx = rng.integers(0, n, size=(5 * n, 2))
+        d[idx[:, 0], idx[:, 1]] = rng.uniform(-1, 0, 5 * n)
+        d = d + d.T
+        np.fill_diagonal(d, np.abs(d).sum(1) + 1.0)
+        h = g2.from_dense(d)
+    elif gen.startswith("cd3d"):
+        h = g2.convdiff3d(20, (50.0, 25.0, 10.0))
+    else:
+        kind, nx = gen.split("_")
+        h = {"lap3d": g2.laplace3d, "lap2d": g2.laplace2d, "ela3d": g2.elasticity3d}[kind](int(nx))
+    col, nc = oracle.greedy_color(h)
+    c = g2.greedy_color(h)
+    assert c.num_colors == nc and np.array_equal(c.color, col)
+    om = oracle.Matrix(h)
+    b, x0 = g2.random_rhs(h.nrows, 0), g2.random_rhs(h.nrows, 1)
+    s = g2.extract_splitting(h)
+    for d_ in ("forward", "backward", "symmetric"):
+        xg, xo = x0.copy(), x0.copy()
+        g2.gs_sequential_sweep(h, s, b, xg, d_)
+        oracle.gs_sweep(om, b, xo, d_)
+        assert np.array_equal(xg, xo), d_
