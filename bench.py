@@ -556,6 +556,7 @@ def secondary_configs(g2, torch):
         st = {}
         for label, kind, cfg in (("jr(w=1)", "jr", (1, 1, 0)), ("gs2 n_j=1", "gs2", (1, 1, 1)),
                                  ("gs2 n_j=3", "gs2", (1, 1, 3)), ("gs2 n_j=10", "gs2", (1, 1, 10))):
+            g2.stationary_solve(a, b, kind, g2.RelaxConfig(*cfg), tol=1e-300, maxit=2)  # warm-up (buffers)
             (_, h), dt = _timed(torch, lambda: g2.stationary_solve(a, b, kind, g2.RelaxConfig(*cfg), tol=1e-300,
                                                                    maxit=50))
             st[label] = {"applications": h.iterations, "rel_res": h.final_rel_res,
