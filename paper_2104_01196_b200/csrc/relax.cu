@@ -109,11 +109,26 @@ __global__ void __launch_bounds__(256) k_resid(int64_t n, SellView<T> Elo, SellV
     }
   }
   if (NORM) {
-    // one partial per warp (no block barrier: a CTA's warps retire independently, as in the plain
-    // pass); k_reduce_many sums them in warp order -- deterministic
+    // one partial per warp, no block barrier (the warps retire as in the plain pass); the
+    // partials are summed by k_reduce_two (fixed order -- deterministic)
     for (int o = 16; o; o >>= 1) v2 += __shfl_xor_sync(0xffffffffu, v2, o);
     if ((threadIdx.x & 31) == 0) partial[((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5] = v2;
   }
+}
+
+// out = sum of npart partials in fixed order: 1024-element chunks summed by one warp each (tree
+// inside the warp), then the chunk sums by one block -- two short launches instead of one
+// 1024-thread block streaming every partial through a single SM
+__global__ void __launch_bounds__(256) k_reduce_chunks(const double* __restrict__ partial, int64_t npart,
+                                                       double* __restrict__ chunk_out) {
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t lo = c * 1024, hi = lo + 1024 < npart ? lo + 1024 : npart;
+  if (lo >= npart) return;
+  double v = 0.0;
+  for (int64_t q = lo + lane; q < hi; q += 32) v += partial[q];
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) chunk_out[c] = v;
 }
 
 // SpMV fused with the reduction CG takes right after it (krylov.py:289-298), per-block partials:
@@ -179,6 +194,16 @@ __global__ void __launch_bounds__(1024) k_reduce_many(const double* __restrict__
     for (int q = 0; q < 32; ++q) t += red[q];
     *out = t;
   }
+}
+
+// two-level fixed-order sum of npart partials stored at buf[0, npart); buf must hold
+// reduce_two_doubles(npart) doubles (the chunk sums follow the partials)
+static int64_t reduce_two_doubles(int64_t npart) { return npart + (npart + 1023) / 1024 + 1; }
+static void reduce_two(double* buf, int64_t npart, double* out, cudaStream_t st) {
+  const int64_t nchunk = (npart + 1023) / 1024;
+  k_reduce_chunks<<<(int)((nchunk * 32 + 255) / 256), 256, 0, st>>>(buf, npart, buf + npart);
+  RS_COUNT_LAUNCH();  // (the caller counts the second launch)
+  k_reduce_many<<<1, 1024, 0, st>>>(buf + npart, nchunk, out);
 }
 
 // bhat = (b - A_full x) + A_pp x   (relax.py:261-264), y and A_pp x from the same row walk
@@ -765,7 +790,7 @@ static int two_stage(Ctx<T>& c, const T* b, T* x, int n_j, int backward, int for
       k_resid<T, kJr, true><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x,
                                                        nullptr, nullptr, b, alt, (T)omega, pf_dist_host(), c.norm_red);
       RS_COUNT_LAUNCH();
-      k_reduce_many<<<1, 1024, 0, c.st>>>(c.norm_red, (int64_t)c.grid() * (kB / 32), c.norm_out);
+      reduce_two(c.norm_red, (int64_t)c.grid() * (kB / 32), c.norm_out, c.st);
       c.norm_out = nullptr;
     } else {
       k_resid<T, kJr><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x, nullptr,
@@ -788,7 +813,7 @@ static int two_stage(Ctx<T>& c, const T* b, T* x, int n_j, int backward, int for
       k_resid<T, kResidRd, true><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x,
                                                             nullptr, nullptr, b, rd, (T)0, pf_dist_host(), c.norm_red);
       RS_COUNT_LAUNCH();
-      k_reduce_many<<<1, 1024, 0, c.st>>>(c.norm_red, (int64_t)c.grid() * (kB / 32), c.norm_out);
+      reduce_two(c.norm_red, (int64_t)c.grid() * (kB / 32), c.norm_out, c.st);
       c.norm_out = nullptr;
     } else {
       k_resid<T, kResidRd><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x, nullptr,
@@ -1261,7 +1286,7 @@ static int jr_sweeps_t(rs_matrix* m, const T* b, T* x, int sweeps, double omega,
       k_resid<T, kJr, true><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, cur,
                                                        nullptr, nullptr, b, nxt, w, pf_dist_host(), norm_red);
       RS_COUNT_LAUNCH();
-      k_reduce_many<<<1, 1024, 0, c.st>>>(norm_red, (int64_t)c.grid() * (kB / 32), norm_out);
+      reduce_two(norm_red, (int64_t)c.grid() * (kB / 32), norm_out, c.st);
     } else {
       k_resid<T, kJr><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, cur, nullptr,
                                                  nullptr, b, nxt, w, pf_dist_host());
@@ -1998,7 +2023,8 @@ int rs_stationary_batch(rs_matrix_t m, int kind, const rs_relax_cfg* cfg, const 
   const bool fused = norm2 && m->nrows > 0 && ((gs2 && c.form == RS_NON_COMPACT) || kind == RS_PC_JR);
   double* red = nullptr;
   int e;
-  if (fused && (e = get_reduction(m, st, (int64_t)grid_for(m->nrows, kB) * (kB / 32), &red))) return e;
+  if (fused && (e = get_reduction(m, st, reduce_two_doubles((int64_t)grid_for(m->nrows, kB) * (kB / 32)), &red)))
+    return e;
   if (norm2 && !fused && (e = spmv_red(m, kRedNorm, x, b, nullptr, norm2, stream))) return e;
   for (int k = 0; k < napps; ++k) {
     double* nk = fused ? norm2 + k : nullptr;

@@ -48,14 +48,18 @@ c = N.RelaxCfg.of(cfg)
 dm = a
 
 
-def batch(with_norms):
-    N.check(lib.rs_stationary_batch(dm.handle, N.PC_KINDS["gs2"], C.byref(c), C.c_void_p(b.data_ptr()),
+def batch(with_norms, kind="gs2", cc=None):
+    N.check(lib.rs_stationary_batch(dm.handle, N.PC_KINDS[kind], C.byref(cc or c), C.c_void_p(b.data_ptr()),
                                     C.c_void_p(x.data_ptr()), K,
                                     C.c_void_p(norms.data_ptr()) if with_norms else None, stream_ptr(0)))
 
 
 out["batch_no_norms_ms"] = round(wall(lambda: batch(False)), 4)
 out["batch_fused_norms_ms"] = round(wall(lambda: batch(True)), 4)
+out["batch_no_norms_ms_again"] = round(wall(lambda: batch(False)), 4)
+cj = N.RelaxCfg.of(g2.RelaxConfig(1, 1, 0))
+out["jr_batch_no_norms_ms"] = round(wall(lambda: batch(False, "jr", cj)), 4)
+out["jr_batch_fused_norms_ms"] = round(wall(lambda: batch(True, "jr", cj)), 4)
 out["stationary_solve_ms"] = round(wall(lambda: g2.stationary_solve(a, b, "gs2", cfg, tol=1e-300, maxit=K, x0=x0)), 4)
 out["stationary_jr_ms"] = round(wall(lambda: g2.stationary_solve(a, b, "jr", g2.RelaxConfig(1, 1, 0), tol=1e-300,
                                                                  maxit=K, x0=x0)), 4)
