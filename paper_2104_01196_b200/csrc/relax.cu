@@ -64,11 +64,13 @@ struct Halo {
 // NORM (kResidRd / kJr): also the block's partial of ||b - A x||^2 into partial[blockIdx.x] -- the
 // stand-alone smoother's residual history (cli.py:140-152) taken from the residual pass the next
 // application computes anyway, instead of an extra SpMV + norm.
-template <typename T, int MODE, bool NORM = false>
+// B: the type b is stored in (double b with T = float: the fp32 preconditioner's right-hand side
+// cast on the fly, (float)b[i] = cast_vector's rounding, sparse.py:244-257)
+template <typename T, int MODE, bool NORM = false, typename B = T>
 __global__ void __launch_bounds__(256) k_resid(int64_t n, SellView<T> Elo, SellView<T> L, SellView<T> U,
                                                SellView<T> Ehi, const T* __restrict__ d, const T* __restrict__ x,
                                                const T* __restrict__ xlo, const T* __restrict__ xhi,
-                                               const T* __restrict__ b, T* __restrict__ out, T w, int pf,
+                                               const B* __restrict__ b, T* __restrict__ out, T w, int pf,
                                                double* __restrict__ partial = nullptr) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (pf && i + pf < n) {
@@ -78,7 +80,7 @@ __global__ void __launch_bounds__(256) k_resid(int64_t n, SellView<T> Elo, SellV
     q -= pf_sell<T>(U, s2, q);
     q -= pf_vec<T>(d, s2, q);
     q -= pf_vec<T>(x, s2, q);
-    if (MODE != kSpmv) q -= pf_vec<T>(b, s2, q);
+    if (MODE != kSpmv) q -= pf_vec<B>(b, s2, q);
   }
   if (!NORM && i >= n) return;
   double v2 = 0.0;
@@ -98,11 +100,11 @@ __global__ void __launch_bounds__(256) k_resid(int64_t n, SellView<T> Elo, SellV
     if (MODE == kSpmv) {
       out[i] = acc;
     } else if (MODE == kResidRd) {
-      const T r = sub_rn<T>(b[i], acc);
+      const T r = sub_rn<T>((T)b[i], acc);
       out[i] = div_rn<T>(r, di);
       if (NORM) v2 = (double)r * (double)r;
     } else if (MODE == kJr) {
-      const T r = sub_rn<T>(b[i], acc);
+      const T r = sub_rn<T>((T)b[i], acc);
       T g = div_rn<T>(r, di);
       out[i] = add_rn<T>(xi, mul_rn<T>(w, g));
       if (NORM) v2 = (double)r * (double)r;
@@ -434,10 +436,12 @@ __global__ void k_scale_rd_f32x2(int64_t n, const double* __restrict__ r, const 
 enum InnerFinal { kNotFinal = 0, kFinalAdd = 1, kFinalSet = 2 };
 
 // one inner JR step: gout = rd - w*(D^-1T gin)  or damped; last step updates x
-template <typename T, int FINAL, bool GAMMA>
+// O / xout: kFinalAdd writes (O)(x + w g) to xout instead of x (the fp32 preconditioner's last
+// step producing the float64 z directly)
+template <typename T, int FINAL, bool GAMMA, typename O = T>
 __global__ void __launch_bounds__(256) k_inner(int64_t n, SellView<T> Tm, const T* __restrict__ rd,
                                                const T* __restrict__ gin, T* __restrict__ gout, T* __restrict__ x,
-                                               T w, T gm, T gm1, int pf) {
+                                               T w, T gm, T gm1, int pf, O* __restrict__ xout = nullptr) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (pf && i + pf < n) {
     const int64_t s2 = (i + pf) >> 5;
@@ -459,8 +463,13 @@ __global__ void __launch_bounds__(256) k_inner(int64_t n, SellView<T> Tm, const 
   T g = sub_rn<T>(rdi, mul_rn<T>(w, t));
   if (GAMMA) g = add_rn<T>(mul_rn<T>(gm1, gi), mul_rn<T>(gm, g));
   if (FINAL == kNotFinal) gout[i] = g;
-  else if (FINAL == kFinalAdd) x[i] = add_rn<T>(xi0, mul_rn<T>(w, g));
-  else x[i] = mul_rn<T>(w, g);
+  else if (FINAL == kFinalAdd) {
+    const T xn = add_rn<T>(xi0, mul_rn<T>(w, g));
+    if (xout) xout[i] = (O)xn;
+    else x[i] = xn;
+  } else {
+    x[i] = mul_rn<T>(w, g);
+  }
 }
 
 // n_j == 0 update: x = x + w*rd (non-compact) or x = w*rd (compact)
@@ -713,6 +722,155 @@ static SellView<T> none_view() {
   return v;
 }
 
+// ---- TMA-staged full-row passes (SpMV, GS2 pass 0, JR; uniform-width triangles, no off-block
+// couplings): one CTA per tile of kTmaRows rows; one thread bulk-copies the tile's column / value
+// slices of L and U (contiguous: slice s starts at 32*uw*s) into shared memory on one mbarrier
+// while the threads load their rows' own operands; the rows are then walked out of shared memory
+// and only the x gathers go to global memory.  Same per-row order and roundings as k_resid
+// (bitwise).  Fewer instructions per byte than the LDG walk: standalone 3% slower (0.242 vs
+// 0.235 ms SpMV at 256^3), but inside the power-capped GMRES cycle the SpMV group drops from
+// 17.7-18.0 to 15.7-15.8 ms per cycle (profiles/ab/r02_tma_rows.txt); RS_ROWS_TMA=0 switches it off.
+constexpr int kTmaRows = 512;
+constexpr int kTmaThreads = 256;
+
+static bool rows_tma_enabled() {
+  static const bool on = !getenv("RS_ROWS_TMA") || atoi(getenv("RS_ROWS_TMA")) != 0;
+  return on;
+}
+
+// the tile's slices [s0, s0 + ns) of a uniform triangle into shared memory (issued by one thread)
+template <typename T>
+__device__ __forceinline__ uint32_t tma_tri(const int32_t* col, const T* val, int uw, int64_t s0, int ns,
+                                            int32_t* scol, T* sval, uint64_t* bar) {
+  const uint32_t cb = (uint32_t)(32 * uw * ns) * 4u, vb = (uint32_t)(32 * uw * ns) * (uint32_t)sizeof(T);
+  if (cb) {
+    bulk_g2s(scol, col + s0 * 32 * uw, cb, bar);
+    bulk_g2s(sval, val + s0 * 32 * uw, vb, bar);
+  }
+  return cb + vb;
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t tma_tri_bytes(int uw, int ns) {
+  return (uint32_t)(32 * uw * ns) * (4u + (uint32_t)sizeof(T));
+}
+
+// acc += sum over the row's slots (shared-memory slice) of v * x[c], ascending (row_accum's order)
+template <typename T>
+__device__ __forceinline__ T smem_row_accum(const int32_t* lc, const T* lv, int uw, const T* __restrict__ x, T acc) {
+  for (int j0 = 0; j0 < uw; j0 += kBatch) {
+    int32_t c[kBatch];
+    T v[kBatch], xv[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const bool ok = j0 + u < uw;
+      c[u] = ok ? lc[32 * (j0 + u)] : -1;
+      v[u] = ok ? lv[32 * (j0 + u)] : (T)0;
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) xv[u] = c[u] >= 0 ? x[c[u]] : (T)0;
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u)
+      if (c[u] >= 0) acc = add_rn<T>(acc, mul_rn<T>(v[u], xv[u]));
+  }
+  return acc;
+}
+
+// k_resid with both triangles staged through shared memory; MODE as k_resid
+template <typename T, int MODE>
+__global__ void __launch_bounds__(kTmaThreads) k_resid_tma(int64_t n, const int32_t* __restrict__ Lc,
+                                                           const T* __restrict__ Lv, int wl,
+                                                           const int32_t* __restrict__ Uc,
+                                                           const T* __restrict__ Uv, int wu,
+                                                           const T* __restrict__ d, const T* __restrict__ x,
+                                                           const T* __restrict__ b, T* __restrict__ out, T w) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ __align__(8) uint64_t bar;
+  const int64_t r0 = (int64_t)blockIdx.x * kTmaRows;
+  // slices [s0, s0 + ns) of each triangle; the arrays hold whole slices, so the copy of a partial
+  // last tile stays inside them
+  const int64_t nsl = (n + 31) >> 5, s0 = r0 >> 5;
+  const int ns = (int)(nsl - s0 < kTmaRows / 32 ? nsl - s0 : kTmaRows / 32);
+  T* sLv = reinterpret_cast<T*>(sm);
+  T* sUv = sLv + (size_t)32 * wl * (kTmaRows / 32);
+  int32_t* sLc = reinterpret_cast<int32_t*>(sUv + (size_t)32 * wu * (kTmaRows / 32));
+  int32_t* sUc = sLc + (size_t)32 * wl * (kTmaRows / 32);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(&bar, tma_tri_bytes<T>(wl, ns) + tma_tri_bytes<T>(wu, ns));
+    tma_tri<T>(Lc, Lv, wl, s0, ns, sLc, sLv, &bar);
+    tma_tri<T>(Uc, Uv, wu, s0, ns, sUc, sUv, &bar);
+  }
+  // the rows' own operands while the slices arrive
+  constexpr int kRpt = kTmaRows / kTmaThreads;
+  T di[kRpt], xi[kRpt], bi[kRpt];
+#pragma unroll
+  for (int q = 0; q < kRpt; ++q) {
+    const int64_t i = r0 + threadIdx.x + q * kTmaThreads;
+    di[q] = i < n ? d[i] : (T)1;
+    xi[q] = i < n ? x[i] : (T)0;
+    bi[q] = (MODE != kSpmv && i < n) ? b[i] : (T)0;
+  }
+  mbar_wait(&bar, 0);
+#pragma unroll
+  for (int q = 0; q < kRpt; ++q) {
+    const int t = threadIdx.x + q * kTmaThreads;  // row within the tile
+    const int64_t i = r0 + t;
+    if (i >= n) continue;
+    const int sl = t >> 5, lane = t & 31;
+    T acc = smem_row_accum<T>(sLc + 32 * wl * sl + lane, sLv + 32 * wl * sl + lane, wl, x, (T)0);
+    acc = add_rn<T>(acc, mul_rn<T>(di[q], xi[q]));
+    acc = smem_row_accum<T>(sUc + 32 * wu * sl + lane, sUv + 32 * wu * sl + lane, wu, x, acc);
+    if (MODE == kSpmv) {
+      out[i] = acc;
+    } else if (MODE == kResidRd) {
+      out[i] = div_rn<T>(sub_rn<T>(bi[q], acc), di[q]);
+    } else if (MODE == kJr) {
+      const T g = div_rn<T>(sub_rn<T>(bi[q], acc), di[q]);
+      out[i] = add_rn<T>(xi[q], mul_rn<T>(w, g));
+    }
+  }
+}
+
+// 0 = not applicable (non-uniform slices, couplings, RS_RESID_TMA=0)
+template <typename T>
+static size_t resid_tma_smem(rs_matrix* m) {
+  const bool on = rows_tma_enabled();
+  const Sell<T>& L = tri<T>(m, 0);
+  const Sell<T>& U = tri<T>(m, 1);
+  if (!on || L.uw < 0 || U.uw < 0 || tri<T>(m, 2).nslots || tri<T>(m, 3).nslots) return 0;
+  const size_t sz = (size_t)kTmaRows * (L.uw + U.uw) * (sizeof(T) + 4);
+  return sz <= 200 * 1024 ? sz : 0;
+}
+
+template <typename T, int MODE>
+static bool launch_resid_tma(rs_matrix* m, const T* x, const T* b, T* out, T w, cudaStream_t st) {
+  const size_t smem = resid_tma_smem<T>(m);
+  if (!smem || m->nrows == 0) return false;
+  const Sell<T>& L = tri<T>(m, 0);
+  const Sell<T>& U = tri<T>(m, 1);
+  static std::atomic<bool> attr[kMaxDevices];
+  if (m->device >= kMaxDevices || !attr[m->device].load(std::memory_order_acquire)) {
+    cudaFuncSetAttribute(k_resid_tma<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (m->device < kMaxDevices) attr[m->device].store(true, std::memory_order_release);
+  }
+  k_resid_tma<T, MODE><<<grid_for(m->nrows, kTmaRows), kTmaThreads, smem, st>>>(
+      m->nrows, L.col, L.val, L.uw, U.col, U.val, U.uw, (const T*)m->d, x, b, out, w);
+  return true;  // (the caller counts the launch)
+}
+
+// one inner step (a TMA-staged variant of this single-triangle pass measured slower inside the
+// cycle: +0.65 ms per GMRES(60) cycle at 256^3, profiles/ab/r02_tma_rows.txt)
+template <typename T, int FINAL, bool GAMMA>
+static void launch_inner(Ctx<T>& c, int backward, const T* rd, const T* gin, T* gout, T* x, T w, T gm, T gm1) {
+  SellView<T> Tm = backward ? c.Usc : c.Lsc;
+  k_inner<T, FINAL, GAMMA><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1, pf_dist_host());
+}
+
 // One inner JR chain from rd; the last step updates x (non-compact add / compact set).
 template <typename T>
 static int inner_chain(Ctx<T>& c, T* rd, T* ga, T* gb, T* x, int n_j, int backward, double omega, double gamma,
@@ -742,29 +900,29 @@ static int inner_chain(Ctx<T>& c, T* rd, T* ga, T* gb, T* x, int n_j, int backwa
     T* gout = bufs[j & 1];
     if (!last) {
       if (damped) {
-        k_inner<T, kNotFinal, true><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1, pf_dist_host());
+        launch_inner<T, kNotFinal, true>(c, backward, rd, gin, gout, x, w, gm, gm1);
         RS_COUNT_LAUNCH();
       }
       else {
-        k_inner<T, kNotFinal, false><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1, pf_dist_host());
+        launch_inner<T, kNotFinal, false>(c, backward, rd, gin, gout, x, w, gm, gm1);
         RS_COUNT_LAUNCH();
       }
     } else if (compact) {
       if (damped) {
-        k_inner<T, kFinalSet, true><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1, pf_dist_host());
+        launch_inner<T, kFinalSet, true>(c, backward, rd, gin, gout, x, w, gm, gm1);
         RS_COUNT_LAUNCH();
       }
       else {
-        k_inner<T, kFinalSet, false><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1, pf_dist_host());
+        launch_inner<T, kFinalSet, false>(c, backward, rd, gin, gout, x, w, gm, gm1);
         RS_COUNT_LAUNCH();
       }
     } else {
       if (damped) {
-        k_inner<T, kFinalAdd, true><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1, pf_dist_host());
+        launch_inner<T, kFinalAdd, true>(c, backward, rd, gin, gout, x, w, gm, gm1);
         RS_COUNT_LAUNCH();
       }
       else {
-        k_inner<T, kFinalAdd, false><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1, pf_dist_host());
+        launch_inner<T, kFinalAdd, false>(c, backward, rd, gin, gout, x, w, gm, gm1);
         RS_COUNT_LAUNCH();
       }
     }
@@ -792,7 +950,7 @@ static int two_stage(Ctx<T>& c, const T* b, T* x, int n_j, int backward, int for
       RS_COUNT_LAUNCH();
       reduce_two(c.norm_red, (int64_t)c.grid() * (kB / 32), c.norm_out, c.st);
       c.norm_out = nullptr;
-    } else {
+    } else if (!launch_resid_tma<T, kJr>(c.m, x, b, alt, (T)omega, c.st)) {
       k_resid<T, kJr><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x, nullptr,
                                                  nullptr, b, alt, (T)omega, pf_dist_host());
     }
@@ -815,7 +973,7 @@ static int two_stage(Ctx<T>& c, const T* b, T* x, int n_j, int backward, int for
       RS_COUNT_LAUNCH();
       reduce_two(c.norm_red, (int64_t)c.grid() * (kB / 32), c.norm_out, c.st);
       c.norm_out = nullptr;
-    } else {
+    } else if (!launch_resid_tma<T, kResidRd>(c.m, x, b, rd, (T)0, c.st)) {
       k_resid<T, kResidRd><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x, nullptr,
                                                        nullptr, b, rd, (T)0, pf_dist_host());
     }
@@ -1287,7 +1445,7 @@ static int jr_sweeps_t(rs_matrix* m, const T* b, T* x, int sweeps, double omega,
                                                        nullptr, nullptr, b, nxt, w, pf_dist_host(), norm_red);
       RS_COUNT_LAUNCH();
       reduce_two(norm_red, (int64_t)c.grid() * (kB / 32), norm_out, c.st);
-    } else {
+    } else if (!launch_resid_tma<T, kJr>(c.m, cur, b, nxt, w, c.st)) {
       k_resid<T, kJr><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, cur, nullptr,
                                                  nullptr, b, nxt, w, pf_dist_host());
     }
@@ -1609,7 +1767,9 @@ static int spmv_t(rs_matrix* m, const T* x, const T* xlo, const T* xhi, T* y, cu
     return RS_ERR_ARG;
   }
   if (c.n) {
-    k_resid<T, kSpmv><<<c.grid(), kB, 0, st>>>(c.n, c.Elo, c.L, c.U, c.Ehi, c.d, x, xlo, xhi, nullptr, y, (T)0, pf_dist_host());
+    if (!launch_resid_tma<T, kSpmv>(m, x, (const T*)nullptr, y, (T)0, st))
+      k_resid<T, kSpmv><<<c.grid(), kB, 0, st>>>(c.n, c.Elo, c.L, c.U, c.Ehi, c.d, x, xlo, xhi, (const T*)nullptr, y,
+                                                 (T)0, pf_dist_host());
     RS_COUNT_LAUNCH();
   }
   RS_CHECK_LAUNCH("spmv");
@@ -1735,6 +1895,66 @@ static int precond_gs2_single(rs_matrix* m, const rs_relax_cfg& cfg, const R* r,
   }
   RS_CHECK_LAUNCH("precond");
   return RS_OK;
+}
+
+// single_inside_double for one SYMMETRIC GS2 sweep (kind sgs2, or gs2 with direction symmetric;
+// n_t = n_k = 1, n_j >= 1, non-compact) without the separate cast passes of the generic path:
+//   forward half from z = 0: precond_gs2_single with the r cast (and overflow check) fused into
+//   its first pass, writing the float32 iterate x32;
+//   backward half: rd = ((float)r - A x32) / d (k_resid reading r as double), n_j inner steps on
+//   D^-1 U, the last one writing z = (double)(x32 + w g).
+// Same operations and roundings as cast_vector -> gs2_apply(float32) -> astype(float64)
+// (krylov.py:116-118, 135-136, relax.py:193-220).
+static int precond_sgs2_f32(rs_matrix* m, const rs_relax_cfg& cfg, const double* r, double* z, long long* overflow,
+                            cudaStream_t st) {
+  Ctx<float> c(m, st);
+  if (!c.n) return RS_OK;
+  void* s_ = nullptr;
+  int e = get_scratch(m, st, &s_);
+  if (e) return e;
+  c.scr = (float*)s_;
+  float* x32 = c.scr + 4 * c.n;  // the generic path's rhs slot (precond_gs2_single uses [0, 3n))
+  rs_relax_cfg fwd = cfg;
+  fwd.direction = RS_FORWARD;
+  if ((e = precond_gs2_single<float, double, float>(m, fwd, r, x32, overflow, st))) return e;
+  float* rd = c.scr;
+  float* bufs[2] = {rd + c.n, rd + 2 * c.n};
+  const float w = (float)cfg.omega, gm = (float)cfg.gamma, gm1 = (float)(1.0 - cfg.gamma);
+  const bool damped = cfg.gamma != 1.0;
+  k_resid<float, kResidRd, false, double><<<c.grid(), kB, 0, st>>>(c.n, none_view<float>(), c.L, c.U,
+                                                                   none_view<float>(), c.d, x32, nullptr, nullptr, r,
+                                                                   rd, 0.0f, pf_dist_host());
+  RS_COUNT_LAUNCH();
+  const float* gin = rd;
+  for (int j = 0; j < cfg.n_j; ++j) {
+    const bool last = j == cfg.n_j - 1;
+    float* gout = bufs[j & 1];
+    if (last) {
+      if (damped)
+        k_inner<float, kFinalAdd, true, double><<<c.grid(), kB, 0, st>>>(c.n, c.Usc, rd, gin, gout, x32, w, gm, gm1,
+                                                                         pf_dist_host(), z);
+      else
+        k_inner<float, kFinalAdd, false, double><<<c.grid(), kB, 0, st>>>(c.n, c.Usc, rd, gin, gout, x32, w, gm, gm1,
+                                                                          pf_dist_host(), z);
+    } else {
+      if (damped)
+        k_inner<float, kNotFinal, true><<<c.grid(), kB, 0, st>>>(c.n, c.Usc, rd, gin, gout, nullptr, w, gm, gm1,
+                                                                  pf_dist_host());
+      else
+        k_inner<float, kNotFinal, false><<<c.grid(), kB, 0, st>>>(c.n, c.Usc, rd, gin, gout, nullptr, w, gm, gm1,
+                                                                   pf_dist_host());
+      gin = gout;
+    }
+    RS_COUNT_LAUNCH();
+  }
+  RS_CHECK_LAUNCH("precond");
+  return RS_OK;
+}
+
+static bool symmetric_f32_fused(int kind, const rs_relax_cfg& cfg) {
+  static const bool unfused = getenv("RS_PRECOND_UNFUSED") && atoi(getenv("RS_PRECOND_UNFUSED")) != 0;
+  return !unfused && (kind == RS_PC_SGS2 || (kind == RS_PC_GS2 && cfg.direction == RS_SYMMETRIC)) &&
+         cfg.n_t * cfg.n_k == 1 && cfg.n_j >= 1 && cfg.form == RS_NON_COMPACT;
 }
 
 static bool single_half_sweep(int kind, const rs_relax_cfg& cfg) {
@@ -1978,6 +2198,7 @@ int rs_precond_apply(rs_matrix_t m, int kind, const rs_relax_cfg* cfg, const dou
     if (cfg->n_j == 0) return precond_gs2_single<double, double, double>(m, *cfg, r, z, nullptr, st);
   }
   if (m->dtype == RS_F64) return precond_body<double>(m, kind, *cfg, r, z, st);
+  if (symmetric_f32_fused(kind, *cfg)) return precond_sgs2_f32(m, *cfg, r, z, (long long*)overflow_flag, st);
   // single_inside_double (krylov.py:116-118, 135-136): cast r, relax in float32, upcast z
   float* rhs = (float*)scr_ + 4 * m->nrows;
   float* zw = (float*)scr_ + 5 * m->nrows;

@@ -876,6 +876,9 @@ def cg(a, b, m=None, tol: float = 1e-9, maxit: int = 10000, x0=None):
     xs = (x, torch.empty_like(x))  # x ping-pong: a speculative iteration never overwrites the answer
     stage = torch.full((2, 3), -1.0, dtype=torch.float64, pin_memory=True)
     fp32 = op is not None and getattr(op, "precision", "same") == "single_inside_double"
+    # overflow index of the fp32 preconditioner (INT64_MAX: none), copied per iteration slot; the
+    # device flag is never reset inside the loop -- the first overflow raises
+    stage_ovf = torch.full((2,), _I64_MAX, dtype=torch.int64, pin_memory=True)
 
     def enqueue(k):
         """CG iteration k entirely on the device (krylov.py:288-308), scalars staged to pinned slot k%2."""
@@ -884,13 +887,10 @@ def cg(a, b, m=None, tol: float = 1e-9, maxit: int = 10000, x0=None):
         chk(lib.rs_spmv_dot(dm.handle, _p(p), _p(ap), _p(pap_s), st), "spmv_dot")
         chk(lib.rs_cg_update(n, _p(rz_s[k % 2]), _p(pap_s), _p(xin), _p(p), _p(xout), _p(r), _p(ap), st), "cg")
         chk(lib.rs_resid_norm2(dm.handle, _p(bt), _p(xout), _p(res_s), st), "resid_norm2")
-        if fp32:
-            _WS.flags[1] = _I64_MAX
         _apply_op(op, r, z, _WS)
         stage[k % 2, 0:2].copy_(ds[0:2], non_blocking=True)
-        if fp32:  # overflowing entry index (INT64_MAX: none), exact in a double below 2^53
-            stage[k % 2, 2:3].copy_(torch.where(_WS.flags[1:2] == _I64_MAX, -1, _WS.flags[1:2]).to(torch.float64),
-                                    non_blocking=True)
+        if fp32:
+            stage_ovf[k % 2:k % 2 + 1].copy_(_WS.flags[1:2], non_blocking=True)
         chk(lib.rs_dot(n, _p(r), _p(z), _p(rz_s[(k + 1) % 2]), _p(work), st), "dot")
         chk(lib.rs_xpby_dev(n, _p(z), _p(rz_s[(k + 1) % 2]), _p(rz_s[k % 2]), _p(p), st), "xpby")
         ev = torch.cuda.Event()
@@ -906,7 +906,8 @@ def cg(a, b, m=None, tol: float = 1e-9, maxit: int = 10000, x0=None):
         ev = ev_next
         ev_next = enqueue(k + 1) if k + 1 < maxit else None
         ev.synchronize()
-        pap, res2, ovf = (float(v) for v in stage[k % 2])
+        pap, res2, _ = (float(v) for v in stage[k % 2])
+        ovf = int(stage_ovf[k % 2])
         if not math.isfinite(pap):
             raise DivergenceError("non-finite curvature in CG")
         if pap <= 0.0:
@@ -919,8 +920,8 @@ def cg(a, b, m=None, tol: float = 1e-9, maxit: int = 10000, x0=None):
         if true_rel <= tol:
             converged = True
             break
-        if ovf >= 0:
-            raise OverflowError(f"entry {int(ovf)} overflows single precision")
+        if ovf != _I64_MAX:
+            raise OverflowError(f"entry {ovf} overflows single precision")
     if k_last >= 0:
         x = xs[(k_last + 1) % 2]
     return finish(x, hist, converged)

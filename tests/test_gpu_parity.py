@@ -886,3 +886,26 @@ def test_device_analysis_equals_reference_greedy_and_sequential_gs(gen):
         g2.gs_sequential_sweep(h, s, b, xg, d_)
         oracle.gs_sweep(om, b, xo, d_)
         assert np.array_equal(xg, xo), d_
+
+
+@pytest.mark.parametrize("gen", ["lap3d_17", "ela3d_5", "cd3d_12", "lap2d_64"])
+def test_fp32_symmetric_preconditioner_fused_bitwise(gen):
+    """single_inside_double with one symmetric GS2 sweep (sgs2(1,1,n_j); the paper's fp32 SGS2,
+    PAPER.md:1308-1321) runs without separate cast passes (r cast fused into the forward half, z
+    upcast fused into the backward half's last step): bitwise the reference arithmetic (oracle)."""
+    kind, nx = gen.split("_")
+    nx = int(nx)
+    h = {"lap3d": g2.laplace3d, "lap2d": g2.laplace2d, "ela3d": g2.elasticity3d,
+         "cd3d": lambda k: g2.convdiff3d(k, (50.0, 25.0, 10.0))}[kind](nx)
+    r = g2.random_rhs(h.nrows, 7)
+    for kind_, cfg, kw in (("sgs2", (1, 1, 1), {}), ("sgs2", (1, 1, 3), {}), ("sgs2", (1, 1, 2), {"gamma": 0.7}),
+                           ("gs2", (1, 1, 2), {"direction": "symmetric", "omega": 0.9}),
+                           ("sgs2", (2, 1, 1), {})):
+        cfgo = g2.RelaxConfig(*cfg, **kw)
+        m = g2.Preconditioner(h, kind_, cfgo, precision="single_inside_double")
+        mo = oracle.Precond(h, kind_, n_t=cfg[0], n_k=cfg[1], n_j=cfg[2], precision="single_inside_double",
+                            **kw)
+        assert np.array_equal(m.apply(r), mo.apply(r)), (kind_, cfg, kw)
+    with pytest.raises(OverflowError):
+        g2.Preconditioner(h, "sgs2", g2.RelaxConfig(1, 1, 1), precision="single_inside_double").apply(
+            np.full(h.nrows, 1e300))
