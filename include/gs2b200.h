@@ -308,13 +308,16 @@ int rs_cast_f32_f64(int64_t n, const float *in, double *out, rs_stream_t stream)
  *   rs_dcgs2_dots   out[0,k) = V^T w, out[k,2k) = V^T u        (one pass)
  *   rs_dcgs2_coef   finalises Hessenberg column j-1 and the tentative column j in
  *                   H (raw, column-major, ldh rows), fills the coefficient block
- *                   coef (2*64+2 doubles)                       (one thread)
+ *                   coef (2*128+2 doubles)                      (one thread)
  *   rs_dcgs2_update row j <- v_j = (u - Q s)/rho, row j+1 <- u' = (w - Q a - gamma v_j)/rho,
  *                   nrm2 = ||u'||^2                             (one pass)
  * With last = 1, rs_dcgs2_coef only finalises column k-2 from out = V^T u (k values,
  * e.g. rs_cgs_pass dots with w = row k-1).  peer != NULL: the sums over ranks run
  * inside the passes (see rs_cgs_pass_peer; flags -> status_out in the update).
- * k <= 64, even ldv, 16-byte aligned rows (odd n: as rs_cgs_pass). */
+ * k <= 128 (k > 64: two segments of at most 64 basis rows each, single process only; the update
+ * then needs seg_tmp = 2n doubles of scratch for the first segment's partial sums, the coefficient
+ * block holds 2*128+2 doubles: s at [0, k-1), a at [128, 128+k-1), 1/rho at 256, gamma at 257;
+ * rs_dcgs2_dots_coef: k <= 64), even ldv, 16-byte aligned rows (odd n: as rs_cgs_pass). */
 typedef struct rs_peer rs_peer;
 int rs_dcgs2_dots(const double *V, int64_t ldv, int k, int64_t n, const double *w, double *out, int *nonfinite,
                   double *work, rs_peer *peer, uint64_t epoch, rs_stream_t stream);
@@ -337,7 +340,7 @@ int rs_dcgs2_coef(int k, const double *dots, double *H, int ldh, double *coef, c
                   rs_stream_t stream);
 int rs_dcgs2_update(const double *V, int64_t ldv, int k, int64_t n, const double *coef, const double *w,
                     double *vrow, double *urow, double *nrm2, double *work, rs_peer *peer, uint64_t epoch,
-                    const int64_t *flags, double *status_out, rs_stream_t stream);
+                    const int64_t *flags, double *status_out, double *seg_tmp, rs_stream_t stream);
 
 /* ---- multi-GPU: NVLink peer-memory collectives ----
  *

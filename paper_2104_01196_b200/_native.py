@@ -113,7 +113,7 @@ _SIGS = {
     "rs_dcgs2_dots_coef": ([_P, _I64, C.c_int, _I64, _P, _P, _P, _P, _P, C.c_uint64, _P, C.c_int, _P, _P, _P,
                             C.c_int, _P, _P, C.c_int, _P], C.c_int),
     "rs_dcgs2_coef": ([C.c_int, _P, _P, C.c_int, _P, _P, C.c_int, _P, C.c_int, _P, _P, C.c_int, _P], C.c_int),
-    "rs_dcgs2_update": ([_P, _I64, C.c_int, _I64, _P, _P, _P, _P, _P, _P, _P, C.c_uint64, _P, _P, _P], C.c_int),
+    "rs_dcgs2_update": ([_P, _I64, C.c_int, _I64, _P, _P, _P, _P, _P, _P, _P, C.c_uint64, _P, _P, _P, _P], C.c_int),
     "rs_peer_destroy": ([_P], C.c_int),
 }
 RS_IPC_HANDLE_BYTES = 64

@@ -383,13 +383,33 @@ static int cgs_chunk_rows3(int k, int64_t n) {
 }
 
 // coefficient block of a DCGS2 update pass (see rs_dcgs2_*): s at [0, k-1), a at
-// [kDcgsA, kDcgsA + k-1), 1/rho at kDcgsRho, gamma at kDcgsRho + 1
-constexpr int kDcgsA = kCgsMaxK;
-constexpr int kDcgsRho = 2 * kCgsMaxK;
-constexpr int kDcgsCoef = 2 * kCgsMaxK + 2;
+// [kDcgsA, kDcgsA + k-1), 1/rho at kDcgsRho, gamma at kDcgsRho + 1.  A DCGS2 step covers up to
+// kDcgsMaxK basis vectors; a pass moves at most kCgsMaxK of them through shared memory, so a step
+// with k > kCgsMaxK runs as two segments (SegArgs).
+constexpr int kDcgsMaxK = 2 * kCgsMaxK;
+constexpr int kDcgsA = kDcgsMaxK;
+constexpr int kDcgsRho = 2 * kDcgsMaxK;
+constexpr int kDcgsCoef = 2 * kDcgsMaxK + 2;
 
-static size_t cgs_smem_bytes(int k, int ch, int stages) {
-  return (size_t)stages * (k + 1) * ch * sizeof(double) + kDcgsCoef * sizeof(double) + kCgsMaxStages * 8 + 16;
+// One segment of a DCGS2 pass over basis rows [coff, coff + k) of a step with more than kCgsMaxK
+// vectors:
+//   DOTS:   uext = the step's tentative row u (outside this segment's tile for the first
+//           segment; staged as an extra row); h_out2 receives the V^T u half of the dots
+//   UPDATE: mode 1 (first segment, every tile row is a Q row): P1 = Q s, P2 = Q a over the tile,
+//           nothing else written; mode 2 (last segment, tile = Q rows + u): the sums continue
+//           from P1 / P2 and the segment writes v_j, u', ||u'||^2 as a whole pass would.
+//   coff: offset of the tile's rows in the coefficient block (s_i = coef[coff + i] ...)
+struct SegArgs {
+  const double* uext = nullptr;
+  double* h_out2 = nullptr;
+  double* P1 = nullptr;
+  double* P2 = nullptr;
+  int mode = 0, coff = 0;
+};
+
+static size_t cgs_smem_bytes(int k, int ch, int stages, int extra = 0) {
+  return (size_t)stages * (k + 1 + extra) * ch * sizeof(double) + kDcgsCoef * sizeof(double) +
+         kCgsMaxStages * 8 + 16;
 }
 
 // DCGS (delayed classical Gram-Schmidt with re-orthogonalisation, rs_dcgs2_*):
@@ -413,7 +433,7 @@ __device__ __forceinline__ void dcgs2_coef_dev(int k, const double* __restrict__
                                                    const int64_t* __restrict__ flags, int unnormalized) {
   // 64 threads: thread i owns Hessenberg row i; the two length-j sums are taken by thread 0 in
   // ascending order from shared memory (deterministic)
-  __shared__ double s_au[kCgsMaxK], s_aw[kCgsMaxK];
+  __shared__ double s_au[kDcgsMaxK], s_aw[kDcgsMaxK];
   __shared__ double s_rho, s_beta, s_gam;
   const int t = threadIdx.x;
   const int j = k - 1;
@@ -499,7 +519,7 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
           double* __restrict__ w, double* __restrict__ partial, int* nonfinite, double* __restrict__ h_out,
           double* __restrict__ nrm2_out, unsigned int* ticket, const PeerArgs pa, const int64_t* flags_in,
           double* status_out, double* __restrict__ vout, double* __restrict__ uout, int opts,
-          const CoefArgs ca) {
+          const CoefArgs ca, const SegArgs sg) {
   // Two warp groups ping-pong the chunks of this CTA's row range (group g takes
   // chunks c = g, g+2, ...), each synchronising on its own named barrier, so one
   // group's update / dots compute overlaps the other's; the TMA ring is shared.
@@ -516,7 +536,7 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
   // older completed phase of that stage
   __shared__ int s_issued[kCgsMaxStages];
   __shared__ bool s_last;
-  const int stage_elems = (k + 1) * ch;
+  const int stage_elems = (k + 1 + (sg.uext ? 1 : 0)) * ch;
   double* st = reinterpret_cast<double*>(smraw);
   double* hs = st + (size_t)kCgsStages * stage_elems;
   uint64_t* bar = reinterpret_cast<uint64_t*>(hs + kDcgsCoef);
@@ -527,8 +547,14 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
   const int nchunks = r1 > r0 ? (int)((r1 - r0 + ch - 1) / ch) : 0;
   if (UPDATE && !DCGS)
     for (int i = tid; i < k; i += kCgsThreads) hs[i] = h_in[i];
-  if (UPDATE && DCGS)
-    for (int i = tid; i < kDcgsCoef; i += kCgsThreads) hs[i] = h_in[i];
+  if (UPDATE && DCGS) {
+    // this segment's coefficients: s and a of rows [coff, coff + k), 1/rho, gamma
+    for (int i = tid; i < k; i += kCgsThreads) {
+      hs[i] = h_in[sg.coff + i];
+      hs[kDcgsA + i] = h_in[kDcgsA + sg.coff + i];
+    }
+    if (tid < 2) hs[kDcgsRho + tid] = h_in[kDcgsRho + tid];
+  }
   if (tid == 0) {
     for (int s = 0; s < kCgsStages; ++s) mbar_init(&bar[s], 1);
     for (int s = 0; s < kCgsMaxStages; ++s) s_issued[s] = 0;
@@ -545,9 +571,10 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     // the GMRES workspace) and which no phase below uses (every loop stops at len)
     const uint32_t bytes = (uint32_t)((len + 1) & ~1) * 8u;
     double* dst = st + (size_t)s * stage_elems;
+    const uint32_t ubytes = sg.uext ? bytes : 0u;
     if (use_tmap == 2) {
       // one 3-D tensor copy: (256 rows) x (ch/256 row blocks) x (k vectors) -> [k][ch]
-      mbar_expect_tx(&bar[s], (uint32_t)k * (uint32_t)ch * 8u + bytes);
+      mbar_expect_tx(&bar[s], (uint32_t)k * (uint32_t)ch * 8u + bytes + ubytes);
       asm volatile(
           "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
           "[%5];" ::"r"(smem_u32(dst)),
@@ -555,17 +582,18 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
           : "memory");
     } else if (use_tmap) {
       // one 2-D tensor copy brings the whole k x ch tile (OOB columns zero-filled)
-      mbar_expect_tx(&bar[s], (uint32_t)k * (uint32_t)ch * 8u + bytes);
+      mbar_expect_tx(&bar[s], (uint32_t)k * (uint32_t)ch * 8u + bytes + ubytes);
       asm volatile(
           "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
               "r"(smem_u32(dst)),
           "l"(reinterpret_cast<uint64_t>(&tmap)), "r"((int)c0), "r"(0), "r"(smem_u32(&bar[s]))
           : "memory");
     } else {
-      mbar_expect_tx(&bar[s], (uint32_t)(k + 1) * bytes);
+      mbar_expect_tx(&bar[s], (uint32_t)(k + 1) * bytes + ubytes);
       for (int i = 0; i < k; ++i) bulk_g2s(dst + (size_t)i * ch, V + (int64_t)i * ldv + c0, bytes, &bar[s]);
     }
     bulk_g2s(dst + (size_t)k * ch, w + c0, bytes, &bar[s]);
+    if (sg.uext) bulk_g2s(dst + (size_t)(k + 1) * ch, sg.uext + c0, bytes, &bar[s]);
     __threadfence_block();
     *(volatile int*)&s_issued[s] = c / kCgsStages + 1;
   };
@@ -593,8 +621,9 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     const double* Vs = st + (size_t)s * stage_elems;
     double* ws = st + (size_t)s * stage_elems + (size_t)k * ch;
     if (UPDATE && DCGS) {
-      // v = (u - Q s) / rho, u' = (w - Q a - gamma v) / rho over the Q rows [0, k-1)
-      const int kq = k - 1;
+      // v = (u - Q s) / rho, u' = (w - Q a - gamma v) / rho over the Q rows [0, k-1) (segment mode
+      // 1: every tile row is a Q row and only the partial sums Q s, Q a are written)
+      const int kq = sg.mode == 1 ? k : k - 1;
       const double* ha = hs + kDcgsA;
       const double irho = hs[kDcgsRho], gam = hs[kDcgsRho + 1];
       if (nsplit > 1) {
@@ -636,6 +665,15 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
           }
           sq = q0 + q1;
           sa = a0 + a1;
+        }
+        if (sg.mode == 1) {
+          sg.P1[c0 + r] = sq;
+          sg.P2[c0 + r] = sa;
+          continue;
+        }
+        if (sg.mode == 2) {
+          sq = sg.P1[c0 + r] + sq;
+          sa = sg.P2[c0 + r] + sa;
         }
         const double u = Vs[(size_t)kq * ch + r];
         const double wv = ws[r];
@@ -692,8 +730,9 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
       }
     }
     if (DOTS && DCGS) {
-      // dual dots against w and against the tile's last basis row u (both from shared memory)
-      const double* us = Vs + (size_t)(k - 1) * ch;
+      // dual dots against w and against the step's tentative row u (both from shared memory): the
+      // tile's last basis row, or the extra staged row of a first segment
+      const double* us = sg.uext ? Vs + (size_t)(k + 1) * ch : Vs + (size_t)(k - 1) * ch;
       if ((opts & 1) && ch <= 32 * kCgsMaxT) {
         // w and u of the lane's rows cached in registers: one shared-memory load per basis
         // element for the two FMAs instead of three (the pass is close to the shared-memory
@@ -829,8 +868,8 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     a = warp_sum(a);
     if (lane == 0) {
       if (pa.boxes) s_pay[o] = a;
-      else if (o < nd) h_out[o] = a;
-      else nrm2_out[0] = a;
+      else if (o < nd) (DCGS && sg.h_out2 && o >= k ? sg.h_out2[o - k] : h_out[o]) = a;
+      else if (nrm2_out) nrm2_out[0] = a;
     }
   }
   if (pa.boxes) {
@@ -847,8 +886,8 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
     __syncthreads();
     peer_allreduce_cta(pa, s_pay, cnt);
     for (int o = tid; o < nout; o += kCgsThreads) {
-      if (o < nd) h_out[o] = s_pay[o];
-      else nrm2_out[0] = s_pay[o];
+      if (o < nd) (DCGS && sg.h_out2 && o >= k ? sg.h_out2[o - k] : h_out[o]) = s_pay[o];
+      else if (nrm2_out) nrm2_out[0] = s_pay[o];
     }
     if (flags_in && tid == 0) {
       status_out[0] = s_pay[nout];
@@ -977,8 +1016,10 @@ int rs_gemv_n_update(const double* V, int64_t ldv, int k, int64_t n, const doubl
 static int cgs_pass(const double* V, int64_t ldv, int k, int64_t n, const double* h_in, double* w, double* h_out,
                     double* nrm2, int* nonfinite, double* work, cudaStream_t st, const rs_peer* peer, uint64_t epoch,
                     const int64_t* flags_in, double* status_out, bool dcgs = false, double* vrow = nullptr,
-                    double* urow = nullptr, const CoefArgs* cap = nullptr) {
+                    double* urow = nullptr, const CoefArgs* cap = nullptr, const SegArgs* sgp = nullptr) {
   const CoefArgs ca = cap ? *cap : CoefArgs();
+  const SegArgs sg = sgp ? *sgp : SegArgs();
+  const int extra = sg.uext ? 1 : 0;
   rs_stream_t stream = (rs_stream_t)st;
   // odd n: see issue() in k_cgs (w and the basis rows must have one readable element past n)
   const bool aligned = (ldv % 2 == 0) && ((uintptr_t)V % 16 == 0) && ((uintptr_t)w % 16 == 0);
@@ -1001,9 +1042,9 @@ static int cgs_pass(const double* V, int64_t ldv, int k, int64_t n, const double
     return RS_ERR_ARG;
   }
   const int ch3 = cgs_chunk_rows3(k, n);
-  const int ch = ch3 ? ch3 : cgs_chunk_rows(k);
-  const int stages = cgs_stages(k, ch);
-  const size_t smem = cgs_smem_bytes(k, ch, stages);
+  const int ch = ch3 ? ch3 : cgs_chunk_rows(k + extra);
+  const int stages = cgs_stages(k + extra, ch);
+  const size_t smem = cgs_smem_bytes(k, ch, stages, extra);
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
   int use_tmap = 0;
@@ -1033,7 +1074,7 @@ static int cgs_pass(const double* V, int64_t ldv, int k, int64_t n, const double
     cudaFuncSetAttribute(k_cgs<u, d, nm, dc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
     k_cgs<u, d, nm, dc><<<nblk, kCgsThreads, smem, st>>>(tmap, use_tmap, V, ldv, k, n, ch, stages, rows, h_in, \
                                                          w, work, nonfinite, h_out, nrm2, ticket, pa, flags_in, \
-                                                         status_out, vrow, urow, opts, ca);                   \
+                                                         status_out, vrow, urow, opts, ca, sg);               \
     RS_COUNT_LAUNCH();                                                                                       \
   } while (0)
   if (dcgs) {
@@ -1074,7 +1115,7 @@ int rs_cgs_pass_peer(const double* V, int64_t ldv, int k, int64_t n, const doubl
 
 // ---------------------------------------------------------------- DCGS2 Arnoldi (delayed re-orthogonalisation)
 namespace rs {
-__global__ void __launch_bounds__(64) k_dcgs2_coef(int k, const double* __restrict__ dots, double* __restrict__ H,
+__global__ void __launch_bounds__(128) k_dcgs2_coef(int k, const double* __restrict__ dots, double* __restrict__ H,
                                                    int ldh, double* __restrict__ coef,
                                                    const double* __restrict__ nrm2_prev, int last, double* stage,
                                                    int stage_ld, const double* __restrict__ status,
@@ -1085,8 +1126,8 @@ __global__ void __launch_bounds__(64) k_dcgs2_coef(int k, const double* __restri
 
 static bool dcgs_ok(const double* V, int64_t ldv, int k, int64_t n, const double* w, const char* who) {
   const bool aligned = (ldv % 2 == 0) && ((uintptr_t)V % 16 == 0) && (!w || (uintptr_t)w % 16 == 0);
-  if (k < 1 || k > kCgsMaxK || n < 0 || !aligned) {
-    set_error(RS_ERR_ARG, std::string(who) + ": needs 1 <= k <= 64 basis vectors, an even leading dimension and "
+  if (k < 1 || k > kDcgsMaxK || n < 0 || !aligned) {
+    set_error(RS_ERR_ARG, std::string(who) + ": needs 1 <= k <= 128 basis vectors, an even leading dimension and "
                                              "16-byte aligned rows");
     return false;
   }
@@ -1100,8 +1141,25 @@ int rs_dcgs2_dots(const double* V, int64_t ldv, int k, int64_t n, const double* 
     set_error(RS_ERR_ARG, "rs_dcgs2_dots: bad arguments");
     return RS_ERR_ARG;
   }
-  return cgs_pass(V, ldv, k, n, nullptr, const_cast<double*>(w), out, nullptr, nonfinite, work, (cudaStream_t)stream,
-                  peer, epoch, nullptr, nullptr, true);
+  if (k <= kCgsMaxK)
+    return cgs_pass(V, ldv, k, n, nullptr, const_cast<double*>(w), out, nullptr, nonfinite, work,
+                    (cudaStream_t)stream, peer, epoch, nullptr, nullptr, true);
+  if (peer) {
+    set_error(RS_ERR_UNSUPPORTED, "rs_dcgs2_dots: k > 64 basis vectors with peer-memory reductions");
+    return RS_ERR_UNSUPPORTED;
+  }
+  // two segments: rows [0, 64) with u = row k-1 staged as an extra row, then rows [64, k)
+  SegArgs s0;
+  s0.uext = V + (int64_t)(k - 1) * ldv;
+  s0.h_out2 = out + k;
+  int e = cgs_pass(V, ldv, kCgsMaxK, n, nullptr, const_cast<double*>(w), out, nullptr, nonfinite, work,
+                   (cudaStream_t)stream, nullptr, 0, nullptr, nullptr, true, nullptr, nullptr, nullptr, &s0);
+  if (e) return e;
+  SegArgs s1;
+  s1.h_out2 = out + k + kCgsMaxK;
+  return cgs_pass(V + (int64_t)kCgsMaxK * ldv, ldv, k - kCgsMaxK, n, nullptr, const_cast<double*>(w), out + kCgsMaxK,
+                  nullptr, nullptr, work, (cudaStream_t)stream, nullptr, 0, nullptr, nullptr, true, nullptr, nullptr,
+                  nullptr, &s1);
 }
 
 int rs_dcgs2_dots_coef(const double* V, int64_t ldv, int k, int64_t n, const double* w, double* out, int* nonfinite,
@@ -1109,7 +1167,7 @@ int rs_dcgs2_dots_coef(const double* V, int64_t ldv, int k, int64_t n, const dou
                        const double* nrm2_prev, double* stage, int stage_ld, const double* status,
                        const int64_t* flags, int unnormalized, rs_stream_t stream) {
   if (!dcgs_ok(V, ldv, k, n, w, "rs_dcgs2_dots_coef")) return RS_ERR_ARG;
-  if (!w || !out || !work || (peer && epoch == 0) || !H || ldh < k || !coef || (k > 1 && !nrm2_prev) ||
+  if (k > kCgsMaxK || !w || !out || !work || (peer && epoch == 0) || !H || ldh < k || !coef || (k > 1 && !nrm2_prev) ||
       (stage && stage_ld < k)) {
     set_error(RS_ERR_ARG, "rs_dcgs2_dots_coef: bad arguments");
     return RS_ERR_ARG;
@@ -1132,13 +1190,13 @@ int rs_dcgs2_dots_coef(const double* V, int64_t ldv, int k, int64_t n, const dou
 int rs_dcgs2_coef(int k, const double* dots, double* H, int ldh, double* coef, const double* nrm2_prev, int last,
                   double* stage, int stage_ld, const double* status, const int64_t* flags, int unnormalized,
                   rs_stream_t stream) {
-  if (k < 1 || k > kCgsMaxK || !dots || !H || ldh < k || (!last && !coef) || (k > 1 && !nrm2_prev) ||
+  if (k < 1 || k > kDcgsMaxK || !dots || !H || ldh < k || (!last && !coef) || (k > 1 && !nrm2_prev) ||
       (stage && stage_ld < k)) {
     set_error(RS_ERR_ARG, "rs_dcgs2_coef: bad arguments");
     return RS_ERR_ARG;
   }
-  k_dcgs2_coef<<<1, 64, 0, (cudaStream_t)stream>>>(k, dots, H, ldh, coef, nrm2_prev, last, k > 1 ? stage : nullptr,
-                                                   stage_ld, status, flags, unnormalized);
+  k_dcgs2_coef<<<1, k > 64 ? kDcgsMaxK : 64, 0, (cudaStream_t)stream>>>(
+      k, dots, H, ldh, coef, nrm2_prev, last, k > 1 ? stage : nullptr, stage_ld, status, flags, unnormalized);
   RS_COUNT_LAUNCH();
   RS_CHECK_LAUNCH("rs_dcgs2_coef");
   return RS_OK;
@@ -1146,15 +1204,30 @@ int rs_dcgs2_coef(int k, const double* dots, double* H, int ldh, double* coef, c
 
 int rs_dcgs2_update(const double* V, int64_t ldv, int k, int64_t n, const double* coef, const double* w,
                     double* vrow, double* urow, double* nrm2, double* work, rs_peer* peer, uint64_t epoch,
-                    const int64_t* flags, double* status_out, rs_stream_t stream) {
+                    const int64_t* flags, double* status_out, double* seg_tmp, rs_stream_t stream) {
   if (!dcgs_ok(V, ldv, k, n, w, "rs_dcgs2_update")) return RS_ERR_ARG;
   if (!coef || !w || !vrow || !urow || !nrm2 || !work || (peer && epoch == 0) || (flags && !status_out) ||
-      (flags && !peer)) {
+      (flags && !peer) || (k > kCgsMaxK && (!seg_tmp || peer))) {
     set_error(RS_ERR_ARG, "rs_dcgs2_update: bad arguments");
     return RS_ERR_ARG;
   }
-  return cgs_pass(V, ldv, k, n, coef, const_cast<double*>(w), nullptr, nrm2, nullptr, work, (cudaStream_t)stream,
-                  peer, epoch, flags, status_out, true, vrow, urow);
+  if (k <= kCgsMaxK)
+    return cgs_pass(V, ldv, k, n, coef, const_cast<double*>(w), nullptr, nrm2, nullptr, work, (cudaStream_t)stream,
+                    peer, epoch, flags, status_out, true, vrow, urow);
+  // two segments: Q s and Q a over rows [0, 64) into seg_tmp, then rows [64, k) (ending with u)
+  // continue those sums and write v_j, u', ||u'||^2
+  SegArgs s0;
+  s0.mode = 1;
+  s0.P1 = seg_tmp;
+  s0.P2 = seg_tmp + n;
+  int e = cgs_pass(V, ldv, kCgsMaxK, n, coef, const_cast<double*>(w), nullptr, nullptr, nullptr, work,
+                   (cudaStream_t)stream, nullptr, 0, nullptr, nullptr, true, vrow, urow, nullptr, &s0);
+  if (e) return e;
+  SegArgs s1 = s0;
+  s1.mode = 2;
+  s1.coff = kCgsMaxK;
+  return cgs_pass(V + (int64_t)kCgsMaxK * ldv, ldv, k - kCgsMaxK, n, coef, const_cast<double*>(w), nullptr, nrm2,
+                  nullptr, work, (cudaStream_t)stream, nullptr, 0, nullptr, nullptr, true, vrow, urow, nullptr, &s1);
 }
 
 int rs_gemv_n(const double* V, int64_t ldv, int k, int64_t n, const double* y, double* out, rs_stream_t stream) {

@@ -230,7 +230,8 @@ class _timed:
             self.e1.record()
 
 
-_DCGS_COEF = 2 * 64 + 2  # rs_dcgs2_* coefficient block (include/gs2b200.h)
+_DCGS_COEF = 2 * 128 + 2  # rs_dcgs2_* coefficient block (include/gs2b200.h)
+_DCGS_MAX_RESTART = 127   # DCGS2 steps of up to 128 basis vectors (two 64-row segments beyond 64)
 _DEFER_NORM = __import__("os").environ.get("RS_DEFER_NORM", "1") != "0"  # A/B switch (profiles/ortho_probe.py)
 _FUSE_COEF = __import__("os").environ.get("RS_DCGS_FUSE_COEF", "1") != "0"  # A/B switch
 _DEFER_START = __import__("os").environ.get("RS_DEFER_START", "1") != "0"  # A/B switch (deferred GMRES start)
@@ -277,6 +278,8 @@ class _Workspace:
         self.H = self._alloc(restart * self.m1, device, zero=True)
         self.dots = self._alloc(2 * self.m1, device, zero=True)
         self.coef = self._alloc(_DCGS_COEF, device, zero=True)
+        # partial sums of the first 64-row segment of a DCGS2 update with more than 64 basis rows
+        self.seg_tmp = self._alloc(2 * n, device) if restart > 63 else None
         # per-step record of the Hessenberg column the coefficient kernel writes straight into
         # page-locked host memory (zero-copy; two slots for the one-step-ahead pipeline)
         self.stage = torch.zeros((2, 2 * self.m1 + 8), dtype=torch.float64, pin_memory=True)
@@ -319,13 +322,14 @@ def _p(t):
 def gmres(a, b, m=None, restart: int = 60, tol: float = 1e-9, maxit: int = 10000, x0=None, ortho: str = "auto"):
     """Restarted right-preconditioned GMRES(m) (krylov.py:162-250) on the GPU.
 
-    ``ortho="auto"`` (default): "dcgs2" when restart <= 63, else "cgs2".
+    ``ortho="auto"`` (default): "dcgs2" when restart <= 127, else "cgs2".
     ``ortho="cgs2"`` (north_star item 4): classical Gram-Schmidt with one
     re-orthogonalisation, three fused passes over the basis per step.
     ``ortho="dcgs2"``: the same CGS2 projections with the re-orthogonalisation
     of v_j delayed into step j+1's first pass (two passes over the basis per
     step instead of three; column j of the Hessenberg is final one step later).
-    Equal to CGS2 in exact arithmetic; restart <= 63.
+    Equal to CGS2 in exact arithmetic; restart <= 127 (steps beyond 64 basis vectors run their
+    passes as two segments).
     ``ortho="mgs"``: the reference's modified Gram-Schmidt loop
     (krylov.py:217-219), one fused update+dot launch per basis vector -- the
     reference-faithful mode (same iteration counts where the reference's are
@@ -382,11 +386,11 @@ def _check_ortho(ortho, n, restart):
     """Validate / resolve the orthogonalisation mode ("auto" -> "dcgs2" where it applies)."""
     if ortho not in ("auto", "cgs2", "mgs", "mgs_ref", "dcgs2"):
         raise ValueError(f"ortho must be 'auto', 'cgs2', 'dcgs2', 'mgs' or 'mgs_ref', got {ortho!r}")
-    dcgs_ok = restart <= 63
+    dcgs_ok = restart <= _DCGS_MAX_RESTART
     if ortho == "auto":
         return "dcgs2" if dcgs_ok else "cgs2"
     if ortho == "dcgs2" and not dcgs_ok:
-        raise ValueError("ortho='dcgs2' needs restart <= 63 (fused basis passes of at most 64 vectors)")
+        raise ValueError(f"ortho='dcgs2' needs restart <= {_DCGS_MAX_RESTART}")
     return ortho
 
 
@@ -460,6 +464,8 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
             else:
                 chk(lib.rs_spmv(dm.handle, _p(src), None, None, _p(dst), st), "spmv")
 
+    if ortho == "dcgs2" and restart > 63 and peer is not None:
+        ortho = "cgs2"  # segmented DCGS2 steps (> 64 basis rows) are single-process only
     blas_order = ortho == "mgs_ref"
     if blas_order and reduce_fn is not None:
         raise ValueError("ortho='mgs_ref' (the reference's BLAS summation order) is single-GPU only")
@@ -627,7 +633,7 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
             spmv(ws.z, ws.w)
             k = jj + 1
             unnorm = int(defer_norm and jj >= 1)
-            if fuse_coef:  # one launch: dots (+ in-kernel rank sum) and the coefficient step
+            if fuse_coef and k <= 64:  # one launch: dots (+ in-kernel rank sum) and the coefficient step
                 with _timed("dcgs_dots"):
                     chk(lib.rs_dcgs2_dots_coef(_p(V), ldv, k, n, _p(ws.w), _p(ws.dots), _p(ws.flags), _p(work), ph,
                                                ep(), _p(ws.H), ldh, _p(ws.coef), _p(nrm2_slot), stage_ptr(jj), m1,
@@ -643,7 +649,8 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
             with _timed("dcgs_update"):
                 chk(lib.rs_dcgs2_update(_p(V), ldv, k, n, _p(ws.coef), _p(ws.w), _p(V[jj]), _p(V[jj + 1]),
                                         _p(nrm2_slot), _p(work), ph, ep(), _p(ws.flags) if ph else None,
-                                        _p(status[1:3]) if ph else None, st), "dcgs2_update")
+                                        _p(status[1:3]) if ph else None,
+                                        _p(ws.seg_tmp) if ws.seg_tmp is not None else None, st), "dcgs2_update")
             if reduce_fn is not None and peer is None:
                 status[1] = (ws.flags[0] & 0xFFFFFFFF).to(torch.float64)
                 status[2] = (ws.flags[1] != _I64_MAX).to(torch.float64)

@@ -529,8 +529,18 @@ def test_gmres_dcgs2_edge_cases():
     x, h = g2.gmres(a, b, pc, restart=30, tol=1e-9, ortho="dcgs2")
     _, h0 = g2.gmres(a, b, pc, restart=30, tol=1e-9, x0=x, ortho="dcgs2")
     assert h0.iterations == 0 or h0.rel_res[0] <= 1e-9
-    with pytest.raises(ValueError, match="restart <= 63"):
-        g2.gmres(a, b, pc, restart=64, ortho="dcgs2")
+    with pytest.raises(ValueError, match="restart <= 127"):
+        g2.gmres(a, b, pc, restart=128, ortho="dcgs2")
+    # restarts beyond 63: steps with more than 64 basis vectors run their passes as two segments
+    for shape, m in (((32, 32, 32), 100), ((25, 24, 23), 127), ((30, 30, 30), 70)):
+        a3 = g2.laplace3d(*shape)
+        b3 = g2.random_rhs(a3.nrows, 0)
+        p3 = g2.Preconditioner(a3, "gs2", g2.RelaxConfig(1, 1, 1))
+        _, hd = g2.gmres(a3, b3, p3, restart=m, tol=1e-9, ortho="dcgs2")
+        _, hc = g2.gmres(a3, b3, p3, restart=m, tol=1e-9, ortho="cgs2")
+        ref = oracle.gmres(a3, b3, oracle.Precond(a3, "gs2", n_j=1), restart=m, tol=1e-9)[1]
+        assert hd.converged and hd.iterations == hc.iterations == len(ref) - 1, (shape, m)
+        np.testing.assert_allclose(hd.rel_res, ref, rtol=1e-6)
     # odd row counts take the fused DCGS2 passes too (one padded element per copied row)
     for shape in ((5, 5), (15, 15, 15), (33, 31, 29)):
         odd = g2.laplace2d(*shape) if len(shape) == 2 else g2.laplace3d(*shape)

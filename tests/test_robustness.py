@@ -44,8 +44,8 @@ def guarded(values):
 
 
 @pytest.mark.parametrize("shape", [(16, 16, 16), (15, 15, 15), (21, 20, 19)])
-@pytest.mark.parametrize("ortho,restart", [("dcgs2", 8), ("dcgs2", 63), ("cgs2", 61), ("cgs2", 64), ("mgs", 9),
-                                           ("mgs_ref", 7)])
+@pytest.mark.parametrize("ortho,restart", [("dcgs2", 8), ("dcgs2", 63), ("dcgs2", 100), ("cgs2", 61), ("cgs2", 64),
+                                           ("mgs", 9), ("mgs_ref", 7)])
 def test_gmres_workspace_guards(shape, ortho, restart):
     from paper_2104_01196_b200 import krylov
 
