@@ -275,6 +275,10 @@ int rs_gemv_n_blas(const double *V, int64_t ldv, int k, int64_t n, const double 
                    rs_stream_t stream);
 /* host ddot in the same order (back substitution `h[i, i+1:j+1] @ y[i+1:j+1]`, krylov.py:243) */
 double rs_host_ddot_blas(int64_t n, const double *x, const double *y);
+/* the Givens step of gmres (krylov.py:224-234) on the host: rotations 0..j-1 applied to column j of
+ * the row-major Hessenberg h (ld columns), rotation j from hypot, g updated; returns |g[j+1]|.
+ * Bitwise the reference's numpy scalar arithmetic (no contraction, libm hypot). */
+double rs_host_givens(double *h, int ld, double *cs, double *sn, double *g, int j);
 
 /* y = y + a*x and y = x + b*y, each product and sum rounded separately (no FMA):
  * the CG updates x += alpha p, r -= alpha Ap, p = z + beta p (krylov.py:296-307) */

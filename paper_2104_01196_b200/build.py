@@ -23,7 +23,9 @@ LIB = OUT / "libgs2b200.so"
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr",
+# host code: -ffp-contract=off keeps a*b + c as two roundings (the reference's numpy arithmetic)
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "-Xcompiler", "-ffp-contract=off",
+         "--expt-relaxed-constexpr",
          f"-I{ROOT / 'include'}", "-Xptxas", "-v"]
 
 

@@ -274,4 +274,30 @@ double rs_host_ddot_blas(int64_t n, const double* x, const double* y) {
   return dot;
 }
 
+// The Givens step of the reference's GMRES (krylov.py:224-234) for column j of the Hessenberg h
+// (row-major, `ld` columns: numpy's (restart+1, restart) array): apply the previous rotations,
+// form rotation j with hypot, update g; returns |g[j+1]|.  The same IEEE double operations in the
+// same order as numpy's scalar arithmetic (each product and sum rounded; the library's host code
+// is compiled with -ffp-contract=off) and the same libm hypot, so the result is bitwise the numpy
+// loop's (krylov._givens_step keeps it as the specification).
+double rs_host_givens(double* h, int ld, double* cs, double* sn, double* g, int j) {
+#define H_(i, c) h[(int64_t)(i) * ld + (c)]
+  for (int i = 0; i < j; ++i) {
+    const double a1 = cs[i] * H_(i, j), a2 = sn[i] * H_(i + 1, j);
+    const double hi = a1 + a2;
+    const double b1 = -sn[i] * H_(i, j), b2 = cs[i] * H_(i + 1, j);
+    H_(i + 1, j) = b1 + b2;
+    H_(i, j) = hi;
+  }
+  const double denom = std::hypot(H_(j, j), H_(j + 1, j));
+  cs[j] = H_(j, j) / denom;
+  sn[j] = H_(j + 1, j) / denom;
+  H_(j, j) = denom;
+  H_(j + 1, j) = 0.0;
+  g[j + 1] = -sn[j] * g[j];
+  g[j] = cs[j] * g[j];
+  return std::fabs(g[j + 1]);
+#undef H_
+}
+
 }  // extern "C"

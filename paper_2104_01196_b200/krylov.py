@@ -118,15 +118,19 @@ class Preconditioner:
         torch = _torch()
         return torch.full((1,), _I64_MAX, dtype=torch.int64, device=device)
 
-    def apply_into(self, r, z, flag=None) -> None:
-        """z = P(r) for float64 CUDA tensors r, z (asynchronous; overflow index lands in ``flag``)."""
+    def apply_into(self, r, z, flag=None, stream=None) -> None:
+        """z = P(r) for float64 CUDA tensors r, z (asynchronous; overflow index lands in ``flag``);
+        ``stream``: a cudaStream_t (ctypes) to launch on, default torch's current stream."""
         if self.kind == "none":
             z.copy_(r)
             return
         dm = self._dev
         fp = C.c_void_p(flag.data_ptr()) if flag is not None else None
-        N.call("rs_precond_apply", dm.handle, N.PC_KINDS[self.kind], C.byref(self._cfg_c), C.c_void_p(r.data_ptr()),
-               C.c_void_p(z.data_ptr()), fp, stream_ptr(dm.device_index))
+        st = stream if stream is not None else stream_ptr(dm.device_index)
+        s = N.load().rs_precond_apply(dm.handle, N.PC_KINDS[self.kind], C.byref(self._cfg_c),
+                                      C.c_void_p(r.data_ptr()), C.c_void_p(z.data_ptr()), fp, st)
+        if s:
+            N.check(s, "rs_precond_apply")
 
     def apply(self, r):
         torch = _torch()
@@ -394,10 +398,12 @@ def _check_ortho(ortho, n, restart):
     return ortho
 
 
-def _apply_op(op, v, z, ws):
+def _apply_op(op, v, z, ws, st=None):
     """z = M v for device vectors, through the fast path or the duck-typed seam."""
     if op is None:
         z.copy_(v)
+    elif isinstance(op, Preconditioner):
+        op.apply_into(v, z, ws.flags[1:2] if op.precision == "single_inside_double" else None, st)
     elif hasattr(op, "apply_into"):
         op.apply_into(v, z, ws.flags[1:2] if getattr(op, "precision", "same") == "single_inside_double" else None)
     else:
@@ -413,7 +419,11 @@ def _apply_op(op, v, z, ws):
 
 def _givens_step(h, cs, sn, g, j):
     """Apply the previous rotations to column j, form rotation j, update g (krylov.py:224-234);
-    returns |g[j+1]| (the unscaled residual estimate)."""
+    returns |g[j+1]| (the unscaled residual estimate).  The arithmetic runs in the library's host
+    code (rs_host_givens: the same IEEE double operations, no contraction, libm hypot) for
+    C-contiguous float64 h (restart + 1 rows); the numpy loop below is its specification."""
+    if h.flags.c_contiguous and h.dtype == np.float64:
+        return N.load().rs_host_givens(h.ctypes.data, h.shape[1], cs.ctypes.data, sn.ctypes.data, g.ctypes.data, j)
     for i in range(j):
         hi = cs[i] * h[i, j] + sn[i] * h[i + 1, j]
         h[i + 1, j] = -sn[i] * h[i, j] + cs[i] * h[i + 1, j]
@@ -619,8 +629,17 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
     # has to happen between the two (RS_DCGS_FUSE_COEF=0 keeps them separate for A/B runs)
     fuse_coef = (peer is not None or reduce_fn is None) and _FUSE_COEF
 
+    stage_ptrs = (C.c_void_p(ws.stage[0].data_ptr()), C.c_void_p(ws.stage[1].data_ptr()))
+
     def stage_ptr(jj):
-        return C.c_void_p(ws.stage[jj % 2].data_ptr()) if jj >= 1 else None
+        return stage_ptrs[jj % 2] if jj >= 1 else None
+
+    # ctypes pointers of the fixed workspace buffers, built once per solve (the per-step host work
+    # is what bounds small, latency-bound problems)
+    pV = [C.c_void_p(V[i].data_ptr()) for i in range(restart + 1)]
+    pVb, pw, pz, pdots, pwork = _p(V), _p(ws.w), _p(ws.z), _p(ws.dots), _p(work)
+    pflags, pH, pcoef, pn2, pst12 = _p(ws.flags), _p(ws.H), _p(ws.coef), _p(nrm2_slot), _p(status[1:3])
+    pseg = _p(ws.seg_tmp) if ws.seg_tmp is not None else None
 
     def enqueue_dcgs(jj):
         """DCGS2 step jj: w = A M u_jj, dual dots, coefficients (finalises Hessenberg column jj-1),
@@ -629,28 +648,34 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
         ep = (lambda: peer.next_reduce_epoch()) if peer is not None else (lambda: 0)
         if jj < restart:
             with _timed("precond"):
-                _apply_op(op, V[jj], ws.z, ws)
-            spmv(ws.z, ws.w)
+                _apply_op(op, V[jj], ws.z, ws, st)
+            with _timed("spmv"):
+                if spmv_fn is not None:
+                    spmv_fn(ws.z, ws.w)
+                else:
+                    s = lib.rs_spmv(dm.handle, pz, None, None, pw, st)
+                    if s:
+                        chk(s, "spmv")
             k = jj + 1
             unnorm = int(defer_norm and jj >= 1)
             if fuse_coef and k <= 64:  # one launch: dots (+ in-kernel rank sum) and the coefficient step
                 with _timed("dcgs_dots"):
-                    chk(lib.rs_dcgs2_dots_coef(_p(V), ldv, k, n, _p(ws.w), _p(ws.dots), _p(ws.flags), _p(work), ph,
-                                               ep(), _p(ws.H), ldh, _p(ws.coef), _p(nrm2_slot), stage_ptr(jj), m1,
-                                               _p(status[1:3]), _p(ws.flags), unnorm, st), "dcgs2_dots_coef")
+                    s = lib.rs_dcgs2_dots_coef(pVb, ldv, k, n, pw, pdots, pflags, pwork, ph, ep(), pH, ldh, pcoef,
+                                               pn2, stage_ptr(jj), m1, pst12, pflags, unnorm, st)
+                    if s:
+                        chk(s, "dcgs2_dots_coef")
             else:
                 with _timed("dcgs_dots"):
-                    chk(lib.rs_dcgs2_dots(_p(V), ldv, k, n, _p(ws.w), _p(ws.dots), _p(ws.flags), _p(work), ph,
-                                          ep(), st), "dcgs2_dots")
+                    chk(lib.rs_dcgs2_dots(pVb, ldv, k, n, pw, pdots, pflags, pwork, ph, ep(), st), "dcgs2_dots")
                 if peer is None:
                     reduce_(ws.dots[:2 * k])
-                chk(lib.rs_dcgs2_coef(k, _p(ws.dots), _p(ws.H), ldh, _p(ws.coef), _p(nrm2_slot), 0, stage_ptr(jj),
-                                      m1, _p(status[1:3]), _p(ws.flags), unnorm, st), "dcgs2_coef")
+                chk(lib.rs_dcgs2_coef(k, pdots, pH, ldh, pcoef, pn2, 0, stage_ptr(jj), m1, pst12, pflags, unnorm, st),
+                    "dcgs2_coef")
             with _timed("dcgs_update"):
-                chk(lib.rs_dcgs2_update(_p(V), ldv, k, n, _p(ws.coef), _p(ws.w), _p(V[jj]), _p(V[jj + 1]),
-                                        _p(nrm2_slot), _p(work), ph, ep(), _p(ws.flags) if ph else None,
-                                        _p(status[1:3]) if ph else None,
-                                        _p(ws.seg_tmp) if ws.seg_tmp is not None else None, st), "dcgs2_update")
+                s = lib.rs_dcgs2_update(pVb, ldv, k, n, pcoef, pw, pV[jj], pV[jj + 1], pn2, pwork, ph, ep(),
+                                        pflags if ph else None, pst12 if ph else None, pseg, st)
+                if s:
+                    chk(s, "dcgs2_update")
             if reduce_fn is not None and peer is None:
                 status[1] = (ws.flags[0] & 0xFFFFFFFF).to(torch.float64)
                 status[2] = (ws.flags[1] != _I64_MAX).to(torch.float64)

@@ -145,3 +145,24 @@ def test_no_oracle_import_in_product():
         txt = f.read_text()
         assert not re.search(r"^\s*(import|from)\s+oracle", txt, re.M), f
         assert "liboracle" not in txt and "orc_" not in txt, f
+
+
+def test_host_givens_is_the_numpy_arithmetic():
+    """rs_host_givens (the GMRES Givens step in the library's host code) is bitwise the numpy loop it
+    replaces (krylov.py:224-234 arithmetic: separately rounded products and sums, libm hypot)."""
+    from paper_2104_01196_b200 import krylov
+
+    rng = np.random.default_rng(3)
+    for _ in range(300):
+        m = int(rng.integers(1, 70))
+        j = int(rng.integers(0, m))
+        h = rng.standard_normal((m + 1, m)) * 10.0 ** rng.integers(-8, 8)
+        cs, sn, g = rng.standard_normal(m), rng.standard_normal(m), rng.standard_normal(m + 1)
+        hf = np.zeros((m + 1, 2 * m))[:, ::2]  # a strided (non-contiguous) copy takes the numpy loop
+        hf[...] = h
+        cs2, sn2, g2 = cs.copy(), sn.copy(), g.copy()
+        r1 = krylov._givens_step(h, cs, sn, g, j)      # library host code (C-contiguous h)
+        r2 = krylov._givens_step(hf, cs2, sn2, g2, j)  # numpy loop (the specification)
+        assert r1 == r2
+        assert np.array_equal(h, hf) and np.array_equal(cs, cs2) and np.array_equal(sn, sn2)
+        assert np.array_equal(g, g2)
