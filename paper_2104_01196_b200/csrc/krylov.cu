@@ -9,6 +9,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -902,6 +903,28 @@ __global__ void __launch_bounds__(kCgsThreads, 1)
   if (tid == 0) *ticket = 0;  // reset for the next launch (stream-ordered)
 }
 
+// The dynamic shared-memory allowance of each k_cgs instance, set once per device to the largest
+// any pass requests (setting it per launch to that launch's size raced between host threads: a
+// smaller value set by one thread made another thread's larger launch invalid)
+constexpr int kCgsSmemAttr = 227 * 1024;
+constexpr int kCgsMaxDevices = 64;
+template <bool U, bool D, bool NM, bool DC>
+static void cgs_smem_attr() {
+  static std::atomic<bool> done[kCgsMaxDevices];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= kCgsMaxDevices || !done[dev].load(std::memory_order_acquire)) {
+    // the opt-in limit covers static + dynamic shared memory
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, k_cgs<U, D, NM, DC>);
+    const int dyn = std::min<int>(kCgsSmemAttr, optin - (int)fa.sharedSizeBytes);
+    cudaFuncSetAttribute(k_cgs<U, D, NM, DC>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    if (dev < kCgsMaxDevices) done[dev].store(true, std::memory_order_release);
+  }
+}
+
 // One modified Gram-Schmidt step (krylov.py:217-219): w -= hprev[0] * v_prev (when
 // v_prev != NULL; product and difference rounded separately like the reference's
 // numpy `w -= h * v`), then out[0] = v_cur . w  (or w . w when v_cur == NULL).
@@ -1071,7 +1094,7 @@ static int cgs_pass(const double* V, int64_t ldv, int k, int64_t n, const double
   static const int opts = env_int("RS_DCGS_REGDOTS", 1) ? 1 : 0;
 #define RS_CGS_LAUNCH(u, d, nm, dc)                                                                          \
   do {                                                                                                       \
-    cudaFuncSetAttribute(k_cgs<u, d, nm, dc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
+    cgs_smem_attr<u, d, nm, dc>();                                                                           \
     k_cgs<u, d, nm, dc><<<nblk, kCgsThreads, smem, st>>>(tmap, use_tmap, V, ldv, k, n, ch, stages, rows, h_in, \
                                                          w, work, nonfinite, h_out, nrm2, ticket, pa, flags_in, \
                                                          status_out, vrow, urow, opts, ca, sg);               \

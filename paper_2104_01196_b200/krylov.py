@@ -417,6 +417,24 @@ def _apply_op(op, v, z, ws, st=None):
         z.copy_(out)
 
 
+def _event_ring(device, size: int = 4):
+    """A recorder of completion events on the current stream, reusing `size` events (the software
+    pipelines hold at most two in flight); creating and recording fresh events per step was a
+    measurable share of the per-step host time of small problems."""
+    torch = _torch()
+    stream = torch.cuda.current_stream(device)
+    evs = [torch.cuda.Event() for _ in range(size)]
+    state = [0]
+
+    def rec():
+        ev = evs[state[0] % size]
+        state[0] += 1
+        ev.record(stream)
+        return ev
+
+    return rec
+
+
 def _givens_step(h, cs, sn, g, j):
     """Apply the previous rotations to column j, form rotation j, update g (krylov.py:224-234);
     returns |g[j+1]| (the unscaled residual estimate).  The arithmetic runs in the library's host
@@ -463,6 +481,7 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
     ws.flags.zero_()
     ws.flags[1] = _I64_MAX
     reduce_ = reduce_fn if reduce_fn is not None else (lambda t: None)
+    next_event = _event_ring(dm.torch_device)
 
     def chk(s, what):
         N.check(s, what)
@@ -611,9 +630,7 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
         slot = jj % 2
         ws.pinned[slot].copy_(scal, non_blocking=True)
         ws.pinned_flags[slot].copy_(ws.flags, non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record()
-        return ev
+        return next_event()
 
     ph = peer.handle if peer is not None else None
     ldh = m1
@@ -695,9 +712,7 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
                     reduce_(ws.dots[:k])
             chk(lib.rs_dcgs2_coef(k, _p(ws.dots), _p(ws.H), ldh, None, _p(nrm2_slot), 1, stage_ptr(jj), m1,
                                   _p(status[1:3]), _p(ws.flags), int(defer_norm), st), "dcgs2_coef")
-        ev = torch.cuda.Event()
-        ev.record()
-        return ev
+        return next_event()
 
     while total < maxit and not converged:
         beta = rnorm
@@ -912,6 +927,8 @@ def cg(a, b, m=None, tol: float = 1e-9, maxit: int = 10000, x0=None):
     # device flag is never reset inside the loop -- the first overflow raises
     stage_ovf = torch.full((2,), _I64_MAX, dtype=torch.int64, pin_memory=True)
 
+    next_event = _event_ring(dev)
+
     def enqueue(k):
         """CG iteration k entirely on the device (krylov.py:288-308), scalars staged to pinned slot k%2."""
         xin, xout = xs[k % 2], xs[(k + 1) % 2]
@@ -925,9 +942,7 @@ def cg(a, b, m=None, tol: float = 1e-9, maxit: int = 10000, x0=None):
             stage_ovf[k % 2:k % 2 + 1].copy_(_WS.flags[1:2], non_blocking=True)
         chk(lib.rs_dot(n, _p(r), _p(z), _p(rz_s[(k + 1) % 2]), _p(work), st), "dot")
         chk(lib.rs_xpby_dev(n, _p(z), _p(rz_s[(k + 1) % 2]), _p(rz_s[k % 2]), _p(p), st), "xpby")
-        ev = torch.cuda.Event()
-        ev.record()
-        return ev
+        return next_event()
 
     # Software pipeline as in gmres: iteration k+1 is enqueued before the host checks iteration k's
     # scalars; a speculative iteration past convergence (or past an error) is never read.
