@@ -117,6 +117,18 @@ int rs_mat_destroy(rs_matrix_t m);
 /* sizes: nrows, ncols, row0, nnz (all stored entries), nnz_l, nnz_u, halo_lo, halo_hi */
 int rs_mat_info(rs_matrix_t m, int64_t *info8, int *dtype);
 
+/* Storage of triangle `which` (0 L, 1 U, 2 E_lo, 3 E_hi): out5 = {uniform slice width or -1,
+ * diagonal-slice entries per slice (0: explicit slots only), padded slots, slices, stencil offsets
+ * (0: no stencil encoding)}.  The diagonal-slice encoding (slices whose rows share each offset's
+ * value: {column - row, lane mask, value} per entry) is built with the handle when every slice of
+ * a strict triangle qualifies; the stencil encoding on top of it when the whole triangle has at
+ * most 8 offsets with one value each (constant-coefficient stencils: per slice only lane masks).
+ * Results are bitwise those of the explicit slots (same entries, same order). */
+int rs_mat_layout(rs_matrix_t m, int which, int64_t *out5);
+/* Drop (enable = 0) or (re)build (enable = 1) the diagonal-slice and stencil encodings of L and U --
+ * an A/B switch for tests and benchmarks; not to be called while the handle is in use.  Synchronises. */
+int rs_mat_set_dia(rs_matrix_t m, int enable);
+
 /* Copy d, and the raw / prescaled strict triangles back as CSR (int64 row_ptr,
  * int64 col_idx) for inspection and tests; any pointer may be NULL.
  * which: 0 = L, 1 = U.  Synchronises. */

@@ -56,6 +56,8 @@ _SIGS = {
     "rs_mat_cast": ([_P, C.c_int, C.POINTER(_P)], C.c_int),
     "rs_mat_destroy": ([_P], C.c_int),
     "rs_mat_info": ([_P, _P, C.POINTER(C.c_int)], C.c_int),
+    "rs_mat_layout": ([_P, C.c_int, _P], C.c_int),
+    "rs_mat_set_dia": ([_P, C.c_int], C.c_int),
     "rs_mat_export_tri": ([_P, C.c_int, _P, _P, _P, _P], C.c_int),
     "rs_mat_export_diag": ([_P, _P], C.c_int),
     "rs_mat_coloring": ([_P, _P, C.POINTER(C.c_int64)], C.c_int),

@@ -242,13 +242,274 @@ __global__ void k_cast_diag(const double* in, T* out, int64_t n) {
 }
 
 template <typename T>
+static void free_stencil(Sell<T>& s);
+template <typename T>
+static void free_dia(Sell<T>& s) {
+  free_stencil(s);
+  cudaFree(s.dia_meta);
+  cudaFree(s.dia_val);
+  cudaFree(s.dia_dval);
+  s.dia_meta = nullptr;
+  s.dia_val = s.dia_dval = nullptr;
+  s.dia_k = 0;
+}
+
+template <typename T>
+static void free_stencil(Sell<T>& s) {
+  cudaFree(s.st_mask);
+  s.st_mask = nullptr;
+  s.st_k = 0;
+}
+
+template <typename T>
 static void free_sell(Sell<T>& s) {
+  free_stencil(s);
+  free_dia(s);
   cudaFree(s.slice_ptr);
   cudaFree(s.col);
   cudaFree(s.val);
   cudaFree(s.dval);
   cudaFree(s.dord);
   s = Sell<T>();
+}
+
+template <typename T>
+__device__ __forceinline__ bool same_bits(T a, T b);
+template <>
+__device__ __forceinline__ bool same_bits<double>(double a, double b) {
+  return __double_as_longlong(a) == __double_as_longlong(b);
+}
+template <>
+__device__ __forceinline__ bool same_bits<float>(float a, float b) {
+  return __float_as_int(a) == __float_as_int(b);
+}
+
+// Diagonal-slice encoding of a SELL triangle (Sell::dia_*), one warp per slice: the rows' entries
+// are merged by offset = column - row (each row's offsets ascend, so repeatedly taking the warp
+// minimum of the lanes' next offsets visits every entry once, in each row's own order); entry k of
+// the slice = {offset, ballot of the lanes holding it, the value they hold}.  Pass 1 (meta ==
+// nullptr) only finds the largest entry count and whether any offset's value (or prescaled value)
+// differs between the rows holding it; pass 2 writes the entries, padded to cap with empty masks.
+template <typename T>
+__global__ void k_dia_encode(int64_t nslices, const int64_t* __restrict__ sp, const int32_t* __restrict__ col,
+                             const T* __restrict__ val, const T* __restrict__ dval, int cap, int2* __restrict__ meta,
+                             T* __restrict__ dv, T* __restrict__ ddv, int* __restrict__ kmax, int* __restrict__ fail) {
+  const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= nslices) return;  // warp-uniform
+  const int64_t p0 = sp[s];
+  const int w = (int)((sp[s + 1] - p0) >> 5);
+  const int64_t i = s * 32 + lane;
+  int j = 0, k = 0;
+  bool bad = false;
+  for (;;) {
+    long long my = LLONG_MAX;
+    T v = (T)0, dvv = (T)0;
+    if (j < w) {
+      const int32_t c = col[p0 + 32 * j + lane];
+      if (c >= 0) {
+        my = (long long)c - (long long)i;
+        v = val[p0 + 32 * j + lane];
+        if (dval) dvv = dval[p0 + 32 * j + lane];
+      }
+    }
+    long long mn = my;
+    for (int o = 16; o; o >>= 1) {
+      const long long t = __shfl_xor_sync(0xffffffffu, mn, o);
+      mn = t < mn ? t : mn;
+    }
+    if (mn == LLONG_MAX) break;
+    const bool has = my == mn;
+    const unsigned mask = __ballot_sync(0xffffffffu, has);
+    const int lead = __ffs(mask) - 1;
+    const T v0 = __shfl_sync(0xffffffffu, v, lead);
+    const T d0 = __shfl_sync(0xffffffffu, dvv, lead);
+    if (has && (!same_bits<T>(v, v0) || !same_bits<T>(dvv, d0))) bad = true;
+    if (mn < INT_MIN || mn > INT_MAX) bad = true;
+    if (meta && lane == 0 && k < cap) {
+      meta[s * cap + k] = make_int2((int)mn, (int)mask);
+      dv[s * cap + k] = v0;
+      if (ddv) ddv[s * cap + k] = d0;
+    }
+    ++k;
+    if (has) ++j;
+  }
+  if (meta && lane == 0)
+    for (int q = k; q < cap; ++q) {
+      meta[s * cap + q] = make_int2(0, 0);
+      dv[s * cap + q] = (T)0;
+      if (ddv) ddv[s * cap + q] = (T)0;
+    }
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 0) {
+    atomicMax(kmax, k);
+    if (bad) atomicOr(fail, 1);
+  }
+}
+
+// Stencil encoding (Sell::st_*), pass 1: the distinct offsets of the diagonal-slice entries, one
+// thread per entry, inserted into a 16-slot table (CAS; the inserting entry records its values as
+// the offset's representative; more than 16 -> flag)
+template <typename T>
+__global__ void k_st_collect(int64_t nent, const int2* __restrict__ meta, const T* __restrict__ dv,
+                             const T* __restrict__ ddv, int* table, T* rep_val, T* rep_dval, int* flag) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nent) return;
+  const int2 e = meta[q];
+  if (e.y == 0) return;
+  for (int t = 0; t < 16; ++t) {
+    const int cur = *(volatile int*)(table + t);
+    if (cur == e.x) return;
+    if (cur == INT_MIN) {
+      const int prev = atomicCAS(table + t, INT_MIN, e.x);
+      if (prev == INT_MIN) {
+        rep_val[t] = dv[q];
+        rep_dval[t] = ddv ? ddv[q] : (T)0;
+        return;
+      }
+      if (prev == e.x) return;
+    }
+  }
+  atomicOr(flag, 1);
+}
+
+template <typename T>
+struct StTab {
+  int k;
+  int off[kStencilMax];
+  T val[kStencilMax];
+  T dval[kStencilMax];
+};
+
+// pass 2: every entry's value (and prescaled value) must be its offset's representative, bit for bit;
+// its lane mask goes to slot t of its slice
+template <typename T>
+__global__ void k_st_masks(int64_t nent, int dk, const int2* __restrict__ meta, const T* __restrict__ dv,
+                           const T* __restrict__ ddv, StTab<T> tab, uint32_t* __restrict__ smask, int* flag) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nent) return;
+  const int2 e = meta[q];
+  if (e.y == 0) return;
+  int t = 0;
+  while (t < tab.k && tab.off[t] != e.x) ++t;
+  if (t == tab.k || !same_bits<T>(dv[q], tab.val[t]) || (ddv && !same_bits<T>(ddv[q], tab.dval[t]))) {
+    atomicOr(flag, 1);
+    return;
+  }
+  smask[(q / dk) * kStencilMax + t] = (uint32_t)e.y;
+}
+
+// Build the stencil encoding of a triangle that has diagonal slices, when it qualifies (at most
+// kStencilMax offsets, one value per offset); otherwise leave it without one.
+template <typename T>
+static int build_stencil(Sell<T>& s) {
+  free_stencil(s);
+  if (!s.dia_k) return RS_OK;
+  const int64_t nent = s.nslices * (int64_t)s.dia_k;
+  int* table = nullptr;
+  T* reps = nullptr;
+  RS_CUDA(cudaMalloc(&table, 20 * sizeof(int)));
+  RS_CUDA(cudaMalloc(&reps, 32 * sizeof(T)));
+  std::vector<int> init(20, INT_MIN);
+  init[16] = 0;
+  RS_CUDA(cudaMemcpy(table, init.data(), 20 * sizeof(int), cudaMemcpyHostToDevice));
+  const int B = 256;
+  k_st_collect<T><<<grid_for(nent, B), B>>>(nent, s.dia_meta, s.dia_val, s.dia_dval, table, reps, reps + 16,
+                                            table + 16);
+  RS_COUNT_LAUNCH();
+  int ht[20];
+  T hr[32];
+  cudaError_t e = cudaMemcpy(ht, table, sizeof(ht), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(hr, reps, sizeof(hr), cudaMemcpyDeviceToHost);
+  int st = e == cudaSuccess ? RS_OK : cuda_error(e, "k_st_collect");
+  std::vector<std::pair<int, int>> offs;  // (offset, table slot)
+  for (int t = 0; t < 16; ++t)
+    if (ht[t] != INT_MIN) offs.push_back({ht[t], t});
+  if (st == RS_OK && !ht[16] && !offs.empty() && (int)offs.size() <= kStencilMax) {
+    std::sort(offs.begin(), offs.end());
+    StTab<T> tab;
+    tab.k = (int)offs.size();
+    for (int t = 0; t < kStencilMax; ++t) {
+      tab.off[t] = t < tab.k ? offs[t].first : 0;
+      tab.val[t] = t < tab.k ? hr[offs[t].second] : (T)0;
+      tab.dval[t] = t < tab.k ? hr[16 + offs[t].second] : (T)0;
+    }
+    int hf = 0;
+    if (cudaMalloc(&s.st_mask, sizeof(uint32_t) * kStencilMax * (size_t)s.nslices) != cudaSuccess) {
+      st = cuda_error(cudaErrorMemoryAllocation, "build_stencil");
+    } else {
+      cudaMemset(s.st_mask, 0, sizeof(uint32_t) * kStencilMax * (size_t)s.nslices);
+      cudaMemset(table + 16, 0, sizeof(int));
+      k_st_masks<T><<<grid_for(nent, B), B>>>(nent, s.dia_k, s.dia_meta, s.dia_val, s.dia_dval, tab, s.st_mask,
+                                              table + 16);
+      RS_COUNT_LAUNCH();
+      e = cudaMemcpy(&hf, table + 16, sizeof(int), cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) st = cuda_error(e, "k_st_masks");
+    }
+    if (st == RS_OK && !hf) {
+      s.st_k = tab.k;
+      for (int t = 0; t < kStencilMax; ++t) {
+        s.st_off[t] = tab.off[t];
+        s.st_val[t] = tab.val[t];
+        s.st_dval[t] = tab.dval[t];
+      }
+    } else {
+      free_stencil(s);
+    }
+  }
+  cudaFree(table);
+  cudaFree(reps);
+  return st;
+}
+
+constexpr int kDiaMaxK = 16;  // entries per slice beyond which a triangle stays explicit
+
+// Build the diagonal-slice encoding of a (local, strictly triangular) SELL triangle when every slice
+// qualifies (k_dia_encode); otherwise leave it unencoded.  Needs the explicit arrays filled.
+template <typename T>
+static int build_dia(Sell<T>& s) {
+  free_dia(s);
+  if (s.nslots == 0 || s.nslices == 0) return RS_OK;
+  int* flags = nullptr;
+  RS_CUDA(cudaMalloc(&flags, 2 * sizeof(int)));
+  RS_CUDA(cudaMemset(flags, 0, 2 * sizeof(int)));
+  const int B = 256;
+  const int grid = grid_for(s.nslices * 32, B);
+  k_dia_encode<T><<<grid, B>>>(s.nslices, s.slice_ptr, s.col, s.val, s.dval, 0, nullptr, nullptr, nullptr, flags,
+                               flags + 1);
+  RS_COUNT_LAUNCH();
+  int h[2] = {0, 0};
+  cudaError_t e = cudaMemcpy(h, flags, sizeof(h), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) {
+    cudaFree(flags);
+    return cuda_error(e, "k_dia_encode");
+  }
+  int st = RS_OK;
+  if (!h[1] && h[0] > 0 && h[0] <= kDiaMaxK) {
+    const int k = h[0];
+    const size_t ne = (size_t)s.nslices * k;
+    if (cudaMalloc(&s.dia_meta, sizeof(int2) * ne) != cudaSuccess ||
+        cudaMalloc(&s.dia_val, sizeof(T) * ne) != cudaSuccess ||
+        (s.dval && cudaMalloc(&s.dia_dval, sizeof(T) * ne) != cudaSuccess)) {
+      free_dia(s);
+      st = cuda_error(cudaErrorMemoryAllocation, "build_dia");
+    } else {
+      RS_CUDA(cudaMemset(flags, 0, 2 * sizeof(int)));
+      k_dia_encode<T><<<grid, B>>>(s.nslices, s.slice_ptr, s.col, s.val, s.dval, k, s.dia_meta, s.dia_val,
+                                   s.dia_dval, flags, flags + 1);
+      RS_COUNT_LAUNCH();
+      e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) {
+        free_dia(s);
+        st = cuda_error(e, "k_dia_encode");
+      } else {
+        s.dia_k = k;
+      }
+    }
+  }
+  cudaFree(flags);
+  if (st == RS_OK && s.dia_k) st = build_stencil(s);
+  return st;
 }
 
 void free_mt_sell(rs_matrix* m) {
@@ -449,6 +710,8 @@ static int build_split(rs_matrix* m, const Src& src) {
           }
           cudaError_t e = cudaDeviceSynchronize();
           if (e != cudaSuccess) status = cuda_error(e, "k_fill");
+          if (status == RS_OK) status = build_dia(L);
+          if (status == RS_OK) status = build_dia(U);
         }
       }
     }
@@ -1213,6 +1476,8 @@ int rs_mat_cast(rs_matrix_t src, int dtype, rs_matrix_t* out) {
         !(st = cast_sell(src->Elo64, m->Elo32, bad, d32)) && !(st = cast_sell(src->Ehi64, m->Ehi32, bad, d32))) {
       cudaError_t e = cudaDeviceSynchronize();
       if (e != cudaSuccess) st = cuda_error(e, "rs_mat_cast");
+      if (st == RS_OK) st = build_dia(m->L32);
+      if (st == RS_OK) st = build_dia(m->U32);
       cudaMemcpy(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost);
       if (st == RS_OK && hb != LLONG_MAX) {
         set_error(RS_ERR_OVERFLOW, "matrix value overflows single precision", hb);
@@ -1249,6 +1514,50 @@ int rs_mat_info(rs_matrix_t m, int64_t* info, int* dtype) {
   info[7] = m->halo_hi;
   if (dtype) *dtype = m->dtype;
   return RS_OK;
+}
+
+int rs_mat_layout(rs_matrix_t m, int which, int64_t* out4) {
+  if (!m || !out4 || which < 0 || which > 3) {
+    set_error(RS_ERR_ARG, "rs_mat_layout: bad arguments");
+    return RS_ERR_ARG;
+  }
+  auto fill = [&](auto& s) {
+    out4[0] = s.uw;
+    out4[1] = s.dia_k;
+    out4[2] = s.nslots;
+    out4[3] = s.nslices;
+    out4[4] = s.st_k;
+  };
+  if (m->dtype == RS_F32) fill(tri<float>(m, which));
+  else fill(tri<double>(m, which));
+  return RS_OK;
+}
+
+int rs_mat_set_dia(rs_matrix_t m, int enable) {
+  if (!m) {
+    set_error(RS_ERR_ARG, "rs_mat_set_dia: null");
+    return RS_ERR_ARG;
+  }
+  std::lock_guard<std::mutex> g(m->build_mu);
+  RS_CUDA(cudaSetDevice(m->device));
+  RS_CUDA(cudaDeviceSynchronize());
+  int st = RS_OK;
+  if (m->dtype == RS_F32) {
+    if (enable) {
+      if (!(st = build_dia(m->L32))) st = build_dia(m->U32);
+    } else {
+      free_dia(m->L32);
+      free_dia(m->U32);
+    }
+  } else {
+    if (enable) {
+      if (!(st = build_dia(m->L64))) st = build_dia(m->U64);
+    } else {
+      free_dia(m->L64);
+      free_dia(m->U64);
+    }
+  }
+  return st;
 }
 
 int rs_mat_export_tri(rs_matrix_t m, int which, int64_t* row_ptr, int64_t* col_idx, void* values, void* dvalues) {

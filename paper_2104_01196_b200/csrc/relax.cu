@@ -27,6 +27,7 @@
 
 #include "rs_internal.cuh"
 #include "sell.cuh"
+#include "stencil.cuh"
 
 namespace rs {
 
@@ -293,7 +294,6 @@ __global__ void __launch_bounds__(256) k_inner0(int64_t n, SellView<T> Tm, const
   const T rdi = div_rn<T>(ri, d[i]);
   T t = (T)0;
   if (!Tm.empty) {
-    const int lane = (int)(i & 31);
     int64_t p0;
     int wd;
     slice_bounds<T>(Tm, i >> 5, p0, wd);
@@ -303,9 +303,9 @@ __global__ void __launch_bounds__(256) k_inner0(int64_t n, SellView<T> Tm, const
       R rk[kBatch];
 #pragma unroll
       for (int u = 0; u < kBatch; ++u) {
-        const bool ok = j0 + u < wd;
-        c[u] = ok ? __ldcs(Tm.col + p0 + 32 * (j0 + u) + lane) : -1;
-        v[u] = ok ? __ldcs(Tm.val + p0 + 32 * (j0 + u) + lane) : (T)0;
+        c[u] = -1;
+        v[u] = (T)0;
+        if (j0 + u < wd) sell_entry<T>(Tm, p0, j0 + u, i, c[u], v[u]);
       }
 #pragma unroll
       for (int u = 0; u < kBatch; ++u) {
@@ -353,13 +353,18 @@ __global__ void __launch_bounds__(256) k_inner_out(int64_t n, SellView<T> Tm, co
     if (GAMMA && gin != rd) q -= pf_vec<T>(gin, s2, q);
   }
   if (i >= n) return;
-  RowFetch<T> ft;
-  ft.start(Tm, i);
+  T t;
   const T rdi = rd[i];
   const T gi = GAMMA ? gin[i] : (T)0;
-  ft.load(0);
-  ft.gather(gin);
-  T t = ft.rest(gin, ft.accum((T)0));
+  if (Tm.sk) {
+    t = stencil_accum<T>(Tm, i, gin, (T)0);
+  } else {
+    RowFetch<T> ft;
+    ft.start(Tm, i);
+    ft.load(0);
+    ft.gather(gin);
+    t = ft.rest(gin, ft.accum((T)0));
+  }
   T g = sub_rn<T>(rdi, mul_rn<T>(w, t));
   if (GAMMA) g = add_rn<T>(mul_rn<T>(gm1, gi), mul_rn<T>(gm, g));
   z[i] = (O)mul_rn<T>(w, g);
@@ -385,6 +390,28 @@ __global__ void __launch_bounds__(256) k_inner_out_nr(int64_t n, SellView<T> Tm,
         if (GAMMA && gin != rd) q -= pf_vec<T>(gin, i2 >> 5, q);
       }
     }
+  }
+  if (Tm.sk) {
+    // stencil encoding: each row's gathers issue with its mask loads (no dependent matrix fetch)
+    T tr[NR], rdi[NR], gi[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int64_t i = base + 256 * r;
+      tr[r] = rdi[r] = gi[r] = (T)0;
+      if (i < n) {
+        rdi[r] = rd[i];
+        if (GAMMA) gi[r] = gin[i];
+        tr[r] = stencil_accum<T>(Tm, i, gin, (T)0);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int64_t i = base + 256 * r;
+      T g = sub_rn<T>(rdi[r], mul_rn<T>(w, tr[r]));
+      if (GAMMA) g = add_rn<T>(mul_rn<T>(gm1, gi[r]), mul_rn<T>(gm, g));
+      if (i < n) z[i] = MID ? (O)g : (O)mul_rn<T>(w, g);
+    }
+    return;
   }
   RowFetch<T> ft[NR];
   T rdi[NR], gi[NR];
@@ -452,14 +479,19 @@ __global__ void __launch_bounds__(256) k_inner(int64_t n, SellView<T> Tm, const 
     if (FINAL == kFinalAdd) q -= pf_vec<T>(x, s2, q);
   }
   if (i >= n) return;
-  RowFetch<T> ft;
-  ft.start(Tm, i);
   const T rdi = rd[i];
   const T gi = GAMMA ? gin[i] : (T)0;
   const T xi0 = FINAL == kFinalAdd ? x[i] : (T)0;
-  ft.load(0);
-  ft.gather(gin);
-  T t = ft.rest(gin, ft.accum((T)0));
+  T t;
+  if (Tm.sk) {
+    t = stencil_accum<T>(Tm, i, gin, (T)0);
+  } else {
+    RowFetch<T> ft;
+    ft.start(Tm, i);
+    ft.load(0);
+    ft.gather(gin);
+    t = ft.rest(gin, ft.accum((T)0));
+  }
   T g = sub_rn<T>(rdi, mul_rn<T>(w, t));
   if (GAMMA) g = add_rn<T>(mul_rn<T>(gm1, gi), mul_rn<T>(gm, g));
   if (FINAL == kNotFinal) gout[i] = g;
@@ -719,6 +751,16 @@ static SellView<T> none_view() {
   v.uw = -1;
   v.s_lo = 0;
   v.s_hi = 0;
+  v.dk = 0;
+  v.dm = nullptr;
+  v.dv = nullptr;
+  v.sk = 0;
+  v.xn = 0;
+  v.smask = nullptr;
+  for (int t = 0; t < kStencilMax; ++t) {
+    v.soff[t] = 0;
+    v.sv[t] = (T)0;
+  }
   return v;
 }
 
@@ -843,12 +885,21 @@ static size_t resid_tma_smem(rs_matrix* m) {
   const Sell<T>& L = tri<T>(m, 0);
   const Sell<T>& U = tri<T>(m, 1);
   if (!on || L.uw < 0 || U.uw < 0 || tri<T>(m, 2).nslots || tri<T>(m, 3).nslots) return 0;
+  // diagonal-slice triangles: no slot arrays to stage (k_resid reads a few broadcast entries)
+  if (dia_enabled() && (L.dia_k || U.dia_k)) return 0;
   const size_t sz = (size_t)kTmaRows * (L.uw + U.uw) * (sizeof(T) + 4);
   return sz <= 200 * 1024 ? sz : 0;
 }
 
 template <typename T, int MODE>
 static bool launch_resid_tma(rs_matrix* m, const T* x, const T* b, T* out, T w, cudaStream_t st) {
+  // stencil-encoded triangles: the TMA-windowed pass (stencil.cuh)
+  if (!tri<T>(m, 2).nslots && !tri<T>(m, 3).nslots && m->nrows > 0) {
+    constexpr int SM = MODE == kSpmv ? kStSpmv : MODE == kResidRd ? kStResidRd : kStJr;
+    if (st_resid<T, SM, T>(m->device, view(tri<T>(m, 0), false), view(tri<T>(m, 1), false), m->nrows,
+                           (const T*)m->d, x, b, out, w, st))
+      return true;
+  }
   const size_t smem = resid_tma_smem<T>(m);
   if (!smem || m->nrows == 0) return false;
   const Sell<T>& L = tri<T>(m, 0);
@@ -868,7 +919,18 @@ static bool launch_resid_tma(rs_matrix* m, const T* x, const T* b, T* out, T w, 
 template <typename T, int FINAL, bool GAMMA>
 static void launch_inner(Ctx<T>& c, int backward, const T* rd, const T* gin, T* gout, T* x, T w, T gm, T gm1) {
   SellView<T> Tm = backward ? c.Usc : c.Lsc;
+  constexpr int SF = FINAL == kNotFinal ? kStMid : FINAL == kFinalSet ? kStSet : kStAdd;
+  if (st_inner<T, SF, GAMMA, T>(c.m->device, Tm, c.n, rd, gin, x, FINAL == kNotFinal ? gout : x, w, gm, gm1, c.st))
+    return;
   k_inner<T, FINAL, GAMMA><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1, pf_dist_host());
+}
+
+// st_inner with the damping chosen at run time (the zero-start preconditioner chains)
+template <typename T, int SF, typename O>
+static bool st_inner_any(int device, const SellView<T>& Tm, int64_t n, const T* rd, const T* gin, const T* xc,
+                         O* out, T w, T gm, T gm1, bool damped, cudaStream_t st) {
+  return damped ? st_inner<T, SF, true, O>(device, Tm, n, rd, gin, xc, out, w, gm, gm1, st)
+                : st_inner<T, SF, false, O>(device, Tm, n, rd, gin, xc, out, w, gm, gm1, st);
 }
 
 // One inner JR chain from rd; the last step updates x (non-compact add / compact set).
@@ -1840,7 +1902,13 @@ static int precond_gs2_single(rs_matrix* m, const rs_relax_cfg& cfg, const R* r,
     RS_COUNT_LAUNCH();
     const T* gin = rd;
     for (int j = 0; j < cfg.n_j; ++j) {
-      if (j == cfg.n_j - 1 && nr == 4) {
+      const bool last = j == cfg.n_j - 1;
+      T* gmid = bufs[j & 1];
+      if (last ? st_inner_any<T, kStSet, O>(m->device, Tm, c.n, rd, gin, (const T*)nullptr, z, w, gm, gm1, damped, st)
+               : st_inner_any<T, kStMid, T>(m->device, Tm, c.n, rd, gin, (const T*)nullptr, gmid, w, gm, gm1, damped,
+                                            st)) {
+        gin = gmid;
+      } else if (j == cfg.n_j - 1 && nr == 4) {
         const int g4 = grid_for(c.n, 4 * kB);
         if (damped) k_inner_out_nr<T, O, true, 4><<<g4, kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1, pf_dist_host());
         else k_inner_out_nr<T, O, false, 4><<<g4, kB, 0, st>>>(c.n, Tm, rd, gin, z, w, gm, gm1, pf_dist_host());
@@ -1921,15 +1989,20 @@ static int precond_sgs2_f32(rs_matrix* m, const rs_relax_cfg& cfg, const double*
   float* bufs[2] = {rd + c.n, rd + 2 * c.n};
   const float w = (float)cfg.omega, gm = (float)cfg.gamma, gm1 = (float)(1.0 - cfg.gamma);
   const bool damped = cfg.gamma != 1.0;
-  k_resid<float, kResidRd, false, double><<<c.grid(), kB, 0, st>>>(c.n, none_view<float>(), c.L, c.U,
-                                                                   none_view<float>(), c.d, x32, nullptr, nullptr, r,
-                                                                   rd, 0.0f, pf_dist_host());
+  if (!st_resid<float, kStResidRd, double>(m->device, c.L, c.U, c.n, c.d, x32, r, rd, 0.0f, st))
+    k_resid<float, kResidRd, false, double><<<c.grid(), kB, 0, st>>>(c.n, none_view<float>(), c.L, c.U,
+                                                                     none_view<float>(), c.d, x32, nullptr, nullptr, r,
+                                                                     rd, 0.0f, pf_dist_host());
   RS_COUNT_LAUNCH();
   const float* gin = rd;
   for (int j = 0; j < cfg.n_j; ++j) {
     const bool last = j == cfg.n_j - 1;
     float* gout = bufs[j & 1];
-    if (last) {
+    if (last ? st_inner_any<float, kStAdd, double>(m->device, c.Usc, c.n, rd, gin, x32, z, w, gm, gm1, damped, st)
+             : st_inner_any<float, kStMid, float>(m->device, c.Usc, c.n, rd, gin, (const float*)nullptr, gout, w, gm,
+                                                  gm1, damped, st)) {
+      gin = gout;
+    } else if (last) {
       if (damped)
         k_inner<float, kFinalAdd, true, double><<<c.grid(), kB, 0, st>>>(c.n, c.Usc, rd, gin, gout, x32, w, gm, gm1,
                                                                          pf_dist_host(), z);

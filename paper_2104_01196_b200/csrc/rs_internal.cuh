@@ -65,7 +65,32 @@ struct Sell {
   T* dord = nullptr;             // [nrows] d[rows[t]] of group-ordered slices (MT / LV), else null
   int uw = -1;                   // every slice has this width (slice_ptr[s] = 32*uw*s), else -1
   int64_t s_lo = 0, s_hi = -1;   // slices outside [s_lo, s_hi) are empty (-1: not computed = all)
+  // Diagonal-slice encoding (built by build_dia when EVERY slice qualifies; the explicit arrays
+  // above stay valid for the kernels that walk slots directly).  Slice s is dia_k entries
+  // {offset = column - row, 32-bit lane mask, value, value / d}: lane r's row holds the entry
+  // (row + offset, value) iff mask bit r is set, and the entries ascend in offset -- so a row's
+  // entries in entry order are its entries in ascending column order (the reference's summation
+  // order) with the same values.  A slice qualifies when each offset's value (and prescaled value)
+  // is bitwise the same in every row that has it (constant-coefficient stencils).  A warp then
+  // reads 8 + 2*sizeof(T) bytes per entry (broadcast) instead of 32 columns and 32 values.
+  int dia_k = 0;                 // entries per slice (0: not encoded)
+  int2* dia_meta = nullptr;      // [nslices * dia_k] {offset, lane mask}
+  T* dia_val = nullptr;          // [nslices * dia_k]
+  T* dia_dval = nullptr;         // [nslices * dia_k] (when dval exists)
+  // Stencil encoding (build_stencil, on top of the diagonal slices): when the whole triangle uses at
+  // most kStencilMax distinct offsets and each offset has ONE value (and one prescaled value) in every
+  // row holding it, the offsets and values are kernel parameters and a slice is only its st_k lane
+  // masks (st_mask[s * kStencilMax + t]: bit r set iff row 32s + r has offset st_off[t]).  A row's
+  // operands are then known before any matrix byte arrives: its gathers x[i + st_off[t]] issue with the
+  // mask loads (speculatively, clamped to the vector) and the mask only selects the terms to add, in
+  // ascending offset = ascending column order.
+  int st_k = 0;
+  int st_off[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  T st_val[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  T st_dval[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  uint32_t* st_mask = nullptr;   // [nslices * kStencilMax]
 };
+constexpr int kStencilMax = 8;
 
 // per (host thread, stream) working memory of a matrix handle
 struct Workspace {

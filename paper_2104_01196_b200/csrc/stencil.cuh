@@ -1,0 +1,388 @@
+// stencil.cuh -- TMA-windowed row passes over stencil-encoded triangles (rs_internal.cuh Sell::st_*).
+//
+// A stencil-encoded triangle is K offsets with one value each plus per-slice lane masks, so a row's
+// operands are the vector at i + offset for each offset.  For a tile of R consecutive rows those
+// are K + 1 contiguous ranges of the gathered vector (offsets closer than kStGap merge into one
+// window): one thread of the CTA copies every window, the tile's lane masks and the tile's own
+// entries of the row vectors (d, b, rd, x) into shared memory with cp.async.bulk on one mbarrier,
+// and the rows are computed out of shared memory.  The copy engine keeps a whole tile's bytes in
+// flight per CTA without registers -- a row of a constant-coefficient stencil moves only ~24-32
+// bytes, too few per thread for thread-per-row loads to cover the HBM latency.  Windows are clamped
+// to the vector and aligned to 16 bytes; an operand outside its window (only at the vector's
+// ends) is read from global memory.  Per row the terms are added in the reference's order (L
+// ascending, d x, U ascending) with the same values: bitwise the explicit-slot kernels.
+#pragma once
+
+#include <mutex>
+#include <set>
+#include <utility>
+
+#include "sell.cuh"
+
+namespace rs {
+
+constexpr int kStWin = 8;        // windows of the gathered vector
+constexpr int kStThreads = 256;  // threads per CTA; a tile is rows = kStThreads * rows-per-thread
+constexpr int kStGap = 64;       // offsets at most this far apart share a window
+
+template <typename T>
+struct StPlan {
+  int n;                        // rows = length of the gathered vector
+  int rows;                     // rows per tile (multiple of kStThreads)
+  int k[2];                     // offsets of L (or the single triangle), U
+  int off[2][kStencilMax];
+  T val[2][kStencilMax];
+  const uint32_t* mask[2];      // Sell::st_mask
+  int nwin;                     // windows of the gathered vector
+  int wlo[kStWin], whi[kStWin];  // offset range of each window
+  int wsm[kStWin];              // shared-memory element offset of each window
+  int win[2][kStencilMax];      // window of each offset
+  int wcen;                     // window holding offset 0 (-1: none)
+  int sm_mask;                  // byte offset of the masks (rows bytes per triangle)
+  int sm_c[3];                  // byte offsets of the center vectors
+};
+
+struct StShared {
+  int ws[kStWin];  // first element of each window (global index)
+  int wl[kStWin];  // elements in each window
+  int clen;        // tile rows whose center operands are staged
+  int interior;    // every operand of every row of the tile is inside its window
+};
+
+template <typename T>
+__device__ __forceinline__ T* st_ptr(unsigned char* sm, int byte_off) {
+  return reinterpret_cast<T*>(sm + byte_off);
+}
+
+// thread 0: window / center ranges of tile r0, expect_tx, then the bulk copies.  C0..C2: the center
+// vectors' types (nullptr = not staged); returns nothing -- every thread then waits on bar.
+template <typename T, typename C0, typename C1, typename C2>
+__device__ __forceinline__ void st_issue(const StPlan<T>& p, int r0, int ntri, const T* __restrict__ gv,
+                                         const C0* c0, const C1* c1, const C2* c2, unsigned char* sm,
+                                         StShared& S, uint64_t* bar) {
+  constexpr int A = 16 / (int)sizeof(T);
+  const int nA = p.n & ~(A - 1);
+  uint32_t bytes = 0;
+  bool interior = r0 + p.rows <= p.n;
+  for (int g = 0; g < p.nwin; ++g) {
+    const int gs0 = r0 + p.wlo[g], ge0 = r0 + p.rows + p.whi[g];
+    const int gs = gs0 < 0 ? 0 : gs0;
+    const int ge = ge0 > p.n ? p.n : ge0;
+    const int cs = gs & ~(A - 1);
+    int ce = (ge + A - 1) & ~(A - 1);
+    if (ce > nA) ce = nA;
+    const int len = ce > cs ? ce - cs : 0;
+    S.ws[g] = cs;
+    S.wl[g] = len;
+    bytes += (uint32_t)len * (uint32_t)sizeof(T);
+    if (gs0 < 0 || ce < ge0) interior = false;
+  }
+  // the tile's masks: whole slices (32 bytes each: kStencilMax words)
+  const int s0 = r0 >> 5;
+  const int nsl_all = (p.n + 31) >> 5;
+  const int nsl = min(p.rows >> 5, nsl_all - s0);
+  bytes += (uint32_t)ntri * (uint32_t)nsl * 32u;
+  // centers: rows [r0, r0 + clen), clen a multiple of 4 (whole 16-byte units of 4- and 8-byte types;
+  // the tile's last rows beyond it read global memory)
+  const int cend = r0 + p.rows < p.n ? r0 + p.rows : p.n;
+  const int clen = cend > r0 ? (cend - r0) & ~3 : 0;
+  S.clen = clen;
+  if (c0) bytes += (uint32_t)clen * (uint32_t)sizeof(C0);
+  if (c1) bytes += (uint32_t)clen * (uint32_t)sizeof(C1);
+  if (c2) bytes += (uint32_t)clen * (uint32_t)sizeof(C2);
+  S.interior = interior ? 1 : 0;
+  mbar_expect_tx(bar, bytes);
+  for (int g = 0; g < p.nwin; ++g)
+    if (S.wl[g]) bulk_g2s(st_ptr<T>(sm, 0) + p.wsm[g], gv + S.ws[g], (uint32_t)S.wl[g] * (uint32_t)sizeof(T), bar);
+  for (int q = 0; q < ntri; ++q)
+    if (nsl > 0) bulk_g2s(sm + p.sm_mask + q * p.rows, p.mask[q] + (size_t)s0 * kStencilMax, (uint32_t)nsl * 32u, bar);
+  if (clen) {
+    if (c0) bulk_g2s(sm + p.sm_c[0], c0 + r0, (uint32_t)clen * (uint32_t)sizeof(C0), bar);
+    if (c1) bulk_g2s(sm + p.sm_c[1], c1 + r0, (uint32_t)clen * (uint32_t)sizeof(C1), bar);
+    if (c2) bulk_g2s(sm + p.sm_c[2], c2 + r0, (uint32_t)clen * (uint32_t)sizeof(C2), bar);
+  }
+}
+
+// element j of the gathered vector through window g: from shared memory, or global memory when
+// outside the window (vector ends only)
+template <typename T>
+__device__ __forceinline__ T st_at(const StPlan<T>& p, const StShared& S, const T* sx, const T* __restrict__ gv, int g,
+                                   int j) {
+  const int r = j - S.ws[g];
+  return (unsigned)r < (unsigned)S.wl[g] ? sx[p.wsm[g] + r] : gv[j];
+}
+
+// acc += sum over the K offsets of triangle q present in row i (mask word m[tt] bit lane)
+template <typename T, int K>
+__device__ __forceinline__ T st_tri_accum(const StPlan<T>& p, const StShared& S, const T* sx,
+                                          const T* __restrict__ gv, int q, const uint32_t* m, int i, bool interior,
+                                          T acc) {
+  const uint32_t bit = 1u << (i & 31);
+  if (interior) {
+#pragma unroll
+    for (int tt = 0; tt < K; ++tt) {
+      if (m[tt] & bit) {
+        const int g = p.win[q][tt];
+        acc = add_rn<T>(acc, mul_rn<T>(p.val[q][tt], sx[p.wsm[g] + (i + p.off[q][tt] - S.ws[g])]));
+      }
+    }
+  } else {
+#pragma unroll
+    for (int tt = 0; tt < K; ++tt)
+      if (m[tt] & bit) acc = add_rn<T>(acc, mul_rn<T>(p.val[q][tt], st_at<T>(p, S, sx, gv, p.win[q][tt], i + p.off[q][tt])));
+  }
+  return acc;
+}
+
+template <int K>
+__device__ __forceinline__ void st_masks(const unsigned char* sm, int off, int t, uint32_t (&m)[K]) {
+  const uint4* mp = reinterpret_cast<const uint4*>(sm + off + (t >> 5) * 32);
+  const uint4 a = mp[0];
+  m[0] = a.x;
+  if (K > 1) m[1 < K ? 1 : 0] = a.y;
+  if (K > 2) m[2 < K ? 2 : 0] = a.z;
+  if (K > 3) m[3 < K ? 3 : 0] = a.w;
+  if (K > 4) {
+    const uint4 b = mp[1];
+    m[4 < K ? 4 : 0] = b.x;
+    if (K > 5) m[5 < K ? 5 : 0] = b.y;
+    if (K > 6) m[6 < K ? 6 : 0] = b.z;
+    if (K > 7) m[7 < K ? 7 : 0] = b.w;
+  }
+}
+
+enum StResidMode { kStSpmv = 0, kStResidRd = 1, kStJr = 2 };
+
+// Full-row pass A x over a stencil L | D | U (both triangles K offsets): y = A x, rd = (b - A x) / d,
+// or the JR update x + w (b - A x) / d -- k_resid's MODEs, same operation forms.
+template <typename T, int MODE, int K, typename B>
+__global__ void __launch_bounds__(kStThreads) k_st_resid(StPlan<T> p, const T* __restrict__ d,
+                                                        const T* __restrict__ x, const B* __restrict__ b,
+                                                        T* __restrict__ out, T w) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ StShared S;
+  __shared__ __align__(8) uint64_t bar;
+  const int r0 = blockIdx.x * p.rows;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    st_issue<T, T, B, T>(p, r0, 2, x, d, MODE == kStSpmv ? (const B*)nullptr : b, (const T*)nullptr, sm, S, &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  const T* sx = st_ptr<T>(sm, 0);
+  const T* sd = st_ptr<T>(sm, p.sm_c[0]);
+  const B* sb = reinterpret_cast<const B*>(sm + p.sm_c[1]);
+  const bool interior = S.interior != 0;
+  const int clen = S.clen;
+  for (int t = threadIdx.x; t < p.rows; t += kStThreads) {
+    const int i = r0 + t;
+    if (i >= p.n) break;
+    uint32_t mL[K], mU[K];
+    st_masks<K>(sm, p.sm_mask, t, mL);
+    st_masks<K>(sm, p.sm_mask + p.rows, t, mU);
+    const T di = t < clen ? sd[t] : d[i];
+    const T xi = interior ? sx[p.wsm[p.wcen] + (i - S.ws[p.wcen])] : st_at<T>(p, S, sx, x, p.wcen, i);
+    T acc = st_tri_accum<T, K>(p, S, sx, x, 0, mL, i, interior, (T)0);
+    acc = add_rn<T>(acc, mul_rn<T>(di, xi));
+    acc = st_tri_accum<T, K>(p, S, sx, x, 1, mU, i, interior, acc);
+    if (MODE == kStSpmv) {
+      out[i] = acc;
+    } else {
+      const T bi = (T)(t < clen ? sb[t] : b[i]);
+      const T g = div_rn<T>(sub_rn<T>(bi, acc), di);
+      out[i] = MODE == kStResidRd ? g : add_rn<T>(xi, mul_rn<T>(w, g));
+    }
+  }
+}
+
+enum StInnerFinal { kStMid = 0, kStSet = 1, kStAdd = 2 };
+
+// One inner JR step over a stencil triangle (prescaled values): g = rd - w (D^-1 T gin) (damped:
+// (1-gm) gin + gm (...)); out = g (kStMid), w g (kStSet) or x + w g (kStAdd), written as O --
+// k_inner / k_inner_out's forms.
+template <typename T, int FINAL, bool GAMMA, int K, typename O>
+__global__ void __launch_bounds__(kStThreads) k_st_inner(StPlan<T> p, const T* __restrict__ rd,
+                                                        const T* __restrict__ gin, const T* __restrict__ xc,
+                                                        O* __restrict__ out, T w, T gm, T gm1) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ StShared S;
+  __shared__ __align__(8) uint64_t bar;
+  const int r0 = blockIdx.x * p.rows;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    st_issue<T, T, T, T>(p, r0, 1, gin, rd, FINAL == kStAdd ? xc : (const T*)nullptr, (const T*)nullptr, sm, S, &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  const T* sx = st_ptr<T>(sm, 0);
+  const T* srd = st_ptr<T>(sm, p.sm_c[0]);
+  const T* sxc = st_ptr<T>(sm, p.sm_c[1]);
+  const bool interior = S.interior != 0;
+  const int clen = S.clen;
+  for (int t = threadIdx.x; t < p.rows; t += kStThreads) {
+    const int i = r0 + t;
+    if (i >= p.n) break;
+    uint32_t m[K];
+    st_masks<K>(sm, p.sm_mask, t, m);
+    const T rdi = t < clen ? srd[t] : rd[i];
+    const T tsum = st_tri_accum<T, K>(p, S, sx, gin, 0, m, i, interior, (T)0);
+    T g = sub_rn<T>(rdi, mul_rn<T>(w, tsum));
+    if (GAMMA) {
+      const T gi = st_at<T>(p, S, sx, gin, p.wcen, i);
+      g = add_rn<T>(mul_rn<T>(gm1, gi), mul_rn<T>(gm, g));
+    }
+    if (FINAL == kStMid) out[i] = (O)g;
+    else if (FINAL == kStSet) out[i] = (O)mul_rn<T>(w, g);
+    else out[i] = (O)add_rn<T>(t < clen ? sxc[t] : xc[i], mul_rn<T>(w, g));
+  }
+}
+
+// ------------------------------------------------------------------ host planning / launch
+static int st_rows_per_tile() {
+  static const int v = getenv("RS_ST_ROWS") ? atoi(getenv("RS_ST_ROWS")) : 1024;
+  return v >= kStThreads && v % kStThreads == 0 ? v : 1024;
+}
+static bool st_enabled() {
+  static const bool on = !getenv("RS_ST_TMA") || atoi(getenv("RS_ST_TMA")) != 0;
+  return on;
+}
+
+// Plan the windows of a pass gathering vector entries at the offsets of `tri[0..ntri)` (and 0 when
+// `center`: x[i] of the full-row pass, gin[i] of a damped inner step); csize: bytes per element of the
+// per-row vectors staged (0: not staged).
+template <typename T>
+static bool st_plan(const SellView<T>* const* tri, int ntri, bool center, int64_t n, const int* csize,
+                    StPlan<T>& p, size_t& smem) {
+  if (!st_enabled() || n <= 0 || n >= (int64_t)INT32_MAX - (1 << 22)) return false;
+  const int K = tri[0]->sk;
+  for (int q = 0; q < ntri; ++q)
+    if (tri[q]->sk != K || K < 1 || K > 4 || !tri[q]->smask) return false;
+  p = StPlan<T>();
+  p.n = (int)n;
+  p.rows = st_rows_per_tile();
+  std::vector<int> offs;
+  for (int q = 0; q < ntri; ++q) {
+    p.k[q] = K;
+    p.mask[q] = tri[q]->smask;
+    for (int tt = 0; tt < K; ++tt) {
+      p.off[q][tt] = tri[q]->soff[tt];
+      p.val[q][tt] = tri[q]->sv[tt];
+      offs.push_back(tri[q]->soff[tt]);
+    }
+  }
+  if (center) offs.push_back(0);
+  std::sort(offs.begin(), offs.end());
+  offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
+  p.nwin = 0;
+  for (size_t a = 0; a < offs.size(); ++a) {
+    if (a == 0 || offs[a] - offs[a - 1] > kStGap) {
+      if (p.nwin == kStWin) return false;
+      p.wlo[p.nwin] = p.whi[p.nwin] = offs[a];
+      ++p.nwin;
+    } else {
+      p.whi[p.nwin - 1] = offs[a];
+    }
+  }
+  auto win_of = [&](int o) {
+    for (int g = 0; g < p.nwin; ++g)
+      if (o >= p.wlo[g] && o <= p.whi[g]) return g;
+    return -1;
+  };
+  for (int q = 0; q < ntri; ++q)
+    for (int tt = 0; tt < K; ++tt) p.win[q][tt] = win_of(p.off[q][tt]);
+  p.wcen = center ? win_of(0) : -1;
+  constexpr int A = 16 / (int)sizeof(T);
+  size_t e = 0;
+  for (int g = 0; g < p.nwin; ++g) {
+    p.wsm[g] = (int)e;
+    e += (size_t)p.rows + (size_t)(p.whi[g] - p.wlo[g]) + 2 * A;
+    e = (e + A - 1) / A * A;
+  }
+  size_t bytes = e * sizeof(T);
+  p.sm_mask = (int)bytes;
+  bytes += (size_t)ntri * p.rows;  // rows / 32 slices x 32 bytes
+  for (int c = 0; c < 3; ++c) {
+    p.sm_c[c] = (int)bytes;
+    bytes += (size_t)p.rows * (size_t)csize[c];
+    bytes = (bytes + 15) / 16 * 16;
+  }
+  smem = bytes;
+  return bytes <= 200 * 1024;
+}
+
+// bulk copies need 16-byte aligned global addresses (window / tile starts are multiples of 16 bytes
+// from the base)
+static bool st_aligned(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+// the dynamic shared-memory allowance of each stencil kernel, set once per (kernel, device)
+template <typename Kern>
+static void st_smem_attr(Kern k, int device) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  const std::pair<const void*, int> key((const void*)k, device);
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count(key)) return;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  done.insert(key);
+}
+
+// k_resid's full-row pass (MODE kStSpmv / kStResidRd / kStJr) on a stencil matrix without couplings;
+// false: not applicable (the caller runs k_resid)
+template <typename T, int MODE, typename B>
+static bool st_resid(int device, const SellView<T>& L, const SellView<T>& U, int64_t n, const T* d, const T* x,
+                     const B* b, T* out, T w, cudaStream_t st) {
+  const SellView<T>* tri[2] = {&L, &U};
+  StPlan<T> p;
+  size_t smem = 0;
+  const int cs[3] = {(int)sizeof(T), MODE == kStSpmv ? 0 : (int)sizeof(B), 0};
+  if (L.sk != U.sk || !st_aligned(x) || !st_aligned(d) || (MODE != kStSpmv && !st_aligned(b)) ||
+      !st_plan<T>(tri, 2, true, n, cs, p, smem))
+    return false;
+  const int grid = (int)((n + p.rows - 1) / p.rows);
+  switch (L.sk) {
+#define RS_ST_RESID(KK)                                                                   \
+  case KK:                                                                                \
+    st_smem_attr(k_st_resid<T, MODE, KK, B>, device);                                      \
+    k_st_resid<T, MODE, KK, B><<<grid, kStThreads, smem, st>>>(p, d, x, b, out, w);       \
+    return true;
+    RS_ST_RESID(1)
+    RS_ST_RESID(2)
+    RS_ST_RESID(3)
+    RS_ST_RESID(4)
+#undef RS_ST_RESID
+    default:
+      return false;
+  }
+}
+
+// one inner step on a stencil triangle Tm (prescaled values); false: not applicable
+template <typename T, int FINAL, bool GAMMA, typename O>
+static bool st_inner(int device, const SellView<T>& Tm, int64_t n, const T* rd, const T* gin, const T* xc, O* out,
+                     T w, T gm, T gm1, cudaStream_t st) {
+  const SellView<T>* tri[1] = {&Tm};
+  StPlan<T> p;
+  size_t smem = 0;
+  const int cs[3] = {(int)sizeof(T), FINAL == kStAdd ? (int)sizeof(T) : 0, 0};
+  if (!st_aligned(gin) || !st_aligned(rd) || (FINAL == kStAdd && !st_aligned(xc)) ||
+      !st_plan<T>(tri, 1, GAMMA, n, cs, p, smem))
+    return false;
+  const int grid = (int)((n + p.rows - 1) / p.rows);
+  switch (Tm.sk) {
+#define RS_ST_INNER(KK)                                                                          \
+  case KK:                                                                                       \
+    st_smem_attr(k_st_inner<T, FINAL, GAMMA, KK, O>, device);                                     \
+    k_st_inner<T, FINAL, GAMMA, KK, O><<<grid, kStThreads, smem, st>>>(p, rd, gin, xc, out, w, gm, gm1); \
+    return true;
+    RS_ST_INNER(1)
+    RS_ST_INNER(2)
+    RS_ST_INNER(3)
+    RS_ST_INNER(4)
+#undef RS_ST_INNER
+    default:
+      return false;
+  }
+}
+
+}  // namespace rs

@@ -193,6 +193,20 @@ class DeviceMatrix:
                C.byref(h))
         return cls(h.value, dev)
 
+    def layout(self, which: int) -> dict:
+        """Storage of triangle `which` (0 L, 1 U, 2 E_lo, 3 E_hi): uniform slice width (-1: varying),
+        diagonal-slice entries per slice (0: explicit slots), padded slots, slices, stencil offsets
+        (0: no stencil encoding)."""
+        out = (C.c_int64 * 5)()
+        N.call("rs_mat_layout", self._h, which, C.cast(out, C.c_void_p))
+        return {"uniform_width": int(out[0]), "dia_k": int(out[1]), "slots": int(out[2]), "slices": int(out[3]),
+                "stencil_k": int(out[4])}
+
+    def set_diagonal_slices(self, enable: bool) -> None:
+        """Drop / rebuild the diagonal-slice and stencil encodings of L and U (A/B switch; results are
+        bitwise the same)."""
+        N.call("rs_mat_set_dia", self._h, 1 if enable else 0)
+
     def single(self) -> "DeviceMatrix":
         """float32 copy with float32 splitting (cast_matrix + extract_splitting, krylov.py:101-103)."""
         if self.dtype == np.float32:
