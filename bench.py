@@ -51,13 +51,22 @@ METRIC = "GMRES+GS2 time-to-solution & GS2 sweep GB/s vs HBM peak at 1/2/4/8 B20
 
 # ---------------------------------------------------------------- byte model
 class Model:
-    """Algorithmic bytes of each kernel of the path (split-CSR, int32 idx, fp64 values, each operand once)."""
+    """Algorithmic bytes of each kernel of the path (each operand once per pass).
 
-    def __init__(self, n: int, nnz_l: int, nnz_u: int, val_bytes: int = 8):
+    Matrix bytes per triangle: split-CSR (int32 idx, fp64 values, the SURVEY §8(d) figure) or, for a
+    stencil-encoded triangle (rs_mat_layout stencil_k > 0: constant-coefficient stencils such as
+    laplace3d / convdiff3d), the 32-byte lane-mask row of each 32-row slice the kernels read (offsets
+    and values are kernel parameters)."""
+
+    def __init__(self, n: int, nnz_l: int, nnz_u: int, val_bytes: int = 8, stencil: bool = False):
         self.n = n
         self.V = 8 * n
-        self.ML = (4 + val_bytes) * nnz_l + 4 * (n + 1)
-        self.MU = (4 + val_bytes) * nnz_u + 4 * (n + 1)
+        self.stencil = stencil
+        if stencil:
+            self.ML = self.MU = 32 * ((n + 31) // 32)
+        else:
+            self.ML = (4 + val_bytes) * nnz_l + 4 * (n + 1)
+            self.MU = (4 + val_bytes) * nnz_u + 4 * (n + 1)
 
     def spmv(self):
         return self.ML + self.MU + 3 * self.V
@@ -234,7 +243,8 @@ class CpuSample:
         self.w = np.empty(n)
         self.z = np.empty(n)
         n_, nl, nu = laplace3d_nnz(nx, nx, nx)
-        self.mod = Model(n_, nl, nu)
+        # the B200 arm's byte count for the same work: laplace3d's triangles are stencil-encoded there
+        self.mod = Model(n_, nl, nu, stencil=True)
 
     def js(self, k: int):
         return [min(self.m - 1, int((s + 0.5) * self.m / k)) for s in range(k)]
@@ -348,9 +358,12 @@ def ours(args):
     n = a.nrows
     b = g2.random_rhs(n, 0, device=f"cuda:{local}")
     pc = g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, n_j))
-    mod = Model(n, a.nnz_l, a.nnz_u)
+    layout = {"L": a.layout(0), "U": a.layout(1)}
+    stencil = layout["L"]["stencil_k"] > 0 and layout["U"]["stencil_k"] > 0
+    mod = Model(n, a.nnz_l, a.nnz_u, stencil=stencil)
+    mod_csr = Model(n, a.nnz_l, a.nnz_u)
     actual_bytes = mod.cycle_actual(m, n_j)
-    model_bytes = mod.cycle(m, n_j)
+    model_bytes = mod_csr.cycle(m, n_j)
     hbm, peak_kind = peaks()
 
     def step():
@@ -432,7 +445,7 @@ def ours(args):
     e2e = {"value": round(actual_bytes / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
            "d2h_bytes_per_step": 8 * n, "ms_per_step": round(e2e_ms, 3), "ms_steps": e2e_steps}
 
-    sweeps = sweep_table(g2, torch, a, mod, hbm, setup) if not args.no_sweeps else None
+    sweeps = sweep_table(g2, torch, a, mod, hbm, setup, mod_csr=mod_csr) if not args.no_sweeps else None
     tts = None
     if not args.no_tts:
         torch.cuda.synchronize()
@@ -456,7 +469,7 @@ def ours(args):
         a5 = g2.laplace3d(512, device=local)
         b5 = g2.random_rhs(a5.nrows, 0, device=f"cuda:{local}")
         pc5 = g2.Preconditioner(a5, "gs2", g2.RelaxConfig(1, 1, n_j))
-        mod5 = Model(a5.nrows, a5.nnz_l, a5.nnz_u)
+        mod5 = Model(a5.nrows, a5.nnz_l, a5.nnz_u, stencil=a5.layout(0)["stencil_k"] > 0)
         g2.gmres(a5, b5, pc5, restart=m, tol=1e-300, maxit=m)
         torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -496,16 +509,19 @@ def ours(args):
                                f"zero-start preconditioner, b = random_rhs(n, 0)",
                    "ortho": "dcgs2 (CGS2 with delayed re-orthogonalisation, 2 basis passes per step)",
                    "bytes_per_step": actual_bytes,
+                   "matrix_layout": layout,
                    "bytes_note": "value = algorithmic bytes of the launched kernel sequence (fused passes counted "
                                  "once) / device time: the whole-cycle HBM throughput",
                    "model_bytes_per_step": model_bytes,
                    "model_gbs": round(model_bytes / (ms * 1e-3) / 1e9, 1),
-                   "model_note": "SURVEY §8(d) model of the cycle (unfused CGS2, 4 basis reads per step): a fixed "
+                   "model_note": "SURVEY §8(d) model of the cycle (split-CSR matrix bytes, unfused CGS2, 4 basis "
+                                 "reads per step): a fixed work figure; with the stencil-encoded triangles and the "
+                                 "fused DCGS2 passes the kernels move fewer bytes, so model_gbs exceeds the HBM peak; "
                                  "work figure, exceeds the HBM peak because the fused kernels move fewer bytes",
                    "ms_per_iteration": round(ms / m, 4),
                    "iterations_per_s": round(m / (ms * 1e-3), 1),
                    "row_iterations_per_s": round(n * m / (ms * 1e-3)),
-                   "l2": "inputs larger than L2 (V basis 61 x 134 MB, matrix 1.7 GB)", "parallelism": "1 GPU",
+                   "l2": "inputs larger than L2 (V basis 61 x 134 MB, vectors 134 MB each)", "parallelism": "1 GPU",
                    "scaling_note": "N > 1 lines run C5 (laplace3d 512^3 in N z-slabs, fixed total problem); the "
                                    "512^3 cycle on this one GPU is c5_one_gpu"},
         "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
@@ -589,9 +605,12 @@ def secondary_configs(g2, torch):
     return out
 
 
-def sweep_table(g2, torch, a, mod, hbm, setup=None, reps: int = 10):
+def sweep_table(g2, torch, a, mod, hbm, setup=None, reps: int = 10, mod_csr=None):
     """Same-device comparison of the paper's relaxations on x != 0 (b = rhs(0), x = rhs(1)).
-    ``setup`` receives the one-off analysis costs the baselines pay (level sets, colouring)."""
+    ``setup`` receives the one-off analysis costs the baselines pay (level sets, colouring).
+    The GS2 / JR / SpMV rows run on the handle's default layout (stencil-encoded triangles for
+    laplace3d, bytes from ``mod``) and again on the explicit SELL slots (``explicit``: the
+    split-CSR kernels every non-stencil matrix runs, bytes from ``mod_csr``)."""
     n = a.nrows
     dev = a.torch_device
     b = g2.random_rhs(n, 0, device=dev)
@@ -621,23 +640,40 @@ def sweep_table(g2, torch, a, mod, hbm, setup=None, reps: int = 10):
             r["frac"] = round(nbytes / (ms * 1e-3) / 1e9 / hbm, 3)
         return r
 
-    for nj in range(4):
-        cfg = g2.RelaxConfig(1, 1, nj)
-        out[f"gs2_nj{nj}"] = timeit(lambda x, cfg=cfg: g2.gs2_apply(a, s, b, x, cfg), mod.gs2_sweep(nj))
-    out["jr"] = timeit(lambda x: g2.jr_sweeps(a, s, b, x, 1), mod.gs2_sweep(0))
+    y = torch.empty_like(b)
+
+    def streaming_rows(md):
+        rows = {}
+        for nj in range(4):
+            cfg = g2.RelaxConfig(1, 1, nj)
+            rows[f"gs2_nj{nj}"] = timeit(lambda x, cfg=cfg: g2.gs2_apply(a, s, b, x, cfg), md.gs2_sweep(nj))
+        rows["jr"] = timeit(lambda x: g2.jr_sweeps(a, s, b, x, 1), md.gs2_sweep(0))
+        rows["spmv"] = timeit(lambda x: g2.spmv(a, x, out=y), md.spmv())
+        return rows
+
+    out.update(streaming_rows(mod))
+    if mod_csr is not None and mod.stencil:
+        a.set_diagonal_slices(False)
+        try:
+            out["explicit"] = streaming_rows(mod_csr)
+            out["explicit"]["note"] = "same sweeps on the explicit SELL-32 slots (split-CSR bytes)"
+        finally:
+            a.set_diagonal_slices(True)
+    out["layout_note"] = ("default rows: " + ("stencil-encoded triangles (lane masks per slice; bytes = vectors + "
+                                              "masks)" if mod.stencil else "explicit SELL-32 slots"))
     out["gs_level_sched"] = timeit(lambda x: g2.gs_sequential_sweep(a, s, b, x, "forward"),
-                                   mod.ML + mod.MU + 3 * mod.V, "level_set_analysis_plus_first_sweep_s")
+                                   (mod_csr or mod).ML + (mod_csr or mod).MU + 3 * mod.V,
+                                   "level_set_analysis_plus_first_sweep_s")
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     coloring = g2.greedy_color(a)
     torch.cuda.synchronize()
     if setup is not None:
         setup["greedy_coloring_s"] = round(time.perf_counter() - t0, 4)
-    out["mt_gs"] = timeit(lambda x: g2.mt_gs_sweep(a, s, coloring, b, x, "forward"), mod.ML + mod.MU + 3 * mod.V,
+    out["mt_gs"] = timeit(lambda x: g2.mt_gs_sweep(a, s, coloring, b, x, "forward"),
+                          (mod_csr or mod).ML + (mod_csr or mod).MU + 3 * mod.V,
                           "mt_colour_ordered_slices_plus_first_sweep_s")
     out["mt_gs"]["colors"] = coloring.num_colors
-    y = torch.empty_like(b)
-    out["spmv"] = timeit(lambda x: g2.spmv(a, x, out=y), mod.spmv())
     # smoother mode (row a14): GS2(1,1,1) applications WITH the per-application residual history
     # (fused into the next application's residual pass); compare with gs2_nj1 (no history)
     cfg1 = g2.RelaxConfig(1, 1, 1)

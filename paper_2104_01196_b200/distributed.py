@@ -548,7 +548,8 @@ def bench_rank(args, metric, Model, laplace3d_nnz, ClockSampler, peaks):
     mod = Model(n, nl, nu)
     model_bytes = mod.cycle(m, 1)
     # this rank's slab: its own rows, its L / U entries (the slab-coupling entries live in E_lo / E_hi)
-    local_mod = Model(A.nrows, A.dm.nnz_l, A.dm.nnz_u)
+    local_mod = Model(A.nrows, A.dm.nnz_l, A.dm.nnz_u,
+                      stencil=A.dm.layout(0)["stencil_k"] > 0 and A.dm.layout(1)["stencil_k"] > 0)
     local_actual = local_mod.cycle_actual(m, 1)
     # value's numerator: the algorithmic bytes of every rank's launched kernels
     actual_bytes = sum(comm.allgather_obj(int(local_actual)))
