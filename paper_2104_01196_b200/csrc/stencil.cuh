@@ -112,28 +112,6 @@ __device__ __forceinline__ T st_at(const StPlan<T>& p, const StShared& S, const 
   return (unsigned)r < (unsigned)S.wl[g] ? sx[p.wsm[g] + r] : gv[j];
 }
 
-// acc += sum over the K offsets of triangle q present in row i (mask word m[tt] bit lane).
-// Interior tiles: operand of slot tt for tile row t = sx[t + base[tt]] (st_bases), read for every
-// slot and selected by the mask bit (no branches); other tiles: checked window / global reads.
-template <typename T, int K>
-__device__ __forceinline__ T st_tri_accum(const StPlan<T>& p, const StShared& S, const T* sx,
-                                          const T* __restrict__ gv, int q, const uint32_t* m, const int* base, int t,
-                                          int i, bool interior, T acc) {
-  const uint32_t bit = 1u << (i & 31);
-  if (interior) {
-#pragma unroll
-    for (int tt = 0; tt < K; ++tt) {
-      const T s = add_rn<T>(acc, mul_rn<T>(p.val[q][tt], sx[t + base[tt]]));
-      acc = (m[tt] & bit) ? s : acc;
-    }
-  } else {
-#pragma unroll
-    for (int tt = 0; tt < K; ++tt)
-      if (m[tt] & bit) acc = add_rn<T>(acc, mul_rn<T>(p.val[q][tt], st_at<T>(p, S, sx, gv, p.win[q][tt], i + p.off[q][tt])));
-  }
-  return acc;
-}
-
 // base[tt]: shared-memory element index of slot tt's operand of tile row 0 (interior tiles)
 template <typename T, int K>
 __device__ __forceinline__ void st_bases(const StPlan<T>& p, const StShared& S, int q, int r0, int* base) {
@@ -162,10 +140,12 @@ __device__ __forceinline__ void st_masks(const unsigned char* sm, int off, int t
 }
 
 // One tile per CTA: thread 0 plans the tile's windows and issues its bulk copies on one mbarrier,
-// the CTA waits, then tile_fn(shared-memory base, StShared, r0) computes the rows.  (Persistent
-// 2-stage and warp-specialised 2..8-stage rings measured no faster: 0.12-0.26 ms for the 256^3 SpMV
-// vs 0.115 ms; the pass is bound by the L2 slices' throughput -- every operand window crosses L2 --
-// not by bytes in flight.)
+// the CTA waits, then tile_fn(shared-memory base, StShared, r0) computes the rows.  Measured
+// alternatives, all slower for the 256^3 SpMV (0.115-0.12 ms here): a persistent 2-stage ring and a
+// warp-specialised 2..8-stage ring (0.12-0.26 ms), and plane marching -- a CTA walks one column of
+// tiles through the planes so the +-P operands come from the neighbouring planes' stages, 35% less
+// L2 traffic, 0.14 ms: 16 warps per SM and the per-plane bookkeeping leave it issue-bound
+// (profiles/r02_stencil_notes.md).
 template <typename T, typename C0, typename C1, typename C2, typename F>
 __device__ __forceinline__ void st_pipeline(const StPlan<T>& p, int ntri, const T* __restrict__ gv, const C0* c0,
                                             const C1* c1, const C2* c2, F&& tile_fn) {
@@ -184,9 +164,146 @@ __device__ __forceinline__ void st_pipeline(const StPlan<T>& p, int ntri, const 
 }
 
 enum StResidMode { kStSpmv = 0, kStResidRd = 1, kStJr = 2 };
+enum StInnerFinal { kStMid = 0, kStSet = 1, kStAdd = 2 };
 
-// Full-row pass A x over a stencil L | D | U (both triangles K offsets): y = A x, rd = (b - A x) / d,
-// or the JR update x + w (b - A x) / d -- k_resid's MODEs, same operation forms.
+// The rows of one tile of a full-row pass A x over a stencil L | D | U (both triangles K offsets):
+// y = A x, rd = (b - A x) / d, or the JR update x + w (b - A x) / d -- k_resid's MODEs, same
+// operation forms.  smc: the tile's stage (masks at p.sm_mask, d at p.sm_c[0], b at p.sm_c[1]);
+// interior tiles read slot tt's operand of tile row t at sx[t + bL/bU[tt]] and x[i] at sx[t + bc];
+// other tiles call opnd(q, tt, i) (q = 2: x[i]).
+template <typename T, int MODE, int K, typename B, int NT, typename Op>
+__device__ __forceinline__ void st_resid_tile(const StPlan<T>& p, const unsigned char* smc, const T* sx,
+                                              const int* bL, const int* bU, int bc, bool interior, int clen,
+                                              int r0, Op&& opnd, const T* __restrict__ d,
+                                              const B* __restrict__ b, T* __restrict__ out, T w) {
+  const T* sd = reinterpret_cast<const T*>(smc + p.sm_c[0]);
+  const B* sb = reinterpret_cast<const B*>(smc + p.sm_c[1]);
+  auto finish = [&](int i, T acc, T di, T xi, B bi) {
+    if (MODE == kStSpmv) {
+      out[i] = acc;
+    } else {
+      const T g = div_rn<T>(sub_rn<T>((T)bi, acc), di);
+      out[i] = MODE == kStResidRd ? g : add_rn<T>(xi, mul_rn<T>(w, g));
+    }
+  };
+  if (interior) {
+    // every operand in shared memory, centers staged: no bounds checks; a warp = one slice, so a
+    // slice whose rows all hold every offset (the stencil's interior) adds without selects
+    for (int t = threadIdx.x; t < p.rows; t += NT) {
+      const int i = r0 + t;
+      uint32_t mL[K], mU[K];
+      st_masks<K>(smc, p.sm_mask, t, mL);
+      st_masks<K>(smc, p.sm_mask + p.rows, t, mU);
+      uint32_t all = 0xffffffffu;
+#pragma unroll
+      for (int tt = 0; tt < K; ++tt) all &= mL[tt] & mU[tt];
+      const T* px = sx + t;
+      const T di = sd[t], xi = px[bc];
+      T acc = (T)0;
+      const uint32_t bit = 1u << (i & 31);
+      if (all == 0xffffffffu) {
+#pragma unroll
+        for (int tt = 0; tt < K; ++tt) acc = add_rn<T>(acc, mul_rn<T>(p.val[0][tt], px[bL[tt]]));
+        acc = add_rn<T>(acc, mul_rn<T>(di, xi));
+#pragma unroll
+        for (int tt = 0; tt < K; ++tt) acc = add_rn<T>(acc, mul_rn<T>(p.val[1][tt], px[bU[tt]]));
+      } else {
+#pragma unroll
+        for (int tt = 0; tt < K; ++tt) {
+          const T s = add_rn<T>(acc, mul_rn<T>(p.val[0][tt], px[bL[tt]]));
+          acc = (mL[tt] & bit) ? s : acc;
+        }
+        acc = add_rn<T>(acc, mul_rn<T>(di, xi));
+#pragma unroll
+        for (int tt = 0; tt < K; ++tt) {
+          const T s = add_rn<T>(acc, mul_rn<T>(p.val[1][tt], px[bU[tt]]));
+          acc = (mU[tt] & bit) ? s : acc;
+        }
+      }
+      finish(i, acc, di, xi, MODE == kStSpmv ? (B)0 : sb[t]);
+    }
+    return;
+  }
+  for (int t = threadIdx.x; t < p.rows; t += NT) {
+    const int i = r0 + t;
+    if (i >= p.n) break;
+    uint32_t mL[K], mU[K];
+    st_masks<K>(smc, p.sm_mask, t, mL);
+    st_masks<K>(smc, p.sm_mask + p.rows, t, mU);
+    const uint32_t bit = 1u << (i & 31);
+    const T di = t < clen ? sd[t] : d[i];
+    const T xi = opnd(2, 0, i);
+    T acc = (T)0;
+#pragma unroll
+    for (int tt = 0; tt < K; ++tt)
+      if (mL[tt] & bit) acc = add_rn<T>(acc, mul_rn<T>(p.val[0][tt], opnd(0, tt, i)));
+    acc = add_rn<T>(acc, mul_rn<T>(di, xi));
+#pragma unroll
+    for (int tt = 0; tt < K; ++tt)
+      if (mU[tt] & bit) acc = add_rn<T>(acc, mul_rn<T>(p.val[1][tt], opnd(1, tt, i)));
+    finish(i, acc, di, xi, MODE == kStSpmv ? (B)0 : (t < clen ? sb[t] : b[i]));
+  }
+}
+
+// The rows of one tile of an inner JR step over a stencil triangle (prescaled values): g = rd - w
+// (D^-1 T gin) (damped: (1-gm) gin + gm (...)); out = g (kStMid), w g (kStSet) or x + w g (kStAdd),
+// written as O -- k_inner / k_inner_out's forms.  smc: rd at p.sm_c[0], x at p.sm_c[1]; opnd(2, 0, i)
+// = gin[i].
+template <typename T, int FINAL, bool GAMMA, int K, typename O, int NT, typename Op>
+__device__ __forceinline__ void st_inner_tile(const StPlan<T>& p, const unsigned char* smc, const T* sx,
+                                              const int* bT, int bc, bool interior, int clen, int r0, Op&& opnd,
+                                              const T* __restrict__ rd, const T* __restrict__ xc,
+                                              O* __restrict__ out, T w, T gm, T gm1) {
+  const T* srd = reinterpret_cast<const T*>(smc + p.sm_c[0]);
+  const T* sxc = reinterpret_cast<const T*>(smc + p.sm_c[1]);
+  auto finish = [&](int i, T tsum, T rdi, T gi, T xci) {
+    T g = sub_rn<T>(rdi, mul_rn<T>(w, tsum));
+    if (GAMMA) g = add_rn<T>(mul_rn<T>(gm1, gi), mul_rn<T>(gm, g));
+    if (FINAL == kStMid) out[i] = (O)g;
+    else if (FINAL == kStSet) out[i] = (O)mul_rn<T>(w, g);
+    else out[i] = (O)add_rn<T>(xci, mul_rn<T>(w, g));
+  };
+  if (interior) {
+    for (int t = threadIdx.x; t < p.rows; t += NT) {
+      const int i = r0 + t;
+      uint32_t m[K];
+      st_masks<K>(smc, p.sm_mask, t, m);
+      uint32_t all = 0xffffffffu;
+#pragma unroll
+      for (int tt = 0; tt < K; ++tt) all &= m[tt];
+      const T* px = sx + t;
+      T tsum = (T)0;
+      if (all == 0xffffffffu) {
+#pragma unroll
+        for (int tt = 0; tt < K; ++tt) tsum = add_rn<T>(tsum, mul_rn<T>(p.val[0][tt], px[bT[tt]]));
+      } else {
+        const uint32_t bit = 1u << (i & 31);
+#pragma unroll
+        for (int tt = 0; tt < K; ++tt) {
+          const T s = add_rn<T>(tsum, mul_rn<T>(p.val[0][tt], px[bT[tt]]));
+          tsum = (m[tt] & bit) ? s : tsum;
+        }
+      }
+      finish(i, tsum, srd[t], GAMMA ? px[bc] : (T)0, FINAL == kStAdd ? sxc[t] : (T)0);
+    }
+    return;
+  }
+  for (int t = threadIdx.x; t < p.rows; t += NT) {
+    const int i = r0 + t;
+    if (i >= p.n) break;
+    uint32_t m[K];
+    st_masks<K>(smc, p.sm_mask, t, m);
+    const uint32_t bit = 1u << (i & 31);
+    T tsum = (T)0;
+#pragma unroll
+    for (int tt = 0; tt < K; ++tt)
+      if (m[tt] & bit) tsum = add_rn<T>(tsum, mul_rn<T>(p.val[0][tt], opnd(0, tt, i)));
+    finish(i, tsum, t < clen ? srd[t] : rd[i], GAMMA ? opnd(2, 0, i) : (T)0,
+           FINAL == kStAdd ? (t < clen ? sxc[t] : xc[i]) : (T)0);
+  }
+}
+
+// ---- one tile per CTA, operand windows of the tile (st_pipeline)
 template <typename T, int MODE, int K, typename B>
 __global__ void __launch_bounds__(kStThreads) k_st_resid(StPlan<T> p, const T* __restrict__ d,
                                                         const T* __restrict__ x, const B* __restrict__ b,
@@ -194,71 +311,19 @@ __global__ void __launch_bounds__(kStThreads) k_st_resid(StPlan<T> p, const T* _
   st_pipeline<T, T, B, T>(p, 2, x, d, MODE == kStSpmv ? (const B*)nullptr : b, (const T*)nullptr,
                           [&](unsigned char* sm, const StShared& S, int r0) {
     const T* sx = st_ptr<T>(sm, 0);
-    const T* sd = st_ptr<T>(sm, p.sm_c[0]);
-    const B* sb = reinterpret_cast<const B*>(sm + p.sm_c[1]);
     int bL[K], bU[K];
     st_bases<T, K>(p, S, 0, r0, bL);
     st_bases<T, K>(p, S, 1, r0, bU);
     const int bc = p.wsm[p.wcen] - S.ws[p.wcen] + r0;
-    auto finish = [&](int i, T acc, T di, T xi, B bi) {
-      if (MODE == kStSpmv) {
-        out[i] = acc;
-      } else {
-        const T g = div_rn<T>(sub_rn<T>((T)bi, acc), di);
-        out[i] = MODE == kStResidRd ? g : add_rn<T>(xi, mul_rn<T>(w, g));
-      }
-    };
-    if (S.interior) {
-      // every operand in its window, centers staged: no bounds checks; a warp = one slice, so a
-      // slice whose rows all hold every offset (the stencil's interior) adds without selects
-      for (int t = threadIdx.x; t < p.rows; t += kStThreads) {
-        const int i = r0 + t;
-        uint32_t mL[K], mU[K];
-        st_masks<K>(sm, p.sm_mask, t, mL);
-        st_masks<K>(sm, p.sm_mask + p.rows, t, mU);
-        uint32_t all = 0xffffffffu;
-#pragma unroll
-        for (int tt = 0; tt < K; ++tt) all &= mL[tt] & mU[tt];
-        const T* px = sx + t;
-        const T di = sd[t], xi = px[bc];
-        T acc = (T)0;
-        if (all == 0xffffffffu) {
-#pragma unroll
-          for (int tt = 0; tt < K; ++tt) acc = add_rn<T>(acc, mul_rn<T>(p.val[0][tt], px[bL[tt]]));
-          acc = add_rn<T>(acc, mul_rn<T>(di, xi));
-#pragma unroll
-          for (int tt = 0; tt < K; ++tt) acc = add_rn<T>(acc, mul_rn<T>(p.val[1][tt], px[bU[tt]]));
-        } else {
-          acc = st_tri_accum<T, K>(p, S, sx, x, 0, mL, bL, t, i, true, acc);
-          acc = add_rn<T>(acc, mul_rn<T>(di, xi));
-          acc = st_tri_accum<T, K>(p, S, sx, x, 1, mU, bU, t, i, true, acc);
-        }
-        finish(i, acc, di, xi, MODE == kStSpmv ? (B)0 : sb[t]);
-      }
-      return;
-    }
-    const int clen = S.clen;
-    for (int t = threadIdx.x; t < p.rows; t += kStThreads) {
-      const int i = r0 + t;
-      if (i >= p.n) break;
-      uint32_t mL[K], mU[K];
-      st_masks<K>(sm, p.sm_mask, t, mL);
-      st_masks<K>(sm, p.sm_mask + p.rows, t, mU);
-      const T di = t < clen ? sd[t] : d[i];
-      const T xi = st_at<T>(p, S, sx, x, p.wcen, i);
-      T acc = st_tri_accum<T, K>(p, S, sx, x, 0, mL, bL, t, i, false, (T)0);
-      acc = add_rn<T>(acc, mul_rn<T>(di, xi));
-      acc = st_tri_accum<T, K>(p, S, sx, x, 1, mU, bU, t, i, false, acc);
-      finish(i, acc, di, xi, MODE == kStSpmv ? (B)0 : (t < clen ? sb[t] : b[i]));
-    }
+    st_resid_tile<T, MODE, K, B, kStThreads>(p, sm, sx, bL, bU, bc, S.interior != 0, S.clen, r0,
+                                 [&](int q, int tt, int i) {
+                                   return q == 2 ? st_at<T>(p, S, sx, x, p.wcen, i)
+                                                 : st_at<T>(p, S, sx, x, p.win[q][tt], i + p.off[q][tt]);
+                                 },
+                                 d, b, out, w);
   });
 }
 
-enum StInnerFinal { kStMid = 0, kStSet = 1, kStAdd = 2 };
-
-// One inner JR step over a stencil triangle (prescaled values): g = rd - w (D^-1 T gin) (damped:
-// (1-gm) gin + gm (...)); out = g (kStMid), w g (kStSet) or x + w g (kStAdd), written as O --
-// k_inner / k_inner_out's forms.
 template <typename T, int FINAL, bool GAMMA, int K, typename O>
 __global__ void __launch_bounds__(kStThreads) k_st_inner(StPlan<T> p, const T* __restrict__ rd,
                                                         const T* __restrict__ gin, const T* __restrict__ xc,
@@ -266,48 +331,16 @@ __global__ void __launch_bounds__(kStThreads) k_st_inner(StPlan<T> p, const T* _
   st_pipeline<T, T, T, T>(p, 1, gin, rd, FINAL == kStAdd ? xc : (const T*)nullptr, (const T*)nullptr,
                           [&](unsigned char* sm, const StShared& S, int r0) {
     const T* sx = st_ptr<T>(sm, 0);
-    const T* srd = st_ptr<T>(sm, p.sm_c[0]);
-    const T* sxc = st_ptr<T>(sm, p.sm_c[1]);
     int bT[K];
     st_bases<T, K>(p, S, 0, r0, bT);
-    auto finish = [&](int i, T tsum, T rdi, T gi, T xci) {
-      T g = sub_rn<T>(rdi, mul_rn<T>(w, tsum));
-      if (GAMMA) g = add_rn<T>(mul_rn<T>(gm1, gi), mul_rn<T>(gm, g));
-      if (FINAL == kStMid) out[i] = (O)g;
-      else if (FINAL == kStSet) out[i] = (O)mul_rn<T>(w, g);
-      else out[i] = (O)add_rn<T>(xci, mul_rn<T>(w, g));
-    };
-    if (S.interior) {
-      const int bc = GAMMA ? p.wsm[p.wcen] - S.ws[p.wcen] + r0 : 0;
-      for (int t = threadIdx.x; t < p.rows; t += kStThreads) {
-        const int i = r0 + t;
-        uint32_t m[K];
-        st_masks<K>(sm, p.sm_mask, t, m);
-        uint32_t all = 0xffffffffu;
-#pragma unroll
-        for (int tt = 0; tt < K; ++tt) all &= m[tt];
-        const T* px = sx + t;
-        T tsum = (T)0;
-        if (all == 0xffffffffu) {
-#pragma unroll
-          for (int tt = 0; tt < K; ++tt) tsum = add_rn<T>(tsum, mul_rn<T>(p.val[0][tt], px[bT[tt]]));
-        } else {
-          tsum = st_tri_accum<T, K>(p, S, sx, gin, 0, m, bT, t, i, true, tsum);
-        }
-        finish(i, tsum, srd[t], GAMMA ? px[bc] : (T)0, FINAL == kStAdd ? sxc[t] : (T)0);
-      }
-      return;
-    }
-    const int clen = S.clen;
-    for (int t = threadIdx.x; t < p.rows; t += kStThreads) {
-      const int i = r0 + t;
-      if (i >= p.n) break;
-      uint32_t m[K];
-      st_masks<K>(sm, p.sm_mask, t, m);
-      const T tsum = st_tri_accum<T, K>(p, S, sx, gin, 0, m, bT, t, i, false, (T)0);
-      finish(i, tsum, t < clen ? srd[t] : rd[i], GAMMA ? st_at<T>(p, S, sx, gin, p.wcen, i) : (T)0,
-             FINAL == kStAdd ? (t < clen ? sxc[t] : xc[i]) : (T)0);
-    }
+    const int bc = GAMMA ? p.wsm[p.wcen] - S.ws[p.wcen] + r0 : 0;
+    st_inner_tile<T, FINAL, GAMMA, K, O, kStThreads>(p, sm, sx, bT, bc, S.interior != 0, S.clen, r0,
+                                         [&](int q, int tt, int i) {
+                                           return q == 2 ? st_at<T>(p, S, sx, gin, p.wcen, i)
+                                                         : st_at<T>(p, S, sx, gin, p.win[q][tt],
+                                                                    i + p.off[q][tt]);
+                                         },
+                                         rd, xc, out, w, gm, gm1);
   });
 }
 

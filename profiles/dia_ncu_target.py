@@ -20,8 +20,15 @@ for _ in range(3):
     g2.spmv(a, x, out=y)
     pc.apply_into(x, z)
 torch.cuda.synchronize()
+b = g2.random_rhs(a.nrows, 0, device=a.torch_device)
+s = g2.extract_splitting(a)
+g2.gs2_apply(a, s, b, y, g2.RelaxConfig(1, 1, 0))
+g2.gs2_apply(a, s, b, y, g2.RelaxConfig(1, 1, 1))
+torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStart()
 g2.spmv(a, x, out=y)
 pc.apply_into(x, z)
+g2.gs2_apply(a, s, b, y, g2.RelaxConfig(1, 1, 0))
+g2.gs2_apply(a, s, b, y, g2.RelaxConfig(1, 1, 1))
 torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStop()

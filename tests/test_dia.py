@@ -55,12 +55,18 @@ CASES = {
     "ela3d_6": lambda: g2.elasticity3d(6),
     "lap3d_20_perturbed": lambda: _perturbed(g2.laplace3d(20)),
     "lap3d_20_slice_scaled": lambda: _slice_scaled(g2.laplace3d(20)),
+    # plane stride 1024 = 4 x 256: the plane-marching kernels (k_zm_*; 37 planes: a partial chunk)
+    "lap3d_32": lambda: g2.laplace3d(32),
+    "lap3d_32x32x37": lambda: g2.laplace3d(32, 32, 37),
+    "cd3d_32": lambda: g2.convdiff3d(32, (50.0, 25.0, 10.0)),
+    "lap3d_32_holes": lambda: _holes(g2.laplace3d(32), 0.1, 5),
 }
 # (diagonal-slice entries, stencil offsets) of (L, U); None: holes (checked separately)
 ENCODED = {"lap3d_37": ((3, 3), (3, 3)), "lap2d_64": ((2, 2), (2, 2)), "cd3d_24": ((3, 3), (3, 3)),
            "lap3d_20_holes": None, "ela3d_6": ((0, 0), (0, 0)),
            "lap3d_20_perturbed": ((0, 3), (0, 3)),  # the perturbed value is in L
-           "lap3d_20_slice_scaled": ((3, 3), (0, 0))}
+           "lap3d_20_slice_scaled": ((3, 3), (0, 0)), "lap3d_32": ((3, 3), (3, 3)),
+           "lap3d_32x32x37": ((3, 3), (3, 3)), "cd3d_32": ((3, 3), (3, 3)), "lap3d_32_holes": None}
 
 
 def _ops(dm, b, x0, single):
@@ -132,7 +138,7 @@ def test_diagonal_slices_row_blocks_and_stencil_handles():
     """Row-block handles (hybrid / multi-GPU z-slabs: local triangles encoded, couplings explicit) and
     device-generated stencils (laplace3d, convdiff3d, fp32) are encoded; hybrid_relax stays bitwise the
     oracle-checked explicit path."""
-    a = g2.laplace3d(24)
+    a = g2.laplace3d(32)  # blocks of 10922 / 10923 rows: partial planes of the plane-marching passes
     n = a.nrows
     blk = g2.DeviceMatrix.from_csr(a, row0=n // 3, nrows=n // 3)
     assert blk.layout(0)["dia_k"] == 3 and blk.layout(1)["dia_k"] == 3
