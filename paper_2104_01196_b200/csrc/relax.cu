@@ -1829,7 +1829,12 @@ static int spmv_t(rs_matrix* m, const T* x, const T* xlo, const T* xhi, T* y, cu
     return RS_ERR_ARG;
   }
   if (c.n) {
-    if (!launch_resid_tma<T, kSpmv>(m, x, (const T*)nullptr, y, (T)0, st))
+    // a row block with off-block couplings on stencil triangles: the TMA-windowed pass adds the
+    // E_lo / E_hi terms in the tiles that hold them
+    StCouple<T> cp = {c.Elo, c.Ehi, xlo, xhi};
+    const bool coupled = !c.Elo.empty || !c.Ehi.empty;
+    if (coupled && st_resid<T, kStSpmv, T>(m->device, c.L, c.U, c.n, c.d, x, (const T*)nullptr, y, (T)0, st, &cp)) {
+    } else if (!launch_resid_tma<T, kSpmv>(m, x, (const T*)nullptr, y, (T)0, st))
       k_resid<T, kSpmv><<<c.grid(), kB, 0, st>>>(c.n, c.Elo, c.L, c.U, c.Ehi, c.d, x, xlo, xhi, (const T*)nullptr, y,
                                                  (T)0, pf_dist_host());
     RS_COUNT_LAUNCH();

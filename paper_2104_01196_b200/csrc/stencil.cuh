@@ -164,6 +164,15 @@ __device__ __forceinline__ void st_pipeline(const StPlan<T>& p, int ntri, const 
 }
 
 enum StResidMode { kStSpmv = 0, kStResidRd = 1, kStJr = 2 };
+
+// off-block couplings of a row block (E_lo | ... | E_hi, explicit SELL; empty views when none) and
+// the halo vectors they index
+template <typename T>
+struct StCouple {
+  SellView<T> lo, hi;
+  const T* xlo;
+  const T* xhi;
+};
 enum StInnerFinal { kStMid = 0, kStSet = 1, kStAdd = 2 };
 
 // The rows of one tile of a full-row pass A x over a stencil L | D | U (both triangles K offsets):
@@ -175,7 +184,8 @@ template <typename T, int MODE, int K, typename B, int NT, typename Op>
 __device__ __forceinline__ void st_resid_tile(const StPlan<T>& p, const unsigned char* smc, const T* sx,
                                               const int* bL, const int* bU, int bc, bool interior, int clen,
                                               int r0, Op&& opnd, const T* __restrict__ d,
-                                              const B* __restrict__ b, T* __restrict__ out, T w) {
+                                              const B* __restrict__ b, T* __restrict__ out, T w,
+                                              const StCouple<T>& cp) {
   const T* sd = reinterpret_cast<const T*>(smc + p.sm_c[0]);
   const B* sb = reinterpret_cast<const B*>(smc + p.sm_c[1]);
   auto finish = [&](int i, T acc, T di, T xi, B bi) {
@@ -233,7 +243,7 @@ __device__ __forceinline__ void st_resid_tile(const StPlan<T>& p, const unsigned
     const uint32_t bit = 1u << (i & 31);
     const T di = t < clen ? sd[t] : d[i];
     const T xi = opnd(2, 0, i);
-    T acc = (T)0;
+    T acc = row_accum<T>(cp.lo, i, cp.xlo, (T)0);  // E_lo columns precede the block's own
 #pragma unroll
     for (int tt = 0; tt < K; ++tt)
       if (mL[tt] & bit) acc = add_rn<T>(acc, mul_rn<T>(p.val[0][tt], opnd(0, tt, i)));
@@ -241,6 +251,7 @@ __device__ __forceinline__ void st_resid_tile(const StPlan<T>& p, const unsigned
 #pragma unroll
     for (int tt = 0; tt < K; ++tt)
       if (mU[tt] & bit) acc = add_rn<T>(acc, mul_rn<T>(p.val[1][tt], opnd(1, tt, i)));
+    acc = row_accum<T>(cp.hi, i, cp.xhi, acc);
     finish(i, acc, di, xi, MODE == kStSpmv ? (B)0 : (t < clen ? sb[t] : b[i]));
   }
 }
@@ -307,7 +318,7 @@ __device__ __forceinline__ void st_inner_tile(const StPlan<T>& p, const unsigned
 template <typename T, int MODE, int K, typename B>
 __global__ void __launch_bounds__(kStThreads) k_st_resid(StPlan<T> p, const T* __restrict__ d,
                                                         const T* __restrict__ x, const B* __restrict__ b,
-                                                        T* __restrict__ out, T w) {
+                                                        T* __restrict__ out, T w, StCouple<T> cp) {
   st_pipeline<T, T, B, T>(p, 2, x, d, MODE == kStSpmv ? (const B*)nullptr : b, (const T*)nullptr,
                           [&](unsigned char* sm, const StShared& S, int r0) {
     const T* sx = st_ptr<T>(sm, 0);
@@ -315,12 +326,17 @@ __global__ void __launch_bounds__(kStThreads) k_st_resid(StPlan<T> p, const T* _
     st_bases<T, K>(p, S, 0, r0, bL);
     st_bases<T, K>(p, S, 1, r0, bU);
     const int bc = p.wsm[p.wcen] - S.ws[p.wcen] + r0;
-    st_resid_tile<T, MODE, K, B, kStThreads>(p, sm, sx, bL, bU, bc, S.interior != 0, S.clen, r0,
+    // tiles holding rows with off-block couplings (a row block's first / last plane) take the
+    // checked path, which adds the E_lo / E_hi terms
+    const int ts0 = r0 >> 5, ts1 = (r0 + p.rows) >> 5;
+    const bool coupled = (!cp.lo.empty && ts0 < cp.lo.s_hi && cp.lo.s_lo < ts1) ||
+                         (!cp.hi.empty && ts0 < cp.hi.s_hi && cp.hi.s_lo < ts1);
+    st_resid_tile<T, MODE, K, B, kStThreads>(p, sm, sx, bL, bU, bc, S.interior != 0 && !coupled, S.clen, r0,
                                  [&](int q, int tt, int i) {
                                    return q == 2 ? st_at<T>(p, S, sx, x, p.wcen, i)
                                                  : st_at<T>(p, S, sx, x, p.win[q][tt], i + p.off[q][tt]);
                                  },
-                                 d, b, out, w);
+                                 d, b, out, w, cp);
   });
 }
 
@@ -437,7 +453,10 @@ static void st_smem_attr(Kern k, int device) {
 // false: not applicable (the caller runs k_resid)
 template <typename T, int MODE, typename B>
 static bool st_resid(int device, const SellView<T>& L, const SellView<T>& U, int64_t n, const T* d, const T* x,
-                     const B* b, T* out, T w, cudaStream_t st) {
+                     const B* b, T* out, T w, cudaStream_t st, const StCouple<T>* couple = nullptr) {
+  StCouple<T> cp = {};
+  cp.lo.empty = cp.hi.empty = true;
+  if (couple) cp = *couple;
   const SellView<T>* tri[2] = {&L, &U};
   StPlan<T> p;
   size_t smem = 0;
@@ -450,7 +469,7 @@ static bool st_resid(int device, const SellView<T>& L, const SellView<T>& U, int
 #define RS_ST_RESID(KK)                                                \
   case KK:                                                             \
     st_smem_attr(k_st_resid<T, MODE, KK, B>, device);                  \
-    k_st_resid<T, MODE, KK, B><<<tiles, kStThreads, smem, st>>>(p, d, x, b, out, w); \
+    k_st_resid<T, MODE, KK, B><<<tiles, kStThreads, smem, st>>>(p, d, x, b, out, w, cp); \
     return true;
     RS_ST_RESID(1)
     RS_ST_RESID(2)
