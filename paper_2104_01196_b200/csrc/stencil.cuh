@@ -2,8 +2,8 @@
 //
 // A stencil-encoded triangle is K offsets with one value each plus per-slice lane masks, so a row's
 // operands are the vector at i + offset for each offset.  For a tile of R consecutive rows those
-// are K + 1 contiguous ranges of the gathered vector (offsets closer than kStGap merge into one
-// window): one thread of the CTA copies every window, the tile's lane masks and the tile's own
+// are K + 1 contiguous ranges of the gathered vector (offsets closer than the gap limit merge into
+// one window: a merged window is smaller than the separate ones whenever the gap is below the tile): one thread of the CTA copies every window, the tile's lane masks and the tile's own
 // entries of the row vectors (d, b, rd, x) into shared memory with cp.async.bulk on one mbarrier,
 // and the rows are computed out of shared memory.  The copy engine keeps a whole tile's bytes in
 // flight per CTA without registers -- a row of a constant-coefficient stencil moves only ~24-32
@@ -23,7 +23,11 @@ namespace rs {
 
 constexpr int kStWin = 8;        // windows of the gathered vector
 constexpr int kStThreads = 256;  // threads per CTA; a tile is rows = kStThreads * rows-per-thread
-constexpr int kStGap = 64;       // offsets at most this far apart share a window
+// offsets at most this far apart share a window (RS_ST_GAP; default: the tile's rows)
+static int st_gap(int rows) {
+  static const int v = getenv("RS_ST_GAP") ? atoi(getenv("RS_ST_GAP")) : -1;
+  return v >= 0 ? v : rows;
+}
 
 template <typename T>
 struct StPlan {
@@ -398,7 +402,7 @@ static bool st_plan(const SellView<T>* const* tri, int ntri, bool center, int64_
   offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
   p.nwin = 0;
   for (size_t a = 0; a < offs.size(); ++a) {
-    if (a == 0 || offs[a] - offs[a - 1] > kStGap) {
+    if (a == 0 || offs[a] - offs[a - 1] > st_gap(p.rows)) {
       if (p.nwin == kStWin) return false;
       p.wlo[p.nwin] = p.whi[p.nwin] = offs[a];
       ++p.nwin;
