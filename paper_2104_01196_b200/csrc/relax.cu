@@ -2269,6 +2269,29 @@ int rs_precond_apply(rs_matrix_t m, int kind, const rs_relax_cfg* cfg, const dou
   // fp64 divisions r_k/d_k make the single pass latency-bound (ncu: 40% DRAM,
   // 0.305 ms) and the two-pass rd = r/d ; z = w(rd - w D^-1L rd) is faster
   // (0.239 ms at 256^3) despite its 2V extra bytes.
+  if (single_half_sweep(kind, *cfg) && cfg->n_j == 1 && m->nrows > 0) {
+    // stencil-encoded triangles: rd and the inner step in one TMA-windowed pass
+    const bool bwd = cfg->direction == RS_BACKWARD;
+    const bool damped = cfg->gamma != 1.0;
+    if (m->dtype == RS_F32) {
+      const SellView<float> Tm = view(tri<float>(m, bwd ? 1 : 0), true);
+      if (st_prec1<float, double, double>(m->device, Tm, m->nrows, r, (const float*)m->d, z, (float)cfg->omega,
+                                          (float)cfg->gamma, (float)(1.0 - cfg->gamma), damped,
+                                          (long long*)overflow_flag, st)) {
+        RS_COUNT_LAUNCH();
+        RS_CHECK_LAUNCH("precond");
+        return RS_OK;
+      }
+    } else {
+      const SellView<double> Tm = view(tri<double>(m, bwd ? 1 : 0), true);
+      if (st_prec1<double, double, double>(m->device, Tm, m->nrows, r, (const double*)m->d, z, cfg->omega,
+                                           cfg->gamma, 1.0 - cfg->gamma, damped, nullptr, st)) {
+        RS_COUNT_LAUNCH();
+        RS_CHECK_LAUNCH("precond");
+        return RS_OK;
+      }
+    }
+  }
   if (single_half_sweep(kind, *cfg)) {
     if (m->dtype == RS_F32) return precond_gs2_single<float, double, double>(m, *cfg, r, z, (long long*)overflow_flag, st);
     // (the one-pass k_inner0 for f64 n_j >= 1 measured 0.268 ms vs 0.222 ms two-pass at 256^3: the

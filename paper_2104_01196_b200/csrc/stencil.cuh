@@ -44,6 +44,8 @@ struct StPlan {
   int wcen;                     // window holding offset 0 (-1: none)
   int sm_mask;                  // byte offset of the masks (rows bytes per triangle)
   int sm_c[3];                  // byte offsets of the center vectors
+  int g2size;                   // element bytes of a second gathered vector (same windows), 0: none
+  int wsm2[kStWin];             // byte offsets of its windows
 };
 
 struct StShared {
@@ -63,7 +65,7 @@ __device__ __forceinline__ T* st_ptr(unsigned char* sm, int byte_off) {
 template <typename T, typename C0, typename C1, typename C2>
 __device__ __forceinline__ void st_issue(const StPlan<T>& p, int r0, int ntri, const T* __restrict__ gv,
                                          const C0* c0, const C1* c1, const C2* c2, unsigned char* sm,
-                                         StShared& S, uint64_t* bar) {
+                                         StShared& S, uint64_t* bar, const unsigned char* gv2 = nullptr) {
   constexpr int A = 16 / (int)sizeof(T);
   const int nA = p.n & ~(A - 1);
   uint32_t bytes = 0;
@@ -78,7 +80,7 @@ __device__ __forceinline__ void st_issue(const StPlan<T>& p, int r0, int ntri, c
     const int len = ce > cs ? ce - cs : 0;
     S.ws[g] = cs;
     S.wl[g] = len;
-    bytes += (uint32_t)len * (uint32_t)sizeof(T);
+    bytes += (uint32_t)len * (uint32_t)(sizeof(T) + (gv2 ? p.g2size : 0));
     if (gs0 < 0 || ce < ge0) interior = false;
   }
   // the tile's masks: whole slices (32 bytes each: kStencilMax words)
@@ -97,7 +99,11 @@ __device__ __forceinline__ void st_issue(const StPlan<T>& p, int r0, int ntri, c
   S.interior = interior ? 1 : 0;
   mbar_expect_tx(bar, bytes);
   for (int g = 0; g < p.nwin; ++g)
-    if (S.wl[g]) bulk_g2s(st_ptr<T>(sm, 0) + p.wsm[g], gv + S.ws[g], (uint32_t)S.wl[g] * (uint32_t)sizeof(T), bar);
+    if (S.wl[g]) {
+      bulk_g2s(st_ptr<T>(sm, 0) + p.wsm[g], gv + S.ws[g], (uint32_t)S.wl[g] * (uint32_t)sizeof(T), bar);
+      if (gv2)
+        bulk_g2s(sm + p.wsm2[g], gv2 + (size_t)S.ws[g] * p.g2size, (uint32_t)S.wl[g] * (uint32_t)p.g2size, bar);
+    }
   for (int q = 0; q < ntri; ++q)
     if (nsl > 0) bulk_g2s(sm + p.sm_mask + q * p.rows, p.mask[q] + (size_t)s0 * kStencilMax, (uint32_t)nsl * 32u, bar);
   if (clen) {
@@ -152,7 +158,8 @@ __device__ __forceinline__ void st_masks(const unsigned char* sm, int off, int t
 // (profiles/r02_stencil_notes.md).
 template <typename T, typename C0, typename C1, typename C2, typename F>
 __device__ __forceinline__ void st_pipeline(const StPlan<T>& p, int ntri, const T* __restrict__ gv, const C0* c0,
-                                            const C1* c1, const C2* c2, F&& tile_fn) {
+                                            const C1* c1, const C2* c2, F&& tile_fn,
+                                            const unsigned char* gv2 = nullptr) {
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ StShared S;
   __shared__ __align__(8) uint64_t bar;
@@ -160,7 +167,7 @@ __device__ __forceinline__ void st_pipeline(const StPlan<T>& p, int ntri, const 
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
-    st_issue<T, C0, C1, C2>(p, r0, ntri, gv, c0, c1, c2, sm, S, &bar);
+    st_issue<T, C0, C1, C2>(p, r0, ntri, gv, c0, c1, c2, sm, S, &bar, gv2);
   }
   __syncthreads();
   mbar_wait(&bar, 0);
@@ -364,6 +371,77 @@ __global__ void __launch_bounds__(kStThreads) k_st_inner(StPlan<T> p, const T* _
   });
 }
 
+// The zero-start GS2(1,1,1) preconditioner in one pass (n_j = 1, from z = 0): rd = (T)r / d for
+// every window element (each division once per element, in shared memory, the same operation as the
+// k_scale_rd pass), then z = (O)(w (rd - w D^-1 T rd)) (damped: g = (1-gm) rd + gm (...)) -- the
+// two-pass k_scale_rd + k_inner<kFinalSet> (or k_inner_out's) result bit for bit, without writing and
+// re-reading rd.  r: float64 (single_inside_double: T = float, the cast and its overflow check --
+// own rows only -- fused as in k_scale_rd_f32x2).
+template <typename T, typename R, typename O, bool GAMMA, int K>
+__global__ void __launch_bounds__(kStThreads) k_st_prec1(StPlan<T> p, const R* __restrict__ r, const T* __restrict__ d,
+                                                        O* __restrict__ z, T w, T gm, T gm1,
+                                                        long long* __restrict__ overflow) {
+  st_pipeline<T, T, T, T>(p, 1, d, (const T*)nullptr, (const T*)nullptr, (const T*)nullptr,
+                          [&](unsigned char* sm, const StShared& S, int r0) {
+    T* sx = reinterpret_cast<T*>(sm);
+    // rd over the windows, in place over the d windows
+    for (int g = 0; g < p.nwin; ++g) {
+      const R* rw = reinterpret_cast<const R*>(sm + p.wsm2[g]);
+      T* dw = sx + p.wsm[g];
+      const int ws = S.ws[g], wl = S.wl[g];
+      for (int e = threadIdx.x; e < wl; e += kStThreads) {
+        const R rv = rw[e];
+        const T tv = (T)rv;
+        if (sizeof(T) < sizeof(R) && overflow && g == p.wcen && ws + e >= r0 && ws + e < r0 + p.rows &&
+            isinf((float)tv) && isfinite((double)rv))
+          atomicMin(overflow, (long long)(ws + e));
+        dw[e] = div_rn<T>(tv, dw[e]);
+      }
+    }
+    __syncthreads();
+    auto rd_at = [&](int j) -> T {  // rd_j outside the windows (vector ends only)
+      return div_rn<T>((T)r[j], d[j]);
+    };
+    const bool interior = S.interior != 0;
+    int bT[K];
+    st_bases<T, K>(p, S, 0, r0, bT);
+    const int bc = p.wsm[p.wcen] - S.ws[p.wcen] + r0;
+    for (int t = threadIdx.x; t < p.rows; t += kStThreads) {
+      const int i = r0 + t;
+      if (i >= p.n) break;
+      uint32_t m[K];
+      st_masks<K>(sm, p.sm_mask, t, m);
+      const uint32_t bit = 1u << (i & 31);
+      T tsum = (T)0, rdi;
+      if (interior) {
+        const T* px = sx + t;
+        rdi = px[bc];
+#pragma unroll
+        for (int tt = 0; tt < K; ++tt) {
+          const T s = add_rn<T>(tsum, mul_rn<T>(p.val[0][tt], px[bT[tt]]));
+          tsum = (m[tt] & bit) ? s : tsum;
+        }
+      } else {
+        auto at = [&](int g, int j) -> T {
+          const int q = j - S.ws[g];
+          return (unsigned)q < (unsigned)S.wl[g] ? sx[p.wsm[g] + q] : rd_at(j);
+        };
+        rdi = at(p.wcen, i);
+        if (sizeof(T) < sizeof(R) && overflow && (unsigned)(i - S.ws[p.wcen]) >= (unsigned)S.wl[p.wcen]) {
+          const R rv = r[i];  // own row outside its window: the cast check here
+          if (isinf((float)(T)rv) && isfinite((double)rv)) atomicMin(overflow, (long long)i);
+        }
+#pragma unroll
+        for (int tt = 0; tt < K; ++tt)
+          if (m[tt] & bit) tsum = add_rn<T>(tsum, mul_rn<T>(p.val[0][tt], at(p.win[0][tt], i + p.off[0][tt])));
+      }
+      T g = sub_rn<T>(rdi, mul_rn<T>(w, tsum));
+      if (GAMMA) g = add_rn<T>(mul_rn<T>(gm1, rdi), mul_rn<T>(gm, g));
+      z[i] = (O)mul_rn<T>(w, g);
+    }
+  }, reinterpret_cast<const unsigned char*>(r));
+}
+
 // ------------------------------------------------------------------ host planning / launch
 static int st_rows_per_tile() {
   static const int v = getenv("RS_ST_ROWS") ? atoi(getenv("RS_ST_ROWS")) : 1024;
@@ -379,7 +457,7 @@ static bool st_enabled() {
 // per-row vectors staged (0: not staged).
 template <typename T>
 static bool st_plan(const SellView<T>* const* tri, int ntri, bool center, int64_t n, const int* csize,
-                    StPlan<T>& p, size_t& smem) {
+                    StPlan<T>& p, size_t& smem, int g2size = 0) {
   if (!st_enabled() || n <= 0 || n >= (int64_t)INT32_MAX - (1 << 22)) return false;
   const int K = tri[0]->sk;
   for (int q = 0; q < ntri; ++q)
@@ -426,6 +504,14 @@ static bool st_plan(const SellView<T>* const* tri, int ntri, bool center, int64_
     e = (e + A - 1) / A * A;
   }
   size_t bytes = e * sizeof(T);
+  p.g2size = g2size;
+  if (g2size) {
+    for (int g = 0; g < p.nwin; ++g) {
+      p.wsm2[g] = (int)bytes;
+      bytes += ((size_t)p.rows + (size_t)(p.whi[g] - p.wlo[g]) + 2 * A) * (size_t)g2size;
+      bytes = (bytes + 15) / 16 * 16;
+    }
+  }
   p.sm_mask = (int)bytes;
   bytes += (size_t)ntri * p.rows;  // rows / 32 slices x 32 bytes
   for (int c = 0; c < 3; ++c) {
@@ -508,6 +594,39 @@ static bool st_inner(int device, const SellView<T>& Tm, int64_t n, const T* rd, 
     RS_ST_INNER(3)
     RS_ST_INNER(4)
 #undef RS_ST_INNER
+    default:
+      return false;
+  }
+}
+
+// the zero-start GS2(1,1,1) preconditioner in one pass (k_st_prec1); false: not applicable
+template <typename T, typename R, typename O>
+static bool st_prec1(int device, const SellView<T>& Tm, int64_t n, const R* r, const T* d, O* z, T w, T gm, T gm1,
+                     bool damped, long long* overflow, cudaStream_t st) {
+  static const bool on = !getenv("RS_ST_PREC1") || atoi(getenv("RS_ST_PREC1")) != 0;
+  const SellView<T>* tri[1] = {&Tm};
+  StPlan<T> p;
+  size_t smem = 0;
+  const int cs[3] = {0, 0, 0};
+  if (!on || !st_aligned(r) || !st_aligned(d) || !st_plan<T>(tri, 1, true, n, cs, p, smem, (int)sizeof(R)))
+    return false;
+  const int tiles = (int)((n + p.rows - 1) / p.rows);
+  switch (Tm.sk) {
+#define RS_ST_PREC1(KK)                                                                              \
+  case KK:                                                                                           \
+    if (damped) {                                                                                    \
+      st_smem_attr(k_st_prec1<T, R, O, true, KK>, device);                                           \
+      k_st_prec1<T, R, O, true, KK><<<tiles, kStThreads, smem, st>>>(p, r, d, z, w, gm, gm1, overflow);  \
+    } else {                                                                                         \
+      st_smem_attr(k_st_prec1<T, R, O, false, KK>, device);                                          \
+      k_st_prec1<T, R, O, false, KK><<<tiles, kStThreads, smem, st>>>(p, r, d, z, w, gm, gm1, overflow); \
+    }                                                                                                \
+    return true;
+    RS_ST_PREC1(1)
+    RS_ST_PREC1(2)
+    RS_ST_PREC1(3)
+    RS_ST_PREC1(4)
+#undef RS_ST_PREC1
     default:
       return false;
   }

@@ -9,6 +9,9 @@ Region order (launch indices are what run_ncu_r02.sh's --launch-skip values assu
      residual norm (k_resid<kResidRd, NORM>), level-scheduled GS (k_gs_levels_cta runs +
      k_mt_color_pdl per level)
   2. one GMRES(60) cycle (DCGS2: k_cgs<0,1,0,1> dots+coef and k_cgs<1,0,1,1> update per step)
+The matrix's triangles are stencil-encoded (round 2): the GS2 / JR / SpMV / preconditioner passes of
+phase 1 are the TMA-windowed k_st_resid / k_st_inner; the same five streaming items then run again on
+the explicit SELL-32 slots (DeviceMatrix.set_diagonal_slices(False): k_resid / k_inner / ...).
 
     python profiles/ncu_kernels.py [--phase sweeps|cycle|all]
 """
@@ -52,12 +55,19 @@ sweeps = [
 ]
 
 
+explicit = sweeps[:5]
+
+
 def cycle():
     g2.gmres(a, b, p64, restart=60, tol=1e-300, maxit=60)
 
 
 for fn in sweeps:  # warm-up: level sets, colour-ordered slices, workspaces
     fn()
+a.set_diagonal_slices(False)
+for fn in explicit:
+    fn()
+a.set_diagonal_slices(True)
 cycle()
 torch.cuda.synchronize()
 cudart = torch.cuda.cudart()
@@ -65,6 +75,10 @@ cudart.cudaProfilerStart()
 if args.phase in ("sweeps", "all"):
     for fn in sweeps:
         fn()
+    a.set_diagonal_slices(False)
+    for fn in explicit:
+        fn()
+    a.set_diagonal_slices(True)
 if args.phase in ("cycle", "all"):
     cycle()
 torch.cuda.synchronize()

@@ -6,13 +6,13 @@
 #   C  --set full on the DCGS2 dots+coef / update kernels at k = 31 and k = 60
 #   D  the driver's launch-list recipe on bench.py (cold-cache, serialised per-launch times)
 NCU=/usr/local/cuda/bin/ncu
-OUT=gpurun_out/ncu_r02
+OUT=gpurun_out/${NCU_OUT:-ncu_r02}
 mkdir -p $OUT
-M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,dram__throughput.avg.pct_of_peak_sustained_elapsed
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,dram__throughput.avg.pct_of_peak_sustained_elapsed,lts__t_sectors.sum
 $NCU --profile-from-start off --clock-control none --metrics $M --csv --log-file $OUT/region_metrics.csv \
   python profiles/ncu_kernels.py > $OUT/A.log 2>&1; echo "A rc=$?"
 $NCU --profile-from-start off --clock-control none --set full --import-source on \
-  -k regex:"k_resid|k_inner|k_scale_rd|k_mt_color|k_spmv_red" -c 20 -f -o $OUT/sweeps \
+  -k regex:"k_st_|k_resid|k_inner|k_scale_rd|k_mt_color|k_spmv_red" -c 40 -f -o $OUT/sweeps \
   python profiles/ncu_kernels.py --phase sweeps > $OUT/B.log 2>&1; echo "B rc=$?"
 for skip in 60 118; do
   $NCU --profile-from-start off --clock-control none --set full --import-source on -k regex:k_cgs \
@@ -26,3 +26,6 @@ for r in sweeps dcgs_skip60 dcgs_skip118; do
   $NCU -i $OUT/$r.ncu-rep --page raw --csv > $OUT/$r.raw.csv 2>/dev/null
 done
 ls -la $OUT
+# keep the merged-back output under gpurun's 64 MiB: the CSV exports stay, the binary reports go
+rm -f $OUT/*.ncu-rep
+du -sh $OUT

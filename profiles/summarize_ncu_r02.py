@@ -24,6 +24,7 @@ PEAK = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROO
 
 n, nl, nu = laplace3d_nnz(256, 256, 256)
 mod = Model(n, nl, nu)
+mst = Model(n, nl, nu, stencil=True)  # stencil-encoded triangles: 32 B of lane masks per slice
 V = mod.V
 
 UNIT = {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "s": 1.0, "byte": 1.0, "Kbyte": 1e3,
@@ -53,15 +54,30 @@ def short(k):
 
 groups = collections.OrderedDict()
 for (i, k), m in launches.items():
-    g = groups.setdefault(short(k), {"launches": 0, "s": 0.0, "rd": 0.0, "wr": 0.0})
+    g = groups.setdefault(short(k), {"launches": 0, "s": 0.0, "rd": 0.0, "wr": 0.0, "l2": 0.0})
     g["launches"] += 1
     g["s"] += m["gpu__time_duration.sum"]
     g["rd"] += m["dram__bytes_read.sum"]
     g["wr"] += m["dram__bytes_write.sum"]
+    g["l2"] += 32.0 * m.get("lts__t_sectors.sum", 0.0)
 
 # algorithmic bytes per launch (SURVEY §8(d) per-row figures x rows; 256^3)
 ML = mod.ML
+MS = mst.ML
 model = {
+    "k_st_resid<double, 1, 3, double>": ("stencil GS2 pass 0: rd = (b - Ax)/d", MS + mst.MU + 4 * V),
+    "k_st_inner<double, 2, 0, 3, double>": ("stencil GS2 inner step, last, x += w g", MS + 3 * V),
+    "k_st_resid<double, 2, 3, double>": ("stencil JR sweep", MS + mst.MU + 4 * V),
+    "k_st_resid<double, 0, 3, double>": ("stencil SpMV y = Ax", mst.spmv()),
+    "k_st_inner<double, 1, 0, 3, double>": ("stencil precond inner step, z = w g", MS + 2 * V),
+    "k_st_inner<float, 1, 0, 3, double>": ("stencil fp32 precond inner, z = (double)(w g)", MS + V // 2 + V),
+    "k_st_prec1<double, double, double, 0, 3>": ("stencil zero-start GS2(1,1,1) preconditioner, one pass",
+                                                 MS + 3 * V),
+    "k_st_prec1<float, double, double, 0, 3>": ("stencil fp32-inside-fp64 GS2(1,1,1) preconditioner, one pass",
+                                                MS + 2 * V + V // 2),
+    "k_resid_tma<double, 1>": ("explicit GS2 pass 0 (TMA col/val)", ML + mod.MU + 4 * V),
+    "k_resid_tma<double, 2>": ("explicit JR sweep (TMA col/val)", ML + mod.MU + 4 * V),
+    "k_resid_tma<double, 0>": ("explicit SpMV (TMA col/val)", mod.spmv()),
     "k_resid<double, 1, 0>": ("GS2 pass 0: r = b - Ax, rd = r/d", ML + mod.MU + 4 * V),
     "k_resid<double, 1, 1>": ("GS2 pass 0 + fused ||r||^2 (smoother)", ML + mod.MU + 4 * V),
     "k_resid<double, 2, 0>": ("JR sweep: x' = x + w(b - Ax)/d", ML + mod.MU + 4 * V),
@@ -83,12 +99,15 @@ lines = ["# ncu summary, round 2 (HEAD " + SHA + ")", "",
          "Captures: `profiles/run_ncu_r02.sh` on one B200 (`--clock-control none`; every launch replayed "
          "cold-cache and serialised, so absolute times are the kernel alone at full clock, not the "
          "power-capped in-cycle times of bench.py). Workload: `profiles/ncu_kernels.py` (laplace3d "
-         "256^3: the sweep table once, then one GMRES(60) cycle). Algorithmic bytes: SURVEY §8(d) per-row "
-         "figures x rows (uniform-width slices read no slice pointers: 4(n+1) B per triangle less).", "",
+         "256^3: the sweep table once -- stencil-encoded triangles, then the streaming passes again on the "
+         "explicit SELL-32 slots -- then one GMRES(60) cycle). Algorithmic bytes: SURVEY §8(d) per-row "
+         "figures x rows; stencil-encoded triangles: the 32-B lane-mask row of each 32-row slice instead of "
+         "the split-CSR bytes (uniform-width explicit slices read no slice pointers: 4(n+1) B per triangle "
+         "less). L2 slice traffic = 32 B x lts__t_sectors (hits, misses and writes).", "",
          f"Roofline denominator: {PEAK} GB/s (MEASURED_PEAKS.json, copy).", "",
          "| kernel | computes | launches | avg us | DRAM read+write per launch (GB) | algorithmic (GB) | "
-         "DRAM / algorithmic | achieved GB/s (DRAM) | frac |",
-         "|---|---|---|---|---|---|---|---|---|"]
+         "DRAM / algorithmic | achieved GB/s (DRAM) | frac | L2 slice traffic (GB) | L2 TB/s |",
+         "|---|---|---|---|---|---|---|---|---|---|---|"]
 for name, g in groups.items():
     if name not in model:
         continue
@@ -100,13 +119,14 @@ for name, g in groups.items():
         alg_tot = sum(mod.dcgs_dots(k) if "0, 1, 0, 1" in name else mod.dcgs_update(k) for k in range(1, cnt + 1))
         alg = alg_tot / cnt
     gbs = dram / t / 1e9
+    l2 = g["l2"] / cnt
     lines.append(f"| `{name}` | {what} | {cnt} | {t * 1e6:.1f} | {dram / 1e9:.4f} | {alg / 1e9:.4f} | "
-                 f"{dram / alg:.3f} | {gbs:.0f} | {gbs / PEAK:.3f} |")
+                 f"{dram / alg:.3f} | {gbs:.0f} | {gbs / PEAK:.3f} | {l2 / 1e9:.3f} | {l2 / t / 1e12:.1f} |")
     traffic[name] = {"launches": cnt, "avg_us": round(t * 1e6, 2), "dram_read": g["rd"] / cnt,
-                     "dram_write": g["wr"] / cnt, "model_bytes": alg}
+                     "dram_write": g["wr"] / cnt, "model_bytes": alg, "l2_bytes": l2}
 # bench.py kernel groups (roofline.traffic): the DCGS2 groups
 for grp, name in (("dcgs_dots", "k_cgs<0, 1, 0, 1>"), ("dcgs_update", "k_cgs<1, 0, 1, 1>"),
-                  ("spmv", "k_resid<double, 0, 0>")):
+                  ("spmv", "k_st_resid<double, 0, 3, double>"), ("precond", "k_st_prec1<double, double, double, 0, 3>")):
     if name in traffic:
         traffic[grp] = dict(traffic[name], kernel=name, capture=traffic["capture"])
 lv = groups.get("k_mt_color_pdl<double>")

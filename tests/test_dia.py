@@ -88,11 +88,14 @@ def _ops(dm, b, x0, single):
     xt = torch.from_numpy(x0).cuda()
     g2.jr_sweeps(dm, g2.extract_splitting(dm, omega=0.7), bt, xt, 2)
     out["jr"] = xt.cpu().numpy()
-    for kind, cfg in (("gs2", g2.RelaxConfig(1, 1, 1)), ("gs2", g2.RelaxConfig(1, 1, 3)), ("sgs2", g2.RelaxConfig(1, 1, 2)),
-                      ("jr", g2.RelaxConfig(2, 1, 0))):
+    # (gs2 n_j = 1 from zero: the one-pass k_st_prec1 on stencil triangles, incl. damped / backward)
+    for tag, kind, cfg in (("", "gs2", g2.RelaxConfig(1, 1, 1)), ("", "gs2", g2.RelaxConfig(1, 1, 3)),
+                           ("", "sgs2", g2.RelaxConfig(1, 1, 2)), ("", "jr", g2.RelaxConfig(2, 1, 0)),
+                           ("_gamma", "gs2", g2.RelaxConfig(1, 1, 1, gamma=0.7)),
+                           ("_bwd", "gs2", g2.RelaxConfig(1, 1, 1, direction="backward", omega=0.9))):
         for prec in ("same", "single_inside_double") if single else ("same",):
             m = g2.Preconditioner(dm, kind, cfg, precision=prec)
-            out[f"prec_{kind}_{cfg.n_j}_{prec}"] = m.apply(bt).cpu().numpy()
+            out[f"prec_{kind}_{cfg.n_j}{tag}_{prec}"] = m.apply(bt).cpu().numpy()
     _, h = g2.gmres(dm, bt, g2.Preconditioner(dm, "gs2", g2.RelaxConfig(1, 1, 1)), restart=20, tol=1e-8, maxit=200)
     out["gmres_hist"] = np.asarray(h.rel_res)
     return out
@@ -133,6 +136,8 @@ def test_diagonal_slices_bitwise_explicit_and_oracle(case):
     oracle.gs2_apply(om, b, xo, g2.RelaxConfig(2, 1, 1))
     assert np.array_equal(enc["gs2_1"], xo)
     assert np.array_equal(enc["prec_gs2_1_same"], oracle.Precond(om, "gs2", n_j=1).apply(b))
+    assert np.array_equal(enc["prec_gs2_1_single_inside_double"],
+                          oracle.Precond(om, "gs2", precision="single_inside_double", n_j=1).apply(b))
 
 
 def test_diagonal_slices_row_blocks_and_stencil_handles():
@@ -186,3 +191,19 @@ def test_coupled_row_block_spmv_bitwise():
                    C.c_void_p(torch.cuda.current_stream().cuda_stream))
             torch.cuda.synchronize()
             assert np.array_equal(y.cpu().numpy(), full[lo:hi]), (nx, nb, p)
+
+
+def test_fused_single_precond_overflow_index():
+    """single_inside_double on a stencil matrix (the one-pass k_st_prec1): a residual entry beyond
+    float32 range raises OverflowError naming the first such row, as the two-pass path and the
+    reference's cast_vector (sparse.py:244-257, krylov.py:116-118)."""
+    a = g2.laplace3d(32)
+    m = g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, 1), precision="single_inside_double")
+    r = g2.random_rhs(a.nrows, 0)
+    for bad in (5, 1000, a.nrows - 1):
+        rr = r.copy()
+        rr[bad] = 1e300
+        rr[bad + 7 if bad + 7 < a.nrows else 0] = -1e300
+        with pytest.raises(OverflowError) as e:
+            m.apply(rr)
+        assert f"entry {min(bad, bad + 7 if bad + 7 < a.nrows else 0)} " in str(e.value), e.value
