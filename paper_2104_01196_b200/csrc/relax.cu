@@ -925,6 +925,15 @@ static void launch_inner(Ctx<T>& c, int backward, const T* rd, const T* gin, T* 
   k_inner<T, FINAL, GAMMA><<<c.grid(), kB, 0, c.st>>>(c.n, Tm, rd, gin, gout, x, w, gm, gm1, pf_dist_host());
 }
 
+// the residual pass with the fused ||b - A x||^2 partials (smoother histories) on stencil triangles,
+// partials laid out as k_resid<..., NORM>'s (reduce_two over c.grid() * kB / 32 slots)
+template <typename T, int SM>
+static bool st_resid_norm(Ctx<T>& c, const T* x, const T* b, T* out, T w, double* partial) {
+  if (tri<T>(c.m, 2).nslots || tri<T>(c.m, 3).nslots || c.n == 0) return false;
+  return st_resid<T, SM, T>(c.m->device, c.L, c.U, c.n, c.d, x, b, out, w, c.st, nullptr, partial,
+                            (int64_t)c.grid() * (kB / 32));
+}
+
 // st_inner with the damping chosen at run time (the zero-start preconditioner chains)
 template <typename T, int SF, typename O>
 static bool st_inner_any(int device, const SellView<T>& Tm, int64_t n, const T* rd, const T* gin, const T* xc,
@@ -1007,8 +1016,9 @@ static int two_stage(Ctx<T>& c, const T* b, T* x, int n_j, int backward, int for
     // bitwise): one fused pass into the spare buffer + copy-back instead of rd pass + update pass
     T* alt = rd + 3 * c.n;
     if (c.norm_out) {
-      k_resid<T, kJr, true><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x,
-                                                       nullptr, nullptr, b, alt, (T)omega, pf_dist_host(), c.norm_red);
+      if (!st_resid_norm<T, kStJr>(c, x, b, alt, (T)omega, c.norm_red))
+        k_resid<T, kJr, true><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x,
+                                                         nullptr, nullptr, b, alt, (T)omega, pf_dist_host(), c.norm_red);
       RS_COUNT_LAUNCH();
       reduce_two(c.norm_red, (int64_t)c.grid() * (kB / 32), c.norm_out, c.st);
       c.norm_out = nullptr;
@@ -1030,8 +1040,9 @@ static int two_stage(Ctx<T>& c, const T* b, T* x, int n_j, int backward, int for
     RS_COUNT_LAUNCH();
   } else if (!compact) {
     if (c.norm_out) {
-      k_resid<T, kResidRd, true><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x,
-                                                            nullptr, nullptr, b, rd, (T)0, pf_dist_host(), c.norm_red);
+      if (!st_resid_norm<T, kStResidRd>(c, x, b, rd, (T)0, c.norm_red))
+        k_resid<T, kResidRd, true><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, x,
+                                                              nullptr, nullptr, b, rd, (T)0, pf_dist_host(), c.norm_red);
       RS_COUNT_LAUNCH();
       reduce_two(c.norm_red, (int64_t)c.grid() * (kB / 32), c.norm_out, c.st);
       c.norm_out = nullptr;
@@ -1503,8 +1514,9 @@ static int jr_sweeps_t(rs_matrix* m, const T* b, T* x, int sweeps, double omega,
     }
     T* nxt = cur == x ? alt : x;
     if (s == 0 && norm_out) {  // the first sweep's residual pass is ||b - A x_in||
-      k_resid<T, kJr, true><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, cur,
-                                                       nullptr, nullptr, b, nxt, w, pf_dist_host(), norm_red);
+      if (!st_resid_norm<T, kStJr>(c, cur, b, nxt, w, norm_red))
+        k_resid<T, kJr, true><<<c.grid(), kB, 0, c.st>>>(c.n, none_view<T>(), c.L, c.U, none_view<T>(), c.d, cur,
+                                                         nullptr, nullptr, b, nxt, w, pf_dist_host(), norm_red);
       RS_COUNT_LAUNCH();
       reduce_two(norm_red, (int64_t)c.grid() * (kB / 32), norm_out, c.st);
     } else if (!launch_resid_tma<T, kJr>(c.m, cur, b, nxt, w, c.st)) {

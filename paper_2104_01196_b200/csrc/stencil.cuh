@@ -191,20 +191,33 @@ enum StInnerFinal { kStMid = 0, kStSet = 1, kStAdd = 2 };
 // operation forms.  smc: the tile's stage (masks at p.sm_mask, d at p.sm_c[0], b at p.sm_c[1]);
 // interior tiles read slot tt's operand of tile row t at sx[t + bL/bU[tt]] and x[i] at sx[t + bc];
 // other tiles call opnd(q, tt, i) (q = 2: x[i]).
-template <typename T, int MODE, int K, typename B, int NT, typename Op>
+// NORM (kStResidRd / kStJr): also ||b - A x||^2 of the rows as per-warp partials, partial[i >> 5] =
+// the warp's 32 rows summed by the same shuffle tree as k_resid's NORM pass (a warp here holds the
+// same 32 rows), so the smoother's residual history is unchanged bit for bit; slots >= npart are
+// not written.
+template <typename T, int MODE, int K, typename B, int NT, bool NORM, typename Op>
 __device__ __forceinline__ void st_resid_tile(const StPlan<T>& p, const unsigned char* smc, const T* sx,
                                               const int* bL, const int* bU, int bc, bool interior, int clen,
                                               int r0, Op&& opnd, const T* __restrict__ d,
                                               const B* __restrict__ b, T* __restrict__ out, T w,
-                                              const StCouple<T>& cp) {
+                                              const StCouple<T>& cp, double* __restrict__ partial, int npart) {
   const T* sd = reinterpret_cast<const T*>(smc + p.sm_c[0]);
   const B* sb = reinterpret_cast<const B*>(smc + p.sm_c[1]);
-  auto finish = [&](int i, T acc, T di, T xi, B bi) {
+  auto finish = [&](int i, T acc, T di, T xi, B bi) -> double {
     if (MODE == kStSpmv) {
       out[i] = acc;
+      return 0.0;
     } else {
-      const T g = div_rn<T>(sub_rn<T>((T)bi, acc), di);
+      const T r = sub_rn<T>((T)bi, acc);
+      const T g = div_rn<T>(r, di);
       out[i] = MODE == kStResidRd ? g : add_rn<T>(xi, mul_rn<T>(w, g));
+      return (double)r * (double)r;
+    }
+  };
+  auto norm_partial = [&](int i, double v2) {
+    if (NORM) {
+      for (int o = 16; o; o >>= 1) v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+      if ((i & 31) == 0 && (i >> 5) < npart) partial[i >> 5] = v2;
     }
   };
   if (interior) {
@@ -241,13 +254,17 @@ __device__ __forceinline__ void st_resid_tile(const StPlan<T>& p, const unsigned
           acc = (mU[tt] & bit) ? s : acc;
         }
       }
-      finish(i, acc, di, xi, MODE == kStSpmv ? (B)0 : sb[t]);
+      norm_partial(i, finish(i, acc, di, xi, MODE == kStSpmv ? (B)0 : sb[t]));
     }
     return;
   }
   for (int t = threadIdx.x; t < p.rows; t += NT) {
     const int i = r0 + t;
-    if (i >= p.n) break;
+    if (i >= p.n) {
+      if (!NORM) break;
+      norm_partial(i, 0.0);  // the warp's rows past the vector: a zero partial (k_resid's layout)
+      continue;
+    }
     uint32_t mL[K], mU[K];
     st_masks<K>(smc, p.sm_mask, t, mL);
     st_masks<K>(smc, p.sm_mask + p.rows, t, mU);
@@ -263,7 +280,7 @@ __device__ __forceinline__ void st_resid_tile(const StPlan<T>& p, const unsigned
     for (int tt = 0; tt < K; ++tt)
       if (mU[tt] & bit) acc = add_rn<T>(acc, mul_rn<T>(p.val[1][tt], opnd(1, tt, i)));
     acc = row_accum<T>(cp.hi, i, cp.xhi, acc);
-    finish(i, acc, di, xi, MODE == kStSpmv ? (B)0 : (t < clen ? sb[t] : b[i]));
+    norm_partial(i, finish(i, acc, di, xi, MODE == kStSpmv ? (B)0 : (t < clen ? sb[t] : b[i])));
   }
 }
 
@@ -326,10 +343,11 @@ __device__ __forceinline__ void st_inner_tile(const StPlan<T>& p, const unsigned
 }
 
 // ---- one tile per CTA, operand windows of the tile (st_pipeline)
-template <typename T, int MODE, int K, typename B>
+template <typename T, int MODE, int K, typename B, bool NORM = false>
 __global__ void __launch_bounds__(kStThreads) k_st_resid(StPlan<T> p, const T* __restrict__ d,
                                                         const T* __restrict__ x, const B* __restrict__ b,
-                                                        T* __restrict__ out, T w, StCouple<T> cp) {
+                                                        T* __restrict__ out, T w, StCouple<T> cp,
+                                                        double* __restrict__ partial = nullptr, int npart = 0) {
   st_pipeline<T, T, B, T>(p, 2, x, d, MODE == kStSpmv ? (const B*)nullptr : b, (const T*)nullptr,
                           [&](unsigned char* sm, const StShared& S, int r0) {
     const T* sx = st_ptr<T>(sm, 0);
@@ -342,12 +360,12 @@ __global__ void __launch_bounds__(kStThreads) k_st_resid(StPlan<T> p, const T* _
     const int ts0 = r0 >> 5, ts1 = (r0 + p.rows) >> 5;
     const bool coupled = (!cp.lo.empty && ts0 < cp.lo.s_hi && cp.lo.s_lo < ts1) ||
                          (!cp.hi.empty && ts0 < cp.hi.s_hi && cp.hi.s_lo < ts1);
-    st_resid_tile<T, MODE, K, B, kStThreads>(p, sm, sx, bL, bU, bc, S.interior != 0 && !coupled, S.clen, r0,
+    st_resid_tile<T, MODE, K, B, kStThreads, NORM>(p, sm, sx, bL, bU, bc, S.interior != 0 && !coupled, S.clen, r0,
                                  [&](int q, int tt, int i) {
                                    return q == 2 ? st_at<T>(p, S, sx, x, p.wcen, i)
                                                  : st_at<T>(p, S, sx, x, p.win[q][tt], i + p.off[q][tt]);
                                  },
-                                 d, b, out, w, cp);
+                                 d, b, out, w, cp, partial, npart);
   });
 }
 
@@ -543,7 +561,8 @@ static void st_smem_attr(Kern k, int device) {
 // false: not applicable (the caller runs k_resid)
 template <typename T, int MODE, typename B>
 static bool st_resid(int device, const SellView<T>& L, const SellView<T>& U, int64_t n, const T* d, const T* x,
-                     const B* b, T* out, T w, cudaStream_t st, const StCouple<T>* couple = nullptr) {
+                     const B* b, T* out, T w, cudaStream_t st, const StCouple<T>* couple = nullptr,
+                     double* partial = nullptr, int64_t npart = 0) {
   StCouple<T> cp = {};
   cp.lo.empty = cp.hi.empty = true;
   if (couple) cp = *couple;
@@ -558,8 +577,13 @@ static bool st_resid(int device, const SellView<T>& L, const SellView<T>& U, int
   switch (L.sk) {
 #define RS_ST_RESID(KK)                                                \
   case KK:                                                             \
-    st_smem_attr(k_st_resid<T, MODE, KK, B>, device);                  \
-    k_st_resid<T, MODE, KK, B><<<tiles, kStThreads, smem, st>>>(p, d, x, b, out, w, cp); \
+    if (partial) {                                                     \
+      st_smem_attr(k_st_resid<T, MODE, KK, B, true>, device);          \
+      k_st_resid<T, MODE, KK, B, true><<<tiles, kStThreads, smem, st>>>(p, d, x, b, out, w, cp, partial, (int)npart); \
+    } else {                                                           \
+      st_smem_attr(k_st_resid<T, MODE, KK, B>, device);                \
+      k_st_resid<T, MODE, KK, B><<<tiles, kStThreads, smem, st>>>(p, d, x, b, out, w, cp); \
+    }                                                                  \
     return true;
     RS_ST_RESID(1)
     RS_ST_RESID(2)

@@ -98,6 +98,11 @@ def _ops(dm, b, x0, single):
             out[f"prec_{kind}_{cfg.n_j}{tag}_{prec}"] = m.apply(bt).cpu().numpy()
     _, h = g2.gmres(dm, bt, g2.Preconditioner(dm, "gs2", g2.RelaxConfig(1, 1, 1)), restart=20, tol=1e-8, maxit=200)
     out["gmres_hist"] = np.asarray(h.rel_res)
+    # the smoother: residual norms fused into the next application's residual pass (NORM partials)
+    for kind, cfg in (("gs2", g2.RelaxConfig(1, 1, 1)), ("jr", g2.RelaxConfig(1, 1, 0, omega=0.8))):
+        xs, hs = g2.stationary_solve(dm, bt, kind, cfg, tol=1e-300, maxit=12, x0=torch.from_numpy(x0).cuda())
+        out[f"smoother_{kind}_hist"] = np.asarray(hs.rel_res)
+        out[f"smoother_{kind}_x"] = xs.cpu().numpy() if hasattr(xs, "cpu") else np.asarray(xs)
     return out
 
 
