@@ -48,6 +48,29 @@ def _slice_scaled(a: g2.CsrMatrix) -> g2.CsrMatrix:
     return g2.CsrMatrix(a.nrows, a.ncols, a.row_ptr, a.col_idx, a.values * f)
 
 
+def _tridiag(n: int) -> g2.CsrMatrix:
+    """1-D Laplacian: one offset per triangle (K = 1); n odd (partial 16-byte units at the end)."""
+    d = np.diag(np.full(n, 2.0)) - np.diag(np.ones(n - 1), 1) - np.diag(np.ones(n - 1), -1)
+    return g2.from_dense(d)
+
+
+def _nine_point(nx: int) -> g2.CsrMatrix:
+    """2-D 9-point stencil: four offsets per triangle (K = 4), constant coefficients."""
+    n = nx * nx
+    rows, cols, vals = [], [], []
+    for y in range(nx):
+        for x in range(nx):
+            i = y * nx + x
+            for dy in (-1, 0, 1):
+                for dx in (-1, 0, 1):
+                    xx, yy = x + dx, y + dy
+                    if 0 <= xx < nx and 0 <= yy < nx:
+                        rows.append(i)
+                        cols.append(yy * nx + xx)
+                        vals.append(8.0 if dx == dy == 0 else -1.0)
+    return g2.from_coo(n, n, np.array(rows), np.array(cols), np.array(vals))
+
+
 CASES = {
     "lap3d_37": lambda: g2.laplace3d(37),  # n % 32 != 0: a partial last slice
     "lap2d_64": lambda: g2.laplace2d(64),
@@ -61,13 +84,16 @@ CASES = {
     "lap3d_32x32x37": lambda: g2.laplace3d(32, 32, 37),
     "cd3d_32": lambda: g2.convdiff3d(32, (50.0, 25.0, 10.0)),
     "lap3d_32_holes": lambda: _holes(g2.laplace3d(32), 0.1, 5),
+    "tridiag_1001": lambda: _tridiag(1001),
+    "nine_point_45": lambda: _nine_point(45),
 }
 # (diagonal-slice entries, stencil offsets) of (L, U); None: holes (checked separately)
 ENCODED = {"lap3d_37": ((3, 3), (3, 3)), "lap2d_64": ((2, 2), (2, 2)), "cd3d_24": ((3, 3), (3, 3)),
            "lap3d_20_holes": None, "ela3d_6": ((0, 0), (0, 0)),
            "lap3d_20_perturbed": ((0, 3), (0, 3)),  # the perturbed value is in L
            "lap3d_20_slice_scaled": ((3, 3), (0, 0)), "lap3d_32": ((3, 3), (3, 3)),
-           "lap3d_32x32x37": ((3, 3), (3, 3)), "cd3d_32": ((3, 3), (3, 3)), "lap3d_32_holes": None}
+           "lap3d_32x32x37": ((3, 3), (3, 3)), "cd3d_32": ((3, 3), (3, 3)), "lap3d_32_holes": None,
+           "tridiag_1001": ((1, 1), (1, 1)), "nine_point_45": ((4, 4), (4, 4))}
 
 
 def _ops(dm, b, x0, single):
