@@ -84,6 +84,10 @@ CASES = {
     "lap3d_32x32x37": lambda: g2.laplace3d(32, 32, 37),
     "cd3d_32": lambda: g2.convdiff3d(32, (50.0, 25.0, 10.0)),
     "lap3d_32_holes": lambda: _holes(g2.laplace3d(32), 0.1, 5),
+    # 4096 / 2048-row planes, a partial last plane, holes in a convection-diffusion stencil
+    "lap3d_64": lambda: g2.laplace3d(64),
+    "lap3d_32x64x21": lambda: g2.laplace3d(32, 64, 21),
+    "cd3d_64_holes": lambda: _holes(g2.convdiff3d(64, (50.0, 25.0, 10.0)), 0.05, 7),
     "tridiag_1001": lambda: _tridiag(1001),
     "nine_point_45": lambda: _nine_point(45),
 }
@@ -93,7 +97,8 @@ ENCODED = {"lap3d_37": ((3, 3), (3, 3)), "lap2d_64": ((2, 2), (2, 2)), "cd3d_24"
            "lap3d_20_perturbed": ((0, 3), (0, 3)),  # the perturbed value is in L
            "lap3d_20_slice_scaled": ((3, 3), (0, 0)), "lap3d_32": ((3, 3), (3, 3)),
            "lap3d_32x32x37": ((3, 3), (3, 3)), "cd3d_32": ((3, 3), (3, 3)), "lap3d_32_holes": None,
-           "tridiag_1001": ((1, 1), (1, 1)), "nine_point_45": ((4, 4), (4, 4))}
+           "tridiag_1001": ((1, 1), (1, 1)), "nine_point_45": ((4, 4), (4, 4)), "lap3d_64": ((3, 3), (3, 3)),
+           "lap3d_32x64x21": ((3, 3), (3, 3)), "cd3d_64_holes": None}
 
 
 def _ops(dm, b, x0, single):
@@ -204,7 +209,7 @@ def test_coupled_row_block_spmv_bitwise():
 
     from paper_2104_01196_b200 import _native as N
 
-    for nx, nb in ((32, 3), (24, 4)):
+    for nx, nb in ((32, 3), (24, 4), (64, 4)):
         a = g2.laplace3d(nx)
         n = a.nrows
         x = g2.random_rhs(n, 1)
