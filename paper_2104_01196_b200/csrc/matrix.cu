@@ -513,6 +513,8 @@ static int build_dia(Sell<T>& s) {
 }
 
 void free_mt_sell(rs_matrix* m) {
+  cudaFree(m->color8);
+  m->color8 = nullptr;
   for (int d = 0; d < 2; ++d) {
     free_sell(m->LV64[d]);
     free_sell(m->LV32[d]);
@@ -1116,6 +1118,12 @@ static int install_coloring(rs_matrix* m, const int64_t* color, int64_t nc) {
     free(m->color);
     m->color = (int64_t*)malloc(sizeof(int64_t) * std::max<int64_t>(n, 1));
     memcpy(m->color, color, sizeof(int64_t) * n);
+  }
+  if (nc <= 255 && n > 0) {
+    std::vector<uint8_t> c8(n);
+    for (int64_t i = 0; i < n; ++i) c8[i] = (uint8_t)color[i];
+    RS_CUDA(cudaMalloc(&m->color8, n));
+    RS_CUDA(cudaMemcpy(m->color8, c8.data(), n, cudaMemcpyHostToDevice));
   }
   return RS_OK;
 }

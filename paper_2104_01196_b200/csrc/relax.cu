@@ -1470,6 +1470,9 @@ static int mt_gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double o
       if (x_zero) {
         k_mt_first<T><<<grid_for(cnt, kB), kB, 0, st>>>(cnt, lv.rows + lo, S.dord + lo, b, x, w, w1, damped);
         x_zero = false;
+      } else if (!tri<T>(m, 2).nslots && !tri<T>(m, 3).nslots &&
+                 st_mt<T>(m->device, c.L, c.U, c.n, m->color8, (int)col, c.d, b, x, w, w1, damped, st)) {
+        // stencil triangles: the TMA-windowed colour pass over the natural row order
       } else {
         k_mt_color<T><<<grid_for(cnt, kB), kB, 0, st>>>(cnt, lv.rows + lo, S.slice_ptr + m->mt_slice_base[col],
                                                         S.col, S.val, S.dord + lo, b, x, w, w1, damped);

@@ -133,6 +133,7 @@ struct rs_matrix {
   rs::Levels fwd, bwd;      // lazily built
   rs::Levels mt;            // multicolor GS: "levels" = colors, rows ascending within a color
   int64_t* color = nullptr; // host, per-row color of the multicolor sweep
+  uint8_t* color8 = nullptr; // device, per-row color when there are at most 255 (stencil MT-GS passes)
   // multicolor GS: the off-diagonal entries (L then U, ascending columns) of the rows of each
   // color, stored as SELL-32 slices in color order (row t of color c = mt.rows[lo_c + t]), so a
   // color sweep reads coalesced slices instead of every other row's slots; mt_slice_base[c] =

@@ -460,6 +460,63 @@ __global__ void __launch_bounds__(kStThreads) k_st_prec1(StPlan<T> p, const R* _
   }, reinterpret_cast<const unsigned char*>(r));
 }
 
+// One colour of a multicolour GS sweep on stencil triangles (mt_gs_sweep, coloring.py:66-88): the
+// rows of colour c update in place, x_i = (b_i - sum_L v x - sum_U v x) / d_i in k_mt_color's form (s
+// from b, one subtraction per entry, L then U ascending; damped: (1 - w) x_i + w q).  Neighbours of
+// a colour-c row are never colour c, so the tile's x windows staged before any write stay valid.
+template <typename T, int K>
+__global__ void __launch_bounds__(kStThreads) k_st_mt(StPlan<T> p, const uint8_t* __restrict__ color, int c,
+                                                     const T* __restrict__ d, const T* __restrict__ b, T* x, T w,
+                                                     T w1, bool damped) {
+  st_pipeline<T, T, T, T>(p, 2, x, d, b, (const T*)nullptr, [&](unsigned char* sm, const StShared& S, int r0) {
+    const T* sx = st_ptr<T>(sm, 0);
+    const T* sd = st_ptr<T>(sm, p.sm_c[0]);
+    const T* sb = st_ptr<T>(sm, p.sm_c[1]);
+    int bL[K], bU[K];
+    st_bases<T, K>(p, S, 0, r0, bL);
+    st_bases<T, K>(p, S, 1, r0, bU);
+    const int bc = p.wsm[p.wcen] - S.ws[p.wcen] + r0;
+    const bool interior = S.interior != 0;
+    const int clen = S.clen;
+    for (int t = threadIdx.x; t < p.rows; t += kStThreads) {
+      const int i = r0 + t;
+      if (i >= p.n) break;
+      if (color[i] != c) continue;
+      uint32_t mL[K], mU[K];
+      st_masks<K>(sm, p.sm_mask, t, mL);
+      st_masks<K>(sm, p.sm_mask + p.rows, t, mU);
+      const uint32_t bit = 1u << (i & 31);
+      T s = t < clen ? sb[t] : b[i];
+      const T di = t < clen ? sd[t] : d[i];
+      T xi;
+      if (interior) {
+        const T* px = sx + t;
+        xi = px[bc];
+#pragma unroll
+        for (int tt = 0; tt < K; ++tt) {
+          const T u = sub_rn<T>(s, mul_rn<T>(p.val[0][tt], px[bL[tt]]));
+          s = (mL[tt] & bit) ? u : s;
+        }
+#pragma unroll
+        for (int tt = 0; tt < K; ++tt) {
+          const T u = sub_rn<T>(s, mul_rn<T>(p.val[1][tt], px[bU[tt]]));
+          s = (mU[tt] & bit) ? u : s;
+        }
+      } else {
+        xi = st_at<T>(p, S, sx, x, p.wcen, i);
+#pragma unroll
+        for (int tt = 0; tt < K; ++tt)
+          if (mL[tt] & bit) s = sub_rn<T>(s, mul_rn<T>(p.val[0][tt], st_at<T>(p, S, sx, x, p.win[0][tt], i + p.off[0][tt])));
+#pragma unroll
+        for (int tt = 0; tt < K; ++tt)
+          if (mU[tt] & bit) s = sub_rn<T>(s, mul_rn<T>(p.val[1][tt], st_at<T>(p, S, sx, x, p.win[1][tt], i + p.off[1][tt])));
+      }
+      const T q = div_rn<T>(s, di);
+      x[i] = damped ? add_rn<T>(mul_rn<T>(w1, xi), mul_rn<T>(w, q)) : q;
+    }
+  });
+}
+
 // ------------------------------------------------------------------ host planning / launch
 static int st_rows_per_tile() {
   static const int v = getenv("RS_ST_ROWS") ? atoi(getenv("RS_ST_ROWS")) : 1024;
@@ -651,6 +708,35 @@ static bool st_prec1(int device, const SellView<T>& Tm, int64_t n, const R* r, c
     RS_ST_PREC1(3)
     RS_ST_PREC1(4)
 #undef RS_ST_PREC1
+    default:
+      return false;
+  }
+}
+
+// one colour pass of the multicolour GS sweep on stencil triangles; false: not applicable
+template <typename T>
+static bool st_mt(int device, const SellView<T>& L, const SellView<T>& U, int64_t n, const uint8_t* color, int c,
+                  const T* d, const T* b, T* x, T w, T w1, bool damped, cudaStream_t st) {
+  static const bool on = !getenv("RS_ST_MT") || atoi(getenv("RS_ST_MT")) != 0;
+  const SellView<T>* tri[2] = {&L, &U};
+  StPlan<T> p;
+  size_t smem = 0;
+  const int cs[3] = {(int)sizeof(T), (int)sizeof(T), 0};
+  if (!on || !color || L.sk != U.sk || !st_aligned(x) || !st_aligned(d) || !st_aligned(b) ||
+      !st_plan<T>(tri, 2, true, n, cs, p, smem))
+    return false;
+  const int tiles = (int)((n + p.rows - 1) / p.rows);
+  switch (L.sk) {
+#define RS_ST_MT(KK)                                                                               \
+  case KK:                                                                                         \
+    st_smem_attr(k_st_mt<T, KK>, device);                                                          \
+    k_st_mt<T, KK><<<tiles, kStThreads, smem, st>>>(p, color, c, d, b, x, w, w1, damped);         \
+    return true;
+    RS_ST_MT(1)
+    RS_ST_MT(2)
+    RS_ST_MT(3)
+    RS_ST_MT(4)
+#undef RS_ST_MT
     default:
       return false;
   }

@@ -46,6 +46,8 @@ def run(a, reps, cycle=True):
         cfg = g2.RelaxConfig(1, 1, nj)
         out[f"gs2_nj{nj}"] = timeit(lambda cfg=cfg: g2.gs2_apply(a, s, b, x, cfg), reps)
     out["jr"] = timeit(lambda: g2.jr_sweeps(a, s, b, x, 1), reps)
+    col = g2.greedy_color(a)
+    out["mt_gs"] = timeit(lambda: g2.mt_gs_sweep(a, s, col, b, x, "forward"), reps)
     for prec in ("same", "single_inside_double"):
         pc = g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, 1), precision=prec)
         z = torch.empty_like(b)

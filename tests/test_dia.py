@@ -119,9 +119,15 @@ def _ops(dm, b, x0, single):
     xt = torch.from_numpy(x0).cuda()
     g2.jr_sweeps(dm, g2.extract_splitting(dm, omega=0.7), bt, xt, 2)
     out["jr"] = xt.cpu().numpy()
+    col = g2.greedy_color(dm)
+    for direction, om in (("forward", 1.0), ("symmetric", 1.0), ("backward", 0.8)):
+        xt = torch.from_numpy(x0).cuda()
+        g2.mt_gs_sweep(dm, g2.extract_splitting(dm, omega=om), col, bt, xt, direction)
+        out[f"mt_{direction}"] = xt.cpu().numpy()
     # (gs2 n_j = 1 from zero: the one-pass k_st_prec1 on stencil triangles, incl. damped / backward)
     for tag, kind, cfg in (("", "gs2", g2.RelaxConfig(1, 1, 1)), ("", "gs2", g2.RelaxConfig(1, 1, 3)),
                            ("", "sgs2", g2.RelaxConfig(1, 1, 2)), ("", "jr", g2.RelaxConfig(2, 1, 0)),
+                           ("", "mt_sgs", g2.RelaxConfig(2, 1, 0)), ("_w", "mt_gs", g2.RelaxConfig(2, 1, 0, omega=0.9)),
                            ("_gamma", "gs2", g2.RelaxConfig(1, 1, 1, gamma=0.7)),
                            ("_bwd", "gs2", g2.RelaxConfig(1, 1, 1, direction="backward", omega=0.9))):
         for prec in ("same", "single_inside_double") if single else ("same",):
@@ -172,6 +178,9 @@ def test_diagonal_slices_bitwise_explicit_and_oracle(case):
     oracle.gs2_apply(om, b, xo, g2.RelaxConfig(2, 1, 1))
     assert np.array_equal(enc["gs2_1"], xo)
     assert np.array_equal(enc["prec_gs2_1_same"], oracle.Precond(om, "gs2", n_j=1).apply(b))
+    xo = x0.copy()
+    oracle.mt_gs_sweep(om, b, xo, "symmetric")
+    assert np.array_equal(enc["mt_symmetric"], xo)
     assert np.array_equal(enc["prec_gs2_1_single_inside_double"],
                           oracle.Precond(om, "gs2", precision="single_inside_double", n_j=1).apply(b))
 
