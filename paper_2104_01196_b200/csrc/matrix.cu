@@ -1191,6 +1191,13 @@ static int device_coloring(rs_matrix* m, bool* done) {
       free(m->color);
       m->color = c64;
       *done = true;
+      if (nc <= 255 && n > 0) {  // per-row colour bytes for the stencil MT-GS passes
+        std::vector<uint8_t> c8(n);
+        for (int64_t i = 0; i < n; ++i) c8[i] = (uint8_t)hc[i];
+        if (cudaMalloc(&m->color8, n) != cudaSuccess ||
+            cudaMemcpy(m->color8, c8.data(), n, cudaMemcpyHostToDevice) != cudaSuccess)
+          status = cuda_error(cudaErrorMemoryAllocation, "device_coloring color8");
+      }
     }
   }
   cudaFree(color);
