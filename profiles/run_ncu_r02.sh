@@ -12,7 +12,7 @@ M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,dram__throug
 $NCU --profile-from-start off --clock-control none --metrics $M --csv --log-file $OUT/region_metrics.csv \
   python profiles/ncu_kernels.py > $OUT/A.log 2>&1; echo "A rc=$?"
 $NCU --profile-from-start off --clock-control none --set full --import-source on \
-  -k regex:"k_st_|k_resid|k_inner|k_scale_rd|k_mt_color|k_spmv_red" -c 40 -f -o $OUT/sweeps \
+  -k regex:"k_st_|k_resid|k_inner|k_scale_rd|k_mt_color|k_spmv_red" -c 48 -f -o $OUT/sweeps \
   python profiles/ncu_kernels.py --phase sweeps > $OUT/B.log 2>&1; echo "B rc=$?"
 for skip in 60 118; do
   $NCU --profile-from-start off --clock-control none --set full --import-source on -k regex:k_cgs \

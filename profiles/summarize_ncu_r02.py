@@ -75,6 +75,7 @@ model = {
                                                  MS + 3 * V),
     "k_st_prec1<float, double, double, 0, 3>": ("stencil fp32-inside-fp64 GS2(1,1,1) preconditioner, one pass",
                                                 MS + 2 * V + V // 2),
+    "k_st_mt<double, 3>": ("stencil MT-GS colour pass (2 colours / sweep)", (MS + mst.MU + 3 * V) / 2),
     "k_resid_tma<double, 1>": ("explicit GS2 pass 0 (TMA col/val)", ML + mod.MU + 4 * V),
     "k_resid_tma<double, 2>": ("explicit JR sweep (TMA col/val)", ML + mod.MU + 4 * V),
     "k_resid_tma<double, 0>": ("explicit SpMV (TMA col/val)", mod.spmv()),
