@@ -65,17 +65,20 @@ for (i, k), m in launches.items():
 ML = mod.ML
 MS = mst.ML
 model = {
-    "k_st_resid<double, 1, 3, double>": ("stencil GS2 pass 0: rd = (b - Ax)/d", MS + mst.MU + 4 * V),
+    "k_st_resid<double, 1, 3, double, 0>": ("stencil GS2 pass 0: rd = (b - Ax)/d", MS + mst.MU + 4 * V),
+    "k_st_resid<double, 1, 3, double, 1>": ("stencil GS2 pass 0 + fused ||r||^2 partials (smoother)",
+                                            MS + mst.MU + 4 * V),
     "k_st_inner<double, 2, 0, 3, double>": ("stencil GS2 inner step, last, x += w g", MS + 3 * V),
-    "k_st_resid<double, 2, 3, double>": ("stencil JR sweep", MS + mst.MU + 4 * V),
-    "k_st_resid<double, 0, 3, double>": ("stencil SpMV y = Ax", mst.spmv()),
+    "k_st_resid<double, 2, 3, double, 0>": ("stencil JR sweep", MS + mst.MU + 4 * V),
+    "k_st_resid<double, 0, 3, double, 0>": ("stencil SpMV y = Ax", mst.spmv()),
     "k_st_inner<double, 1, 0, 3, double>": ("stencil precond inner step, z = w g", MS + 2 * V),
     "k_st_inner<float, 1, 0, 3, double>": ("stencil fp32 precond inner, z = (double)(w g)", MS + V // 2 + V),
     "k_st_prec1<double, double, double, 0, 3>": ("stencil zero-start GS2(1,1,1) preconditioner, one pass",
                                                  MS + 3 * V),
     "k_st_prec1<float, double, double, 0, 3>": ("stencil fp32-inside-fp64 GS2(1,1,1) preconditioner, one pass",
                                                 MS + 2 * V + V // 2),
-    "k_st_mt<double, 3>": ("stencil MT-GS colour pass (2 colours / sweep)", (MS + mst.MU + 3 * V) / 2),
+    "k_st_mt<double, 3>": ("stencil MT-GS colour pass (all rows' b, d, x read: colours interleave; the colour's x "
+                           "written)", MS + mst.MU + 3 * V + V // 2),
     "k_resid_tma<double, 1>": ("explicit GS2 pass 0 (TMA col/val)", ML + mod.MU + 4 * V),
     "k_resid_tma<double, 2>": ("explicit JR sweep (TMA col/val)", ML + mod.MU + 4 * V),
     "k_resid_tma<double, 0>": ("explicit SpMV (TMA col/val)", mod.spmv()),
@@ -127,7 +130,7 @@ for name, g in groups.items():
                      "dram_write": g["wr"] / cnt, "model_bytes": alg, "l2_bytes": l2}
 # bench.py kernel groups (roofline.traffic): the DCGS2 groups
 for grp, name in (("dcgs_dots", "k_cgs<0, 1, 0, 1>"), ("dcgs_update", "k_cgs<1, 0, 1, 1>"),
-                  ("spmv", "k_st_resid<double, 0, 3, double>"), ("precond", "k_st_prec1<double, double, double, 0, 3>")):
+                  ("spmv", "k_st_resid<double, 0, 3, double, 0>"), ("precond", "k_st_prec1<double, double, double, 0, 3>")):
     if name in traffic:
         traffic[grp] = dict(traffic[name], kernel=name, capture=traffic["capture"])
 lv = groups.get("k_mt_color_pdl<double>")
