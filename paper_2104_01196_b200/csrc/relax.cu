@@ -183,6 +183,15 @@ __global__ void __launch_bounds__(256) k_spmv_red(int64_t n, SellView<double> L,
   }
 }
 
+// block partials of k_spmv_red from its warps' partials: out[b] = ((0 + w[8b]) + w[8b+1]) + ... + w[8b+7]
+__global__ void k_sum8(const double* __restrict__ w, int64_t nblk, double* __restrict__ out) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nblk) return;
+  double t = 0.0;
+  for (int q = 0; q < 8; ++q) t += w[b * 8 + q];
+  out[b] = t;
+}
+
 // out = sum of nblk partials, one 1024-thread block, fixed order (deterministic)
 __global__ void __launch_bounds__(1024) k_reduce_many(const double* __restrict__ partial, int64_t nblk,
                                                       double* __restrict__ out) {
@@ -2134,13 +2143,24 @@ static int spmv_red(rs_matrix_t m, int mode, const double* x, const double* b, d
   const int64_t nblk = std::max<int64_t>(grid_for(std::max<int64_t>(n, 1), kB), 1);
   int e;
   double* red = nullptr;
-  if ((e = get_reduction(m, st, nblk, &red))) return e;
+  if ((e = get_reduction(m, st, 9 * nblk, &red))) return e;  // block partials, then 8 warp partials each
   SellView<double> Lv = view(m->L64, false), Uv = view(m->U64, false);
   const double* d = (const double*)m->d;
-  if (mode == kRedDot)
+  // stencil triangles: the TMA-windowed pass writes one partial per warp (same rows, same shuffle
+  // tree as k_spmv_red's warps) and k_sum8 forms k_spmv_red's block partials from them in its order
+  double* wp = red + nblk;
+  const bool stv = n && (mode == kRedDot ? st_resid<double, kStSpmvDot, double>(m->device, Lv, Uv, n, d, x, b, y,
+                                                                              0.0, st, nullptr, wp, 8 * nblk)
+                                         : st_resid<double, kStNorm2, double>(m->device, Lv, Uv, n, d, x, b, y, 0.0,
+                                                                             st, nullptr, wp, 8 * nblk));
+  if (stv) {
+    RS_COUNT_LAUNCH();
+    k_sum8<<<grid_for(nblk, kB), kB, 0, st>>>(wp, nblk, red);
+  } else if (mode == kRedDot) {
     k_spmv_red<kRedDot><<<nblk, kB, 0, st>>>(n, Lv, Uv, d, x, b, y, red, pf_dist_host());
-  else
+  } else {
     k_spmv_red<kRedNorm><<<nblk, kB, 0, st>>>(n, Lv, Uv, d, x, b, y, red, pf_dist_host());
+  }
   RS_COUNT_LAUNCH();
   k_reduce_many<<<1, 1024, 0, st>>>(red, nblk, out);
   RS_COUNT_LAUNCH();

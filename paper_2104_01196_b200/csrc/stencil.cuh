@@ -174,7 +174,9 @@ __device__ __forceinline__ void st_pipeline(const StPlan<T>& p, int ntri, const 
   tile_fn(sm, S, r0);
 }
 
-enum StResidMode { kStSpmv = 0, kStResidRd = 1, kStJr = 2 };
+// kStSpmvDot: y = A x and the per-warp partials of x . y (CG's p^T A p); kStNorm2: only the partials
+// of ||b - A x||^2 (nothing stored) -- k_spmv_red's two modes, same per-row and per-warp arithmetic
+enum StResidMode { kStSpmv = 0, kStResidRd = 1, kStJr = 2, kStSpmvDot = 3, kStNorm2 = 4 };
 
 // off-block couplings of a row block (E_lo | ... | E_hi, explicit SELL; empty views when none) and
 // the halo vectors they index
@@ -207,6 +209,12 @@ __device__ __forceinline__ void st_resid_tile(const StPlan<T>& p, const unsigned
     if (MODE == kStSpmv) {
       out[i] = acc;
       return 0.0;
+    } else if (MODE == kStSpmvDot) {
+      out[i] = acc;
+      return (double)xi * (double)acc;
+    } else if (MODE == kStNorm2) {
+      const double t = (double)sub_rn<T>((T)bi, acc);
+      return t * t;
     } else {
       const T r = sub_rn<T>((T)bi, acc);
       const T g = div_rn<T>(r, di);
@@ -254,7 +262,7 @@ __device__ __forceinline__ void st_resid_tile(const StPlan<T>& p, const unsigned
           acc = (mU[tt] & bit) ? s : acc;
         }
       }
-      norm_partial(i, finish(i, acc, di, xi, MODE == kStSpmv ? (B)0 : sb[t]));
+      norm_partial(i, finish(i, acc, di, xi, (MODE == kStSpmv || MODE == kStSpmvDot) ? (B)0 : sb[t]));
     }
     return;
   }
@@ -280,7 +288,7 @@ __device__ __forceinline__ void st_resid_tile(const StPlan<T>& p, const unsigned
     for (int tt = 0; tt < K; ++tt)
       if (mU[tt] & bit) acc = add_rn<T>(acc, mul_rn<T>(p.val[1][tt], opnd(1, tt, i)));
     acc = row_accum<T>(cp.hi, i, cp.xhi, acc);
-    norm_partial(i, finish(i, acc, di, xi, MODE == kStSpmv ? (B)0 : (t < clen ? sb[t] : b[i])));
+    norm_partial(i, finish(i, acc, di, xi, (MODE == kStSpmv || MODE == kStSpmvDot) ? (B)0 : (t < clen ? sb[t] : b[i])));
   }
 }
 
@@ -348,7 +356,8 @@ __global__ void __launch_bounds__(kStThreads) k_st_resid(StPlan<T> p, const T* _
                                                         const T* __restrict__ x, const B* __restrict__ b,
                                                         T* __restrict__ out, T w, StCouple<T> cp,
                                                         double* __restrict__ partial = nullptr, int npart = 0) {
-  st_pipeline<T, T, B, T>(p, 2, x, d, MODE == kStSpmv ? (const B*)nullptr : b, (const T*)nullptr,
+  st_pipeline<T, T, B, T>(p, 2, x, d, (MODE == kStSpmv || MODE == kStSpmvDot) ? (const B*)nullptr : b,
+                          (const T*)nullptr,
                           [&](unsigned char* sm, const StShared& S, int r0) {
     const T* sx = st_ptr<T>(sm, 0);
     int bL[K], bU[K];
@@ -626,8 +635,9 @@ static bool st_resid(int device, const SellView<T>& L, const SellView<T>& U, int
   const SellView<T>* tri[2] = {&L, &U};
   StPlan<T> p;
   size_t smem = 0;
-  const int cs[3] = {(int)sizeof(T), MODE == kStSpmv ? 0 : (int)sizeof(B), 0};
-  if (L.sk != U.sk || !st_aligned(x) || !st_aligned(d) || (MODE != kStSpmv && !st_aligned(b)) ||
+  constexpr bool kNoB = MODE == kStSpmv || MODE == kStSpmvDot;
+  const int cs[3] = {(int)sizeof(T), kNoB ? 0 : (int)sizeof(B), 0};
+  if (L.sk != U.sk || !st_aligned(x) || !st_aligned(d) || (!kNoB && !st_aligned(b)) ||
       !st_plan<T>(tri, 2, true, n, cs, p, smem))
     return false;
   const int tiles = (int)((n + p.rows - 1) / p.rows);

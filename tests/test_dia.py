@@ -135,6 +135,13 @@ def _ops(dm, b, x0, single):
             out[f"prec_{kind}_{cfg.n_j}{tag}_{prec}"] = m.apply(bt).cpu().numpy()
     _, h = g2.gmres(dm, bt, g2.Preconditioner(dm, "gs2", g2.RelaxConfig(1, 1, 1)), restart=20, tol=1e-8, maxit=200)
     out["gmres_hist"] = np.asarray(h.rel_res)
+    # CG: SpMV fused with p^T A p, and the true-residual norm (rs_spmv_dot / rs_resid_norm2)
+    # (non-symmetric matrices may stop with NotSpdError: the same step on both layouts)
+    try:
+        _, hc = g2.cg(dm, bt, g2.Preconditioner(dm, "sgs2", g2.RelaxConfig(1, 1, 1)), tol=1e-8, maxit=150)
+        out["cg_hist"] = np.asarray(hc.rel_res)
+    except RuntimeError as e:
+        out["cg_hist"] = np.array([float(len(str(e)))])
     # the smoother: residual norms fused into the next application's residual pass (NORM partials)
     for kind, cfg in (("gs2", g2.RelaxConfig(1, 1, 1)), ("jr", g2.RelaxConfig(1, 1, 0, omega=0.8))):
         xs, hs = g2.stationary_solve(dm, bt, kind, cfg, tol=1e-300, maxit=12, x0=torch.from_numpy(x0).cuda())
