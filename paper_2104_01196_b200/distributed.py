@@ -213,12 +213,17 @@ class ThreadComm(Comm):
             torch.cuda.current_stream().synchronize()
 
     def allreduce_sum_(self, t):
+        # every copy another thread reads is complete before the barrier that publishes it, and
+        # every read of another thread's copy is complete before the barrier after which that copy
+        # may be replaced (the threads' streams are independent: no cross-stream ordering otherwise)
         self._sync_stream()
         self.sh.slots[self.rank] = t.clone()
+        self._sync_stream()
         self.sh.bar.wait()
         acc = self.sh.slots[0].clone()
         for r in range(1, self.size):
             acc += self.sh.slots[r].to(acc.device)
+        self._sync_stream()
         self.sh.bar.wait()
         t.copy_(acc)
 
@@ -241,6 +246,7 @@ class ThreadComm(Comm):
         with self.sh.lock:
             for peer, t in sends:
                 self.sh.mail[(self.rank, peer)] = t.clone()
+        self._sync_stream()  # the clones are complete before the receivers read them
         self.sh.bar.wait()
         for peer, t in recvs:
             t.copy_(self.sh.mail[(peer, self.rank)])
