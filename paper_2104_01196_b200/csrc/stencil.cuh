@@ -22,7 +22,14 @@
 namespace rs {
 
 constexpr int kStWin = 8;        // windows of the gathered vector
-constexpr int kStThreads = 256;  // threads per CTA; a tile is rows = kStThreads * rows-per-thread
+// threads per CTA; a tile is rows = kStThreads * rows-per-thread.  128 threads x 512-row tiles (4 rows
+// per thread, ~8 CTAs per SM) measured best: 256 x 1024 / 512 x 1024 / 64 x 512 ran the 256^3 SpMV
+// at 0.104 / 0.154 / 0.092 ms and the GS2 sweep at 0.182 / 0.265 / 0.194 ms vs 0.094 / 0.175 ms
+// (profiles/ab/r02_stencil_threads.txt)
+#ifndef RS_ST_THREADS
+#define RS_ST_THREADS 128
+#endif
+constexpr int kStThreads = RS_ST_THREADS;
 // offsets at most this far apart share a window (RS_ST_GAP; default: the tile's rows)
 static int st_gap(int rows) {
   static const int v = getenv("RS_ST_GAP") ? atoi(getenv("RS_ST_GAP")) : -1;
@@ -528,8 +535,8 @@ __global__ void __launch_bounds__(kStThreads) k_st_mt(StPlan<T> p, const uint8_t
 
 // ------------------------------------------------------------------ host planning / launch
 static int st_rows_per_tile() {
-  static const int v = getenv("RS_ST_ROWS") ? atoi(getenv("RS_ST_ROWS")) : 1024;
-  return v >= kStThreads && v % kStThreads == 0 ? v : 1024;
+  static const int v = getenv("RS_ST_ROWS") ? atoi(getenv("RS_ST_ROWS")) : 512;
+  return v >= kStThreads && v % kStThreads == 0 ? v : 512;
 }
 static bool st_enabled() {
   static const bool on = !getenv("RS_ST_TMA") || atoi(getenv("RS_ST_TMA")) != 0;
