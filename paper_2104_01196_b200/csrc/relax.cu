@@ -1544,10 +1544,12 @@ static int jr_sweeps_t(rs_matrix* m, const T* b, T* x, int sweeps, double omega,
 }
 
 // One cooperative launch per half-sweep (falls back to per-level launches if the
-// device cannot co-schedule the grid).  level_ptr and the barrier words live on device.
-// RS_GS_MODE: "barrier" (default, one grid barrier per level), "syncfree" (per-row
-// done flags), "launch" (one kernel launch per level).  Measured at 256^3
-// (766 levels): 8.3 ms / 42.7 ms (no backoff) / 8.6 ms.
+// device cannot co-schedule the grid).  level_ptr and the barrier words live on device (per
+// handle: these modes are not reentrant -- opt-in A/B modes only).
+// RS_GS_MODE: "barrier" (one grid barrier per level), "syncfree" (per-row done flags),
+// "launch" (one kernel launch per level).  Measured at 256^3 (766 levels): 8.3 ms / 42.7 ms
+// (no backoff) / 8.6 ms.  Default: level-ordered slices with PDL-chained launches per level
+// (structurally symmetric patterns, ~3.2 ms) and plain per-level launches otherwise.
 enum GsMode { kGsBarrier = 0, kGsSyncfree = 1, kGsLaunch = 2, kGsOrdered = 3, kGsOrderedLaunch = 4 };
 static int gs_mode() {
   static const int mode = [] {
@@ -1786,7 +1788,10 @@ static int gs_sweep_t(rs_matrix* m, const T* b, T* x, int direction, double omeg
       }
       continue;
     }
-    if (gs_cooperative<T>(m, lv, c, b, x, xL, xU, w, w1, damped, bwd, st) == RS_OK) {
+    // structurally non-symmetric patterns: one launch per level (reentrant: no per-handle barrier
+    // words); the cooperative single-launch sweeps only when RS_GS_MODE selects them
+    if ((gs_mode() == kGsBarrier || gs_mode() == kGsSyncfree || gs_mode() == kGsLaunch) &&
+        gs_cooperative<T>(m, lv, c, b, x, xL, xU, w, w1, damped, bwd, st) == RS_OK) {
       pdl_ok = true;
       continue;
     }

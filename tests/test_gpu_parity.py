@@ -776,9 +776,22 @@ def test_concurrent_solves_share_matrix_and_preconditioner():
     s = g2.extract_splitting(a)
     rhs = [g2.random_rhs(n, 10 + i, device="cuda") for i in range(4)]
     x0 = g2.random_rhs(n, 99, device="cuda")
+    # a structurally non-symmetric pattern (level-scheduled GS: the snapshot + per-level path)
+    rng = np.random.default_rng(1)
+    nn = 2000
+    dn = np.zeros((nn, nn))
+    idx = rng.integers(0, nn, size=(12000, 2))
+    dn[idx[:, 0], idx[:, 1]] = rng.uniform(-1, 1, 12000)
+    np.fill_diagonal(dn, np.abs(dn).sum(1) + 1.0)
+    an = g2.from_dense(dn).device()
+    sn = g2.extract_splitting(an)
+    bn = [torch.from_numpy(rng.standard_normal(nn)).cuda() for _ in range(4)]
 
     def work(i):
         out = {}
+        xn = torch.zeros(nn, dtype=torch.float64, device="cuda")
+        g2.gs_sequential_sweep(an, sn, bn[i], xn, "symmetric")
+        out["gs_nonsym"] = xn
         for k, pc in pcs.items():
             out[k] = pc.apply(rhs[i])
         x = x0.clone()
