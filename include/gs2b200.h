@@ -330,7 +330,8 @@ int rs_cast_f32_f64(int64_t n, const float *in, double *out, rs_stream_t stream)
  * With last = 1, rs_dcgs2_coef only finalises column k-2 from out = V^T u (k values,
  * e.g. rs_cgs_pass dots with w = row k-1).  peer != NULL: the sums over ranks run
  * inside the passes (see rs_cgs_pass_peer; flags -> status_out in the update).
- * k <= 128 (k > 64: two segments of at most 64 basis rows each, single process only; the update
+ * k <= 128 (k > 64: two segments of at most 64 basis rows each -- with peer, the dots' 2k sums over
+ * ranks run as one allreduce after the two passes (2k <= the mailbox capacity); the update
  * then needs seg_tmp = 2n doubles of scratch for the first segment's partial sums, the coefficient
  * block holds 2*128+2 doubles: s at [0, k-1), a at [128, 128+k-1), 1/rho at 256, gamma at 257;
  * rs_dcgs2_dots_coef: k <= 64), even ldv, 16-byte aligned rows (odd n: as rs_cgs_pass). */

@@ -1167,11 +1167,13 @@ int rs_dcgs2_dots(const double* V, int64_t ldv, int k, int64_t n, const double* 
   if (k <= kCgsMaxK)
     return cgs_pass(V, ldv, k, n, nullptr, const_cast<double*>(w), out, nullptr, nonfinite, work,
                     (cudaStream_t)stream, peer, epoch, nullptr, nullptr, true);
-  if (peer) {
-    set_error(RS_ERR_UNSUPPORTED, "rs_dcgs2_dots: k > 64 basis vectors with peer-memory reductions");
-    return RS_ERR_UNSUPPORTED;
+  // two segments: rows [0, 64) with u = row k-1 staged as an extra row, then rows [64, k); with
+  // peer-memory reductions the 2k rank-local dots are summed over ranks by one allreduce launch
+  // after them (the same rank-order sum as the in-kernel one)
+  if (peer && 2 * k > peer->rcap) {
+    set_error(RS_ERR_ARG, "rs_dcgs2_dots: 2k dots exceed the peer mailbox capacity");
+    return RS_ERR_ARG;
   }
-  // two segments: rows [0, 64) with u = row k-1 staged as an extra row, then rows [64, k)
   SegArgs s0;
   s0.uext = V + (int64_t)(k - 1) * ldv;
   s0.h_out2 = out + k;
@@ -1180,9 +1182,11 @@ int rs_dcgs2_dots(const double* V, int64_t ldv, int k, int64_t n, const double* 
   if (e) return e;
   SegArgs s1;
   s1.h_out2 = out + k + kCgsMaxK;
-  return cgs_pass(V + (int64_t)kCgsMaxK * ldv, ldv, k - kCgsMaxK, n, nullptr, const_cast<double*>(w), out + kCgsMaxK,
-                  nullptr, nullptr, work, (cudaStream_t)stream, nullptr, 0, nullptr, nullptr, true, nullptr, nullptr,
-                  nullptr, &s1);
+  e = cgs_pass(V + (int64_t)kCgsMaxK * ldv, ldv, k - kCgsMaxK, n, nullptr, const_cast<double*>(w), out + kCgsMaxK,
+               nullptr, nullptr, work, (cudaStream_t)stream, nullptr, 0, nullptr, nullptr, true, nullptr, nullptr,
+               nullptr, &s1);
+  if (e || !peer) return e;
+  return peer_allreduce_launch(peer, epoch, out, 2 * k, nullptr, 0, nullptr, nullptr, (cudaStream_t)stream);
 }
 
 int rs_dcgs2_dots_coef(const double* V, int64_t ldv, int k, int64_t n, const double* w, double* out, int* nonfinite,
@@ -1230,7 +1234,7 @@ int rs_dcgs2_update(const double* V, int64_t ldv, int k, int64_t n, const double
                     const int64_t* flags, double* status_out, double* seg_tmp, rs_stream_t stream) {
   if (!dcgs_ok(V, ldv, k, n, w, "rs_dcgs2_update")) return RS_ERR_ARG;
   if (!coef || !w || !vrow || !urow || !nrm2 || !work || (peer && epoch == 0) || (flags && !status_out) ||
-      (flags && !peer) || (k > kCgsMaxK && (!seg_tmp || peer))) {
+      (flags && !peer) || (k > kCgsMaxK && !seg_tmp)) {
     set_error(RS_ERR_ARG, "rs_dcgs2_update: bad arguments");
     return RS_ERR_ARG;
   }
@@ -1238,7 +1242,8 @@ int rs_dcgs2_update(const double* V, int64_t ldv, int k, int64_t n, const double
     return cgs_pass(V, ldv, k, n, coef, const_cast<double*>(w), nullptr, nrm2, nullptr, work, (cudaStream_t)stream,
                     peer, epoch, flags, status_out, true, vrow, urow);
   // two segments: Q s and Q a over rows [0, 64) into seg_tmp, then rows [64, k) (ending with u)
-  // continue those sums and write v_j, u', ||u'||^2
+  // continue those sums and write v_j, u', ||u'||^2 (summed over ranks in the second segment's
+  // last CTA when peer reductions are on: the first segment has no reductions)
   SegArgs s0;
   s0.mode = 1;
   s0.P1 = seg_tmp;
@@ -1250,7 +1255,7 @@ int rs_dcgs2_update(const double* V, int64_t ldv, int k, int64_t n, const double
   s1.mode = 2;
   s1.coff = kCgsMaxK;
   return cgs_pass(V + (int64_t)kCgsMaxK * ldv, ldv, k - kCgsMaxK, n, coef, const_cast<double*>(w), nullptr, nrm2,
-                  nullptr, work, (cudaStream_t)stream, nullptr, 0, nullptr, nullptr, true, vrow, urow, nullptr, &s1);
+                  nullptr, work, (cudaStream_t)stream, peer, epoch, flags, status_out, true, vrow, urow, nullptr, &s1);
 }
 
 int rs_gemv_n(const double* V, int64_t ldv, int k, int64_t n, const double* y, double* out, rs_stream_t stream) {

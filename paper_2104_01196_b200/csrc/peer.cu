@@ -6,6 +6,8 @@
 // three CGS2 passes run inside the CGS kernel itself (krylov.cu, last CTA);
 // this file holds the mailbox object, the halo push/wait kernel and a
 // standalone one-CTA allreduce for the few per-cycle norms.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
@@ -191,11 +193,34 @@ int rs_peer_connect(rs_peer* p, const void* handles) {
   return upload_boxes(p);
 }
 
+// Thread ranks sharing one device share one context.  Under lazy module loading the first launch
+// of a kernel may wait for the context's running work -- including another rank's collective,
+// which spins until this rank contributes: a deadlock broken only by the collective's timeout
+// (the CUDA lazy-loading caveat on kernels that rely on running concurrently).  Separate
+// processes (the production layout: one rank per GPU) have separate contexts and are unaffected.
+static bool lazy_module_loading() {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuModuleGetLoadingMode", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
+      q != cudaDriverEntryPointSuccess)
+    return false;
+  CUmoduleLoadingMode mode = CU_MODULE_EAGER_LOADING;
+  if (reinterpret_cast<PFN_cuModuleGetLoadingMode_v11070>(fn)(&mode) != CUDA_SUCCESS) return false;
+  return mode == CU_MODULE_LAZY_LOADING;
+}
+
 int rs_peer_connect_local(rs_peer* p, rs_peer* const* peers) {
   if (!p || !peers || p->d_boxes) {
     set_error(RS_ERR_ARG, "rs_peer_connect_local: bad arguments (or already connected)");
     return RS_ERR_ARG;
   }
+  for (int r = 0; r < p->nranks; ++r)
+    if (r != p->rank && peers[r]->device == p->device && lazy_module_loading()) {
+      set_error(RS_ERR_UNSUPPORTED,
+                "rs_peer_connect_local: ranks sharing one GPU need CUDA_MODULE_LOADING=EAGER (set before CUDA "
+                "initialises): a lazily loaded kernel's first launch can wait on another rank's spinning collective");
+      return RS_ERR_UNSUPPORTED;
+    }
   p->boxes.assign(p->nranks, nullptr);
   p->opened.assign(p->nranks, false);
   for (int r = 0; r < p->nranks; ++r) p->boxes[r] = peers[r]->box;

@@ -29,7 +29,7 @@ from dataclasses import dataclass, replace
 import numpy as np
 
 from . import _native as N
-from .krylov import ConvergenceHistory, _Workspace, _check_ortho, _gmres_device, _p
+from .krylov import _DCGS_MAX_RESTART, ConvergenceHistory, _Workspace, _check_ortho, _gmres_device, _p
 from .relax import BlockPartition, RelaxConfig
 from .sparse import CsrMatrix, DeviceMatrix, _torch
 
@@ -482,7 +482,7 @@ def gmres(A: DistMatrix, b_local, m: HybridPreconditioner | None = None, restart
         raise ValueError(f"distributed gmres supports ortho 'auto', 'cgs2' or 'dcgs2', got {ortho!r}")
     if ortho == "auto":
         even = all(int(hi - lo) % 2 == 0 for lo, hi in zip(A.offsets[:-1], A.offsets[1:]))
-        ortho = "dcgs2" if restart <= 63 and even else "cgs2"
+        ortho = "dcgs2" if restart <= _DCGS_MAX_RESTART and even else "cgs2"
     _check_ortho(ortho, A.dm.nrows, restart)
     if not tol > 0:
         raise ValueError(f"tol must be positive, got {tol}")

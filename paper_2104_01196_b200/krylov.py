@@ -493,8 +493,6 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
             else:
                 chk(lib.rs_spmv(dm.handle, _p(src), None, None, _p(dst), st), "spmv")
 
-    if ortho == "dcgs2" and restart > 63 and peer is not None:
-        ortho = "cgs2"  # segmented DCGS2 steps (> 64 basis rows) are single-process only
     blas_order = ortho == "mgs_ref"
     if blas_order and reduce_fn is not None:
         raise ValueError("ortho='mgs_ref' (the reference's BLAS summation order) is single-GPU only")

@@ -11,8 +11,11 @@ the DCGS2 kernels), threads (2 host threads on their own streams sharing one han
 Every check compares with the oracle or the serial result, so a silent corruption also fails.
 """
 
+import os
 import sys
 import threading
+
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")  # thread ranks share one GPU (peer.cu: lazy_module_loading)
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent

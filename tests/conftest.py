@@ -1,4 +1,5 @@
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -8,6 +9,11 @@ import pytest
 ROOT = Path(__file__).resolve().parent.parent
 GOLDEN = ROOT / "tests" / "golden"
 sys.path.insert(0, str(ROOT))
+
+# Thread ranks sharing one GPU (ThreadComm peer tests) need eager module loading: under lazy loading
+# a kernel's first launch can wait on another rank's spinning peer collective (rs_peer_connect_local
+# refuses to connect them otherwise).  Read when CUDA initialises, i.e. after this import.
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 
 def pytest_configure(config):

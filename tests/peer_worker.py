@@ -87,6 +87,12 @@ def main():
     _, h2_p = gd.gmres(A_p, b, pc2_p, restart=30, tol=1e-9)
     out["its_nt2_nccl"], out["its_nt2_peer"] = h2_n.iterations, h2_p.iterations
     out["history_nt2_bitwise"] = bool(np.array_equal(h2_n.rel_res, h2_p.rel_res))
+    # restart 80: DCGS2 steps past 64 basis vectors (two-segment passes, dots summed by one peer
+    # allreduce after them) against the NCCL reductions
+    _, h8_n = gd.gmres(A_n, b, pc_n, restart=80, tol=1e-9)
+    _, h8_p = gd.gmres(A_p, b, pc_p, restart=80, tol=1e-9)
+    out["its_m80_nccl"], out["its_m80_peer"] = h8_n.iterations, h8_p.iterations
+    out["history_m80_bitwise"] = bool(np.array_equal(h8_n.rel_res, h8_p.rel_res))
     golden = json.loads((ROOT / "tests" / "golden" / "gmres.json").read_text())
     key = f"lap3d_{nx}__m60__hybrid_gs2_1_1_1__P{world}"
     out["its_reference"] = golden["runs"].get(key, {}).get("iterations")
@@ -119,6 +125,8 @@ def main():
     ok = out["spmv_bitwise"] and out["allreduce_rank_order"] and out["converged"]
     ok &= out["its_peer"] == out["its_nccl"] if world <= 2 else abs(out["its_peer"] - out["its_nccl"]) <= 2
     ok &= abs(out["its_cgs2_peer"] - out["its_peer"]) <= 2
+    ok &= h8_p.converged and (out["its_m80_peer"] == out["its_m80_nccl"] if world <= 2
+                              else abs(out["its_m80_peer"] - out["its_m80_nccl"]) <= 2)
     if world <= 2:
         ok &= out["history_bitwise"] and out["history_nt2_bitwise"] and out["history_cgs2_bitwise"]
     if out["its_reference"] is not None:

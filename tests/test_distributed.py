@@ -295,6 +295,42 @@ def test_peer_mailboxes_thread_ranks_bitwise(nparts, gmres_golden):
         assert abs(len(peer[0][0]) - 1 - gmres_golden["runs"][key]["iterations"]) <= 1
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("nparts,restart", [(2, 80), (4, 127)])
+def test_peer_segmented_dcgs2_thread_ranks(nparts, restart):
+    """DCGS2 steps with more than 64 basis vectors (two 64-row segments) on the peer-memory path:
+    the 2k segment dots are summed over ranks by one peer allreduce after the two passes and the
+    update's norm / flags in the second segment's last CTA.  Histories and iterates bitwise equal
+    to the host rank-order reductions, and the same count as CGS2 at the same P."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2104_01196_b200 as g2
+    from paper_2104_01196_b200 import distributed as gd
+
+    a = g2.laplace3d(32)
+
+    def fn(ortho):
+        def run(comm):
+            A = gd.DistMatrix.from_csr(comm, a)
+            b = gd.local_rhs(A, 0)
+            pc = gd.HybridPreconditioner(A, g2.RelaxConfig(1, 1, 1))
+            x, h = gd.gmres(A, b, pc, restart=restart, tol=1e-9, ortho=ortho)
+            out = (np.asarray(h.rel_res), x.cpu().numpy())
+            A.close()
+            return out
+        return run
+
+    host = _run_ranks_cls(nparts, fn("dcgs2"), ThreadComm)
+    peer = _run_ranks_cls(nparts, fn("dcgs2"), _ThreadPeerComm)
+    cgs2 = _run_ranks_cls(nparts, fn("cgs2"), _ThreadPeerComm)
+    assert len(peer[0][0]) - 1 > 64  # the run reaches the segmented steps
+    for r in range(nparts):
+        assert np.array_equal(host[r][0], peer[r][0]), f"rank {r}: histories differ"
+        assert np.array_equal(host[r][1], peer[r][1]), f"rank {r}: iterates differ"
+    assert len(peer[0][0]) == len(cgs2[0][0])
+    np.testing.assert_allclose(peer[0][0], cgs2[0][0], rtol=1e-6)
+
+
 def _slab_blocks(n, plane, world):
     """(lo, hi, halo_lo, halo_hi) of the C5 z-slab partition (BlockPartition.regular, relax.py:89-92)
     of a grid with `plane` rows per z-plane: one plane of halo per neighbour (7-point stencil)."""

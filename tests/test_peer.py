@@ -71,4 +71,4 @@ def test_peer_collectives_match_nccl(nproc):
     assert res["ok"], res
     assert res["spmv_bitwise"] and res["allreduce_rank_order"]
     if nproc <= 2:
-        assert res["history_bitwise"] and res["history_nt2_bitwise"]
+        assert res["history_bitwise"] and res["history_nt2_bitwise"] and res["history_m80_bitwise"]
