@@ -359,6 +359,17 @@ int rs_dcgs2_update(const double *V, int64_t ldv, int k, int64_t n, const double
                     double *vrow, double *urow, double *nrm2, double *work, rs_peer *peer, uint64_t epoch,
                     const int64_t *flags, double *status_out, double *seg_tmp, rs_stream_t stream);
 
+/* CUDA graphs of captured launch sequences (the GMRES host loop captures each Arnoldi step of a
+ * small, launch-latency-bound problem once and replays it every cycle; no reference counterpart).
+ * rs_graph_begin starts a thread-local capture on a non-default stream; every library call made on
+ * that stream until rs_graph_end is recorded, not run; rs_graph_launch replays it.  The launch
+ * counter counts replayed kernels, not captured ones. */
+typedef struct rs_graph rs_graph;
+int rs_graph_begin(rs_stream_t stream);
+int rs_graph_end(rs_stream_t stream, rs_graph **out);
+int rs_graph_launch(rs_graph *g, rs_stream_t stream);
+int rs_graph_destroy(rs_graph *g);
+
 /* ---- multi-GPU: NVLink peer-memory collectives ----
  *
  * Replaces the reference's distributed halo exchange / dot allreduce seam

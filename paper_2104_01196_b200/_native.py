@@ -91,6 +91,10 @@ _SIGS = {
     "rs_gemv_n_blas": ([_P, _I64, C.c_int, _I64, _P, _P, _P], C.c_int),
     "rs_host_ddot_blas": ([_I64, _P, _P], C.c_double),
     "rs_host_givens": ([_P, C.c_int, _P, _P, _P, C.c_int], C.c_double),
+    "rs_graph_begin": ([_P], C.c_int),
+    "rs_graph_end": ([_P, C.POINTER(_P)], C.c_int),
+    "rs_graph_launch": ([_P, _P], C.c_int),
+    "rs_graph_destroy": ([_P], C.c_int),
     "rs_axpy": ([_I64, C.c_double, _P, _P, _P], C.c_int),
     "rs_xpby": ([_I64, _P, C.c_double, _P, _P], C.c_int),
     "rs_cg_update": ([_I64, _P, _P, _P, _P, _P, _P, _P, _P], C.c_int),

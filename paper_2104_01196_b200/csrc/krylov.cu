@@ -1424,4 +1424,74 @@ int rs_cast_f32_f64(int64_t n, const float* in, double* out, rs_stream_t stream)
   return RS_OK;
 }
 
+// ---- CUDA graphs of whole Arnoldi steps (latency-bound small problems) ----
+// The host captures the launches of one step into a graph once and replays it every cycle; the
+// kernels counted while capturing did not run, so the counter moves from capture to replay.
+struct rs_graph {
+  cudaGraphExec_t exec = nullptr;
+  long long kernels = 0;
+};
+
+int rs_graph_begin(rs_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!st) {
+    set_error(RS_ERR_ARG, "rs_graph_begin: the legacy default stream cannot be captured");
+    return RS_ERR_ARG;
+  }
+  RS_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  return RS_OK;
+}
+
+int rs_graph_end(rs_stream_t stream, rs_graph** out) {
+  if (!out) {
+    set_error(RS_ERR_ARG, "rs_graph_end: bad arguments");
+    return RS_ERR_ARG;
+  }
+  *out = nullptr;
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture((cudaStream_t)stream, &g);
+  if (e != cudaSuccess || !g) {
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    return cuda_error(e != cudaSuccess ? e : cudaErrorStreamCaptureInvalidated, "rs_graph_end (capture)");
+  }
+  size_t nn = 0;
+  cudaGraphGetNodes(g, nullptr, &nn);
+  std::vector<cudaGraphNode_t> nodes(nn);
+  if (nn) cudaGraphGetNodes(g, nodes.data(), &nn);
+  long long kernels = 0;
+  for (size_t i = 0; i < nn; ++i) {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(nodes[i], &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++kernels;
+  }
+  rs_graph* r = new rs_graph();
+  r->kernels = kernels;
+  e = cudaGraphInstantiate(&r->exec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    delete r;
+    return cuda_error(e, "rs_graph_end (instantiate)");
+  }
+  uncount_launches(kernels);
+  *out = r;
+  return RS_OK;
+}
+
+int rs_graph_launch(rs_graph* g, rs_stream_t stream) {
+  if (!g || !g->exec) {
+    set_error(RS_ERR_ARG, "rs_graph_launch: bad arguments");
+    return RS_ERR_ARG;
+  }
+  RS_CUDA(cudaGraphLaunch(g->exec, (cudaStream_t)stream));
+  uncount_launches(-g->kernels);
+  return RS_OK;
+}
+
+int rs_graph_destroy(rs_graph* g) {
+  if (!g) return RS_OK;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  delete g;
+  return RS_OK;
+}
+
 }  // extern "C"

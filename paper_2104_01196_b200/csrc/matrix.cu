@@ -24,6 +24,7 @@ namespace rs {
 
 static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void uncount_launches(long long n) { g_launches.fetch_sub(n, std::memory_order_relaxed); }
 
 static thread_local std::string g_err;
 static thread_local int64_t g_err_index = -1;

@@ -43,6 +43,7 @@ int cuda_error(cudaError_t e, const char* where);
 
 // number of kernels this library has launched (rs_launch_count, bench evidence)
 void count_launch();
+void uncount_launches(long long n);  // graph capture: counted launches that did not run (n < 0: replayed)
 #define RS_COUNT_LAUNCH() ::rs::count_launch()
 
 #define RS_CHECK_LAUNCH(where)                                   \

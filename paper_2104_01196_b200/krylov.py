@@ -238,6 +238,77 @@ _DCGS_COEF = 2 * 128 + 2  # rs_dcgs2_* coefficient block (include/gs2b200.h)
 _DCGS_MAX_RESTART = 127   # DCGS2 steps of up to 128 basis vectors (two 64-row segments beyond 64)
 _DEFER_NORM = __import__("os").environ.get("RS_DEFER_NORM", "1") != "0"  # A/B switch (profiles/ortho_probe.py)
 _FUSE_COEF = __import__("os").environ.get("RS_DCGS_FUSE_COEF", "1") != "0"  # A/B switch
+# CUDA graphs of whole DCGS2 Arnoldi steps for small (launch-latency-bound) single-GPU solves
+_GRAPHS = __import__("os").environ.get("RS_GRAPH", "1") != "0"
+_GRAPH_MAX_N = int(__import__("os").environ.get("RS_GRAPH_MAX_N", str(1 << 20)))
+
+
+class _StepGraphs:
+    """Per-thread cache of captured DCGS2 Arnoldi steps (rs_graph_*), valid for one (workspace,
+    matrix, operator, stream, step layout) key: step jj's launches reference only the fixed
+    workspace buffers, so one capture serves every cycle and every later solve with the same key.
+    A step runs eagerly the first time (lazy allocations, kernel attributes), is captured the
+    second time and replayed from then on.  Only the last key's graphs are kept."""
+
+    _tls = threading.local()
+
+    @classmethod
+    def get(cls, key, refs):
+        import weakref
+
+        g = getattr(cls._tls, "g", None)
+        if g is not None and g.key == key and all(r() is o for r, o in zip(g.refs, refs)):
+            return g
+        if g is not None:
+            g.close()
+        g = cls()
+        g.key = key
+        g.refs = [weakref.ref(o) for o in refs]
+        cls._tls.g = g
+        return g
+
+    def __init__(self):
+        self.graphs = {}
+        self.seen = set()
+        self.broken = False
+
+    def run(self, jj, body, st):
+        """Run step jj's launches through its graph (capturing it on the second visit)."""
+        lib = N.load()
+        g = self.graphs.get(jj)
+        if g is None and not self.broken and jj in self.seen:
+            N.check(lib.rs_graph_begin(st), "rs_graph_begin")
+            try:
+                body()
+            finally:
+                h = C.c_void_p()
+                s = lib.rs_graph_end(st, C.byref(h))
+            if s:
+                self.broken = True  # a launch that cannot be captured: this key runs eagerly
+            else:
+                g = self.graphs[jj] = h
+        if g is None:
+            self.seen.add(jj)
+            body()
+            return
+        N.check(lib.rs_graph_launch(g, st), "rs_graph_launch")
+
+    def close(self):
+        lib = N.load()
+        for h in self.graphs.values():
+            lib.rs_graph_destroy(h)
+        self.graphs.clear()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 -- interpreter shutdown
+            pass
+
+
+def _graphs_apply(n, ortho, op, peer, reduce_fn, spmv_fn) -> bool:
+    return (_GRAPHS and ortho == "dcgs2" and n <= _GRAPH_MAX_N and peer is None and reduce_fn is None
+            and spmv_fn is None and (op is None or isinstance(op, Preconditioner)) and KernelTimer._active is None)
 _DEFER_START = __import__("os").environ.get("RS_DEFER_START", "1") != "0"  # A/B switch (deferred GMRES start)
 
 
@@ -372,7 +443,16 @@ def gmres(a, b, m=None, restart: int = 60, tol: float = 1e-9, maxit: int = 10000
              else torch.from_numpy(np.array(x0, dtype=np.float64)).to(dev))
     ortho = _check_ortho(ortho, n, restart)
     op = _as_operator(m)
-    x, hist, conv = _gmres_device(dm, bt, x, op, restart, tol, maxit, ortho=ortho, x_zero=x0 is None)
+    cur = torch.cuda.current_stream(dev)
+    if cur.cuda_stream == 0 and _graphs_apply(n, ortho, op, None, None, None):
+        # the legacy default stream cannot be captured: run the solve on this thread's side stream
+        side = _side_stream(dev)
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            x, hist, conv = _gmres_device(dm, bt, x, op, restart, tol, maxit, ortho=ortho, x_zero=x0 is None)
+        cur.wait_stream(side)
+    else:
+        x, hist, conv = _gmres_device(dm, bt, x, op, restart, tol, maxit, ortho=ortho, x_zero=x0 is None)
     if numpy_out or cpu_tensor_out:
         # D2H through page-locked memory (torch's caching host allocator): DMA-speed read-back
         host = torch.empty(n, dtype=torch.float64, pin_memory=True)
@@ -381,8 +461,27 @@ def gmres(a, b, m=None, restart: int = 60, tol: float = 1e-9, maxit: int = 10000
     return x, ConvergenceHistory(np.array(hist), conv)
 
 
+_SIDE = threading.local()
+
+
+def _side_stream(dev):
+    """This thread's non-default stream on ``dev`` (graph capture needs one)."""
+    torch = _torch()
+    d = getattr(_SIDE, "d", None)
+    if d is None:
+        d = _SIDE.d = {}
+    key = str(dev)
+    if key not in d:
+        d[key] = torch.cuda.Stream(device=dev)
+    return d[key]
+
+
 def release_workspace() -> None:
-    """Free this thread's cached GMRES basis (the next solve re-allocates it)."""
+    """Free this thread's cached GMRES basis and step graphs (the next solve re-creates them)."""
+    g = getattr(_StepGraphs._tls, "g", None)
+    if g is not None:
+        g.close()
+        _StepGraphs._tls.g = None
     _Workspace._tls.ws = None
 
 
@@ -656,7 +755,19 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
     pflags, pH, pcoef, pn2, pst12 = _p(ws.flags), _p(ws.H), _p(ws.coef), _p(nrm2_slot), _p(status[1:3])
     pseg = _p(ws.seg_tmp) if ws.seg_tmp is not None else None
 
+    graphs = None
+    if _graphs_apply(n, ortho, op, peer, reduce_fn, spmv_fn) and st.value:
+        graphs = _StepGraphs.get((n, restart, st.value, dm.handle.value, defer_norm, fuse_coef),
+                                 [ws, dm] + ([op] if op is not None else []))
+
     def enqueue_dcgs(jj):
+        if graphs is not None:
+            graphs.run(jj, lambda: dcgs_body(jj), st)
+        else:
+            dcgs_body(jj)
+        return next_event()
+
+    def dcgs_body(jj):
         """DCGS2 step jj: w = A M u_jj, dual dots, coefficients (finalises Hessenberg column jj-1),
         v_jj = reorthogonalised u_jj, u_jj+1 = next tentative vector; jj == restart only finalises
         the last column.  Column jj-1 (rows 0..jj) goes to pinned slot jj % 2."""
@@ -710,7 +821,6 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
                     reduce_(ws.dots[:k])
             chk(lib.rs_dcgs2_coef(k, _p(ws.dots), _p(ws.H), ldh, None, _p(nrm2_slot), 1, stage_ptr(jj), m1,
                                   _p(status[1:3]), _p(ws.flags), int(defer_norm), st), "dcgs2_coef")
-        return next_event()
 
     while total < maxit and not converged:
         beta = rnorm

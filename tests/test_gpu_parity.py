@@ -932,3 +932,49 @@ def test_fp32_symmetric_preconditioner_fused_bitwise(gen):
     with pytest.raises(OverflowError):
         g2.Preconditioner(h, "sgs2", g2.RelaxConfig(1, 1, 1), precision="single_inside_double").apply(
             np.full(h.nrows, 1e300))
+
+
+def test_gmres_step_graphs_match_eager():
+    """Small single-GPU DCGS2 solves replay each Arnoldi step from a captured CUDA graph (the step
+    runs eagerly once, is captured on its second visit): histories and iterates bitwise the eager
+    launches, across cycles and across solves sharing the graphs, for GS2 / SGS2 / fp32-inside /
+    level-scheduled and multicolour GS, damped JR, no preconditioner, segmented restarts, and on a
+    caller's non-default stream."""
+    from paper_2104_01196_b200 import _native, krylov
+
+    a = g2.laplace2d(64)
+    b = g2.random_rhs(a.nrows, 0)
+    cases = [(g2.Preconditioner(a, "gs2", g2.RelaxConfig(2, 1, 1)), 30),
+             (g2.Preconditioner(a, "sgs2", g2.RelaxConfig(1, 1, 1)), 20),
+             (g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, 1), precision="single_inside_double"), 30),
+             (None, 30), (g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, 1)), 80),
+             (g2.Preconditioner(a, "gs_seq", g2.RelaxConfig(2)), 30), (g2.Preconditioner(a, "mt_gs"), 30),
+             (g2.Preconditioner(a, "jr", g2.RelaxConfig(2, omega=0.8)), 30)]
+    lib = _native.load()
+    try:
+        for pc, m in cases:
+            krylov._GRAPHS = False
+            x0, h0 = g2.gmres(a, b, pc, restart=m, tol=1e-10, maxit=400)
+            krylov._GRAPHS = True
+            for rep in range(2):
+                l0 = lib.rs_launch_count()
+                x1, h1 = g2.gmres(a, b, pc, restart=m, tol=1e-10, maxit=400)
+                torch.cuda.synchronize()
+                assert np.array_equal(h0.rel_res, h1.rel_res), (pc and pc.kind, m, rep)
+                assert np.array_equal(x0, x1), (pc and pc.kind, m, rep)
+                assert lib.rs_launch_count() > l0
+            g = krylov._StepGraphs._tls.g
+            assert g is not None and not g.broken and len(g.graphs) > 0
+        # a caller's own stream is captured directly
+        s = torch.cuda.Stream()
+        bt = torch.from_numpy(b).cuda()
+        with torch.cuda.stream(s):
+            for _ in range(2):
+                x2, h2 = g2.gmres(a, bt, cases[0][0], restart=30, tol=1e-10, maxit=400)
+        s.synchronize()
+        krylov._GRAPHS = False
+        x3, h3 = g2.gmres(a, bt, cases[0][0], restart=30, tol=1e-10, maxit=400)
+        assert np.array_equal(h2.rel_res, h3.rel_res) and torch.equal(x2, x3)
+    finally:
+        krylov._GRAPHS = True
+        krylov.release_workspace()
