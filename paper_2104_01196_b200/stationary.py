@@ -25,12 +25,14 @@ import math
 import numpy as np
 
 from . import _native as N
+from . import krylov as _krylov
 from .krylov import ConvergenceHistory
 from .relax import RelaxConfig, _check_system
 from .sparse import _is_tensor, _torch, as_device, stream_ptr
 
 STATIONARY_KINDS = ("jr", "gs_seq", "sgs_seq", "mt_gs", "mt_sgs", "gs2", "sgs2")
 DIVERGENCE_LIMIT = 1e12  # cli.py:45
+_BATCH = 64  # applications per device batch (the host reads one batch of norms at a time)
 
 
 def stationary_solve(a, b, kind: str = "gs2", cfg: RelaxConfig | None = None, tol: float = 1e-9,
@@ -63,13 +65,54 @@ def stationary_solve(a, b, kind: str = "gs2", cfg: RelaxConfig | None = None, to
         x = x0.to(dev, torch.float64).clone() if _is_tensor(x0) else torch.from_numpy(
             np.array(x0, dtype=np.float64)).to(dev)
     _check_system(dm, bt, x)
+    graphs = _krylov._GRAPHS and dm.nrows <= _krylov._GRAPH_MAX_N and not exact_norms
+    cur = torch.cuda.current_stream(dev)
+    if graphs and cur.cuda_stream == 0:
+        # the legacy default stream cannot be captured: run on this thread's side stream
+        side = _krylov._side_stream(dev)
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            x, hist_arr, converged = _stationary(dm, bt, x, kind, cfg, tol, maxit, exact_norms, graphs)
+        cur.wait_stream(side)
+    else:
+        x, hist_arr, converged = _stationary(dm, bt, x, kind, cfg, tol, maxit, exact_norms, graphs)
+    if numpy_out:
+        return x.cpu().numpy(), ConvergenceHistory(hist_arr, converged)
+    return x, ConvergenceHistory(hist_arr, converged)
+
+
+def _stationary(dm, bt, x, kind, cfg, tol, maxit, exact_norms, graphs):
+    torch = _torch()
+    dev = dm.torch_device
     lib = N.load()
     st = stream_ptr(dm.device_index)
     c = N.RelaxCfg.of(cfg)
     kc = N.PC_KINDS[kind]
     n = dm.nrows
 
+    full = {"seen": False, "graph": None, "broken": False}
+
     def apply(napps, norms=None):
+        if graphs and napps == _BATCH and norms is not None and st.value:
+            # full batches replay one captured graph (the first runs eagerly: lazy workspaces)
+            if full["graph"] is None and full["seen"] and not full["broken"]:
+                N.check(lib.rs_graph_begin(st), "rs_graph_begin")
+                try:
+                    launch(napps, norms)
+                finally:
+                    h = C.c_void_p()
+                    s = lib.rs_graph_end(st, C.byref(h))
+                if s:
+                    full["broken"] = True
+                else:
+                    full["graph"] = h
+            if full["graph"] is not None:
+                N.check(lib.rs_graph_launch(full["graph"], st), "rs_graph_launch")
+                return
+            full["seen"] = True
+        launch(napps, norms)
+
+    def launch(napps, norms=None):
         if napps > 0 or norms is not None:
             N.check(lib.rs_stationary_batch(dm.handle, kc, C.byref(c), C.c_void_p(bt.data_ptr()),
                                             C.c_void_p(x.data_ptr()), int(napps),
@@ -159,11 +202,10 @@ def stationary_solve(a, b, kind: str = "gs2", cfg: RelaxConfig | None = None, to
                 apply(stop)
             if total >= maxit:
                 done = True
-            batch = min(64, 2 * batch)
-    hist_arr = np.array(hist)
-    if numpy_out:
-        return x.cpu().numpy(), ConvergenceHistory(hist_arr, converged)
-    return x, ConvergenceHistory(hist_arr, converged)
+            batch = min(_BATCH, 2 * batch)
+    if full["graph"] is not None:
+        lib.rs_graph_destroy(full["graph"])
+    return x, np.array(hist), converged
 
 
 def _dot_blas_host(lib, n, vec, scal, st):

@@ -978,3 +978,24 @@ def test_gmres_step_graphs_match_eager():
     finally:
         krylov._GRAPHS = True
         krylov.release_workspace()
+
+
+def test_stationary_batch_graphs_match_eager():
+    """The smoother's full 64-application batches replay one captured graph on small problems:
+    histories and iterates bitwise the eager batches (GS2, SGS2, JR, MT-GS, level-scheduled GS)."""
+    from paper_2104_01196_b200 import krylov
+
+    a = g2.laplace2d(48)
+    b = g2.random_rhs(a.nrows, 0)
+    try:
+        for kind, cfg in (("gs2", g2.RelaxConfig(2, 1, 1)), ("sgs2", g2.RelaxConfig(1, 1, 2)),
+                          ("jr", g2.RelaxConfig(1, 1, 1, omega=0.8)), ("mt_gs", g2.RelaxConfig()),
+                          ("gs_seq", g2.RelaxConfig())):
+            krylov._GRAPHS = False
+            x0, h0 = g2.stationary_solve(a, b, kind, cfg, tol=1e-8, maxit=700)
+            krylov._GRAPHS = True
+            x1, h1 = g2.stationary_solve(a, b, kind, cfg, tol=1e-8, maxit=700)
+            assert h0.iterations > 130, kind  # at least two full batches
+            assert np.array_equal(h0.rel_res, h1.rel_res) and np.array_equal(x0, x1), kind
+    finally:
+        krylov._GRAPHS = True
