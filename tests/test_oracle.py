@@ -316,3 +316,20 @@ def test_oracle_stationary_histories(label, stationary_golden):
         conv = hist[-1] <= want["tol"]
     assert conv == want["converged"]
     assert hist == want["rel_res"]
+
+
+def test_c4_oracle_fixture_reproduces():
+    """tests/golden/oracle_c4.json (the C4 histories beyond the reference's 16^3) is what the pinned
+    oracle computes: re-run the 32^3 entries here."""
+    import json
+    from pathlib import Path
+
+    import paper_2104_01196_b200 as g2
+
+    runs = json.loads((Path(__file__).parent / "golden" / "oracle_c4.json").read_text())["runs"]
+    a = g2.convdiff3d(32, (50.0, 25.0, 10.0))
+    b = g2.random_rhs(a.nrows, 0)
+    for prec in ("same", "single_inside_double"):
+        m = oracle.Precond(a, "gs2", g2.RelaxConfig(1, 1, 2), precision=prec)
+        _, hist, conv = oracle.gmres(a, b, m, restart=60, tol=1e-9)
+        assert conv and np.array_equal(hist, np.asarray(runs[f"cd3d_32__m60__gs2_1_1_2__{prec}"]["rel_res"]))
