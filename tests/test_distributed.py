@@ -407,3 +407,37 @@ def test_gloo_c5_slab_exchange_and_reductions(world):
     for p in procs:
         p.join(timeout=60)
     assert res == {r: True for r in range(world)}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nx", [64, 128])
+@pytest.mark.parametrize("nparts", [2, 4, 8])
+def test_c5_partition_counts_beyond_golden(nx, nparts):
+    """C5's z-slab hybrid block-Jacobi GS2(1,1,1) at 64^3 and 128^3 (beyond the reference's 32^3
+    goldens): P thread ranks on the NVLink-peer path reach the oracle's iteration count (the
+    reference algorithm with P blocks, tests/golden/make_c5_oracle.py) and its final residual."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import json
+    from pathlib import Path
+
+    import paper_2104_01196_b200 as g2
+    from paper_2104_01196_b200 import distributed as gd
+
+    want = json.loads((Path(__file__).parent / "golden" / "oracle_c5.json").read_text())["runs"][
+        f"lap3d_{nx}__m60__hybrid_gs2_1_1_1__P{nparts}"]
+    a = g2.laplace3d(nx)
+
+    def fn(comm):
+        A = gd.DistMatrix.from_csr(comm, a)
+        b = gd.local_rhs(A, 0)
+        pc = gd.HybridPreconditioner(A, g2.RelaxConfig(1, 1, 1))
+        _, h = gd.gmres(A, b, pc, restart=60, tol=1e-9)
+        A.close()
+        return h.iterations, h.converged, h.final_rel_res
+
+    res = _run_ranks_cls(nparts, fn, _ThreadPeerComm)
+    assert all(r == res[0] for r in res)
+    its, conv, rel = res[0]
+    print(nx, nparts, its, want["iterations"], rel)
+    assert conv and its == want["iterations"], (its, want["iterations"])

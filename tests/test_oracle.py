@@ -333,3 +333,14 @@ def test_c4_oracle_fixture_reproduces():
         m = oracle.Precond(a, "gs2", g2.RelaxConfig(1, 1, 2), precision=prec)
         _, hist, conv = oracle.gmres(a, b, m, restart=60, tol=1e-9)
         assert conv and np.array_equal(hist, np.asarray(runs[f"cd3d_32__m60__gs2_1_1_2__{prec}"]["rel_res"]))
+
+
+def test_c5_oracle_fixture_agrees_with_reference(gmres_golden):
+    """tests/golden/oracle_c5.json (C5's slab partition beyond the reference's 32^3) meets the one
+    reference golden it overlaps: laplace3d 64^3 with 8 hybrid blocks, 360 iterations."""
+    import json
+    from pathlib import Path
+
+    runs = json.loads((Path(__file__).parent / "golden" / "oracle_c5.json").read_text())["runs"]
+    key = "lap3d_64__m60__hybrid_gs2_1_1_1__P8"
+    assert runs[key]["iterations"] == gmres_golden["runs"][key]["iterations"] == 360
