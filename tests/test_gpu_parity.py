@@ -1020,3 +1020,20 @@ def test_c4_oracle_histories(nx, prec):
     assert np.array_equal(np.asarray(h.rel_res), np.asarray(want["rel_res"])), (nx, prec)
     _, hd = g2.gmres(a, b, m, restart=60, tol=1e-9)
     assert hd.converged and hd.iterations == want["iterations"], (hd.iterations, want["iterations"])
+
+
+@pytest.mark.parametrize("nx", [32, 64])
+@pytest.mark.parametrize("nj", [1, 3])
+def test_c3_oracle_counts(nx, nj):
+    """C3 (elasticity 27-point, 3 dof/node) GMRES(60) + GS2(1,1,n_j) at 32^3 and the config's 64^3:
+    the oracle's iteration counts (tests/golden/make_c3_oracle.py; the reference's goldens stop at
+    smaller elasticity grids)."""
+    import json
+    from pathlib import Path
+
+    want = json.loads((Path(__file__).parent / "golden" / "oracle_c3.json").read_text())["runs"][
+        f"el3d_{nx}__m60__gs2_1_1_{nj}"]
+    a = g2.elasticity3d(nx)
+    b = g2.random_rhs(a.nrows, 0)
+    _, h = g2.gmres(a, b, g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, nj)), restart=60, tol=1e-9, maxit=3000)
+    assert h.converged and h.iterations == want["iterations"], (h.iterations, want["iterations"])
