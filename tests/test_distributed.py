@@ -441,3 +441,31 @@ def test_c5_partition_counts_beyond_golden(nx, nparts):
     its, conv, rel = res[0]
     print(nx, nparts, its, want["iterations"], rel)
     assert conv and its == want["iterations"], (its, want["iterations"])
+
+
+@pytest.mark.gpu
+def test_distributed_dcgs2_odd_slabs_refused():
+    """Slabs with odd row counts: ortho='auto' takes CGS2 (counts as the reference's hybrid), an
+    explicit ortho='dcgs2' is refused up front on every rank (no collective is entered)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2104_01196_b200 as g2
+    from paper_2104_01196_b200 import distributed as gd
+
+    a = g2.laplace3d(9)  # 729 rows over 3 ranks: 243 each
+
+    def fn(ortho):
+        def run(comm):
+            A = gd.DistMatrix.from_csr(comm, a)
+            b = gd.local_rhs(A, 0)
+            try:
+                return gd.gmres(A, b, gd.HybridPreconditioner(A, g2.RelaxConfig(1, 1, 1)), restart=30,
+                                tol=1e-9, ortho=ortho)[1].iterations
+            finally:
+                A.close()
+        return run
+
+    its = _run_ranks(3, fn("auto"))
+    assert len(set(its)) == 1 and its[0] > 0
+    with pytest.raises(ValueError, match="even row count"):
+        _run_ranks(3, fn("dcgs2"))
