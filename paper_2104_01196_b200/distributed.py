@@ -480,13 +480,8 @@ def gmres(A: DistMatrix, b_local, m: HybridPreconditioner | None = None, restart
     see krylov.gmres).  "auto" resolves on the global shape so every rank picks the same mode."""
     if ortho not in ("auto", "cgs2", "dcgs2"):
         raise ValueError(f"distributed gmres supports ortho 'auto', 'cgs2' or 'dcgs2', got {ortho!r}")
-    even = all(int(hi - lo) % 2 == 0 for lo, hi in zip(A.offsets[:-1], A.offsets[1:]))
     if ortho == "auto":
-        ortho = "dcgs2" if restart <= _DCGS_MAX_RESTART and even else "cgs2"
-    elif ortho == "dcgs2" and not even:
-        # the single-GPU odd-n DCGS2 passes are not wired through the distributed halo / peer path
-        raise ValueError("distributed ortho='dcgs2' needs an even row count on every rank (ortho='auto' "
-                         "takes CGS2 there)")
+        ortho = "dcgs2" if restart <= _DCGS_MAX_RESTART else "cgs2"
     _check_ortho(ortho, A.dm.nrows, restart)
     if not tol > 0:
         raise ValueError(f"tol must be positive, got {tol}")

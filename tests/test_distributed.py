@@ -444,28 +444,35 @@ def test_c5_partition_counts_beyond_golden(nx, nparts):
 
 
 @pytest.mark.gpu
-def test_distributed_dcgs2_odd_slabs_refused():
-    """Slabs with odd row counts: ortho='auto' takes CGS2 (counts as the reference's hybrid), an
-    explicit ortho='dcgs2' is refused up front on every rank (no collective is entered)."""
+@pytest.mark.parametrize("nx,nparts", [(33, 3), (31, 2)])
+def test_distributed_dcgs2_odd_slabs(nx, nparts):
+    """Slabs with odd row counts (33^3 over 3 ranks: 11,979 rows each; 31^3 over 2: 14,896 / 14,895)
+    take DCGS2 like even ones (the passes read one padded element past an odd row): host rank-order
+    and NVLink-peer reductions bitwise, same count as CGS2, at restart 60 and 80 (segmented)."""
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
     import paper_2104_01196_b200 as g2
     from paper_2104_01196_b200 import distributed as gd
 
-    a = g2.laplace3d(9)  # 729 rows over 3 ranks: 243 each
+    a = g2.laplace3d(nx)
 
-    def fn(ortho):
+    def fn(ortho, restart):
         def run(comm):
             A = gd.DistMatrix.from_csr(comm, a)
             b = gd.local_rhs(A, 0)
             try:
-                return gd.gmres(A, b, gd.HybridPreconditioner(A, g2.RelaxConfig(1, 1, 1)), restart=30,
-                                tol=1e-9, ortho=ortho)[1].iterations
+                x, h = gd.gmres(A, b, gd.HybridPreconditioner(A, g2.RelaxConfig(1, 1, 1)), restart=restart,
+                                tol=1e-9, ortho=ortho)
+                return np.asarray(h.rel_res), x.cpu().numpy(), A.hi - A.lo
             finally:
                 A.close()
         return run
 
-    its = _run_ranks(3, fn("auto"))
-    assert len(set(its)) == 1 and its[0] > 0
-    with pytest.raises(ValueError, match="even row count"):
-        _run_ranks(3, fn("dcgs2"))
+    for restart in (60, 80):
+        host = _run_ranks_cls(nparts, fn("auto", restart), ThreadComm)
+        peer = _run_ranks_cls(nparts, fn("dcgs2", restart), _ThreadPeerComm)
+        cgs2 = _run_ranks_cls(nparts, fn("cgs2", restart), _ThreadPeerComm)
+        assert any(r[2] % 2 for r in host)
+        for r in range(nparts):
+            assert np.array_equal(host[r][0], peer[r][0]) and np.array_equal(host[r][1], peer[r][1]), (restart, r)
+        assert len(peer[0][0]) == len(cgs2[0][0]), restart
