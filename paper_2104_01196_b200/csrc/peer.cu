@@ -10,6 +10,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -214,11 +215,18 @@ int rs_peer_connect_local(rs_peer* p, rs_peer* const* peers) {
     set_error(RS_ERR_ARG, "rs_peer_connect_local: bad arguments (or already connected)");
     return RS_ERR_ARG;
   }
+  // Same-device ranks also need a hardware work queue per stream: with the default 8 connections
+  // streams share queues, and a rank's kernel queued behind another rank's spinning collective in
+  // the same queue never starts (5 thread ranks hung this way; 32 connections run them).
+  const char* conn = getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+  const bool wide = conn && atoi(conn) >= 32;
   for (int r = 0; r < p->nranks; ++r)
-    if (r != p->rank && peers[r]->device == p->device && lazy_module_loading()) {
+    if (r != p->rank && peers[r]->device == p->device && (lazy_module_loading() || !wide)) {
       set_error(RS_ERR_UNSUPPORTED,
-                "rs_peer_connect_local: ranks sharing one GPU need CUDA_MODULE_LOADING=EAGER (set before CUDA "
-                "initialises): a lazily loaded kernel's first launch can wait on another rank's spinning collective");
+                "rs_peer_connect_local: ranks sharing one GPU need CUDA_MODULE_LOADING=EAGER and "
+                "CUDA_DEVICE_MAX_CONNECTIONS=32 (set before CUDA initialises): a lazily loaded kernel's first "
+                "launch, or a kernel queued behind another rank's spinning collective in a shared hardware "
+                "queue, waits on that collective");
       return RS_ERR_UNSUPPORTED;
     }
   p->boxes.assign(p->nranks, nullptr);

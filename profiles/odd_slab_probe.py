@@ -3,6 +3,7 @@
 single-GPU hybrid count."""
 import os, sys, traceback
 os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]

@@ -16,6 +16,7 @@ import sys
 import threading
 
 os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")  # thread ranks share one GPU (peer.cu: lazy_module_loading)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent

@@ -2,6 +2,7 @@
 CGS2) -- prints each rank's outcome (debug probe for the segmented peer path)."""
 import os, sys, traceback, threading, time
 os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT)); sys.path.insert(0, str(ROOT / "tests"))

@@ -14,6 +14,9 @@ sys.path.insert(0, str(ROOT))
 # a kernel's first launch can wait on another rank's spinning peer collective (rs_peer_connect_local
 # refuses to connect them otherwise).  Read when CUDA initialises, i.e. after this import.
 os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+# ... and one hardware work queue per stream (the default 8 are shared between streams: a rank's
+# kernel queued behind another rank's spinning collective never starts)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 
 def pytest_configure(config):

@@ -262,7 +262,7 @@ def _run_ranks_cls(nranks, fn, cls):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("nparts", [3, 8])
+@pytest.mark.parametrize("nparts", [3, 5, 8])
 def test_peer_mailboxes_thread_ranks_bitwise(nparts, gmres_golden):
     """P ranks as threads on one GPU: the NVLink-peer code path (mailbox halo push / wait kernel,
     allreduces fused into the DCGS2 kernels) at P = 3 and 8 -- the 8-rank layout the 8-GPU box
