@@ -65,6 +65,7 @@ def mt_gs_sweep(a, s: Splitting, coloring: Coloring, b, x, direction: str = "for
         col = np.ascontiguousarray(coloring.color, dtype=np.int64)
         if int(nc.value) != coloring.num_colors or not np.array_equal(cur[: dm.nrows], col):
             N.call("rs_mat_set_coloring", dm.handle, col.ctypes.data, int(coloring.num_colors))
+            dm.layout_epoch += 1
         dm._mt_coloring = coloring
     bv, xv = _vectors(dm, b, x)
     N.call("rs_mt_gs_sweep", dm.handle, bv.ptr, xv.ptr, N.DIRECTIONS[direction], float(s.omega),

@@ -757,7 +757,9 @@ def _gmres_device(dm: DeviceMatrix, b, x, op, restart, tol, maxit, spmv_fn=None,
 
     graphs = None
     if _graphs_apply(n, ortho, op, peer, reduce_fn, spmv_fn) and st.value:
-        graphs = _StepGraphs.get((n, restart, st.value, dm.handle.value, defer_norm, fuse_coef),
+        odev = op.device_matrix if op is not None else None
+        graphs = _StepGraphs.get((n, restart, st.value, dm.handle.value, dm.layout_epoch, defer_norm, fuse_coef,
+                                  odev.layout_epoch if odev is not None else -1),
                                  [ws, dm] + ([op] if op is not None else []))
 
     def enqueue_dcgs(jj):

@@ -160,6 +160,7 @@ class DeviceMatrix:
         self.dtype = np.dtype(np.float32 if dt.value == N.RS_F32 else np.float64)
         self._host = weakref.ref(host) if host is not None else None
         self._single = None
+        self.layout_epoch = 0  # bumped whenever device buffers of the handle are rebuilt
         self._lib = N.load()
 
     # construction ---------------------------------------------------------
@@ -206,6 +207,7 @@ class DeviceMatrix:
         """Drop / rebuild the diagonal-slice and stencil encodings of L and U (A/B switch; results are
         bitwise the same)."""
         N.call("rs_mat_set_dia", self._h, 1 if enable else 0)
+        self.layout_epoch += 1  # captured launch graphs (krylov._StepGraphs) hold the old buffers
 
     def single(self) -> "DeviceMatrix":
         """float32 copy with float32 splitting (cast_matrix + extract_splitting, krylov.py:101-103)."""

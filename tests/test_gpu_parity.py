@@ -1037,3 +1037,28 @@ def test_c3_oracle_counts(nx, nj):
     b = g2.random_rhs(a.nrows, 0)
     _, h = g2.gmres(a, b, g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, nj)), restart=60, tol=1e-9, maxit=3000)
     assert h.converged and h.iterations == want["iterations"], (h.iterations, want["iterations"])
+
+
+def test_gmres_step_graphs_follow_layout_changes():
+    """A handle whose buffers are rebuilt (diagonal-slice / stencil encodings dropped and rebuilt)
+    invalidates the captured step graphs: later solves re-capture and stay bitwise."""
+    from paper_2104_01196_b200 import krylov
+
+    a = g2.laplace3d(24)
+    b = g2.random_rhs(a.nrows, 0)
+    pc = g2.Preconditioner(a, "gs2", g2.RelaxConfig(1, 1, 1))
+    dm = pc.device_matrix
+    try:
+        _, h0 = g2.gmres(a, b, pc, restart=30, tol=1e-10)
+        _, h1 = g2.gmres(a, b, pc, restart=30, tol=1e-10)
+        g_before = krylov._StepGraphs._tls.g
+        dm.set_diagonal_slices(False)
+        _, h2 = g2.gmres(a, b, pc, restart=30, tol=1e-10)
+        assert krylov._StepGraphs._tls.g is not g_before
+        dm.set_diagonal_slices(True)
+        _, h3 = g2.gmres(a, b, pc, restart=30, tol=1e-10)
+        _, h4 = g2.gmres(a, b, pc, restart=30, tol=1e-10)
+        for h in (h1, h2, h3, h4):
+            assert np.array_equal(h0.rel_res, h.rel_res)
+    finally:
+        krylov.release_workspace()
