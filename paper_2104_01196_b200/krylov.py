@@ -240,7 +240,7 @@ _DEFER_NORM = __import__("os").environ.get("RS_DEFER_NORM", "1") != "0"  # A/B s
 _FUSE_COEF = __import__("os").environ.get("RS_DCGS_FUSE_COEF", "1") != "0"  # A/B switch
 # CUDA graphs of whole DCGS2 Arnoldi steps for small (launch-latency-bound) single-GPU solves
 _GRAPHS = __import__("os").environ.get("RS_GRAPH", "1") != "0"
-_GRAPH_MAX_N = int(__import__("os").environ.get("RS_GRAPH_MAX_N", str(1 << 20)))
+_GRAPH_MAX_N = int(__import__("os").environ.get("RS_GRAPH_MAX_N", str(1 << 22)))
 
 
 class _StepGraphs:
