@@ -295,6 +295,8 @@ class _StepGraphs:
 
     def close(self):
         lib = N.load()
+        if self.graphs:
+            _torch().cuda.synchronize()  # a speculative replay may still be running
         for h in self.graphs.values():
             lib.rs_graph_destroy(h)
         self.graphs.clear()
@@ -980,6 +982,19 @@ def cg(a, b, m=None, tol: float = 1e-9, maxit: int = 10000, x0=None):
         raise ValueError("cg needs a double-precision matrix")
     n = dm.nrows
     dev = dm.torch_device
+    graphs = (_GRAPHS and n <= _GRAPH_MAX_N and KernelTimer._active is None
+              and (m is None or isinstance(m, Preconditioner)))
+    cur = torch.cuda.current_stream(dev)
+    if graphs and cur.cuda_stream == 0:
+        # the legacy default stream cannot be captured: the same solve on this thread's side stream
+        side = _side_stream(dev)
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            out = cg(a, b, m, tol, maxit, x0)
+        cur.wait_stream(side)
+        if _is_tensor(out[0]) and out[0].is_cuda:
+            out[0].record_stream(cur)
+        return out
     st = stream_ptr(dm.device_index)
     numpy_out = not _is_tensor(b)
     bt = b.to(dev, torch.float64) if _is_tensor(b) else torch.from_numpy(np.ascontiguousarray(b, np.float64)).to(dev)
@@ -1039,7 +1054,34 @@ def cg(a, b, m=None, tol: float = 1e-9, maxit: int = 10000, x0=None):
 
     next_event = _event_ring(dev)
 
+    # small problems: the two iteration parities are captured as CUDA graphs on their second visit
+    # and replayed (every buffer below is fixed for the solve)
+    cgraph = {"g": {}, "seen": set(), "broken": not (graphs and st.value)}
+
     def enqueue(k):
+        par = k % 2
+        if not cgraph["broken"]:
+            g = cgraph["g"].get(par)
+            if g is None and par in cgraph["seen"]:
+                N.check(lib.rs_graph_begin(st), "rs_graph_begin")
+                try:
+                    cg_body(k)
+                finally:
+                    h = C.c_void_p()
+                    s = lib.rs_graph_end(st, C.byref(h))
+                if s:
+                    cgraph["broken"] = True
+                    cg_body(k)
+                    return next_event()
+                g = cgraph["g"][par] = h
+            if g is not None:
+                N.check(lib.rs_graph_launch(g, st), "rs_graph_launch")
+                return next_event()
+            cgraph["seen"].add(par)
+        cg_body(k)
+        return next_event()
+
+    def cg_body(k):
         """CG iteration k entirely on the device (krylov.py:288-308), scalars staged to pinned slot k%2."""
         xin, xout = xs[k % 2], xs[(k + 1) % 2]
         # SpMV fused with p^T A p, and the true residual norm without storing b - A x
@@ -1052,7 +1094,6 @@ def cg(a, b, m=None, tol: float = 1e-9, maxit: int = 10000, x0=None):
             stage_ovf[k % 2:k % 2 + 1].copy_(_WS.flags[1:2], non_blocking=True)
         chk(lib.rs_dot(n, _p(r), _p(z), _p(rz_s[(k + 1) % 2]), _p(work), st), "dot")
         chk(lib.rs_xpby_dev(n, _p(z), _p(rz_s[(k + 1) % 2]), _p(rz_s[k % 2]), _p(p), st), "xpby")
-        return next_event()
 
     # Software pipeline as in gmres: iteration k+1 is enqueued before the host checks iteration k's
     # scalars; a speculative iteration past convergence (or past an error) is never read.
@@ -1079,6 +1120,10 @@ def cg(a, b, m=None, tol: float = 1e-9, maxit: int = 10000, x0=None):
             break
         if ovf != _I64_MAX:
             raise OverflowError(f"entry {ovf} overflows single precision")
+    if cgraph["g"]:
+        torch.cuda.current_stream(dev).synchronize()  # a speculative replay may still be running
+        for g in cgraph["g"].values():
+            lib.rs_graph_destroy(g)
     if k_last >= 0:
         x = xs[(k_last + 1) % 2]
     return finish(x, hist, converged)

@@ -1062,3 +1062,27 @@ def test_gmres_step_graphs_follow_layout_changes():
             assert np.array_equal(h0.rel_res, h.rel_res)
     finally:
         krylov.release_workspace()
+
+
+def test_cg_graphs_match_eager():
+    """Small PCG solves replay the two iteration parities from captured graphs: histories and
+    iterates bitwise the eager launches (SGS2, fp32-inside SGS2, JR, none)."""
+    from paper_2104_01196_b200 import krylov
+
+    a = g2.laplace2d(64)
+    b = g2.random_rhs(a.nrows, 0)
+    try:
+        for m in (g2.Preconditioner(a, "sgs2", g2.RelaxConfig(1, 1, 1)),
+                  g2.Preconditioner(a, "sgs2", g2.RelaxConfig(1, 1, 1), precision="single_inside_double"),
+                  g2.Preconditioner(a, "jr", g2.RelaxConfig(2, omega=0.8)), None):
+            krylov._GRAPHS = False
+            x0, h0 = g2.cg(a, b, m, tol=1e-10)
+            krylov._GRAPHS = True
+            x1, h1 = g2.cg(a, b, m, tol=1e-10)
+            assert h0.iterations > 10
+            assert np.array_equal(h0.rel_res, h1.rel_res) and np.array_equal(x0, x1)
+        bt = torch.from_numpy(b).cuda()
+        xt, ht = g2.cg(a, bt, g2.Preconditioner(a, "sgs2", g2.RelaxConfig(1, 1, 1)), tol=1e-10)
+        assert xt.is_cuda and ht.converged
+    finally:
+        krylov._GRAPHS = True
