@@ -150,61 +150,64 @@ def _stationary(dm, bt, x, kind, cfg, tol, maxit, exact_norms, graphs):
         hist.append(rel)
         return rel
 
-    if exact_norms:
-        t = torch.empty_like(x)
-        r = torch.empty_like(x)
+    try:
+        if exact_norms:
+            t = torch.empty_like(x)
+            r = torch.empty_like(x)
 
-        def true_rn2():
-            N.check(lib.rs_spmv(dm.handle, C.c_void_p(x.data_ptr()), None, None, C.c_void_p(t.data_ptr()), st),
-                    "spmv")
-            torch.sub(bt, t, out=r)
-            return _dot_blas_host(lib, n, r, scal, st)
+            def true_rn2():
+                N.check(lib.rs_spmv(dm.handle, C.c_void_p(x.data_ptr()), None, None, C.c_void_p(t.data_ptr()), st),
+                        "spmv")
+                torch.sub(bt, t, out=r)
+                return _dot_blas_host(lib, n, r, scal, st)
 
-        rel = record(true_rn2())
-        converged = rel <= tol
-        for _ in range(maxit):
-            if converged:
-                break
-            apply(1)
             rel = record(true_rn2())
-            if not np.isfinite(rel) or rel > DIVERGENCE_LIMIT:
-                break
             converged = rel <= tol
-    else:
-        norms = torch.empty(65, dtype=torch.float64, device=dev)
-        host = torch.empty(65, dtype=torch.float64, pin_memory=True)
-        snap = torch.empty_like(x)
-        apply(0, norms)  # ||b - A x0||^2
-        host[:1].copy_(norms[:1])
-        rel = record(float(host[0]))
-        converged = rel <= tol
-        done = converged or maxit == 0
-        total = 0
-        batch = 1
-        while not done:
-            k = min(batch, maxit - total)
-            snap.copy_(x)
-            apply(k, norms)
-            host[:k + 1].copy_(norms[:k + 1])  # synchronises the stream
-            stop = k
-            for q in range(1, k + 1):
-                rel = record(float(host[q]))
-                total += 1
-                if not np.isfinite(rel) or rel > DIVERGENCE_LIMIT:
-                    done = True
-                elif rel <= tol:
-                    converged = done = True
-                if done:
-                    stop = q
+            for _ in range(maxit):
+                if converged:
                     break
-            if stop < k:  # overshoot: restore the batch's start and re-run the first `stop` applications
-                x.copy_(snap)
-                apply(stop)
-            if total >= maxit:
-                done = True
-            batch = min(_BATCH, 2 * batch)
-    if full["graph"] is not None:
-        lib.rs_graph_destroy(full["graph"])
+                apply(1)
+                rel = record(true_rn2())
+                if not np.isfinite(rel) or rel > DIVERGENCE_LIMIT:
+                    break
+                converged = rel <= tol
+        else:
+            norms = torch.empty(65, dtype=torch.float64, device=dev)
+            host = torch.empty(65, dtype=torch.float64, pin_memory=True)
+            snap = torch.empty_like(x)
+            apply(0, norms)  # ||b - A x0||^2
+            host[:1].copy_(norms[:1])
+            rel = record(float(host[0]))
+            converged = rel <= tol
+            done = converged or maxit == 0
+            total = 0
+            batch = 1
+            while not done:
+                k = min(batch, maxit - total)
+                snap.copy_(x)
+                apply(k, norms)
+                host[:k + 1].copy_(norms[:k + 1])  # synchronises the stream
+                stop = k
+                for q in range(1, k + 1):
+                    rel = record(float(host[q]))
+                    total += 1
+                    if not np.isfinite(rel) or rel > DIVERGENCE_LIMIT:
+                        done = True
+                    elif rel <= tol:
+                        converged = done = True
+                    if done:
+                        stop = q
+                        break
+                if stop < k:  # overshoot: restore the batch's start and re-run the first `stop` applications
+                    x.copy_(snap)
+                    apply(stop)
+                if total >= maxit:
+                    done = True
+                batch = min(_BATCH, 2 * batch)
+    finally:
+        if full["graph"] is not None:
+            torch.cuda.current_stream(dev).synchronize()  # no replay still in flight
+            lib.rs_graph_destroy(full["graph"])
     return x, np.array(hist), converged
 
 
